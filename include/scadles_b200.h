@@ -1,0 +1,154 @@
+/*
+ * scadles_b200.h — C-ABI of the B200-native ScaDLES gradient-aggregation hot path.
+ *
+ * The reference (streamsgd, pure Python/numpy) has no FFI: its drop-in surface is the
+ * Python module API of `streamsgd.comm` and `streamsgd.nn.sgd_momentum_step`, resolved by
+ * the engine as `comm.<fn>` at call time (reference pkg/src/streamsgd/engine.py:18,253-270,
+ * 282-283).  Each entry point below replaces one of those functions (cited per entry) and is
+ * what a ctypes / cffi binding of that module binds.
+ *
+ * Conventions
+ *   - Every data pointer is a caller-owned DEVICE pointer unless documented as host.
+ *   - Nothing is allocated, synchronised or kept in globals.  Scratch comes from a caller
+ *     workspace sized by the matching *_workspace_bytes() query.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Return value: SG_OK (0) or a negative SG_ERR_* status; sg_status_string() names it.
+ *   - A "bucket" is the flattened per-worker gradient (reference nn.py:122-124):
+ *     k worker rows of `dim` elements, row j at base + j*ld.
+ *   - Top-k key: NaN sorts below every number, -0 == +0, ties go to the lower index,
+ *     kept indices ascending (reference comm.py:90-96).
+ */
+#ifndef SCADLES_B200_H
+#define SCADLES_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_ABI_VERSION 1
+
+#define SG_OK 0
+#define SG_ERR_INVALID (-1)     /* bad argument (the reference raises ValueError) */
+#define SG_ERR_CUDA (-2)        /* a CUDA launch failed */
+#define SG_ERR_WORKSPACE (-3)   /* workspace NULL or smaller than the query */
+#define SG_ERR_UNSUPPORTED (-4) /* shape outside this build's limits (dim >= 2^31, k > 64) */
+
+/* Per-worker gate state.  Mirrors CompressionState (reference comm.py:99-119); lives in
+ * device memory, one per worker, mutated in place by sg_topk_gate_* / sg_gate_update. */
+typedef struct sg_gate_state {
+    double cr;            /* compression ratio in (0, 1]                         */
+    double delta;         /* threshold delta >= 0                                */
+    double ewma_factor;   /* in (0, 1); 0.9 by default                          */
+    double ewma_full;     /* EWMA of |g|^2                                        */
+    double ewma_topk;     /* EWMA of |topk(g)|^2                                  */
+    int64_t n_compressed;
+    int64_t n_uncompressed;
+    int32_t raw_gate;     /* gate on per-iteration norms instead of the EWMAs     */
+    int32_t initialized;  /* first call seeds the EWMAs (comm.py:143-146)         */
+} sg_gate_state;
+
+int sg_abi_version(void);
+const char* sg_status_string(int status);
+
+/* m = max(1, ceil(cr*dim - 1e-12)), host arithmetic; -1 if cr outside (0, 1].
+ * Replaces comm.topk_count (comm.py:81-87). */
+int64_t sg_topk_count(int64_t dim, double cr);
+
+/* ---- Top-k + squared norms + adaptive gate (items 3 and 4) -------------------------------
+ * Replaces comm.topk_sparsify (comm.py:90-96) and comm.compression_gate (comm.py:129-160),
+ * batched over the k workers of one GPU.  For worker j:
+ *   idx[j*m .. j*m+m)   kept indices, strictly ascending (uint32)
+ *   val[j*m .. j*m+m)   g[idx] (copies, bit-exact)
+ *   norms2[2j], [2j+1]  s_full = g.g and s_topk = val.val in float64 (deterministic order)
+ * If `states` is non-NULL the gate is applied: states[j] is updated exactly as comm.py:143-159
+ * (IEEE round-to-nearest, no contraction), decision[j] = 1 iff compressed, rho[j] = ratio.
+ * `ld` is the row stride in elements; rows must be 16-byte aligned for the vector path
+ * (unaligned rows fall back to scalar loads, still on the GPU). */
+size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m);
+size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m);
+int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m,
+                     uint32_t* idx, float* val, double* norms2,
+                     sg_gate_state* states, uint8_t* decision, double* rho,
+                     void* workspace, size_t workspace_bytes, void* stream);
+int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m,
+                     uint32_t* idx, double* val, double* norms2,
+                     sg_gate_state* states, uint8_t* decision, double* rho,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* Gate update alone from precomputed norms2[2k] (comm.py:143-160). */
+int sg_gate_update(const double* norms2, int k, sg_gate_state* states,
+                   uint8_t* decision, double* rho, void* stream);
+
+/* ---- Weighted aggregation with decompression (item 2 + sparse merge) ----------------------
+ * Replaces comm.weighted_aggregate (comm.py:67-78) with densify (comm.py:45-50) folded in:
+ *   out = sum_j weights[j] * densify(payload_j), folded in ascending j, float64 round-to-
+ *   nearest arithmetic (acc = acc + w_j*x_j, no FMA), rounded once to the output type.
+ * Worker j is sparse iff compressed != NULL && compressed[j] != 0 (device bytes); its payload
+ * is idx/val[row_ptr[j] .. row_ptr[j+1]) (device int64 row_ptr, indices ascending < dim).
+ * Otherwise it is dense: dense + j*ld_dense.  `weights` is a HOST array of nw doubles (the
+ * caller passes r = S/sum(S) from comm.weights_from_rates, or 1/n; never batch sizes).
+ * With params/momentum_buf non-NULL the momentum-SGD step (nn.py:161-172) is fused into the
+ * epilogue using the float64 aggregate: buf = buf*mu + (agg + wd*p); p = p - lr*buf
+ * (first_step: buf treated as zeros).  `out` may be NULL when the step is fused. */
+size_t sg_aggregate_workspace_bytes(int nw, int64_t dim);
+int sg_weighted_aggregate_f32(int nw, const double* weights, const uint8_t* compressed,
+                              const float* dense, int64_t ld_dense,
+                              const uint32_t* idx, const float* val, const int64_t* row_ptr,
+                              int64_t dim, float* out,
+                              float* params, float* momentum_buf,
+                              double lr, double momentum, double weight_decay, int first_step,
+                              void* workspace, size_t workspace_bytes, void* stream);
+int sg_weighted_aggregate_f64(int nw, const double* weights, const uint8_t* compressed,
+                              const double* dense, int64_t ld_dense,
+                              const uint32_t* idx, const double* val, const int64_t* row_ptr,
+                              int64_t dim, double* out,
+                              double* params, double* momentum_buf,
+                              double lr, double momentum, double weight_decay, int first_step,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- Momentum SGD (nn.sgd_momentum_step, nn.py:161-172) -----------------------------------
+ * buf = buf*mu; buf = buf + (g + wd*p); p = p - lr*buf, float64 round-to-nearest per element,
+ * in place.  first_step != 0 means the lazily created zero buffer (nn.py:167-168). */
+int sg_sgd_momentum_f32(float* params, float* momentum_buf, const float* grad, int64_t dim,
+                        double lr, double momentum, double weight_decay, int first_step,
+                        void* stream);
+int sg_sgd_momentum_f64(double* params, double* momentum_buf, const double* grad, int64_t dim,
+                        double lr, double momentum, double weight_decay, int first_step,
+                        void* stream);
+
+/* ---- Streaming sampler batch gather (item 5) ----------------------------------------------
+ * Replaces the id -> sample map and _materialize (engine.py:223-227, 201-204) plus the
+ * injected rows of datagen.inject (datagen.py:182-210).  Row r of the output batch is the
+ * train sample rows[r] (device int64, already resolved pools[d][a % len]); features are
+ * x[r,:] = train_x[rows[r],:] + augment[rows[r],:] (float64 add, bit-exact), labels copied.
+ * rows for all devices are concatenated (CSR by device on the host side). */
+int sg_gather_batch_f64(const double* train_x, const double* augment, const int64_t* train_y,
+                        int64_t feature_dim, const int64_t* rows, int64_t n_rows,
+                        double* x_out, int64_t* y_out, void* stream);
+int sg_gather_batch_f32(const float* train_x, const float* augment, const int64_t* train_y,
+                        int64_t feature_dim, const int64_t* rows, int64_t n_rows,
+                        float* x_out, int64_t* y_out, void* stream);
+/* Resolve stream ids to train rows on device: for device d with contiguous drawn ids
+ * [head[d], head[d]+b[d]) the row is pool[d][(head[d]+i) % pool_len[d]] (engine.py:223-227);
+ * out is CSR by device (out_ptr[d] .. out_ptr[d]+b[d]); pools are CSR (pool_ptr, pool_rows). */
+int sg_resolve_stream_rows(int n_dev, const int64_t* head, const int64_t* b,
+                           const int64_t* out_ptr, const int64_t* pool_ptr,
+                           const int64_t* pool_rows, int64_t total, int64_t* out,
+                           void* stream);
+/* Non-IID injection (datagen.py:182-210): recipient d's batch is its own rows
+ * base_rows[base_ptr[d] .. base_ptr[d+1]) followed, for every plan entry k whose sender
+ * senders[k] != d (plan order = ascending sender), by the sender's rows at the pick
+ * positions picks[pick_ptr[k] .. pick_ptr[k+1]) (positions into the sender's pre-injection
+ * batch, drawn on the host with the reference's numpy RNG).  out_ptr is the CSR of the
+ * augmented batches (host-computed sizes). */
+int sg_inject_rows(int n_dev, const int64_t* base_ptr, const int64_t* base_rows, int n_send,
+                   const int32_t* senders, const int64_t* pick_ptr, const int64_t* picks,
+                   const int64_t* out_ptr, int64_t* out_rows, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCADLES_B200_H */

@@ -1,0 +1,182 @@
+// Shared device helpers for the ScaDLES B200 hot path (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/scadles_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "scadles_b200 is built for sm_100a only"
+#endif
+
+#define SG_DEV __device__ __forceinline__
+
+namespace sg {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int MAX_WORKERS = 64;
+
+// ---------------------------------------------------------------------------------------
+// Top-k ordering key.  The reference orders by np.lexsort((arange, -|g|)) (comm.py:94):
+// descending |g|, NaN last (below every number), -0 == +0, ties to the lower index.
+// key = isnan(x) ? 0 : bits(|x|) + 1 is monotone in |x| with those properties and never
+// overflows because bits(|x|) <= bits(inf) for non-NaN x.
+// ---------------------------------------------------------------------------------------
+template <typename T> struct KeyOf;
+template <> struct KeyOf<float> {
+    using K = uint32_t;
+    static constexpr K KMAX = 0x7f800001u;
+    static constexpr int BITS = 32;
+    static SG_DEV K key(float x) {
+        uint32_t b = __float_as_uint(x) & 0x7fffffffu;
+        return b > 0x7f800000u ? 0u : b + 1u;
+    }
+};
+template <> struct KeyOf<double> {
+    using K = unsigned long long;
+    static constexpr K KMAX = 0x7ff0000000000001ull;
+    static constexpr int BITS = 64;
+    static SG_DEV K key(double x) {
+        unsigned long long b = (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+        return b > 0x7ff0000000000000ull ? 0ull : b + 1ull;
+    }
+};
+
+// 16-byte vectors (one 128-bit LDG per thread per round).
+template <typename T> struct Vec16;
+template <> struct Vec16<float> {
+    using V = float4;
+    using I = uint4;
+    static constexpr int N = 4;
+    static SG_DEV float get(const V& v, int c) { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
+};
+template <> struct Vec16<double> {
+    using V = double2;
+    using I = uint2;
+    static constexpr int N = 2;
+    static SG_DEV double get(const V& v, int c) { return c == 0 ? v.x : v.y; }
+};
+
+// Streaming 128-bit loads: read-only path, no L1 allocation (each byte is read once).
+SG_DEV float4 ld_stream(const float4* p) {
+    float4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+        : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+SG_DEV double2 ld_stream(const double2* p) {
+    double2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+SG_DEV uint4 ld_stream(const uint4* p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+SG_DEV uint2 ld_stream(const uint2* p) {
+    uint2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+
+// Relaxed gpu-scope 64-bit status words for decoupled look-back (flag and value share
+// one word, so single-copy atomicity is all the ordering the protocol needs).
+SG_DEV unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+SG_DEV void st_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+SG_DEV unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <typename K> SG_DEV K warp_max(K v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        K u = __shfl_xor_sync(FULL, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+// Fixed-order butterfly: every lane ends with the same bits regardless of scheduling.
+SG_DEV double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+SG_DEV unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+template <typename K> SG_DEV int bitlen(K x) {
+    if (sizeof(K) == 8) return 64 - __clzll((long long)x);
+    return 32 - __clz((int)x);
+}
+
+// Look-back status word: [63:62] flag, [61:0] value.
+constexpr unsigned long long ST_FLAG_AGG = 1ull << 62;
+constexpr unsigned long long ST_FLAG_PRE = 2ull << 62;
+constexpr unsigned long long ST_VALUE = (1ull << 62) - 1;
+
+// Warp-cooperative decoupled look-back (Merrill & Garland).  Called by all 32 lanes of one
+// warp; `status` points at this worker's tile array; returns the exclusive prefix of `tile`
+// and publishes the inclusive one.  Values are summed as integers, so packed counters work
+// as long as no field overflows.
+SG_DEV unsigned long long lookback(unsigned long long* status, long long tile,
+                                   unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed(status, ST_FLAG_PRE | agg);
+        return 0;
+    }
+    if (lane == 0) st_relaxed(status + tile, ST_FLAG_AGG | agg);
+    unsigned long long prefix = 0;
+    long long look = tile - 1;
+    for (;;) {
+        long long i = look - lane;
+        unsigned long long s = i >= 0 ? ld_relaxed(status + i) : ST_FLAG_PRE;
+        while (__any_sync(FULL, (s >> 62) == 0)) {
+            if ((s >> 62) == 0) {
+                __nanosleep(20);
+                s = ld_relaxed(status + i);
+            }
+        }
+        unsigned pre = __ballot_sync(FULL, (s >> 62) == 2);
+        if (pre) {
+            int first = __ffs(pre) - 1;
+            prefix += warp_sum_u64(lane <= first ? (s & ST_VALUE) : 0ull);
+            break;
+        }
+        prefix += warp_sum_u64(s & ST_VALUE);
+        look -= 32;
+    }
+    if (lane == 0) st_relaxed(status + tile, ST_FLAG_PRE | (prefix + agg));
+    return prefix;
+}
+
+// IEEE binary64 round-to-nearest, never contracted into FMA: bit parity with numpy.
+SG_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
+SG_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+SG_DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
+SG_DEV double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+inline int num_sms() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace sg

@@ -1,0 +1,227 @@
+"""Per-GPU hot path: k local workers' gate -> exchange -> weighted aggregate -> momentum SGD.
+
+This is the B200 restatement of the per-iteration section of ``Simulation.run_iteration``
+(reference engine.py:248-286) for one process per GPU:
+
+* the bucket (item 1) is a ``[k, ld]`` float32 tensor, one row per local worker, rows
+  16-byte aligned, canonical parameter order;
+* ``sg_topk_gate`` computes every local worker's Top-k payload, squared norms and gate
+  decision in one launch sequence (comm.compression_gate at engine.py:253);
+* workers are sharded contiguously: rank r owns global workers [r*k, (r+1)*k);
+* exchange, one per step:
+    P == 1  -> no collective; the aggregate kernel reads each worker's decision on device
+               and folds dense rows or sparse payloads (no host synchronisation at all);
+    P > 1   -> all-gather the W decisions; if every worker compressed, all-gather the fixed-
+               size (idx, val) payloads and merge all W on every rank (identical bytes on
+               every rank, deterministic); otherwise each rank folds its local workers into a
+               partial dense sum and the partials are all-reduced;
+* momentum SGD (nn.sgd_momentum_step, engine.py:282-283) is fused into the merge epilogue
+  when the merge produces the final aggregate, so the float64 aggregate feeds the update
+  without a round trip through HBM.
+
+Weights are the reference's r_j = S_j / sum(S) (rate_matched, engine.py:266-267) or 1/n
+(fixed_batch, 268-269); the caller passes them, never batch sizes (SURVEY §0 trap 1).
+
+The collective logic is written against an ``ops`` object so that the host protocol can be
+exercised with the gloo backend on CPU in tests; the product constructs it with
+:class:`CudaOps`, whose every method is an sm_100a kernel launch.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _capi, comm, kernels
+
+
+class CudaOps:
+    """The device operations of the hot path: thin calls into libscadles_b200.so."""
+
+    name = "cuda"
+
+    def __init__(self, device: torch.device):
+        kernels.require_cuda()
+        self.device = device
+
+    def topk_gate(self, bucket, dim, m, states, out):
+        return kernels.topk_gate(bucket, m, states, dim=dim, out=out)
+
+    def aggregate(self, weights, dim, **kw):
+        return kernels.weighted_aggregate(weights, dim, **kw)
+
+    def sgd(self, params, buf, grad, lr, momentum, weight_decay, first):
+        kernels.sgd_momentum(params, buf, grad, lr, momentum, weight_decay, first)
+
+    def gate_records(self, states):
+        return kernels.gate_states_numpy(states)
+
+    def make_states(self, records):
+        return kernels.gate_states_tensor(records, self.device)
+
+
+@dataclass
+class StepInfo:
+    path: str  # "local", "sparse-allgather" or "dense-allreduce"
+    decisions: torch.Tensor | None  # this rank's u8 decisions (device)
+
+
+def _padded(dim: int) -> int:
+    return (dim + 3) // 4 * 4
+
+
+class GradientExchange:
+    """One rank's share of W workers: gate, exchange and update for a flat gradient of ``dim``."""
+
+    def __init__(
+        self,
+        dim: int,
+        n_workers: int,
+        *,
+        cr: float = 0.01,
+        delta: float = 0.3,
+        ewma_factor: float = 0.9,
+        raw_gate: bool = False,
+        compression: bool = True,
+        momentum: float = 0.9,
+        weight_decay: float = 0.0,
+        group=None,
+        ops=None,
+        device: torch.device | None = None,
+        dtype: torch.dtype = torch.float32,
+    ):
+        self.group = group
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.rank = dist.get_rank(group) if group is not None else 0
+        if n_workers % self.world:
+            raise ValueError("workers must divide evenly over ranks")
+        self.W = n_workers
+        self.k = n_workers // self.world
+        self.lo = self.rank * self.k
+        self.dim = dim
+        self.ld = _padded(dim)
+        self.cr = cr
+        self.compression = compression
+        self.m = comm.topk_count(dim, cr) if compression else dim
+        self.momentum = momentum
+        self.weight_decay = weight_decay
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
+        self.ops = ops if ops is not None else CudaOps(device)
+        self.dtype = dtype
+        k, m = self.k, self.m
+        z = dict(device=device)
+        self.bucket = torch.zeros((k, self.ld), dtype=dtype, **z)
+        self.params = torch.zeros(dim, dtype=dtype, **z)
+        self.momentum_buf = torch.zeros(dim, dtype=dtype, **z)
+        self.first_step = True
+        recs = np.zeros(k, dtype=_capi.GATE_STATE_DTYPE)
+        recs["cr"], recs["delta"], recs["ewma_factor"] = cr, delta, ewma_factor
+        recs["raw_gate"] = int(raw_gate)
+        self.states = self.ops.make_states(recs)
+        if compression:
+            self.idx = torch.empty((k, m), dtype=torch.int32, **z)
+            self.val = torch.empty((k, m), dtype=dtype, **z)
+            self.norms2 = torch.empty((k, 2), dtype=torch.float64, **z)
+            self.decision = torch.empty(k, dtype=torch.uint8, **z)
+            self.rho = torch.empty(k, dtype=torch.float64, **z)
+            self.row_ptr_local = torch.arange(0, (k + 1) * m, m, dtype=torch.int64, **z)
+            if self.world > 1:
+                self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
+                self.idx_all = torch.empty((self.W, m), dtype=torch.int32, **z)
+                self.val_all = torch.empty((self.W, m), dtype=dtype, **z)
+                self.row_ptr_all = torch.arange(0, (self.W + 1) * m, m, dtype=torch.int64, **z)
+        self.partial = torch.empty(dim, dtype=dtype, **z) if self.world > 1 else None
+        self.aggregate = None
+        self.steps = 0
+
+    # -- the step ---------------------------------------------------------------------------
+
+    def gate(self) -> None:
+        """Top-k + norms + gate for every local worker (no host synchronisation)."""
+        self.ops.topk_gate(
+            self.bucket, self.dim, self.m, self.states,
+            (self.idx, self.val, self.norms2, self.decision, self.rho),
+        )
+
+    def step(self, weights, lr: float, *, keep_aggregate: bool = False) -> StepInfo:
+        """One synchronous iteration over the gradients currently in ``bucket``.
+
+        ``weights`` holds all W aggregation weights (host float64).  With
+        ``keep_aggregate`` the aggregated gradient is also written to ``self.aggregate``.
+        """
+        w = np.asarray(weights, dtype=np.float64)
+        if w.shape != (self.W,):
+            raise ValueError("one weight per worker required")
+        dim, first = self.dim, self.first_step
+        opt = dict(params=self.params, momentum_buf=self.momentum_buf, lr=lr,
+                   momentum=self.momentum, weight_decay=self.weight_decay, first_step=first)
+        if keep_aggregate and self.aggregate is None:
+            self.aggregate = torch.empty(dim, dtype=self.dtype, device=self.device)
+        out = self.aggregate if keep_aggregate else None
+        if self.compression:
+            self.gate()
+        if self.world == 1:
+            if self.compression:
+                self.ops.aggregate(w, dim, compressed=self.decision, dense=self.bucket, idx=self.idx,
+                                   val=self.val, row_ptr=self.row_ptr_local, out=out, **opt)
+            else:
+                self.ops.aggregate(w, dim, dense=self.bucket, out=out, **opt)
+            path = "local"
+        else:
+            path = self._exchange(w, out, opt)
+        self.first_step = False
+        self.steps += 1
+        return StepInfo(path, self.decision if self.compression else None)
+
+    def _exchange(self, w, out, opt) -> str:
+        g = self.group
+        dim = self.dim
+        if self.compression:
+            dist.all_gather_into_tensor(self.dec_all, self.decision, group=g)
+            all_compressed = bool(self.dec_all.min().item() == 1)
+        else:
+            all_compressed = False
+        if all_compressed:
+            dist.all_gather_into_tensor(self.idx_all.view(-1), self.idx.view(-1), group=g)
+            dist.all_gather_into_tensor(self.val_all.view(-1), self.val.view(-1), group=g)
+            self.ops.aggregate(w, dim, compressed=self.dec_all, idx=self.idx_all, val=self.val_all,
+                               row_ptr=self.row_ptr_all, out=out, **opt)
+            return "sparse-allgather"
+        wl = w[self.lo:self.lo + self.k]
+        if self.compression:
+            self.ops.aggregate(wl, dim, compressed=self.decision, dense=self.bucket, idx=self.idx,
+                               val=self.val, row_ptr=self.row_ptr_local, out=self.partial)
+        else:
+            self.ops.aggregate(wl, dim, dense=self.bucket, out=self.partial)
+        dist.all_reduce(self.partial, op=dist.ReduceOp.SUM, group=g)
+        if out is not None:
+            out.copy_(self.partial)
+        self.ops.sgd(self.params, self.momentum_buf, self.partial, opt["lr"], self.momentum,
+                     self.weight_decay, opt["first_step"])
+        return "dense-allreduce"
+
+    # -- host views (synchronising) -----------------------------------------------------------
+
+    def gate_counters(self) -> np.ndarray:
+        return self.ops.gate_records(self.states)
+
+    def volume(self) -> tuple[int, int]:
+        """(floats_sent, bytes_sent) of this rank's workers so far (comm.account_volume)."""
+        if self.compression:
+            rec = self.gate_counters()
+            nc = int(rec["n_compressed"].sum())
+            nu = int(rec["n_uncompressed"].sum())
+        else:
+            nc, nu = 0, self.steps * self.k
+        floats = nc * self.m + nu * self.dim
+        nbytes = nc * self.m * (comm.FLOAT_BYTES + comm.INDEX_BYTES) + nu * self.dim * comm.FLOAT_BYTES
+        return floats, nbytes
+
+    def param_checksum(self) -> float:
+        """Replica check (engine.py:284-286): identical on every rank by construction."""
+        return float(self.params.double().sum().item())

@@ -1,0 +1,200 @@
+"""Torch-tensor wrappers over the C-ABI (device memory and streams come from PyTorch).
+
+Every function here launches the sm_100a kernels of ``libscadles_b200.so`` on the current
+torch CUDA stream and returns without synchronising.  Inputs must be CUDA tensors; there is
+no CPU path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _capi
+
+_GATE_BYTES = _capi.GATE_STATE_DTYPE.itemsize
+
+
+def require_cuda(t: torch.Tensor | None = None) -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("scadles_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    if t is not None and not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Workspace:
+    """Grow-only device scratch buffer owned by the Python caller (one per device)."""
+
+    _cache: dict[int, torch.Tensor] = {}
+
+    @classmethod
+    def get(cls, nbytes: int, device: torch.device) -> torch.Tensor:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        buf = cls._cache.get(idx)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            cls._cache[idx] = buf
+        return buf
+
+
+def gate_states_tensor(states: np.ndarray, device: torch.device) -> torch.Tensor:
+    """Pack a GATE_STATE_DTYPE record array into a device byte tensor."""
+    raw = np.ascontiguousarray(states, dtype=_capi.GATE_STATE_DTYPE).view(np.uint8)
+    return torch.from_numpy(raw.copy()).to(device)
+
+
+def gate_states_numpy(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(_capi.GATE_STATE_DTYPE).copy()
+
+
+def topk_workspace_bytes(dtype: torch.dtype, k: int, dim: int, m: int) -> int:
+    lib = _capi.load()
+    fn = lib.sg_topk_workspace_bytes_f32 if dtype == torch.float32 else lib.sg_topk_workspace_bytes_f64
+    return int(fn(k, dim, m))
+
+
+def topk_gate(
+    g: torch.Tensor,
+    m: int,
+    states: torch.Tensor | None = None,
+    *,
+    dim: int | None = None,
+    out: tuple | None = None,
+):
+    """Batched Top-k + norms (+ gate) over the rows of ``g`` ([k, ld] or [D]).
+
+    Returns (idx int32 [k, m] (uint32 bits), val [k, m], norms2 f64 [k, 2], decision u8 [k],
+    rho f64 [k]); decision/rho are None without ``states``.
+    """
+    require_cuda(g)
+    if g.dtype not in (torch.float32, torch.float64):
+        raise ValueError("gradient bucket must be float32 or float64")
+    g2 = g.unsqueeze(0) if g.dim() == 1 else g
+    if g2.dim() != 2 or g2.stride(1) != 1:
+        raise ValueError("bucket must be [k, ld] with unit inner stride")
+    k = g2.shape[0]
+    ld = g2.stride(0) if k > 1 else g2.shape[1]
+    D = int(dim if dim is not None else g2.shape[1])
+    dev = g.device
+    if out is None:
+        idx = torch.empty((k, m), dtype=torch.int32, device=dev)
+        val = torch.empty((k, m), dtype=g.dtype, device=dev)
+        norms2 = torch.empty((k, 2), dtype=torch.float64, device=dev)
+        decision = torch.empty(k, dtype=torch.uint8, device=dev) if states is not None else None
+        rho = torch.empty(k, dtype=torch.float64, device=dev) if states is not None else None
+    else:
+        idx, val, norms2, decision, rho = out
+    if states is not None and states.numel() != k * _GATE_BYTES:
+        raise ValueError("one gate state per worker required")
+    nbytes = topk_workspace_bytes(g.dtype, k, D, m)
+    if nbytes == 0:
+        raise ValueError("invalid top-k shape")
+    ws = Workspace.get(nbytes, dev)
+    lib = _capi.load()
+    fn = lib.sg_topk_gate_f32 if g.dtype == torch.float32 else lib.sg_topk_gate_f64
+    st = fn(
+        g2.data_ptr(), k, ld, D, m, idx.data_ptr(), val.data_ptr(), norms2.data_ptr(),
+        _ptr(states), _ptr(decision), _ptr(rho), ws.data_ptr(), ws.numel(), _stream(),
+    )
+    _capi.check(st, "sg_topk_gate")
+    return idx, val, norms2, decision, rho
+
+
+def gate_update(norms2: torch.Tensor, states: torch.Tensor):
+    require_cuda(norms2)
+    k = norms2.shape[0]
+    decision = torch.empty(k, dtype=torch.uint8, device=norms2.device)
+    rho = torch.empty(k, dtype=torch.float64, device=norms2.device)
+    st = _capi.load().sg_gate_update(norms2.data_ptr(), k, states.data_ptr(), decision.data_ptr(), rho.data_ptr(), _stream())
+    _capi.check(st, "sg_gate_update")
+    return decision, rho
+
+
+def weighted_aggregate(
+    weights,
+    dim: int,
+    *,
+    compressed: torch.Tensor | None = None,
+    dense: torch.Tensor | None = None,
+    idx: torch.Tensor | None = None,
+    val: torch.Tensor | None = None,
+    row_ptr: torch.Tensor | None = None,
+    out: torch.Tensor | None = None,
+    params: torch.Tensor | None = None,
+    momentum_buf: torch.Tensor | None = None,
+    lr: float = 0.0,
+    momentum: float = 0.0,
+    weight_decay: float = 0.0,
+    first_step: bool = False,
+    dtype: torch.dtype | None = None,
+):
+    """sum_j w_j * densify(payload_j) (+ optional fused momentum-SGD) on the GPU."""
+    w, wp = _capi.weights_ptr(np.asarray(weights, dtype=np.float64))
+    nw = len(w)
+    ref = next(t for t in (dense, val, params, out) if t is not None)
+    require_cuda(ref)
+    dt = dtype or ref.dtype
+    dev = ref.device
+    ld = 0
+    if dense is not None:
+        d2 = dense.unsqueeze(0) if dense.dim() == 1 else dense
+        if d2.stride(-1) != 1:
+            raise ValueError("dense rows need unit stride")
+        ld = d2.stride(0) if d2.shape[0] > 1 else d2.shape[1]
+        dense = d2
+    if out is None and params is None:
+        out = torch.empty(dim, dtype=dt, device=dev)
+    ws = None
+    nbytes = 0
+    if compressed is not None:
+        nbytes = int(_capi.load().sg_aggregate_workspace_bytes(nw, dim))
+        ws = Workspace.get(nbytes, dev)
+    fn = _capi.load().sg_weighted_aggregate_f32 if dt == torch.float32 else _capi.load().sg_weighted_aggregate_f64
+    st = fn(
+        nw, wp, _ptr(compressed), _ptr(dense), ld, _ptr(idx), _ptr(val), _ptr(row_ptr), dim,
+        _ptr(out), _ptr(params), _ptr(momentum_buf), float(lr), float(momentum), float(weight_decay),
+        int(bool(first_step)), _ptr(ws), nbytes if ws is not None else 0, _stream(),
+    )
+    _capi.check(st, "sg_weighted_aggregate")
+    return out
+
+
+def sgd_momentum(params, momentum_buf, grad, lr, momentum, weight_decay, first_step):
+    require_cuda(params)
+    lib = _capi.load()
+    fn = lib.sg_sgd_momentum_f32 if params.dtype == torch.float32 else lib.sg_sgd_momentum_f64
+    st = fn(params.data_ptr(), momentum_buf.data_ptr(), grad.data_ptr(), params.numel(), float(lr),
+            float(momentum), float(weight_decay), int(bool(first_step)), _stream())
+    _capi.check(st, "sg_sgd_momentum")
+
+
+def resolve_stream_rows(head, b, out_ptr, pool_ptr, pool_rows, total, out):
+    st = _capi.load().sg_resolve_stream_rows(
+        len(head), head.data_ptr(), b.data_ptr(), out_ptr.data_ptr(), pool_ptr.data_ptr(),
+        pool_rows.data_ptr(), int(total), out.data_ptr(), _stream())
+    _capi.check(st, "sg_resolve_stream_rows")
+
+
+def inject_rows(base_ptr, base_rows, senders, pick_ptr, picks, out_ptr, out_rows):
+    n_dev = base_ptr.numel() - 1
+    st = _capi.load().sg_inject_rows(
+        n_dev, base_ptr.data_ptr(), base_rows.data_ptr(), senders.numel(), _ptr(senders) if senders.numel() else None,
+        _ptr(pick_ptr) if senders.numel() else None, _ptr(picks) if picks.numel() else None,
+        out_ptr.data_ptr(), out_rows.data_ptr(), _stream())
+    _capi.check(st, "sg_inject_rows")
+
+
+def gather_batch(train_x, augment, train_y, rows, x_out, y_out):
+    lib = _capi.load()
+    fn = lib.sg_gather_batch_f64 if train_x.dtype == torch.float64 else lib.sg_gather_batch_f32
+    st = fn(train_x.data_ptr(), _ptr(augment), _ptr(train_y), train_x.shape[1], rows.data_ptr(),
+            rows.numel(), x_out.data_ptr(), _ptr(y_out), _stream())
+    _capi.check(st, "sg_gather_batch")

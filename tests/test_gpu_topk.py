@@ -1,0 +1,133 @@
+"""GPU parity: Top-k sparsification (item 3) against the reference golden vectors and the oracle.
+
+Bar: indices bit-exact (same set, ascending), values bit-exact (copies of the input)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_npz
+from oracle import comm_ref
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_topk_float64_dropin(cuda):
+    from paper_2301_08897_b200 import comm
+
+    z, meta = load_npz("topk")
+    for i, mt in enumerate(meta):
+        g = z[f"g{i}"]
+        sp = comm.topk_sparsify(g, mt["cr"])
+        assert sp.nnz == mt["m"], (i, mt)
+        assert np.array_equal(sp.indices, z[f"idx{i}"]), (i, mt)
+        got, want = sp.values, z[f"val{i}"]
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (i, mt)
+
+
+def test_golden_topk_float32_path(cuda):
+    from paper_2301_08897_b200 import kernels
+
+    z, meta = load_npz("topk")
+    n = 0
+    for i, mt in enumerate(meta):
+        g = z[f"g{i}"]
+        g32 = g.astype(np.float32)
+        if not np.array_equal(g32.astype(np.float64), g, equal_nan=True):
+            continue  # not float32-representable
+        idx, val, norms2, _, _ = kernels.topk_gate(torch.from_numpy(g32).to(cuda), mt["m"])
+        assert np.array_equal(idx[0].cpu().numpy().astype(np.int64), z[f"idx{i}"]), (i, mt)
+        assert np.array_equal(val[0].cpu().numpy().view(np.uint32), z[f"val{i}"].astype(np.float32).view(np.uint32))
+        n += 1
+    assert n >= 24
+
+
+def _family(fam: str, D: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal(D, dtype=np.float32)
+    if fam == "normal":
+        return z
+    if fam == "heavy":
+        return (np.sign(z) * np.exp(1.5 * rng.standard_normal(D, dtype=np.float32))).astype(np.float32)
+    if fam == "ties":
+        g = (np.round(z * 8) / 8).astype(np.float32)
+        g[D // 2] = g[0]
+        g[D // 3] = -g[0]
+        g[D - 1] = abs(g[0])
+        return g
+    if fam == "edge":
+        g = z.copy()
+        g[rng.integers(0, D, 64)] = 0.0
+        g[rng.integers(0, D, 64)] = -0.0
+        g[D // 7] = np.nan
+        g[D // 5] = np.inf
+        g[D // 3] = -np.inf
+        return g
+    raise ValueError(fam)
+
+
+@pytest.mark.parametrize("D", [1, 3, 17, 4096, 4097, 100_003, 1 << 20, (1 << 22) + 5])
+@pytest.mark.parametrize("cr", [0.001, 0.01, 0.1, 0.5, 1.0])
+@pytest.mark.parametrize("fam", ["normal", "heavy", "ties", "edge"])
+def test_topk_matches_oracle(cuda, D, cr, fam):
+    from paper_2301_08897_b200 import kernels
+
+    if fam == "edge" and D < 8:
+        pytest.skip("edge family needs room")
+    g = _family(fam, D, seed=D * 7 + int(cr * 1000))
+    m = comm_ref.topk_count(D, cr)
+    idx, val, norms2, _, _ = kernels.topk_gate(torch.from_numpy(g).to(cuda), m)
+    want = comm_ref.topk_indices_threshold(g.astype(np.float64), m)
+    got = idx[0].cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, want)
+    assert np.array_equal(val[0].cpu().numpy().view(np.uint32), g[want].view(np.uint32))
+    g64 = g.astype(np.float64)
+    s_full = float(g64 @ g64)
+    s_topk = float(g64[want] @ g64[want])
+    n = norms2[0].cpu().numpy()
+    for a, b in ((n[0], s_full), (n[1], s_topk)):
+        if np.isfinite(b):
+            assert abs(a - b) <= 1e-10 * abs(b) + 1e-300
+        else:
+            assert np.isnan(a) == np.isnan(b)
+
+
+def test_topk_batched_rows_and_padding(cuda):
+    """k workers in one launch, rows with a padded leading dimension."""
+    from paper_2301_08897_b200 import kernels
+
+    k, D, ld = 8, 300_001, 300_004
+    rng = np.random.default_rng(3)
+    host = np.zeros((k, ld), dtype=np.float32)
+    for j in range(k):
+        host[j, :D] = _family(["normal", "heavy", "ties", "edge"][j % 4], D, seed=100 + j)
+    dev = torch.from_numpy(host).to(cuda)
+    for cr in (0.01, 0.1):
+        m = comm_ref.topk_count(D, cr)
+        idx, val, norms2, _, _ = kernels.topk_gate(dev, m, dim=D)
+        for j in range(k):
+            want = comm_ref.topk_indices_threshold(host[j, :D].astype(np.float64), m)
+            assert np.array_equal(idx[j].cpu().numpy().astype(np.int64), want), (j, cr)
+
+
+def test_topk_float64_large_matches_lexsort(cuda):
+    from paper_2301_08897_b200 import comm
+
+    rng = np.random.default_rng(11)
+    g = rng.normal(size=200_001)
+    g[::1000] = g[0]
+    for cr in (0.001, 0.01, 0.1):
+        sp = comm.topk_sparsify(g, cr)
+        idx, _ = comm_ref.topk(g, cr, "lexsort")
+        assert np.array_equal(sp.indices, idx)
+
+
+def test_topk_constant_and_all_nan(cuda):
+    """Pathological ties: every key equal -> the lowest m indices (fallback path)."""
+    from paper_2301_08897_b200 import kernels
+
+    for fill in (1.5, 0.0, np.nan):
+        g = np.full(1 << 18, fill, dtype=np.float32)
+        m = comm_ref.topk_count(g.size, 0.01)
+        idx, _, _, _, _ = kernels.topk_gate(torch.from_numpy(g).to(cuda), m)
+        assert np.array_equal(idx[0].cpu().numpy(), np.arange(m))
