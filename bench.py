@@ -1,0 +1,390 @@
+#!/usr/bin/env python3
+"""Benchmark of the ScaDLES gradient-aggregation hot path on B200.
+
+One step = one synchronous iteration of the hot path over one batch of synthetic gradients
+of ResNet-152 size (60,192,808 fp32 elements) for W = 8 workers: per-worker Top-k (cr 0.01)
++ squared norms + EWMA gate, the exchange (local at N=1; decision all-gather then sparse
+all-gather or dense all-reduce over NCCL at N>1), the stream-rate-weighted aggregation with
+decompression, and the fused momentum-SGD update.  Workers are sharded k = W/N per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  `value` = aggregated gradient elements per second for the
+whole job (W*D per step / device time, max over ranks); `e2e` = the same through the public
+API with host (pinned) gradient buffers copied in and the aggregate copied out every step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+R_DIM = 60_192_808  # ResNet-152 parameter count (torchvision)
+METRIC = "aggregated grad elems/sec & HBM GB/s (%roofline) per step at 1/2/4/8 B200 vs CPU"
+UNIT = "elem/s"
+MEASURED = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["topk", "dense"], default="topk")
+    ap.add_argument("--dim", type=int, default=R_DIM)
+    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--cr", type=float, default=0.01)
+    ap.add_argument("--delta", type=float, default=0.3)
+    ap.add_argument("--family", choices=["heavy", "normal"], default="heavy")
+    ap.add_argument("--cpu-dim", type=int, default=1 << 22, help="per-worker gradient length of the CPU sample")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        d = json.loads(MEASURED.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def rates_weights(W: int):
+    from paper_2301_08897_b200 import comm
+    from paper_2301_08897_b200.streams import RateDistribution, derive_seed, sample_rates
+
+    rates = sample_rates(RateDistribution("uniform", 38, 24), W, derive_seed(0, "rates"))
+    return rates, comm.weights_from_rates(rates)
+
+
+# ---------------------------------------------------------------------------------------
+# CPU leg: the oracle port of the reference path (oracle/comm_ref.py), timed on host cores
+# ---------------------------------------------------------------------------------------
+def _cpu_gate(args):
+    g, cr, delta = args
+    from oracle import comm_ref
+
+    st = comm_ref.GateState(cr, delta)
+    c, payload, _, _, _ = comm_ref.gate(g, st, "lexsort")
+    return c, payload
+
+
+def cpu_synthetic(W: int, D: int, family: str, seed: int = 0):
+    rng = np.random.default_rng(seed)
+    out = []
+    for j in range(W):
+        z = rng.standard_normal(D, dtype=np.float32)
+        if family == "heavy":
+            g = np.sign(z) * np.exp(1.5 * rng.standard_normal(D, dtype=np.float32))
+        else:
+            g = z
+        out.append((g * (1 + 0.1 * j)).astype(np.float32).astype(np.float64))
+    return out
+
+
+def cpu_step_time(grads, weights, cr, delta, compression, pool):
+    """One reference step on the host: W gates (process pool), aggregate, momentum SGD."""
+    from oracle import comm_ref
+
+    D = len(grads[0])
+    t0 = time.perf_counter()
+    if compression:
+        res = pool.map(_cpu_gate, [(g, cr, delta) for g in grads])
+        payloads = [(D, *p) if c else p for c, p in res]
+    else:
+        payloads = grads
+    agg = comm_ref.aggregate(payloads, weights)
+    comm_ref.sgd_momentum(np.zeros(D), None, agg, 0.01, 0.9, 1e-4)
+    return time.perf_counter() - t0
+
+
+def cpu_measure(args, W, steps, warmup=1):
+    import multiprocessing as mp
+
+    _, w = rates_weights(W)
+    grads = cpu_synthetic(W, args.cpu_dim, args.family)
+    cores = min(W, os.cpu_count() or 1)
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        for _ in range(warmup):
+            cpu_step_time(grads, w, args.cr, args.delta, args.workload == "topk", pool)
+        times = [cpu_step_time(grads, w, args.cr, args.delta, args.workload == "topk", pool) for _ in range(steps)]
+    t = statistics.median(times)
+    return {
+        "value": W * args.cpu_dim / t,
+        "unit": UNIT,
+        "cores": cores,
+        "kind": "port",
+        "sample": f"W={W} workers x D={args.cpu_dim} f64 (fp32-valued) per step, oracle/comm_ref.py "
+                  f"(np.lexsort Top-k as comm.py:94), {cores}-process pool for the gates, "
+                  f"median of {steps} steps; host cpu_count={os.cpu_count()}",
+        "step_s": t,
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    W = args.workers
+    cb = cpu_measure(args, W, steps=args.steps, warmup=args.warmup)
+    line = {
+        "metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": cb["step_s"] * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"ResNet-152-sized weighted Top-k aggregation (cr {args.cr}, delta {args.delta}), "
+                               f"{W} workers, CPU sample D={args.cpu_dim}",
+                   "family": args.family},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu_id), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def synth_bucket(ex, family, rank_lo, seed=0):
+    import torch
+
+    dev = ex.device
+    for j in range(ex.k):
+        gen = torch.Generator(device=dev).manual_seed(seed * 1000 + rank_lo + j)
+        z = torch.randn(ex.dim, device=dev, generator=gen)
+        if family == "heavy":
+            z = torch.sign(z) * torch.exp(1.5 * torch.randn(ex.dim, device=dev, generator=gen))
+        ex.bucket[j, :ex.dim].copy_(z * (1 + 0.1 * (rank_lo + j)))
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2301_08897_b200 import build, comm, exchange, kernels
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    build.build()
+    W, D = args.workers, args.dim
+    rates, w = rates_weights(W)
+    lr = 0.1 * sum(rates) / (W * 64)  # scale_lr(base 0.1, sum S, n*64), nn.py:184-190
+    compression = args.workload == "topk"
+    ex = exchange.GradientExchange(D, W, cr=args.cr, delta=args.delta, compression=compression, momentum=0.9,
+                                   weight_decay=1e-4, group=group, device=dev)
+    synth_bucket(ex, args.family, ex.lo)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if group is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def reduce_max(x: float) -> float:
+        if group is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timing -------------------------------------------------------
+    for _ in range(args.warmup):
+        ex.step(w, lr)
+    K = args.steps
+    ev_topk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    clocks = Clocks(cvd.split(",")[local] if cvd else local)
+    barrier()
+    clocks.start()
+    launches0 = kernels.LAUNCHES["n"]
+    paths = []
+    s_ev.record()
+    for i in range(K):
+        info = ex.step(w, lr, topk_events=ev_topk[i] if compression else None)
+        paths.append(info.path)
+    e_ev.record()
+    barrier()
+    clk = clocks.stop()
+    launches = kernels.LAUNCHES["n"] - launches0
+    t_ms = reduce_max(s_ev.elapsed_time(e_ev))
+    topk_ms = [a.elapsed_time(b) for a, b in ev_topk] if compression else []
+    value = W * D * K / (t_ms / 1e3)
+    hbm, hbm_kind = peaks()
+    m = ex.m
+    k = ex.k
+    roof = None
+    if compression:
+        topk_avg = statistics.mean(topk_ms) / 1e3
+        alg = k * (4 * D + 8 * m)
+        achieved = alg / topk_avg / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / "traffic.json"
+        if tf.exists():
+            try:
+                traffic = json.loads(tf.read_text()).get(f"topk_k{k}_cr{args.cr}")
+            except Exception:
+                traffic = None
+        roof = {"kernel": "sg_topk_gate_f32 (Top-k + norms + gate launch sequence)", "bound": "hbm",
+                "achieved": achieved, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "alg_bytes_per_launch": alg, "avg_launch_us": topk_avg * 1e6}
+    # whole-step algorithmic HBM bytes per GPU (SGD fused: 16 B/elem)
+    all_sparse = all(p in ("local", "sparse-allgather") for p in paths) and compression and \
+        bool((ex.decision == 1).all().item())
+    if compression and all_sparse:
+        step_bytes = k * (4 * D + 8 * m) + W * 8 * m + 16 * D
+    elif compression:
+        step_bytes = k * (4 * D + 8 * m) + k * 4 * D + 16 * D
+    else:
+        step_bytes = k * 4 * D + 16 * D
+    step_s = t_ms / 1e3 / K
+    step_roof = {"bytes_per_step": step_bytes, "achieved": step_bytes / step_s / 1e9, "frac": step_bytes / step_s / 1e9 / hbm}
+
+    # ---- end to end through the public API with host buffers --------------------------
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((k, ex.ld), dtype=torch.float32, pin_memory=True)
+        host.copy_(ex.bucket)
+        agg_host = torch.empty(D, dtype=torch.float32, pin_memory=True)
+        dec_host = torch.empty(k, dtype=torch.uint8, pin_memory=True)
+        ke = max(3, K // 4)
+        for _ in range(2):
+            ex.bucket.copy_(host, non_blocking=True)
+            ex.step(w, lr, keep_aggregate=True)
+            agg_host.copy_(ex.aggregate, non_blocking=True)
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        s2.record()
+        for _ in range(ke):
+            ex.bucket.copy_(host, non_blocking=True)
+            ex.step(w, lr, keep_aggregate=True)
+            agg_host.copy_(ex.aggregate, non_blocking=True)
+            if compression:
+                dec_host.copy_(ex.decision, non_blocking=True)
+        e2.record()
+        barrier()
+        te = reduce_max(s2.elapsed_time(e2))
+        e2e = {"value": W * D * ke / (te / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(k * ex.ld * 4),
+               "d2h_bytes_per_step": int(D * 4 + (k if compression else 0)), "steps": ke,
+               "path": "GradientExchange.step on pinned host gradients, aggregate copied back"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_measure(args, W, steps=args.cpu_steps)
+        cpu = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (f64 accumulation)", "data": "synthetic",
+            "config": {
+                "workload": (f"ResNet-152-sized adaptive Top-k aggregation: W={W} workers x D={D}, cr={args.cr}, "
+                             f"delta={args.delta}, S1 rates {rates}, gate+exchange+weighted merge+fused momentum SGD"
+                             if compression else
+                             f"ResNet-152-sized weighted dense aggregation: W={W} workers x D={D}, S1 rates {rates}, "
+                             f"+ fused momentum SGD"),
+                "family": args.family, "workers_per_gpu": k, "parallelism": f"workers sharded {k}/GPU over {world} GPU(s)",
+                "l2": "inputs larger than L2 (k x 241 MB bucket per GPU)", "paths": sorted(set(paths)),
+            },
+            "roofline": roof,
+            "step_roofline": step_roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if roof is not None:
+            line["topk_us"] = {"mean": statistics.mean(topk_ms) * 1e3, "min": min(topk_ms) * 1e3}
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -65,6 +65,8 @@ int64_t sg_topk_count(int64_t dim, double cr);
  *   norms2[2j], [2j+1]  s_full = g.g and s_topk = val.val in float64 (deterministic order)
  * If `states` is non-NULL the gate is applied: states[j] is updated exactly as comm.py:143-159
  * (IEEE round-to-nearest, no contraction), decision[j] = 1 iff compressed, rho[j] = ratio.
+ * f32 only: if `tile_off` is non-NULL it receives, per worker, the [ceil(dim/4096)+1] merge
+ * offsets (number of kept indices below t*4096) that sg_weighted_aggregate_* accepts.
  * `ld` is the row stride in elements; rows must be 16-byte aligned for the vector path
  * (unaligned rows fall back to scalar loads, still on the GPU). */
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m);
@@ -72,6 +74,7 @@ size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m);
 int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m,
                      uint32_t* idx, float* val, double* norms2,
                      sg_gate_state* states, uint8_t* decision, double* rho,
+                     int32_t* tile_off,
                      void* workspace, size_t workspace_bytes, void* stream);
 int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m,
                      uint32_t* idx, double* val, double* norms2,
@@ -87,7 +90,10 @@ int sg_gate_update(const double* norms2, int k, sg_gate_state* states,
  *   out = sum_j weights[j] * densify(payload_j), folded in ascending j, float64 round-to-
  *   nearest arithmetic (acc = acc + w_j*x_j, no FMA), rounded once to the output type.
  * Worker j is sparse iff compressed != NULL && compressed[j] != 0 (device bytes); its payload
- * is idx/val[row_ptr[j] .. row_ptr[j+1]) (device int64 row_ptr, indices ascending < dim).
+ * is idx/val[row_ptr[j] .. row_ptr[j+1]) (device int64 row_ptr, indices ascending < dim);
+ * `tile_off` ([nw][ceil(dim/4096)+1] int32, row-relative, from sg_topk_gate_f32) may be NULL,
+ * in which case it is computed into the workspace.  `dense` may be NULL only if every
+ * worker is compressed.
  * Otherwise it is dense: dense + j*ld_dense.  `weights` is a HOST array of nw doubles (the
  * caller passes r = S/sum(S) from comm.weights_from_rates, or 1/n; never batch sizes).
  * With params/momentum_buf non-NULL the momentum-SGD step (nn.py:161-172) is fused into the
@@ -97,14 +103,14 @@ size_t sg_aggregate_workspace_bytes(int nw, int64_t dim);
 int sg_weighted_aggregate_f32(int nw, const double* weights, const uint8_t* compressed,
                               const float* dense, int64_t ld_dense,
                               const uint32_t* idx, const float* val, const int64_t* row_ptr,
-                              int64_t dim, float* out,
+                              const int32_t* tile_off, int64_t dim, float* out,
                               float* params, float* momentum_buf,
                               double lr, double momentum, double weight_decay, int first_step,
                               void* workspace, size_t workspace_bytes, void* stream);
 int sg_weighted_aggregate_f64(int nw, const double* weights, const uint8_t* compressed,
                               const double* dense, int64_t ld_dense,
                               const uint32_t* idx, const double* val, const int64_t* row_ptr,
-                              int64_t dim, double* out,
+                              const int32_t* tile_off, int64_t dim, double* out,
                               double* params, double* momentum_buf,
                               double lr, double momentum, double weight_decay, int first_step,
                               void* workspace, size_t workspace_bytes, void* stream);

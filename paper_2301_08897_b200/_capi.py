@@ -61,18 +61,18 @@ SIGNATURES = {
     "sg_topk_count": (c_int64, [c_int64, c_double]),
     "sg_topk_workspace_bytes_f32": (c_size_t, [c_int, c_int64, c_int64]),
     "sg_topk_workspace_bytes_f64": (c_size_t, [c_int, c_int64, c_int64]),
-    "sg_topk_gate_f32": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
+    "sg_topk_gate_f32": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
     "sg_topk_gate_f64": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
     "sg_gate_update": (c_int, [_P, c_int, _P, _P, _P, _P]),
     "sg_aggregate_workspace_bytes": (c_size_t, [c_int, c_int64]),
     "sg_weighted_aggregate_f32": (
         c_int,
-        [c_int, POINTER(c_double), _P, _P, c_int64, _P, _P, _P, c_int64, _P, _P, _P,
+        [c_int, POINTER(c_double), _P, _P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, _P,
          c_double, c_double, c_double, c_int, _P, c_size_t, _P],
     ),
     "sg_weighted_aggregate_f64": (
         c_int,
-        [c_int, POINTER(c_double), _P, _P, c_int64, _P, _P, _P, c_int64, _P, _P, _P,
+        [c_int, POINTER(c_double), _P, _P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, _P,
          c_double, c_double, c_double, c_int, _P, c_size_t, _P],
     ),
     "sg_sgd_momentum_f32": (c_int, [_P, _P, _P, c_int64, c_double, c_double, c_double, c_int, _P]),

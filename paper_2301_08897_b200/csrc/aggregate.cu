@@ -4,25 +4,35 @@
 // for each worker in order acc += w_j * densify(g_j)), comm.py:45-50 (densify) and
 // nn.py:161-172 (sgd_momentum_step).
 //
-// Output-tile merge: every CTA owns one 4096-element output tile held as float64 in shared
-// memory.  Workers are folded in ascending order (a __syncthreads between workers): a dense
-// worker streams its tile with 128-bit loads, a sparse worker streams only the (idx, val)
-// pairs that fall in the tile, located through a per-worker tile-offset table built by
-// k_tile_offsets from the ascending indices.  No atomics, so the result is deterministic
-// and identical on every rank.  Arithmetic is binary64 round-to-nearest without contraction
-// (acc = acc + w*x), which is exactly numpy's `acc += weight * densify(g)` on the upcast
-// inputs; the single rounding to the output type happens once, at the store.  Positions a
-// sparse worker does not keep would add w*(+0.0) in the reference: a no-op on an accumulator
-// that starts at +0.0, so they are skipped.  With params/buf the momentum-SGD step runs in
-// the epilogue on the unrounded float64 aggregate (nn.py:169-171 operation order).
+// Output-tile merge: every CTA owns one 4096-element output tile; each thread owns 16
+// positions (four 16-byte groups, coalesced) and keeps their float64 accumulators in
+// registers.  Workers are folded in ascending order:
+//   dense worker   -> 128-bit streaming loads of its tile (next dense worker prefetched),
+//                     acc = acc + w*x;
+//   sparse worker  -> its (idx, val) pairs inside the tile (located by a per-worker tile
+//                     offset table: from sg_topk_gate's writer or k_tile_offsets) are staged
+//                     in shared memory for ALL sparse workers with one batched load, then
+//                     scattered into a zeroed shared tile S, and every thread adds w*S[q] for
+//                     its positions and re-zeroes them.
+// Positions a sparse worker does not keep contribute w*(+0.0) in the reference: adding a
+// zero to an accumulator that starts at +0.0 (and therefore is never -0.0) is the identity,
+// so S = 0 there reproduces it bit-for-bit.  All arithmetic is binary64 round-to-nearest
+// without contraction, i.e. numpy's `acc += weight * densify(g)` on the upcast inputs; the
+// single rounding to the output type happens at the store.  With params/buf the momentum
+// step runs in the epilogue on the unrounded float64 aggregate (nn.py:169-171 order), with
+// p and buf loaded in the prologue so their latency overlaps the fold.  No atomics: the
+// result is deterministic and identical on every rank.
 #include "common.cuh"
 
 namespace sg {
 
 constexpr int AG_THREADS = 256;
-constexpr int AG_TILE = 4096;  // 16 elements per thread
-constexpr int AG_PER_THREAD = AG_TILE / AG_THREADS;
-static_assert(AG_PER_THREAD == 16, "4 groups of 4 consecutive elements per thread");
+constexpr int AG_TILE = 4096;
+constexpr int AG_GROUPS = 4;  // 4 groups of 4 consecutive elements per thread
+
+template <typename TI> struct AgTraits;
+template <> struct AgTraits<float> { static constexpr int ECAP = 4096; };
+template <> struct AgTraits<double> { static constexpr int ECAP = 1024; };
 
 template <typename TI> SG_DEV void load4(const TI* p, double (&o)[4]);
 template <> SG_DEV void load4<float>(const float* p, double (&o)[4]) {
@@ -40,6 +50,27 @@ template <> SG_DEV void load4_rw<float>(const float* p, double (&o)[4]) {
     o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
 }
 template <> SG_DEV void load4_rw<double>(const double* p, double (&o)[4]) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0];
+    const double2 b = reinterpret_cast<const double2*>(p)[1];
+    o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+}
+// Raw 4-element loads (no conversion): streaming for read-once inputs, cached for p/buf.
+template <typename T> SG_DEV void stream4(const T* p, T (&o)[4]);
+template <> SG_DEV void stream4<float>(const float* p, float (&o)[4]) {
+    const float4 v = ld_stream(reinterpret_cast<const float4*>(p));
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+template <> SG_DEV void stream4<double>(const double* p, double (&o)[4]) {
+    const double2 a = ld_stream(reinterpret_cast<const double2*>(p));
+    const double2 b = ld_stream(reinterpret_cast<const double2*>(p) + 1);
+    o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+}
+template <typename T> SG_DEV void raw4(const T* p, T (&o)[4]);
+template <> SG_DEV void raw4<float>(const float* p, float (&o)[4]) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+template <> SG_DEV void raw4<double>(const double* p, double (&o)[4]) {
     const double2 a = reinterpret_cast<const double2*>(p)[0];
     const double2 b = reinterpret_cast<const double2*>(p)[1];
     o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
@@ -62,26 +93,37 @@ SG_DEV void sgd_elem(double g, double& p, double& b, double lr, double mu, doubl
     b = buf;
 }
 
-// off[j][t] = number of row-j entries with index < t*AG_TILE, t in [0, ntiles].
+// off[j][t] = number of row-j entries with index < t*AG_TILE, t in [0, ntiles]; one thread
+// per entry writes the boundaries between its predecessor's tile and its own.
 __global__ void k_tile_offsets(const uint32_t* __restrict__ idx, const long long* __restrict__ row_ptr,
                                const uint8_t* __restrict__ comp, long long ntiles, int* __restrict__ off) {
+    constexpr int U = 4;  // entries per thread per iteration (independent loads in flight)
     const int j = blockIdx.y;
     if (comp && !comp[j]) return;
     const long long r0 = row_ptr[j], nnz = row_ptr[j + 1] - r0;
     int* o = off + (long long)j * (ntiles + 1);
     const uint32_t* ix = idx + r0;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    const long long first = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x * U;
+    const long long first = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * U;
     if (nnz == 0) {
-        for (long long t = first; t <= ntiles; t += stride) o[t] = 0;
+        for (long long t = first / U; t <= ntiles; t += stride / U) o[t] = 0;
         return;
     }
-    for (long long p = first; p < nnz; p += stride) {
-        const long long tc = ix[p] / AG_TILE;
-        const long long tp = p ? (long long)(ix[p - 1] / AG_TILE) : -1;
-        for (long long t = tp + 1; t <= tc; ++t) o[t] = (int)p;
-        if (p == nnz - 1)
-            for (long long t = tc + 1; t <= ntiles; ++t) o[t] = (int)nnz;
+    for (long long p0 = first; p0 < nnz; p0 += stride) {
+        long long tl[U + 1];
+#pragma unroll
+        for (int u = 0; u <= U; ++u) {
+            const long long p = p0 + u - 1;
+            tl[u] = p < 0 ? -1 : (p < nnz ? (long long)(ix[p] / AG_TILE) : -2);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = p0 + u;
+            if (p >= nnz) break;
+            for (long long t = tl[u] + 1; t <= tl[u + 1]; ++t) o[t] = (int)p;
+            if (p == nnz - 1)
+                for (long long t = tl[u + 1] + 1; t <= ntiles; ++t) o[t] = (int)nnz;
+        }
     }
 }
 
@@ -102,77 +144,362 @@ template <typename TI, typename TO> struct AggArgs {
 };
 
 template <typename TI, typename TO>
-__global__ void __launch_bounds__(AG_THREADS)
+__global__ void __launch_bounds__(AG_THREADS, 2)
 k_aggregate(const AggArgs<TI, TO> a) {
-    __shared__ double acc[AG_TILE];
+    constexpr int ECAP = AgTraits<TI>::ECAP;
+    __shared__ TI S[AG_TILE];
+    __shared__ uint16_t ent_pos[ECAP];
+    __shared__ TI ent_val[ECAP];
+    __shared__ long long s_lo[MAX_WORKERS];
+    __shared__ int s_cnt[MAX_WORKERS];
+    __shared__ int s_pre[MAX_WORKERS + 1];
     __shared__ uint8_t s_comp[MAX_WORKERS];
-    __shared__ long long s_rp[MAX_WORKERS];
     const int tid = threadIdx.x;
     const long long tile = blockIdx.x;
     const long long tb = tile * AG_TILE;
     const bool full = a.vec_ok && tb + AG_TILE <= a.dim;
-    for (int i = tid; i < a.nw; i += AG_THREADS) {
-        s_comp[i] = a.comp ? a.comp[i] : 0;
-        s_rp[i] = a.row_ptr ? a.row_ptr[i] : 0;
+    const bool first = a.first != 0;
+
+    // prologue: optimizer state loads in flight first, then the sparse ranges
+    TO pv[AG_GROUPS][4], bv[AG_GROUPS][4];
+    if (a.p && full) {
+#pragma unroll
+        for (int r = 0; r < AG_GROUPS; ++r) {
+            const long long e = tb + r * (AG_THREADS * 4) + tid * 4;
+            raw4<TO>(a.p + e, pv[r]);
+            if (!first) raw4<TO>(a.buf + e, bv[r]);
+            else bv[r][0] = bv[r][1] = bv[r][2] = bv[r][3] = (TO)0;
+        }
+    }
+    for (int j = tid; j < a.nw; j += AG_THREADS) {
+        const uint8_t c = a.comp ? a.comp[j] : 0;
+        s_comp[j] = c;
+        int n = 0;
+        if (c) {
+            const int* o = a.off + (long long)j * (a.ntiles + 1);
+            const int lo = o[tile], hi = o[tile + 1];
+            s_lo[j] = a.row_ptr[j] + lo;
+            n = hi - lo;
+        }
+        s_cnt[j] = n;
     }
 #pragma unroll
-    for (int q = 0; q < AG_PER_THREAD; ++q) acc[q * AG_THREADS + tid] = 0.0;
+    for (int r = 0; r < AG_GROUPS; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) S[r * (AG_THREADS * 4) + tid * 4 + c] = (TI)0;
     __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int j = 0; j < a.nw; ++j) {
+            s_pre[j] = acc;
+            acc += s_cnt[j];
+        }
+        s_pre[a.nw] = acc;
+    }
+    __syncthreads();
+    const int E = s_pre[a.nw];
+
+    // stage entries [e0, e0 + n) of the flattened (worker-major) tile entry list
+    auto stage = [&](int e0, int n) {
+        for (int q = tid; q < n; q += AG_THREADS) {
+            const int e = e0 + q;
+            int lo = 0, hi = a.nw;  // s_pre[lo] <= e < s_pre[hi]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= e) lo = mid;
+                else hi = mid;
+            }
+            const long long gi = s_lo[lo] + (e - s_pre[lo]);
+            ent_pos[q] = (uint16_t)(a.idx[gi] - (uint32_t)tb);
+            ent_val[q] = a.val[gi];
+        }
+    };
+    int st_lo = 0, st_hi = 0;
+    if (E > 0) {
+        st_hi = E < ECAP ? E : ECAP;
+        stage(0, st_hi);
+    }
+    __syncthreads();
+
+    double acc[AG_GROUPS][4];
+#pragma unroll
+    for (int r = 0; r < AG_GROUPS; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+
+    TI x[AG_GROUPS][4];
+    auto load_dense = [&](int j) {
+        const TI* row = a.dense + (long long)j * a.ld + tb;
+#pragma unroll
+        for (int r = 0; r < AG_GROUPS; ++r) {
+            const int e = r * (AG_THREADS * 4) + tid * 4;
+            if (full) {
+                stream4<TI>(row + e, x[r]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) x[r][c] = tb + e + c < a.dim ? row[e + c] : (TI)0;
+            }
+        }
+    };
+    int loaded = -1;
     for (int j = 0; j < a.nw; ++j) {
         const double wj = a.w[j];
         if (!s_comp[j]) {
-            const TI* row = a.dense + (long long)j * a.ld + tb;
+            if (loaded != j) load_dense(j);
+            TI xc[AG_GROUPS][4];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int e = r * (AG_THREADS * 4) + tid * 4;
-                double x[4];
-                if (full) {
-                    load4<TI>(row + e, x);
-                } else {
+            for (int r = 0; r < AG_GROUPS; ++r)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) x[c] = tb + e + c < a.dim ? (double)row[e + c] : 0.0;
+                for (int c = 0; c < 4; ++c) xc[r][c] = x[r][c];
+            // prefetch the next dense worker while folding this one
+            int nxt = j + 1;
+            while (nxt < a.nw && s_comp[nxt] && s_cnt[nxt] == 0) ++nxt;
+            if (nxt < a.nw && !s_comp[nxt]) {
+                load_dense(nxt);
+                loaded = nxt;
+            }
+#pragma unroll
+            for (int r = 0; r < AG_GROUPS; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] = dadd(acc[r][c], dmul(wj, (double)xc[r][c]));
+        } else if (s_cnt[j] > 0) {
+            int e = s_pre[j];
+            const int e_end = e + s_cnt[j];
+            while (e < e_end) {
+                if (e >= st_hi) {  // uniform: refill the staging buffer
+                    __syncthreads();
+                    st_lo = e;
+                    st_hi = (E - e) < ECAP ? E : e + ECAP;
+                    stage(st_lo, st_hi - st_lo);
+                    __syncthreads();
                 }
+                const int piece = e_end < st_hi ? e_end : st_hi;
+                for (int q = e + tid; q < piece; q += AG_THREADS) S[ent_pos[q - st_lo]] = ent_val[q - st_lo];
+                e = piece;
+            }
+            __syncthreads();
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[e + c] = dadd(acc[e + c], dmul(wj, x[c]));
-            }
-        } else {
-            const int* o = a.off + (long long)j * (a.ntiles + 1);
-            const long long lo = s_rp[j] + o[tile], hi = s_rp[j] + o[tile + 1];
-            for (long long i = lo + tid; i < hi; i += AG_THREADS) {
-                const int pos = (int)(a.idx[i] - (uint32_t)tb);
-                acc[pos] = dadd(acc[pos], dmul(wj, (double)a.val[i]));
-            }
+            for (int r = 0; r < AG_GROUPS; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int q = r * (AG_THREADS * 4) + tid * 4 + c;
+                    const TI s = S[q];
+                    acc[r][c] = dadd(acc[r][c], dmul(wj, (double)s));
+                    S[q] = (TI)0;
+                }
+            __syncthreads();
         }
-        __syncthreads();
     }
-    const bool first = a.first != 0;
+
+    // epilogue
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < AG_GROUPS; ++r) {
         const int e = r * (AG_THREADS * 4) + tid * 4;
-        double g[4] = {acc[e], acc[e + 1], acc[e + 2], acc[e + 3]};
         if (full) {
-            if (a.out) store4<TO>(a.out + tb + e, g);
+            if (a.out) store4<TO>(a.out + tb + e, acc[r]);
             if (a.p) {
-                double pv[4], bv[4] = {0.0, 0.0, 0.0, 0.0};
-                load4_rw<TO>(a.p + tb + e, pv);
-                if (!first) load4_rw<TO>(a.buf + tb + e, bv);
+                double pd[4], bd[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) sgd_elem(g[c], pv[c], bv[c], a.lr, a.mu, a.wd, first);
-                store4<TO>(a.p + tb + e, pv);
-                store4<TO>(a.buf + tb + e, bv);
+                for (int c = 0; c < 4; ++c) {
+                    pd[c] = (double)pv[r][c];
+                    bd[c] = (double)bv[r][c];
+                    sgd_elem(acc[r][c], pd[c], bd[c], a.lr, a.mu, a.wd, first);
+                }
+                store4<TO>(a.p + tb + e, pd);
+                store4<TO>(a.buf + tb + e, bd);
             }
         } else {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const long long q = tb + e + c;
                 if (q >= a.dim) continue;
-                if (a.out) a.out[q] = (TO)g[c];
+                if (a.out) a.out[q] = (TO)acc[r][c];
                 if (a.p) {
-                    double pv = a.p[q], bv = first ? 0.0 : (double)a.buf[q];
-                    sgd_elem(g[c], pv, bv, a.lr, a.mu, a.wd, first);
-                    a.p[q] = (TO)pv;
-                    a.buf[q] = (TO)bv;
+                    double pq = a.p[q], bq = first ? 0.0 : (double)a.buf[q];
+                    sgd_elem(acc[r][c], pq, bq, a.lr, a.mu, a.wd, first);
+                    a.p[q] = (TO)pq;
+                    a.buf[q] = (TO)bq;
                 }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// k_merge: the float32 fast path of k_aggregate.  Thread t owns the 16 contiguous positions
+// [16t, 16t+16) of the tile.  All sparse workers' in-tile entries are staged into shared
+// memory with one batched load (worker-major); for worker j each thread binary-searches its
+// first entry and merges its <= 16 entries into register accumulators, so workers are
+// folded in order without a block barrier per worker.  Dense rows and p/buf use L1-cached
+// 128-bit loads (the two 16-byte halves of each sector come from consecutive instructions).
+// ---------------------------------------------------------------------------------------
+constexpr int MG_ECAP = 4096;
+
+template <typename TO>
+__global__ void __launch_bounds__(AG_THREADS, 2)
+k_merge(const AggArgs<float, TO> a) {
+    __shared__ uint16_t ent_pos[MG_ECAP];
+    __shared__ float ent_val[MG_ECAP];
+    __shared__ long long s_lo[MAX_WORKERS];
+    __shared__ int s_cnt[MAX_WORKERS];
+    __shared__ int s_pre[MAX_WORKERS + 1];
+    __shared__ uint8_t s_comp[MAX_WORKERS];
+    const int tid = threadIdx.x;
+    const long long tile = blockIdx.x;
+    const long long tb = tile * AG_TILE;
+    const int q0 = tid * 16;
+    const bool full = a.vec_ok && tb + AG_TILE <= a.dim;
+    const bool first = a.first != 0;
+
+    float pv[16], bv[16];
+    if (a.p && full) {
+        const float4* pp = reinterpret_cast<const float4*>(a.p + tb + q0);
+        const float4* bp = reinterpret_cast<const float4*>(a.buf + tb + q0);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const float4 u = pp[r];
+            pv[4 * r] = u.x; pv[4 * r + 1] = u.y; pv[4 * r + 2] = u.z; pv[4 * r + 3] = u.w;
+            if (!first) {
+                const float4 z = bp[r];
+                bv[4 * r] = z.x; bv[4 * r + 1] = z.y; bv[4 * r + 2] = z.z; bv[4 * r + 3] = z.w;
+            } else {
+                bv[4 * r] = bv[4 * r + 1] = bv[4 * r + 2] = bv[4 * r + 3] = 0.f;
+            }
+        }
+    }
+    for (int j = tid; j < a.nw; j += AG_THREADS) {
+        const uint8_t c = a.comp ? a.comp[j] : 0;
+        s_comp[j] = c;
+        int n = 0;
+        if (c) {
+            const int* o = a.off + (long long)j * (a.ntiles + 1);
+            const int lo = o[tile], hi = o[tile + 1];
+            s_lo[j] = a.row_ptr[j] + lo;
+            n = hi - lo;
+        }
+        s_cnt[j] = n;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int j = 0; j < a.nw; ++j) {
+            s_pre[j] = acc;
+            acc += s_cnt[j];
+        }
+        s_pre[a.nw] = acc;
+    }
+    __syncthreads();
+    const int E = s_pre[a.nw];
+    // stage entries [e0, e1) (whole workers) of the flattened worker-major entry list
+    auto stage = [&](int e0, int e1) {
+        for (int q = tid; q < e1 - e0; q += AG_THREADS) {
+            const int e = e0 + q;
+            int lo = 0, hi = a.nw;  // s_pre[lo] <= e < s_pre[hi]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= e) lo = mid;
+                else hi = mid;
+            }
+            const long long gi = s_lo[lo] + (e - s_pre[lo]);
+            ent_pos[q] = (uint16_t)(a.idx[gi] - (uint32_t)tb);
+            ent_val[q] = a.val[gi];
+        }
+    };
+    // the staged window holds whole workers [w_lo, w_hi)
+    int w_lo = 0, w_hi = 0;
+    auto fill = [&](int j0) {
+        int j1 = j0;
+        while (j1 < a.nw && s_pre[j1 + 1] - s_pre[j0] <= MG_ECAP) ++j1;
+        if (j1 == j0) j1 = j0 + 1;  // cannot happen for f32 (<= 4096 entries per worker)
+        stage(s_pre[j0], s_pre[j1]);
+        w_lo = j0;
+        w_hi = j1;
+    };
+    if (E > 0) fill(0);
+    __syncthreads();
+
+    double acc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+    for (int j = 0; j < a.nw; ++j) {
+        const double wj = a.w[j];
+        if (!s_comp[j]) {
+            float x[16];
+            const float* row = a.dense + (long long)j * a.ld + tb + q0;
+            if (full) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const float4 u = reinterpret_cast<const float4*>(row)[r];
+                    x[4 * r] = u.x; x[4 * r + 1] = u.y; x[4 * r + 2] = u.z; x[4 * r + 3] = u.w;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) x[c] = tb + q0 + c < a.dim ? row[c] : 0.f;
+            }
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[c] = dadd(acc[c], dmul(wj, (double)x[c]));
+        } else if (s_cnt[j] > 0) {
+            if (j >= w_hi) {  // uniform across the block
+                __syncthreads();
+                fill(j);
+                __syncthreads();
+            }
+            const int base = s_pre[w_lo];
+            int i = s_pre[j] - base, end = i + s_cnt[j];
+            {  // first entry with pos >= q0
+                int lo = i, hi = end;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if ((int)ent_pos[mid] < q0) lo = mid + 1;
+                    else hi = mid;
+                }
+                i = lo;
+            }
+            int pos = i < end ? (int)ent_pos[i] : 1 << 30;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                if (pos == q0 + c) {
+                    acc[c] = dadd(acc[c], dmul(wj, (double)ent_val[i]));
+                    ++i;
+                    pos = i < end ? (int)ent_pos[i] : 1 << 30;
+                }
+            }
+        }
+    }
+    if (full) {
+        if (a.out) {
+            float4* op = reinterpret_cast<float4*>(a.out + tb + q0);
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                op[r] = make_float4((float)acc[4 * r], (float)acc[4 * r + 1], (float)acc[4 * r + 2], (float)acc[4 * r + 3]);
+        }
+        if (a.p) {
+            float4* pp = reinterpret_cast<float4*>(a.p + tb + q0);
+            float4* bp = reinterpret_cast<float4*>(a.buf + tb + q0);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double pd[4], bd[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    pd[c] = (double)pv[4 * r + c];
+                    bd[c] = (double)bv[4 * r + c];
+                    sgd_elem(acc[4 * r + c], pd[c], bd[c], a.lr, a.mu, a.wd, first);
+                }
+                pp[r] = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
+                bp[r] = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const long long q = tb + q0 + c;
+            if (q >= a.dim) continue;
+            if (a.out) a.out[q] = (TO)acc[c];
+            if (a.p) {
+                double pq = a.p[q], bq = first ? 0.0 : (double)a.buf[q];
+                sgd_elem(acc[c], pq, bq, a.lr, a.mu, a.wd, first);
+                a.p[q] = (TO)pq;
+                a.buf[q] = (TO)bq;
             }
         }
     }
@@ -206,9 +533,9 @@ inline long long ag_tiles(long long dim) { return (dim + AG_TILE - 1) / AG_TILE;
 
 template <typename TI, typename TO>
 int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dense, long long ld,
-              const uint32_t* idx, const TI* val, const long long* row_ptr, long long dim, TO* out,
-              TO* p, TO* buf, double lr, double mu, double wd, int first, void* ws, size_t ws_bytes,
-              cudaStream_t stream) {
+              const uint32_t* idx, const TI* val, const long long* row_ptr, const int* tile_off,
+              long long dim, TO* out, TO* p, TO* buf, double lr, double mu, double wd, int first,
+              void* ws, size_t ws_bytes, cudaStream_t stream) {
     if (nw < 1 || dim < 1 || !weights || (!out && !p)) return SG_ERR_INVALID;
     if (nw > MAX_WORKERS || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
     if (p && !buf) return SG_ERR_INVALID;
@@ -217,12 +544,15 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
     if (!dense && !comp) return SG_ERR_INVALID;
     if (dense && ld < dim) return SG_ERR_INVALID;
     const long long ntiles = ag_tiles(dim);
-    int* off = nullptr;
-    if (comp) {
+    const int* off = tile_off;
+    if (comp && !off) {
         const size_t need = sizeof(int) * (size_t)nw * (size_t)(ntiles + 1);
         if (!ws || ws_bytes < need) return SG_ERR_WORKSPACE;
-        off = reinterpret_cast<int*>(ws);
-        k_tile_offsets<<<dim3(64, nw), 256, 0, stream>>>(idx, row_ptr, comp, ntiles, off);
+        int* o = reinterpret_cast<int*>(ws);
+        // rows are sized on the device; a fixed grid strides over each row
+        long long blocks = ((long long)num_sms() * 8 + nw - 1) / nw;
+        k_tile_offsets<<<dim3((unsigned)blocks, nw), 256, 0, stream>>>(idx, row_ptr, comp, ntiles, o);
+        off = o;
     }
     AggArgs<TI, TO> a;
     for (int j = 0; j < nw; ++j) a.w[j] = weights[j];
@@ -248,7 +578,10 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
     if (out) vec = vec && reinterpret_cast<size_t>(out) % 16 == 0;
     if (p) vec = vec && reinterpret_cast<size_t>(p) % 16 == 0 && reinterpret_cast<size_t>(buf) % 16 == 0;
     a.vec_ok = vec;
-    k_aggregate<TI, TO><<<(unsigned)ntiles, AG_THREADS, 0, stream>>>(a);
+    if constexpr (sizeof(TI) == 4 && sizeof(TO) == 4)
+        k_merge<TO><<<(unsigned)ntiles, AG_THREADS, 0, stream>>>(a);
+    else
+        k_aggregate<TI, TO><<<(unsigned)ntiles, AG_THREADS, 0, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
@@ -279,26 +612,26 @@ size_t sg_aggregate_workspace_bytes(int nw, int64_t dim) {
 
 int sg_weighted_aggregate_f32(int nw, const double* weights, const uint8_t* compressed,
                               const float* dense, int64_t ld_dense, const uint32_t* idx,
-                              const float* val, const int64_t* row_ptr, int64_t dim, float* out,
-                              float* params, float* momentum_buf, double lr, double momentum,
-                              double weight_decay, int first_step, void* workspace,
-                              size_t workspace_bytes, void* stream) {
+                              const float* val, const int64_t* row_ptr, const int32_t* tile_off,
+                              int64_t dim, float* out, float* params, float* momentum_buf,
+                              double lr, double momentum, double weight_decay, int first_step,
+                              void* workspace, size_t workspace_bytes, void* stream) {
     return aggregate<float, float>(nw, weights, compressed, dense, ld_dense, idx, val,
-                                   reinterpret_cast<const long long*>(row_ptr), dim, out, params,
-                                   momentum_buf, lr, momentum, weight_decay, first_step, workspace,
-                                   workspace_bytes, (cudaStream_t)stream);
+                                   reinterpret_cast<const long long*>(row_ptr), tile_off, dim, out,
+                                   params, momentum_buf, lr, momentum, weight_decay, first_step,
+                                   workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 int sg_weighted_aggregate_f64(int nw, const double* weights, const uint8_t* compressed,
                               const double* dense, int64_t ld_dense, const uint32_t* idx,
-                              const double* val, const int64_t* row_ptr, int64_t dim, double* out,
-                              double* params, double* momentum_buf, double lr, double momentum,
-                              double weight_decay, int first_step, void* workspace,
-                              size_t workspace_bytes, void* stream) {
+                              const double* val, const int64_t* row_ptr, const int32_t* tile_off,
+                              int64_t dim, double* out, double* params, double* momentum_buf,
+                              double lr, double momentum, double weight_decay, int first_step,
+                              void* workspace, size_t workspace_bytes, void* stream) {
     return aggregate<double, double>(nw, weights, compressed, dense, ld_dense, idx, val,
-                                     reinterpret_cast<const long long*>(row_ptr), dim, out, params,
-                                     momentum_buf, lr, momentum, weight_decay, first_step, workspace,
-                                     workspace_bytes, (cudaStream_t)stream);
+                                     reinterpret_cast<const long long*>(row_ptr), tile_off, dim, out,
+                                     params, momentum_buf, lr, momentum, weight_decay, first_step,
+                                     workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 int sg_sgd_momentum_f32(float* params, float* momentum_buf, const float* grad, int64_t dim,

@@ -1,25 +1,36 @@
 // Top-k sparsification + squared norms + adaptive compression gate (items 3 and 4).
 //
-// Replaces reference pkg/src/streamsgd/comm.py:90-96 (topk_sparsify: lexsort on -|g| with
-// index tie-break, kept indices re-sorted ascending) and comm.py:129-160 (compression_gate:
-// s_full = g.g, s_topk = v.v, EWMA, rho, decision) for the k workers of one GPU at once.
+// Replaces reference pkg/src/streamsgd/comm.py:90-96 (topk_sparsify: np.lexsort on -|g| with
+// the index as tie-break, first m re-sorted ascending) and comm.py:129-160
+// (compression_gate: s_full = g.g, s_topk = v.v, EWMA, rho, decision) for the k workers of
+// one GPU in one launch sequence, with no host synchronisation.
 //
-// Pipeline per call (all on one stream, no host synchronisation):
-//   k_estimate  one CTA per worker: zero the call's scratch, read a stratified random sample
-//               of S keys from HBM and select the r_est-th largest -> a threshold `est`
-//               that is below the true m-th largest key with overwhelming probability.
-//   k_main      the single full read of the bucket: persistent CTAs take 16 KB tiles by
-//               ticket, compute fp64 sum of squares per tile, and stably compact every
-//               element with key >= est into a candidate buffer (~1.2-2 m entries) using a
-//               decoupled look-back scan, so candidates stay in ascending index order.
-//   k_select    2048-bin radix-select rounds over the candidates (L2-resident) with a
-//               range-normalised digit; the last CTA of each round picks the bin.  If the
-//               estimate undershot (fewer than m candidates) or the buffer overflowed (heavy
-//               ties), the rounds run over the full row instead: same result, slower.
-//   k_final     stable compaction of {key > T} U {first `need` keys == T} -> idx/val in
-//               ascending index order, plus per-tile fp64 sum of kept squares.
-//   k_gate      fixed-order reduction of the per-tile partials -> norms2, then the gate
-//               update in IEEE round-to-nearest (comm.py:143-159 order of operations).
+//   k_estimate  one CTA per worker: zero the call's small scratch, read a stratified random
+//               sample of S keys and radix-select its r_est-th largest -> `est`, below the
+//               true m-th largest key with probability ~1 - 1e-9.
+//   k_main      THE full read of the bucket (4 B/element).  grid = (B, k); CTA b owns a
+//               contiguous range of 16 KB tiles ("segment") and walks it with the next
+//               tile's 128-bit loads in flight, accumulating the fp64 sum of squares and
+//               appending every element with key >= est to the segment's candidate list
+//               (global index + value, ascending).  No inter-CTA dependency, so the pass
+//               streams at HBM bandwidth; the candidate lists are ~1.2-2 m entries in total
+//               and stay L2-resident.  It also builds the round-0 radix histogram of the
+//               candidate keys (1024 bins over [est, sample max], top bin open-ended); the
+//               last CTA of each worker finds the bin holding rank m.
+//   k_main(fb)  only if fewer than m keys reached `est` (estimate undershot): the same pass
+//               with est = 0.  Early-exits otherwise.
+//   k_collect   one CTA per segment: counts the segment's candidates above the rank-m bin
+//               and appends those inside it (key, index) to a boundary buffer.  Its last CTA
+//               finishes the select in shared memory (T, the m-th largest key), resolves ties
+//               at T by index (the first `need` indices among keys == T are kept), counts the
+//               kept elements per segment and scans them into per-segment output bases.
+//   k_resolve   only for oversized boundary sets (heavy ties): multi-CTA radix rounds.
+//   k_write     one CTA per segment: kept = key > T or (key == T and idx <= idx_cut); an
+//               in-CTA ordered scan places them at the segment's base -> idx/val ascending,
+//               plus the fp64 sum of kept squares and the per-4096-element merge offsets.
+//               (Oversized-tie mode: a decoupled look-back over segments with the exact
+//               tie rank instead.)  Its last CTA reduces the norms in a fixed order and
+//               applies the gate in IEEE round-to-nearest (comm.py:143-159 operation order).
 #include "common.cuh"
 
 namespace sg {
@@ -28,50 +39,57 @@ constexpr int TK_THREADS = 256;
 constexpr int TK_ROUNDS = 4;  // 16-byte vectors per thread per tile
 constexpr int TK_NW = TK_THREADS / 32;
 static_assert(TK_ROUNDS * TK_NW == 32, "one warp scans the per-(round, warp) totals");
+constexpr int H0_BITS = 10;
+constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
+constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
+constexpr int MERGE_TILE = 4096;
+constexpr int RESOLVE_SMEM = 16384;  // boundary entries resolved inside one CTA
 
-enum { MODE_CAND = 0, MODE_FULL = 1 };
+enum { MODE_NORMAL = 0, MODE_FALLBACK = 1 };
+enum { WR_FAST = 0, WR_SLOW = 1 };
 
 template <typename T> struct TopkTraits;
 template <> struct TopkTraits<float> {
-    static constexpr int SAMPLE = 32768;  // keys in shared memory: 128 KB
-    static constexpr int ROUNDS_MAX = 3;  // ceil(31 / 11)
+    static constexpr int SAMPLE = 16384;
+    static constexpr int ROUNDS_MAX = 3;  // after round 0: <= 31 bits left (open top bin)
 };
 template <> struct TopkTraits<double> {
-    static constexpr int SAMPLE = 16384;
-    static constexpr int ROUNDS_MAX = 6;  // ceil(63 / 11)
+    static constexpr int SAMPLE = 8192;
+    static constexpr int ROUNDS_MAX = 6;  // after round 0: <= 63 bits left (open top bin)
 };
 
 template <typename T> constexpr int tile_elems() { return TK_THREADS * TK_ROUNDS * Vec16<T>::N; }
 
 template <typename K> struct SelState {
-    K lo;                      // current key range [lo, lo + span]
-    K span;
+    K est, smax;               // from k_estimate
+    K lo, span;                // current key range [lo, lo + span]
     K T;                       // final threshold key
     unsigned long long rank;   // remaining 1-based rank from the top inside the range
-    unsigned long long gt;     // elements above the range (all kept)
-    unsigned long long n_src;  // elements in the source (candidates or the full row)
-    int shift;
+    unsigned long long h;      // keys inside the range
+    unsigned idx_cut;          // keys == T are kept iff index <= idx_cut (fast mode)
+    int shift0, shift;         // round-0 / current digit shift
     int done;
-    int mode;
-    int error;
+    int mode;                  // MODE_NORMAL / MODE_FALLBACK
+    int wmode;                 // WR_FAST / WR_SLOW
 };
 
 // --------------------------------------------------------------------------------------
-// Host-side layout of the caller workspace.
+// Host-side plan of the caller workspace.
 // --------------------------------------------------------------------------------------
 struct TopkPlan {
-    int k;
+    int k, nseg, tps;  // segments per worker, tiles per segment
     long long dim, m;
-    long long s_eff, stride, r_est, cap;
-    long long nt_main, nt_fin;
-    size_t off_status_main, off_status_fin, off_hist, off_ctr, off_count, off_maxkey, zero_end;
-    size_t off_est, off_sel, off_sum_main, off_sum_fin, off_cidx, off_cval, total;
+    long long s_eff, stride, r_est;
+    long long ntiles, segcap;
+    size_t off_count, off_maxkey, off_ctr, off_bndn, off_hist0, off_hist0fb, off_histr, off_status, zero_end;
+    size_t off_sel, off_cnt, off_tstart, off_segcnt, off_seggt, off_segbase, off_pmain, off_pwrite,
+        off_cidx, off_cval, off_bkey, off_bidx, total;
 };
 
-template <typename T> TopkPlan make_plan(int k, long long dim, long long m) {
+template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int segs_per_worker) {
     using K = typename KeyOf<T>::K;
     TopkPlan p{};
     p.k = k;
@@ -79,62 +97,66 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m) {
     p.m = m;
     const long long S = TopkTraits<T>::SAMPLE;
     p.s_eff = dim < S ? dim : S;
-    p.stride = dim / (p.s_eff > 0 ? p.s_eff : 1);
+    p.stride = dim / p.s_eff;
     if (p.s_eff == dim) {
         p.r_est = m;  // exact sample: est is the true m-th largest key
-        p.cap = dim;
     } else {
-        // Keep enough sample ranks that count(key >= est) >= m fails with probability
-        // ~1e-9 (6 sigma of the binomial sample count) plus a constant for tiny m.
+        // count(key >= est) < m needs a 6-sigma binomial deviation of the sample (~1e-9).
         const double q = (double)m / (double)dim;
         const double mean = q * (double)p.s_eff;
         const double sd = __builtin_sqrt(mean * (1.0 - q) + 1.0);
-        long long r = (long long)(mean + 6.0 * sd + 8.0) + 1;
-        p.r_est = r;
-        if (r >= p.s_eff) {
-            p.cap = dim;
-        } else {
-            const double expect = (double)r * (double)dim / (double)p.s_eff;
-            const double c = expect * 1.25 + 4096.0;
-            p.cap = c >= (double)dim ? dim : (long long)c;
-        }
+        p.r_est = (long long)(mean + 6.0 * sd + 8.0) + 1;
     }
-    p.cap = (p.cap + 3) / 4 * 4;
     const long long te = tile_elems<T>();
-    p.nt_main = (dim + te - 1) / te;
-    const long long src_max = p.cap > dim ? p.cap : dim;
-    p.nt_fin = (src_max + te - 1) / te;
+    p.ntiles = (dim + te - 1) / te;
+    long long segs = segs_per_worker < 1 ? 1 : segs_per_worker;
+    if (segs > BMAX) segs = BMAX;
+    if (segs > p.ntiles) segs = p.ntiles;
+    p.tps = (int)((p.ntiles + segs - 1) / segs);
+    p.nseg = (int)((p.ntiles + p.tps - 1) / p.tps);
+    p.segcap = (long long)p.tps * te;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
-    p.off_status_main = take(sizeof(unsigned long long) * (size_t)k * p.nt_main);
-    p.off_status_fin = take(sizeof(unsigned long long) * (size_t)k * p.nt_fin);
-    p.off_hist = take(sizeof(unsigned) * (size_t)k * TopkTraits<T>::ROUNDS_MAX * SEL_BINS);
-    p.off_ctr = take(sizeof(unsigned) * (2 + (size_t)k * TopkTraits<T>::ROUNDS_MAX));
-    p.off_count = take(sizeof(unsigned long long) * (size_t)k);
-    p.off_maxkey = take(sizeof(K) * (size_t)k);
+    p.off_count = take(sizeof(unsigned long long) * 2 * k);  // [pass][k]
+    p.off_maxkey = take(sizeof(K) * k);
+    p.off_ctr = take(sizeof(unsigned) * (8 + 8 * (size_t)k));
+    p.off_bndn = take(sizeof(unsigned long long) * k);
+    p.off_hist0 = take(sizeof(unsigned) * (size_t)k * H0_BINS);
+    p.off_hist0fb = take(sizeof(unsigned) * (size_t)k * H0_BINS);
+    p.off_histr = take(sizeof(unsigned) * (size_t)k * TopkTraits<T>::ROUNDS_MAX * SEL_BINS);
+    p.off_status = take(sizeof(unsigned long long) * (size_t)k * p.nseg);
     p.zero_end = o;
-    p.off_est = take(sizeof(K) * (size_t)k);
-    p.off_sel = take(sizeof(SelState<K>) * (size_t)k);
-    p.off_sum_main = take(sizeof(double) * (size_t)k * p.nt_main);
-    p.off_sum_fin = take(sizeof(double) * (size_t)k * p.nt_fin);
-    p.off_cidx = take(sizeof(uint32_t) * (size_t)k * p.cap);
-    p.off_cval = take(sizeof(T) * (size_t)k * p.cap);
+    p.off_sel = take(sizeof(SelState<K>) * k);
+    p.off_cnt = take(sizeof(unsigned) * (size_t)k * p.ntiles);
+    p.off_tstart = take(sizeof(unsigned) * (size_t)k * p.ntiles);
+    p.off_segcnt = take(sizeof(unsigned) * (size_t)k * p.nseg);
+    p.off_seggt = take(sizeof(unsigned) * (size_t)k * p.nseg);
+    p.off_segbase = take(sizeof(unsigned) * (size_t)k * p.nseg);
+    p.off_pmain = take(sizeof(double) * (size_t)k * p.nseg);
+    p.off_pwrite = take(sizeof(double) * (size_t)k * p.nseg);
+    const size_t cap = (size_t)k * p.nseg * p.segcap;
+    p.off_cidx = take(sizeof(uint32_t) * cap);
+    p.off_cval = take(sizeof(T) * cap);
+    p.off_bkey = take(sizeof(K) * cap);
+    p.off_bidx = take(sizeof(uint32_t) * cap);
     p.total = o + 256;  // slack for base alignment
     return p;
 }
 
 // --------------------------------------------------------------------------------------
-// Shared select helper: warp 0 locates the bin holding the rank-th largest element.
-// hist has SEL_BINS counters (bins past the range are zero).  Lane L owns the 64 bins
-// [2047-64L-63, 2047-64L]; a warp scan from the top finds the owning lane, which walks
-// its bins.  Returns (bin, count strictly above the bin); bin = -1 if rank > total.
+// Radix-select helpers.
 // --------------------------------------------------------------------------------------
+// Warp-cooperative: locate the bin holding the rank-th largest element of an NB-bin
+// histogram.  Lane L owns the PER bins ending at top_L = NB-1-PER*L; it reads them in a
+// lane-rotated order so the 32 lanes never hit the same shared-memory bank.
+template <int NB>
 SG_DEV void find_bin_from_top(const unsigned* hist, unsigned long long rank, int& bin,
                               unsigned long long& above) {
+    constexpr int PER = NB / 32;
     const int lane = threadIdx.x & 31;
-    const int top = SEL_BINS - 1 - 64 * lane;
+    const int top = NB - 1 - PER * lane;
     unsigned long long s = 0;
-    for (int i = 0; i < 64; ++i) s += hist[top - i];
+    for (int i = 0; i < PER; ++i) s += hist[top - ((i + lane) & (PER - 1))];
     unsigned long long incl = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -152,7 +174,7 @@ SG_DEV void find_bin_from_top(const unsigned* hist, unsigned long long rank, int
     unsigned long long a = 0;
     if (lane == f) {
         unsigned long long cum = incl - s;
-        for (int i = 0; i < 64; ++i) {
+        for (int i = 0; i < PER; ++i) {
             const unsigned h = hist[top - i];
             if (cum + h >= rank) {
                 b = top - i;
@@ -166,38 +188,41 @@ SG_DEV void find_bin_from_top(const unsigned* hist, unsigned long long rank, int
     above = __shfl_sync(FULL, a, f);
 }
 
-template <typename K> SG_DEV int digit_shift(K span) {
+template <typename K> SG_DEV int digit_shift(K span, int bits) {
     const int bl = bitlen<K>(span);
-    return bl > SEL_BITS ? bl - SEL_BITS : 0;
+    return bl > bits ? bl - bits : 0;
 }
 
-// Advance a select state after the bin holding the remaining rank was found.
-template <typename K> SG_DEV void advance(SelState<K>& s, int bin, unsigned long long above) {
-    if (bin < 0) {
-        s.error = 1;
-        s.done = 1;
-        s.T = 0;
-        return;
-    }
+// Digit of `key` in a range starting at lo with shift s and an open-ended top bin.
+template <typename K> SG_DEV unsigned digit(K key, K lo, int shift, unsigned nb) {
+    const K d = (key - lo) >> shift;
+    return d >= (K)(nb - 1) ? nb - 1 : (unsigned)d;
+}
+
+// Narrow the state to bin `bin` of an nb-bin round whose top bin is open-ended.
+template <typename K>
+SG_DEV void narrow(SelState<K>& s, int bin, unsigned long long above, unsigned long long h,
+                   unsigned nb, int next_bits) {
     const K off = (K)bin << s.shift;
     s.rank -= above;
-    s.gt += above;
-    s.lo += off;
-    if (s.shift == 0) {
-        s.span = 0;
-        s.T = s.lo;
+    s.h = h;
+    const K lo = s.lo + off;
+    const K rest = s.span - off;
+    K span = rest;
+    if ((unsigned)bin != nb - 1) {
+        const K width = ((K)1 << s.shift) - 1;
+        span = rest < width ? rest : width;
+    }
+    s.lo = lo;
+    s.span = span;
+    if (span == 0) {
+        s.T = lo;
         s.done = 1;
         return;
     }
-    const K width = ((K)1 << s.shift) - 1;
-    const K rest = s.span - off;
-    s.span = rest < width ? rest : width;
-    s.shift = digit_shift<K>(s.span);
+    s.shift = digit_shift<K>(span, next_bits);
 }
 
-// --------------------------------------------------------------------------------------
-// k_estimate: zero scratch, sample, select the r_est-th largest sample key.
-// --------------------------------------------------------------------------------------
 SG_DEV unsigned long long mix64(unsigned long long x) {
     x ^= x >> 33;
     x *= 0xff51afd7ed558ccdull;
@@ -207,86 +232,192 @@ SG_DEV unsigned long long mix64(unsigned long long x) {
     return x;
 }
 
+// In-block radix select of the rank-th largest of n keys (shared memory) inside st's range.
+template <typename K, int THREADS>
+SG_DEV void block_select(const K* keys, long long n, SelState<K>& st, unsigned* hist) {
+    const int tid = threadIdx.x;
+    for (int round = 0; round < 8; ++round) {
+        __syncthreads();
+        if (st.done) break;
+        for (int i = tid; i < SEL_BINS; i += THREADS) hist[i] = 0;
+        __syncthreads();
+        const K lo = st.lo, span = st.span;
+        const int shift = st.shift;
+        for (long long i = tid; i < n; i += THREADS) {
+            const K key = keys[i];
+            if (key >= lo && key - lo <= span) atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            int bin;
+            unsigned long long above;
+            find_bin_from_top<SEL_BINS>(hist, st.rank, bin, above);
+            if (tid == 0) {
+                if (bin < 0) {
+                    st.done = 1;  // inconsistent counts (cannot happen): keep the lowest key
+                    st.T = st.lo;
+                } else {
+                    narrow<K>(st, bin, above, hist[bin], SEL_BINS, SEL_BITS);
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// In-block: the r-th SMALLEST (1-based) of the u32 values v[i] with flag[i] set; three
+// radix rounds (11, 11, 10 bits), each bin located by a warp scan from the top with the
+// rank mirrored (r-th smallest of N = (N - r + 1)-th largest).
+template <int THREADS>
+SG_DEV unsigned block_select_small_u32(const unsigned* v, const uint8_t* flag, long long n,
+                                       unsigned long long r, unsigned* hist, unsigned* s_res) {
+    const int tid = threadIdx.x;
+    unsigned lo = 0;
+    unsigned long long rank = r;
+    const int shifts[3] = {21, 10, 0};
+    for (int round = 0; round < 3; ++round) {
+        const int shift = shifts[round];
+        const unsigned nb = round == 2 ? 1024u : 2048u;
+        for (int i = tid; i < SEL_BINS; i += THREADS) hist[i] = 0;
+        __syncthreads();
+        for (long long i = tid; i < n; i += THREADS) {
+            if (!flag[i]) continue;
+            const unsigned x = v[i];
+            if (x < lo) continue;
+            const unsigned long long d = ((unsigned long long)(x - lo)) >> shift;
+            if (d < nb) atomicAdd(&hist[d], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            unsigned long long tot = 0;
+            for (int i = tid; i < SEL_BINS; i += 32) tot += hist[i];
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+            int bin;
+            unsigned long long above;
+            find_bin_from_top<SEL_BINS>(hist, tot - rank + 1, bin, above);
+            if (tid == 0) {
+                const unsigned long long below = tot - above - hist[bin];
+                s_res[0] = lo + ((unsigned)bin << shift);
+                s_res[1] = (unsigned)(rank - below);
+            }
+        }
+        __syncthreads();
+        lo = s_res[0];
+        rank = s_res[1];
+        __syncthreads();
+    }
+    return lo;
+}
+
+// --------------------------------------------------------------------------------------
+// k_estimate
+// --------------------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(EST_THREADS)
-k_estimate(const T* __restrict__ g, long long ld, long long s_eff, long long stride,
-           long long r_est, typename KeyOf<T>::K* __restrict__ est,
-           uint4* __restrict__ zero, long long zero_vec) {
+k_estimate(const T* __restrict__ g, long long ld, long long s_eff, long long stride, long long r_est,
+           SelState<typename KeyOf<T>::K>* __restrict__ sel, uint4* __restrict__ zero, long long zero_vec) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* sk = reinterpret_cast<K*>(smem_raw);
     __shared__ unsigned hist[SEL_BINS];
     __shared__ SelState<K> st;
+    __shared__ K s_min[32], s_max[32];
     const int w = blockIdx.x, tid = threadIdx.x;
-
-    // Zero the per-call scratch (look-back status words, histograms, counters).
     for (long long i = (long long)w * EST_THREADS + tid; i < zero_vec; i += (long long)gridDim.x * EST_THREADS)
         zero[i] = make_uint4(0, 0, 0, 0);
 
     const T* row = g + (long long)w * ld;
-    for (long long i = tid; i < s_eff; i += EST_THREADS) {
-        long long pos = i * stride;
-        if (stride > 1) pos += (long long)(mix64((unsigned long long)i * 0x9e3779b97f4a7c15ull + (unsigned long long)w) % (unsigned long long)stride);
-        sk[i] = KO::key(row[pos]);
+    K mn = KO::KMAX, mx = 0;
+    constexpr int BATCH = 8;
+    const unsigned long long ustride = (unsigned long long)stride;
+    for (long long base = 0; base < s_eff; base += (long long)EST_THREADS * BATCH) {
+        T v[BATCH];
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+            const long long i = base + (long long)u * EST_THREADS + tid;
+            long long pos = i * stride;
+            if (stride > 1) {
+                // multiply-high keeps the offset uniform in [0, stride) without a division
+                const unsigned h = (unsigned)mix64((unsigned long long)i * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
+                pos += (long long)(((unsigned long long)h * ustride) >> 32);
+            }
+            v[u] = i < s_eff ? __ldg(row + pos) : (T)0;
+        }
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+            const long long i = base + (long long)u * EST_THREADS + tid;
+            if (i < s_eff) {
+                const K key = KO::key(v[u]);
+                sk[i] = key;
+                mn = key < mn ? key : mn;
+                mx = key > mx ? key : mx;
+            }
+        }
     }
-    if (tid == 0) {
-        st.lo = 0;
-        st.span = KO::KMAX;
-        st.rank = (unsigned long long)r_est;
-        st.gt = 0;
-        st.n_src = (unsigned long long)s_eff;
-        st.shift = digit_shift<K>(st.span);
-        st.done = 0;
-        st.mode = MODE_FULL;
-        st.error = 0;
-        st.T = 0;
+    for (int o = 16; o > 0; o >>= 1) {
+        const K a = __shfl_xor_sync(FULL, mn, o), b = __shfl_xor_sync(FULL, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+    if ((tid & 31) == 0) {
+        s_min[tid >> 5] = mn;
+        s_max[tid >> 5] = mx;
     }
     __syncthreads();
-    if (r_est > s_eff) {
-        if (tid == 0) est[w] = 0;
-        return;
-    }
-    for (int round = 0; round < TopkTraits<T>::ROUNDS_MAX + 1; ++round) {
-        for (int i = tid; i < SEL_BINS; i += EST_THREADS) hist[i] = 0;
-        __syncthreads();
-        const K lo = st.lo, span = st.span;
-        const int shift = st.shift;
-        for (long long i = tid; i < s_eff; i += EST_THREADS) {
-            const K key = sk[i];
-            if (key >= lo && key - lo <= span) atomicAdd(&hist[(unsigned)((key - lo) >> shift)], 1u);
+    if (tid == 0) {
+        K a = KO::KMAX, b = 0;
+        for (int i = 0; i < EST_THREADS / 32; ++i) {
+            a = s_min[i] < a ? s_min[i] : a;
+            b = s_max[i] > b ? s_max[i] : b;
         }
-        __syncthreads();
-        if (tid < 32) {
-            int bin;
-            unsigned long long above;
-            find_bin_from_top(hist, st.rank, bin, above);
-            if (tid == 0) advance<K>(st, bin, above);
+        st.lo = a;
+        st.span = b - a;
+        st.shift = digit_shift<K>(st.span, SEL_BITS);
+        st.rank = (unsigned long long)r_est;
+        st.h = 0;
+        st.T = 0;
+        st.done = r_est > s_eff;
+        st.smax = b;
+        if (!st.done && st.span == 0) {
+            st.done = 1;
+            st.T = a;
         }
-        __syncthreads();
-        if (st.done) break;
     }
-    if (tid == 0) est[w] = st.done && !st.error ? st.T : (K)0;
+    block_select<K, EST_THREADS>(sk, s_eff, st, hist);
+    if (tid == 0) {
+        SelState<K> o = st;
+        o.est = r_est > s_eff ? (K)0 : st.T;
+        o.shift0 = digit_shift<K>(o.smax > o.est ? o.smax - o.est : (K)0, H0_BITS);
+        o.done = 0;
+        o.mode = MODE_NORMAL;
+        o.wmode = WR_FAST;
+        o.idx_cut = 0xffffffffu;
+        sel[w] = o;
+    }
 }
 
 // --------------------------------------------------------------------------------------
-// k_main: the single streaming pass over the bucket.
+// k_main: the streaming pass (pass 0) or the fallback pass (pass 1).
 // --------------------------------------------------------------------------------------
 template <typename T> struct MainArgs {
     const T* g;
-    long long ld, dim, ntiles, cap;
-    int k, vec_ok;
-    const typename KeyOf<T>::K* est;
-    uint32_t* cidx;
+    long long ld, dim, ntiles, m, segcap;
+    int k, vec_ok, pass, nseg, tps;
+    SelState<typename KeyOf<T>::K>* sel;
+    unsigned* cnt;      // [k][ntiles]
+    unsigned* tstart;   // [k][ntiles] offset of the tile's first candidate in its segment
+    unsigned* segcnt;   // [k][nseg]
+    uint32_t* cidx;     // [k][nseg][segcap]
     T* cval;
-    unsigned long long* status;
-    unsigned* ticket;
-    double* sumsq;
-    unsigned long long* count;
+    double* pmain;      // [k][nseg]
+    unsigned long long* count;  // [2][k]
     typename KeyOf<T>::K* maxkey;
+    unsigned* hist0;    // [k][H0_BINS] (pass-specific)
+    unsigned* done;     // [k] (pass-specific)
 };
 
-// Per-lane exclusive prefix and warp total of a small count n (0..4) via 3 ballots.
+// Per-lane exclusive prefix and warp total of a small count n (0..7) via 3 ballots.
 SG_DEV void warp_scan_small(unsigned n, unsigned& excl, unsigned& total) {
     const unsigned b0 = __ballot_sync(FULL, n & 1u);
     const unsigned b1 = __ballot_sync(FULL, n & 2u);
@@ -297,73 +428,88 @@ SG_DEV void warp_scan_small(unsigned n, unsigned& excl, unsigned& total) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TK_THREADS)
+SG_DEV void load_tile(const T* row, long long base, long long dim, bool vec, typename Vec16<T>::V (&x)[TK_ROUNDS]) {
+    using VT = Vec16<T>;
+    constexpr int V = VT::N;
+    const int tid = threadIdx.x;
+    if (vec && base + tile_elems<T>() <= dim) {
+        const typename VT::V* src = reinterpret_cast<const typename VT::V*>(row + base);
+#pragma unroll
+        for (int r = 0; r < TK_ROUNDS; ++r) x[r] = ld_stream(src + r * TK_THREADS + tid);
+    } else {
+#pragma unroll
+        for (int r = 0; r < TK_ROUNDS; ++r) {
+            T t[V];
+#pragma unroll
+            for (int c = 0; c < V; ++c) {
+                const long long e = base + (long long)(r * TK_THREADS + tid) * V + c;
+                t[c] = e < dim ? row[e] : (T)0;
+            }
+            if constexpr (V == 4) x[r] = make_float4(t[0], t[1], t[2], t[3]);
+            else x[r] = make_double2(t[0], t[1]);
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TK_THREADS, 4)
 k_main(MainArgs<T> a) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
     using VT = Vec16<T>;
     constexpr int V = VT::N;
     constexpr int TILE = tile_elems<T>();
-    __shared__ unsigned s_ticket;
+    __shared__ unsigned hist[H0_BINS];
     __shared__ unsigned s_wtot[32];
     __shared__ unsigned s_woff[32];
-    __shared__ double s_wsum[TK_NW];
-    __shared__ K s_wmax[TK_NW];
-    __shared__ unsigned long long s_base;
-    __shared__ K s_blkmax[MAX_WORKERS];
+    __shared__ double s_red[TK_NW];
+    __shared__ K s_kmax[TK_NW];
+    __shared__ unsigned s_run, s_tbase;
+    __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned long long total = (unsigned long long)a.k * (unsigned long long)a.ntiles;
-    for (int i = tid; i < a.k; i += TK_THREADS) s_blkmax[i] = 0;
-
-    for (;;) {
-        if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
-        __syncthreads();
-        const unsigned long long t = s_ticket;
-        if (t >= total) break;
-        const int w = (int)(t / (unsigned long long)a.ntiles);
-        const long long tile = (long long)(t - (unsigned long long)w * a.ntiles);
-        const T* row = a.g + (long long)w * a.ld;
+    const int w = blockIdx.y, seg = blockIdx.x;
+    SelState<K>* stp = a.sel + w;
+    if (a.pass == 1 && stp->mode != MODE_FALLBACK) return;
+    const K est = a.pass == 1 ? (K)0 : stp->est;
+    const int shift0 = a.pass == 1 ? digit_shift<K>(KO::KMAX, H0_BITS) : stp->shift0;
+    for (int i = tid; i < H0_BINS; i += TK_THREADS) hist[i] = 0;
+    if (tid == 0) s_run = 0;
+    const T* row = a.g + (long long)w * a.ld;
+    const bool vec = a.vec_ok;
+    const long long t_begin = (long long)seg * a.tps;
+    const long long t_end = t_begin + a.tps < a.ntiles ? t_begin + a.tps : a.ntiles;
+    uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
+    T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
+    double ss = 0.0;
+    K mx = 0;
+    typename VT::V x[TK_ROUNDS];
+    if (t_begin < t_end) load_tile<T>(row, t_begin * TILE, a.dim, vec, x);
+    __syncthreads();
+    for (long long tile = t_begin; tile < t_end; ++tile) {
         const long long base = tile * TILE;
-        const K est = a.est[w];
-
         T v[TK_ROUNDS][V];
+#pragma unroll
+        for (int r = 0; r < TK_ROUNDS; ++r)
+#pragma unroll
+            for (int c = 0; c < V; ++c) v[r][c] = VT::get(x[r], c);
+        if (tile + 1 < t_end) load_tile<T>(row, base + TILE, a.dim, vec, x);  // next tile in flight
         unsigned cm[TK_ROUNDS];
-        double ss = 0.0;
-        K mx = 0;
-        if (a.vec_ok && base + TILE <= a.dim) {
-            typename VT::V x[TK_ROUNDS];
-            const typename VT::V* src = reinterpret_cast<const typename VT::V*>(row + base);
+        const bool full = base + TILE <= a.dim;
 #pragma unroll
-            for (int r = 0; r < TK_ROUNDS; ++r) x[r] = ld_stream(src + r * TK_THREADS + tid);
+        for (int r = 0; r < TK_ROUNDS; ++r) {
+            cm[r] = 0;
 #pragma unroll
-            for (int r = 0; r < TK_ROUNDS; ++r) {
-                cm[r] = 0;
-#pragma unroll
-                for (int c = 0; c < V; ++c) {
-                    const T e = VT::get(x[r], c);
-                    v[r][c] = e;
-                    const K key = KO::key(e);
+            for (int c = 0; c < V; ++c) {
+                const bool ok = full || base + (long long)(r * TK_THREADS + tid) * V + c < a.dim;
+                const T e = v[r][c];
+                const K key = KO::key(e);
+                if (ok) {
                     mx = key > mx ? key : mx;
-                    cm[r] |= (key >= est ? 1u : 0u) << c;
                     ss = fma((double)e, (double)e, ss);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < TK_ROUNDS; ++r) {
-                cm[r] = 0;
-#pragma unroll
-                for (int c = 0; c < V; ++c) {
-                    const long long e = base + (long long)(r * TK_THREADS + tid) * V + c;
-                    const bool ok = e < a.dim;
-                    const T x = ok ? row[e] : (T)0;
-                    v[r][c] = x;
-                    const K key = KO::key(x);
-                    if (ok) {
-                        mx = key > mx ? key : mx;
-                        ss = fma((double)x, (double)x, ss);
+                    if (key >= est) {
+                        cm[r] |= 1u << c;
+                        atomicAdd(&hist[digit<K>(key, est, shift0, H0_BINS)], 1u);
                     }
-                    cm[r] |= (ok && key >= est ? 1u : 0u) << c;
                 }
             }
         }
@@ -374,116 +520,288 @@ k_main(MainArgs<T> a) {
             warp_scan_small(__popc(cm[r]), lp[r], tot);
             if (lane == 0) s_wtot[r * TK_NW + warp] = tot;
         }
-        ss = warp_sum(ss);
-        mx = warp_max<K>(mx);
-        if (lane == 0) {
-            s_wsum[warp] = ss;
-            s_wmax[warp] = mx;
-        }
         __syncthreads();
         if (warp == 0) {
-            const unsigned x = s_wtot[lane];
-            unsigned incl = x;
+            const unsigned xw = s_wtot[lane];
+            unsigned incl = xw;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned y = __shfl_up_sync(FULL, incl, o);
                 if (lane >= o) incl += y;
             }
-            s_woff[lane] = incl - x;
-            const unsigned tot = __shfl_sync(FULL, incl, 31);
-            const unsigned long long pre = lookback(a.status + (long long)w * a.ntiles, tile, tot);
-            if (lane == 0) {
-                s_base = pre;
-                double tsum = 0.0;
-                K tmax = 0;
-                for (int i = 0; i < TK_NW; ++i) {
-                    tsum = dadd(tsum, s_wsum[i]);
-                    tmax = s_wmax[i] > tmax ? s_wmax[i] : tmax;
-                }
-                a.sumsq[(long long)w * a.ntiles + tile] = tsum;
-                if (tmax > s_blkmax[w]) s_blkmax[w] = tmax;
-                if (tile == a.ntiles - 1) a.count[w] = pre + tot;
+            s_woff[lane] = incl - xw;
+            if (lane == 31) {
+                const long long ti = (long long)w * a.ntiles + tile;
+                a.cnt[ti] = incl;
+                a.tstart[ti] = s_run;
+                s_tbase = s_run;
+                s_run += incl;
             }
         }
         __syncthreads();
-        const unsigned long long b = s_base;
-        uint32_t* cidx = a.cidx + (long long)w * a.cap;
-        T* cval = a.cval + (long long)w * a.cap;
+        const unsigned tb = s_tbase;
 #pragma unroll
         for (int r = 0; r < TK_ROUNDS; ++r) {
             if (!cm[r]) continue;
-            unsigned long long pos = b + s_woff[r * TK_NW + warp] + lp[r];
+            unsigned pos = tb + s_woff[r * TK_NW + warp] + lp[r];
 #pragma unroll
             for (int c = 0; c < V; ++c) {
                 if ((cm[r] >> c) & 1u) {
-                    if (pos < (unsigned long long)a.cap) {
-                        cidx[pos] = (uint32_t)(base + (long long)(r * TK_THREADS + tid) * V + c);
-                        cval[pos] = v[r][c];
-                    }
+                    ci[pos] = (uint32_t)(base + (long long)(r * TK_THREADS + tid) * V + c);
+                    cv[pos] = v[r][c];
                     ++pos;
                 }
             }
         }
     }
+    // per-segment partials: fixed element order and fixed reduction tree -> deterministic
+    ss = warp_sum(ss);
+    mx = warp_max<K>(mx);
+    if (lane == 0) {
+        s_red[warp] = ss;
+        s_kmax[warp] = mx;
+    }
     __syncthreads();
-    for (int i = tid; i < a.k; i += TK_THREADS)
-        if (s_blkmax[i]) atomicMax(a.maxkey + i, s_blkmax[i]);
+    if (tid == 0) {
+        double t = 0.0;
+        K km = 0;
+        for (int i = 0; i < TK_NW; ++i) {
+            t = dadd(t, s_red[i]);
+            km = s_kmax[i] > km ? s_kmax[i] : km;
+        }
+        a.pmain[(long long)w * a.nseg + seg] = t;
+        a.segcnt[(long long)w * a.nseg + seg] = s_run;
+        if (km) atomicMax(a.maxkey + w, km);
+        if (s_run) atomicAdd(a.count + (long long)a.pass * a.k + w, (unsigned long long)s_run);
+    }
+    unsigned* gh = a.hist0 + (long long)w * H0_BINS;
+    for (int i = tid; i < H0_BINS; i += TK_THREADS)
+        if (hist[i]) atomicAdd(gh + i, hist[i]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.done + w, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // last CTA of this worker: round-0 pick
+    for (int i = tid; i < H0_BINS; i += TK_THREADS) hist[i] = __ldcg(gh + i);
+    __syncthreads();
+    if (warp == 0) {
+        SelState<K> s = *stp;
+        const unsigned long long C = __ldcg(a.count + (long long)a.pass * a.k + w);
+        const K maxk = __ldcg(a.maxkey + w);
+        if (C < (unsigned long long)a.m) {
+            if (lane == 0) {  // estimate undershot (pass 0 only): run the fallback pass
+                s.mode = MODE_FALLBACK;
+                *stp = s;
+            }
+        } else {
+            s.lo = est;
+            s.span = maxk - est;
+            s.shift = shift0;
+            s.rank = (unsigned long long)a.m;
+            s.done = 0;
+            if (a.pass == 1) s.est = 0;
+            int bin;
+            unsigned long long above;
+            find_bin_from_top<H0_BINS>(hist, s.rank, bin, above);
+            if (lane == 0) {
+                if (bin < 0) {
+                    s.done = 1;
+                    s.T = est;
+                } else {
+                    narrow<K>(s, bin, above, hist[bin], H0_BINS, SEL_BITS);
+                }
+                *stp = s;
+            }
+        }
+    }
 }
 
 // --------------------------------------------------------------------------------------
-// k_select: one radix-select round.  grid = (blocks_per_worker, k).
+// k_collect: per-segment counts above the rank-m bin + boundary entries; last CTA resolves.
 // --------------------------------------------------------------------------------------
-template <typename T> struct SelArgs {
-    const T* g;
-    long long ld, dim, cap, m;
-    const T* cval;
-    const unsigned long long* count;
-    const typename KeyOf<T>::K* est;
-    const typename KeyOf<T>::K* maxkey;
+template <typename T> struct CollectArgs {
+    long long segcap, cap;
+    int nseg, tps;
     SelState<typename KeyOf<T>::K>* sel;
+    const unsigned* segcnt;
+    const uint32_t* cidx;
+    const T* cval;
+    unsigned* seggt;               // [k][nseg]
+    unsigned* segbase;             // [k][nseg]
+    typename KeyOf<T>::K* bkey;    // [k][cap]
+    uint32_t* bidx;
+    unsigned long long* bndn;      // [k]
+    unsigned* done;                // [k]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(TK_THREADS)
+k_collect(CollectArgs<T> a) {
+    using KO = KeyOf<T>;
+    using K = typename KO::K;
+    constexpr int TILE = tile_elems<T>();
+    __shared__ unsigned s_gt[TK_NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = blockIdx.y, seg = blockIdx.x;
+    const SelState<K> st = a.sel[w];
+    const K lo = st.lo, span = st.span;
+    const long long n = a.segcnt[(long long)w * a.nseg + seg];
+    const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
+    const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
+    K* bk = a.bkey + (long long)w * a.cap;
+    uint32_t* bi = a.bidx + (long long)w * a.cap;
+    unsigned gt = 0;
+    for (long long i0 = 0; i0 < n; i0 += TK_THREADS) {
+        const long long i = i0 + tid;
+        bool in = false;
+        K key = 0;
+        if (i < n) {
+            key = KO::key(cv[i]);
+            in = key >= lo && key - lo <= span;
+            gt += key >= lo && key - lo > span;
+        }
+        const unsigned bal = __ballot_sync(FULL, in);
+        if (bal) {
+            unsigned long long base = 0;
+            const int leader = __ffs(bal) - 1;
+            if (lane == leader) base = atomicAdd(a.bndn + w, (unsigned long long)__popc(bal));
+            base = __shfl_sync(FULL, base, leader);
+            if (in) {
+                const unsigned long long q = base + __popc(bal & lanemask_lt());
+                bk[q] = key;
+                bi[q] = ci[i];
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(FULL, gt, o);
+    if (lane == 0) s_gt[warp] = gt;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned t = 0;
+        for (int i = 0; i < TK_NW; ++i) t += s_gt[i];
+        a.seggt[(long long)w * a.nseg + seg] = t;
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// k_resolve_small: one CTA per worker finishes the select in shared memory when the
+// boundary is small (the normal case): T, the tie cut by index, per-segment output bases.
+// --------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(1024)
+k_resolve_small(CollectArgs<T> a) {
+    using K = typename KeyOf<T>::K;
+    constexpr int TILE = tile_elems<T>();
+    constexpr int NT = 1024;
+    __shared__ unsigned hist[SEL_BINS];
+    __shared__ SelState<K> sst;
+    __shared__ unsigned s_eq, s_res[2];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = blockIdx.x;
+    const unsigned long long h = a.bndn[w];
+    if (h > RESOLVE_SMEM) {
+        if (tid == 0) {
+            SelState<K> s = a.sel[w];
+            s.wmode = WR_SLOW;
+            a.sel[w] = s;
+        }
+        return;
+    }
+    K* sk = reinterpret_cast<K*>(smem_raw);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + RESOLVE_SMEM);
+    uint8_t* sf = reinterpret_cast<uint8_t*>(si + RESOLVE_SMEM);
+    unsigned* kb = reinterpret_cast<unsigned*>(sf + RESOLVE_SMEM);  // [nseg]
+    const K* bk = a.bkey + (long long)w * a.cap;
+    const uint32_t* bi = a.bidx + (long long)w * a.cap;
+    for (long long i = tid; i < (long long)h; i += NT) {
+        sk[i] = bk[i];
+        si[i] = bi[i];
+    }
+    for (int i = tid; i < a.nseg; i += NT) kb[i] = 0;
+    if (tid == 0) {
+        sst = a.sel[w];
+        s_eq = 0;
+    }
+    block_select<K, NT>(sk, (long long)h, sst, hist);
+    const K T_ = sst.T;
+    const unsigned long long need = sst.rank;
+    // ties at T: keep the `need` lowest indices among keys == T
+    unsigned eqc = 0;
+    for (long long i = tid; i < (long long)h; i += NT) {
+        const bool e = sk[i] == T_;
+        sf[i] = e;
+        eqc += e;
+    }
+    atomicAdd(&s_eq, eqc);
+    __syncthreads();
+    unsigned cut = 0xffffffffu;
+    if ((unsigned long long)s_eq > need) cut = block_select_small_u32<NT>(si, sf, (long long)h, need, hist, s_res);
+    __syncthreads();
+    // kept boundary entries per segment
+    for (long long i = tid; i < (long long)h; i += NT) {
+        const K key = sk[i];
+        if (key > T_ || (key == T_ && si[i] <= cut)) atomicAdd(&kb[(si[i] / TILE) / a.tps], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // exclusive scan over segments of (count above the bin + kept boundary)
+        unsigned carry = 0;
+        for (int s0 = 0; s0 < a.nseg; s0 += 32) {
+            const int s = s0 + lane;
+            const unsigned v = s < a.nseg ? a.seggt[(long long)w * a.nseg + s] + kb[s] : 0u;
+            unsigned incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (s < a.nseg) a.segbase[(long long)w * a.nseg + s] = carry + incl - v;
+            carry += __shfl_sync(FULL, incl, 31);
+        }
+        if (lane == 0) {
+            SelState<K> s = sst;
+            s.idx_cut = cut;
+            s.wmode = WR_FAST;
+            s.done = 1;
+            a.sel[w] = s;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// k_resolve: one multi-CTA radix round over an oversized boundary set (slow mode only).
+// --------------------------------------------------------------------------------------
+template <typename T> struct ResolveArgs {
+    long long cap;
+    SelState<typename KeyOf<T>::K>* sel;
+    const typename KeyOf<T>::K* bkey;
+    const unsigned long long* bndn;
     unsigned* hist;   // [k][ROUNDS_MAX][SEL_BINS]
     unsigned* done;   // [k][ROUNDS_MAX]
 };
 
-template <typename T> SG_DEV SelState<typename KeyOf<T>::K> initial_state(const SelArgs<T>& a, int w) {
-    using K = typename KeyOf<T>::K;
-    SelState<K> s;
-    const unsigned long long c = a.count[w];
-    const K mk = a.maxkey[w];
-    const bool cand = c >= (unsigned long long)a.m && c <= (unsigned long long)a.cap;
-    s.mode = cand ? MODE_CAND : MODE_FULL;
-    s.n_src = cand ? c : (unsigned long long)a.dim;
-    s.lo = cand ? a.est[w] : (K)0;
-    s.span = mk >= s.lo ? mk - s.lo : (K)0;
-    s.shift = digit_shift<K>(s.span);
-    s.rank = (unsigned long long)a.m;
-    s.gt = 0;
-    s.T = 0;
-    s.done = 0;
-    s.error = 0;
-    return s;
-}
-
 template <typename T>
 __global__ void __launch_bounds__(256)
-k_select(SelArgs<T> a, int round) {
-    using KO = KeyOf<T>;
-    using K = typename KO::K;
+k_resolve(ResolveArgs<T> a, int round) {
+    using K = typename KeyOf<T>::K;
     __shared__ unsigned hist[SEL_BINS];
     __shared__ SelState<K> st;
     __shared__ int s_last;
     const int w = blockIdx.y, tid = threadIdx.x;
-    if (tid == 0) st = round == 0 ? initial_state<T>(a, w) : a.sel[w];
+    if (tid == 0) st = a.sel[w];
     for (int i = tid; i < SEL_BINS; i += 256) hist[i] = 0;
     __syncthreads();
-    if (st.done) return;
+    if (st.done || st.wmode != WR_SLOW) return;
     const K lo = st.lo, span = st.span;
     const int shift = st.shift;
-    const long long n = (long long)st.n_src;
-    const T* src = st.mode == MODE_CAND ? a.cval + (long long)w * a.cap : a.g + (long long)w * a.ld;
+    const long long n = (long long)a.bndn[w];
+    const K* src = a.bkey + (long long)w * a.cap;
     for (long long i = (long long)blockIdx.x * 256 + tid; i < n; i += (long long)gridDim.x * 256) {
-        const K key = KO::key(src[i]);
-        if (key >= lo && key - lo <= span) atomicAdd(&hist[(unsigned)((key - lo) >> shift)], 1u);
+        const K key = src[i];
+        if (key >= lo && key - lo <= span) atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
     }
     __syncthreads();
     unsigned* gh = a.hist + ((long long)w * TopkTraits<T>::ROUNDS_MAX + round) * SEL_BINS;
@@ -491,10 +809,7 @@ k_select(SelArgs<T> a, int round) {
         if (hist[i]) atomicAdd(gh + i, hist[i]);
     __threadfence();
     __syncthreads();
-    if (tid == 0) {
-        const unsigned prev = atomicAdd(a.done + w * TopkTraits<T>::ROUNDS_MAX + round, 1u);
-        s_last = prev == gridDim.x - 1;
-    }
+    if (tid == 0) s_last = atomicAdd(a.done + w * TopkTraits<T>::ROUNDS_MAX + round, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -503,214 +818,48 @@ k_select(SelArgs<T> a, int round) {
     if (tid < 32) {
         int bin;
         unsigned long long above;
-        find_bin_from_top(hist, st.rank, bin, above);
+        find_bin_from_top<SEL_BINS>(hist, st.rank, bin, above);
         if (tid == 0) {
             SelState<K> s = st;
-            advance<K>(s, bin, above);
+            if (bin < 0) {
+                s.done = 1;
+                s.T = s.lo;
+            } else {
+                narrow<K>(s, bin, above, hist[bin], SEL_BINS, SEL_BITS);
+            }
             a.sel[w] = s;
         }
     }
 }
 
 // --------------------------------------------------------------------------------------
-// k_final: stable compaction of the kept set into idx/val (ascending index order).
+// k_write: ordered compaction of the kept set + merge offsets + (last CTA) norms and gate.
 // --------------------------------------------------------------------------------------
-template <typename T> struct FinArgs {
-    const T* g;
-    long long ld, dim, cap, m, nt_fin;
-    int k, vec_ok;
+template <typename T> struct WriteArgs {
+    long long ntiles, segcap, m;
+    int k, nseg, tps;
+    const SelState<typename KeyOf<T>::K>* sel;
+    const unsigned* tstart;
+    const unsigned* segcnt;
+    const unsigned* segbase;
     const uint32_t* cidx;
     const T* cval;
-    const SelState<typename KeyOf<T>::K>* sel;
-    unsigned long long* status;
-    unsigned* ticket;
+    unsigned long long* status;   // [k][nseg] (slow mode look-back)
+    unsigned* done;
     uint32_t* idx;
     T* val;
-    double* sumsq;
+    int* tile_off;                // [k][ntiles+1] or null (f32 merge offsets)
+    double* pwrite;               // [k][nseg]
+    const double* pmain;          // [k][nseg]
+    double* norms2;
+    sg_gate_state* states;
+    uint8_t* decision;
+    double* rho;
 };
 
 constexpr unsigned long long CNT_BITS = 31;
 constexpr unsigned long long CNT_MASK = (1ull << CNT_BITS) - 1;
 
-template <typename T>
-__global__ void __launch_bounds__(TK_THREADS)
-k_final(FinArgs<T> a) {
-    using KO = KeyOf<T>;
-    using K = typename KO::K;
-    using VT = Vec16<T>;
-    constexpr int V = VT::N;
-    constexpr int TILE = tile_elems<T>();
-    __shared__ long long s_tstart[MAX_WORKERS + 1];
-    __shared__ K s_T[MAX_WORKERS];
-    __shared__ unsigned long long s_need[MAX_WORKERS];
-    __shared__ long long s_n[MAX_WORKERS];
-    __shared__ int s_mode[MAX_WORKERS];
-    __shared__ unsigned s_ticket;
-    __shared__ unsigned s_gtot[32], s_etot[32], s_goff[32], s_eoff[32];
-    __shared__ double s_wsum[TK_NW];
-    __shared__ unsigned long long s_gb, s_eb;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        long long acc = 0;
-        for (int w = 0; w < a.k; ++w) {
-            const SelState<K> s = a.sel[w];
-            s_tstart[w] = acc;
-            s_T[w] = s.T;
-            s_need[w] = s.rank;
-            s_n[w] = (long long)s.n_src;
-            s_mode[w] = s.mode;
-            acc += ((long long)s.n_src + TILE - 1) / TILE;
-        }
-        s_tstart[a.k] = acc;
-    }
-    __syncthreads();
-    const long long total = s_tstart[a.k];
-    for (;;) {
-        if (tid == 0) s_ticket = atomicAdd(a.ticket, 1u);
-        __syncthreads();
-        const long long t = s_ticket;
-        if (t >= total) break;
-        int w = 0;
-        while (s_tstart[w + 1] <= t) ++w;
-        const long long tile = t - s_tstart[w];
-        const long long n = s_n[w];
-        const long long base = tile * TILE;
-        const K T_ = s_T[w];
-        const unsigned long long need = s_need[w];
-        const bool cand = s_mode[w] == MODE_CAND;
-        const T* vsrc = cand ? a.cval + (long long)w * a.cap : a.g + (long long)w * a.ld;
-        const uint32_t* isrc = a.cidx + (long long)w * a.cap;
-
-        T v[TK_ROUNDS][V];
-        uint32_t ix[TK_ROUNDS][V];
-        unsigned gm[TK_ROUNDS], em[TK_ROUNDS];
-        const bool vec = base + TILE <= n && (cand || a.vec_ok);
-        if (vec) {
-            typename VT::V x[TK_ROUNDS];
-            typename VT::I xi[TK_ROUNDS];
-            const typename VT::V* s = reinterpret_cast<const typename VT::V*>(vsrc + base);
-#pragma unroll
-            for (int r = 0; r < TK_ROUNDS; ++r) x[r] = ld_stream(s + r * TK_THREADS + tid);
-            if (cand) {
-                const typename VT::I* si = reinterpret_cast<const typename VT::I*>(isrc + base);
-#pragma unroll
-                for (int r = 0; r < TK_ROUNDS; ++r) xi[r] = ld_stream(si + r * TK_THREADS + tid);
-            }
-#pragma unroll
-            for (int r = 0; r < TK_ROUNDS; ++r) {
-                gm[r] = em[r] = 0;
-#pragma unroll
-                for (int c = 0; c < V; ++c) {
-                    const T e = VT::get(x[r], c);
-                    v[r][c] = e;
-                    uint32_t id;
-                    if (cand) {
-                        if constexpr (V == 4) id = c == 0 ? xi[r].x : c == 1 ? xi[r].y : c == 2 ? xi[r].z : xi[r].w;
-                        else id = c == 0 ? xi[r].x : xi[r].y;
-                    } else {
-                        id = (uint32_t)(base + (long long)(r * TK_THREADS + tid) * V + c);
-                    }
-                    ix[r][c] = id;
-                    const K key = KO::key(e);
-                    gm[r] |= (key > T_ ? 1u : 0u) << c;
-                    em[r] |= (key == T_ ? 1u : 0u) << c;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < TK_ROUNDS; ++r) {
-                gm[r] = em[r] = 0;
-#pragma unroll
-                for (int c = 0; c < V; ++c) {
-                    const long long e = base + (long long)(r * TK_THREADS + tid) * V + c;
-                    const bool ok = e < n;
-                    const T x = ok ? vsrc[e] : (T)0;
-                    v[r][c] = x;
-                    ix[r][c] = ok ? (cand ? isrc[e] : (uint32_t)e) : 0u;
-                    const K key = KO::key(x);
-                    gm[r] |= (ok && key > T_ ? 1u : 0u) << c;
-                    em[r] |= (ok && key == T_ ? 1u : 0u) << c;
-                }
-            }
-        }
-        unsigned lg[TK_ROUNDS], le[TK_ROUNDS];
-#pragma unroll
-        for (int r = 0; r < TK_ROUNDS; ++r) {
-            unsigned tg, te;
-            warp_scan_small(__popc(gm[r]), lg[r], tg);
-            warp_scan_small(__popc(em[r]), le[r], te);
-            if (lane == 0) {
-                s_gtot[r * TK_NW + warp] = tg;
-                s_etot[r * TK_NW + warp] = te;
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const unsigned xg = s_gtot[lane], xe = s_etot[lane];
-            unsigned ig = xg, ie = xe;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned yg = __shfl_up_sync(FULL, ig, o);
-                const unsigned ye = __shfl_up_sync(FULL, ie, o);
-                if (lane >= o) {
-                    ig += yg;
-                    ie += ye;
-                }
-            }
-            s_goff[lane] = ig - xg;
-            s_eoff[lane] = ie - xe;
-            const unsigned long long tg = __shfl_sync(FULL, ig, 31), te = __shfl_sync(FULL, ie, 31);
-            const unsigned long long pre =
-                lookback(a.status + (long long)w * a.nt_fin, tile, (tg << CNT_BITS) | te);
-            if (lane == 0) {
-                s_gb = pre >> CNT_BITS;
-                s_eb = pre & CNT_MASK;
-            }
-        }
-        __syncthreads();
-        const unsigned long long gb = s_gb, eb = s_eb;
-        uint32_t* oi = a.idx + (long long)w * a.m;
-        T* ov = a.val + (long long)w * a.m;
-        double ss = 0.0;
-#pragma unroll
-        for (int r = 0; r < TK_ROUNDS; ++r) {
-            unsigned long long g0 = gb + s_goff[r * TK_NW + warp] + lg[r];
-            unsigned long long e0 = eb + s_eoff[r * TK_NW + warp] + le[r];
-#pragma unroll
-            for (int c = 0; c < V; ++c) {
-                const bool isg = (gm[r] >> c) & 1u, ise = (em[r] >> c) & 1u;
-                bool keep = false;
-                unsigned long long pos = 0;
-                if (isg) {
-                    keep = true;
-                    pos = g0 + (e0 < need ? e0 : need);
-                } else if (ise && e0 < need) {
-                    keep = true;
-                    pos = g0 + e0;
-                }
-                if (keep && pos < (unsigned long long)a.m) {
-                    oi[pos] = ix[r][c];
-                    ov[pos] = v[r][c];
-                    ss = fma((double)v[r][c], (double)v[r][c], ss);
-                }
-                g0 += isg;
-                e0 += ise;
-            }
-        }
-        ss = warp_sum(ss);
-        if (lane == 0) s_wsum[warp] = ss;
-        __syncthreads();
-        if (tid == 0) {
-            double tsum = 0.0;
-            for (int i = 0; i < TK_NW; ++i) tsum = dadd(tsum, s_wsum[i]);
-            a.sumsq[(long long)w * a.nt_fin + tile] = tsum;
-        }
-    }
-}
-
-// --------------------------------------------------------------------------------------
-// Gate: EWMA update and decision exactly as comm.py:143-159.
-// --------------------------------------------------------------------------------------
 SG_DEV void gate_math(sg_gate_state& s, double s_full, double s_topk, uint8_t& dec, double& rho) {
     if (!s.initialized) {
         s.ewma_full = s_full;
@@ -732,43 +881,199 @@ SG_DEV void gate_math(sg_gate_state& s, double s_full, double s_topk, uint8_t& d
     rho = r;
 }
 
-SG_DEV double block_sum_fixed(const double* p, long long n, double* red) {
-    const int tid = threadIdx.x;
-    double acc = 0.0;
-    for (long long i = tid; i < n; i += 256) acc = dadd(acc, p[i]);
-    red[tid] = acc;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (tid < s) red[tid] = dadd(red[tid], red[tid + s]);
-        __syncthreads();
-    }
-    const double r = red[0];
-    __syncthreads();
-    return r;
-}
+constexpr int WR_EPT = 4;                      // consecutive entries per thread per chunk
+constexpr int WR_CHUNK = TK_THREADS * WR_EPT;  // 1024
 
 template <typename T>
-__global__ void __launch_bounds__(256)
-k_gate(const double* sum_main, long long nt_main, const double* sum_fin, long long nt_fin,
-       const SelState<typename KeyOf<T>::K>* sel, double* norms2, sg_gate_state* states,
-       uint8_t* decision, double* rho) {
-    __shared__ double red[256];
+__global__ void __launch_bounds__(TK_THREADS)
+k_write(WriteArgs<T> a) {
+    using KO = KeyOf<T>;
+    using K = typename KO::K;
     constexpr int TILE = tile_elems<T>();
-    const int w = blockIdx.x;
-    const double s_full = block_sum_fixed(sum_main + (long long)w * nt_main, nt_main, red);
-    const long long nft = ((long long)sel[w].n_src + TILE - 1) / TILE;
-    const double s_topk = block_sum_fixed(sum_fin + (long long)w * nt_fin, nft, red);
-    if (threadIdx.x == 0) {
-        norms2[2 * w] = s_full;
-        norms2[2 * w + 1] = s_topk;
-        if (states) {
-            sg_gate_state s = states[w];
-            uint8_t d;
-            double r;
-            gate_math(s, s_full, s_topk, d, r);
-            states[w] = s;
-            if (decision) decision[w] = d;
-            if (rho) rho[w] = r;
+    constexpr bool OFFS = TILE == MERGE_TILE;
+    __shared__ unsigned s_gw[TK_NW], s_ew[TK_NW];
+    __shared__ unsigned long long s_gb, s_eb;
+    __shared__ double s_red[TK_NW];
+    __shared__ int s_last;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned* s_ts = reinterpret_cast<unsigned*>(smem_raw);  // [tps] tile starts of this segment
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = blockIdx.y, seg = blockIdx.x;
+    const SelState<K> st = a.sel[w];
+    const K T_ = st.T;
+    const unsigned cut = st.idx_cut;
+    const unsigned long long need = st.rank;
+    const bool slow = st.wmode == WR_SLOW;
+    const long long n = a.segcnt[(long long)w * a.nseg + seg];
+    const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
+    const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
+    const long long t0 = (long long)seg * a.tps;
+    const int nt = (int)(t0 + a.tps < a.ntiles ? a.tps : a.ntiles - t0);
+    int* toff = (OFFS && a.tile_off) ? a.tile_off + (long long)w * (a.ntiles + 1) : nullptr;
+    if (toff)
+        for (int j = tid; j < nt; j += TK_THREADS) s_ts[j] = a.tstart[(long long)w * a.ntiles + t0 + j];
+
+    unsigned long long gb, eb;  // kept-before counters (fast mode: gb only)
+    if (!slow) {
+        gb = a.segbase[(long long)w * a.nseg + seg];
+        eb = 0;
+    } else {
+        // pass 1: counts, then a decoupled look-back over this worker's segments
+        unsigned gc = 0, ec = 0;
+        for (long long i = tid; i < n; i += TK_THREADS) {
+            const K key = KO::key(cv[i]);
+            gc += key > T_;
+            ec += key == T_;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            gc += __shfl_xor_sync(FULL, gc, o);
+            ec += __shfl_xor_sync(FULL, ec, o);
+        }
+        if (lane == 0) {
+            s_gw[warp] = gc;
+            s_ew[warp] = ec;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long gtot = 0, etot = 0;
+            for (int i = 0; i < TK_NW; ++i) {
+                gtot += s_gw[i];
+                etot += s_ew[i];
+            }
+            const unsigned long long pre =
+                lookback(a.status + (long long)w * a.nseg, seg, (gtot << CNT_BITS) | etot);
+            if (lane == 0) {
+                s_gb = pre >> CNT_BITS;
+                s_eb = pre & CNT_MASK;
+            }
+        }
+        __syncthreads();
+        gb = s_gb;
+        eb = s_eb;
+    }
+    __syncthreads();
+    uint32_t* oi = a.idx + (long long)w * a.m;
+    T* ov = a.val + (long long)w * a.m;
+    double ss = 0.0;
+    for (long long c0 = 0; c0 < n; c0 += WR_CHUNK) {
+        unsigned kflag = 0, eflag = 0;
+        T vv[WR_EPT];
+        uint32_t ii[WR_EPT];
+#pragma unroll
+        for (int u = 0; u < WR_EPT; ++u) {
+            const long long e = c0 + tid * WR_EPT + u;
+            vv[u] = (T)0;
+            ii[u] = 0;
+            if (e < n) {
+                vv[u] = cv[e];
+                ii[u] = ci[e];
+                const K key = KO::key(vv[u]);
+                if (!slow) {
+                    kflag |= (key > T_ || (key == T_ && ii[u] <= cut) ? 1u : 0u) << u;
+                } else {
+                    kflag |= (key > T_ ? 1u : 0u) << u;
+                    eflag |= (key == T_ ? 1u : 0u) << u;
+                }
+            }
+        }
+        unsigned gx, gt_, ex = 0, et_ = 0;
+        warp_scan_small(__popc(kflag), gx, gt_);
+        if (slow) warp_scan_small(__popc(eflag), ex, et_);
+        if (lane == 0) {
+            s_gw[warp] = gt_;
+            s_ew[warp] = et_;
+        }
+        __syncthreads();
+        unsigned long long g0 = gb, e0 = eb, gsum = 0, esum = 0;
+        for (int i = 0; i < TK_NW; ++i) {
+            if (i < warp) {
+                g0 += s_gw[i];
+                e0 += s_ew[i];
+            }
+            gsum += s_gw[i];
+            esum += s_ew[i];
+        }
+        g0 += gx;
+        e0 += ex;
+#pragma unroll
+        for (int u = 0; u < WR_EPT; ++u) {
+            const long long e = c0 + tid * WR_EPT + u;
+            if (e >= n) break;
+            const unsigned long long kb4 = slow ? g0 + (e0 < need ? e0 : need) : g0;
+            if (toff) {
+                // tiles whose first candidate is entry e: merge offset = kept before e
+                int lo = 0, hi = nt;  // first j with s_ts[j] >= e
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if ((long long)s_ts[mid] < e) lo = mid + 1;
+                    else hi = mid;
+                }
+                for (int j = lo; j < nt && (long long)s_ts[j] == e; ++j) toff[t0 + j] = (int)kb4;
+            }
+            const bool isk = (kflag >> u) & 1u, ise = (eflag >> u) & 1u;
+            bool keep = false;
+            unsigned long long pos = 0;
+            if (isk) {
+                keep = true;
+                pos = kb4;
+            } else if (ise && e0 < need) {
+                keep = true;
+                pos = g0 + e0;
+            }
+            if (keep && pos < (unsigned long long)a.m) {
+                oi[pos] = ii[u];
+                ov[pos] = vv[u];
+                ss = fma((double)vv[u], (double)vv[u], ss);
+            }
+            g0 += isk;
+            e0 += ise;
+        }
+        gb += gsum;
+        eb += esum;
+        __syncthreads();
+    }
+    if (toff && tid == 0) {
+        // tiles with no candidate at or after the last entry: offset = kept total so far
+        const unsigned long long kept = slow ? gb + (eb < need ? eb : need) : gb;
+        for (int j = 0; j < nt; ++j)
+            if ((long long)s_ts[j] >= n) toff[t0 + j] = (int)kept;
+        if (t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) s_red[warp] = ss;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int i = 0; i < TK_NW; ++i) s = dadd(s, s_red[i]);
+        a.pwrite[(long long)w * a.nseg + seg] = s;
+    }
+    // last CTA overall: fixed-order norm reductions + gate
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.done, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int ww = warp; ww < a.k; ww += TK_NW) {
+        double sf = 0.0, sk = 0.0;
+        for (int i = lane; i < a.nseg; i += 32) {
+            sf = dadd(sf, __ldcg(a.pmain + (long long)ww * a.nseg + i));
+            sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nseg + i));
+        }
+        sf = warp_sum(sf);
+        sk = warp_sum(sk);
+        if (lane == 0) {
+            a.norms2[2 * ww] = sf;
+            a.norms2[2 * ww + 1] = sk;
+            if (a.states) {
+                sg_gate_state s = a.states[ww];
+                uint8_t d;
+                double r;
+                gate_math(s, sf, sk, d, r);
+                a.states[ww] = s;
+                if (a.decision) a.decision[ww] = d;
+                if (a.rho) a.rho[ww] = r;
+            }
         }
     }
 }
@@ -789,106 +1094,156 @@ __global__ void k_gate_update(const double* norms2, int k, sg_gate_state* states
 // --------------------------------------------------------------------------------------
 // Host launcher.
 // --------------------------------------------------------------------------------------
+template <typename T> int segments_per_worker(int k) {
+    int dev = 0, sms = 148, per_sm = 4;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_main<T>, TK_THREADS, 0) != cudaSuccess)
+        per_sm = 4;
+    if (per_sm < 1) per_sm = 1;
+    const int s = sms * per_sm / k;
+    return s < 1 ? 1 : s;
+}
+
 template <typename T>
 int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint32_t* idx, T* val,
-              double* norms2, sg_gate_state* states, uint8_t* decision, double* rho, void* ws,
-              size_t ws_bytes, cudaStream_t stream) {
+              double* norms2, sg_gate_state* states, uint8_t* decision, double* rho, int* tile_off,
+              void* ws, size_t ws_bytes, cudaStream_t stream) {
     using K = typename KeyOf<T>::K;
+    constexpr int TILE = tile_elems<T>();
     if (!g || !idx || !val || !norms2 || k < 1 || dim < 1 || m < 1 || m > dim || ld < dim)
         return SG_ERR_INVALID;
     if (k > MAX_WORKERS || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
-    const TopkPlan p = make_plan<T>(k, dim, m);
+    if (tile_off && TILE != MERGE_TILE) return SG_ERR_INVALID;
+    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k));
     if (!ws || ws_bytes < p.total) return SG_ERR_WORKSPACE;
     unsigned char* base = reinterpret_cast<unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
     auto at = [&](size_t off) { return base + off; };
-    unsigned long long* st_main = reinterpret_cast<unsigned long long*>(at(p.off_status_main));
-    unsigned long long* st_fin = reinterpret_cast<unsigned long long*>(at(p.off_status_fin));
-    unsigned* hist = reinterpret_cast<unsigned*>(at(p.off_hist));
-    unsigned* ctr = reinterpret_cast<unsigned*>(at(p.off_ctr));
     unsigned long long* count = reinterpret_cast<unsigned long long*>(at(p.off_count));
     K* maxkey = reinterpret_cast<K*>(at(p.off_maxkey));
-    K* est = reinterpret_cast<K*>(at(p.off_est));
+    unsigned* ctr = reinterpret_cast<unsigned*>(at(p.off_ctr));
+    unsigned long long* bndn = reinterpret_cast<unsigned long long*>(at(p.off_bndn));
+    unsigned* hist0 = reinterpret_cast<unsigned*>(at(p.off_hist0));
+    unsigned* hist0fb = reinterpret_cast<unsigned*>(at(p.off_hist0fb));
+    unsigned* histr = reinterpret_cast<unsigned*>(at(p.off_histr));
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(at(p.off_status));
     SelState<K>* sel = reinterpret_cast<SelState<K>*>(at(p.off_sel));
-    double* sum_main = reinterpret_cast<double*>(at(p.off_sum_main));
-    double* sum_fin = reinterpret_cast<double*>(at(p.off_sum_fin));
+    unsigned* cnt = reinterpret_cast<unsigned*>(at(p.off_cnt));
+    unsigned* tstart = reinterpret_cast<unsigned*>(at(p.off_tstart));
+    unsigned* segcnt = reinterpret_cast<unsigned*>(at(p.off_segcnt));
+    unsigned* seggt = reinterpret_cast<unsigned*>(at(p.off_seggt));
+    unsigned* segbase = reinterpret_cast<unsigned*>(at(p.off_segbase));
+    double* pmain = reinterpret_cast<double*>(at(p.off_pmain));
+    double* pwrite = reinterpret_cast<double*>(at(p.off_pwrite));
     uint32_t* cidx = reinterpret_cast<uint32_t*>(at(p.off_cidx));
     T* cval = reinterpret_cast<T*>(at(p.off_cval));
+    K* bkey = reinterpret_cast<K*>(at(p.off_bkey));
+    uint32_t* bidx = reinterpret_cast<uint32_t*>(at(p.off_bidx));
+    // counters: [1] write done, [8 + w] main done, [8 + k + w] fb done, [8 + 2k + w] collect
+    // done, [8 + 3k + w*ROUNDS + r] resolve done
+    unsigned* c_main = ctr + 8;
+    unsigned* c_fb = ctr + 8 + k;
+    unsigned* c_col = ctr + 8 + 2 * k;
+    unsigned* c_res = ctr + 8 + 3 * k;
+    const long long capw = (long long)p.nseg * p.segcap;
 
     const bool vec_ok = (reinterpret_cast<size_t>(g) % 16 == 0) && ((ld * (long long)sizeof(T)) % 16 == 0);
     const int sms = num_sms();
 
-    // 1. estimate (+ zero the scratch)
+    // 1. estimate (+ zero the small scratch, incl. the slow-mode look-back status words)
     const size_t est_smem = sizeof(K) * (size_t)TopkTraits<T>::SAMPLE;
     cudaFuncSetAttribute(k_estimate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)est_smem);
-    k_estimate<T><<<k, EST_THREADS, est_smem, stream>>>(g, ld, p.s_eff, p.stride, p.r_est, est,
+    k_estimate<T><<<k, EST_THREADS, est_smem, stream>>>(g, ld, p.s_eff, p.stride, p.r_est, sel,
                                                          reinterpret_cast<uint4*>(base),
                                                          (long long)(p.zero_end / 16));
-    // 2. main streaming pass
+    // 2. main streaming pass, then the (normally empty) fallback pass
     MainArgs<T> ma;
     ma.g = g;
     ma.ld = ld;
     ma.dim = dim;
-    ma.ntiles = p.nt_main;
-    ma.cap = p.cap;
+    ma.ntiles = p.ntiles;
+    ma.m = m;
+    ma.segcap = p.segcap;
     ma.k = k;
     ma.vec_ok = vec_ok;
-    ma.est = est;
+    ma.pass = 0;
+    ma.nseg = p.nseg;
+    ma.tps = p.tps;
+    ma.sel = sel;
+    ma.cnt = cnt;
+    ma.tstart = tstart;
+    ma.segcnt = segcnt;
     ma.cidx = cidx;
     ma.cval = cval;
-    ma.status = st_main;
-    ma.ticket = ctr;
-    ma.sumsq = sum_main;
+    ma.pmain = pmain;
     ma.count = count;
     ma.maxkey = maxkey;
-    long long tiles = (long long)k * p.nt_main;
-    long long grid_main = (long long)sms * 8;
-    if (grid_main > tiles) grid_main = tiles;
-    k_main<T><<<(unsigned)grid_main, TK_THREADS, 0, stream>>>(ma);
-    // 3. select rounds
-    SelArgs<T> sa;
-    sa.g = g;
-    sa.ld = ld;
-    sa.dim = dim;
-    sa.cap = p.cap;
-    sa.m = m;
-    sa.cval = cval;
-    sa.count = count;
-    sa.est = est;
-    sa.maxkey = maxkey;
-    sa.sel = sel;
-    sa.hist = hist;
-    sa.done = ctr + 2;
-    long long per_worker = (long long)sms * 4 / k;
-    if (per_worker < 8) per_worker = 8;
-    const long long need_blocks = (p.cap + 256 * 16 - 1) / (256 * 16);
-    if (per_worker > need_blocks) per_worker = need_blocks < 8 ? 8 : need_blocks;
-    dim3 sgrid((unsigned)per_worker, (unsigned)k);
-    for (int r = 0; r < TopkTraits<T>::ROUNDS_MAX; ++r) k_select<T><<<sgrid, 256, 0, stream>>>(sa, r);
-    // 4. final compaction
-    FinArgs<T> fa;
-    fa.g = g;
-    fa.ld = ld;
-    fa.dim = dim;
-    fa.cap = p.cap;
-    fa.m = m;
-    fa.nt_fin = p.nt_fin;
-    fa.k = k;
-    fa.vec_ok = vec_ok;
-    fa.cidx = cidx;
-    fa.cval = cval;
-    fa.sel = sel;
-    fa.status = st_fin;
-    fa.ticket = ctr + 1;
-    fa.idx = idx;
-    fa.val = val;
-    fa.sumsq = sum_fin;
-    long long grid_fin = (long long)sms * 8;
-    const long long fin_need = (long long)k * ((p.cap + tile_elems<T>() - 1) / tile_elems<T>());
-    if (grid_fin > fin_need) grid_fin = fin_need > 0 ? fin_need : 1;
-    k_final<T><<<(unsigned)grid_fin, TK_THREADS, 0, stream>>>(fa);
-    // 5. norms + gate
-    k_gate<T><<<k, 256, 0, stream>>>(sum_main, p.nt_main, sum_fin, p.nt_fin, sel, norms2, states,
-                                     decision, rho);
+    ma.hist0 = hist0;
+    ma.done = c_main;
+    const dim3 sgrid((unsigned)p.nseg, (unsigned)k);
+    k_main<T><<<sgrid, TK_THREADS, 0, stream>>>(ma);
+    ma.pass = 1;
+    ma.hist0 = hist0fb;
+    ma.done = c_fb;
+    k_main<T><<<sgrid, TK_THREADS, 0, stream>>>(ma);
+    // 3. per-segment counts + boundary, in-CTA resolve
+    CollectArgs<T> ca;
+    ca.segcap = p.segcap;
+    ca.cap = capw;
+    ca.nseg = p.nseg;
+    ca.tps = p.tps;
+    ca.sel = sel;
+    ca.segcnt = segcnt;
+    ca.cidx = cidx;
+    ca.cval = cval;
+    ca.seggt = seggt;
+    ca.segbase = segbase;
+    ca.bkey = bkey;
+    ca.bidx = bidx;
+    ca.bndn = bndn;
+    ca.done = c_col;
+    k_collect<T><<<sgrid, TK_THREADS, 0, stream>>>(ca);
+    const size_t res_smem = (sizeof(K) + sizeof(uint32_t) + 1) * RESOLVE_SMEM + sizeof(unsigned) * BMAX;
+    cudaFuncSetAttribute(k_resolve_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem);
+    k_resolve_small<T><<<k, 1024, res_smem, stream>>>(ca);
+    // 4. slow mode only: multi-CTA select rounds over an oversized boundary
+    ResolveArgs<T> ra;
+    ra.cap = capw;
+    ra.sel = sel;
+    ra.bkey = bkey;
+    ra.bndn = bndn;
+    ra.hist = histr;
+    ra.done = c_res;
+    const unsigned rper = (unsigned)((sms * 2 + k - 1) / k);
+    for (int r = 0; r < TopkTraits<T>::ROUNDS_MAX; ++r)
+        k_resolve<T><<<dim3(rper, (unsigned)k), 256, 0, stream>>>(ra, r);
+    // 5. ordered write + norms + gate
+    WriteArgs<T> wa;
+    wa.ntiles = p.ntiles;
+    wa.segcap = p.segcap;
+    wa.m = m;
+    wa.k = k;
+    wa.nseg = p.nseg;
+    wa.tps = p.tps;
+    wa.sel = sel;
+    wa.tstart = tstart;
+    wa.segcnt = segcnt;
+    wa.segbase = segbase;
+    wa.cidx = cidx;
+    wa.cval = cval;
+    wa.status = status;
+    wa.done = ctr + 1;
+    wa.idx = idx;
+    wa.val = val;
+    wa.tile_off = tile_off;
+    wa.pwrite = pwrite;
+    wa.pmain = pmain;
+    wa.norms2 = norms2;
+    wa.states = states;
+    wa.decision = decision;
+    wa.rho = rho;
+    const size_t wr_smem = sizeof(unsigned) * (size_t)p.tps;
+    k_write<T><<<sgrid, TK_THREADS, wr_smem, stream>>>(wa);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
@@ -899,25 +1254,26 @@ using namespace sg;
 extern "C" {
 
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m) {
-    if (k < 1 || dim < 1 || m < 1 || m > dim) return 0;
-    return make_plan<float>(k, dim, m).total;
+    if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
+    return make_plan<float>(k, dim, m, segments_per_worker<float>(k)).total;
 }
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m) {
-    if (k < 1 || dim < 1 || m < 1 || m > dim) return 0;
-    return make_plan<double>(k, dim, m).total;
+    if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
+    return make_plan<double>(k, dim, m, segments_per_worker<double>(k)).total;
 }
 
 int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m, uint32_t* idx,
                      float* val, double* norms2, sg_gate_state* states, uint8_t* decision,
-                     double* rho, void* workspace, size_t workspace_bytes, void* stream) {
-    return topk_gate<float>(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, workspace,
-                            workspace_bytes, (cudaStream_t)stream);
+                     double* rho, int32_t* tile_off, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+    return topk_gate<float>(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, tile_off,
+                            workspace, workspace_bytes, (cudaStream_t)stream);
 }
 int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m, uint32_t* idx,
                      double* val, double* norms2, sg_gate_state* states, uint8_t* decision,
                      double* rho, void* workspace, size_t workspace_bytes, void* stream) {
-    return topk_gate<double>(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, workspace,
-                             workspace_bytes, (cudaStream_t)stream);
+    return topk_gate<double>(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, nullptr,
+                             workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 int sg_gate_update(const double* norms2, int k, sg_gate_state* states, uint8_t* decision,

@@ -47,8 +47,8 @@ class CudaOps:
         kernels.require_cuda()
         self.device = device
 
-    def topk_gate(self, bucket, dim, m, states, out):
-        return kernels.topk_gate(bucket, m, states, dim=dim, out=out)
+    def topk_gate(self, bucket, dim, m, states, out, tile_off=None):
+        return kernels.topk_gate(bucket, m, states, dim=dim, out=out, tile_off=tile_off)
 
     def aggregate(self, weights, dim, **kw):
         return kernels.weighted_aggregate(weights, dim, **kw)
@@ -130,11 +130,15 @@ class GradientExchange:
             self.decision = torch.empty(k, dtype=torch.uint8, **z)
             self.rho = torch.empty(k, dtype=torch.float64, **z)
             self.row_ptr_local = torch.arange(0, (k + 1) * m, m, dtype=torch.int64, **z)
+            nt1 = kernels.merge_tiles(dim) + 1
+            self.tile_off = torch.empty((k, nt1), dtype=torch.int32, **z) if dtype == torch.float32 else None
             if self.world > 1:
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
                 self.idx_all = torch.empty((self.W, m), dtype=torch.int32, **z)
                 self.val_all = torch.empty((self.W, m), dtype=dtype, **z)
                 self.row_ptr_all = torch.arange(0, (self.W + 1) * m, m, dtype=torch.int64, **z)
+                self.tile_off_all = (torch.empty((self.W, nt1), dtype=torch.int32, **z)
+                                     if self.tile_off is not None else None)
         self.partial = torch.empty(dim, dtype=dtype, **z) if self.world > 1 else None
         self.aggregate = None
         self.steps = 0
@@ -145,14 +149,16 @@ class GradientExchange:
         """Top-k + norms + gate for every local worker (no host synchronisation)."""
         self.ops.topk_gate(
             self.bucket, self.dim, self.m, self.states,
-            (self.idx, self.val, self.norms2, self.decision, self.rho),
+            (self.idx, self.val, self.norms2, self.decision, self.rho), self.tile_off,
         )
 
-    def step(self, weights, lr: float, *, keep_aggregate: bool = False) -> StepInfo:
+    def step(self, weights, lr: float, *, keep_aggregate: bool = False, topk_events=None) -> StepInfo:
         """One synchronous iteration over the gradients currently in ``bucket``.
 
         ``weights`` holds all W aggregation weights (host float64).  With
         ``keep_aggregate`` the aggregated gradient is also written to ``self.aggregate``.
+        ``topk_events`` = (start, end) CUDA events recorded around the Top-k/gate launch
+        sequence on the current stream (bench.py's per-kernel roofline timing).
         """
         w = np.asarray(weights, dtype=np.float64)
         if w.shape != (self.W,):
@@ -164,11 +170,16 @@ class GradientExchange:
             self.aggregate = torch.empty(dim, dtype=self.dtype, device=self.device)
         out = self.aggregate if keep_aggregate else None
         if self.compression:
+            if topk_events is not None:
+                topk_events[0].record()
             self.gate()
+            if topk_events is not None:
+                topk_events[1].record()
         if self.world == 1:
             if self.compression:
                 self.ops.aggregate(w, dim, compressed=self.decision, dense=self.bucket, idx=self.idx,
-                                   val=self.val, row_ptr=self.row_ptr_local, out=out, **opt)
+                                   val=self.val, row_ptr=self.row_ptr_local, tile_off=self.tile_off,
+                                   out=out, **opt)
             else:
                 self.ops.aggregate(w, dim, dense=self.bucket, out=out, **opt)
             path = "local"
@@ -189,13 +200,16 @@ class GradientExchange:
         if all_compressed:
             dist.all_gather_into_tensor(self.idx_all.view(-1), self.idx.view(-1), group=g)
             dist.all_gather_into_tensor(self.val_all.view(-1), self.val.view(-1), group=g)
+            if self.tile_off is not None:
+                dist.all_gather_into_tensor(self.tile_off_all.view(-1), self.tile_off.view(-1), group=g)
             self.ops.aggregate(w, dim, compressed=self.dec_all, idx=self.idx_all, val=self.val_all,
-                               row_ptr=self.row_ptr_all, out=out, **opt)
+                               row_ptr=self.row_ptr_all, tile_off=self.tile_off_all, out=out, **opt)
             return "sparse-allgather"
         wl = w[self.lo:self.lo + self.k]
         if self.compression:
             self.ops.aggregate(wl, dim, compressed=self.decision, dense=self.bucket, idx=self.idx,
-                               val=self.val, row_ptr=self.row_ptr_local, out=self.partial)
+                               val=self.val, row_ptr=self.row_ptr_local, tile_off=self.tile_off,
+                               out=self.partial)
         else:
             self.ops.aggregate(wl, dim, dense=self.bucket, out=self.partial)
         dist.all_reduce(self.partial, op=dist.ReduceOp.SUM, group=g)

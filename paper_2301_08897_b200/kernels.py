@@ -14,6 +14,15 @@ from . import _capi
 
 _GATE_BYTES = _capi.GATE_STATE_DTYPE.itemsize
 
+# Kernel launches issued through this module (each C-ABI entry point launches a fixed
+# sequence; see csrc/topk.cu and csrc/aggregate.cu).  bench.py reports the count.
+LAUNCHES = {"n": 0}
+TOPK_LAUNCHES = {torch.float32: 1 + 2 + 1 + 1 + 3 + 1, torch.float64: 1 + 2 + 1 + 1 + 6 + 1}
+
+
+def _count(n: int) -> None:
+    LAUNCHES["n"] += n
+
 
 def require_cuda(t: torch.Tensor | None = None) -> None:
     if not torch.cuda.is_available():
@@ -55,6 +64,13 @@ def gate_states_numpy(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy().view(_capi.GATE_STATE_DTYPE).copy()
 
 
+MERGE_TILE = 4096
+
+
+def merge_tiles(dim: int) -> int:
+    return (dim + MERGE_TILE - 1) // MERGE_TILE
+
+
 def topk_workspace_bytes(dtype: torch.dtype, k: int, dim: int, m: int) -> int:
     lib = _capi.load()
     fn = lib.sg_topk_workspace_bytes_f32 if dtype == torch.float32 else lib.sg_topk_workspace_bytes_f64
@@ -68,6 +84,7 @@ def topk_gate(
     *,
     dim: int | None = None,
     out: tuple | None = None,
+    tile_off: torch.Tensor | None = None,
 ):
     """Batched Top-k + norms (+ gate) over the rows of ``g`` ([k, ld] or [D]).
 
@@ -99,12 +116,16 @@ def topk_gate(
         raise ValueError("invalid top-k shape")
     ws = Workspace.get(nbytes, dev)
     lib = _capi.load()
-    fn = lib.sg_topk_gate_f32 if g.dtype == torch.float32 else lib.sg_topk_gate_f64
-    st = fn(
-        g2.data_ptr(), k, ld, D, m, idx.data_ptr(), val.data_ptr(), norms2.data_ptr(),
-        _ptr(states), _ptr(decision), _ptr(rho), ws.data_ptr(), ws.numel(), _stream(),
-    )
+    args = [g2.data_ptr(), k, ld, D, m, idx.data_ptr(), val.data_ptr(), norms2.data_ptr(),
+            _ptr(states), _ptr(decision), _ptr(rho)]
+    if g.dtype == torch.float32:
+        st = lib.sg_topk_gate_f32(*args, _ptr(tile_off), ws.data_ptr(), ws.numel(), _stream())
+    else:
+        if tile_off is not None:
+            raise ValueError("tile offsets are produced by the float32 path only")
+        st = lib.sg_topk_gate_f64(*args, ws.data_ptr(), ws.numel(), _stream())
     _capi.check(st, "sg_topk_gate")
+    _count(TOPK_LAUNCHES[g.dtype])
     return idx, val, norms2, decision, rho
 
 
@@ -115,6 +136,7 @@ def gate_update(norms2: torch.Tensor, states: torch.Tensor):
     rho = torch.empty(k, dtype=torch.float64, device=norms2.device)
     st = _capi.load().sg_gate_update(norms2.data_ptr(), k, states.data_ptr(), decision.data_ptr(), rho.data_ptr(), _stream())
     _capi.check(st, "sg_gate_update")
+    _count(1)
     return decision, rho
 
 
@@ -127,6 +149,7 @@ def weighted_aggregate(
     idx: torch.Tensor | None = None,
     val: torch.Tensor | None = None,
     row_ptr: torch.Tensor | None = None,
+    tile_off: torch.Tensor | None = None,
     out: torch.Tensor | None = None,
     params: torch.Tensor | None = None,
     momentum_buf: torch.Tensor | None = None,
@@ -154,16 +177,17 @@ def weighted_aggregate(
         out = torch.empty(dim, dtype=dt, device=dev)
     ws = None
     nbytes = 0
-    if compressed is not None:
+    if compressed is not None and tile_off is None:
         nbytes = int(_capi.load().sg_aggregate_workspace_bytes(nw, dim))
         ws = Workspace.get(nbytes, dev)
     fn = _capi.load().sg_weighted_aggregate_f32 if dt == torch.float32 else _capi.load().sg_weighted_aggregate_f64
     st = fn(
-        nw, wp, _ptr(compressed), _ptr(dense), ld, _ptr(idx), _ptr(val), _ptr(row_ptr), dim,
+        nw, wp, _ptr(compressed), _ptr(dense), ld, _ptr(idx), _ptr(val), _ptr(row_ptr), _ptr(tile_off), dim,
         _ptr(out), _ptr(params), _ptr(momentum_buf), float(lr), float(momentum), float(weight_decay),
         int(bool(first_step)), _ptr(ws), nbytes if ws is not None else 0, _stream(),
     )
     _capi.check(st, "sg_weighted_aggregate")
+    _count(1 + (1 if ws is not None else 0))
     return out
 
 
@@ -174,6 +198,7 @@ def sgd_momentum(params, momentum_buf, grad, lr, momentum, weight_decay, first_s
     st = fn(params.data_ptr(), momentum_buf.data_ptr(), grad.data_ptr(), params.numel(), float(lr),
             float(momentum), float(weight_decay), int(bool(first_step)), _stream())
     _capi.check(st, "sg_sgd_momentum")
+    _count(1)
 
 
 def resolve_stream_rows(head, b, out_ptr, pool_ptr, pool_rows, total, out):
@@ -181,6 +206,7 @@ def resolve_stream_rows(head, b, out_ptr, pool_ptr, pool_rows, total, out):
         len(head), head.data_ptr(), b.data_ptr(), out_ptr.data_ptr(), pool_ptr.data_ptr(),
         pool_rows.data_ptr(), int(total), out.data_ptr(), _stream())
     _capi.check(st, "sg_resolve_stream_rows")
+    _count(1)
 
 
 def inject_rows(base_ptr, base_rows, senders, pick_ptr, picks, out_ptr, out_rows):
@@ -190,6 +216,7 @@ def inject_rows(base_ptr, base_rows, senders, pick_ptr, picks, out_ptr, out_rows
         _ptr(pick_ptr) if senders.numel() else None, _ptr(picks) if picks.numel() else None,
         out_ptr.data_ptr(), out_rows.data_ptr(), _stream())
     _capi.check(st, "sg_inject_rows")
+    _count(1)
 
 
 def gather_batch(train_x, augment, train_y, rows, x_out, y_out):
@@ -198,3 +225,4 @@ def gather_batch(train_x, augment, train_y, rows, x_out, y_out):
     st = fn(train_x.data_ptr(), _ptr(augment), _ptr(train_y), train_x.shape[1], rows.data_ptr(),
             rows.numel(), x_out.data_ptr(), _ptr(y_out), _stream())
     _capi.check(st, "sg_gather_batch")
+    _count(1)

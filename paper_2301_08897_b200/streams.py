@@ -1,0 +1,269 @@
+"""Streaming-rate-driven variable-batch sampler and non-IID injection, staged on the device
+(item 5).  Mirrors ``streamsgd.streams`` / ``streamsgd.datagen`` (reference
+pkg/src/streamsgd/streams.py, datagen.py) and the sampler section of
+``Simulation.run_iteration`` (engine.py:213-242, _materialize 201-204).
+
+Host side (identical numpy calls and seeds, so every random draw matches the reference):
+  ``derive_seed``, ``RateDistribution``/``sample_rates``, ``compute_batch_size``,
+  ``streaming_wait``, ``StreamBuffer`` (the FIFO of pending sample ids is always one
+  contiguous id range, so it is kept as (head, next_id, credit) instead of a deque),
+  ``injection_plan`` / ``injection_picks``, ``partition``.
+Device side (sm_100a kernels via the C-ABI): :class:`DeviceSampler` resolves drawn id
+ranges to train rows (pools[d][a % len]), builds the injected batches, and gathers
+x = train_x[rows] + augment[rows] (binary64 add, bit-exact) into one batch tensor.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels
+
+FLOOR_EPS = 1e-9  # streams.py:19
+PERSISTENCE = "persistence"
+TRUNCATION = "truncation"
+RETENTION_POLICIES = (PERSISTENCE, TRUNCATION)
+RATE_KINDS = ("uniform", "normal")
+MODE_FIXED_BATCH = "fixed_batch"
+MODE_RATE_MATCHED = "rate_matched"
+
+
+def derive_seed(master: int, label: str) -> int:
+    """Labelled sha256 seed (config.py:235-238)."""
+    digest = hashlib.sha256(f"{master}:{label}".encode()).digest()
+    return int.from_bytes(digest[:8], "little")
+
+
+class WouldBlock(Exception):
+    """A batch draw needs more samples than the buffer holds (streams.py:28-33)."""
+
+    def __init__(self, shortfall: int):
+        super().__init__(f"buffer short by {shortfall} samples")
+        self.shortfall = shortfall
+
+
+@dataclass
+class RateDistribution:
+    """streams.py:36-55: uniform with the given mean/std, or normal."""
+
+    kind: str
+    mean: float
+    std: float = 0.0
+
+    def __post_init__(self):
+        if self.kind not in RATE_KINDS:
+            raise ValueError(f"unknown rate distribution kind: {self.kind!r}")
+        if self.mean <= 0:
+            raise ValueError("rate distribution mean must be positive")
+        if self.std < 0:
+            raise ValueError("rate distribution std must be non-negative")
+
+
+def sample_rates(dist: RateDistribution, n: int, seed: int) -> list[int]:
+    """Integer rates, rounded to nearest and clamped >= 1 (streams.py:58-69)."""
+    if n < 1:
+        raise ValueError("need at least one device rate")
+    rng = np.random.default_rng(seed)
+    if dist.kind == "uniform":
+        half = dist.std * math.sqrt(3.0)
+        raw = rng.uniform(dist.mean - half, dist.mean + half, n)
+    else:
+        raw = rng.normal(dist.mean, dist.std, n)
+    return [int(r) for r in np.maximum(1, np.rint(raw).astype(int))]
+
+
+def compute_batch_size(mode: str, rate: int, b_min: int, b_max: int, fixed_batch: int) -> int:
+    """engine.py:93-99: fixed batch, or the rate clamped to [b_min, b_max]."""
+    if mode == MODE_FIXED_BATCH:
+        return fixed_batch
+    if mode == MODE_RATE_MATCHED:
+        return min(max(rate, b_min), b_max)
+    raise ValueError(f"unknown mode: {mode!r}")
+
+
+def streaming_wait(buffer_len: int, b: int, rate: int) -> float:
+    """Seconds until b samples are available (streams.py:130-134)."""
+    if rate < 1:
+        raise ValueError("rate must be >= 1")
+    return max(0.0, (b - buffer_len) / rate)
+
+
+class StreamBuffer:
+    """FIFO of pending sample ids fed at a fixed rate (streams.py:72-127).
+
+    Ids are issued consecutively and drawn/retained from the front, so the pending set is
+    always the contiguous range [head, next_id); a draw returns ``range(head, head + b)``.
+    """
+
+    def __init__(self, rate: int, policy: str = PERSISTENCE):
+        if rate < 1:
+            raise ValueError("stream rate must be >= 1")
+        if policy not in RETENTION_POLICIES:
+            raise ValueError(f"unknown retention policy: {policy!r}")
+        self.rate = rate
+        self.policy = policy
+        self.head = 0
+        self.next_id = 0
+        self.fractional_credit = 0.0
+
+    def __len__(self) -> int:
+        return self.next_id - self.head
+
+    @property
+    def pending(self) -> range:
+        return range(self.head, self.next_id)
+
+    def enqueue_arrivals(self, elapsed: float) -> int:
+        if elapsed < 0:
+            raise ValueError("elapsed time must be non-negative")
+        exact = self.rate * elapsed + self.fractional_credit
+        added = int(math.floor(exact + FLOOR_EPS))
+        self.fractional_credit = min(max(exact - added, 0.0), math.nextafter(1.0, 0.0))
+        self.next_id += added
+        return added
+
+    def draw_batch(self, b: int) -> range:
+        if b < 1:
+            raise ValueError("batch size must be >= 1")
+        if len(self) < b:
+            raise WouldBlock(b - len(self))
+        ids = range(self.head, self.head + b)
+        self.head += b
+        return ids
+
+    def apply_retention(self) -> int:
+        if self.policy == PERSISTENCE:
+            return 0
+        discard = max(0, len(self) - self.rate)
+        self.head += discard
+        return discard
+
+
+def partition(train_y: np.ndarray, n_devices: int, mode: str, labels_per_device: int, seed: int) -> list[np.ndarray]:
+    """Train-index pools per device (datagen.py:110-144), same RNG calls as the reference."""
+    if mode not in ("iid", "noniid"):
+        raise ValueError(f"unknown partition mode: {mode!r}")
+    rng = np.random.default_rng(seed)
+    n = n_devices
+    if mode == "iid":
+        perm = rng.permutation(len(train_y))
+        return [np.sort(p) for p in np.array_split(perm, n)]
+    labels = np.unique(train_y)
+    k = len(labels)
+    lpd = labels_per_device
+    if k % lpd != 0:
+        raise ValueError(f"{k} labels cannot be split into groups of {lpd}")
+    groups = k // lpd
+    if n * lpd < k or n < groups:
+        raise ValueError(f"{n} devices cannot cover {k} labels at {lpd} labels/device")
+    order = rng.permutation(labels)
+    members: list[list[int]] = [[] for _ in range(groups)]
+    for d in range(n):
+        members[d % groups].append(d)
+    pools: list[np.ndarray] = [np.empty(0, dtype=np.int64)] * n
+    for g in range(groups):
+        idx = rng.permutation(np.flatnonzero(np.isin(train_y, order[g * lpd:(g + 1) * lpd])))
+        for d, part in zip(members[g], np.array_split(idx, len(members[g]))):
+            pools[d] = np.sort(part)
+    return pools
+
+
+def injection_plan(n_devices: int, alpha: float, beta: float, batch_sizes, seed: int) -> list[tuple[int, int]]:
+    """ceil(alpha*n) senders (sorted choice), each sharing ceil(beta*b_i) (datagen.py:162-179)."""
+    if n_devices < 2:
+        raise ValueError("injection needs at least two devices")
+    if len(batch_sizes) != n_devices:
+        raise ValueError("one batch size per device required")
+    n_senders = math.ceil(alpha * n_devices)
+    if n_senders == 0:
+        return []
+    rng = np.random.default_rng(seed)
+    senders = np.sort(rng.choice(n_devices, size=n_senders, replace=False))
+    return [(int(i), math.ceil(beta * batch_sizes[i])) for i in senders]
+
+
+def injection_picks(plan, batch_sizes, rng: np.random.Generator) -> list[np.ndarray]:
+    """Positions each sender shares, drawn exactly as datagen.inject does (datagen.py:200-203)."""
+    picks = []
+    for sender, count in plan:
+        if count == 0:
+            picks.append(np.zeros(0, dtype=np.int64))
+            continue
+        picks.append(np.asarray(rng.choice(batch_sizes[sender], size=count, replace=False), dtype=np.int64))
+    return picks
+
+
+def injection_bytes(plan, n_devices: int, sample_bytes: int) -> int:
+    """Bytes moved by one injection step: every (sender, recipient) copy (datagen.py:208)."""
+    return sum(c * (n_devices - 1) * sample_bytes for _, c in plan if c)
+
+
+class DeviceSampler:
+    """Per-iteration batch staging on the GPU.
+
+    ``train_x`` (float64 or float32), ``train_y`` and the pools live on the device; the
+    per-epoch augmentation table is generated on the host with the reference's RNG
+    (engine.py:180-185) and uploaded once per epoch.
+    """
+
+    def __init__(self, train_x: np.ndarray, train_y: np.ndarray, pools: list[np.ndarray], *,
+                 device: torch.device | None = None, dtype: torch.dtype = torch.float64):
+        kernels.require_cuda()
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.dtype = dtype
+        self.train_x = torch.from_numpy(np.ascontiguousarray(train_x)).to(self.device, dtype=dtype)
+        self.train_y = torch.from_numpy(np.asarray(train_y, dtype=np.int64)).to(self.device)
+        lens = [len(p) for p in pools]
+        self.pool_ptr = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int64, device=self.device)
+        self.pool_rows = torch.from_numpy(np.concatenate([np.asarray(p, dtype=np.int64) for p in pools])).to(self.device)
+        self.n_dev = len(pools)
+        self.augment = None
+
+    def set_augmentation(self, table: np.ndarray | None) -> None:
+        self.augment = None if table is None else torch.from_numpy(np.ascontiguousarray(table)).to(self.device, dtype=self.dtype)
+
+    def stage(self, draws: list[range], plan=None, picks=None):
+        """Rows of every device's batch (CSR) and the gathered batch.
+
+        ``draws[d]`` is the id range drawn from device d's StreamBuffer; ``plan``/``picks``
+        come from :func:`injection_plan` / :func:`injection_picks`.  Returns
+        (x [rows, F], y [rows], ptr [n_dev + 1] host int64) with device d's batch in
+        rows ptr[d]:ptr[d+1] in the reference's order (own samples, then injected ones).
+        """
+        dev = self.device
+        b = np.array([len(r) for r in draws], dtype=np.int64)
+        head = np.array([r.start for r in draws], dtype=np.int64)
+        base_ptr = np.concatenate([[0], np.cumsum(b)])
+        total = int(base_ptr[-1])
+        rows = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+        kernels.resolve_stream_rows(
+            torch.from_numpy(head).to(dev), torch.from_numpy(b).to(dev), torch.from_numpy(base_ptr).to(dev),
+            self.pool_ptr, self.pool_rows, total, rows)
+        ptr = base_ptr
+        if plan:
+            counts = np.array([c for _, c in plan], dtype=np.int64)
+            sizes = b.copy()
+            for (s, c) in plan:
+                sizes += c
+                sizes[s] -= c
+            ptr = np.concatenate([[0], np.cumsum(sizes)])
+            out_rows = torch.empty(max(int(ptr[-1]), 1), dtype=torch.int64, device=dev)
+            pick_ptr = np.concatenate([[0], np.cumsum(counts)])
+            all_picks = np.concatenate(picks) if len(picks) else np.zeros(0, dtype=np.int64)
+            kernels.inject_rows(
+                torch.from_numpy(base_ptr).to(dev), rows,
+                torch.tensor([s for s, _ in plan], dtype=torch.int32, device=dev),
+                torch.from_numpy(pick_ptr).to(dev),
+                torch.from_numpy(all_picks.astype(np.int64)).to(dev) if all_picks.size else torch.zeros(1, dtype=torch.int64, device=dev),
+                torch.from_numpy(ptr).to(dev), out_rows)
+            rows = out_rows
+        n = int(ptr[-1])
+        x = torch.empty((n, self.train_x.shape[1]), dtype=self.dtype, device=dev)
+        y = torch.empty(n, dtype=torch.int64, device=dev)
+        kernels.gather_batch(self.train_x, self.augment, self.train_y, rows[:n], x, y)
+        return x, y, ptr

@@ -102,12 +102,16 @@ def test_topk_batched_rows_and_padding(cuda):
     for j in range(k):
         host[j, :D] = _family(["normal", "heavy", "ties", "edge"][j % 4], D, seed=100 + j)
     dev = torch.from_numpy(host).to(cuda)
-    for cr in (0.01, 0.1):
+    nt = kernels.merge_tiles(D)
+    for cr in (0.001, 0.01, 0.1):
         m = comm_ref.topk_count(D, cr)
-        idx, val, norms2, _, _ = kernels.topk_gate(dev, m, dim=D)
+        toff = torch.full((k, nt + 1), -7, dtype=torch.int32, device=cuda)
+        idx, val, norms2, _, _ = kernels.topk_gate(dev, m, dim=D, tile_off=toff)
         for j in range(k):
             want = comm_ref.topk_indices_threshold(host[j, :D].astype(np.float64), m)
             assert np.array_equal(idx[j].cpu().numpy().astype(np.int64), want), (j, cr)
+            bounds = np.searchsorted(want, np.arange(nt + 1) * kernels.MERGE_TILE)
+            assert np.array_equal(toff[j].cpu().numpy(), bounds), (j, cr)
 
 
 def test_topk_float64_large_matches_lexsort(cuda):
