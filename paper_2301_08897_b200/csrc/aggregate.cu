@@ -141,6 +141,7 @@ template <typename TI, typename TO> struct AggArgs {
     long long ld, dim, ntiles;
     double lr, mu, wd;
     int nw, first, vec_ok;
+    int pipe;  // k_merge_pipe owns all-sparse calls: k_merge then exits
 };
 
 template <typename TI, typename TO>
@@ -326,37 +327,55 @@ k_aggregate(const AggArgs<TI, TO> a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// k_merge: the float32 fast path of k_aggregate.  Thread t owns the 16 contiguous positions
-// [16t, 16t+16) of the tile.  All sparse workers' in-tile entries are staged into shared
-// memory with one batched load (worker-major); for worker j each thread binary-searches its
-// first entry and merges its <= 16 entries into register accumulators, so workers are
-// folded in order without a block barrier per worker.  Dense rows and p/buf use L1-cached
-// 128-bit loads (the two 16-byte halves of each sector come from consecutive instructions).
+// k_merge: the float32 fast path of k_aggregate.  512 threads; thread t owns the 8
+// contiguous positions [8t, 8t+8) of the 4096-element tile.  Dense workers are folded in
+// float64 registers.  Sparse workers are folded entry-driven: all of them are staged into
+// shared memory with one batched load (worker-major), the running float64 tile moves to
+// shared memory for the run of sparse workers, and each staged entry updates its position
+// (unique within a worker, so one barrier per worker keeps the ascending-worker fold order).
+// p/buf for the fused momentum-SGD step are loaded first so their latency hides under the
+// fold.
 // ---------------------------------------------------------------------------------------
+constexpr int MP_MAXW = 16;
+constexpr int MG_THREADS = 512;
+constexpr int MG_PER = 8;
 constexpr int MG_ECAP = 4096;
+constexpr size_t MG_SMEM = AG_TILE * sizeof(double) + MG_ECAP * (sizeof(float) + sizeof(uint16_t)) +
+                           AG_TILE * sizeof(unsigned);
 
 template <typename TO>
-__global__ void __launch_bounds__(AG_THREADS, 2)
+__global__ void __launch_bounds__(MG_THREADS, 2)
 k_merge(const AggArgs<float, TO> a) {
-    __shared__ uint16_t ent_pos[MG_ECAP];
-    __shared__ float ent_val[MG_ECAP];
+    extern __shared__ __align__(128) unsigned char mg_smem[];
+    double* acc_s = reinterpret_cast<double*>(mg_smem);                   // [AG_TILE]
+    float* ent_val = reinterpret_cast<float*>(acc_s + AG_TILE);            // [MG_ECAP]
+    uint16_t* ent_pos = reinterpret_cast<uint16_t*>(ent_val + MG_ECAP);    // [MG_ECAP]
     __shared__ long long s_lo[MAX_WORKERS];
     __shared__ int s_cnt[MAX_WORKERS];
     __shared__ int s_pre[MAX_WORKERS + 1];
     __shared__ uint8_t s_comp[MAX_WORKERS];
     const int tid = threadIdx.x;
-    const long long tile = blockIdx.x;
+    __shared__ int s_skip;
+    if (tid == 0) {
+        int all = a.pipe && a.nw <= MP_MAXW;
+        for (int j = 0; j < a.nw && all; ++j) all = a.comp && a.comp[j] != 0;
+        s_skip = all;
+    }
+    __syncthreads();
+    if (s_skip) return;  // the pipelined kernel merged this call
+    for (long long tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    __syncthreads();  // shared memory of the previous tile is no longer read
     const long long tb = tile * AG_TILE;
-    const int q0 = tid * 16;
+    const int q0 = tid * MG_PER;
     const bool full = a.vec_ok && tb + AG_TILE <= a.dim;
     const bool first = a.first != 0;
 
-    float pv[16], bv[16];
+    float pv[MG_PER], bv[MG_PER];
     if (a.p && full) {
         const float4* pp = reinterpret_cast<const float4*>(a.p + tb + q0);
         const float4* bp = reinterpret_cast<const float4*>(a.buf + tb + q0);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < 2; ++r) {
             const float4 u = pp[r];
             pv[4 * r] = u.x; pv[4 * r + 1] = u.y; pv[4 * r + 2] = u.z; pv[4 * r + 3] = u.w;
             if (!first) {
@@ -367,7 +386,7 @@ k_merge(const AggArgs<float, TO> a) {
             }
         }
     }
-    for (int j = tid; j < a.nw; j += AG_THREADS) {
+    for (int j = tid; j < a.nw; j += MG_THREADS) {
         const uint8_t c = a.comp ? a.comp[j] : 0;
         s_comp[j] = c;
         int n = 0;
@@ -380,21 +399,35 @@ k_merge(const AggArgs<float, TO> a) {
         s_cnt[j] = n;
     }
     __syncthreads();
-    if (tid == 0) {
-        int acc = 0;
-        for (int j = 0; j < a.nw; ++j) {
-            s_pre[j] = acc;
-            acc += s_cnt[j];
+    if (tid < 32) {  // exclusive scan of the per-worker entry counts (nw <= 64)
+        const int lane = tid;
+        const int c0 = lane < a.nw ? s_cnt[lane] : 0;
+        const int c1 = lane + 32 < a.nw ? s_cnt[lane + 32] : 0;
+        int i0 = c0, i1 = c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y0 = __shfl_up_sync(FULL, i0, o), y1 = __shfl_up_sync(FULL, i1, o);
+            if (lane >= o) {
+                i0 += y0;
+                i1 += y1;
+            }
         }
-        s_pre[a.nw] = acc;
+        const int tot0 = __shfl_sync(FULL, i0, 31);
+        if (lane < a.nw) s_pre[lane] = i0 - c0;
+        if (lane + 32 < a.nw) s_pre[lane + 32] = tot0 + i1 - c1;
+        if (lane == 31) s_pre[a.nw] = a.nw <= 32 ? tot0 : tot0 + i1;
     }
     __syncthreads();
     const int E = s_pre[a.nw];
-    // stage entries [e0, e1) (whole workers) of the flattened worker-major entry list
-    auto stage = [&](int e0, int e1) {
-        for (int q = tid; q < e1 - e0; q += AG_THREADS) {
+    int st_lo = 0, st_hi = 0;  // staged entry window [st_lo, st_hi) (whole workers)
+    auto fill = [&](int j0) {
+        int j1 = j0;
+        while (j1 < a.nw && s_pre[j1 + 1] - s_pre[j0] <= MG_ECAP) ++j1;
+        if (j1 == j0) j1 = j0 + 1;  // cannot happen for f32 (<= 4096 entries per worker)
+        const int e0 = s_pre[j0], e1 = s_pre[j1];
+        for (int q = tid; q < e1 - e0; q += MG_THREADS) {
             const int e = e0 + q;
-            int lo = 0, hi = a.nw;  // s_pre[lo] <= e < s_pre[hi]
+            int lo = j0, hi = j1;  // s_pre[lo] <= e < s_pre[hi]
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
                 if (s_pre[mid] <= e) lo = mid;
@@ -404,80 +437,130 @@ k_merge(const AggArgs<float, TO> a) {
             ent_pos[q] = (uint16_t)(a.idx[gi] - (uint32_t)tb);
             ent_val[q] = a.val[gi];
         }
-    };
-    // the staged window holds whole workers [w_lo, w_hi)
-    int w_lo = 0, w_hi = 0;
-    auto fill = [&](int j0) {
-        int j1 = j0;
-        while (j1 < a.nw && s_pre[j1 + 1] - s_pre[j0] <= MG_ECAP) ++j1;
-        if (j1 == j0) j1 = j0 + 1;  // cannot happen for f32 (<= 4096 entries per worker)
-        stage(s_pre[j0], s_pre[j1]);
-        w_lo = j0;
-        w_hi = j1;
+        st_lo = e0;
+        st_hi = e1;
     };
     if (E > 0) fill(0);
-    __syncthreads();
 
-    double acc[16];
+    double acc[MG_PER];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) acc[c] = 0.0;
-    for (int j = 0; j < a.nw; ++j) {
+    for (int c = 0; c < MG_PER; ++c) acc[c] = 0.0;
+    bool all_sparse = a.nw <= 32 && E <= MG_ECAP;
+    for (int j = 0; j < a.nw && all_sparse; ++j) all_sparse = s_comp[j] != 0;
+    if (all_sparse) {
+        // Fast path (every worker sparse, whole tile staged): one pass records which workers
+        // touch each position; positions with one contributor take +0 + w*v directly, the
+        // rare collided ones are folded in ascending worker order by their lowest worker.
+        // who[q]: bitmask of the workers keeping position q; acc_s[q] is written only for
+        // touched positions and read only where the mask is non-zero.
+        unsigned* who = reinterpret_cast<unsigned*>(ent_pos + MG_ECAP);
+        *reinterpret_cast<uint4*>(who + q0) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(who + q0 + 4) = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        for (int e = tid; e < E; e += MG_THREADS) {
+            int lo = 0, hi = a.nw;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= e) lo = mid;
+                else hi = mid;
+            }
+            atomicOr(&who[ent_pos[e]], 1u << lo);
+        }
+        __syncthreads();
+        for (int e = tid; e < E; e += MG_THREADS) {
+            int lo = 0, hi = a.nw;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= e) lo = mid;
+                else hi = mid;
+            }
+            const int q = ent_pos[e];
+            const unsigned m = who[q];
+            double r;
+            if ((m & (m - 1)) == 0) {
+                r = dadd(0.0, dmul(a.w[lo], (double)ent_val[e]));
+            } else {
+                if (__ffs(m) - 1 != lo) continue;  // the lowest contributor folds the position
+                r = 0.0;
+                for (unsigned mm = m; mm; mm &= mm - 1) {
+                    const int j = __ffs(mm) - 1;
+                    int l = s_pre[j], h = s_pre[j + 1];  // entry of worker j at position q
+                    while (l < h) {
+                        const int mid = (l + h) >> 1;
+                        if ((int)ent_pos[mid] < q) l = mid + 1;
+                        else h = mid;
+                    }
+                    r = dadd(r, dmul(a.w[j], (double)ent_val[l]));
+                }
+            }
+            acc_s[q] = r;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < MG_PER; ++c) {
+            const int q = q0 + c;
+            if (who[q]) acc[c] = acc_s[q];
+        }
+    }
+    bool in_smem = false;  // uniform: the running tile lives in acc_s during a sparse run
+    for (int j = 0; j < (all_sparse ? 0 : a.nw); ++j) {
         const double wj = a.w[j];
         if (!s_comp[j]) {
-            float x[16];
+            float x[MG_PER];
             const float* row = a.dense + (long long)j * a.ld + tb + q0;
             if (full) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
+                for (int r = 0; r < 2; ++r) {
                     const float4 u = reinterpret_cast<const float4*>(row)[r];
                     x[4 * r] = u.x; x[4 * r + 1] = u.y; x[4 * r + 2] = u.z; x[4 * r + 3] = u.w;
                 }
             } else {
 #pragma unroll
-                for (int c = 0; c < 16; ++c) x[c] = tb + q0 + c < a.dim ? row[c] : 0.f;
+                for (int c = 0; c < MG_PER; ++c) x[c] = tb + q0 + c < a.dim ? row[c] : 0.f;
+            }
+            if (in_smem) {
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < MG_PER; ++c) acc[c] = acc_s[q0 + c];
+                in_smem = false;
             }
 #pragma unroll
-            for (int c = 0; c < 16; ++c) acc[c] = dadd(acc[c], dmul(wj, (double)x[c]));
+            for (int c = 0; c < MG_PER; ++c) acc[c] = dadd(acc[c], dmul(wj, (double)x[c]));
         } else if (s_cnt[j] > 0) {
-            if (j >= w_hi) {  // uniform across the block
-                __syncthreads();
+            if (!in_smem) {
+#pragma unroll
+                for (int c = 0; c < MG_PER; ++c) acc_s[q0 + c] = acc[c];
+                in_smem = true;
+            }
+            __syncthreads();  // previous worker's updates (and the staging) are complete
+            if (s_pre[j] >= st_hi) {
                 fill(j);
                 __syncthreads();
             }
-            const int base = s_pre[w_lo];
-            int i = s_pre[j] - base, end = i + s_cnt[j];
-            {  // first entry with pos >= q0
-                int lo = i, hi = end;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if ((int)ent_pos[mid] < q0) lo = mid + 1;
-                    else hi = mid;
-                }
-                i = lo;
-            }
-            int pos = i < end ? (int)ent_pos[i] : 1 << 30;
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                if (pos == q0 + c) {
-                    acc[c] = dadd(acc[c], dmul(wj, (double)ent_val[i]));
-                    ++i;
-                    pos = i < end ? (int)ent_pos[i] : 1 << 30;
-                }
+            const int e0 = s_pre[j] - st_lo, e1 = e0 + s_cnt[j];
+            for (int e = e0 + tid; e < e1; e += MG_THREADS) {
+                const int q = ent_pos[e];
+                acc_s[q] = dadd(acc_s[q], dmul(wj, (double)ent_val[e]));
             }
         }
+    }
+    if (in_smem) {
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < MG_PER; ++c) acc[c] = acc_s[q0 + c];
     }
     if (full) {
         if (a.out) {
             float4* op = reinterpret_cast<float4*>(a.out + tb + q0);
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
+            for (int r = 0; r < 2; ++r)
                 op[r] = make_float4((float)acc[4 * r], (float)acc[4 * r + 1], (float)acc[4 * r + 2], (float)acc[4 * r + 3]);
         }
         if (a.p) {
             float4* pp = reinterpret_cast<float4*>(a.p + tb + q0);
             float4* bp = reinterpret_cast<float4*>(a.buf + tb + q0);
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < 2; ++r) {
                 double pd[4], bd[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -491,7 +574,7 @@ k_merge(const AggArgs<float, TO> a) {
         }
     } else {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < MG_PER; ++c) {
             const long long q = tb + q0 + c;
             if (q >= a.dim) continue;
             if (a.out) a.out[q] = (TO)acc[c];
@@ -500,6 +583,252 @@ k_merge(const AggArgs<float, TO> a) {
                 sgd_elem(acc[c], pq, bq, a.lr, a.mu, a.wd, first);
                 a.p[q] = (TO)pq;
                 a.buf[q] = (TO)bq;
+            }
+        }
+    }
+    }  // tile loop
+}
+
+// ---------------------------------------------------------------------------------------
+// k_merge_pipe: persistent, software-pipelined merge + fused momentum SGD for the case the
+// hot path produces (every worker sparse, float32).  2 CTAs per SM; CTA b owns the
+// contiguous tile range [b*tpb, (b+1)*tpb) and loads its slice of the per-worker tile
+// offsets once.  While tile i is merged, tile i+1's p/buf are already in flight into
+// registers and its sparse entries into the other half of a double-buffered shared staging
+// area (cp.async / LDGSTS).  Per tile: atomicOr records which workers keep each position;
+// single-contributor positions take +0 + w*v directly, collided ones are folded in
+// ascending worker order by their lowest worker (the reference's fold), untouched
+// positions get the g = +0 update; each thread then applies momentum SGD to its 8
+// contiguous positions from registers and stores them with 128-bit stores.
+// ---------------------------------------------------------------------------------------
+constexpr int MP_ECAP = 2048;
+
+inline size_t mp_smem_bytes(int tpb) {
+    return (size_t)AG_TILE * sizeof(double) + 2 * MP_ECAP * (sizeof(uint32_t) + sizeof(float) + 1) +
+           AG_TILE * sizeof(unsigned) + (size_t)MP_MAXW * (tpb + 1) * sizeof(int);
+}
+
+template <typename TO>
+__global__ void __launch_bounds__(MG_THREADS, 2)
+k_merge_pipe(const AggArgs<float, TO> a, int tpb) {
+    extern __shared__ __align__(128) unsigned char mp_smem[];
+    double* acc_s = reinterpret_cast<double*>(mp_smem);                  // [TILE]
+    uint32_t* eidx = reinterpret_cast<uint32_t*>(acc_s + AG_TILE);       // [2][ECAP]
+    float* evl = reinterpret_cast<float*>(eidx + 2 * MP_ECAP);           // [2][ECAP]
+    unsigned* who = reinterpret_cast<unsigned*>(evl + 2 * MP_ECAP);      // [TILE]
+    uint8_t* ewk = reinterpret_cast<uint8_t*>(who + AG_TILE);            // [2][ECAP] worker ids
+    int* soff = reinterpret_cast<int*>(ewk + 2 * MP_ECAP);               // [nw][tpb + 1]
+    __shared__ int s_pre[3][MP_MAXW + 1];
+    __shared__ long long s_rp[MP_MAXW];
+    __shared__ int s_ok;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nw = a.nw;
+    if (tid == 0) {
+        int ok = nw <= MP_MAXW;
+        for (int j = 0; j < nw && ok; ++j) ok = a.comp[j] != 0;
+        s_ok = ok;
+    }
+    __syncthreads();
+    if (!s_ok) return;  // not all-sparse: k_merge handles this call
+    const long long t_begin = (long long)blockIdx.x * tpb;
+    if (t_begin >= a.ntiles) return;
+    const int nt = (int)(a.ntiles - t_begin < tpb ? a.ntiles - t_begin : tpb);
+    for (int q = tid; q < nw * (nt + 1); q += MG_THREADS) {
+        const int j = q / (nt + 1), i = q - j * (nt + 1);
+        soff[j * (tpb + 1) + i] = a.off[(long long)j * (a.ntiles + 1) + t_begin + i];
+    }
+    for (int q = tid; q < AG_TILE; q += MG_THREADS) who[q] = 0;
+    if (tid < nw) s_rp[tid] = a.row_ptr[tid];
+    const bool first = a.first != 0;
+    const int q0 = tid * MG_PER;
+    auto entry_prefix = [&](int i) {  // warp 0: exclusive prefix of tile i's per-worker counts
+        int c = 0;
+        if (lane < nw) c = soff[lane * (tpb + 1) + i + 1] - soff[lane * (tpb + 1) + i];
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane < nw) s_pre[i % 3][lane] = incl - c;
+        if (lane == 31) s_pre[i % 3][nw] = incl;
+    };
+    auto worker_of = [&](const int* pre, int e) {
+        int lo = 0, hi = nw;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= e) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    };
+    auto stage = [&](int i, int c0, int c1) {  // all threads: entries [c0, c1) of tile i, async
+        const int* pre = s_pre[i % 3];
+        const int slot = i & 1;
+        for (int e = c0 + tid; e < c1; e += MG_THREADS) {
+            const int j = worker_of(pre, e);
+            const long long gi = s_rp[j] + soff[j * (tpb + 1) + i] + (e - pre[j]);
+            cp_async4(eidx + slot * MP_ECAP + (e - c0), a.idx + gi);
+            cp_async4(evl + slot * MP_ECAP + (e - c0), a.val + gi);
+            ewk[slot * MP_ECAP + (e - c0)] = (uint8_t)j;
+        }
+        cp_async_commit();
+    };
+    auto load_pb = [&](int i, float (&pv)[MG_PER], float (&bv)[MG_PER]) {
+        const long long tb = (t_begin + i) * AG_TILE;
+        if (tb + AG_TILE <= a.dim) {
+            const float4* pp = reinterpret_cast<const float4*>(a.p + tb + q0);
+            const float4* bp = reinterpret_cast<const float4*>(a.buf + tb + q0);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const float4 u = pp[r], z = bp[r];
+                pv[4 * r] = u.x; pv[4 * r + 1] = u.y; pv[4 * r + 2] = u.z; pv[4 * r + 3] = u.w;
+                bv[4 * r] = z.x; bv[4 * r + 1] = z.y; bv[4 * r + 2] = z.z; bv[4 * r + 3] = z.w;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < MG_PER; ++c) {
+                const bool ok = tb + q0 + c < a.dim;
+                pv[c] = ok ? a.p[tb + q0 + c] : 0.f;
+                bv[c] = ok ? a.buf[tb + q0 + c] : 0.f;
+            }
+        }
+    };
+    __syncthreads();  // soff, who ready
+    if (warp == 0) {
+        entry_prefix(0);
+        if (nt > 1) entry_prefix(1);
+    }
+    __syncthreads();
+    {
+        const int E0 = s_pre[0][nw];
+        stage(0, 0, E0 < MP_ECAP ? E0 : MP_ECAP);
+    }
+    float pv[MG_PER], bv[MG_PER];
+    load_pb(0, pv, bv);
+    for (int i = 0; i < nt; ++i) {
+        const long long tb = (t_begin + i) * AG_TILE;
+        const int slot = i & 1;
+        const int* pre = s_pre[i % 3];
+        const int E = pre[nw];
+        // prefetch tile i+1: entries (async) and p/buf (registers); prefix of tile i+2
+        float pn[MG_PER], bn[MG_PER];
+        if (i + 1 < nt) {
+            const int E1 = s_pre[(i + 1) % 3][nw];
+            stage(i + 1, 0, E1 < MP_ECAP ? E1 : MP_ECAP);
+            load_pb(i + 1, pn, bn);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        if (warp == 0 && i + 2 < nt) entry_prefix(i + 2);
+        __syncthreads();  // S1: tile i's entries landed; who clear
+        const uint32_t* ei = eidx + slot * MP_ECAP;
+        const float* ev = evl + slot * MP_ECAP;
+        const uint8_t* ew = ewk + slot * MP_ECAP;
+        for (int c0 = 0; c0 < E; c0 += MP_ECAP) {
+            const int c1 = E - c0 < MP_ECAP ? E : c0 + MP_ECAP;
+            if (c0 > 0) {  // oversized tile (rare): synchronous restage of the next chunk
+                __syncthreads();
+                stage(i, c0, c1);
+                cp_async_wait<0>();
+                __syncthreads();
+            }
+            for (int e = c0 + tid; e < c1; e += MG_THREADS)
+                atomicOr(&who[ei[e - c0] - (uint32_t)tb], 1u << ew[e - c0]);
+        }
+        __syncthreads();  // S2: contributor masks complete
+        for (int c0 = 0; c0 < E; c0 += MP_ECAP) {
+            const int c1 = E - c0 < MP_ECAP ? E : c0 + MP_ECAP;
+            if (c0 > 0) {
+                __syncthreads();
+                stage(i, c0, c1);
+                cp_async_wait<0>();
+                __syncthreads();
+            } else if (E > MP_ECAP) {  // chunk 0 was overwritten by the pass above: restage it
+                __syncthreads();
+                stage(i, 0, MP_ECAP);
+                cp_async_wait<0>();
+                __syncthreads();
+            }
+            for (int e = c0 + tid; e < c1; e += MG_THREADS) {
+                const int j = ew[e - c0];
+                const int q = (int)(ei[e - c0] - (uint32_t)tb);
+                const unsigned m = who[q];
+                double r;
+                if ((m & (m - 1)) == 0) {
+                    r = dadd(0.0, dmul(a.w[j], (double)ev[e - c0]));
+                } else {
+                    if (__ffs(m) - 1 != j) continue;  // the lowest contributor folds the position
+                    r = 0.0;
+                    const uint32_t want = (uint32_t)tb + (uint32_t)q;
+                    for (unsigned mm = m; mm; mm &= mm - 1) {
+                        const int jj = __ffs(mm) - 1;
+                        double v;
+                        if (jj == j) {
+                            v = ev[e - c0];
+                        } else if (pre[jj] >= c0 && pre[jj + 1] <= c1) {
+                            // worker jj's entry at this index, in the staged (ascending) list
+                            int l = pre[jj] - c0, h = pre[jj + 1] - c0;
+                            while (l < h) {
+                                const int mid = (l + h) >> 1;
+                                if (ei[mid] < want) l = mid + 1;
+                                else h = mid;
+                            }
+                            v = ev[l];
+                        } else {  // oversized tile: that worker is outside this chunk
+                            const long long base = s_rp[jj] + soff[jj * (tpb + 1) + i];
+                            int l = 0, h = pre[jj + 1] - pre[jj];
+                            while (l < h) {
+                                const int mid = (l + h) >> 1;
+                                if (a.idx[base + mid] < want) l = mid + 1;
+                                else h = mid;
+                            }
+                            v = a.val[base + l];
+                        }
+                        r = dadd(r, dmul(a.w[jj], v));
+                    }
+                }
+                acc_s[q] = r;
+            }
+        }
+        __syncthreads();  // S3: aggregate values of the touched positions are in acc_s
+        const bool full = tb + AG_TILE <= a.dim;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // two halves of 4 positions keep the fp64 temporaries small
+            const int qh = q0 + 4 * h;
+            const uint4 mk = *reinterpret_cast<const uint4*>(who + qh);
+            double g[4] = {mk.x ? acc_s[qh] : 0.0, mk.y ? acc_s[qh + 1] : 0.0, mk.z ? acc_s[qh + 2] : 0.0,
+                           mk.w ? acc_s[qh + 3] : 0.0};
+            *reinterpret_cast<uint4*>(who + qh) = make_uint4(0, 0, 0, 0);
+            double pd[4], bd[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                pd[c] = (double)pv[4 * h + c];
+                bd[c] = (double)bv[4 * h + c];
+                sgd_elem(g[c], pd[c], bd[c], a.lr, a.mu, a.wd, first);
+            }
+            if (full) {
+                *reinterpret_cast<float4*>(a.p + tb + qh) = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
+                *reinterpret_cast<float4*>(a.buf + tb + qh) = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
+                if (a.out)
+                    *reinterpret_cast<float4*>(a.out + tb + qh) = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const long long q = tb + qh + c;
+                    if (q >= a.dim) continue;
+                    a.p[q] = (float)pd[c];
+                    a.buf[q] = (float)bd[c];
+                    if (a.out) a.out[q] = (TO)g[c];
+                }
+            }
+        }
+        if (i + 1 < nt) {
+#pragma unroll
+            for (int c = 0; c < MG_PER; ++c) {
+                pv[c] = pn[c];
+                bv[c] = bn[c];
             }
         }
     }
@@ -573,13 +902,31 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
     a.wd = wd;
     a.nw = nw;
     a.first = first;
+    a.pipe = 0;
     bool vec = true;
     if (dense) vec = vec && reinterpret_cast<size_t>(dense) % 16 == 0 && (ld * (long long)sizeof(TI)) % 16 == 0;
     if (out) vec = vec && reinterpret_cast<size_t>(out) % 16 == 0;
     if (p) vec = vec && reinterpret_cast<size_t>(p) % 16 == 0 && reinterpret_cast<size_t>(buf) % 16 == 0;
     a.vec_ok = vec;
     if constexpr (sizeof(TI) == 4 && sizeof(TO) == 4)
-        k_merge<TO><<<(unsigned)ntiles, AG_THREADS, 0, stream>>>(a);
+    {
+        const int sms = num_sms();
+        a.pipe = comp && vec && p && nw <= MP_MAXW;
+        if (a.pipe) {
+            const int tpb = (int)((ntiles + 2 * sms - 1) / (2 * sms));
+            const size_t sm = mp_smem_bytes(tpb);
+            if (sm <= 110 * 1024) {
+                cudaFuncSetAttribute(k_merge_pipe<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                k_merge_pipe<TO><<<(unsigned)((ntiles + tpb - 1) / tpb), MG_THREADS, sm, stream>>>(a, tpb);
+            } else {
+                a.pipe = 0;
+            }
+        }
+        cudaFuncSetAttribute(k_merge<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM);
+        long long grid = (long long)sms * 2;
+        if (grid > ntiles) grid = ntiles;
+        k_merge<TO><<<(unsigned)grid, MG_THREADS, MG_SMEM, stream>>>(a);
+    }
     else
         k_aggregate<TI, TO><<<(unsigned)ntiles, AG_THREADS, 0, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;

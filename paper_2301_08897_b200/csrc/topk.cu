@@ -46,7 +46,7 @@ constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
-constexpr int RESOLVE_SMEM = 16384;  // boundary entries resolved inside one CTA
+constexpr int NSUB_MAX = 2048;      // collect/write sub-ranges per worker
 
 enum { MODE_NORMAL = 0, MODE_FALLBACK = 1 };
 enum { WR_FAST = 0, WR_SLOW = 1 };
@@ -55,10 +55,12 @@ template <typename T> struct TopkTraits;
 template <> struct TopkTraits<float> {
     static constexpr int SAMPLE = 16384;
     static constexpr int ROUNDS_MAX = 3;  // after round 0: <= 31 bits left (open top bin)
+    static constexpr int RES = 12288;     // boundary entries resolved inside one CTA
 };
 template <> struct TopkTraits<double> {
     static constexpr int SAMPLE = 8192;
     static constexpr int ROUNDS_MAX = 6;  // after round 0: <= 63 bits left (open top bin)
+    static constexpr int RES = 8192;
 };
 
 template <typename T> constexpr int tile_elems() { return TK_THREADS * TK_ROUNDS * Vec16<T>::N; }
@@ -81,12 +83,13 @@ template <typename K> struct SelState {
 // --------------------------------------------------------------------------------------
 struct TopkPlan {
     int k, nseg, tps;  // segments per worker, tiles per segment
+    int split, nsub;   // CTAs per segment in the collect/write passes, nseg * split
     long long dim, m;
     long long s_eff, stride, r_est;
     long long ntiles, segcap;
     size_t off_count, off_maxkey, off_ctr, off_bndn, off_hist0, off_hist0fb, off_histr, off_status, zero_end;
     size_t off_sel, off_cnt, off_tstart, off_segcnt, off_seggt, off_segbase, off_pmain, off_pwrite,
-        off_cidx, off_cval, off_bkey, off_bidx, total;
+        off_cidx, off_cval, off_bkey, off_bidx, off_bpos, total;
 };
 
 template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int segs_per_worker) {
@@ -95,8 +98,8 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.k = k;
     p.dim = dim;
     p.m = m;
-    const long long S = TopkTraits<T>::SAMPLE;
-    p.s_eff = dim < S ? dim : S;
+    const long long S = TopkTraits<T>::SAMPLE;  // a multiple of CHUNK
+    p.s_eff = dim <= S ? dim : S;
     p.stride = dim / p.s_eff;
     if (p.s_eff == dim) {
         p.r_est = m;  // exact sample: est is the true m-th largest key
@@ -115,6 +118,11 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.tps = (int)((p.ntiles + segs - 1) / segs);
     p.nseg = (int)((p.ntiles + p.tps - 1) / p.tps);
     p.segcap = (long long)p.tps * te;
+    {
+        const int want = NSUB_MAX / (p.nseg * k);
+        p.split = want < 1 ? 1 : (want > 16 ? 16 : want);
+        p.nsub = p.nseg * p.split;  // <= max(nseg, NSUB_MAX / k) <= NSUB_MAX
+    }
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
     p.off_count = take(sizeof(unsigned long long) * 2 * k);  // [pass][k]
@@ -124,21 +132,22 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.off_hist0 = take(sizeof(unsigned) * (size_t)k * H0_BINS);
     p.off_hist0fb = take(sizeof(unsigned) * (size_t)k * H0_BINS);
     p.off_histr = take(sizeof(unsigned) * (size_t)k * TopkTraits<T>::ROUNDS_MAX * SEL_BINS);
-    p.off_status = take(sizeof(unsigned long long) * (size_t)k * p.nseg);
+    p.off_status = take(sizeof(unsigned long long) * (size_t)k * p.nsub);
     p.zero_end = o;
     p.off_sel = take(sizeof(SelState<K>) * k);
     p.off_cnt = take(sizeof(unsigned) * (size_t)k * p.ntiles);
     p.off_tstart = take(sizeof(unsigned) * (size_t)k * p.ntiles);
     p.off_segcnt = take(sizeof(unsigned) * (size_t)k * p.nseg);
-    p.off_seggt = take(sizeof(unsigned) * (size_t)k * p.nseg);
-    p.off_segbase = take(sizeof(unsigned) * (size_t)k * p.nseg);
+    p.off_seggt = take(sizeof(unsigned) * (size_t)k * p.nsub);
+    p.off_segbase = take(sizeof(unsigned) * (size_t)k * p.nsub);
     p.off_pmain = take(sizeof(double) * (size_t)k * p.nseg);
-    p.off_pwrite = take(sizeof(double) * (size_t)k * p.nseg);
+    p.off_pwrite = take(sizeof(double) * (size_t)k * p.nsub);
     const size_t cap = (size_t)k * p.nseg * p.segcap;
     p.off_cidx = take(sizeof(uint32_t) * cap);
     p.off_cval = take(sizeof(T) * cap);
     p.off_bkey = take(sizeof(K) * cap);
     p.off_bidx = take(sizeof(uint32_t) * cap);
+    p.off_bpos = take(sizeof(uint32_t) * cap);
     p.total = o + 256;  // slack for base alignment
     return p;
 }
@@ -310,90 +319,115 @@ SG_DEV unsigned block_select_small_u32(const unsigned* v, const uint8_t* flag, l
 }
 
 // --------------------------------------------------------------------------------------
-// k_estimate
+// k_estimate: the sample is S/32 randomly placed 32-element chunks (one per stratum of the
+// row, so every warp load is one coalesced 128-byte line for f32); est is the lower edge of
+// the 2048-bin histogram bin (over the sample's key range) that holds the r_est-th largest
+// sample key -- never above that key, so count(key >= est) >= m keeps its ~1 - 1e-9 odds.
+// With dim <= S the "sample" is the whole row and est is a lower bound of the true T.
 // --------------------------------------------------------------------------------------
+constexpr int CHUNK = 32;
+
 template <typename T>
 __global__ void __launch_bounds__(EST_THREADS)
-k_estimate(const T* __restrict__ g, long long ld, long long s_eff, long long stride, long long r_est,
+k_estimate(const T* __restrict__ g, long long ld, long long dim, long long s_eff, long long r_est,
            SelState<typename KeyOf<T>::K>* __restrict__ sel, uint4* __restrict__ zero, long long zero_vec) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     K* sk = reinterpret_cast<K*>(smem_raw);
     __shared__ unsigned hist[SEL_BINS];
-    __shared__ SelState<K> st;
     __shared__ K s_min[32], s_max[32];
-    const int w = blockIdx.x, tid = threadIdx.x;
+    __shared__ K s_lo, s_span;
+    __shared__ int s_shift;
+    const int w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (long long i = (long long)w * EST_THREADS + tid; i < zero_vec; i += (long long)gridDim.x * EST_THREADS)
         zero[i] = make_uint4(0, 0, 0, 0);
-
+    for (int i = tid; i < SEL_BINS; i += EST_THREADS) hist[i] = 0;
     const T* row = g + (long long)w * ld;
     K mn = KO::KMAX, mx = 0;
-    constexpr int BATCH = 8;
-    const unsigned long long ustride = (unsigned long long)stride;
-    for (long long base = 0; base < s_eff; base += (long long)EST_THREADS * BATCH) {
-        T v[BATCH];
-#pragma unroll
-        for (int u = 0; u < BATCH; ++u) {
-            const long long i = base + (long long)u * EST_THREADS + tid;
-            long long pos = i * stride;
-            if (stride > 1) {
-                // multiply-high keeps the offset uniform in [0, stride) without a division
-                const unsigned h = (unsigned)mix64((unsigned long long)i * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
-                pos += (long long)(((unsigned long long)h * ustride) >> 32);
-            }
-            v[u] = i < s_eff ? __ldg(row + pos) : (T)0;
+    if (s_eff == dim) {
+        for (long long i = tid; i < s_eff; i += EST_THREADS) {
+            const K key = KO::key(row[i]);
+            sk[i] = key;
+            mn = key < mn ? key : mn;
+            mx = key > mx ? key : mx;
         }
+    } else {
+        const long long nch = s_eff / CHUNK;
+        const long long stratum = dim / nch;  // >= CHUNK because dim > s_eff
+        constexpr int WARPS = EST_THREADS / 32;
+        constexpr int BATCH = 4;
+        for (long long c0 = warp; c0 < nch; c0 += (long long)WARPS * BATCH) {
+            T v[BATCH];
 #pragma unroll
-        for (int u = 0; u < BATCH; ++u) {
-            const long long i = base + (long long)u * EST_THREADS + tid;
-            if (i < s_eff) {
-                const K key = KO::key(v[u]);
-                sk[i] = key;
-                mn = key < mn ? key : mn;
-                mx = key > mx ? key : mx;
+            for (int u = 0; u < BATCH; ++u) {
+                const long long c = c0 + (long long)u * WARPS;
+                v[u] = (T)0;
+                if (c < nch) {
+                    const unsigned h = (unsigned)mix64((unsigned long long)c * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
+                    const long long off = (long long)(((unsigned long long)h * (unsigned long long)(stratum - CHUNK + 1)) >> 32);
+                    v[u] = __ldg(row + c * stratum + off + lane);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const long long c = c0 + (long long)u * WARPS;
+                if (c < nch) {
+                    const K key = KO::key(v[u]);
+                    sk[c * CHUNK + lane] = key;
+                    mn = key < mn ? key : mn;
+                    mx = key > mx ? key : mx;
+                }
             }
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
-        const K a = __shfl_xor_sync(FULL, mn, o), b = __shfl_xor_sync(FULL, mx, o);
-        mn = a < mn ? a : mn;
-        mx = b > mx ? b : mx;
+        const K x = __shfl_xor_sync(FULL, mn, o), y = __shfl_xor_sync(FULL, mx, o);
+        mn = x < mn ? x : mn;
+        mx = y > mx ? y : mx;
     }
-    if ((tid & 31) == 0) {
-        s_min[tid >> 5] = mn;
-        s_max[tid >> 5] = mx;
+    if (lane == 0) {
+        s_min[warp] = mn;
+        s_max[warp] = mx;
     }
     __syncthreads();
     if (tid == 0) {
-        K a = KO::KMAX, b = 0;
+        K x = KO::KMAX, y = 0;
         for (int i = 0; i < EST_THREADS / 32; ++i) {
-            a = s_min[i] < a ? s_min[i] : a;
-            b = s_max[i] > b ? s_max[i] : b;
+            x = s_min[i] < x ? s_min[i] : x;
+            y = s_max[i] > y ? s_max[i] : y;
         }
-        st.lo = a;
-        st.span = b - a;
-        st.shift = digit_shift<K>(st.span, SEL_BITS);
-        st.rank = (unsigned long long)r_est;
-        st.h = 0;
-        st.T = 0;
-        st.done = r_est > s_eff;
-        st.smax = b;
-        if (!st.done && st.span == 0) {
-            st.done = 1;
-            st.T = a;
-        }
+        s_lo = x;
+        s_span = y - x;
+        s_shift = digit_shift<K>(y - x, SEL_BITS);
     }
-    block_select<K, EST_THREADS>(sk, s_eff, st, hist);
-    if (tid == 0) {
-        SelState<K> o = st;
-        o.est = r_est > s_eff ? (K)0 : st.T;
-        o.shift0 = digit_shift<K>(o.smax > o.est ? o.smax - o.est : (K)0, H0_BITS);
-        o.done = 0;
-        o.mode = MODE_NORMAL;
-        o.wmode = WR_FAST;
-        o.idx_cut = 0xffffffffu;
-        sel[w] = o;
+    __syncthreads();
+    const K lo = s_lo;
+    const int shift = s_shift;
+    const long long ns = (s_eff / CHUNK) * CHUNK == s_eff || s_eff == dim ? s_eff : (s_eff / CHUNK) * CHUNK;
+    if (r_est <= ns) {
+        for (long long i = tid; i < ns; i += EST_THREADS) atomicAdd(&hist[digit<K>(sk[i], lo, shift, SEL_BINS)], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        K est = 0;
+        if (r_est <= ns) {
+            int bin;
+            unsigned long long above;
+            find_bin_from_top<SEL_BINS>(hist, (unsigned long long)r_est, bin, above);
+            est = bin < 0 ? (K)0 : lo + ((K)bin << shift);
+        }
+        if (lane == 0) {
+            SelState<K> o{};
+            o.smax = s_lo + s_span;
+            o.est = est;
+            o.shift0 = digit_shift<K>(o.smax > est ? o.smax - est : (K)0, H0_BITS);
+            o.done = 0;
+            o.mode = MODE_NORMAL;
+            o.wmode = WR_FAST;
+            o.idx_cut = 0xffffffffu;
+            sel[w] = o;
+        }
     }
 }
 
@@ -451,6 +485,230 @@ SG_DEV void load_tile(const T* row, long long base, long long dim, bool vec, typ
     }
 }
 
+// Segment epilogue shared by both main-pass kernels: fixed-tree partial norm, segment count,
+// max key, round-0 histogram flush; the last CTA of each worker picks the rank-m bin (or
+// flags the fallback pass when fewer than m keys reached est).
+template <typename T>
+SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typename KeyOf<T>::K mx, unsigned run,
+                        unsigned* hist, typename KeyOf<T>::K est, int shift0) {
+    using K = typename KeyOf<T>::K;
+    __shared__ double s_red[32];
+    __shared__ K s_kmax[32];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    SelState<K>* stp = a.sel + w;
+    ss = warp_sum(ss);
+    mx = warp_max<K>(mx);
+    if (lane == 0) {
+        s_red[warp] = ss;
+        s_kmax[warp] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        K km = 0;
+        for (int i = 0; i < nw; ++i) {
+            t = dadd(t, s_red[i]);
+            km = s_kmax[i] > km ? s_kmax[i] : km;
+        }
+        a.pmain[(long long)w * a.nseg + seg] = t;
+        a.segcnt[(long long)w * a.nseg + seg] = run;
+        if (km) atomicMax(a.maxkey + w, km);
+        if (run) atomicAdd(a.count + (long long)a.pass * a.k + w, (unsigned long long)run);
+    }
+    unsigned* gh = a.hist0 + (long long)w * H0_BINS;
+    for (int i = tid; i < H0_BINS; i += blockDim.x)
+        if (hist[i]) atomicAdd(gh + i, hist[i]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.done + w, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int i = tid; i < H0_BINS; i += blockDim.x) hist[i] = __ldcg(gh + i);
+    __syncthreads();
+    if (warp == 0) {
+        SelState<K> s = *stp;
+        const unsigned long long C = __ldcg(a.count + (long long)a.pass * a.k + w);
+        const K maxk = __ldcg(a.maxkey + w);
+        if (C < (unsigned long long)a.m) {
+            if (lane == 0) {  // estimate undershot (pass 0 only): run the fallback pass
+                s.mode = MODE_FALLBACK;
+                *stp = s;
+            }
+        } else {
+            s.lo = est;
+            s.span = maxk - est;
+            s.shift = shift0;
+            s.rank = (unsigned long long)a.m;
+            s.done = 0;
+            if (a.pass == 1) s.est = 0;
+            int bin;
+            unsigned long long above;
+            find_bin_from_top<H0_BINS>(hist, s.rank, bin, above);
+            if (lane == 0) {
+                if (bin < 0) {
+                    s.done = 1;
+                    s.T = est;
+                } else {
+                    narrow<K>(s, bin, above, hist[bin], H0_BINS, SEL_BITS);
+                }
+                *stp = s;
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// k_main_tma: float32 main pass fed by TMA bulk copies.  One elected thread keeps
+// MN_STAGES 16 KB tiles of the segment in flight (cp.async.bulk -> shared memory ring,
+// mbarrier completion, L2 evict-first); each thread owns 16 contiguous elements of a tile,
+// read from shared memory in a lane-rotated order that is bank-conflict free.  Per float4:
+// 4 fp64 FMAs for the sum of squares and one |max| test against the candidate threshold;
+// the rare candidates are placed with one warp scan per tile (index order preserved).
+// --------------------------------------------------------------------------------------
+constexpr int MN_STAGES = 4;
+constexpr int MN_TILE = 4096;
+
+__global__ void __launch_bounds__(TK_THREADS, 3)
+k_main_tma(MainArgs<float> a) {
+    using K = uint32_t;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* ring = reinterpret_cast<float*>(smem_raw);
+    __shared__ __align__(8) unsigned long long full[MN_STAGES];
+    __shared__ unsigned hist[H0_BINS];
+    __shared__ unsigned s_wtot[TK_NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = blockIdx.y, seg = blockIdx.x;
+    SelState<K>* stp = a.sel + w;
+    if (a.pass == 1 && stp->mode != MODE_FALLBACK) return;
+    const K est = a.pass == 1 ? 0u : stp->est;
+    const int shift0 = a.pass == 1 ? digit_shift<K>(KeyOf<float>::KMAX, H0_BITS) : stp->shift0;
+    const bool take_all = est == 0;
+    const float thr = take_all ? 0.f : __uint_as_float(est - 1u);  // key >= est <=> |x| >= thr
+    for (int i = tid; i < H0_BINS; i += TK_THREADS) hist[i] = 0;
+    const float* row = a.g + (long long)w * a.ld;
+    const long long t_begin = (long long)seg * a.tps;
+    const long long t_end = t_begin + a.tps < a.ntiles ? t_begin + a.tps : a.ntiles;
+    const int ntl = (int)(t_end - t_begin);
+    uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
+    float* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
+    unsigned long long policy = 0;
+    auto issue = [&](int i) {  // tile t_begin + i -> stage i % MN_STAGES (full tiles only)
+        const long long base = (t_begin + i) * MN_TILE;
+        if (base + MN_TILE > a.dim) return;
+        const int s = i % MN_STAGES;
+        mbar_expect_tx(&full[s], MN_TILE * 4);
+        bulk_g2s(ring + s * MN_TILE, row + base, MN_TILE * 4, &full[s], policy);
+    };
+    if (tid == 0) {
+        policy = policy_evict_first();
+        for (int s = 0; s < MN_STAGES; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+        for (int i = 0; i < MN_STAGES && i < ntl; ++i) issue(i);
+    }
+    __syncthreads();
+    double ss = 0.0, ss1 = 0.0;
+    K mx = 0;
+    unsigned run = 0;
+    const int rot = (lane >> 1) & 3;
+    for (int i = 0; i < ntl; ++i) {
+        const long long tile = t_begin + i;
+        const long long base = tile * MN_TILE;
+        const bool full_tile = base + MN_TILE <= a.dim;
+        const int s = i % MN_STAGES;
+        const float* tb = full_tile ? ring + s * MN_TILE : nullptr;
+        float4 y[4];
+        if (full_tile) {
+            mbar_wait(&full[s], (unsigned)(i / MN_STAGES) & 1u);
+            const float4* t4 = reinterpret_cast<const float4*>(tb);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) y[r] = t4[tid * 4 + ((r + rot) & 3)];
+        } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const long long e = base + tid * 16 + ((r + rot) & 3) * 4;
+                y[r].x = e < a.dim ? row[e] : 0.f;
+                y[r].y = e + 1 < a.dim ? row[e + 1] : 0.f;
+                y[r].z = e + 2 < a.dim ? row[e + 2] : 0.f;
+                y[r].w = e + 3 < a.dim ? row[e + 3] : 0.f;
+            }
+        }
+        // candidate mask over this thread's 16 contiguous elements (bit b <-> element 16*tid+b)
+        unsigned M = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const float4 v = y[r];
+            double& sr = (r & 1) ? ss1 : ss;  // two chains: half the DFMA dependency depth
+            sr = fma((double)v.x, (double)v.x, sr);
+            sr = fma((double)v.y, (double)v.y, sr);
+            sr = fma((double)v.z, (double)v.z, sr);
+            sr = fma((double)v.w, (double)v.w, sr);
+            const unsigned m4 = (fabsf(v.x) >= thr ? 1u : 0u) | (fabsf(v.y) >= thr ? 2u : 0u) |
+                                (fabsf(v.z) >= thr ? 4u : 0u) | (fabsf(v.w) >= thr ? 8u : 0u);
+            M |= m4 << (((r + rot) & 3) * 4);
+        }
+        if (take_all) M = 0xffffu;  // fallback pass: every element (NaN included) is a candidate
+        if (!full_tile) {
+            const long long left = a.dim - base - tid * 16;
+            M &= left >= 16 ? 0xffffu : (left <= 0 ? 0u : ((1u << left) - 1u));
+        }
+        // ordered placement: warp scan of the per-thread counts, block offsets via smem
+        const unsigned n = __popc(M);
+        unsigned incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_wtot[warp] = incl;
+        __syncthreads();
+        unsigned woff = 0, total = 0;
+#pragma unroll
+        for (int j = 0; j < TK_NW; ++j) {
+            const unsigned t = s_wtot[j];
+            woff += j < warp ? t : 0u;
+            total += t;
+        }
+        // the warp's candidates are processed cooperatively: lane k takes the warp's k-th one
+        const unsigned wtot = __shfl_sync(FULL, incl, 31);
+        for (unsigned k0 = 0; k0 < wtot; k0 += 32) {
+            const unsigned k = k0 + lane;
+            int o = 0;  // owner lane: first lane with incl > k
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const unsigned t = __shfl_sync(FULL, incl, o + step - 1);
+                if (t <= k) o += step;
+            }
+            const unsigned Mo = __shfl_sync(FULL, M, o);
+            const unsigned eo = __shfl_sync(FULL, incl - n, o);
+            if (k < wtot) {
+                const int bit = (int)__fns(Mo, 0, (int)(k - eo) + 1);
+                const int off = (warp * 32 + o) * 16 + bit;
+                const float val = full_tile ? tb[off] : row[base + off];
+                const K key = KeyOf<float>::key(val);
+                mx = key > mx ? key : mx;
+                atomicAdd(&hist[digit<K>(key, est, shift0, H0_BINS)], 1u);
+                const unsigned pos = run + woff + k;
+                ci[pos] = (uint32_t)(base + off);
+                cv[pos] = val;
+            }
+        }
+        if (tid == 0) {
+            const long long ti = (long long)w * a.ntiles + tile;
+            a.cnt[ti] = total;
+            a.tstart[ti] = run;
+        }
+        run += total;
+        __syncthreads();  // stage s fully consumed (and s_wtot free) before it is refilled
+        if (tid == 0 && i + MN_STAGES < ntl) {
+            fence_proxy_async();
+            issue(i + MN_STAGES);
+        }
+    }
+    main_finish<float>(a, w, seg, dadd(ss, ss1), mx, run, hist, est, shift0);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(TK_THREADS, 4)
 k_main(MainArgs<T> a) {
@@ -462,10 +720,7 @@ k_main(MainArgs<T> a) {
     __shared__ unsigned hist[H0_BINS];
     __shared__ unsigned s_wtot[32];
     __shared__ unsigned s_woff[32];
-    __shared__ double s_red[TK_NW];
-    __shared__ K s_kmax[TK_NW];
     __shared__ unsigned s_run, s_tbase;
-    __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, seg = blockIdx.x;
     SelState<K>* stp = a.sel + w;
@@ -554,76 +809,27 @@ k_main(MainArgs<T> a) {
             }
         }
     }
-    // per-segment partials: fixed element order and fixed reduction tree -> deterministic
-    ss = warp_sum(ss);
-    mx = warp_max<K>(mx);
-    if (lane == 0) {
-        s_red[warp] = ss;
-        s_kmax[warp] = mx;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double t = 0.0;
-        K km = 0;
-        for (int i = 0; i < TK_NW; ++i) {
-            t = dadd(t, s_red[i]);
-            km = s_kmax[i] > km ? s_kmax[i] : km;
-        }
-        a.pmain[(long long)w * a.nseg + seg] = t;
-        a.segcnt[(long long)w * a.nseg + seg] = s_run;
-        if (km) atomicMax(a.maxkey + w, km);
-        if (s_run) atomicAdd(a.count + (long long)a.pass * a.k + w, (unsigned long long)s_run);
-    }
-    unsigned* gh = a.hist0 + (long long)w * H0_BINS;
-    for (int i = tid; i < H0_BINS; i += TK_THREADS)
-        if (hist[i]) atomicAdd(gh + i, hist[i]);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(a.done + w, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // last CTA of this worker: round-0 pick
-    for (int i = tid; i < H0_BINS; i += TK_THREADS) hist[i] = __ldcg(gh + i);
-    __syncthreads();
-    if (warp == 0) {
-        SelState<K> s = *stp;
-        const unsigned long long C = __ldcg(a.count + (long long)a.pass * a.k + w);
-        const K maxk = __ldcg(a.maxkey + w);
-        if (C < (unsigned long long)a.m) {
-            if (lane == 0) {  // estimate undershot (pass 0 only): run the fallback pass
-                s.mode = MODE_FALLBACK;
-                *stp = s;
-            }
-        } else {
-            s.lo = est;
-            s.span = maxk - est;
-            s.shift = shift0;
-            s.rank = (unsigned long long)a.m;
-            s.done = 0;
-            if (a.pass == 1) s.est = 0;
-            int bin;
-            unsigned long long above;
-            find_bin_from_top<H0_BINS>(hist, s.rank, bin, above);
-            if (lane == 0) {
-                if (bin < 0) {
-                    s.done = 1;
-                    s.T = est;
-                } else {
-                    narrow<K>(s, bin, above, hist[bin], H0_BINS, SEL_BITS);
-                }
-                *stp = s;
-            }
-        }
-    }
+    main_finish<T>(a, w, seg, ss, mx, s_run, hist, est, shift0);
 }
 
 // --------------------------------------------------------------------------------------
 // k_collect: per-segment counts above the rank-m bin + boundary entries; last CTA resolves.
 // --------------------------------------------------------------------------------------
+// Sub-range i of a segment's n candidates for the split collect/write passes: starts are
+// 4-aligned so the writer's 16-byte loads stay aligned.
+SG_DEV long long sub_lo(long long n, int i, int split) {
+    return i == 0 ? 0 : ((n * i / split) & ~3ll);
+}
+SG_DEV int sub_of(long long n, long long off, int split) {
+    int i = split - 1;
+    while (i > 0 && sub_lo(n, i, split) > off) --i;
+    return i;
+}
+
 template <typename T> struct CollectArgs {
     long long segcap, cap;
-    int nseg, tps;
+    int nseg, tps, split, nsub;
+    uint32_t* bpos;                // [k][cap] boundary entry's position in its segment list
     SelState<typename KeyOf<T>::K>* sel;
     const unsigned* segcnt;
     const uint32_t* cidx;
@@ -644,44 +850,72 @@ k_collect(CollectArgs<T> a) {
     constexpr int TILE = tile_elems<T>();
     __shared__ unsigned s_gt[TK_NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int w = blockIdx.y, seg = blockIdx.x;
+    const int w = blockIdx.y, sub = blockIdx.x, seg = sub / a.split, part = sub % a.split;
     const SelState<K> st = a.sel[w];
     const K lo = st.lo, span = st.span;
-    const long long n = a.segcnt[(long long)w * a.nseg + seg];
+    const long long nseg_c = a.segcnt[(long long)w * a.nseg + seg];
+    const long long i_lo = sub_lo(nseg_c, part, a.split);
+    const long long i_hi = part + 1 == a.split ? nseg_c : sub_lo(nseg_c, part + 1, a.split);
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     K* bk = a.bkey + (long long)w * a.cap;
     uint32_t* bi = a.bidx + (long long)w * a.cap;
-    unsigned gt = 0;
-    for (long long i0 = 0; i0 < n; i0 += TK_THREADS) {
-        const long long i = i0 + tid;
-        bool in = false;
-        K key = 0;
-        if (i < n) {
-            key = KO::key(cv[i]);
-            in = key >= lo && key - lo <= span;
-            gt += key >= lo && key - lo > span;
+    // boundary entries are staged in shared memory and appended with one global atomic
+    constexpr int CU = 4, CSTAGE = 2 * CU * TK_THREADS;
+    __shared__ K st_key[CSTAGE];
+    __shared__ uint32_t st_idx[CSTAGE];
+    __shared__ uint32_t st_pos[CSTAGE];
+    __shared__ unsigned s_n;
+    __shared__ unsigned long long s_base;
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    auto flush = [&]() {
+        const unsigned cnt = s_n;
+        if (cnt == 0) return;
+        if (tid == 0) s_base = atomicAdd(a.bndn + w, (unsigned long long)cnt);
+        __syncthreads();
+        uint32_t* bp = a.bpos + (long long)w * a.cap;
+        for (unsigned q = tid; q < cnt; q += TK_THREADS) {
+            bk[s_base + q] = st_key[q];
+            bi[s_base + q] = st_idx[q];
+            bp[s_base + q] = st_pos[q];
         }
-        const unsigned bal = __ballot_sync(FULL, in);
-        if (bal) {
-            unsigned long long base = 0;
-            const int leader = __ffs(bal) - 1;
-            if (lane == leader) base = atomicAdd(a.bndn + w, (unsigned long long)__popc(bal));
-            base = __shfl_sync(FULL, base, leader);
-            if (in) {
-                const unsigned long long q = base + __popc(bal & lanemask_lt());
-                bk[q] = key;
-                bi[q] = ci[i];
+        __syncthreads();
+        if (tid == 0) s_n = 0;
+        __syncthreads();
+    };
+    unsigned gt = 0;
+    for (long long i0 = i_lo; i0 < i_hi; i0 += CU * TK_THREADS) {
+        T v[CU];
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+            const long long i = i0 + u * TK_THREADS + tid;
+            v[u] = i < i_hi ? cv[i] : (T)0;
+        }
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+            const long long i = i0 + u * TK_THREADS + tid;
+            if (i >= i_hi) continue;
+            const K key = KO::key(v[u]);
+            gt += key >= lo && key - lo > span;
+            if (key >= lo && key - lo <= span) {
+                const unsigned q = atomicAdd(&s_n, 1u);
+                st_key[q] = key;
+                st_idx[q] = ci[i];
+                st_pos[q] = (uint32_t)i;
             }
         }
+        __syncthreads();
+        if (s_n > CSTAGE - CU * TK_THREADS) flush();
     }
+    flush();
     for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(FULL, gt, o);
     if (lane == 0) s_gt[warp] = gt;
     __syncthreads();
     if (tid == 0) {
         unsigned t = 0;
         for (int i = 0; i < TK_NW; ++i) t += s_gt[i];
-        a.seggt[(long long)w * a.nseg + seg] = t;
+        a.seggt[(long long)w * a.nsub + sub] = t;
     }
 }
 
@@ -698,11 +932,12 @@ k_resolve_small(CollectArgs<T> a) {
     __shared__ unsigned hist[SEL_BINS];
     __shared__ SelState<K> sst;
     __shared__ unsigned s_eq, s_res[2];
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.x;
+    constexpr int RES = TopkTraits<T>::RES;
     const unsigned long long h = a.bndn[w];
-    if (h > RESOLVE_SMEM) {
+    if (h > RES) {
         if (tid == 0) {
             SelState<K> s = a.sel[w];
             s.wmode = WR_SLOW;
@@ -711,16 +946,19 @@ k_resolve_small(CollectArgs<T> a) {
         return;
     }
     K* sk = reinterpret_cast<K*>(smem_raw);
-    uint32_t* si = reinterpret_cast<uint32_t*>(sk + RESOLVE_SMEM);
-    uint8_t* sf = reinterpret_cast<uint8_t*>(si + RESOLVE_SMEM);
-    unsigned* kb = reinterpret_cast<unsigned*>(sf + RESOLVE_SMEM);  // [nseg]
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + RES);
+    uint32_t* sp = si + RES;                               // position in the segment list
+    unsigned* kb = sp + RES;                               // [nsub]
+    uint8_t* sf = reinterpret_cast<uint8_t*>(kb + NSUB_MAX);
     const K* bk = a.bkey + (long long)w * a.cap;
     const uint32_t* bi = a.bidx + (long long)w * a.cap;
+    const uint32_t* bpp = a.bpos + (long long)w * a.cap;
     for (long long i = tid; i < (long long)h; i += NT) {
         sk[i] = bk[i];
         si[i] = bi[i];
+        sp[i] = bpp[i];
     }
-    for (int i = tid; i < a.nseg; i += NT) kb[i] = 0;
+    for (int i = tid; i < a.nsub; i += NT) kb[i] = a.seggt[(long long)w * a.nsub + i];
     if (tid == 0) {
         sst = a.sel[w];
         s_eq = 0;
@@ -743,22 +981,26 @@ k_resolve_small(CollectArgs<T> a) {
     // kept boundary entries per segment
     for (long long i = tid; i < (long long)h; i += NT) {
         const K key = sk[i];
-        if (key > T_ || (key == T_ && si[i] <= cut)) atomicAdd(&kb[(si[i] / TILE) / a.tps], 1u);
+        if (key > T_ || (key == T_ && si[i] <= cut)) {
+            const int seg = (int)((si[i] / TILE) / a.tps);
+            const long long nsc = a.segcnt[(long long)w * a.nseg + seg];
+            atomicAdd(&kb[seg * a.split + sub_of(nsc, sp[i], a.split)], 1u);
+        }
     }
     __syncthreads();
     if (warp == 0) {
-        // exclusive scan over segments of (count above the bin + kept boundary)
+        // exclusive scan over sub-ranges of (count above the bin + kept boundary)
         unsigned carry = 0;
-        for (int s0 = 0; s0 < a.nseg; s0 += 32) {
+        for (int s0 = 0; s0 < a.nsub; s0 += 32) {
             const int s = s0 + lane;
-            const unsigned v = s < a.nseg ? a.seggt[(long long)w * a.nseg + s] + kb[s] : 0u;
+            const unsigned v = s < a.nsub ? kb[s] : 0u;
             unsigned incl = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned y = __shfl_up_sync(FULL, incl, o);
                 if (lane >= o) incl += y;
             }
-            if (s < a.nseg) a.segbase[(long long)w * a.nseg + s] = carry + incl - v;
+            if (s < a.nsub) a.segbase[(long long)w * a.nsub + s] = carry + incl - v;
             carry += __shfl_sync(FULL, incl, 31);
         }
         if (lane == 0) {
@@ -837,7 +1079,7 @@ k_resolve(ResolveArgs<T> a, int round) {
 // --------------------------------------------------------------------------------------
 template <typename T> struct WriteArgs {
     long long ntiles, segcap, m;
-    int k, nseg, tps;
+    int k, nseg, tps, split, nsub;
     const SelState<typename KeyOf<T>::K>* sel;
     const unsigned* tstart;
     const unsigned* segcnt;
@@ -895,16 +1137,19 @@ k_write(WriteArgs<T> a) {
     __shared__ unsigned long long s_gb, s_eb;
     __shared__ double s_red[TK_NW];
     __shared__ int s_last;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned* s_ts = reinterpret_cast<unsigned*>(smem_raw);  // [tps] tile starts of this segment
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int w = blockIdx.y, seg = blockIdx.x;
+    const int w = blockIdx.y, sub = blockIdx.x, seg = sub / a.split, part = sub % a.split;
     const SelState<K> st = a.sel[w];
     const K T_ = st.T;
     const unsigned cut = st.idx_cut;
     const unsigned long long need = st.rank;
     const bool slow = st.wmode == WR_SLOW;
-    const long long n = a.segcnt[(long long)w * a.nseg + seg];
+    const long long nsc = a.segcnt[(long long)w * a.nseg + seg];
+    const long long i_lo = sub_lo(nsc, part, a.split);
+    const long long n = part + 1 == a.split ? nsc : sub_lo(nsc, part + 1, a.split);  // end of the sub-range
+    const bool last_part = part + 1 == a.split;
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     const long long t0 = (long long)seg * a.tps;
@@ -915,12 +1160,12 @@ k_write(WriteArgs<T> a) {
 
     unsigned long long gb, eb;  // kept-before counters (fast mode: gb only)
     if (!slow) {
-        gb = a.segbase[(long long)w * a.nseg + seg];
+        gb = a.segbase[(long long)w * a.nsub + sub];
         eb = 0;
     } else {
         // pass 1: counts, then a decoupled look-back over this worker's segments
         unsigned gc = 0, ec = 0;
-        for (long long i = tid; i < n; i += TK_THREADS) {
+        for (long long i = i_lo + tid; i < n; i += TK_THREADS) {
             const K key = KO::key(cv[i]);
             gc += key > T_;
             ec += key == T_;
@@ -941,7 +1186,7 @@ k_write(WriteArgs<T> a) {
                 etot += s_ew[i];
             }
             const unsigned long long pre =
-                lookback(a.status + (long long)w * a.nseg, seg, (gtot << CNT_BITS) | etot);
+                lookback(a.status + (long long)w * a.nsub, sub, (gtot << CNT_BITS) | etot);
             if (lane == 0) {
                 s_gb = pre >> CNT_BITS;
                 s_eb = pre & CNT_MASK;
@@ -955,18 +1200,35 @@ k_write(WriteArgs<T> a) {
     uint32_t* oi = a.idx + (long long)w * a.m;
     T* ov = a.val + (long long)w * a.m;
     double ss = 0.0;
-    for (long long c0 = 0; c0 < n; c0 += WR_CHUNK) {
+    __shared__ unsigned s_kb[WR_CHUNK];  // kept-before count per entry of the chunk (merge offsets)
+    for (long long c0 = i_lo; c0 < n; c0 += WR_CHUNK) {
         unsigned kflag = 0, eflag = 0;
         T vv[WR_EPT];
         uint32_t ii[WR_EPT];
+        const long long e0i = c0 + tid * WR_EPT;
+        if constexpr (sizeof(T) == 4) {
+            if (e0i + WR_EPT <= n) {  // segment base and chunk start are 16-byte aligned
+                const float4 v4 = *reinterpret_cast<const float4*>(cv + e0i);
+                const uint4 i4 = *reinterpret_cast<const uint4*>(ci + e0i);
+                vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
+                ii[0] = i4.x; ii[1] = i4.y; ii[2] = i4.z; ii[3] = i4.w;
+            } else {
+#pragma unroll
+                for (int u = 0; u < WR_EPT; ++u) {
+                    vv[u] = e0i + u < n ? cv[e0i + u] : (T)0;
+                    ii[u] = e0i + u < n ? ci[e0i + u] : 0u;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < WR_EPT; ++u) {
+                vv[u] = e0i + u < n ? cv[e0i + u] : (T)0;
+                ii[u] = e0i + u < n ? ci[e0i + u] : 0u;
+            }
+        }
 #pragma unroll
         for (int u = 0; u < WR_EPT; ++u) {
-            const long long e = c0 + tid * WR_EPT + u;
-            vv[u] = (T)0;
-            ii[u] = 0;
-            if (e < n) {
-                vv[u] = cv[e];
-                ii[u] = ci[e];
+            if (e0i + u < n) {
                 const K key = KO::key(vv[u]);
                 if (!slow) {
                     kflag |= (key > T_ || (key == T_ && ii[u] <= cut) ? 1u : 0u) << u;
@@ -997,19 +1259,10 @@ k_write(WriteArgs<T> a) {
         e0 += ex;
 #pragma unroll
         for (int u = 0; u < WR_EPT; ++u) {
-            const long long e = c0 + tid * WR_EPT + u;
+            const long long e = e0i + u;
             if (e >= n) break;
             const unsigned long long kb4 = slow ? g0 + (e0 < need ? e0 : need) : g0;
-            if (toff) {
-                // tiles whose first candidate is entry e: merge offset = kept before e
-                int lo = 0, hi = nt;  // first j with s_ts[j] >= e
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if ((long long)s_ts[mid] < e) lo = mid + 1;
-                    else hi = mid;
-                }
-                for (int j = lo; j < nt && (long long)s_ts[j] == e; ++j) toff[t0 + j] = (int)kb4;
-            }
+            if (toff) s_kb[tid * WR_EPT + u] = (unsigned)kb4;
             const bool isk = (kflag >> u) & 1u, ise = (eflag >> u) & 1u;
             bool keep = false;
             unsigned long long pos = 0;
@@ -1031,13 +1284,22 @@ k_write(WriteArgs<T> a) {
         gb += gsum;
         eb += esum;
         __syncthreads();
+        if (toff) {
+            // tiles whose first candidate lies in this chunk: merge offset = kept before it
+            const long long c1 = c0 + WR_CHUNK < n ? c0 + WR_CHUNK : n;
+            for (int j = tid; j < nt; j += TK_THREADS) {
+                const long long t = s_ts[j];
+                if (t >= c0 && t < c1) toff[t0 + j] = (int)s_kb[t - c0];
+            }
+            __syncthreads();
+        }
     }
-    if (toff && tid == 0) {
-        // tiles with no candidate at or after the last entry: offset = kept total so far
+    if (toff && last_part) {
+        // tiles with no candidate at or after the segment's last entry: offset = kept total
         const unsigned long long kept = slow ? gb + (eb < need ? eb : need) : gb;
-        for (int j = 0; j < nt; ++j)
+        for (int j = tid; j < nt; j += TK_THREADS)
             if ((long long)s_ts[j] >= n) toff[t0 + j] = (int)kept;
-        if (t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
+        if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }
     ss = warp_sum(ss);
     if (lane == 0) s_red[warp] = ss;
@@ -1045,7 +1307,7 @@ k_write(WriteArgs<T> a) {
     if (tid == 0) {
         double s = 0.0;
         for (int i = 0; i < TK_NW; ++i) s = dadd(s, s_red[i]);
-        a.pwrite[(long long)w * a.nseg + seg] = s;
+        a.pwrite[(long long)w * a.nsub + sub] = s;
     }
     // last CTA overall: fixed-order norm reductions + gate
     __threadfence();
@@ -1058,8 +1320,8 @@ k_write(WriteArgs<T> a) {
         double sf = 0.0, sk = 0.0;
         for (int i = lane; i < a.nseg; i += 32) {
             sf = dadd(sf, __ldcg(a.pmain + (long long)ww * a.nseg + i));
-            sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nseg + i));
         }
+        for (int i = lane; i < a.nsub; i += 32) sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nsub + i));
         sf = warp_sum(sf);
         sk = warp_sum(sk);
         if (lane == 0) {
@@ -1094,12 +1356,23 @@ __global__ void k_gate_update(const double* norms2, int k, sg_gate_state* states
 // --------------------------------------------------------------------------------------
 // Host launcher.
 // --------------------------------------------------------------------------------------
+constexpr size_t MN_SMEM = (size_t)MN_STAGES * MN_TILE * sizeof(float);
+
 template <typename T> int segments_per_worker(int k) {
     int dev = 0, sms = 148, per_sm = 4;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_main<T>, TK_THREADS, 0) != cudaSuccess)
-        per_sm = 4;
+    cudaError_t e;
+    if constexpr (sizeof(T) == 4) {
+        cudaFuncSetAttribute(k_main_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MN_SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_main_tma, TK_THREADS, MN_SMEM);
+    } else {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_main<T>, TK_THREADS, 0);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        per_sm = sizeof(T) == 4 ? 3 : 4;
+    }
     if (per_sm < 1) per_sm = 1;
     const int s = sms * per_sm / k;
     return s < 1 ? 1 : s;
@@ -1153,7 +1426,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     // 1. estimate (+ zero the small scratch, incl. the slow-mode look-back status words)
     const size_t est_smem = sizeof(K) * (size_t)TopkTraits<T>::SAMPLE;
     cudaFuncSetAttribute(k_estimate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)est_smem);
-    k_estimate<T><<<k, EST_THREADS, est_smem, stream>>>(g, ld, p.s_eff, p.stride, p.r_est, sel,
+    k_estimate<T><<<k, EST_THREADS, est_smem, stream>>>(g, ld, dim, p.s_eff, p.r_est, sel,
                                                          reinterpret_cast<uint4*>(base),
                                                          (long long)(p.zero_end / 16));
     // 2. main streaming pass, then the (normally empty) fallback pass
@@ -1181,17 +1454,31 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ma.hist0 = hist0;
     ma.done = c_main;
     const dim3 sgrid((unsigned)p.nseg, (unsigned)k);
-    k_main<T><<<sgrid, TK_THREADS, 0, stream>>>(ma);
+    bool tma = false;
+    if constexpr (sizeof(T) == 4) tma = vec_ok;
+    auto launch_main = [&]() {
+        if constexpr (sizeof(T) == 4) {
+            if (tma) {
+                k_main_tma<<<sgrid, TK_THREADS, MN_SMEM, stream>>>(ma);
+                return;
+            }
+        }
+        k_main<T><<<sgrid, TK_THREADS, 0, stream>>>(ma);
+    };
+    launch_main();
     ma.pass = 1;
     ma.hist0 = hist0fb;
     ma.done = c_fb;
-    k_main<T><<<sgrid, TK_THREADS, 0, stream>>>(ma);
+    launch_main();
     // 3. per-segment counts + boundary, in-CTA resolve
     CollectArgs<T> ca;
     ca.segcap = p.segcap;
     ca.cap = capw;
     ca.nseg = p.nseg;
     ca.tps = p.tps;
+    ca.split = p.split;
+    ca.nsub = p.nsub;
+    ca.bpos = reinterpret_cast<uint32_t*>(at(p.off_bpos));
     ca.sel = sel;
     ca.segcnt = segcnt;
     ca.cidx = cidx;
@@ -1202,8 +1489,9 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ca.bidx = bidx;
     ca.bndn = bndn;
     ca.done = c_col;
-    k_collect<T><<<sgrid, TK_THREADS, 0, stream>>>(ca);
-    const size_t res_smem = (sizeof(K) + sizeof(uint32_t) + 1) * RESOLVE_SMEM + sizeof(unsigned) * BMAX;
+    const dim3 subgrid((unsigned)p.nsub, (unsigned)k);
+    k_collect<T><<<subgrid, TK_THREADS, 0, stream>>>(ca);
+    const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES + sizeof(unsigned) * NSUB_MAX;
     cudaFuncSetAttribute(k_resolve_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem);
     k_resolve_small<T><<<k, 1024, res_smem, stream>>>(ca);
     // 4. slow mode only: multi-CTA select rounds over an oversized boundary
@@ -1225,6 +1513,8 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.k = k;
     wa.nseg = p.nseg;
     wa.tps = p.tps;
+    wa.split = p.split;
+    wa.nsub = p.nsub;
     wa.sel = sel;
     wa.tstart = tstart;
     wa.segcnt = segcnt;
@@ -1243,7 +1533,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.decision = decision;
     wa.rho = rho;
     const size_t wr_smem = sizeof(unsigned) * (size_t)p.tps;
-    k_write<T><<<sgrid, TK_THREADS, wr_smem, stream>>>(wa);
+    k_write<T><<<subgrid, TK_THREADS, wr_smem, stream>>>(wa);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

@@ -187,7 +187,8 @@ def weighted_aggregate(
         int(bool(first_step)), _ptr(ws), nbytes if ws is not None else 0, _stream(),
     )
     _capi.check(st, "sg_weighted_aggregate")
-    _count(1 + (1 if ws is not None else 0))
+    pipe = dt == torch.float32 and compressed is not None and params is not None
+    _count(1 + (1 if pipe else 0) + (1 if ws is not None else 0))
     return out
 
 
