@@ -265,15 +265,16 @@ def run_ours(args):
         return float(t.item())
 
     # ---- device-resident timing -------------------------------------------------------
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    clocks = Clocks(cvd.split(",")[local] if cvd else local)
+    clocks.start()  # sampled over warm-up, timed region and the e2e leg (>= several hundred ms)
+    time.sleep(0.3)
     for _ in range(args.warmup):
         ex.step(w, lr)
     K = args.steps
     ev_topk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
-    clocks = Clocks(cvd.split(",")[local] if cvd else local)
     barrier()
-    clocks.start()
     launches0 = kernels.LAUNCHES["n"]
     paths = []
     s_ev.record()
@@ -282,7 +283,6 @@ def run_ours(args):
         paths.append(info.path)
     e_ev.record()
     barrier()
-    clk = clocks.stop()
     launches = kernels.LAUNCHES["n"] - launches0
     t_ms = reduce_max(s_ev.elapsed_time(e_ev))
     topk_ms = [a.elapsed_time(b) for a, b in ev_topk] if compression else []
@@ -345,6 +345,7 @@ def run_ours(args):
                "d2h_bytes_per_step": int(D * 4 + (k if compression else 0)), "steps": ke,
                "path": "GradientExchange.step on pinned host gradients, aggregate copied back"}
 
+    clk = clocks.stop()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_measure(args, W, steps=args.cpu_steps)

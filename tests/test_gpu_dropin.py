@@ -1,0 +1,137 @@
+"""GPU parity of the drop-in surface: the reference training loop's gate/aggregate/step calls
+replayed through paper_2301_08897_b200.{comm,nn} (float64 kernels) against the recorded
+reference run, the live reference engine with the modules swapped in (metrics.csv
+byte-identical), and the device-staged sampler + injection (item 5)."""
+
+import io
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def test_engine_replay_bit_exact(cuda):
+    """12 iterations of config 1 (4 devices, S-weighted, cr .1, delta .5): every gate decision,
+    aggregate and post-step parameter vector equals the reference's bit-for-bit."""
+    from paper_2301_08897_b200 import comm, nn
+
+    z = np.load(GOLDEN / "engine_replay.npz")
+    cfg = json.loads((GOLDEN / "config1.json").read_text())
+    cr, delta = cfg["compression"]["cr"], cfg["compression"]["delta"]
+    states = [comm.CompressionState(cr=cr, delta=delta) for _ in range(4)]
+    opts = [nn.OptimizerState(momentum=float(z["momentum"]), weight_decay=float(z["weight_decay"])) for _ in range(4)]
+    params = [z["p0"].copy() for _ in range(4)]
+    for it in range(z["g"].shape[0]):
+        payloads = []
+        for d in range(4):
+            dec = comm.compression_gate(z["g"][it, d], states[d])
+            assert dec.compressed == bool(z["dec"][it, d]), (it, d)
+            assert abs(dec.ratio - float(z["rho"][it, d])) <= 1e-12
+            payloads.append(dec.payload)
+        agg = comm.weighted_aggregate(payloads, z["w"][it])
+        assert np.array_equal(agg.view(np.uint64), z["agg"][it].view(np.uint64)), it
+        for d in range(4):
+            nn.sgd_momentum_step(opts[d], params[d], agg, float(z["lr"][it]))
+        for d in range(4):
+            assert np.array_equal(params[d].view(np.uint64), z["params"][it].view(np.uint64)), (it, d)
+
+
+def _reference_engine():
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "streamsgd").exists():
+        pytest.skip("reference package not installed in baseline/_ref")
+    sys.path.insert(0, str(ref))
+    import streamsgd.cli as cli
+    import streamsgd.config as config
+    import streamsgd.engine as engine
+
+    return cli, config, engine
+
+
+def test_live_dropin_metrics_csv_byte_identical(cuda):
+    """The unmodified reference loop with comm/nn swapped for this package (dropin.install)
+    writes a metrics.csv byte-identical to the reference run's."""
+    import csv
+
+    from paper_2301_08897_b200 import dropin
+
+    cli, config, engine = _reference_engine()
+    cfg = config.parse_config((GOLDEN / "config1.json").read_text())
+    saved = dropin.install(engine)
+    try:
+        result = engine.run_experiment(cfg)
+    finally:
+        dropin.uninstall(engine, saved)
+    buf = io.StringIO()
+    w = csv.writer(buf, lineterminator="\n")
+    w.writerow(cli.metrics_columns(cfg.n_devices))
+    for row in result.metrics:
+        w.writerow(cli.metrics_row(row))
+    assert buf.getvalue() == (GOLDEN / "config1_metrics.csv").read_text()
+
+
+def test_device_sampler_and_injection_match_reference(cuda):
+    from paper_2301_08897_b200 import streams
+
+    z = np.load(GOLDEN / "sampler.npz")
+    pools = [z[f"pool{d}"] for d in range(8)]
+    ds = streams.DeviceSampler(z["train_x"], z["train_y"], pools, device=cuda)
+    ds.set_augmentation(z["augment"])
+    # 20 ids per device starting at 57: rows = pools[d][a % len(pool)] (engine.py:223-227)
+    draws = [range(57, 77) for _ in range(8)]
+    x, y, ptr = ds.stage(draws)
+    want_rows = z["rows"]
+    want_x = z["train_x"][want_rows] + z["augment"][want_rows]
+    assert np.array_equal(x.cpu().numpy().view(np.uint64), want_x.view(np.uint64))
+    assert np.array_equal(y.cpu().numpy(), z["train_y"][want_rows])
+    assert ptr.tolist() == list(range(0, 161, 20))
+    # injection: device-built augmented batches equal datagen.inject's lists
+    inj = json.loads((GOLDEN / "injection.json").read_text())
+    bs = [31, 30, 8, 30, 42, 66, 22, 14]
+    for case in inj:
+        plan = streams.injection_plan(8, case["alpha"], case["beta"], bs,
+                                      streams.derive_seed(0, f"inject-plan:{case['it']}"))
+        rng = np.random.default_rng(streams.derive_seed(0, f"inject-draw:{case['it']}"))
+        picks = streams.injection_picks(plan, bs, rng)
+        # identity pools so rows == stream ids: pool d = [100d, 100d + 100)
+        ident = [np.arange(100 * d, 100 * d + 100) for d in range(8)]
+        tx = np.arange(800, dtype=np.float64)[:, None] * np.ones((1, 3))
+        s2 = streams.DeviceSampler(tx, np.arange(800), ident, device=cuda)
+        x, y, ptr = s2.stage([range(0, bs[d]) for d in range(8)], plan, picks)
+        got = [y[ptr[d]:ptr[d + 1]].cpu().tolist() for d in range(8)]
+        assert got == case["batches"], case["it"]
+
+
+def test_stream_buffer_drives_device_sampler(cuda):
+    """Persistence-policy buffers over several iterations: the device rows equal the deque
+    reference's ids mapped through the pools."""
+    from oracle import streams_ref
+    from paper_2301_08897_b200 import streams
+
+    z = np.load(GOLDEN / "sampler.npz")
+    pools = [z[f"iidpool{d}"] for d in range(8)]
+    ds = streams.DeviceSampler(z["train_x"], z["train_y"], pools, device=cuda)
+    rates = [31, 30, 1, 30, 42, 66, 22, 14]
+    bufs = [streams.StreamBuffer(r) for r in rates]
+    refs = [streams_ref.DequeBuffer(r) for r in rates]
+    b = [min(max(r, 8), 1024) for r in rates]
+    for it in range(6):
+        wait = max(streams.streaming_wait(len(q), b[d], rates[d]) for d, q in enumerate(bufs))
+        for q, r in zip(bufs, refs):
+            q.enqueue_arrivals(wait)
+            r.enqueue(wait)
+        draws = [q.draw_batch(b[d]) for d, q in enumerate(bufs)]
+        want = [[int(pools[d][a % len(pools[d])]) for a in r.draw(b[d])] for d, r in enumerate(refs)]
+        x, y, ptr = ds.stage(draws)
+        for d in range(8):
+            assert y[ptr[d]:ptr[d + 1]].cpu().tolist() == z["train_y"][want[d]].tolist()
+        for q, r in zip(bufs, refs):
+            q.enqueue_arrivals(1.0 + 0.001 * sum(b))
+            r.enqueue(1.0 + 0.001 * sum(b))
