@@ -81,6 +81,14 @@ int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m,
                      sg_gate_state* states, uint8_t* decision, double* rho,
                      void* workspace, size_t workspace_bytes, void* stream);
 
+/* Diagnostics of the most recent sg_topk_gate_* call that used `workspace` (same k, dim, m):
+ * out[4j..4j+3] (device int64) = {candidates kept by the main pass, boundary entries, fallback
+ * pass taken (0/1), oversized-tie write mode (0/1)} for worker j. */
+int sg_topk_stats_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes,
+                      int64_t* out, void* stream);
+int sg_topk_stats_f64(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes,
+                      int64_t* out, void* stream);
+
 /* Gate update alone from precomputed norms2[2k] (comm.py:143-160). */
 int sg_gate_update(const double* norms2, int k, sg_gate_state* states,
                    uint8_t* decision, double* rho, void* stream);

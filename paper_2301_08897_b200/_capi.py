@@ -64,6 +64,8 @@ SIGNATURES = {
     "sg_topk_gate_f32": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
     "sg_topk_gate_f64": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
     "sg_gate_update": (c_int, [_P, c_int, _P, _P, _P, _P]),
+    "sg_topk_stats_f32": (c_int, [c_int, c_int64, c_int64, _P, c_size_t, _P, _P]),
+    "sg_topk_stats_f64": (c_int, [c_int, c_int64, c_int64, _P, c_size_t, _P, _P]),
     "sg_aggregate_workspace_bytes": (c_size_t, [c_int, c_int64]),
     "sg_weighted_aggregate_f32": (
         c_int,

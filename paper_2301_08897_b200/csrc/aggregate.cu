@@ -918,6 +918,7 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
             if (sm <= 110 * 1024) {
                 cudaFuncSetAttribute(k_merge_pipe<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 k_merge_pipe<TO><<<(unsigned)((ntiles + tpb - 1) / tpb), MG_THREADS, sm, stream>>>(a, tpb);
+                debug_sync("k_merge_pipe", stream);
             } else {
                 a.pipe = 0;
             }
@@ -926,6 +927,7 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
         long long grid = (long long)sms * 2;
         if (grid > ntiles) grid = ntiles;
         k_merge<TO><<<(unsigned)grid, MG_THREADS, MG_SMEM, stream>>>(a);
+        debug_sync("k_merge", stream);
     }
     else
         k_aggregate<TI, TO><<<(unsigned)ntiles, AG_THREADS, 0, stream>>>(a);

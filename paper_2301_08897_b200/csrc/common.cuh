@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "../../include/scadles_b200.h"
 
@@ -217,6 +219,17 @@ SG_DEV void cp_async4(void* dst, const void* src) {
 }
 SG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N> SG_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// SG_DEBUG_SYNC=1: synchronise after every launch and report the first failing kernel.
+inline void debug_sync(const char* what, cudaStream_t stream) {
+    static const bool on = [] {
+        const char* e = getenv("SG_DEBUG_SYNC");
+        return e && *e == '1';
+    }();
+    if (!on) return;
+    const cudaError_t e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) fprintf(stderr, "[scadles_b200] %s: %s\n", what, cudaGetErrorString(e));
+}
 
 inline int num_sms() {
     int dev = 0, n = 148;

@@ -39,7 +39,7 @@ constexpr int TK_THREADS = 256;
 constexpr int TK_ROUNDS = 4;  // 16-byte vectors per thread per tile
 constexpr int TK_NW = TK_THREADS / 32;
 static_assert(TK_ROUNDS * TK_NW == 32, "one warp scans the per-(round, warp) totals");
-constexpr int H0_BITS = 10;
+constexpr int H0_BITS = 12;
 constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
@@ -567,7 +567,7 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
 // 4 fp64 FMAs for the sum of squares and one |max| test against the candidate threshold;
 // the rare candidates are placed with one warp scan per tile (index order preserved).
 // --------------------------------------------------------------------------------------
-constexpr int MN_STAGES = 4;
+constexpr int MN_STAGES = 3;
 constexpr int MN_TILE = 4096;
 
 __global__ void __launch_bounds__(TK_THREADS, 3)
@@ -612,48 +612,26 @@ k_main_tma(MainArgs<float> a) {
     K mx = 0;
     unsigned run = 0;
     const int rot = (lane >> 1) & 3;
-    for (int i = 0; i < ntl; ++i) {
-        const long long tile = t_begin + i;
-        const long long base = tile * MN_TILE;
-        const bool full_tile = base + MN_TILE <= a.dim;
-        const int s = i % MN_STAGES;
-        const float* tb = full_tile ? ring + s * MN_TILE : nullptr;
-        float4 y[4];
-        if (full_tile) {
-            mbar_wait(&full[s], (unsigned)(i / MN_STAGES) & 1u);
-            const float4* t4 = reinterpret_cast<const float4*>(tb);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) y[r] = t4[tid * 4 + ((r + rot) & 3)];
-        } else {
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const long long e = base + tid * 16 + ((r + rot) & 3) * 4;
-                y[r].x = e < a.dim ? row[e] : 0.f;
-                y[r].y = e + 1 < a.dim ? row[e + 1] : 0.f;
-                y[r].z = e + 2 < a.dim ? row[e + 2] : 0.f;
-                y[r].w = e + 3 < a.dim ? row[e + 3] : 0.f;
-            }
+    // full tiles come from the TMA ring; a partial last tile (only ever the row's last) is
+    // read directly after the loop, so the hot loop carries no bounds logic
+    const int nfull = (t_end * MN_TILE <= a.dim) ? ntl : ntl - 1;
+    auto place = [&](unsigned M, long long base, const float* src, unsigned n, unsigned incl, unsigned woff) {
+        // lane-local ordered writes of this thread's candidates (usually 0-2 of them)
+        unsigned pos = run + woff + incl - n;
+        while (M) {
+            const int b = __ffs(M) - 1;
+            M &= M - 1;
+            const int off = tid * 16 + b;
+            const float val = src[off];
+            const K key = KeyOf<float>::key(val);
+            mx = key > mx ? key : mx;
+            atomicAdd(&hist[digit<K>(key, est, shift0, H0_BINS)], 1u);
+            ci[pos] = (uint32_t)(base + off);
+            cv[pos] = val;
+            ++pos;
         }
-        // candidate mask over this thread's 16 contiguous elements (bit b <-> element 16*tid+b)
-        unsigned M = 0;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const float4 v = y[r];
-            double& sr = (r & 1) ? ss1 : ss;  // two chains: half the DFMA dependency depth
-            sr = fma((double)v.x, (double)v.x, sr);
-            sr = fma((double)v.y, (double)v.y, sr);
-            sr = fma((double)v.z, (double)v.z, sr);
-            sr = fma((double)v.w, (double)v.w, sr);
-            const unsigned m4 = (fabsf(v.x) >= thr ? 1u : 0u) | (fabsf(v.y) >= thr ? 2u : 0u) |
-                                (fabsf(v.z) >= thr ? 4u : 0u) | (fabsf(v.w) >= thr ? 8u : 0u);
-            M |= m4 << (((r + rot) & 3) * 4);
-        }
-        if (take_all) M = 0xffffu;  // fallback pass: every element (NaN included) is a candidate
-        if (!full_tile) {
-            const long long left = a.dim - base - tid * 16;
-            M &= left >= 16 ? 0xffffu : (left <= 0 ? 0u : ((1u << left) - 1u));
-        }
-        // ordered placement: warp scan of the per-thread counts, block offsets via smem
+    };
+    auto scan_and_place = [&](unsigned M, long long base, long long tile, const float* src) {
         const unsigned n = __popc(M);
         unsigned incl = n;
 #pragma unroll
@@ -670,41 +648,61 @@ k_main_tma(MainArgs<float> a) {
             woff += j < warp ? t : 0u;
             total += t;
         }
-        // the warp's candidates are processed cooperatively: lane k takes the warp's k-th one
-        const unsigned wtot = __shfl_sync(FULL, incl, 31);
-        for (unsigned k0 = 0; k0 < wtot; k0 += 32) {
-            const unsigned k = k0 + lane;
-            int o = 0;  // owner lane: first lane with incl > k
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const unsigned t = __shfl_sync(FULL, incl, o + step - 1);
-                if (t <= k) o += step;
-            }
-            const unsigned Mo = __shfl_sync(FULL, M, o);
-            const unsigned eo = __shfl_sync(FULL, incl - n, o);
-            if (k < wtot) {
-                const int bit = (int)__fns(Mo, 0, (int)(k - eo) + 1);
-                const int off = (warp * 32 + o) * 16 + bit;
-                const float val = full_tile ? tb[off] : row[base + off];
-                const K key = KeyOf<float>::key(val);
-                mx = key > mx ? key : mx;
-                atomicAdd(&hist[digit<K>(key, est, shift0, H0_BINS)], 1u);
-                const unsigned pos = run + woff + k;
-                ci[pos] = (uint32_t)(base + off);
-                cv[pos] = val;
-            }
-        }
+        if (M) place(M, base, src, n, incl, woff);
         if (tid == 0) {
             const long long ti = (long long)w * a.ntiles + tile;
             a.cnt[ti] = total;
             a.tstart[ti] = run;
         }
         run += total;
+    };
+    for (int i = 0; i < nfull; ++i) {
+        const long long tile = t_begin + i;
+        const long long base = tile * MN_TILE;
+        const int s = i % MN_STAGES;
+        const float* tb = ring + s * MN_TILE;
+        mbar_wait(&full[s], (unsigned)(i / MN_STAGES) & 1u);
+        const float4* t4 = reinterpret_cast<const float4*>(tb);
+        float4 y[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) y[r] = t4[tid * 4 + ((r + rot) & 3)];
+        // candidate mask over this thread's 16 contiguous elements (bit b <-> element 16*tid+b)
+        unsigned M = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const float4 v = y[r];
+            double& sr = (r & 1) ? ss1 : ss;  // two chains: half the DFMA dependency depth
+            sr = fma((double)v.x, (double)v.x, sr);
+            sr = fma((double)v.y, (double)v.y, sr);
+            sr = fma((double)v.z, (double)v.z, sr);
+            sr = fma((double)v.w, (double)v.w, sr);
+            const unsigned m4 = (fabsf(v.x) >= thr ? 1u : 0u) | (fabsf(v.y) >= thr ? 2u : 0u) |
+                                (fabsf(v.z) >= thr ? 4u : 0u) | (fabsf(v.w) >= thr ? 8u : 0u);
+            M |= m4 << (((r + rot) & 3) * 4);
+        }
+        if (take_all) M = 0xffffu;  // fallback pass: every element (NaN included) is a candidate
+        scan_and_place(M, base, tile, tb);
         __syncthreads();  // stage s fully consumed (and s_wtot free) before it is refilled
         if (tid == 0 && i + MN_STAGES < ntl) {
             fence_proxy_async();
             issue(i + MN_STAGES);
         }
+    }
+    if (nfull < ntl) {  // partial last tile of the row: direct loads, bounds-checked
+        const long long tile = t_begin + nfull;
+        const long long base = tile * MN_TILE;
+        const long long left = a.dim - base - tid * 16;
+        const float* src = row + base;
+        unsigned M = 0;
+        for (int b = 0; b < 16; ++b) {
+            if (b >= left) break;
+            const float x = src[tid * 16 + b];
+            double& sr = (b & 1) ? ss1 : ss;
+            sr = fma((double)x, (double)x, sr);
+            if (take_all || fabsf(x) >= thr) M |= 1u << b;
+        }
+        scan_and_place(M, base, tile, src);
+        __syncthreads();
     }
     main_finish<float>(a, w, seg, dadd(ss, ss1), mx, run, hist, est, shift0);
 }
@@ -885,28 +883,33 @@ k_collect(CollectArgs<T> a) {
         __syncthreads();
     };
     unsigned gt = 0;
-    for (long long i0 = i_lo; i0 < i_hi; i0 += CU * TK_THREADS) {
+    const int lo32 = (int)i_lo, hi32 = (int)i_hi;
+    const K span_hi = span;
+    for (int i0 = lo32; i0 < hi32; i0 += CU * TK_THREADS) {
         T v[CU];
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
-            const long long i = i0 + u * TK_THREADS + tid;
-            v[u] = i < i_hi ? cv[i] : (T)0;
+            const int i = i0 + u * TK_THREADS + tid;
+            v[u] = i < hi32 ? cv[i] : (T)0;
         }
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
-            const long long i = i0 + u * TK_THREADS + tid;
-            if (i >= i_hi) continue;
+            const int i = i0 + u * TK_THREADS + tid;
             const K key = KO::key(v[u]);
-            gt += key >= lo && key - lo > span;
-            if (key >= lo && key - lo <= span) {
+            const K d = key - lo;  // wraps for key < lo: then d > span_hi, but key < lo is not "above"
+            const bool ok = i < hi32 && key >= lo;
+            gt += ok && d > span_hi;
+            if (ok && d <= span_hi) {
                 const unsigned q = atomicAdd(&s_n, 1u);
                 st_key[q] = key;
                 st_idx[q] = ci[i];
                 st_pos[q] = (uint32_t)i;
             }
         }
+        // every thread must see the same s_n before anyone appends again: the barrier
+        // inside __syncthreads_or orders all reads before the next iteration's atomics
         __syncthreads();
-        if (s_n > CSTAGE - CU * TK_THREADS) flush();
+        if (__syncthreads_or(s_n > CSTAGE - CU * TK_THREADS)) flush();
     }
     flush();
     for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(FULL, gt, o);
@@ -1196,109 +1199,117 @@ k_write(WriteArgs<T> a) {
         gb = s_gb;
         eb = s_eb;
     }
-    __syncthreads();
     uint32_t* oi = a.idx + (long long)w * a.m;
     T* ov = a.val + (long long)w * a.m;
     double ss = 0.0;
     __shared__ unsigned s_kb[WR_CHUNK];  // kept-before count per entry of the chunk (merge offsets)
-    for (long long c0 = i_lo; c0 < n; c0 += WR_CHUNK) {
-        unsigned kflag = 0, eflag = 0;
+    __shared__ int s_jc;
+    // 32-bit bookkeeping: segment positions < 2^31, output positions < m < 2^31
+    const int lo32 = (int)i_lo, n32 = (int)n;
+    unsigned g32 = (unsigned)gb, e32 = (unsigned)eb;
+    const unsigned need32 = (unsigned)(need < 0xffffffffull ? need : 0xffffffffull);
+    __syncthreads();  // s_ts complete (fast mode has no barrier above)
+    if (toff && tid == 0) {  // first tile of this segment whose first candidate is >= i_lo
+        int l = 0, h = nt;
+        while (l < h) {
+            const int mid = (l + h) >> 1;
+            if ((int)s_ts[mid] < lo32) l = mid + 1;
+            else h = mid;
+        }
+        s_jc = l;
+    }
+    __syncthreads();
+    int jc = toff ? s_jc : 0;
+    for (int c0 = lo32; c0 < n32; c0 += WR_CHUNK) {
+        const int c1 = c0 + WR_CHUNK < n32 ? c0 + WR_CHUNK : n32;
+        const int e0i = c0 + tid * WR_EPT;
         T vv[WR_EPT];
         uint32_t ii[WR_EPT];
-        const long long e0i = c0 + tid * WR_EPT;
-        if constexpr (sizeof(T) == 4) {
-            if (e0i + WR_EPT <= n) {  // segment base and chunk start are 16-byte aligned
+        if (sizeof(T) == 4 && e0i + WR_EPT <= n32) {  // segment base and chunk start are 16-byte aligned
+            if constexpr (sizeof(T) == 4) {
                 const float4 v4 = *reinterpret_cast<const float4*>(cv + e0i);
                 const uint4 i4 = *reinterpret_cast<const uint4*>(ci + e0i);
                 vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
                 ii[0] = i4.x; ii[1] = i4.y; ii[2] = i4.z; ii[3] = i4.w;
-            } else {
-#pragma unroll
-                for (int u = 0; u < WR_EPT; ++u) {
-                    vv[u] = e0i + u < n ? cv[e0i + u] : (T)0;
-                    ii[u] = e0i + u < n ? ci[e0i + u] : 0u;
-                }
             }
         } else {
 #pragma unroll
             for (int u = 0; u < WR_EPT; ++u) {
-                vv[u] = e0i + u < n ? cv[e0i + u] : (T)0;
-                ii[u] = e0i + u < n ? ci[e0i + u] : 0u;
+                const bool ok = e0i + u < n32;
+                vv[u] = ok ? cv[e0i + u] : (T)0;
+                ii[u] = ok ? ci[e0i + u] : 0u;
             }
         }
+        unsigned kflag = 0, eflag = 0;
 #pragma unroll
         for (int u = 0; u < WR_EPT; ++u) {
-            if (e0i + u < n) {
-                const K key = KO::key(vv[u]);
-                if (!slow) {
-                    kflag |= (key > T_ || (key == T_ && ii[u] <= cut) ? 1u : 0u) << u;
-                } else {
-                    kflag |= (key > T_ ? 1u : 0u) << u;
-                    eflag |= (key == T_ ? 1u : 0u) << u;
-                }
+            const K key = KO::key(vv[u]);
+            const bool ok = e0i + u < n32;
+            if (!slow) {
+                kflag |= (ok && (key > T_ || (key == T_ && ii[u] <= cut)) ? 1u : 0u) << u;
+            } else {
+                kflag |= (ok && key > T_ ? 1u : 0u) << u;
+                eflag |= (ok && key == T_ ? 1u : 0u) << u;
             }
         }
-        unsigned gx, gt_, ex = 0, et_ = 0;
-        warp_scan_small(__popc(kflag), gx, gt_);
-        if (slow) warp_scan_small(__popc(eflag), ex, et_);
-        if (lane == 0) {
-            s_gw[warp] = gt_;
-            s_ew[warp] = et_;
+        // warp-inclusive scans of the per-thread counts (packed: kept in the low half,
+        // ties at T in the high half; both <= 4 * 32)
+        const unsigned cnt = __popc(kflag) | ((unsigned)__popc(eflag) << 16);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
         }
+        if (lane == 31) s_gw[warp] = incl;
         __syncthreads();
-        unsigned long long g0 = gb, e0 = eb, gsum = 0, esum = 0;
+        unsigned wb = 0, tot = 0;
+#pragma unroll
         for (int i = 0; i < TK_NW; ++i) {
-            if (i < warp) {
-                g0 += s_gw[i];
-                e0 += s_ew[i];
-            }
-            gsum += s_gw[i];
-            esum += s_ew[i];
+            const unsigned t = s_gw[i];
+            wb += i < warp ? t : 0u;
+            tot += t;
         }
-        g0 += gx;
-        e0 += ex;
+        const unsigned ex = wb + incl - cnt;
+        unsigned gpos = g32 + (ex & 0xffffu), epos = e32 + (ex >> 16);
 #pragma unroll
         for (int u = 0; u < WR_EPT; ++u) {
-            const long long e = e0i + u;
-            if (e >= n) break;
-            const unsigned long long kb4 = slow ? g0 + (e0 < need ? e0 : need) : g0;
-            if (toff) s_kb[tid * WR_EPT + u] = (unsigned)kb4;
             const bool isk = (kflag >> u) & 1u, ise = (eflag >> u) & 1u;
-            bool keep = false;
-            unsigned long long pos = 0;
-            if (isk) {
+            const unsigned kb4 = slow ? gpos + (epos < need32 ? epos : need32) : gpos;
+            if (toff) s_kb[tid * WR_EPT + u] = kb4;
+            bool keep = isk;
+            unsigned pos = kb4;
+            if (slow && ise && epos < need32) {
                 keep = true;
-                pos = kb4;
-            } else if (ise && e0 < need) {
-                keep = true;
-                pos = g0 + e0;
+                pos = gpos + epos;
             }
-            if (keep && pos < (unsigned long long)a.m) {
+            if (keep && pos < (unsigned)a.m) {
                 oi[pos] = ii[u];
                 ov[pos] = vv[u];
                 ss = fma((double)vv[u], (double)vv[u], ss);
             }
-            g0 += isk;
-            e0 += ise;
+            gpos += isk;
+            epos += ise;
         }
-        gb += gsum;
-        eb += esum;
-        __syncthreads();
+        g32 += tot & 0xffffu;
+        e32 += tot >> 16;
+        __syncthreads();  // s_gw reuse; s_kb complete
         if (toff) {
             // tiles whose first candidate lies in this chunk: merge offset = kept before it
-            const long long c1 = c0 + WR_CHUNK < n ? c0 + WR_CHUNK : n;
-            for (int j = tid; j < nt; j += TK_THREADS) {
-                const long long t = s_ts[j];
-                if (t >= c0 && t < c1) toff[t0 + j] = (int)s_kb[t - c0];
+            for (;;) {
+                const int j = jc + tid;
+                const bool in = j < nt && (int)s_ts[j] < c1;
+                if (in) toff[t0 + j] = (int)s_kb[s_ts[j] - c0];
+                const int c = __syncthreads_count(in);
+                jc += c;
+                if (c < TK_THREADS) break;
             }
-            __syncthreads();
         }
     }
     if (toff && last_part) {
         // tiles with no candidate at or after the segment's last entry: offset = kept total
-        const unsigned long long kept = slow ? gb + (eb < need ? eb : need) : gb;
-        for (int j = tid; j < nt; j += TK_THREADS)
-            if ((long long)s_ts[j] >= n) toff[t0 + j] = (int)kept;
+        const unsigned kept = slow ? g32 + (e32 < need32 ? e32 : need32) : g32;
+        for (int j = jc + tid; j < nt; j += TK_THREADS) toff[t0 + j] = (int)kept;
         if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }
     ss = warp_sum(ss);
@@ -1338,6 +1349,20 @@ k_write(WriteArgs<T> a) {
             }
         }
     }
+}
+
+// Diagnostics of the last sg_topk_gate call on this workspace, per worker:
+// {candidates, boundary entries, fallback pass taken, oversized-tie (slow) write mode}.
+template <typename T>
+__global__ void k_topk_stats(const SelState<typename KeyOf<T>::K>* sel, const unsigned long long* count,
+                             const unsigned long long* bndn, int k, long long* out) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= k) return;
+    const bool fb = sel[w].mode == MODE_FALLBACK;
+    out[4 * w] = (long long)(fb ? count[k + w] : count[w]);
+    out[4 * w + 1] = (long long)bndn[w];
+    out[4 * w + 2] = fb;
+    out[4 * w + 3] = sel[w].wmode == WR_SLOW;
 }
 
 __global__ void k_gate_update(const double* norms2, int k, sg_gate_state* states, uint8_t* decision,
@@ -1429,6 +1454,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     k_estimate<T><<<k, EST_THREADS, est_smem, stream>>>(g, ld, dim, p.s_eff, p.r_est, sel,
                                                          reinterpret_cast<uint4*>(base),
                                                          (long long)(p.zero_end / 16));
+    debug_sync("k_estimate", stream);
     // 2. main streaming pass, then the (normally empty) fallback pass
     MainArgs<T> ma;
     ma.g = g;
@@ -1466,10 +1492,12 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
         k_main<T><<<sgrid, TK_THREADS, 0, stream>>>(ma);
     };
     launch_main();
+    debug_sync("k_main", stream);
     ma.pass = 1;
     ma.hist0 = hist0fb;
     ma.done = c_fb;
     launch_main();
+    debug_sync("k_main(fb)", stream);
     // 3. per-segment counts + boundary, in-CTA resolve
     CollectArgs<T> ca;
     ca.segcap = p.segcap;
@@ -1491,9 +1519,11 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ca.done = c_col;
     const dim3 subgrid((unsigned)p.nsub, (unsigned)k);
     k_collect<T><<<subgrid, TK_THREADS, 0, stream>>>(ca);
+    debug_sync("k_collect", stream);
     const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES + sizeof(unsigned) * NSUB_MAX;
     cudaFuncSetAttribute(k_resolve_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem);
     k_resolve_small<T><<<k, 1024, res_smem, stream>>>(ca);
+    debug_sync("k_resolve_small", stream);
     // 4. slow mode only: multi-CTA select rounds over an oversized boundary
     ResolveArgs<T> ra;
     ra.cap = capw;
@@ -1505,6 +1535,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     const unsigned rper = (unsigned)((sms * 2 + k - 1) / k);
     for (int r = 0; r < TopkTraits<T>::ROUNDS_MAX; ++r)
         k_resolve<T><<<dim3(rper, (unsigned)k), 256, 0, stream>>>(ra, r);
+    debug_sync("k_resolve", stream);
     // 5. ordered write + norms + gate
     WriteArgs<T> wa;
     wa.ntiles = p.ntiles;
@@ -1534,6 +1565,21 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.rho = rho;
     const size_t wr_smem = sizeof(unsigned) * (size_t)p.tps;
     k_write<T><<<subgrid, TK_THREADS, wr_smem, stream>>>(wa);
+    debug_sync("k_write", stream);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+template <typename T>
+int topk_stats(int k, long long dim, long long m, const void* ws, size_t ws_bytes, int64_t* out, cudaStream_t stream) {
+    using K = typename KeyOf<T>::K;
+    if (!ws || !out || k < 1 || dim < 1 || m < 1 || m > dim) return SG_ERR_INVALID;
+    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k));
+    if (ws_bytes < p.total) return SG_ERR_WORKSPACE;
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    k_topk_stats<T><<<1, 64, 0, stream>>>(reinterpret_cast<const SelState<K>*>(base + p.off_sel),
+                                          reinterpret_cast<const unsigned long long*>(base + p.off_count),
+                                          reinterpret_cast<const unsigned long long*>(base + p.off_bndn), k,
+                                          reinterpret_cast<long long*>(out));
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
@@ -1564,6 +1610,15 @@ int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m,
                      double* rho, void* workspace, size_t workspace_bytes, void* stream) {
     return topk_gate<double>(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, nullptr,
                              workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int sg_topk_stats_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes, int64_t* out,
+                      void* stream) {
+    return topk_stats<float>(k, dim, m, workspace, workspace_bytes, out, (cudaStream_t)stream);
+}
+int sg_topk_stats_f64(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes, int64_t* out,
+                      void* stream) {
+    return topk_stats<double>(k, dim, m, workspace, workspace_bytes, out, (cudaStream_t)stream);
 }
 
 int sg_gate_update(const double* norms2, int k, sg_gate_state* states, uint8_t* decision,

@@ -129,6 +129,16 @@ def topk_gate(
     return idx, val, norms2, decision, rho
 
 
+def topk_stats(dtype: torch.dtype, k: int, dim: int, m: int, device: torch.device) -> np.ndarray:
+    """Per-worker {candidates, boundary, fallback, slow} of the last topk_gate call (synchronises)."""
+    ws = Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device)
+    out = torch.zeros((k, 4), dtype=torch.int64, device=device)
+    lib = _capi.load()
+    fn = lib.sg_topk_stats_f32 if dtype == torch.float32 else lib.sg_topk_stats_f64
+    _capi.check(fn(k, dim, m, ws.data_ptr(), ws.numel(), out.data_ptr(), _stream()), "sg_topk_stats")
+    return out.cpu().numpy()
+
+
 def gate_update(norms2: torch.Tensor, states: torch.Tensor):
     require_cuda(norms2)
     k = norms2.shape[0]

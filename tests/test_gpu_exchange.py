@@ -92,3 +92,22 @@ def test_step_at_resnet152_size_properties(cuda):
     total = float(ex.aggregate.double().sum())
     want_total = sum(w[j] * float(ex.val[j].double().sum()) for j in range(W))
     assert abs(total - want_total) <= 1e-6 * sum(w[j] * float(ex.val[j].double().abs().sum()) for j in range(W))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multi_gpu_exchange_matches_single_gpu(cuda):
+    """torchrun over all visible GPUs (NCCL): sparse all-gather path bit-identical to one GPU,
+    dense all-reduce path within fp32 tolerance, replicas identical on every rank."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    n = 4 if torch.cuda.device_count() >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", str(ROOT / "tools" / "multi_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert rep["ok"] and rep["world"] == n

@@ -34,7 +34,9 @@ def main():
     for _ in range(args.steps):
         info = ex.step(w, 0.01)
     torch.cuda.synchronize()
-    print(info.path, ex.decision.cpu().tolist())
+    from paper_2301_08897_b200 import kernels
+    st = kernels.topk_stats(torch.float32, ex.k, ex.dim, ex.m, dev)
+    print(info.path, ex.decision.cpu().tolist(), "m", ex.m, "stats[C, boundary, fb, slow]", st.tolist())
 
 
 if __name__ == "__main__":
