@@ -141,7 +141,7 @@ template <typename TI, typename TO> struct AggArgs {
     long long ld, dim, ntiles;
     double lr, mu, wd;
     int nw, first, vec_ok;
-    int pipe;  // k_merge_pipe owns all-sparse calls: k_merge then exits
+    int pipe;  // k_merge_ws owns all-sparse calls: k_merge then exits
 };
 
 template <typename TI, typename TO>
@@ -590,38 +590,63 @@ k_merge(const AggArgs<float, TO> a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// k_merge_pipe: persistent, software-pipelined merge + fused momentum SGD for the case the
-// hot path produces (every worker sparse, float32).  2 CTAs per SM; CTA b owns the
-// contiguous tile range [b*tpb, (b+1)*tpb) and loads its slice of the per-worker tile
-// offsets once.  While tile i is merged, tile i+1's p/buf are already in flight into
-// registers and its sparse entries into the other half of a double-buffered shared staging
-// area (cp.async / LDGSTS).  Per tile: atomicOr records which workers keep each position;
-// single-contributor positions take +0 + w*v directly, collided ones are folded in
-// ascending worker order by their lowest worker (the reference's fold), untouched
-// positions get the g = +0 update; each thread then applies momentum SGD to its 8
-// contiguous positions from registers and stores them with 128-bit stores.
+// k_merge_ws: persistent, warp-specialised merge + fused momentum SGD for the case the hot
+// path produces (every worker sparse, float32, <= 16 workers).  One CTA per SM owns the
+// contiguous tile range [b*tpb, (b+1)*tpb); a tile's entries (worker-major, ascending index
+// inside a worker) are processed in chunks of <= MW_ECAP entries (one unless oversized).
+//   producer warps (12): warp w stages worker w's run (w < nw) of the next chunk with
+//     cp.async (LDGSTS) while, for the current chunk, (1) each entry is pushed onto its
+//     position's list, head[q] <- atomicExch(head[q], node), node = {value, worker, next};
+//     (2) each list's head entry folds the list in ascending worker order -- the reference's
+//     fold (comm.py:70-78): +0 (or the previous chunk's partial), then + w_j * v_j -- into
+//     the tile's float64 value slot and marks the position.  A named-barrier arrive hands
+//     the tile (values + byte marks, double-buffered) to the consumers.
+//   consumer warps (16): p/buf tiles arrive by TMA bulk copies (cp.async.bulk, mbarrier
+//     completion, L2 evict-first) into a 3-stage shared ring; thread t owns positions
+//     {4t..4t+3} and {2048+4t..+3}: g = marked ? value : +0, momentum SGD (nn.py:167-171
+//     order, binary64), 128-bit global stores; marks are cleared and the hand-off buffer
+//     and ring stage released.
+// The streaming SGD never waits on a CTA-wide barrier.
 // ---------------------------------------------------------------------------------------
-constexpr int MP_ECAP = 2048;
+constexpr int MW_CONS = 512;
+constexpr int MW_PROD = 384;
+constexpr int MW_PW = MW_PROD / 32;
+constexpr int MW_THREADS = MW_CONS + MW_PROD;
+constexpr int MW_ECAP = 1024;
+constexpr int MW_STAGES = 3;
+constexpr int MW_SLOTS = 3;  // entry staging: two chunks in flight ahead of the one processed
+constexpr int MW_HALF = AG_TILE / 2;
+constexpr unsigned MW_NIL = 0xffffu;
+enum { BAR_FULL = 1, BAR_EMPTY = 3, BAR_PROD = 5, BAR_CONS = 6 };
 
-inline size_t mp_smem_bytes(int tpb) {
-    return (size_t)AG_TILE * sizeof(double) + 2 * MP_ECAP * (sizeof(uint32_t) + sizeof(float) + 1) +
-           AG_TILE * sizeof(unsigned) + (size_t)MP_MAXW * (tpb + 1) * sizeof(int);
+inline size_t mw_smem_bytes(int tpb) {
+    return (size_t)MW_STAGES * 2 * AG_TILE * sizeof(float)             // p/buf ring [S][2][TILE]
+           + 2 * AG_TILE * sizeof(double)                                // values [2][TILE]
+           + (size_t)AG_TILE * sizeof(unsigned)                          // heads [TILE]
+           + (size_t)MW_ECAP * sizeof(uint2)                             // nodes [ECAP]
+           + MW_SLOTS * (size_t)MW_ECAP * (sizeof(uint32_t) + sizeof(float) + 1)  // staging [3][ECAP]
+           + 2 * AG_TILE                                                 // marks [2][TILE]
+           + (size_t)MP_MAXW * (tpb + 1) * sizeof(int);                  // offsets slice
 }
 
 template <typename TO>
-__global__ void __launch_bounds__(MG_THREADS, 2)
-k_merge_pipe(const AggArgs<float, TO> a, int tpb) {
-    extern __shared__ __align__(128) unsigned char mp_smem[];
-    double* acc_s = reinterpret_cast<double*>(mp_smem);                  // [TILE]
-    uint32_t* eidx = reinterpret_cast<uint32_t*>(acc_s + AG_TILE);       // [2][ECAP]
-    float* evl = reinterpret_cast<float*>(eidx + 2 * MP_ECAP);           // [2][ECAP]
-    unsigned* who = reinterpret_cast<unsigned*>(evl + 2 * MP_ECAP);      // [TILE]
-    uint8_t* ewk = reinterpret_cast<uint8_t*>(who + AG_TILE);            // [2][ECAP] worker ids
-    int* soff = reinterpret_cast<int*>(ewk + 2 * MP_ECAP);               // [nw][tpb + 1]
-    __shared__ int s_pre[3][MP_MAXW + 1];
+__global__ void __launch_bounds__(MW_THREADS, 1)
+k_merge_ws(const AggArgs<float, TO> a, int tpb) {
+    extern __shared__ __align__(128) unsigned char mw_smem[];
+    float* ring = reinterpret_cast<float*>(mw_smem);                     // [S][2][TILE]
+    double* acc = reinterpret_cast<double*>(ring + MW_STAGES * 2 * AG_TILE);  // [2][TILE]
+    uint2* node = reinterpret_cast<uint2*>(acc + 2 * AG_TILE);           // [ECAP]
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(node + MW_ECAP);        // [SLOTS][ECAP]
+    float* sval = reinterpret_cast<float*>(sidx + MW_SLOTS * MW_ECAP);   // [SLOTS][ECAP]
+    unsigned* head = reinterpret_cast<unsigned*>(sval + MW_SLOTS * MW_ECAP);  // [TILE]
+    uint8_t* mark = reinterpret_cast<uint8_t*>(head + AG_TILE);          // [2][TILE]
+    uint8_t* swk = mark + 2 * AG_TILE;                                   // [SLOTS][ECAP] worker ids
+    int* soff = reinterpret_cast<int*>(swk + MW_SLOTS * MW_ECAP);        // [nw][tpb + 1]
+    __shared__ int4 s_hdr[MW_SLOTS];  // staged chunk: {tile, c0, entries, last}
+    __shared__ __align__(8) unsigned long long fullb[MW_STAGES];
     __shared__ long long s_rp[MP_MAXW];
     __shared__ int s_ok;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int nw = a.nw;
     if (tid == 0) {
         int ok = nw <= MP_MAXW;
@@ -633,202 +658,206 @@ k_merge_pipe(const AggArgs<float, TO> a, int tpb) {
     const long long t_begin = (long long)blockIdx.x * tpb;
     if (t_begin >= a.ntiles) return;
     const int nt = (int)(a.ntiles - t_begin < tpb ? a.ntiles - t_begin : tpb);
-    for (int q = tid; q < nw * (nt + 1); q += MG_THREADS) {
+    const int sw = tpb + 1;
+    // ring stage s <- p/buf of tile i (full tiles only; a partial last tile is read directly)
+    unsigned long long policy = 0;
+    auto issue = [&](int i) {
+        const long long tb = (t_begin + i) * AG_TILE;
+        if (tb + AG_TILE > a.dim) return;
+        const int s = i % MW_STAGES;
+        mbar_expect_tx(&fullb[s], 2 * AG_TILE * sizeof(float));
+        bulk_g2s(ring + (s * 2) * AG_TILE, a.p + tb, AG_TILE * sizeof(float), &fullb[s], policy);
+        bulk_g2s(ring + (s * 2 + 1) * AG_TILE, a.buf + tb, AG_TILE * sizeof(float), &fullb[s], policy);
+    };
+    if (tid == 0) {
+        policy = policy_evict_first();
+        for (int s = 0; s < MW_STAGES; ++s) mbar_init(&fullb[s], 1);
+        fence_mbar_init();
+        for (int i = 0; i < MW_STAGES && i < nt; ++i) issue(i);
+    }
+    for (int q = tid; q < nw * (nt + 1); q += MW_THREADS) {
         const int j = q / (nt + 1), i = q - j * (nt + 1);
-        soff[j * (tpb + 1) + i] = a.off[(long long)j * (a.ntiles + 1) + t_begin + i];
+        soff[j * sw + i] = a.off[(long long)j * (a.ntiles + 1) + t_begin + i];
     }
-    for (int q = tid; q < AG_TILE; q += MG_THREADS) who[q] = 0;
+    for (int q = tid; q < AG_TILE; q += MW_THREADS) head[q] = MW_NIL;
+    for (int q = tid; q < 2 * AG_TILE / 4; q += MW_THREADS) reinterpret_cast<unsigned*>(mark)[q] = 0u;
     if (tid < nw) s_rp[tid] = a.row_ptr[tid];
-    const bool first = a.first != 0;
-    const int q0 = tid * MG_PER;
-    auto entry_prefix = [&](int i) {  // warp 0: exclusive prefix of tile i's per-worker counts
-        int c = 0;
-        if (lane < nw) c = soff[lane * (tpb + 1) + i + 1] - soff[lane * (tpb + 1) + i];
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane < nw) s_pre[i % 3][lane] = incl - c;
-        if (lane == 31) s_pre[i % 3][nw] = incl;
-    };
-    auto worker_of = [&](const int* pre, int e) {
-        int lo = 0, hi = nw;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (pre[mid] <= e) lo = mid;
-            else hi = mid;
-        }
-        return lo;
-    };
-    auto stage = [&](int i, int c0, int c1) {  // all threads: entries [c0, c1) of tile i, async
-        const int* pre = s_pre[i % 3];
-        const int slot = i & 1;
-        for (int e = c0 + tid; e < c1; e += MG_THREADS) {
-            const int j = worker_of(pre, e);
-            const long long gi = s_rp[j] + soff[j * (tpb + 1) + i] + (e - pre[j]);
-            cp_async4(eidx + slot * MP_ECAP + (e - c0), a.idx + gi);
-            cp_async4(evl + slot * MP_ECAP + (e - c0), a.val + gi);
-            ewk[slot * MP_ECAP + (e - c0)] = (uint8_t)j;
-        }
-        cp_async_commit();
-    };
-    auto load_pb = [&](int i, float (&pv)[MG_PER], float (&bv)[MG_PER]) {
-        const long long tb = (t_begin + i) * AG_TILE;
-        if (tb + AG_TILE <= a.dim) {
-            const float4* pp = reinterpret_cast<const float4*>(a.p + tb + q0);
-            const float4* bp = reinterpret_cast<const float4*>(a.buf + tb + q0);
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const float4 u = pp[r], z = bp[r];
-                pv[4 * r] = u.x; pv[4 * r + 1] = u.y; pv[4 * r + 2] = u.z; pv[4 * r + 3] = u.w;
-                bv[4 * r] = z.x; bv[4 * r + 1] = z.y; bv[4 * r + 2] = z.z; bv[4 * r + 3] = z.w;
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < MG_PER; ++c) {
-                const bool ok = tb + q0 + c < a.dim;
-                pv[c] = ok ? a.p[tb + q0 + c] : 0.f;
-                bv[c] = ok ? a.buf[tb + q0 + c] : 0.f;
-            }
-        }
-    };
-    __syncthreads();  // soff, who ready
-    if (warp == 0) {
-        entry_prefix(0);
-        if (nt > 1) entry_prefix(1);
-    }
     __syncthreads();
-    {
-        const int E0 = s_pre[0][nw];
-        stage(0, 0, E0 < MP_ECAP ? E0 : MP_ECAP);
-    }
-    float pv[MG_PER], bv[MG_PER];
-    load_pb(0, pv, bv);
-    for (int i = 0; i < nt; ++i) {
-        const long long tb = (t_begin + i) * AG_TILE;
-        const int slot = i & 1;
-        const int* pre = s_pre[i % 3];
-        const int E = pre[nw];
-        // prefetch tile i+1: entries (async) and p/buf (registers); prefix of tile i+2
-        float pn[MG_PER], bn[MG_PER];
-        if (i + 1 < nt) {
-            const int E1 = s_pre[(i + 1) % 3][nw];
-            stage(i + 1, 0, E1 < MP_ECAP ? E1 : MP_ECAP);
-            load_pb(i + 1, pn, bn);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        if (warp == 0 && i + 2 < nt) entry_prefix(i + 2);
-        __syncthreads();  // S1: tile i's entries landed; who clear
-        const uint32_t* ei = eidx + slot * MP_ECAP;
-        const float* ev = evl + slot * MP_ECAP;
-        const uint8_t* ew = ewk + slot * MP_ECAP;
-        for (int c0 = 0; c0 < E; c0 += MP_ECAP) {
-            const int c1 = E - c0 < MP_ECAP ? E : c0 + MP_ECAP;
-            if (c0 > 0) {  // oversized tile (rare): synchronous restage of the next chunk
-                __syncthreads();
-                stage(i, c0, c1);
-                cp_async_wait<0>();
-                __syncthreads();
+
+    if (tid >= MW_CONS) {
+        // ------------------------------- producers -------------------------------
+        const int pt = tid - MW_CONS, lane = pt & 31, pw = pt >> 5;
+        // per-warp view of tile i: lane j < nw holds worker j's entry count and start
+        auto tile_runs = [&](int i, int& cnt, int& pre, int& tot) {
+            cnt = lane < nw ? soff[lane * sw + i + 1] - soff[lane * sw + i] : 0;
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
             }
-            for (int e = c0 + tid; e < c1; e += MG_THREADS)
-                atomicOr(&who[ei[e - c0] - (uint32_t)tb], 1u << ew[e - c0]);
-        }
-        __syncthreads();  // S2: contributor masks complete
-        for (int c0 = 0; c0 < E; c0 += MP_ECAP) {
-            const int c1 = E - c0 < MP_ECAP ? E : c0 + MP_ECAP;
-            if (c0 > 0) {
-                __syncthreads();
-                stage(i, c0, c1);
-                cp_async_wait<0>();
-                __syncthreads();
-            } else if (E > MP_ECAP) {  // chunk 0 was overwritten by the pass above: restage it
-                __syncthreads();
-                stage(i, 0, MP_ECAP);
-                cp_async_wait<0>();
-                __syncthreads();
-            }
-            for (int e = c0 + tid; e < c1; e += MG_THREADS) {
-                const int j = ew[e - c0];
-                const int q = (int)(ei[e - c0] - (uint32_t)tb);
-                const unsigned m = who[q];
-                double r;
-                if ((m & (m - 1)) == 0) {
-                    r = dadd(0.0, dmul(a.w[j], (double)ev[e - c0]));
-                } else {
-                    if (__ffs(m) - 1 != j) continue;  // the lowest contributor folds the position
-                    r = 0.0;
-                    const uint32_t want = (uint32_t)tb + (uint32_t)q;
-                    for (unsigned mm = m; mm; mm &= mm - 1) {
-                        const int jj = __ffs(mm) - 1;
-                        double v;
-                        if (jj == j) {
-                            v = ev[e - c0];
-                        } else if (pre[jj] >= c0 && pre[jj + 1] <= c1) {
-                            // worker jj's entry at this index, in the staged (ascending) list
-                            int l = pre[jj] - c0, h = pre[jj + 1] - c0;
-                            while (l < h) {
-                                const int mid = (l + h) >> 1;
-                                if (ei[mid] < want) l = mid + 1;
-                                else h = mid;
-                            }
-                            v = ev[l];
-                        } else {  // oversized tile: that worker is outside this chunk
-                            const long long base = s_rp[jj] + soff[jj * (tpb + 1) + i];
-                            int l = 0, h = pre[jj + 1] - pre[jj];
-                            while (l < h) {
-                                const int mid = (l + h) >> 1;
-                                if (a.idx[base + mid] < want) l = mid + 1;
-                                else h = mid;
-                            }
-                            v = a.val[base + l];
-                        }
-                        r = dadd(r, dmul(a.w[jj], v));
+            pre = incl - cnt;
+            tot = __shfl_sync(FULL, incl, 31);
+        };
+        // Staging cursor: the next chunk to stage is entries [c0, min(E, c0 + ECAP)) of tile
+        // ci (cnt/pre: the tile's per-worker runs); ci == nt marks the end.
+        int ci = 0, cc0 = 0, cE, ccnt, cpre;
+        tile_runs(0, ccnt, cpre, cE);
+        auto stage_next = [&](int slot) {  // stage the cursor's chunk into slot (async), advance
+            if (ci < nt) {
+                const int c1 = cE - cc0 < MW_ECAP ? cE : cc0 + MW_ECAP;
+                for (int j = pw; j < nw; j += MW_PW) {
+                    const int pj = __shfl_sync(FULL, cpre, j), nj = __shfl_sync(FULL, ccnt, j);
+                    const int lo = pj > cc0 ? pj : cc0, hi = pj + nj < c1 ? pj + nj : c1;
+                    const long long g0 = s_rp[j] + soff[j * sw + ci] - pj;
+                    for (int e = lo + lane; e < hi; e += 32) {
+                        cp_async4(sidx + slot * MW_ECAP + (e - cc0), a.idx + g0 + e);
+                        cp_async4(sval + slot * MW_ECAP + (e - cc0), a.val + g0 + e);
+                        swk[slot * MW_ECAP + (e - cc0)] = (uint8_t)j;
                     }
                 }
-                acc_s[q] = r;
+                if (pt == 0) s_hdr[slot] = make_int4(ci, cc0, c1 - cc0, c1 == cE);
+                if (c1 < cE) {
+                    cc0 = c1;
+                } else {
+                    ++ci;
+                    cc0 = 0;
+                    if (ci < nt) tile_runs(ci, ccnt, cpre, cE);
+                }
+            } else if (pt == 0) {
+                s_hdr[slot] = make_int4(nt, 0, 0, 1);
             }
+            cp_async_commit();  // one group per call (possibly empty) keeps the wait counts uniform
+        };
+        stage_next(0);
+        stage_next(1);
+        for (int s = 0;; ++s) {
+            const int slot = s % MW_SLOTS;
+            cp_async_wait<1>();
+            // chunk s is visible; chunk s - 1's lists are consumed, so its slot (the one
+            // restaged below), the nodes and the heads are free
+            bar_sync(BAR_PROD, MW_PROD);
+            const int4 hd = s_hdr[slot];
+            const int i = hd.x, c0 = hd.y, ne = hd.z;
+            if (i >= nt) break;
+            stage_next((s + 2) % MW_SLOTS);
+            const int b = i & 1;
+            const uint32_t tb = (uint32_t)((t_begin + i) * AG_TILE);
+            double* ab = acc + b * AG_TILE;
+            uint8_t* mb = mark + b * AG_TILE;
+            const uint32_t* si = sidx + slot * MW_ECAP;
+            const float* sv = sval + slot * MW_ECAP;
+            const uint8_t* sw8 = swk + slot * MW_ECAP;
+            // (1) push every entry onto its position's list
+            for (int n = pt; n < ne; n += MW_PROD) {
+                const unsigned q = si[n] - tb;
+                const float v = sv[n];
+                const unsigned j = sw8[n];
+                const unsigned old = atomicExch(head + q, (unsigned)n);
+                node[n] = make_uint2(__float_as_uint(v), (j << 16) | (old & 0xffffu));
+            }
+            bar_sync(BAR_PROD, MW_PROD);
+            if (c0 == 0 && i >= 2) bar_sync(BAR_EMPTY + b, MW_CONS + MW_PROD);  // buffer b released
+            // (2) each list's head entry folds its position in ascending worker order
+            for (int n = pt; n < ne; n += MW_PROD) {
+                const unsigned q = si[n] - tb;
+                const uint2 nd = node[n];
+                if (head[q] != (unsigned)n) continue;
+                double r = 0.0;
+                if (c0 > 0 && mb[q]) r = ab[q];  // partial of an earlier chunk of this tile
+                if ((nd.y & 0xffffu) == MW_NIL) {
+                    r = dadd(r, dmul(a.w[nd.y >> 16], (double)__uint_as_float(nd.x)));
+                } else {
+                    int prev = -1;
+                    for (;;) {
+                        int best = MP_MAXW;
+                        float bvv = 0.f;
+                        for (unsigned p = (unsigned)n; p != MW_NIL;) {
+                            const uint2 x = node[p];
+                            const int j = (int)(x.y >> 16);
+                            if (j > prev && j < best) {
+                                best = j;
+                                bvv = __uint_as_float(x.x);
+                            }
+                            p = x.y & 0xffffu;
+                        }
+                        if (best == MP_MAXW) break;
+                        r = dadd(r, dmul(a.w[best], (double)bvv));
+                        prev = best;
+                    }
+                }
+                ab[q] = r;
+                mb[q] = 1;
+                head[q] = MW_NIL;
+            }
+            if (hd.w) bar_arrive(BAR_FULL + b, MW_CONS + MW_PROD);  // buffer b holds tile i's values
         }
-        __syncthreads();  // S3: aggregate values of the touched positions are in acc_s
+        return;  // consumers release buffer b after tile i only when tile i + 2 exists
+    }
+
+    // ------------------------------- consumers -------------------------------
+    const bool first = a.first != 0;
+    const int q0 = 4 * tid;  // positions q0 + {0..3} and MW_HALF + q0 + {0..3}
+    for (int i = 0; i < nt; ++i) {
+        const long long tb = (t_begin + i) * AG_TILE;
+        const int b = i & 1, s = i % MW_STAGES;
         const bool full = tb + AG_TILE <= a.dim;
+        if (full) mbar_wait(&fullb[s], (unsigned)(i / MW_STAGES) & 1u);
+        bar_sync(BAR_FULL + b, MW_CONS + MW_PROD);
+        const double* ab = acc + b * AG_TILE;
+        uint8_t* mb = mark + b * AG_TILE;
+        const float* rp = ring + (s * 2) * AG_TILE;
+        const float* rb = ring + (s * 2 + 1) * AG_TILE;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // two halves of 4 positions keep the fp64 temporaries small
-            const int qh = q0 + 4 * h;
-            const uint4 mk = *reinterpret_cast<const uint4*>(who + qh);
-            double g[4] = {mk.x ? acc_s[qh] : 0.0, mk.y ? acc_s[qh + 1] : 0.0, mk.z ? acc_s[qh + 2] : 0.0,
-                           mk.w ? acc_s[qh + 3] : 0.0};
-            *reinterpret_cast<uint4*>(who + qh) = make_uint4(0, 0, 0, 0);
-            double pd[4], bd[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                pd[c] = (double)pv[4 * h + c];
-                bd[c] = (double)bv[4 * h + c];
-                sgd_elem(g[c], pd[c], bd[c], a.lr, a.mu, a.wd, first);
-            }
+        for (int hh = 0; hh < 2; ++hh) {
+            const int qh = hh * MW_HALF + q0;
+            const unsigned mk = *reinterpret_cast<const unsigned*>(mb + qh);
+            const double g[4] = {(mk & 0xffu) ? ab[qh] : 0.0, (mk & 0xff00u) ? ab[qh + 1] : 0.0,
+                                 (mk & 0xff0000u) ? ab[qh + 2] : 0.0, (mk & 0xff000000u) ? ab[qh + 3] : 0.0};
+            if (mk) *reinterpret_cast<unsigned*>(mb + qh) = 0u;
+            const long long e = tb + qh;
+            float pv[4], bv[4];
             if (full) {
-                *reinterpret_cast<float4*>(a.p + tb + qh) = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
-                *reinterpret_cast<float4*>(a.buf + tb + qh) = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
-                if (a.out)
-                    *reinterpret_cast<float4*>(a.out + tb + qh) = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+                const float4 u = *reinterpret_cast<const float4*>(rp + qh);
+                const float4 z = *reinterpret_cast<const float4*>(rb + qh);
+                pv[0] = u.x; pv[1] = u.y; pv[2] = u.z; pv[3] = u.w;
+                bv[0] = z.x; bv[1] = z.y; bv[2] = z.z; bv[3] = z.w;
             } else {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const long long q = tb + qh + c;
-                    if (q >= a.dim) continue;
-                    a.p[q] = (float)pd[c];
-                    a.buf[q] = (float)bd[c];
-                    if (a.out) a.out[q] = (TO)g[c];
+                    const bool ok = e + c < a.dim;
+                    pv[c] = ok ? a.p[e + c] : 0.f;
+                    bv[c] = ok ? a.buf[e + c] : 0.f;
+                }
+            }
+            double pd[4], bd[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                pd[c] = (double)pv[c];
+                bd[c] = (double)bv[c];
+                sgd_elem(g[c], pd[c], bd[c], a.lr, a.mu, a.wd, first);
+            }
+            if (full) {
+                *reinterpret_cast<float4*>(a.p + e) = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
+                *reinterpret_cast<float4*>(a.buf + e) = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
+                if (a.out)
+                    *reinterpret_cast<float4*>(a.out + e) = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (e + c >= a.dim) continue;
+                    a.p[e + c] = (float)pd[c];
+                    a.buf[e + c] = (float)bd[c];
+                    if (a.out) a.out[e + c] = (TO)g[c];
                 }
             }
         }
-        if (i + 1 < nt) {
-#pragma unroll
-            for (int c = 0; c < MG_PER; ++c) {
-                pv[c] = pn[c];
-                bv[c] = bn[c];
+        if (i + 2 < nt) bar_arrive(BAR_EMPTY + b, MW_CONS + MW_PROD);  // the producer may refill buffer b
+        if (i + MW_STAGES < nt) {
+            bar_sync(BAR_CONS, MW_CONS);  // ring stage s fully read
+            if (tid == 0) {
+                fence_proxy_async();
+                issue(i + MW_STAGES);
             }
         }
     }
@@ -913,15 +942,16 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
         const int sms = num_sms();
         a.pipe = comp && vec && p && nw <= MP_MAXW;
         if (a.pipe) {
-            const int tpb = (int)((ntiles + 2 * sms - 1) / (2 * sms));
-            const size_t sm = mp_smem_bytes(tpb);
-            if (sm <= 110 * 1024) {
-                cudaFuncSetAttribute(k_merge_pipe<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                k_merge_pipe<TO><<<(unsigned)((ntiles + tpb - 1) / tpb), MG_THREADS, sm, stream>>>(a, tpb);
-                debug_sync("k_merge_pipe", stream);
-            } else {
-                a.pipe = 0;
-            }
+            // one CTA per SM; the per-CTA offsets slice bounds the tiles per CTA (227 KB of
+            // shared memory, static included): larger rows run in more than one wave
+            const size_t budget = 227 * 1024 - 1024;
+            const int tpb_max = (int)((budget - mw_smem_bytes(0)) / (MP_MAXW * sizeof(int)));
+            int tpb = (int)((ntiles + sms - 1) / sms);
+            if (tpb > tpb_max) tpb = tpb_max;
+            const size_t sm = mw_smem_bytes(tpb);
+            cudaFuncSetAttribute(k_merge_ws<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            k_merge_ws<TO><<<(unsigned)((ntiles + tpb - 1) / tpb), MW_THREADS, sm, stream>>>(a, tpb);
+            debug_sync("k_merge_ws", stream);
         }
         cudaFuncSetAttribute(k_merge<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM);
         long long grid = (long long)sms * 2;

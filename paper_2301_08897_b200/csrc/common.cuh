@@ -220,6 +220,10 @@ SG_DEV void cp_async4(void* dst, const void* src) {
 SG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N> SG_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Named CTA barriers (id 0 is __syncthreads): producer/consumer hand-offs between warp roles.
+SG_DEV void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+SG_DEV void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 // SG_DEBUG_SYNC=1: synchronise after every launch and report the first failing kernel.
 inline void debug_sync(const char* what, cudaStream_t stream) {
     static const bool on = [] {
