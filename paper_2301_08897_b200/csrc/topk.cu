@@ -46,7 +46,9 @@ constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
+constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
 constexpr int NSUB_MAX = 2048;      // collect/write sub-ranges per worker
+constexpr int CW_PER_SM = 6;        // resident collect/write CTAs per SM (one wave)
 
 enum { MODE_NORMAL = 0, MODE_FALLBACK = 1 };
 enum { WR_FAST = 0, WR_SLOW = 1 };
@@ -92,7 +94,7 @@ struct TopkPlan {
         off_cidx, off_cval, off_bkey, off_bidx, off_bpos, total;
 };
 
-template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int segs_per_worker) {
+template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int segs_per_worker, long long cta_target) {
     using K = typename KeyOf<T>::K;
     TopkPlan p{};
     p.k = k;
@@ -119,15 +121,19 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.nseg = (int)((p.ntiles + p.tps - 1) / p.tps);
     p.segcap = (long long)p.tps * te;
     {
-        const int want = NSUB_MAX / (p.nseg * k);
-        p.split = want < 1 ? 1 : (want > 16 ? 16 : want);
-        p.nsub = p.nseg * p.split;  // <= max(nseg, NSUB_MAX / k) <= NSUB_MAX
+        // collect/write: about one wave of CTAs (cta_target) over all sub-ranges, each CTA
+        // streaming its sub-range with the next chunk's loads in flight
+        long long want = cta_target / ((long long)p.nseg * k);
+        const long long cap = NSUB_MAX / p.nseg;
+        if (want > cap) want = cap;
+        p.split = want < 1 ? 1 : (int)want;
+        p.nsub = p.nseg * p.split;  // <= max(nseg, NSUB_MAX) = NSUB_MAX
     }
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
     p.off_count = take(sizeof(unsigned long long) * 2 * k);  // [pass][k]
     p.off_maxkey = take(sizeof(K) * k);
-    p.off_ctr = take(sizeof(unsigned) * (8 + 8 * (size_t)k));
+    p.off_ctr = take(sizeof(unsigned) * (8 + 16 * (size_t)k));  // see the counter map in topk_gate
     p.off_bndn = take(sizeof(unsigned long long) * k);
     p.off_hist0 = take(sizeof(unsigned) * (size_t)k * H0_BINS);
     p.off_hist0fb = take(sizeof(unsigned) * (size_t)k * H0_BINS);
@@ -816,11 +822,17 @@ k_main(MainArgs<T> a) {
 // Sub-range i of a segment's n candidates for the split collect/write passes: starts are
 // 4-aligned so the writer's 16-byte loads stay aligned.
 SG_DEV long long sub_lo(long long n, int i, int split) {
-    return i == 0 ? 0 : ((n * i / split) & ~3ll);
+    // floor(n * i / split) in 32-bit: n = q * split + r  =>  q * i + (r * i) / split
+    const unsigned nn = (unsigned)n, sp = (unsigned)split;
+    const unsigned q = nn / sp, r = nn - q * sp;
+    return i == 0 ? 0 : (long long)((q * (unsigned)i + (r * (unsigned)i) / sp) & ~3u);
 }
 SG_DEV int sub_of(long long n, long long off, int split) {
-    int i = split - 1;
+    // the largest i with sub_lo(n, i) <= off: a proportional guess, then a short walk
+    int i = n > 0 ? (int)(((unsigned long long)off * (unsigned)split) / (unsigned long long)n) : 0;
+    if (i > split - 1) i = split - 1;
     while (i > 0 && sub_lo(n, i, split) > off) --i;
+    while (i + 1 < split && sub_lo(n, i + 1, split) <= off) ++i;
     return i;
 }
 
@@ -840,78 +852,104 @@ template <typename T> struct CollectArgs {
     unsigned* done;                // [k]
 };
 
+// Load the N consecutive candidate entries [e0, e0 + N) of a segment list (clipped at hi):
+// 16-byte loads when the run is whole (segment bases and sub-range starts are 4-aligned).
+template <typename T, int N>
+SG_DEV void load16(const T* cv, int e0, int hi, T (&v)[N]) {
+    if (e0 + N <= hi) {
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+            for (int r = 0; r < N / 4; ++r) {
+                const float4 x = *reinterpret_cast<const float4*>(cv + e0 + 4 * r);
+                v[4 * r] = x.x; v[4 * r + 1] = x.y; v[4 * r + 2] = x.z; v[4 * r + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < N / 2; ++r) {
+                const double2 x = *reinterpret_cast<const double2*>(cv + e0 + 2 * r);
+                v[2 * r] = x.x; v[2 * r + 1] = x.y;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < N; ++u) v[u] = e0 + u < hi ? cv[e0 + u] : (T)0;
+    }
+}
+template <int N>
+SG_DEV void load16_idx(const uint32_t* ci, int e0, int hi, uint32_t (&x)[N]) {
+    if (e0 + N <= hi) {
+#pragma unroll
+        for (int r = 0; r < N / 4; ++r) {
+            const uint4 y = *reinterpret_cast<const uint4*>(ci + e0 + 4 * r);
+            x[4 * r] = y.x; x[4 * r + 1] = y.y; x[4 * r + 2] = y.z; x[4 * r + 3] = y.w;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < N; ++u) x[u] = e0 + u < hi ? ci[e0 + u] : 0u;
+    }
+}
+constexpr int CL_EPT = 8;                       // consecutive entries per thread
+constexpr int CL_SPAN = TK_THREADS * CL_EPT;    // 2048 entries per CTA pass
+
 template <typename T>
-__global__ void __launch_bounds__(TK_THREADS)
+__global__ void __launch_bounds__(TK_THREADS, CW_PER_SM)
 k_collect(CollectArgs<T> a) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
-    constexpr int TILE = tile_elems<T>();
     __shared__ unsigned s_gt[TK_NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, sub = blockIdx.x, seg = sub / a.split, part = sub % a.split;
     const SelState<K> st = a.sel[w];
     const K lo = st.lo, span = st.span;
     const long long nseg_c = a.segcnt[(long long)w * a.nseg + seg];
-    const long long i_lo = sub_lo(nseg_c, part, a.split);
-    const long long i_hi = part + 1 == a.split ? nseg_c : sub_lo(nseg_c, part + 1, a.split);
+    const int lo32 = (int)sub_lo(nseg_c, part, a.split);
+    const int hi32 = (int)(part + 1 == a.split ? nseg_c : sub_lo(nseg_c, part + 1, a.split));
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     K* bk = a.bkey + (long long)w * a.cap;
     uint32_t* bi = a.bidx + (long long)w * a.cap;
-    // boundary entries are staged in shared memory and appended with one global atomic
-    constexpr int CU = 4, CSTAGE = 2 * CU * TK_THREADS;
-    __shared__ K st_key[CSTAGE];
-    __shared__ uint32_t st_idx[CSTAGE];
-    __shared__ uint32_t st_pos[CSTAGE];
-    __shared__ unsigned s_n;
-    __shared__ unsigned long long s_base;
-    if (tid == 0) s_n = 0;
-    __syncthreads();
-    auto flush = [&]() {
-        const unsigned cnt = s_n;
-        if (cnt == 0) return;
-        if (tid == 0) s_base = atomicAdd(a.bndn + w, (unsigned long long)cnt);
-        __syncthreads();
-        uint32_t* bp = a.bpos + (long long)w * a.cap;
-        for (unsigned q = tid; q < cnt; q += TK_THREADS) {
-            bk[s_base + q] = st_key[q];
-            bi[s_base + q] = st_idx[q];
-            bp[s_base + q] = st_pos[q];
-        }
-        __syncthreads();
-        if (tid == 0) s_n = 0;
-        __syncthreads();
-    };
+    uint32_t* bp = a.bpos + (long long)w * a.cap;
     unsigned gt = 0;
-    const int lo32 = (int)i_lo, hi32 = (int)i_hi;
-    const K span_hi = span;
-    for (int i0 = lo32; i0 < hi32; i0 += CU * TK_THREADS) {
-        T v[CU];
+    T v[CL_EPT];
+    if (lo32 < hi32) load16<T, CL_EPT>(cv, lo32 + tid * CL_EPT, hi32, v);
+    for (int base = lo32; base < hi32; base += CL_SPAN) {
+        const int e0 = base + tid * CL_EPT;
+        T x[CL_EPT];
 #pragma unroll
-        for (int u = 0; u < CU; ++u) {
-            const int i = i0 + u * TK_THREADS + tid;
-            v[u] = i < hi32 ? cv[i] : (T)0;
+        for (int u = 0; u < CL_EPT; ++u) x[u] = v[u];
+        if (base + CL_SPAN < hi32) load16<T, CL_EPT>(cv, e0 + CL_SPAN, hi32, v);  // next chunk in flight
+        unsigned bm = 0;  // entries inside the rank-m bin (the boundary)
+#pragma unroll
+        for (int u = 0; u < CL_EPT; ++u) {
+            const K key = KO::key(x[u]);
+            const K d = key - lo;  // wraps for key < lo: excluded by the key >= lo test
+            const bool ok = e0 + u < hi32 && key >= lo;
+            gt += ok && d > span;
+            bm |= (ok && d <= span ? 1u : 0u) << u;
         }
+        // warp-aggregated append: one global atomic per warp that holds boundary entries
+        const unsigned nb = __popc(bm);
+        if (__any_sync(FULL, nb != 0)) {
+            unsigned incl = nb;
 #pragma unroll
-        for (int u = 0; u < CU; ++u) {
-            const int i = i0 + u * TK_THREADS + tid;
-            const K key = KO::key(v[u]);
-            const K d = key - lo;  // wraps for key < lo: then d > span_hi, but key < lo is not "above"
-            const bool ok = i < hi32 && key >= lo;
-            gt += ok && d > span_hi;
-            if (ok && d <= span_hi) {
-                const unsigned q = atomicAdd(&s_n, 1u);
-                st_key[q] = key;
-                st_idx[q] = ci[i];
-                st_pos[q] = (uint32_t)i;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            unsigned long long wbase = 0;
+            if (lane == 31) wbase = atomicAdd(a.bndn + w, (unsigned long long)incl);
+            wbase = __shfl_sync(FULL, wbase, 31);
+            unsigned long long q = wbase + incl - nb;
+            while (bm) {
+                const int u = __ffs(bm) - 1;
+                bm &= bm - 1;
+                bk[q] = KO::key(x[u]);
+                bi[q] = ci[e0 + u];
+                bp[q] = (uint32_t)(e0 + u);
+                ++q;
             }
         }
-        // every thread must see the same s_n before anyone appends again: the barrier
-        // inside __syncthreads_or orders all reads before the next iteration's atomics
-        __syncthreads();
-        if (__syncthreads_or(s_n > CSTAGE - CU * TK_THREADS)) flush();
     }
-    flush();
     for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(FULL, gt, o);
     if (lane == 0) s_gt[warp] = gt;
     __syncthreads();
@@ -1129,8 +1167,177 @@ SG_DEV void gate_math(sg_gate_state& s, double s_full, double s_topk, uint8_t& d
 constexpr int WR_EPT = 4;                      // consecutive entries per thread per chunk
 constexpr int WR_CHUNK = TK_THREADS * WR_EPT;  // 1024
 
+// Sub-range epilogue of k_write: fixed-order partial norm of the kept values.
 template <typename T>
-__global__ void __launch_bounds__(TK_THREADS)
+SG_DEV void write_tail(const WriteArgs<T>& a, double ss) {
+    __shared__ double s_red[TK_NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = blockIdx.y, sub = blockIdx.x;
+    ss = warp_sum(ss);
+    if (lane == 0) s_red[warp] = ss;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int i = 0; i < TK_NW; ++i) s = dadd(s, s_red[i]);
+        a.pwrite[(long long)w * a.nsub + sub] = s;
+    }
+}
+
+// After k_write: fixed-order reductions of the per-segment / per-sub-range partial norms and
+// the gate (comm.py:129-160), one CTA.
+template <typename T>
+__global__ void __launch_bounds__(TK_THREADS) k_finish(WriteArgs<T> a) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int ww = warp; ww < a.k; ww += TK_NW) {
+        double sf = 0.0, sk = 0.0;
+        for (int i = lane; i < a.nseg; i += 32) {
+            sf = dadd(sf, __ldcg(a.pmain + (long long)ww * a.nseg + i));
+        }
+        for (int i = lane; i < a.nsub; i += 32) sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nsub + i));
+        sf = warp_sum(sf);
+        sk = warp_sum(sk);
+        if (lane == 0) {
+            a.norms2[2 * ww] = sf;
+            a.norms2[2 * ww + 1] = sk;
+            if (a.states) {
+                sg_gate_state s = a.states[ww];
+                uint8_t d;
+                double r;
+                gate_math(s, sf, sk, d, r);
+                a.states[ww] = s;
+                if (a.decision) a.decision[ww] = d;
+                if (a.rho) a.rho[ww] = r;
+            }
+        }
+    }
+}
+
+// Fast-mode write (T and the tie cut are final).  The CTA streams its sub-range in chunks of
+// WF_SPAN entries, thread t owning WF_EPT consecutive entries, with the next chunk's loads in
+// flight while the current one is processed: one block scan of the kept counts gives every
+// kept entry its output slot; the kept run is compacted in shared memory and stored
+// coalesced; each thread sets the merge offsets of the tiles whose first candidate lies in
+// its run (read off the tile changes between consecutive candidate indices).
+constexpr int WF_EPT = 4;
+constexpr int WF_SPAN = TK_THREADS * WF_EPT;  // 1024 entries per chunk
+
+template <typename T>
+SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
+                         typename KeyOf<T>::K T_, unsigned cut, unsigned char* stage) {
+    using KO = KeyOf<T>;
+    using K = typename KO::K;
+    __shared__ unsigned s_wt[TK_NW];
+    __shared__ uint32_t s_wl[TK_NW];  // last candidate index of each warp's run in the chunk
+    __shared__ uint32_t s_carry;      // last candidate index before the chunk
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = blockIdx.y, sub = blockIdx.x, seg = sub / a.split, part = sub % a.split;
+    const long long nsc = a.segcnt[(long long)w * a.nseg + seg];
+    const int lo32 = (int)sub_lo(nsc, part, a.split);
+    const int n32 = (int)(part + 1 == a.split ? nsc : sub_lo(nsc, part + 1, a.split));
+    const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
+    const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
+    uint32_t* oi = a.idx + (long long)w * a.m;
+    T* ov = a.val + (long long)w * a.m;
+    T v[WF_EPT];
+    uint32_t ii[WF_EPT];
+    if (lo32 < n32) {
+        load16<T, WF_EPT>(cv, lo32 + tid * WF_EPT, n32, v);
+        load16_idx<WF_EPT>(ci, lo32 + tid * WF_EPT, n32, ii);
+    }
+    if (tid == 0) s_carry = toff && lo32 > 0 && lo32 < n32 ? ci[lo32 - 1] : 0u;
+    unsigned g32 = a.segbase[(long long)w * a.nsub + sub];
+    T* st_v = reinterpret_cast<T*>(stage);                        // [WF_SPAN]
+    uint32_t* st_i = reinterpret_cast<uint32_t*>(st_v + WF_SPAN);  // [WF_SPAN]
+    double ss = 0.0;
+    for (int base = lo32; base < n32; base += WF_SPAN) {
+        const int e0 = base + tid * WF_EPT;
+        T x[WF_EPT];
+        uint32_t xi[WF_EPT];
+#pragma unroll
+        for (int u = 0; u < WF_EPT; ++u) {
+            x[u] = v[u];
+            xi[u] = ii[u];
+        }
+        if (base + WF_SPAN < n32) {  // next chunk in flight
+            load16<T, WF_EPT>(cv, e0 + WF_SPAN, n32, v);
+            load16_idx<WF_EPT>(ci, e0 + WF_SPAN, n32, ii);
+        }
+        unsigned kf = 0;
+#pragma unroll
+        for (int u = 0; u < WF_EPT; ++u) {
+            const K key = KO::key(x[u]);
+            kf |= (e0 + u < n32 && (key > T_ || (key == T_ && xi[u] <= cut)) ? 1u : 0u) << u;
+        }
+        const unsigned cnt = __popc(kf);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t left = __shfl_up_sync(FULL, xi[WF_EPT - 1], 1);
+        if (lane == 31) {
+            s_wt[warp] = incl;
+            s_wl[warp] = xi[WF_EPT - 1];
+        }
+        __syncthreads();
+        unsigned wb = 0, tot = 0;
+#pragma unroll
+        for (int i = 0; i < TK_NW; ++i) {
+            const unsigned t = s_wt[i];
+            wb += i < warp ? t : 0u;
+            tot += t;
+        }
+        const unsigned pos = g32 + wb + incl - cnt;  // output slot of this thread's first kept entry
+        if (toff && e0 < n32) {
+            // merge offsets: every tile t with tile(previous candidate) < t <= tile(this
+            // candidate) starts at this candidate: toff[t] = kept entries before it
+            const uint32_t prev = lane > 0 ? left : (warp > 0 ? s_wl[warp - 1] : s_carry);
+            int tp = e0 == 0 ? (int)t0 - 1 : (int)(prev >> MERGE_SHIFT);
+            const int ul = (e0 + WF_EPT <= n32 ? WF_EPT : n32 - e0) - 1;  // last valid entry
+            if ((int)(xi[ul] >> MERGE_SHIFT) != tp) {  // a tile starts in this run (rare)
+#pragma unroll
+                for (int u = 0; u < WF_EPT; ++u) {
+                    if (u > ul) break;
+                    const int tc = (int)(xi[u] >> MERGE_SHIFT);
+                    for (int t = tp + 1; t <= tc; ++t) toff[t] = (int)(pos + __popc(kf & ((1u << u) - 1u)));
+                    tp = tc;
+                }
+            }
+        }
+        // compact into shared memory, then coalesced stores of the chunk's kept run
+        unsigned lp = wb + incl - cnt;
+        while (kf) {
+            const int u = __ffs(kf) - 1;
+            kf &= kf - 1;
+            st_i[lp] = xi[u];
+            st_v[lp] = x[u];
+            ++lp;
+        }
+        __syncthreads();
+        for (unsigned q = tid; q < tot; q += TK_THREADS) {
+            if (g32 + q < (unsigned)a.m) {
+                const T y = st_v[q];
+                oi[g32 + q] = st_i[q];
+                ov[g32 + q] = y;
+                ss = fma((double)y, (double)y, ss);
+            }
+        }
+        if (tid == TK_THREADS - 1) s_carry = xi[WF_EPT - 1];  // the next chunk's predecessor
+        g32 += tot;
+        __syncthreads();  // s_wt, s_wl and the staging are reused
+    }
+    if (toff && part + 1 == a.split) {
+        // tiles after the segment's last candidate (to the segment end): offset = kept total
+        const int tl = nsc > 0 ? (int)(ci[nsc - 1] >> MERGE_SHIFT) : (int)t0 - 1;
+        for (int t = tl + 1 + tid; t < (int)(t0 + nt); t += TK_THREADS) toff[t] = (int)g32;
+        if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
+    }
+    return ss;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TK_THREADS, CW_PER_SM)
 k_write(WriteArgs<T> a) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
@@ -1138,8 +1345,6 @@ k_write(WriteArgs<T> a) {
     constexpr bool OFFS = TILE == MERGE_TILE;
     __shared__ unsigned s_gw[TK_NW], s_ew[TK_NW];
     __shared__ unsigned long long s_gb, s_eb;
-    __shared__ double s_red[TK_NW];
-    __shared__ int s_last;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned* s_ts = reinterpret_cast<unsigned*>(smem_raw);  // [tps] tile starts of this segment
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1158,9 +1363,16 @@ k_write(WriteArgs<T> a) {
     const long long t0 = (long long)seg * a.tps;
     const int nt = (int)(t0 + a.tps < a.ntiles ? a.tps : a.ntiles - t0);
     int* toff = (OFFS && a.tile_off) ? a.tile_off + (long long)w * (a.ntiles + 1) : nullptr;
-    if (toff)
-        for (int j = tid; j < nt; j += TK_THREADS) s_ts[j] = a.tstart[(long long)w * a.ntiles + t0 + j];
 
+    if (!slow) {
+        write_tail<T>(a, write_fast<T>(a, nt, t0, toff, T_, cut,
+                                       smem_raw + align_up(sizeof(unsigned) * (size_t)a.tps, 16)));
+        return;
+    }
+    if (toff) {
+        for (int j = tid; j < nt; j += TK_THREADS) s_ts[j] = a.tstart[(long long)w * a.ntiles + t0 + j];
+        __syncthreads();
+    }
     unsigned long long gb, eb;  // kept-before counters (fast mode: gb only)
     if (!slow) {
         gb = a.segbase[(long long)w * a.nsub + sub];
@@ -1312,43 +1524,7 @@ k_write(WriteArgs<T> a) {
         for (int j = jc + tid; j < nt; j += TK_THREADS) toff[t0 + j] = (int)kept;
         if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }
-    ss = warp_sum(ss);
-    if (lane == 0) s_red[warp] = ss;
-    __syncthreads();
-    if (tid == 0) {
-        double s = 0.0;
-        for (int i = 0; i < TK_NW; ++i) s = dadd(s, s_red[i]);
-        a.pwrite[(long long)w * a.nsub + sub] = s;
-    }
-    // last CTA overall: fixed-order norm reductions + gate
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(a.done, 1u) == gridDim.x * gridDim.y - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int ww = warp; ww < a.k; ww += TK_NW) {
-        double sf = 0.0, sk = 0.0;
-        for (int i = lane; i < a.nseg; i += 32) {
-            sf = dadd(sf, __ldcg(a.pmain + (long long)ww * a.nseg + i));
-        }
-        for (int i = lane; i < a.nsub; i += 32) sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nsub + i));
-        sf = warp_sum(sf);
-        sk = warp_sum(sk);
-        if (lane == 0) {
-            a.norms2[2 * ww] = sf;
-            a.norms2[2 * ww + 1] = sk;
-            if (a.states) {
-                sg_gate_state s = a.states[ww];
-                uint8_t d;
-                double r;
-                gate_math(s, sf, sk, d, r);
-                a.states[ww] = s;
-                if (a.decision) a.decision[ww] = d;
-                if (a.rho) a.rho[ww] = r;
-            }
-        }
-    }
+    write_tail<T>(a, ss);
 }
 
 // Diagnostics of the last sg_topk_gate call on this workspace, per worker:
@@ -1413,7 +1589,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
         return SG_ERR_INVALID;
     if (k > MAX_WORKERS || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
     if (tile_off && TILE != MERGE_TILE) return SG_ERR_INVALID;
-    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k));
+    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k), (long long)num_sms() * CW_PER_SM);
     if (!ws || ws_bytes < p.total) return SG_ERR_WORKSPACE;
     unsigned char* base = reinterpret_cast<unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
     auto at = [&](size_t off) { return base + off; };
@@ -1437,8 +1613,8 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     T* cval = reinterpret_cast<T*>(at(p.off_cval));
     K* bkey = reinterpret_cast<K*>(at(p.off_bkey));
     uint32_t* bidx = reinterpret_cast<uint32_t*>(at(p.off_bidx));
-    // counters: [1] write done, [8 + w] main done, [8 + k + w] fb done, [8 + 2k + w] collect
-    // done, [8 + 3k + w*ROUNDS + r] resolve done
+    // counters: [1] write (slow-mode look-back), [8 + w] main done, [8 + k + w] fb done,
+    // [8 + 2k + w] collect, [8 + 3k + w * ROUNDS_MAX + r] resolve rounds
     unsigned* c_main = ctr + 8;
     unsigned* c_fb = ctr + 8 + k;
     unsigned* c_col = ctr + 8 + 2 * k;
@@ -1563,9 +1739,12 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.states = states;
     wa.decision = decision;
     wa.rho = rho;
-    const size_t wr_smem = sizeof(unsigned) * (size_t)p.tps;
+    const size_t wr_smem = align_up(sizeof(unsigned) * (size_t)p.tps, 16) + (size_t)WF_SPAN * (sizeof(T) + sizeof(uint32_t));
+    cudaFuncSetAttribute(k_write<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wr_smem);
     k_write<T><<<subgrid, TK_THREADS, wr_smem, stream>>>(wa);
     debug_sync("k_write", stream);
+    k_finish<T><<<1, TK_THREADS, 0, stream>>>(wa);
+    debug_sync("k_finish", stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
@@ -1573,7 +1752,7 @@ template <typename T>
 int topk_stats(int k, long long dim, long long m, const void* ws, size_t ws_bytes, int64_t* out, cudaStream_t stream) {
     using K = typename KeyOf<T>::K;
     if (!ws || !out || k < 1 || dim < 1 || m < 1 || m > dim) return SG_ERR_INVALID;
-    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k));
+    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k), (long long)num_sms() * CW_PER_SM);
     if (ws_bytes < p.total) return SG_ERR_WORKSPACE;
     const unsigned char* base = reinterpret_cast<const unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
     k_topk_stats<T><<<1, 64, 0, stream>>>(reinterpret_cast<const SelState<K>*>(base + p.off_sel),
@@ -1591,11 +1770,11 @@ extern "C" {
 
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m) {
     if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
-    return make_plan<float>(k, dim, m, segments_per_worker<float>(k)).total;
+    return make_plan<float>(k, dim, m, segments_per_worker<float>(k), (long long)num_sms() * CW_PER_SM).total;
 }
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m) {
     if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
-    return make_plan<double>(k, dim, m, segments_per_worker<double>(k)).total;
+    return make_plan<double>(k, dim, m, segments_per_worker<double>(k), (long long)num_sms() * CW_PER_SM).total;
 }
 
 int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m, uint32_t* idx,
