@@ -100,8 +100,10 @@ int sg_gate_update(const double* norms2, int k, sg_gate_state* states,
  * Worker j is sparse iff compressed != NULL && compressed[j] != 0 (device bytes); its payload
  * is idx/val[row_ptr[j] .. row_ptr[j+1]) (device int64 row_ptr, indices ascending < dim);
  * `tile_off` ([nw][ceil(dim/4096)+1] int32, row-relative, from sg_topk_gate_f32) may be NULL,
- * in which case it is computed into the workspace.  `dense` may be NULL only if every
- * worker is compressed.
+ * in which case it is computed into the workspace.  When `tile_off` is given, worker j's
+ * entry count is tile_off[j][last] and only row_ptr[0 .. nw) (the row starts) are read, so
+ * the rows may sit apart (e.g. inside a gathered multi-rank buffer).  `dense` may be NULL
+ * only if every worker is compressed.
  * Otherwise it is dense: dense + j*ld_dense.  `weights` is a HOST array of nw doubles (the
  * caller passes r = S/sum(S) from comm.weights_from_rates, or 1/n; never batch sizes).
  * With params/momentum_buf non-NULL the momentum-SGD step (nn.py:161-172) is fused into the

@@ -123,16 +123,44 @@ class GradientExchange:
         recs["cr"], recs["delta"], recs["ewma_factor"] = cr, delta, ewma_factor
         recs["raw_gate"] = int(raw_gate)
         self.states = self.ops.make_states(recs)
+        self.packed = compression and self.world > 1 and dtype == torch.float32
         if compression:
-            self.idx = torch.empty((k, m), dtype=torch.int32, **z)
-            self.val = torch.empty((k, m), dtype=dtype, **z)
+            nt1 = kernels.merge_tiles(dim) + 1
+            if self.packed:
+                # One send buffer per rank, gathered by ONE all-gather per step (32-bit words):
+                #   [decisions (k bytes, 16-byte padded) | idx [k][m] | val [k][m] | tile_off [k][nt1]]
+                # The Top-k kernels write straight into these views.
+                dw = (k + 15) // 16 * 4
+                words = (dw + 2 * k * m + k * nt1 + 3) // 4 * 4
+                self.pack_words, self.pack_dw = words, dw
+                self.pack = torch.zeros(words, dtype=torch.int32, **z)
+                self.decision = self.pack[:dw].view(torch.uint8)[:k]
+                self.idx = self.pack[dw:dw + k * m].view(k, m)
+                self.val = self.pack[dw + k * m:dw + 2 * k * m].view(torch.float32).view(k, m)
+                self.tile_off = self.pack[dw + 2 * k * m:dw + 2 * k * m + k * nt1].view(k, nt1)
+            else:
+                self.idx = torch.empty((k, m), dtype=torch.int32, **z)
+                self.val = torch.empty((k, m), dtype=dtype, **z)
+                self.decision = torch.empty(k, dtype=torch.uint8, **z)
+                self.tile_off = torch.empty((k, nt1), dtype=torch.int32, **z) if dtype == torch.float32 else None
             self.norms2 = torch.empty((k, 2), dtype=torch.float64, **z)
-            self.decision = torch.empty(k, dtype=torch.uint8, **z)
             self.rho = torch.empty(k, dtype=torch.float64, **z)
             self.row_ptr_local = torch.arange(0, (k + 1) * m, m, dtype=torch.int64, **z)
-            nt1 = kernels.merge_tiles(dim) + 1
-            self.tile_off = torch.empty((k, nt1), dtype=torch.int32, **z) if dtype == torch.float32 else None
-            if self.world > 1:
+            if self.packed:
+                P, words, dw = self.world, self.pack_words, self.pack_dw
+                self.pack_all = torch.empty(P * words, dtype=torch.int32, **z)
+                rows = self.pack_all.view(P, words)
+                self.dec_view = rows[:, :dw].view(torch.uint8)[:, :k]
+                self.toff_view = rows[:, dw + 2 * k * m:dw + 2 * k * m + k * nt1]
+                # merge inputs: idx / val bases inside the gathered buffer; worker (r, j) at
+                # r * words + j * m words from either base
+                self.idx_all = self.pack_all[dw:]
+                self.val_all = self.pack_all[dw + k * m:].view(torch.float32)
+                starts = [r * words + j * m for r in range(P) for j in range(k)]
+                self.row_ptr_all = torch.tensor(starts + [starts[-1] + m], dtype=torch.int64, device=device)
+                self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
+                self.tile_off_all = torch.empty((self.W, nt1), dtype=torch.int32, **z)
+            elif self.world > 1:
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
                 self.idx_all = torch.empty((self.W, m), dtype=torch.int32, **z)
                 self.val_all = torch.empty((self.W, m), dtype=dtype, **z)
@@ -192,7 +220,19 @@ class GradientExchange:
     def _exchange(self, w, out, opt) -> str:
         g = self.group
         dim = self.dim
-        if self.compression:
+        if self.packed:
+            # one all-gather carries every rank's decisions, payloads and merge offsets; the
+            # decisions and offsets are regrouped contiguously on device before the host
+            # reads the decisions
+            dist.all_gather_into_tensor(self.pack_all, self.pack, group=g)
+            self.dec_all.view(self.world, self.k).copy_(self.dec_view)
+            self.tile_off_all.view(self.world, self.k, -1).copy_(self.toff_view.view(self.world, self.k, -1))
+            if bool(self.dec_all.min().item() == 1):
+                self.ops.aggregate(w, dim, compressed=self.dec_all, idx=self.idx_all, val=self.val_all,
+                                   row_ptr=self.row_ptr_all, tile_off=self.tile_off_all, out=out, **opt)
+                return "sparse-allgather"
+            all_compressed = False
+        elif self.compression:
             dist.all_gather_into_tensor(self.dec_all, self.decision, group=g)
             all_compressed = bool(self.dec_all.min().item() == 1)
         else:

@@ -47,6 +47,9 @@ class OracleOps:
             val[j] = torch.from_numpy(v.astype(np.float32))
             norms2[j, 0], norms2[j, 1] = s_full, s_topk
             decision[j], rho[j] = int(c), r
+            if tile_off is not None:  # the merge offsets sg_topk_gate_f32 produces
+                edges = np.arange(tile_off.shape[1], dtype=np.int64) * 4096
+                tile_off[j] = torch.from_numpy(np.searchsorted(i, edges).astype(np.int32))
             for f in ("ewma_full", "ewma_topk", "n_compressed", "n_uncompressed"):
                 states[j][f] = getattr(st, f)
             states[j]["initialized"] = 1
@@ -56,7 +59,9 @@ class OracleOps:
         payloads = []
         for j in range(len(weights)):
             if compressed is not None and int(compressed[j]):
-                lo, hi = int(row_ptr[j]), int(row_ptr[j + 1])
+                # with tile offsets only the row starts are read (rows may sit apart)
+                lo = int(row_ptr[j])
+                hi = lo + int(tile_off[j, -1]) if tile_off is not None else int(row_ptr[j + 1])
                 flat_i, flat_v = idx.reshape(-1), val.reshape(-1)
                 payloads.append((dim, flat_i[lo:hi].numpy().astype(np.int64), flat_v[lo:hi].numpy().astype(np.float64)))
             else:
