@@ -97,6 +97,7 @@ SG_DEV void sgd_elem(double g, double& p, double& b, double lr, double mu, doubl
 // per entry writes the boundaries between its predecessor's tile and its own.
 __global__ void k_tile_offsets(const uint32_t* __restrict__ idx, const long long* __restrict__ row_ptr,
                                const uint8_t* __restrict__ comp, long long ntiles, int* __restrict__ off) {
+    pdl_enter();
     constexpr int U = 4;  // entries per thread per iteration (independent loads in flight)
     const int j = blockIdx.y;
     if (comp && !comp[j]) return;
@@ -147,6 +148,7 @@ template <typename TI, typename TO> struct AggArgs {
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(AG_THREADS, 2)
 k_aggregate(const AggArgs<TI, TO> a) {
+    pdl_enter();
     constexpr int ECAP = AgTraits<TI>::ECAP;
     __shared__ TI S[AG_TILE];
     __shared__ uint16_t ent_pos[ECAP];
@@ -346,6 +348,7 @@ constexpr size_t MG_SMEM = AG_TILE * sizeof(double) + MG_ECAP * (sizeof(float) +
 template <typename TO>
 __global__ void __launch_bounds__(MG_THREADS, 2)
 k_merge(const AggArgs<float, TO> a) {
+    pdl_enter();
     extern __shared__ __align__(128) unsigned char mg_smem[];
     double* acc_s = reinterpret_cast<double*>(mg_smem);                   // [AG_TILE]
     float* ent_val = reinterpret_cast<float*>(acc_s + AG_TILE);            // [MG_ECAP]
@@ -632,6 +635,7 @@ inline size_t mw_smem_bytes(int tpb) {
 template <typename TO>
 __global__ void __launch_bounds__(MW_THREADS, 1)
 k_merge_ws(const AggArgs<float, TO> a, int tpb) {
+    pdl_enter();
     extern __shared__ __align__(128) unsigned char mw_smem[];
     float* ring = reinterpret_cast<float*>(mw_smem);                     // [S][2][TILE]
     double* acc = reinterpret_cast<double*>(ring + MW_STAGES * 2 * AG_TILE);  // [2][TILE]
@@ -867,6 +871,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_sgd(T* __restrict__ p, T* __restrict__ buf, const T* __restrict__ g, long long dim, double lr,
       double mu, double wd, int first, int vec_ok) {
+    pdl_enter();
     const long long nvec = vec_ok ? dim / 4 : 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
@@ -909,7 +914,7 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
         int* o = reinterpret_cast<int*>(ws);
         // rows are sized on the device; a fixed grid strides over each row
         long long blocks = ((long long)num_sms() * 8 + nw - 1) / nw;
-        k_tile_offsets<<<dim3((unsigned)blocks, nw), 256, 0, stream>>>(idx, row_ptr, comp, ntiles, o);
+        launch_pdl(k_tile_offsets, dim3(dim3((unsigned)blocks, nw)), dim3(256), 0, stream, idx, row_ptr, comp, ntiles, o);
         off = o;
     }
     AggArgs<TI, TO> a;
@@ -950,17 +955,17 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
             if (tpb > tpb_max) tpb = tpb_max;
             const size_t sm = mw_smem_bytes(tpb);
             cudaFuncSetAttribute(k_merge_ws<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            k_merge_ws<TO><<<(unsigned)((ntiles + tpb - 1) / tpb), MW_THREADS, sm, stream>>>(a, tpb);
+            launch_pdl(k_merge_ws<TO>, dim3((unsigned)((ntiles + tpb - 1) / tpb)), dim3(MW_THREADS), sm, stream, a, tpb);
             debug_sync("k_merge_ws", stream);
         }
         cudaFuncSetAttribute(k_merge<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM);
         long long grid = (long long)sms * 2;
         if (grid > ntiles) grid = ntiles;
-        k_merge<TO><<<(unsigned)grid, MG_THREADS, MG_SMEM, stream>>>(a);
+        launch_pdl(k_merge<TO>, dim3((unsigned)grid), dim3(MG_THREADS), MG_SMEM, stream, a);
         debug_sync("k_merge", stream);
     }
     else
-        k_aggregate<TI, TO><<<(unsigned)ntiles, AG_THREADS, 0, stream>>>(a);
+        launch_pdl(k_aggregate<TI, TO>, dim3((unsigned)ntiles), dim3(AG_THREADS), 0, stream, a);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
@@ -974,7 +979,7 @@ int sgd(T* p, T* buf, const T* g, long long dim, double lr, double mu, double wd
     const long long cap = (long long)num_sms() * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k_sgd<T><<<(unsigned)blocks, 256, 0, stream>>>(p, buf, g, dim, lr, mu, wd, first, vec_ok);
+    launch_pdl(k_sgd<T>, dim3((unsigned)blocks), dim3(256), 0, stream, p, buf, g, dim, lr, mu, wd, first, vec_ok);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

@@ -224,6 +224,42 @@ template <int N> SG_DEV void cp_async_wait() { asm volatile("cp.async.wait_group
 SG_DEV void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 SG_DEV void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// Programmatic dependent launch: every kernel of the chain is launched with programmatic
+// stream serialisation, lets its dependent grid launch as soon as all of its own CTAs are
+// running (pdl_trigger) and waits for its prerequisite grid before touching its outputs
+// (pdl_wait, a no-op without the launch attribute).  Every kernel calls both first thing,
+// so completion stays transitive along the chain.  SG_PDL=0 turns the attribute off.
+SG_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SG_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+SG_DEV void pdl_enter() {
+    pdl_trigger();
+    pdl_wait();
+}
+
+inline bool pdl_on() {
+    static const bool on = [] {
+        const char* e = getenv("SG_PDL");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // SG_DEBUG_SYNC=1: synchronise after every launch and report the first failing kernel.
 inline void debug_sync(const char* what, cudaStream_t stream) {
     static const bool on = [] {

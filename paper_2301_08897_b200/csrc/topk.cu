@@ -337,6 +337,7 @@ template <typename T>
 __global__ void __launch_bounds__(EST_THREADS)
 k_estimate(const T* __restrict__ g, long long ld, long long dim, long long s_eff, long long r_est,
            SelState<typename KeyOf<T>::K>* __restrict__ sel, uint4* __restrict__ zero, long long zero_vec) {
+    pdl_enter();
     using KO = KeyOf<T>;
     using K = typename KO::K;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -578,6 +579,7 @@ constexpr int MN_TILE = 4096;
 
 __global__ void __launch_bounds__(TK_THREADS, 3)
 k_main_tma(MainArgs<float> a) {
+    pdl_enter();
     using K = uint32_t;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
@@ -716,6 +718,7 @@ k_main_tma(MainArgs<float> a) {
 template <typename T>
 __global__ void __launch_bounds__(TK_THREADS, 4)
 k_main(MainArgs<T> a) {
+    pdl_enter();
     using KO = KeyOf<T>;
     using K = typename KO::K;
     using VT = Vec16<T>;
@@ -894,6 +897,7 @@ constexpr int CL_SPAN = TK_THREADS * CL_EPT;    // 2048 entries per CTA pass
 template <typename T>
 __global__ void __launch_bounds__(TK_THREADS, CW_PER_SM)
 k_collect(CollectArgs<T> a) {
+    pdl_enter();
     using KO = KeyOf<T>;
     using K = typename KO::K;
     __shared__ unsigned s_gt[TK_NW];
@@ -967,6 +971,7 @@ k_collect(CollectArgs<T> a) {
 template <typename T>
 __global__ void __launch_bounds__(1024)
 k_resolve_small(CollectArgs<T> a) {
+    pdl_enter();
     using K = typename KeyOf<T>::K;
     constexpr int TILE = tile_elems<T>();
     constexpr int NT = 1024;
@@ -1069,6 +1074,7 @@ template <typename T> struct ResolveArgs {
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_resolve(ResolveArgs<T> a, int round) {
+    pdl_enter();
     using K = typename KeyOf<T>::K;
     __shared__ unsigned hist[SEL_BINS];
     __shared__ SelState<K> st;
@@ -1187,6 +1193,7 @@ SG_DEV void write_tail(const WriteArgs<T>& a, double ss) {
 // the gate (comm.py:129-160), one CTA.
 template <typename T>
 __global__ void __launch_bounds__(TK_THREADS) k_finish(WriteArgs<T> a) {
+    pdl_enter();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int ww = warp; ww < a.k; ww += TK_NW) {
         double sf = 0.0, sk = 0.0;
@@ -1339,6 +1346,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
 template <typename T>
 __global__ void __launch_bounds__(TK_THREADS, CW_PER_SM)
 k_write(WriteArgs<T> a) {
+    pdl_enter();
     using KO = KeyOf<T>;
     using K = typename KO::K;
     constexpr int TILE = tile_elems<T>();
@@ -1532,6 +1540,7 @@ k_write(WriteArgs<T> a) {
 template <typename T>
 __global__ void k_topk_stats(const SelState<typename KeyOf<T>::K>* sel, const unsigned long long* count,
                              const unsigned long long* bndn, int k, long long* out) {
+    pdl_enter();
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= k) return;
     const bool fb = sel[w].mode == MODE_FALLBACK;
@@ -1543,6 +1552,7 @@ __global__ void k_topk_stats(const SelState<typename KeyOf<T>::K>* sel, const un
 
 __global__ void k_gate_update(const double* norms2, int k, sg_gate_state* states, uint8_t* decision,
                               double* rho) {
+    pdl_enter();
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= k) return;
     sg_gate_state s = states[w];
@@ -1627,7 +1637,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     // 1. estimate (+ zero the small scratch, incl. the slow-mode look-back status words)
     const size_t est_smem = sizeof(K) * (size_t)TopkTraits<T>::SAMPLE;
     cudaFuncSetAttribute(k_estimate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)est_smem);
-    k_estimate<T><<<k, EST_THREADS, est_smem, stream>>>(g, ld, dim, p.s_eff, p.r_est, sel,
+    launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), est_smem, stream, g, ld, dim, p.s_eff, p.r_est, sel,
                                                          reinterpret_cast<uint4*>(base),
                                                          (long long)(p.zero_end / 16));
     debug_sync("k_estimate", stream);
@@ -1661,11 +1671,11 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     auto launch_main = [&]() {
         if constexpr (sizeof(T) == 4) {
             if (tma) {
-                k_main_tma<<<sgrid, TK_THREADS, MN_SMEM, stream>>>(ma);
+                launch_pdl(k_main_tma, dim3(sgrid), dim3(TK_THREADS), MN_SMEM, stream, ma);
                 return;
             }
         }
-        k_main<T><<<sgrid, TK_THREADS, 0, stream>>>(ma);
+        launch_pdl(k_main<T>, dim3(sgrid), dim3(TK_THREADS), 0, stream, ma);
     };
     launch_main();
     debug_sync("k_main", stream);
@@ -1694,11 +1704,11 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ca.bndn = bndn;
     ca.done = c_col;
     const dim3 subgrid((unsigned)p.nsub, (unsigned)k);
-    k_collect<T><<<subgrid, TK_THREADS, 0, stream>>>(ca);
+    launch_pdl(k_collect<T>, dim3(subgrid), dim3(TK_THREADS), 0, stream, ca);
     debug_sync("k_collect", stream);
     const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES + sizeof(unsigned) * NSUB_MAX;
     cudaFuncSetAttribute(k_resolve_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem);
-    k_resolve_small<T><<<k, 1024, res_smem, stream>>>(ca);
+    launch_pdl(k_resolve_small<T>, dim3(k), dim3(1024), res_smem, stream, ca);
     debug_sync("k_resolve_small", stream);
     // 4. slow mode only: multi-CTA select rounds over an oversized boundary
     ResolveArgs<T> ra;
@@ -1710,7 +1720,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ra.done = c_res;
     const unsigned rper = (unsigned)((sms * 2 + k - 1) / k);
     for (int r = 0; r < TopkTraits<T>::ROUNDS_MAX; ++r)
-        k_resolve<T><<<dim3(rper, (unsigned)k), 256, 0, stream>>>(ra, r);
+        launch_pdl(k_resolve<T>, dim3(dim3(rper, (unsigned)k)), dim3(256), 0, stream, ra, r);
     debug_sync("k_resolve", stream);
     // 5. ordered write + norms + gate
     WriteArgs<T> wa;
@@ -1741,9 +1751,9 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.rho = rho;
     const size_t wr_smem = align_up(sizeof(unsigned) * (size_t)p.tps, 16) + (size_t)WF_SPAN * (sizeof(T) + sizeof(uint32_t));
     cudaFuncSetAttribute(k_write<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wr_smem);
-    k_write<T><<<subgrid, TK_THREADS, wr_smem, stream>>>(wa);
+    launch_pdl(k_write<T>, dim3(subgrid), dim3(TK_THREADS), wr_smem, stream, wa);
     debug_sync("k_write", stream);
-    k_finish<T><<<1, TK_THREADS, 0, stream>>>(wa);
+    launch_pdl(k_finish<T>, dim3(1), dim3(TK_THREADS), 0, stream, wa);
     debug_sync("k_finish", stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
@@ -1755,7 +1765,7 @@ int topk_stats(int k, long long dim, long long m, const void* ws, size_t ws_byte
     const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k), (long long)num_sms() * CW_PER_SM);
     if (ws_bytes < p.total) return SG_ERR_WORKSPACE;
     const unsigned char* base = reinterpret_cast<const unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
-    k_topk_stats<T><<<1, 64, 0, stream>>>(reinterpret_cast<const SelState<K>*>(base + p.off_sel),
+    launch_pdl(k_topk_stats<T>, dim3(1), dim3(64), 0, stream, reinterpret_cast<const SelState<K>*>(base + p.off_sel),
                                           reinterpret_cast<const unsigned long long*>(base + p.off_count),
                                           reinterpret_cast<const unsigned long long*>(base + p.off_bndn), k,
                                           reinterpret_cast<long long*>(out));
@@ -1803,7 +1813,7 @@ int sg_topk_stats_f64(int k, int64_t dim, int64_t m, const void* workspace, size
 int sg_gate_update(const double* norms2, int k, sg_gate_state* states, uint8_t* decision,
                    double* rho, void* stream) {
     if (!norms2 || !states || k < 1) return SG_ERR_INVALID;
-    k_gate_update<<<(k + 63) / 64, 64, 0, (cudaStream_t)stream>>>(norms2, k, states, decision, rho);
+    launch_pdl(k_gate_update, dim3((k + 63) / 64), dim3(64), 0, (cudaStream_t)stream, norms2, k, states, decision, rho);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
