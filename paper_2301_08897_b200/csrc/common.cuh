@@ -195,6 +195,9 @@ SG_DEV unsigned long long policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+SG_DEV void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 SG_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
     unsigned done = 0;
     do {

@@ -44,6 +44,7 @@ constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
+constexpr int EST_G = 16;        // sampling CTAs per worker (k_sample)
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
 constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
@@ -90,7 +91,7 @@ struct TopkPlan {
     long long s_eff, stride, r_est;
     long long ntiles, segcap;
     size_t off_count, off_maxkey, off_ctr, off_bndn, off_hist0, off_hist0fb, off_histr, off_status, zero_end;
-    size_t off_sel, off_cnt, off_tstart, off_segcnt, off_seggt, off_segbase, off_pmain, off_pwrite,
+    size_t off_sel, off_samp, off_mm, off_cnt, off_tstart, off_segcnt, off_seggt, off_segbase, off_pmain, off_pwrite,
         off_cidx, off_cval, off_bkey, off_bidx, off_bpos, total;
 };
 
@@ -141,6 +142,8 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.off_status = take(sizeof(unsigned long long) * (size_t)k * p.nsub);
     p.zero_end = o;
     p.off_sel = take(sizeof(SelState<K>) * k);
+    p.off_samp = take(sizeof(K) * (size_t)k * TopkTraits<T>::SAMPLE);
+    p.off_mm = take(sizeof(K) * (size_t)k * EST_G * 2);
     p.off_cnt = take(sizeof(unsigned) * (size_t)k * p.ntiles);
     p.off_tstart = take(sizeof(unsigned) * (size_t)k * p.ntiles);
     p.off_segcnt = take(sizeof(unsigned) * (size_t)k * p.nseg);
@@ -325,35 +328,34 @@ SG_DEV unsigned block_select_small_u32(const unsigned* v, const uint8_t* flag, l
 }
 
 // --------------------------------------------------------------------------------------
-// k_estimate: the sample is S/32 randomly placed 32-element chunks (one per stratum of the
-// row, so every warp load is one coalesced 128-byte line for f32); est is the lower edge of
-// the 2048-bin histogram bin (over the sample's key range) that holds the r_est-th largest
-// sample key -- never above that key, so count(key >= est) >= m keeps its ~1 - 1e-9 odds.
-// With dim <= S the "sample" is the whole row and est is a lower bound of the true T.
+// Candidate threshold estimate.  The sample is S/32 randomly placed 32-element chunks (one
+// per stratum of the row, so every warp load is one coalesced 128-byte line for f32).
 // --------------------------------------------------------------------------------------
 constexpr int CHUNK = 32;
 
+// k_sample: EST_G CTAs per worker gather the sample in parallel (one random 32-element chunk
+// per stratum; a warp's chunk loads all in flight) into the workspace, with per-CTA key
+// ranges; they also clear the small scratch (incl. the slow-mode look-back words).
 template <typename T>
-__global__ void __launch_bounds__(EST_THREADS)
-k_estimate(const T* __restrict__ g, long long ld, long long dim, long long s_eff, long long r_est,
-           SelState<typename KeyOf<T>::K>* __restrict__ sel, uint4* __restrict__ zero, long long zero_vec) {
+__global__ void __launch_bounds__(256)
+k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
+         typename KeyOf<T>::K* __restrict__ samp, typename KeyOf<T>::K* __restrict__ mm,
+         uint4* __restrict__ zero, long long zero_vec) {
     pdl_enter();
     using KO = KeyOf<T>;
     using K = typename KO::K;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    K* sk = reinterpret_cast<K*>(smem_raw);
-    __shared__ unsigned hist[SEL_BINS];
-    __shared__ K s_min[32], s_max[32];
-    __shared__ K s_lo, s_span;
-    __shared__ int s_shift;
-    const int w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (long long i = (long long)w * EST_THREADS + tid; i < zero_vec; i += (long long)gridDim.x * EST_THREADS)
+    __shared__ K s_min[8], s_max[8];
+    const int x = blockIdx.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long cta = (long long)w * gridDim.x + x;
+    for (long long i = cta * 256 + tid; i < zero_vec; i += (long long)gridDim.x * gridDim.y * 256)
         zero[i] = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < SEL_BINS; i += EST_THREADS) hist[i] = 0;
     const T* row = g + (long long)w * ld;
+    K* sk = samp + (long long)w * TopkTraits<T>::SAMPLE;
     K mn = KO::KMAX, mx = 0;
-    if (s_eff == dim) {
-        for (long long i = tid; i < s_eff; i += EST_THREADS) {
+    if (s_eff == dim) {  // the sample is the whole row
+        const long long slice = (dim + gridDim.x - 1) / gridDim.x;
+        const long long lo = x * slice, hi = lo + slice < dim ? lo + slice : dim;
+        for (long long i = lo + tid; i < hi; i += 256) {
             const K key = KO::key(row[i]);
             sk[i] = key;
             mn = key < mn ? key : mn;
@@ -362,13 +364,13 @@ k_estimate(const T* __restrict__ g, long long ld, long long dim, long long s_eff
     } else {
         const long long nch = s_eff / CHUNK;
         const long long stratum = dim / nch;  // >= CHUNK because dim > s_eff
-        constexpr int WARPS = EST_THREADS / 32;
+        const int gw = x * 8 + warp, nwarps = gridDim.x * 8;
         constexpr int BATCH = 4;
-        for (long long c0 = warp; c0 < nch; c0 += (long long)WARPS * BATCH) {
+        for (long long c0 = gw; c0 < nch; c0 += (long long)nwarps * BATCH) {
             T v[BATCH];
 #pragma unroll
             for (int u = 0; u < BATCH; ++u) {
-                const long long c = c0 + (long long)u * WARPS;
+                const long long c = c0 + (long long)u * nwarps;
                 v[u] = (T)0;
                 if (c < nch) {
                     const unsigned h = (unsigned)mix64((unsigned long long)c * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
@@ -378,7 +380,7 @@ k_estimate(const T* __restrict__ g, long long ld, long long dim, long long s_eff
             }
 #pragma unroll
             for (int u = 0; u < BATCH; ++u) {
-                const long long c = c0 + (long long)u * WARPS;
+                const long long c = c0 + (long long)u * nwarps;
                 if (c < nch) {
                     const K key = KO::key(v[u]);
                     sk[c * CHUNK + lane] = key;
@@ -389,9 +391,9 @@ k_estimate(const T* __restrict__ g, long long ld, long long dim, long long s_eff
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
-        const K x = __shfl_xor_sync(FULL, mn, o), y = __shfl_xor_sync(FULL, mx, o);
-        mn = x < mn ? x : mn;
-        mx = y > mx ? y : mx;
+        const K a = __shfl_xor_sync(FULL, mn, o), b = __shfl_xor_sync(FULL, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
     }
     if (lane == 0) {
         s_min[warp] = mn;
@@ -399,19 +401,55 @@ k_estimate(const T* __restrict__ g, long long ld, long long dim, long long s_eff
     }
     __syncthreads();
     if (tid == 0) {
-        K x = KO::KMAX, y = 0;
-        for (int i = 0; i < EST_THREADS / 32; ++i) {
-            x = s_min[i] < x ? s_min[i] : x;
-            y = s_max[i] > y ? s_max[i] : y;
+        K a = KO::KMAX, b = 0;
+        for (int i = 0; i < 8; ++i) {
+            a = s_min[i] < a ? s_min[i] : a;
+            b = s_max[i] > b ? s_max[i] : b;
         }
-        s_lo = x;
-        s_span = y - x;
-        s_shift = digit_shift<K>(y - x, SEL_BITS);
+        mm[cta * 2] = a;
+        mm[cta * 2 + 1] = b;
+    }
+}
+
+// k_estimate: one CTA per worker; est = the lower edge of the 2048-bin histogram bin (over the
+// sample's key range) that holds the r_est-th largest sample key -- never above that key, so
+// count(key >= est) >= m keeps its ~1 - 1e-9 odds.  With dim <= S the "sample" is the whole
+// row and est is a lower bound of the true T.
+template <typename T>
+__global__ void __launch_bounds__(EST_THREADS)
+k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf<T>::K* __restrict__ samp,
+           const typename KeyOf<T>::K* __restrict__ mm, int G, SelState<typename KeyOf<T>::K>* __restrict__ sel) {
+    pdl_enter();
+    using KO = KeyOf<T>;
+    using K = typename KO::K;
+    __shared__ unsigned hist[SEL_BINS];
+    __shared__ K s_lo, s_span;
+    __shared__ int s_shift;
+    const int w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < SEL_BINS; i += EST_THREADS) hist[i] = 0;
+    if (warp == 0) {
+        K a = KO::KMAX, b = 0;
+        for (int i = lane; i < G; i += 32) {
+            const K x = mm[((long long)w * G + i) * 2], y = mm[((long long)w * G + i) * 2 + 1];
+            a = x < a ? x : a;
+            b = y > b ? y : b;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const K x = __shfl_xor_sync(FULL, a, o), y = __shfl_xor_sync(FULL, b, o);
+            a = x < a ? x : a;
+            b = y > b ? y : b;
+        }
+        if (lane == 0) {
+            s_lo = a;
+            s_span = b - a;
+            s_shift = digit_shift<K>(b - a, SEL_BITS);
+        }
     }
     __syncthreads();
     const K lo = s_lo;
     const int shift = s_shift;
     const long long ns = (s_eff / CHUNK) * CHUNK == s_eff || s_eff == dim ? s_eff : (s_eff / CHUNK) * CHUNK;
+    const K* sk = samp + (long long)w * TopkTraits<T>::SAMPLE;
     if (r_est <= ns) {
         for (long long i = tid; i < ns; i += EST_THREADS) atomicAdd(&hist[digit<K>(sk[i], lo, shift, SEL_BINS)], 1u);
     }
@@ -1634,12 +1672,14 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     const bool vec_ok = (reinterpret_cast<size_t>(g) % 16 == 0) && ((ld * (long long)sizeof(T)) % 16 == 0);
     const int sms = num_sms();
 
-    // 1. estimate (+ zero the small scratch, incl. the slow-mode look-back status words)
-    const size_t est_smem = sizeof(K) * (size_t)TopkTraits<T>::SAMPLE;
-    cudaFuncSetAttribute(k_estimate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)est_smem);
-    launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), est_smem, stream, g, ld, dim, p.s_eff, p.r_est, sel,
-                                                         reinterpret_cast<uint4*>(base),
-                                                         (long long)(p.zero_end / 16));
+    // 1. sample (+ zero the small scratch, incl. the slow-mode look-back status words), estimate
+    K* samp = reinterpret_cast<K*>(at(p.off_samp));
+    K* mm = reinterpret_cast<K*>(at(p.off_mm));
+    launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm,
+               reinterpret_cast<uint4*>(base), (long long)(p.zero_end / 16));
+    debug_sync("k_sample", stream);
+    launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), 0, stream, dim, p.s_eff, p.r_est,
+               (const K*)samp, (const K*)mm, EST_G, sel);
     debug_sync("k_estimate", stream);
     // 2. main streaming pass, then the (normally empty) fallback pass
     MainArgs<T> ma;
