@@ -263,6 +263,36 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+SG_DEV unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Cooperative launch (every CTA co-resident, for an in-kernel grid barrier) with programmatic
+// stream serialisation; without PDL support for the combination it launches cooperative only.
+template <typename... KArgs, typename... Args>
+inline void launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                        Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
+    if (cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) != cudaSuccess && cfg.numAttrs == 2) {
+        cudaGetLastError();
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    }
+}
+
 // SG_DEBUG_SYNC=1: synchronise after every launch and report the first failing kernel.
 inline void debug_sync(const char* what, cudaStream_t stream) {
     static const bool on = [] {

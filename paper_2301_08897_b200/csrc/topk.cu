@@ -1003,32 +1003,19 @@ k_collect(CollectArgs<T> a) {
 }
 
 // --------------------------------------------------------------------------------------
-// k_resolve_small: one CTA per worker finishes the select in shared memory when the
+// resolve_small: one CTA per worker finishes the select in shared memory when the
 // boundary is small (the normal case): T, the tie cut by index, per-segment output bases.
 // --------------------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(1024)
-k_resolve_small(CollectArgs<T> a) {
-    pdl_enter();
+SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, unsigned* hist) {
     using K = typename KeyOf<T>::K;
     constexpr int TILE = tile_elems<T>();
     constexpr int NT = 1024;
-    __shared__ unsigned hist[SEL_BINS];
+    constexpr int RES = TopkTraits<T>::RES;
     __shared__ SelState<K> sst;
     __shared__ unsigned s_eq, s_res[2];
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int w = blockIdx.x;
-    constexpr int RES = TopkTraits<T>::RES;
-    const unsigned long long h = a.bndn[w];
-    if (h > RES) {
-        if (tid == 0) {
-            SelState<K> s = a.sel[w];
-            s.wmode = WR_SLOW;
-            a.sel[w] = s;
-        }
-        return;
-    }
     K* sk = reinterpret_cast<K*>(smem_raw);
     uint32_t* si = reinterpret_cast<uint32_t*>(sk + RES);
     uint32_t* sp = si + RES;                               // position in the segment list
@@ -1098,64 +1085,110 @@ k_resolve_small(CollectArgs<T> a) {
 }
 
 // --------------------------------------------------------------------------------------
-// k_resolve: one multi-CTA radix round over an oversized boundary set (slow mode only).
+// k_resolve: grid (G, k), one launch.  Every CTA reads all k boundary counts, so the common
+// case (every boundary fits one CTA's shared memory) needs no grid-wide step: CTA 0 of each
+// worker resolves it in shared memory (resolve_small) and the other CTAs exit.  If some
+// worker's boundary is oversized (heavy ties), all G*k CTAs -- co-resident by cooperative
+// launch -- run the radix rounds over that worker's boundary keys in global memory with a
+// grid barrier between the histogram and the bin pick; its write then takes the slow mode.
 // --------------------------------------------------------------------------------------
 template <typename T> struct ResolveArgs {
-    long long cap;
     SelState<typename KeyOf<T>::K>* sel;
-    const typename KeyOf<T>::K* bkey;
-    const unsigned long long* bndn;
-    unsigned* hist;   // [k][ROUNDS_MAX][SEL_BINS]
-    unsigned* done;   // [k][ROUNDS_MAX]
+    unsigned* hist;   // [k][ROUNDS_MAX][SEL_BINS] (zeroed per call)
+    unsigned* bar;    // grid-barrier counter (zeroed per call)
 };
 
+template <typename K>
+SG_DEV SelState<K> ld_cg_state(const SelState<K>* p) {
+    static_assert(sizeof(SelState<K>) % 8 == 0, "SelState is read as 64-bit words");
+    SelState<K> s;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(p);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(SelState<K>) / 8); ++i) dst[i] = __ldcg(src + i);
+    return s;
+}
+
+SG_DEV void grid_barrier(unsigned* ctr, unsigned nblocks, unsigned& gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned target = (gen + 1) * nblocks;
+        atomicAdd(ctr, 1u);
+        while (ld_acquire_gpu(ctr) < target) __nanosleep(64);
+        __threadfence();
+    }
+    ++gen;
+    __syncthreads();
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256)
-k_resolve(ResolveArgs<T> a, int round) {
+__global__ void __launch_bounds__(1024)
+k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
     pdl_enter();
     using K = typename KeyOf<T>::K;
+    constexpr int RES = TopkTraits<T>::RES;
+    constexpr int NT = 1024;
     __shared__ unsigned hist[SEL_BINS];
+    __shared__ int s_any;
     __shared__ SelState<K> st;
-    __shared__ int s_last;
-    const int w = blockIdx.y, tid = threadIdx.x;
-    if (tid == 0) st = a.sel[w];
-    for (int i = tid; i < SEL_BINS; i += 256) hist[i] = 0;
-    __syncthreads();
-    if (st.done || st.wmode != WR_SLOW) return;
-    const K lo = st.lo, span = st.span;
-    const int shift = st.shift;
-    const long long n = (long long)a.bndn[w];
-    const K* src = a.bkey + (long long)w * a.cap;
-    for (long long i = (long long)blockIdx.x * 256 + tid; i < n; i += (long long)gridDim.x * 256) {
-        const K key = src[i];
-        if (key >= lo && key - lo <= span) atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
+    const int x = blockIdx.x, w = blockIdx.y, tid = threadIdx.x;
+    if (tid == 0) {
+        int any = 0;
+        for (int j = 0; j < (int)gridDim.y; ++j) any |= a.bndn[j] > (unsigned long long)RES;
+        s_any = any;
     }
     __syncthreads();
-    unsigned* gh = a.hist + ((long long)w * TopkTraits<T>::ROUNDS_MAX + round) * SEL_BINS;
-    for (int i = tid; i < SEL_BINS; i += 256)
-        if (hist[i]) atomicAdd(gh + i, hist[i]);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(a.done + w * TopkTraits<T>::ROUNDS_MAX + round, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int i = tid; i < SEL_BINS; i += 256) hist[i] = __ldcg(gh + i);
-    __syncthreads();
-    if (tid < 32) {
-        int bin;
-        unsigned long long above;
-        find_bin_from_top<SEL_BINS>(hist, st.rank, bin, above);
-        if (tid == 0) {
-            SelState<K> s = st;
-            if (bin < 0) {
-                s.done = 1;
-                s.T = s.lo;
-            } else {
-                narrow<K>(s, bin, above, hist[bin], SEL_BINS, SEL_BITS);
+    const unsigned long long h = a.bndn[w];
+    const bool slow = h > (unsigned long long)RES;
+    if (x == 0 && !slow) resolve_small<T>(a, w, h, hist);
+    if (!s_any) return;  // uniform over the grid
+    // slow mode: radix rounds over the oversized boundary sets
+    const unsigned nblocks = gridDim.x * gridDim.y;
+    unsigned gen = 0;
+    const K* src = a.bkey + (long long)w * a.cap;
+    for (int round = 0; round < TopkTraits<T>::ROUNDS_MAX; ++round) {
+        if (tid == 0) st = ld_cg_state(r.sel + w);
+        for (int i = tid; i < SEL_BINS; i += NT) hist[i] = 0;
+        __syncthreads();
+        unsigned* gh = r.hist + ((long long)w * TopkTraits<T>::ROUNDS_MAX + round) * SEL_BINS;
+        if (slow && !st.done) {
+            const K lo = st.lo, span = st.span;
+            const int shift = st.shift;
+            for (long long i = (long long)x * NT + tid; i < (long long)h; i += (long long)gridDim.x * NT) {
+                const K key = src[i];
+                if (key >= lo && key - lo <= span) atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
             }
-            a.sel[w] = s;
+            __syncthreads();
+            for (int i = tid; i < SEL_BINS; i += NT)
+                if (hist[i]) atomicAdd(gh + i, hist[i]);
         }
+        grid_barrier(r.bar, nblocks, gen);
+        if (slow && !st.done && x == 0) {
+            for (int i = tid; i < SEL_BINS; i += NT) hist[i] = __ldcg(gh + i);
+            __syncthreads();
+            if (tid < 32) {
+                int bin;
+                unsigned long long above;
+                find_bin_from_top<SEL_BINS>(hist, st.rank, bin, above);
+                if (tid == 0) {
+                    SelState<K> s = st;
+                    if (bin < 0) {
+                        s.done = 1;
+                        s.T = s.lo;
+                    } else {
+                        narrow<K>(s, bin, above, hist[bin], SEL_BINS, SEL_BITS);
+                    }
+                    r.sel[w] = s;
+                }
+            }
+        }
+        grid_barrier(r.bar, nblocks, gen);
+    }
+    if (slow && x == 0 && tid == 0) {
+        SelState<K> s = ld_cg_state(r.sel + w);
+        s.wmode = WR_SLOW;
+        r.sel[w] = s;
     }
 }
 
@@ -1746,21 +1779,17 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     const dim3 subgrid((unsigned)p.nsub, (unsigned)k);
     launch_pdl(k_collect<T>, dim3(subgrid), dim3(TK_THREADS), 0, stream, ca);
     debug_sync("k_collect", stream);
+    // 4. resolve: in-CTA for the normal boundary, cooperative radix rounds for oversized ones
     const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES + sizeof(unsigned) * NSUB_MAX;
-    cudaFuncSetAttribute(k_resolve_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem);
-    launch_pdl(k_resolve_small<T>, dim3(k), dim3(1024), res_smem, stream, ca);
-    debug_sync("k_resolve_small", stream);
-    // 4. slow mode only: multi-CTA select rounds over an oversized boundary
+    cudaFuncSetAttribute(k_resolve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem);
     ResolveArgs<T> ra;
-    ra.cap = capw;
     ra.sel = sel;
-    ra.bkey = bkey;
-    ra.bndn = bndn;
     ra.hist = histr;
-    ra.done = c_res;
-    const unsigned rper = (unsigned)((sms * 2 + k - 1) / k);
-    for (int r = 0; r < TopkTraits<T>::ROUNDS_MAX; ++r)
-        launch_pdl(k_resolve<T>, dim3(dim3(rper, (unsigned)k)), dim3(256), 0, stream, ra, r);
+    ra.bar = c_res;
+    int gres = sms / k;  // one 1024-thread CTA per SM: the whole grid is co-resident
+    if (gres > 16) gres = 16;
+    if (gres < 1) gres = 1;
+    launch_coop(k_resolve<T>, dim3((unsigned)gres, (unsigned)k), dim3(1024), res_smem, stream, ca, ra);
     debug_sync("k_resolve", stream);
     // 5. ordered write + norms + gate
     WriteArgs<T> wa;

@@ -17,7 +17,7 @@ _GATE_BYTES = _capi.GATE_STATE_DTYPE.itemsize
 # Kernel launches issued through this module (each C-ABI entry point launches a fixed
 # sequence; see csrc/topk.cu and csrc/aggregate.cu).  bench.py reports the count.
 LAUNCHES = {"n": 0}
-TOPK_LAUNCHES = {torch.float32: 2 + 2 + 1 + 1 + 3 + 1 + 1, torch.float64: 2 + 2 + 1 + 1 + 6 + 1 + 1}
+TOPK_LAUNCHES = {torch.float32: 2 + 2 + 1 + 1 + 1 + 1, torch.float64: 2 + 2 + 1 + 1 + 1 + 1}
 
 
 def _count(n: int) -> None:
@@ -42,15 +42,16 @@ def _stream() -> int:
 class Workspace:
     """Grow-only device scratch buffer owned by the Python caller (one per device)."""
 
-    _cache: dict[int, torch.Tensor] = {}
+    _cache: dict[tuple[int, int], torch.Tensor] = {}
 
     @classmethod
-    def get(cls, nbytes: int, device: torch.device) -> torch.Tensor:
+    def get(cls, nbytes: int, device: torch.device, slot: int = 0) -> torch.Tensor:
+        """``slot`` separates calls that may run concurrently on different streams."""
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        buf = cls._cache.get(idx)
+        buf = cls._cache.get((idx, slot))
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
-            cls._cache[idx] = buf
+            cls._cache[(idx, slot)] = buf
         return buf
 
 
@@ -85,8 +86,12 @@ def topk_gate(
     dim: int | None = None,
     out: tuple | None = None,
     tile_off: torch.Tensor | None = None,
+    workspace_slot: int = 0,
 ):
     """Batched Top-k + norms (+ gate) over the rows of ``g`` ([k, ld] or [D]).
+
+    ``workspace_slot`` selects a separate scratch buffer for calls issued concurrently on
+    different streams.
 
     Returns (idx int32 [k, m] (uint32 bits), val [k, m], norms2 f64 [k, 2], decision u8 [k],
     rho f64 [k]); decision/rho are None without ``states``.
@@ -114,7 +119,7 @@ def topk_gate(
     nbytes = topk_workspace_bytes(g.dtype, k, D, m)
     if nbytes == 0:
         raise ValueError("invalid top-k shape")
-    ws = Workspace.get(nbytes, dev)
+    ws = Workspace.get(nbytes, dev, workspace_slot)
     lib = _capi.load()
     args = [g2.data_ptr(), k, ld, D, m, idx.data_ptr(), val.data_ptr(), norms2.data_ptr(),
             _ptr(states), _ptr(decision), _ptr(rho)]
@@ -129,9 +134,9 @@ def topk_gate(
     return idx, val, norms2, decision, rho
 
 
-def topk_stats(dtype: torch.dtype, k: int, dim: int, m: int, device: torch.device) -> np.ndarray:
+def topk_stats(dtype: torch.dtype, k: int, dim: int, m: int, device: torch.device, workspace_slot: int = 0) -> np.ndarray:
     """Per-worker {candidates, boundary, fallback, slow} of the last topk_gate call (synchronises)."""
-    ws = Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device)
+    ws = Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, workspace_slot)
     out = torch.zeros((k, 4), dtype=torch.int64, device=device)
     lib = _capi.load()
     fn = lib.sg_topk_stats_f32 if dtype == torch.float32 else lib.sg_topk_stats_f64
