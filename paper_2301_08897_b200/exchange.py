@@ -160,6 +160,10 @@ class GradientExchange:
                 self.row_ptr_all = torch.tensor(starts + [starts[-1] + m], dtype=torch.int64, device=device)
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
                 self.tile_off_all = torch.empty((self.W, nt1), dtype=torch.int32, **z)
+                self._dec_host = (torch.empty(self.W, dtype=torch.uint8, pin_memory=True)
+                                  if device.type == "cuda" else None)
+                self._dec_ready = torch.cuda.Event() if device.type == "cuda" else None
+                self._merge = None
             elif self.world > 1:
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
                 self.idx_all = torch.empty((self.W, m), dtype=torch.int32, **z)
@@ -225,13 +229,31 @@ class GradientExchange:
             # decisions and offsets are regrouped contiguously on device before the host
             # reads the decisions
             dist.all_gather_into_tensor(self.pack_all, self.pack, group=g)
-            self.dec_all.view(self.world, self.k).copy_(self.dec_view)
-            self.tile_off_all.view(self.world, self.k, -1).copy_(self.toff_view.view(self.world, self.k, -1))
-            if bool(self.dec_all.min().item() == 1):
-                self.ops.aggregate(w, dim, compressed=self.dec_all, idx=self.idx_all, val=self.val_all,
-                                   row_ptr=self.row_ptr_all, tile_off=self.tile_off_all, out=out, **opt)
+            if self._dec_host is not None:
+                # the step's one host synchronisation: the W decision bytes go to pinned memory
+                # first; the device-side regrouping of decisions and offsets for the merge is
+                # enqueued behind them and runs while the host waits and launches the merge
+                self._dec_host.view(self.world, self.k).copy_(self.dec_view, non_blocking=True)
+                self._dec_ready.record()
+                self.dec_all.view(self.world, self.k).copy_(self.dec_view)
+                self.tile_off_all.view(self.world, self.k, -1).copy_(self.toff_view.view(self.world, self.k, -1))
+                self._dec_ready.synchronize()
+                all_compressed = bool(self._dec_host.numpy().min() == 1)
+            else:
+                self.dec_all.view(self.world, self.k).copy_(self.dec_view)
+                self.tile_off_all.view(self.world, self.k, -1).copy_(self.toff_view.view(self.world, self.k, -1))
+                all_compressed = bool(self.dec_all.min().item() == 1)
+            if all_compressed:
+                if isinstance(self.ops, CudaOps):
+                    if self._merge is None:
+                        self._merge = kernels.MergeLauncher(self.W, dim, self.dec_all, self.idx_all, self.val_all,
+                                                            self.row_ptr_all, self.tile_off_all, self.params,
+                                                            self.momentum_buf, self.momentum, self.weight_decay)
+                    self._merge(w, opt["lr"], opt["first_step"], out)
+                else:
+                    self.ops.aggregate(w, dim, compressed=self.dec_all, idx=self.idx_all, val=self.val_all,
+                                       row_ptr=self.row_ptr_all, tile_off=self.tile_off_all, out=out, **opt)
                 return "sparse-allgather"
-            all_compressed = False
         elif self.compression:
             dist.all_gather_into_tensor(self.dec_all, self.decision, group=g)
             all_compressed = bool(self.dec_all.min().item() == 1)

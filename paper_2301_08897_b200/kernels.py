@@ -207,6 +207,32 @@ def weighted_aggregate(
     return out
 
 
+class MergeLauncher:
+    """The all-sparse float32 merge + fused SGD with every pointer bound once (the multi-GPU
+    exchange launches it right after its one host synchronisation, so the host path between
+    the decision read and the launch is a single ctypes call)."""
+
+    def __init__(self, nw: int, dim: int, compressed, idx, val, row_ptr, tile_off, params, momentum_buf,
+                 momentum: float, weight_decay: float):
+        require_cuda(params)
+        self._fn = _capi.load().sg_weighted_aggregate_f32
+        self._nw, self._dim = nw, dim
+        self._w = np.zeros(nw, dtype=np.float64)
+        _, self._wp = _capi.weights_ptr(self._w)
+        self._ptrs = (compressed.data_ptr(), idx.data_ptr(), val.data_ptr(), row_ptr.data_ptr(),
+                      tile_off.data_ptr())
+        self._p, self._b = params.data_ptr(), momentum_buf.data_ptr()
+        self._mu, self._wd = float(momentum), float(weight_decay)
+
+    def __call__(self, weights, lr: float, first_step: bool, out: torch.Tensor | None = None) -> None:
+        self._w[:] = weights
+        comp, idx, val, rp, toff = self._ptrs
+        st = self._fn(self._nw, self._wp, comp, None, 0, idx, val, rp, toff, self._dim, _ptr(out), self._p,
+                      self._b, float(lr), self._mu, self._wd, int(bool(first_step)), None, 0, _stream())
+        _capi.check(st, "sg_weighted_aggregate")
+        _count(2)
+
+
 def sgd_momentum(params, momentum_buf, grad, lr, momentum, weight_decay, first_step):
     require_cuda(params)
     lib = _capi.load()

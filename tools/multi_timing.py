@@ -39,14 +39,15 @@ def main():
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     rows = []
-    orig_agg = ex.ops.aggregate
+    from paper_2301_08897_b200 import kernels
 
-    def timed_agg(*a, **k):
+    orig_call = kernels.MergeLauncher.__call__
+
+    def timed_call(self, *a, **k):
         ev[3].record()
-        r = orig_agg(*a, **k)
-        return r
+        return orig_call(self, *a, **k)
 
-    ex.ops.aggregate = timed_agg
+    kernels.MergeLauncher.__call__ = timed_call
     orig_ag = dist.all_gather_into_tensor
 
     def timed_ag(out, inp, group=None):
