@@ -306,7 +306,7 @@ def run_ours(args):
                 "achieved": achieved, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "alg_bytes_per_launch": alg, "avg_launch_us": topk_avg * 1e6}
     # whole-step algorithmic HBM bytes per GPU (SGD fused: 16 B/elem)
-    all_sparse = all(p in ("local", "sparse-allgather") for p in paths) and compression and \
+    all_sparse = all(p in ("local", "sparse-allgather", "sparse-peer") for p in paths) and compression and \
         bool((ex.decision == 1).all().item())
     if compression and all_sparse:
         step_bytes = k * (4 * D + 8 * m) + W * 8 * m + 16 * D

@@ -125,6 +125,28 @@ int sg_weighted_aggregate_f64(int nw, const double* weights, const uint8_t* comp
                               double lr, double momentum, double weight_decay, int first_step,
                               void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Multi-GPU merge over peer memory (one process per GPU, NVLink) -----------------------
+ * The all-sparse case of sg_weighted_aggregate_f32 with fused momentum SGD, where worker j's
+ * payload is addressed by per-worker device pointers that may point into other GPUs' memory
+ * (peer-mapped symmetric buffers): idx_ptrs[j] / val_ptrs[j] hold its m ascending entries and
+ * tile_off_ptrs[j] its [ceil(dim/4096)+1] merge offsets (from sg_topk_gate_f32), so the
+ * payload exchange is fused into the merge (each rank reads the remote entries over NVLink
+ * while it streams its parameters).  The three pointer arrays are HOST arrays of nw <= 16
+ * device pointers; `compressed` is the (local) device array of nw decision bytes and must be
+ * all ones -- the caller checks the decisions first (workers that did not compress are
+ * exchanged densely); with a zero byte the kernel writes nothing.  Replaces the
+ * comm.weighted_aggregate (comm.py:67-78) + nn.sgd_momentum_step (nn.py:161-172) pair of
+ * engine.py:270-283 for the all-compressed iteration. */
+int sg_weighted_aggregate_peers_f32(int nw, const double* weights, const uint8_t* compressed,
+                                    const uint32_t* const* idx_ptrs, const float* const* val_ptrs,
+                                    const int32_t* const* tile_off_ptrs, int64_t dim, float* out,
+                                    float* params, float* momentum_buf, double lr, double momentum,
+                                    double weight_decay, int first_step, void* stream);
+
+/* dst[i * each + b] = src[i][b] for i < nsrc (<= 64 device pointers in a HOST array; peers'
+ * memory allowed): gathers the ranks' decision bytes before the host reads them. */
+int sg_gather_bytes(int nsrc, const uint8_t* const* src, int64_t each, uint8_t* dst, void* stream);
+
 /* ---- Momentum SGD (nn.sgd_momentum_step, nn.py:161-172) -----------------------------------
  * buf = buf*mu; buf = buf + (g + wd*p); p = p - lr*buf, float64 round-to-nearest per element,
  * in place.  first_step != 0 means the lazily created zero buffer (nn.py:167-168). */

@@ -128,8 +128,17 @@ __global__ void k_tile_offsets(const uint32_t* __restrict__ idx, const long long
     }
 }
 
+constexpr int PEER_MAXW = 16;  // workers whose payloads may sit in other GPUs' memory
+
 template <typename TI, typename TO> struct AggArgs {
     double w[MAX_WORKERS];
+    // peer mode (sg_weighted_aggregate_peers_f32): worker j's idx/val/tile offsets are read
+    // through these device pointers (possibly another GPU's memory over NVLink) instead of
+    // idx/val + row_ptr[j] and off + j*(ntiles+1)
+    const uint32_t* idxw[PEER_MAXW];
+    const TI* valw[PEER_MAXW];
+    const int* offw[PEER_MAXW];
+    int peer;
     const uint8_t* comp;
     const TI* dense;
     const uint32_t* idx;
@@ -338,7 +347,7 @@ k_aggregate(const AggArgs<TI, TO> a) {
 // p/buf for the fused momentum-SGD step are loaded first so their latency hides under the
 // fold.
 // ---------------------------------------------------------------------------------------
-constexpr int MP_MAXW = 16;
+constexpr int MP_MAXW = PEER_MAXW;
 constexpr int MG_THREADS = 512;
 constexpr int MG_PER = 8;
 constexpr int MG_ECAP = 4096;
@@ -648,7 +657,8 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
     int* soff = reinterpret_cast<int*>(swk + MW_SLOTS * MW_ECAP);        // [nw][tpb + 1]
     __shared__ int4 s_hdr[MW_SLOTS];  // staged chunk: {tile, c0, entries, last}
     __shared__ __align__(8) unsigned long long fullb[MW_STAGES];
-    __shared__ long long s_rp[MP_MAXW];
+    __shared__ const uint32_t* s_ib[MP_MAXW];  // worker j's entries (local, or a peer GPU's)
+    __shared__ const float* s_vb[MP_MAXW];
     __shared__ int s_ok;
     const int tid = threadIdx.x;
     const int nw = a.nw;
@@ -681,11 +691,14 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
     }
     for (int q = tid; q < nw * (nt + 1); q += MW_THREADS) {
         const int j = q / (nt + 1), i = q - j * (nt + 1);
-        soff[j * sw + i] = a.off[(long long)j * (a.ntiles + 1) + t_begin + i];
+        soff[j * sw + i] = a.peer ? a.offw[j][t_begin + i] : a.off[(long long)j * (a.ntiles + 1) + t_begin + i];
     }
     for (int q = tid; q < AG_TILE; q += MW_THREADS) head[q] = MW_NIL;
     for (int q = tid; q < 2 * AG_TILE / 4; q += MW_THREADS) reinterpret_cast<unsigned*>(mark)[q] = 0u;
-    if (tid < nw) s_rp[tid] = a.row_ptr[tid];
+    if (tid < nw) {
+        s_ib[tid] = a.peer ? a.idxw[tid] : a.idx + a.row_ptr[tid];
+        s_vb[tid] = a.peer ? a.valw[tid] : a.val + a.row_ptr[tid];
+    }
     __syncthreads();
 
     if (tid >= MW_CONS) {
@@ -713,10 +726,12 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
                 for (int j = pw; j < nw; j += MW_PW) {
                     const int pj = __shfl_sync(FULL, cpre, j), nj = __shfl_sync(FULL, ccnt, j);
                     const int lo = pj > cc0 ? pj : cc0, hi = pj + nj < c1 ? pj + nj : c1;
-                    const long long g0 = s_rp[j] + soff[j * sw + ci] - pj;
+                    const long long g0 = soff[j * sw + ci] - pj;
+                    const uint32_t* ib = s_ib[j];
+                    const float* vb = s_vb[j];
                     for (int e = lo + lane; e < hi; e += 32) {
-                        cp_async4(sidx + slot * MW_ECAP + (e - cc0), a.idx + g0 + e);
-                        cp_async4(sval + slot * MW_ECAP + (e - cc0), a.val + g0 + e);
+                        cp_async4(sidx + slot * MW_ECAP + (e - cc0), ib + g0 + e);
+                        cp_async4(sval + slot * MW_ECAP + (e - cc0), vb + g0 + e);
                         swk[slot * MW_ECAP + (e - cc0)] = (uint8_t)j;
                     }
                 }
@@ -937,6 +952,7 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
     a.nw = nw;
     a.first = first;
     a.pipe = 0;
+    a.peer = 0;
     bool vec = true;
     if (dense) vec = vec && reinterpret_cast<size_t>(dense) % 16 == 0 && (ld * (long long)sizeof(TI)) % 16 == 0;
     if (out) vec = vec && reinterpret_cast<size_t>(out) % 16 == 0;
@@ -981,6 +997,62 @@ int sgd(T* p, T* buf, const T* g, long long dim, double lr, double mu, double wd
     if (blocks < 1) blocks = 1;
     launch_pdl(k_sgd<T>, dim3((unsigned)blocks), dim3(256), 0, stream, p, buf, g, dim, lr, mu, wd, first, vec_ok);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+// Merge + fused SGD over workers whose payloads are addressed per worker (peer GPUs).
+int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const uint32_t* const* idx_ptrs,
+                    const float* const* val_ptrs, const int32_t* const* off_ptrs, long long dim, float* out,
+                    float* p, float* buf, double lr, double mu, double wd, int first, cudaStream_t stream) {
+    if (nw < 1 || dim < 1 || !weights || !comp || !idx_ptrs || !val_ptrs || !off_ptrs || !p || !buf)
+        return SG_ERR_INVALID;
+    if (nw > PEER_MAXW || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
+    if (reinterpret_cast<size_t>(p) % 16 || reinterpret_cast<size_t>(buf) % 16 ||
+        (out && reinterpret_cast<size_t>(out) % 16))
+        return SG_ERR_UNSUPPORTED;
+    const long long ntiles = ag_tiles(dim);
+    AggArgs<float, float> a = {};
+    for (int j = 0; j < nw; ++j) {
+        if (!idx_ptrs[j] || !val_ptrs[j] || !off_ptrs[j]) return SG_ERR_INVALID;
+        a.w[j] = weights[j];
+        a.idxw[j] = idx_ptrs[j];
+        a.valw[j] = val_ptrs[j];
+        a.offw[j] = off_ptrs[j];
+    }
+    a.peer = 1;
+    a.comp = comp;
+    a.out = out;
+    a.p = p;
+    a.buf = buf;
+    a.dim = dim;
+    a.ntiles = ntiles;
+    a.lr = lr;
+    a.mu = mu;
+    a.wd = wd;
+    a.nw = nw;
+    a.first = first;
+    a.vec_ok = 1;
+    a.pipe = 1;
+    const int sms = num_sms();
+    const size_t budget = 227 * 1024 - 1024;
+    const int tpb_max = (int)((budget - mw_smem_bytes(0)) / (MP_MAXW * sizeof(int)));
+    int tpb = (int)((ntiles + sms - 1) / sms);
+    if (tpb > tpb_max) tpb = tpb_max;
+    const size_t sm = mw_smem_bytes(tpb);
+    cudaFuncSetAttribute(k_merge_ws<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_pdl(k_merge_ws<float>, dim3((unsigned)((ntiles + tpb - 1) / tpb)), dim3(MW_THREADS), sm, stream, a, tpb);
+    debug_sync("k_merge_ws(peers)", stream);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+struct GatherSrc {
+    const uint8_t* p[MAX_WORKERS];
+};
+
+__global__ void k_gather_bytes(GatherSrc src, int nsrc, long long each, uint8_t* __restrict__ dst) {
+    pdl_enter();
+    const long long n = (long long)nsrc * each;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = src.p[i / each][i % each];
 }
 
 }  // namespace sg
@@ -1030,6 +1102,29 @@ int sg_sgd_momentum_f64(double* params, double* momentum_buf, const double* grad
                         void* stream) {
     return sgd<double>(params, momentum_buf, grad, dim, lr, momentum, weight_decay, first_step,
                        (cudaStream_t)stream);
+}
+
+int sg_weighted_aggregate_peers_f32(int nw, const double* weights, const uint8_t* compressed,
+                                    const uint32_t* const* idx_ptrs, const float* const* val_ptrs,
+                                    const int32_t* const* tile_off_ptrs, int64_t dim, float* out,
+                                    float* params, float* momentum_buf, double lr, double momentum,
+                                    double weight_decay, int first_step, void* stream) {
+    return aggregate_peers(nw, weights, compressed, idx_ptrs, val_ptrs, tile_off_ptrs, dim, out, params,
+                           momentum_buf, lr, momentum, weight_decay, first_step, (cudaStream_t)stream);
+}
+
+int sg_gather_bytes(int nsrc, const uint8_t* const* src, int64_t each, uint8_t* dst, void* stream) {
+    if (nsrc < 1 || nsrc > MAX_WORKERS || each < 1 || !src || !dst) return SG_ERR_INVALID;
+    GatherSrc g;
+    for (int i = 0; i < nsrc; ++i) {
+        if (!src[i]) return SG_ERR_INVALID;
+        g.p[i] = src[i];
+    }
+    const long long n = (long long)nsrc * each;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 1024) blocks = 1024;
+    launch_pdl(k_gather_bytes, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream, g, nsrc, (long long)each, dst);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
 }  // extern "C"

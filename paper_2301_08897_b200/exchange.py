@@ -29,6 +29,7 @@ exercised with the gloo backend on CPU in tests; the product constructs it with
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -133,7 +134,22 @@ class GradientExchange:
                 dw = (k + 15) // 16 * 4
                 words = (dw + 2 * k * m + k * nt1 + 3) // 4 * 4
                 self.pack_words, self.pack_dw = words, dw
-                self.pack = torch.zeros(words, dtype=torch.int32, **z)
+                self._symm = None
+                if device.type == "cuda" and os.environ.get("SG_P2P", "1") != "0":
+                    # symmetric (peer-mapped) send buffer: the merge reads the other ranks'
+                    # payloads in place over NVLink instead of an all-gather
+                    try:
+                        import torch.distributed._symmetric_memory as symm_mem
+
+                        pack = symm_mem.empty(words, dtype=torch.int32, device=device)
+                        pack.zero_()
+                        grp = group if group is not None else dist.group.WORLD
+                        self._symm = symm_mem.rendezvous(pack, grp.group_name)
+                        self.pack = pack
+                    except Exception:  # no peer mapping on this system: NCCL all-gather path
+                        self._symm = None
+                if self._symm is None:
+                    self.pack = torch.zeros(words, dtype=torch.int32, **z)
                 self.decision = self.pack[:dw].view(torch.uint8)[:k]
                 self.idx = self.pack[dw:dw + k * m].view(k, m)
                 self.val = self.pack[dw + k * m:dw + 2 * k * m].view(torch.float32).view(k, m)
@@ -146,7 +162,20 @@ class GradientExchange:
             self.norms2 = torch.empty((k, 2), dtype=torch.float64, **z)
             self.rho = torch.empty(k, dtype=torch.float64, **z)
             self.row_ptr_local = torch.arange(0, (k + 1) * m, m, dtype=torch.int64, **z)
-            if self.packed:
+            if self.packed and self._symm is not None:
+                P, words, dw = self.world, self.pack_words, self.pack_dw
+                off0 = self.pack.data_ptr() - self._symm.buffer_ptrs[self.rank]
+                bases = [self._symm.buffer_ptrs[r] + off0 for r in range(P)]  # rank r's pack
+                self._dec_ptrs = bases
+                idx_p = [b + 4 * (dw + j * m) for b in bases for j in range(k)]
+                val_p = [b + 4 * (dw + k * m + j * m) for b in bases for j in range(k)]
+                off_p = [b + 4 * (dw + 2 * k * m + j * nt1) for b in bases for j in range(k)]
+                self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
+                self._dec_host = torch.empty(self.W, dtype=torch.uint8, pin_memory=True)
+                self._dec_ready = torch.cuda.Event()
+                self._peer_merge = kernels.PeerMergeLauncher(dim, self.dec_all, idx_p, val_p, off_p, self.params,
+                                                             self.momentum_buf, momentum, weight_decay)
+            elif self.packed:
                 P, words, dw = self.world, self.pack_words, self.pack_dw
                 self.pack_all = torch.empty(P * words, dtype=torch.int32, **z)
                 rows = self.pack_all.view(P, words)
@@ -224,6 +253,23 @@ class GradientExchange:
     def _exchange(self, w, out, opt) -> str:
         g = self.group
         dim = self.dim
+        if self.packed and self._symm is not None:
+            # Peer path: every rank's Top-k wrote its symmetric send buffer; after a device-side
+            # barrier the W decision bytes are gathered (the step's one host read) and the merge
+            # streams the other ranks' payloads over NVLink in place.  A second barrier keeps
+            # the next step's Top-k from overwriting a buffer a peer is still reading.
+            self._symm.barrier(channel=0)
+            kernels.gather_bytes(self._dec_ptrs, self.k, self.dec_all)
+            self._dec_host.copy_(self.dec_all, non_blocking=True)
+            self._dec_ready.record()
+            self._dec_ready.synchronize()
+            if bool(self._dec_host.numpy().min() == 1):
+                self._peer_merge(w, opt["lr"], opt["first_step"], out)
+                self._symm.barrier(channel=0)
+                return "sparse-peer"
+            path = self._dense_exchange(w, out, opt)
+            self._symm.barrier(channel=0)
+            return path
         if self.packed:
             # one all-gather carries every rank's decisions, payloads and merge offsets; the
             # decisions and offsets are regrouped contiguously on device before the host
@@ -267,6 +313,12 @@ class GradientExchange:
             self.ops.aggregate(w, dim, compressed=self.dec_all, idx=self.idx_all, val=self.val_all,
                                row_ptr=self.row_ptr_all, tile_off=self.tile_off_all, out=out, **opt)
             return "sparse-allgather"
+        return self._dense_exchange(w, out, opt)
+
+    def _dense_exchange(self, w, out, opt) -> str:
+        """Mixed decisions: local partial (dense rows + local payloads), all-reduce, SGD."""
+        g = self.group
+        dim = self.dim
         wl = w[self.lo:self.lo + self.k]
         if self.compression:
             self.ops.aggregate(wl, dim, compressed=self.decision, dense=self.bucket, idx=self.idx,

@@ -7,6 +7,8 @@ no CPU path.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -231,6 +233,41 @@ class MergeLauncher:
                       self._b, float(lr), self._mu, self._wd, int(bool(first_step)), None, 0, _stream())
         _capi.check(st, "sg_weighted_aggregate")
         _count(2)
+
+
+class PeerMergeLauncher:
+    """sg_weighted_aggregate_peers_f32 with every pointer bound once: worker j's payload and
+    merge offsets are read through raw device addresses (other GPUs' symmetric buffers)."""
+
+    def __init__(self, dim: int, compressed: torch.Tensor, idx_ptrs, val_ptrs, off_ptrs, params, momentum_buf,
+                 momentum: float, weight_decay: float):
+        require_cuda(params)
+        nw = len(idx_ptrs)
+        self._fn = _capi.load().sg_weighted_aggregate_peers_f32
+        self._nw, self._dim = nw, dim
+        self._w = np.zeros(nw, dtype=np.float64)
+        _, self._wp = _capi.weights_ptr(self._w)
+        arr = ctypes.c_void_p * nw
+        self._ip, self._vp, self._op = arr(*idx_ptrs), arr(*val_ptrs), arr(*off_ptrs)
+        self._comp = compressed.data_ptr()
+        self._p, self._b = params.data_ptr(), momentum_buf.data_ptr()
+        self._mu, self._wd = float(momentum), float(weight_decay)
+
+    def __call__(self, weights, lr: float, first_step: bool, out: torch.Tensor | None = None) -> None:
+        self._w[:] = weights
+        st = self._fn(self._nw, self._wp, self._comp, self._ip, self._vp, self._op, self._dim, _ptr(out),
+                      self._p, self._b, float(lr), self._mu, self._wd, int(bool(first_step)), _stream())
+        _capi.check(st, "sg_weighted_aggregate_peers_f32")
+        _count(1)
+
+
+def gather_bytes(src_ptrs, each: int, dst: torch.Tensor) -> None:
+    """dst[i*each:(i+1)*each] = bytes at device address src_ptrs[i] (peers' memory allowed)."""
+    require_cuda(dst)
+    arr = (ctypes.c_void_p * len(src_ptrs))(*src_ptrs)
+    _capi.check(_capi.load().sg_gather_bytes(len(src_ptrs), arr, int(each), dst.data_ptr(), _stream()),
+                "sg_gather_bytes")
+    _count(1)
 
 
 def sgd_momentum(params, momentum_buf, grad, lr, momentum, weight_decay, first_step):

@@ -104,10 +104,15 @@ def test_multi_gpu_exchange_matches_single_gpu(cuda):
 
     from conftest import ROOT
 
+    import os
+
     n = 4 if torch.cuda.device_count() >= 4 else 2
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29533", str(ROOT / "tools" / "multi_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
-    assert rep["ok"] and rep["world"] == n
+    # peer path (symmetric buffers read in place by the merge) and the NCCL all-gather path
+    for p2p, sparse_path in (("1", "sparse-peer"), ("0", "sparse-allgather")):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", "--master-port", "2953" + p2p, str(ROOT / "tools" / "multi_check.py")]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "SG_P2P": p2p})
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+        assert rep["ok"] and rep["world"] == n
+        assert rep["cases"][0]["paths"] == [sparse_path] * 3, rep["cases"][0]

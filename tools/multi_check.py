@@ -64,7 +64,7 @@ def main():
         case = {"family": family, "paths": paths, "ranks_identical": same}
         if rank == 0:
             p1, a1, paths1 = run(family, cr, delta, None, dev)
-            if paths[-1] == "sparse-allgather":
+            if paths[-1] in ("sparse-allgather", "sparse-peer"):
                 case["bit_identical_to_1gpu"] = bool(np.array_equal(p, p1) and np.array_equal(a, a1))
                 ok &= case["bit_identical_to_1gpu"]
             else:

@@ -41,33 +41,29 @@ def main():
     rows = []
     from paper_2301_08897_b200 import kernels
 
-    orig_call = kernels.MergeLauncher.__call__
+    # ev0 step start | ev1 Top-k done | ev2 right before the merge launch | ev3 merge done
+    for cls in (kernels.MergeLauncher, kernels.PeerMergeLauncher):
+        orig = cls.__call__
 
-    def timed_call(self, *a, **k):
-        ev[3].record()
-        return orig_call(self, *a, **k)
+        def timed(self, *a, _orig=orig, **k):
+            ev[2].record()
+            r = _orig(self, *a, **k)
+            ev[3].record()
+            return r
 
-    kernels.MergeLauncher.__call__ = timed_call
-    orig_ag = dist.all_gather_into_tensor
-
-    def timed_ag(out, inp, group=None):
-        ev[1].record()
-        r = orig_ag(out, inp, group=group)
-        ev[2].record()
-        return r
-
-    dist.all_gather_into_tensor = timed_ag
+        cls.__call__ = timed
     for _ in range(10):
         dist.barrier()
         torch.cuda.synchronize()
         ev[0].record()
-        ex.step(w, 0.01)
+        info = ex.step(w, 0.01, topk_events=(torch.cuda.Event(), ev[1]))
         ev[4].record()
         torch.cuda.synchronize()
         rows.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
                      ev[3].elapsed_time(ev[4]), ev[0].elapsed_time(ev[4])])
     med = np.median(np.array(rows), axis=0) * 1000
-    rep = dict(rank=rank, topk_us=med[0], allgather_us=med[1], check_gap_us=med[2], merge_us=med[3], step_us=med[4])
+    rep = dict(rank=rank, path=info.path, topk_us=med[0], exchange_and_check_us=med[1], merge_us=med[2],
+               tail_us=med[3], step_us=med[4])
     print(json.dumps({k: (round(v, 1) if isinstance(v, float) else v) for k, v in rep.items()}), flush=True)
     dist.destroy_process_group()
 
