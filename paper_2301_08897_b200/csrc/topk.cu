@@ -206,6 +206,53 @@ SG_DEV void find_bin_from_top(const unsigned* hist, unsigned long long rank, int
     above = __shfl_sync(FULL, a, f);
 }
 
+// Block-cooperative version (every thread calls it; the result is broadcast): thread t owns
+// the NB/THREADS bins below NB-1-(NB/THREADS)*t; one block scan of the per-thread sums from
+// the top locates the bin, two barriers instead of a one-warp serial walk.
+template <int NB, int THREADS>
+SG_DEV void block_find_bin_from_top(const unsigned* hist, unsigned long long rank, int& bin,
+                                    unsigned long long& above) {
+    constexpr int PER = NB / THREADS;
+    static_assert(PER >= 1 && NB % THREADS == 0, "bins per thread");
+    __shared__ unsigned long long s_wsum[THREADS / 32];
+    __shared__ int s_bin;
+    __shared__ unsigned long long s_above;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int top = NB - 1 - PER * tid;
+    unsigned long long s = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) s += hist[top - i];
+    unsigned long long incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    if (tid == 0) s_bin = -1;
+    __syncthreads();
+    unsigned long long wb = 0;
+    for (int i = 0; i < warp; ++i) wb += s_wsum[i];
+    incl += wb;
+    const unsigned long long ex = incl - s;
+    if (ex < rank && incl >= rank) {  // exactly one thread holds the rank
+        unsigned long long cum = ex;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const unsigned h = hist[top - i];
+            if (cum + h >= rank) {
+                s_bin = top - i;
+                s_above = cum;
+                break;
+            }
+            cum += h;
+        }
+    }
+    __syncthreads();
+    bin = s_bin;
+    above = s_above;
+}
+
 template <typename K> SG_DEV int digit_shift(K span, int bits) {
     const int bl = bitlen<K>(span);
     return bl > bits ? bl - bits : 0;
@@ -266,17 +313,15 @@ SG_DEV void block_select(const K* keys, long long n, SelState<K>& st, unsigned* 
             if (key >= lo && key - lo <= span) atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
         }
         __syncthreads();
-        if (tid < 32) {
-            int bin;
-            unsigned long long above;
-            find_bin_from_top<SEL_BINS>(hist, st.rank, bin, above);
-            if (tid == 0) {
-                if (bin < 0) {
-                    st.done = 1;  // inconsistent counts (cannot happen): keep the lowest key
-                    st.T = st.lo;
-                } else {
-                    narrow<K>(st, bin, above, hist[bin], SEL_BINS, SEL_BITS);
-                }
+        int bin;
+        unsigned long long above;
+        block_find_bin_from_top<SEL_BINS, THREADS>(hist, st.rank, bin, above);
+        if (tid == 0) {
+            if (bin < 0) {
+                st.done = 1;  // inconsistent counts (cannot happen): keep the lowest key
+                st.T = st.lo;
+            } else {
+                narrow<K>(st, bin, above, hist[bin], SEL_BINS, SEL_BITS);
             }
         }
     }
@@ -454,15 +499,15 @@ k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf
         for (long long i = tid; i < ns; i += EST_THREADS) atomicAdd(&hist[digit<K>(sk[i], lo, shift, SEL_BINS)], 1u);
     }
     __syncthreads();
-    if (warp == 0) {
-        K est = 0;
-        if (r_est <= ns) {
-            int bin;
-            unsigned long long above;
-            find_bin_from_top<SEL_BINS>(hist, (unsigned long long)r_est, bin, above);
-            est = bin < 0 ? (K)0 : lo + ((K)bin << shift);
-        }
-        if (lane == 0) {
+    K est = 0;
+    if (r_est <= ns) {  // uniform
+        int bin;
+        unsigned long long above;
+        block_find_bin_from_top<SEL_BINS, EST_THREADS>(hist, (unsigned long long)r_est, bin, above);
+        est = bin < 0 ? (K)0 : lo + ((K)bin << shift);
+    }
+    {
+        if (tid == 0) {
             SelState<K> o{};
             o.smax = s_lo + s_span;
             o.est = est;
@@ -572,35 +617,33 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
     __threadfence();
     for (int i = tid; i < H0_BINS; i += blockDim.x) hist[i] = __ldcg(gh + i);
     __syncthreads();
-    if (warp == 0) {
-        SelState<K> s = *stp;
-        const unsigned long long C = __ldcg(a.count + (long long)a.pass * a.k + w);
-        const K maxk = __ldcg(a.maxkey + w);
-        if (C < (unsigned long long)a.m) {
-            if (lane == 0) {  // estimate undershot (pass 0 only): run the fallback pass
-                s.mode = MODE_FALLBACK;
-                *stp = s;
-            }
-        } else {
-            s.lo = est;
-            s.span = maxk - est;
-            s.shift = shift0;
-            s.rank = (unsigned long long)a.m;
-            s.done = 0;
-            if (a.pass == 1) s.est = 0;
-            int bin;
-            unsigned long long above;
-            find_bin_from_top<H0_BINS>(hist, s.rank, bin, above);
-            if (lane == 0) {
-                if (bin < 0) {
-                    s.done = 1;
-                    s.T = est;
-                } else {
-                    narrow<K>(s, bin, above, hist[bin], H0_BINS, SEL_BITS);
-                }
-                *stp = s;
-            }
+    const unsigned long long C = __ldcg(a.count + (long long)a.pass * a.k + w);
+    if (C < (unsigned long long)a.m) {
+        if (tid == 0) {  // estimate undershot (pass 0 only): run the fallback pass
+            SelState<K> s = *stp;
+            s.mode = MODE_FALLBACK;
+            *stp = s;
         }
+        return;
+    }
+    int bin;
+    unsigned long long above;
+    block_find_bin_from_top<H0_BINS, TK_THREADS>(hist, (unsigned long long)a.m, bin, above);
+    if (tid == 0) {
+        SelState<K> s = *stp;
+        s.lo = est;
+        s.span = __ldcg(a.maxkey + w) - est;
+        s.shift = shift0;
+        s.rank = (unsigned long long)a.m;
+        s.done = 0;
+        if (a.pass == 1) s.est = 0;
+        if (bin < 0) {
+            s.done = 1;
+            s.T = est;
+        } else {
+            narrow<K>(s, bin, above, hist[bin], H0_BINS, SEL_BITS);
+        }
+        *stp = s;
     }
 }
 
@@ -1016,11 +1059,20 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
     __shared__ unsigned s_eq, s_res[2];
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef SG_PHASES
+    long long ph[8];
+    int nph = 0;
+    ph[nph++] = clock64();
+#define SG_PH() do { __syncthreads(); if (nph < 8) ph[nph++] = clock64(); } while (0)
+#else
+#define SG_PH() do {} while (0)
+#endif
     K* sk = reinterpret_cast<K*>(smem_raw);
     uint32_t* si = reinterpret_cast<uint32_t*>(sk + RES);
     uint32_t* sp = si + RES;                               // position in the segment list
     unsigned* kb = sp + RES;                               // [nsub]
-    uint8_t* sf = reinterpret_cast<uint8_t*>(kb + NSUB_MAX);
+    unsigned* sc = kb + NSUB_MAX;                          // [nseg] segment candidate counts
+    uint8_t* sf = reinterpret_cast<uint8_t*>(sc + BMAX);
     const K* bk = a.bkey + (long long)w * a.cap;
     const uint32_t* bi = a.bidx + (long long)w * a.cap;
     const uint32_t* bpp = a.bpos + (long long)w * a.cap;
@@ -1030,11 +1082,14 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
         sp[i] = bpp[i];
     }
     for (int i = tid; i < a.nsub; i += NT) kb[i] = a.seggt[(long long)w * a.nsub + i];
+    for (int i = tid; i < a.nseg; i += NT) sc[i] = a.segcnt[(long long)w * a.nseg + i];
     if (tid == 0) {
         sst = a.sel[w];
         s_eq = 0;
     }
+    SG_PH();
     block_select<K, NT>(sk, (long long)h, sst, hist);
+    SG_PH();
     const K T_ = sst.T;
     const unsigned long long need = sst.rank;
     // ties at T: keep the `need` lowest indices among keys == T
@@ -1047,41 +1102,76 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
     atomicAdd(&s_eq, eqc);
     __syncthreads();
     unsigned cut = 0xffffffffu;
-    if ((unsigned long long)s_eq > need) cut = block_select_small_u32<NT>(si, sf, (long long)h, need, hist, s_res);
+    if ((unsigned long long)s_eq > need) {
+        if (s_eq <= (unsigned)SEL_BINS) {
+            // a small tie group: list its indices, and the cut is the one with need-1 smaller
+            // (indices are distinct positions)
+            __shared__ unsigned s_tn, s_cut;
+            if (tid == 0) s_tn = 0;
+            __syncthreads();
+            for (long long i = tid; i < (long long)h; i += NT)
+                if (sf[i]) hist[atomicAdd(&s_tn, 1u)] = si[i];
+            __syncthreads();
+            const unsigned n = s_tn;
+            for (unsigned j = tid; j < n; j += NT) {
+                const unsigned x = hist[j];
+                unsigned c = 0;
+                for (unsigned q = 0; q < n; ++q) c += hist[q] < x;
+                if (c == (unsigned)need - 1u) s_cut = x;
+            }
+            __syncthreads();
+            cut = s_cut;
+        } else {
+            cut = block_select_small_u32<NT>(si, sf, (long long)h, need, hist, s_res);
+        }
+    }
     __syncthreads();
+    SG_PH();
     // kept boundary entries per segment
     for (long long i = tid; i < (long long)h; i += NT) {
         const K key = sk[i];
         if (key > T_ || (key == T_ && si[i] <= cut)) {
             const int seg = (int)((si[i] / TILE) / a.tps);
-            const long long nsc = a.segcnt[(long long)w * a.nseg + seg];
-            atomicAdd(&kb[seg * a.split + sub_of(nsc, sp[i], a.split)], 1u);
+            atomicAdd(&kb[seg * a.split + sub_of((long long)sc[seg], sp[i], a.split)], 1u);
         }
     }
     __syncthreads();
-    if (warp == 0) {
-        // exclusive scan over sub-ranges of (count above the bin + kept boundary)
-        unsigned carry = 0;
-        for (int s0 = 0; s0 < a.nsub; s0 += 32) {
-            const int s = s0 + lane;
-            const unsigned v = s < a.nsub ? kb[s] : 0u;
-            unsigned incl = v;
+    SG_PH();
+    // exclusive scan over sub-ranges of (count above the bin + kept boundary): thread t owns
+    // sub-ranges 2t, 2t+1 (nsub <= NSUB_MAX = 2 * NT)
+    {
+        __shared__ unsigned s_ws[NT / 32];
+        const int s0 = 2 * tid;
+        const unsigned v0 = s0 < a.nsub ? kb[s0] : 0u, v1 = s0 + 1 < a.nsub ? kb[s0 + 1] : 0u;
+        const unsigned v = v0 + v1;
+        unsigned incl = v;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (s < a.nsub) a.segbase[(long long)w * a.nsub + s] = carry + incl - v;
-            carry += __shfl_sync(FULL, incl, 31);
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
         }
-        if (lane == 0) {
-            SelState<K> s = sst;
-            s.idx_cut = cut;
-            s.wmode = WR_FAST;
-            s.done = 1;
-            a.sel[w] = s;
-        }
+        if (lane == 31) s_ws[warp] = incl;
+        __syncthreads();
+        unsigned wb = 0;
+        for (int i = 0; i < warp; ++i) wb += s_ws[i];
+        const unsigned ex = wb + incl - v;
+        if (s0 < a.nsub) a.segbase[(long long)w * a.nsub + s0] = ex;
+        if (s0 + 1 < a.nsub) a.segbase[(long long)w * a.nsub + s0 + 1] = ex + v0;
     }
+    if (tid == 0) {
+        SelState<K> s = sst;
+        s.idx_cut = cut;
+        s.wmode = WR_FAST;
+        s.done = 1;
+        a.sel[w] = s;
+    }
+#ifdef SG_PHASES
+    SG_PH();
+    if (tid == 0 && w == 0)
+        printf("[resolve w0 h=%llu eq=%u nsub=%d] load %lld select %lld ties %lld kept %lld scan %lld cycles\n", h, s_eq,
+               a.nsub, ph[1] - ph[0], ph[2] - ph[1], ph[3] - ph[2], ph[4] - ph[3], ph[5] - ph[4]);
+#endif
+#undef SG_PH
 }
 
 // --------------------------------------------------------------------------------------
@@ -1130,19 +1220,14 @@ k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
     constexpr int RES = TopkTraits<T>::RES;
     constexpr int NT = 1024;
     __shared__ unsigned hist[SEL_BINS];
-    __shared__ int s_any;
     __shared__ SelState<K> st;
     const int x = blockIdx.x, w = blockIdx.y, tid = threadIdx.x;
-    if (tid == 0) {
-        int any = 0;
-        for (int j = 0; j < (int)gridDim.y; ++j) any |= a.bndn[j] > (unsigned long long)RES;
-        s_any = any;
-    }
-    __syncthreads();
+    // any oversized boundary? (every CTA reaches the same answer)
+    const bool any = __syncthreads_or(tid < (int)gridDim.y && a.bndn[tid] > (unsigned long long)RES);
     const unsigned long long h = a.bndn[w];
     const bool slow = h > (unsigned long long)RES;
     if (x == 0 && !slow) resolve_small<T>(a, w, h, hist);
-    if (!s_any) return;  // uniform over the grid
+    if (!any) return;  // uniform over the grid
     // slow mode: radix rounds over the oversized boundary sets
     const unsigned nblocks = gridDim.x * gridDim.y;
     unsigned gen = 0;
@@ -1266,12 +1351,17 @@ template <typename T>
 __global__ void __launch_bounds__(TK_THREADS) k_finish(WriteArgs<T> a) {
     pdl_enter();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // all partials in one parallel round trip, then fixed-order sums from shared memory
+    extern __shared__ __align__(16) unsigned char fin_smem[];
+    double* pm = reinterpret_cast<double*>(fin_smem);  // [k][nseg]
+    double* pw = pm + (size_t)a.k * a.nseg;            // [k][nsub]
+    for (int i = tid; i < a.k * a.nseg; i += TK_THREADS) pm[i] = __ldcg(a.pmain + i);
+    for (int i = tid; i < a.k * a.nsub; i += TK_THREADS) pw[i] = __ldcg(a.pwrite + i);
+    __syncthreads();
     for (int ww = warp; ww < a.k; ww += TK_NW) {
         double sf = 0.0, sk = 0.0;
-        for (int i = lane; i < a.nseg; i += 32) {
-            sf = dadd(sf, __ldcg(a.pmain + (long long)ww * a.nseg + i));
-        }
-        for (int i = lane; i < a.nsub; i += 32) sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nsub + i));
+        for (int i = lane; i < a.nseg; i += 32) sf = dadd(sf, pm[(long long)ww * a.nseg + i]);
+        for (int i = lane; i < a.nsub; i += 32) sk = dadd(sk, pw[(long long)ww * a.nsub + i]);
         sf = warp_sum(sf);
         sk = warp_sum(sk);
         if (lane == 0) {
@@ -1780,7 +1870,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     launch_pdl(k_collect<T>, dim3(subgrid), dim3(TK_THREADS), 0, stream, ca);
     debug_sync("k_collect", stream);
     // 4. resolve: in-CTA for the normal boundary, cooperative radix rounds for oversized ones
-    const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES + sizeof(unsigned) * NSUB_MAX;
+    const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES + sizeof(unsigned) * (NSUB_MAX + BMAX);
     cudaFuncSetAttribute(k_resolve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem);
     ResolveArgs<T> ra;
     ra.sel = sel;
@@ -1822,7 +1912,9 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     cudaFuncSetAttribute(k_write<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wr_smem);
     launch_pdl(k_write<T>, dim3(subgrid), dim3(TK_THREADS), wr_smem, stream, wa);
     debug_sync("k_write", stream);
-    launch_pdl(k_finish<T>, dim3(1), dim3(TK_THREADS), 0, stream, wa);
+    const size_t fin_smem = sizeof(double) * (size_t)k * (p.nseg + p.nsub);
+    cudaFuncSetAttribute(k_finish<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem);
+    launch_pdl(k_finish<T>, dim3(1), dim3(TK_THREADS), fin_smem, stream, wa);
     debug_sync("k_finish", stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
