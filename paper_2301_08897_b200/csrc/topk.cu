@@ -730,13 +730,16 @@ k_main_tma(MainArgs<float> a) {
         }
         if (lane == 31) s_wtot[warp] = incl;
         __syncthreads();
-        unsigned woff = 0, total = 0;
+        // this warp's offset and the tile total: a shuffle scan over the TK_NW warp totals
+        const unsigned wt = lane < TK_NW ? s_wtot[lane] : 0u;
+        unsigned wi = wt;
 #pragma unroll
-        for (int j = 0; j < TK_NW; ++j) {
-            const unsigned t = s_wtot[j];
-            woff += j < warp ? t : 0u;
-            total += t;
+        for (int o = 1; o < TK_NW; o <<= 1) {
+            const unsigned y = __shfl_up_sync(FULL, wi, o);
+            if (lane >= o) wi += y;
         }
+        const unsigned woff = __shfl_sync(FULL, wi - wt, warp);
+        const unsigned total = __shfl_sync(FULL, wi, TK_NW - 1);
         if (M) place(M, base, src, n, incl, woff);
         if (tid == 0) {
             const long long ti = (long long)w * a.ntiles + tile;
@@ -745,12 +748,13 @@ k_main_tma(MainArgs<float> a) {
         }
         run += total;
     };
+    int s = 0;
+    unsigned phase = 0;  // ring stage of tile i and its mbarrier parity, advanced incrementally
     for (int i = 0; i < nfull; ++i) {
         const long long tile = t_begin + i;
         const long long base = tile * MN_TILE;
-        const int s = i % MN_STAGES;
         const float* tb = ring + s * MN_TILE;
-        mbar_wait(&full[s], (unsigned)(i / MN_STAGES) & 1u);
+        mbar_wait(&full[s], phase);
         const float4* t4 = reinterpret_cast<const float4*>(tb);
         float4 y[4];
 #pragma unroll
@@ -775,6 +779,10 @@ k_main_tma(MainArgs<float> a) {
         if (tid == 0 && i + MN_STAGES < ntl) {
             fence_proxy_async();
             issue(i + MN_STAGES);
+        }
+        if (++s == MN_STAGES) {
+            s = 0;
+            phase ^= 1u;
         }
     }
     if (nfull < ntl) {  // partial last tile of the row: direct loads, bounds-checked
