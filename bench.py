@@ -276,12 +276,12 @@ def run_ours(args):
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     launches0 = kernels.LAUNCHES["n"]
-    paths = []
+    infos = []
     s_ev.record()
     for i in range(K):
-        info = ex.step(w, lr, topk_events=ev_topk[i] if compression else None)
-        paths.append(info.path)
+        infos.append(ex.step(w, lr, topk_events=ev_topk[i] if compression else None))
     e_ev.record()
+    paths = [info.path for info in infos]  # (read after the timed region: may wait for decisions)
     barrier()
     launches = kernels.LAUNCHES["n"] - launches0
     t_ms = reduce_max(s_ev.elapsed_time(e_ev))

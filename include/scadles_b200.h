@@ -143,6 +143,23 @@ int sg_weighted_aggregate_peers_f32(int nw, const double* weights, const uint8_t
                                     float* params, float* momentum_buf, double lr, double momentum,
                                     double weight_decay, int first_step, void* stream);
 
+/* The dense side of a mixed multi-GPU step, enqueued unconditionally and guarded on the
+ * gathered decisions `guard[0..guard_n)` (device bytes): a no-op unless some worker did not
+ * compress.  sg_weighted_partial_f32 folds this rank's workers (dense rows or payloads, the
+ * sg_weighted_aggregate_f32 argument meaning) into `out` (the rank's partial, float32);
+ * sg_peer_reduce_sgd_f32 sums the nranks partials (HOST array of device pointers, peers'
+ * memory allowed, 16-byte aligned) in ascending rank order in float64 and applies momentum
+ * SGD (nn.py:161-172), writing the aggregate to `out` if non-NULL.  Together they replace the
+ * partial + all-reduce + SGD of engine.py:270-283 when decisions are mixed, without a host
+ * read of the decisions. */
+int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compressed, const float* dense,
+                            int64_t ld_dense, const uint32_t* idx, const float* val, const int64_t* row_ptr,
+                            const int32_t* tile_off, int64_t dim, float* out, const uint8_t* guard,
+                            int guard_n, void* workspace, size_t workspace_bytes, void* stream);
+int sg_peer_reduce_sgd_f32(int nranks, const float* const* partials, const uint8_t* guard, int guard_n,
+                           int64_t dim, float* out, float* params, float* momentum_buf, double lr,
+                           double momentum, double weight_decay, int first_step, void* stream);
+
 /* dst[i * each + b] = src[i][b] for i < nsrc (<= 64 device pointers in a HOST array; peers'
  * memory allowed): gathers the ranks' decision bytes before the host reads them. */
 int sg_gather_bytes(int nsrc, const uint8_t* const* src, int64_t each, uint8_t* dst, void* stream);

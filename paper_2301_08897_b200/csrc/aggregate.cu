@@ -152,6 +152,10 @@ template <typename TI, typename TO> struct AggArgs {
     double lr, mu, wd;
     int nw, first, vec_ok;
     int pipe;  // k_merge_ws owns all-sparse calls: k_merge then exits
+    // device-side guard on a decision array (multi-GPU steps enqueue both exchange paths):
+    // guard_mode 1 = run only if every guard byte is non-zero, 2 = only if some byte is zero
+    const uint8_t* guard;
+    int guard_n, guard_mode;
 };
 
 template <typename TI, typename TO>
@@ -371,6 +375,11 @@ k_merge(const AggArgs<float, TO> a) {
     if (tid == 0) {
         int all = a.pipe && a.nw <= MP_MAXW;
         for (int j = 0; j < a.nw && all; ++j) all = a.comp && a.comp[j] != 0;
+        if (a.guard_mode) {
+            int any0 = 0;
+            for (int j = 0; j < a.guard_n; ++j) any0 |= a.guard[j] == 0;
+            all |= a.guard_mode == 2 ? !any0 : any0;  // guarded off
+        }
         s_skip = all;
     }
     __syncthreads();
@@ -913,7 +922,8 @@ template <typename TI, typename TO>
 int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dense, long long ld,
               const uint32_t* idx, const TI* val, const long long* row_ptr, const int* tile_off,
               long long dim, TO* out, TO* p, TO* buf, double lr, double mu, double wd, int first,
-              void* ws, size_t ws_bytes, cudaStream_t stream) {
+              void* ws, size_t ws_bytes, cudaStream_t stream, const uint8_t* guard = nullptr,
+              int guard_n = 0, int guard_mode = 0) {
     if (nw < 1 || dim < 1 || !weights || (!out && !p)) return SG_ERR_INVALID;
     if (nw > MAX_WORKERS || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
     if (p && !buf) return SG_ERR_INVALID;
@@ -953,6 +963,9 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
     a.first = first;
     a.pipe = 0;
     a.peer = 0;
+    a.guard = guard;
+    a.guard_n = guard_n;
+    a.guard_mode = guard_mode;
     bool vec = true;
     if (dense) vec = vec && reinterpret_cast<size_t>(dense) % 16 == 0 && (ld * (long long)sizeof(TI)) % 16 == 0;
     if (out) vec = vec && reinterpret_cast<size_t>(out) % 16 == 0;
@@ -1044,6 +1057,56 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
+struct PeerRows {
+    const float* p[MAX_WORKERS];
+};
+
+// The dense exchange of a mixed multi-GPU step without a collective library: every rank's
+// local partial sum sits in a peer-mapped buffer; g = sum over ranks in ascending rank order
+// (float64), then momentum SGD (nn.py:167-171 order, binary64).  Guarded: a no-op unless some
+// worker in `guard` did not compress.
+__global__ void __launch_bounds__(256)
+k_peer_reduce_sgd(PeerRows src, int P, const uint8_t* __restrict__ guard, int gn, long long dim,
+                  float* __restrict__ out, float* __restrict__ p, float* __restrict__ b, double lr, double mu,
+                  double wd, int first) {
+    pdl_enter();
+    __shared__ int s_run;
+    if (threadIdx.x == 0) {
+        int any0 = 0;
+        for (int j = 0; j < gn; ++j) any0 |= guard[j] == 0;
+        s_run = any0;
+    }
+    __syncthreads();
+    if (!s_run) return;
+    const long long n4 = dim / 4, stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        double g[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int r = 0; r < P; ++r) {
+            const float4 x = reinterpret_cast<const float4*>(src.p[r])[i];
+            g[0] = dadd(g[0], (double)x.x);
+            g[1] = dadd(g[1], (double)x.y);
+            g[2] = dadd(g[2], (double)x.z);
+            g[3] = dadd(g[3], (double)x.w);
+        }
+        const float4 pv = reinterpret_cast<const float4*>(p)[i], bv = reinterpret_cast<const float4*>(b)[i];
+        double pd[4] = {pv.x, pv.y, pv.z, pv.w}, bd[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sgd_elem(g[c], pd[c], bd[c], lr, mu, wd, first != 0);
+        reinterpret_cast<float4*>(p)[i] = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
+        reinterpret_cast<float4*>(b)[i] = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
+        if (out) reinterpret_cast<float4*>(out)[i] = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+    }
+    for (long long q = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < dim; q += stride) {
+        double g = 0.0;
+        for (int r = 0; r < P; ++r) g = dadd(g, (double)src.p[r][q]);
+        double pq = p[q], bq = b[q];
+        sgd_elem(g, pq, bq, lr, mu, wd, first != 0);
+        p[q] = (float)pq;
+        b[q] = (float)bq;
+        if (out) out[q] = (float)g;
+    }
+}
+
 struct GatherSrc {
     const uint8_t* p[MAX_WORKERS];
 };
@@ -1111,6 +1174,40 @@ int sg_weighted_aggregate_peers_f32(int nw, const double* weights, const uint8_t
                                     double weight_decay, int first_step, void* stream) {
     return aggregate_peers(nw, weights, compressed, idx_ptrs, val_ptrs, tile_off_ptrs, dim, out, params,
                            momentum_buf, lr, momentum, weight_decay, first_step, (cudaStream_t)stream);
+}
+
+int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compressed, const float* dense,
+                            int64_t ld_dense, const uint32_t* idx, const float* val, const int64_t* row_ptr,
+                            const int32_t* tile_off, int64_t dim, float* out, const uint8_t* guard,
+                            int guard_n, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!out || !guard || guard_n < 1 || guard_n > MAX_WORKERS) return SG_ERR_INVALID;
+    return aggregate<float, float>(nw, weights, compressed, dense, ld_dense, idx, val,
+                                   reinterpret_cast<const long long*>(row_ptr), tile_off, dim, out, nullptr,
+                                   nullptr, 0.0, 0.0, 0.0, 0, workspace, workspace_bytes, (cudaStream_t)stream,
+                                   guard, guard_n, 2);
+}
+
+int sg_peer_reduce_sgd_f32(int nranks, const float* const* partials, const uint8_t* guard, int guard_n,
+                           int64_t dim, float* out, float* params, float* momentum_buf, double lr,
+                           double momentum, double weight_decay, int first_step, void* stream) {
+    if (nranks < 1 || nranks > MAX_WORKERS || !partials || !guard || guard_n < 1 || guard_n > MAX_WORKERS ||
+        dim < 1 || !params || !momentum_buf)
+        return SG_ERR_INVALID;
+    PeerRows r;
+    for (int i = 0; i < nranks; ++i) {
+        if (!partials[i] || reinterpret_cast<size_t>(partials[i]) % 16) return SG_ERR_UNSUPPORTED;
+        r.p[i] = partials[i];
+    }
+    if (reinterpret_cast<size_t>(params) % 16 || reinterpret_cast<size_t>(momentum_buf) % 16 ||
+        (out && reinterpret_cast<size_t>(out) % 16))
+        return SG_ERR_UNSUPPORTED;
+    long long blocks = (dim / 4 + 255) / 256;
+    const long long cap = (long long)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    launch_pdl(k_peer_reduce_sgd, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream, r, nranks, guard,
+               guard_n, (long long)dim, out, params, momentum_buf, lr, momentum, weight_decay, first_step);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
 int sg_gather_bytes(int nsrc, const uint8_t* const* src, int64_t each, uint8_t* dst, void* stream) {

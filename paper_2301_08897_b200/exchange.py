@@ -30,7 +30,6 @@ exercised with the gloo backend on CPU in tests; the product constructs it with
 from __future__ import annotations
 
 import os
-from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -64,10 +63,22 @@ class CudaOps:
         return kernels.gate_states_tensor(records, self.device)
 
 
-@dataclass
 class StepInfo:
-    path: str  # "local", "sparse-allgather" or "dense-allreduce"
-    decisions: torch.Tensor | None  # this rank's u8 decisions (device)
+    """What a step did.  ``path`` is "local", "sparse-peer"/"dense-peer" (peer-memory
+    exchange), "sparse-allgather" or "dense-allreduce"; on the peer path it is resolved
+    lazily (reading it waits for the step's decisions), so the step itself never blocks."""
+
+    def __init__(self, path, decisions, resolve=None):
+        self._path = path
+        self._resolve = resolve
+        self.decisions = decisions  # this rank's u8 decisions (device)
+
+    @property
+    def path(self) -> str:
+        if self._path is None:
+            self._path = self._resolve()
+            self._resolve = None
+        return self._path
 
 
 def _padded(dim: int) -> int:
@@ -171,10 +182,19 @@ class GradientExchange:
                 val_p = [b + 4 * (dw + k * m + j * m) for b in bases for j in range(k)]
                 off_p = [b + 4 * (dw + 2 * k * m + j * nt1) for b in bases for j in range(k)]
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
-                self._dec_host = torch.empty(self.W, dtype=torch.uint8, pin_memory=True)
-                self._dec_ready = torch.cuda.Event()
                 self._peer_merge = kernels.PeerMergeLauncher(dim, self.dec_all, idx_p, val_p, off_p, self.params,
                                                              self.momentum_buf, momentum, weight_decay)
+                # mixed decisions: each rank's partial in a peer-mapped buffer, reduced in rank order
+                import torch.distributed._symmetric_memory as symm_mem
+
+                self._partial_buf = symm_mem.empty(self.ld, dtype=torch.float32, device=device)
+                grp = group if group is not None else dist.group.WORLD
+                ph = symm_mem.rendezvous(self._partial_buf, grp.group_name)
+                poff = self._partial_buf.data_ptr() - ph.buffer_ptrs[self.rank]
+                self._dense = kernels.GuardedDenseLaunchers(
+                    k, dim, self.ld, self.decision, self.idx, self.val, self.row_ptr_local, self.tile_off,
+                    self._partial_buf, [ph.buffer_ptrs[r] + poff for r in range(P)], self.dec_all,
+                    self.params, self.momentum_buf, momentum, weight_decay)
             elif self.packed:
                 P, words, dw = self.world, self.pack_words, self.pack_dw
                 self.pack_all = torch.empty(P * words, dtype=torch.int32, **z)
@@ -248,28 +268,39 @@ class GradientExchange:
             path = self._exchange(w, out, opt)
         self.first_step = False
         self.steps += 1
-        return StepInfo(path, self.decision if self.compression else None)
+        dec = self.decision if self.compression else None
+        if callable(path):
+            return StepInfo(None, dec, path)
+        return StepInfo(path, dec)
 
     def _exchange(self, w, out, opt) -> str:
         g = self.group
         dim = self.dim
         if self.packed and self._symm is not None:
-            # Peer path: every rank's Top-k wrote its symmetric send buffer; after a device-side
-            # barrier the W decision bytes are gathered (the step's one host read) and the merge
-            # streams the other ranks' payloads over NVLink in place.  A second barrier keeps
-            # the next step's Top-k from overwriting a buffer a peer is still reading.
+            # Peer path, no host synchronisation: after a device barrier (every rank's Top-k has
+            # written its symmetric send buffer) the W decisions are gathered on device, and both
+            # exchanges are enqueued with device-side guards on them -- the all-compressed merge,
+            # which reads the other ranks' payloads in place over NVLink, and the mixed case's
+            # partial + rank-ordered reduction + SGD.  The last barrier keeps the next step's
+            # Top-k from overwriting a buffer a peer is still reading.
+            lr, first = opt["lr"], opt["first_step"]
             self._symm.barrier(channel=0)
             kernels.gather_bytes(self._dec_ptrs, self.k, self.dec_all)
-            self._dec_host.copy_(self.dec_all, non_blocking=True)
-            self._dec_ready.record()
-            self._dec_ready.synchronize()
-            if bool(self._dec_host.numpy().min() == 1):
-                self._peer_merge(w, opt["lr"], opt["first_step"], out)
-                self._symm.barrier(channel=0)
-                return "sparse-peer"
-            path = self._dense_exchange(w, out, opt)
+            self._peer_merge(w, lr, first, out)
+            self._dense.partial(w[self.lo:self.lo + self.k], self.bucket)
             self._symm.barrier(channel=0)
-            return path
+            self._dense.reduce_sgd(lr, first, out)
+            self._symm.barrier(channel=0)
+            dec_host = torch.empty(self.W, dtype=torch.uint8, pin_memory=True)
+            dec_host.copy_(self.dec_all, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record()
+
+            def resolve():
+                ready.synchronize()
+                return "sparse-peer" if int(dec_host.numpy().min()) == 1 else "dense-peer"
+
+            return resolve
         if self.packed:
             # one all-gather carries every rank's decisions, payloads and merge offsets; the
             # decisions and offsets are regrouped contiguously on device before the host

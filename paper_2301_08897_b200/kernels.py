@@ -261,6 +261,41 @@ class PeerMergeLauncher:
         _count(1)
 
 
+class GuardedDenseLaunchers:
+    """The mixed-decision side of a multi-GPU step, enqueued every step and guarded on the
+    gathered decisions: this rank's partial (sg_weighted_partial_f32) into its peer-mapped
+    buffer, and the rank-ordered reduction + SGD over every rank's partial
+    (sg_peer_reduce_sgd_f32).  Both are no-ops when every worker compressed."""
+
+    def __init__(self, k: int, dim: int, ld: int, compressed, idx, val, row_ptr, tile_off, partial: torch.Tensor,
+                 partial_ptrs, guard: torch.Tensor, params, momentum_buf, momentum: float, weight_decay: float):
+        lib = _capi.load()
+        self._part, self._red = lib.sg_weighted_partial_f32, lib.sg_peer_reduce_sgd_f32
+        self._k, self._dim, self._ld = k, dim, ld
+        self._w = np.zeros(k, dtype=np.float64)
+        _, self._wp = _capi.weights_ptr(self._w)
+        self._comp, self._idx, self._val = compressed.data_ptr(), idx.data_ptr(), val.data_ptr()
+        self._rp, self._toff = row_ptr.data_ptr(), tile_off.data_ptr()
+        self._partial = partial.data_ptr()
+        self._pp = (ctypes.c_void_p * len(partial_ptrs))(*partial_ptrs)
+        self._guard, self._gn = guard.data_ptr(), guard.numel()
+        self._p, self._b = params.data_ptr(), momentum_buf.data_ptr()
+        self._mu, self._wd = float(momentum), float(weight_decay)
+
+    def partial(self, local_weights, bucket: torch.Tensor) -> None:
+        self._w[:] = local_weights
+        st = self._part(self._k, self._wp, self._comp, bucket.data_ptr(), self._ld, self._idx, self._val, self._rp,
+                        self._toff, self._dim, self._partial, self._guard, self._gn, None, 0, _stream())
+        _capi.check(st, "sg_weighted_partial_f32")
+        _count(1)
+
+    def reduce_sgd(self, lr: float, first_step: bool, out: torch.Tensor | None = None) -> None:
+        st = self._red(len(self._pp), self._pp, self._guard, self._gn, self._dim, _ptr(out), self._p, self._b,
+                       float(lr), self._mu, self._wd, int(bool(first_step)), _stream())
+        _capi.check(st, "sg_peer_reduce_sgd_f32")
+        _count(1)
+
+
 def gather_bytes(src_ptrs, each: int, dst: torch.Tensor) -> None:
     """dst[i*each:(i+1)*each] = bytes at device address src_ptrs[i] (peers' memory allowed)."""
     require_cuda(dst)
