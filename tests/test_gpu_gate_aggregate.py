@@ -151,3 +151,75 @@ def test_float32_aggregate_is_correctly_rounded(cuda):
     pw, bw = comm_ref.sgd_momentum(p0.astype(np.float64), b0.astype(np.float64), want, 0.05, 0.9, 1e-4)
     assert np.array_equal(p.cpu().numpy().view(np.uint32), pw.astype(np.float32).view(np.uint32))
     assert np.array_equal(b.cpu().numpy().view(np.uint32), bw.astype(np.float32).view(np.uint32))
+
+
+def test_guarded_dense_exchange_and_peer_merge(cuda):
+    """The multi-GPU entry points on one GPU (peer pointers may be local): two "ranks" of two
+    workers each.  Mixed decisions: each rank's guarded partial (sg_weighted_partial_f32),
+    summed in rank order with momentum SGD (sg_peer_reduce_sgd_f32), equals the oracle fold +
+    SGD within the fp32 tolerance, and the all-sparse merge over per-worker pointers
+    (sg_weighted_aggregate_peers_f32) is a no-op.  All compressed: the reverse, and the peer
+    merge is bit-identical to sg_weighted_aggregate_f32 on the same payloads."""
+    from paper_2301_08897_b200 import kernels
+
+    D, k, P = 100_003, 2, 2
+    W = k * P
+    rng = np.random.default_rng(7)
+    G = [rng.standard_normal(D).astype(np.float32) * (1 + j) for j in range(W)]
+    w = comm_ref.rate_weights([31, 30, 1, 30])
+    m = comm_ref.topk_count(D, 0.01)
+    ld = (D + 3) // 4 * 4
+    p0 = rng.standard_normal(D).astype(np.float32)
+    b0 = rng.standard_normal(D).astype(np.float32)
+    lr, mu, wd = 0.05, 0.9, 1e-4
+    nt1 = kernels.merge_tiles(D) + 1
+    ranks = []
+    for r in range(P):
+        bucket = torch.zeros((k, ld), dtype=torch.float32, device=cuda)
+        for j in range(k):
+            bucket[j, :D] = torch.from_numpy(G[r * k + j]).to(cuda)
+        idx = torch.empty((k, m), dtype=torch.int32, device=cuda)
+        val = torch.empty((k, m), dtype=torch.float32, device=cuda)
+        toff = torch.empty((k, nt1), dtype=torch.int32, device=cuda)
+        kernels.topk_gate(bucket, m, dim=D, out=(idx, val, torch.empty((k, 2), dtype=torch.float64, device=cuda),
+                                               None, None), tile_off=toff)
+        ranks.append((bucket, idx, val, toff))
+    payload = [(D, ranks[j // k][1][j % k].cpu().numpy().astype(np.int64), ranks[j // k][2][j % k].cpu().numpy().astype(np.float64))
+               for j in range(W)]
+    rp = torch.arange(0, (k + 1) * m, m, dtype=torch.int64, device=cuda)
+    for mixed in (True, False):
+        dec = [1, 0, 1, 1] if mixed else [1, 1, 1, 1]
+        dec_all = torch.tensor(dec, dtype=torch.uint8, device=cuda)
+        params = torch.from_numpy(p0.copy()).to(cuda)
+        buf = torch.from_numpy(b0.copy()).to(cuda)
+        partials = [torch.zeros(ld, dtype=torch.float32, device=cuda) for _ in range(P)]
+        merge = kernels.PeerMergeLauncher(D, dec_all, [ranks[j // k][1][j % k].data_ptr() for j in range(W)],
+                                          [ranks[j // k][2][j % k].data_ptr() for j in range(W)],
+                                          [ranks[j // k][3][j % k].data_ptr() for j in range(W)], params, buf, mu, wd)
+        merge(w, lr, False)
+        for r in range(P):
+            dl = kernels.GuardedDenseLaunchers(k, D, ld, dec_all[r * k:(r + 1) * k], ranks[r][1], ranks[r][2], rp,
+                                               ranks[r][3], partials[r], [t.data_ptr() for t in partials], dec_all,
+                                               params, buf, mu, wd)
+            dl.partial(w[r * k:(r + 1) * k], ranks[r][0])
+        dl.reduce_sgd(lr, False)
+        torch.cuda.synchronize()
+        pl = [payload[j] if dec[j] else G[j].astype(np.float64) for j in range(W)]
+        agg = comm_ref.aggregate(pl, w)
+        pw, bw = comm_ref.sgd_momentum(p0.astype(np.float64), b0.astype(np.float64), agg, lr, mu, wd)
+        got = params.cpu().numpy().astype(np.float64)
+        if mixed:
+            assert np.max(np.abs(got - pw)) <= 1e-5 * np.max(np.abs(pw))
+        else:
+            # bit-identical to the single-buffer merge of the same payloads
+            p2 = torch.from_numpy(p0.copy()).to(cuda)
+            b2 = torch.from_numpy(b0.copy()).to(cuda)
+            idx_all = torch.cat([ranks[r][1] for r in range(P)])
+            val_all = torch.cat([ranks[r][2] for r in range(P)])
+            toff_all = torch.cat([ranks[r][3] for r in range(P)])
+            rp_all = torch.arange(0, (W + 1) * m, m, dtype=torch.int64, device=cuda)
+            kernels.weighted_aggregate(w, D, compressed=dec_all, idx=idx_all, val=val_all, row_ptr=rp_all,
+                                       tile_off=toff_all, params=p2, momentum_buf=b2, lr=lr, momentum=mu,
+                                       weight_decay=wd, first_step=False)
+            assert torch.equal(params, p2) and torch.equal(buf, b2)
+            assert np.max(np.abs(got - pw)) <= 1e-5 * np.max(np.abs(pw))
