@@ -187,6 +187,7 @@ class GradientExchange:
                 # mixed decisions: each rank's partial in a peer-mapped buffer, reduced in rank order
                 import torch.distributed._symmetric_memory as symm_mem
 
+                self._side = None
                 self._partial_buf = symm_mem.empty(self.ld, dtype=torch.float32, device=device)
                 grp = group if group is not None else dist.group.WORLD
                 ph = symm_mem.rendezvous(self._partial_buf, grp.group_name)
@@ -284,12 +285,22 @@ class GradientExchange:
             # partial + rank-ordered reduction + SGD.  The last barrier keeps the next step's
             # Top-k from overwriting a buffer a peer is still reading.
             lr, first = opt["lr"], opt["first_step"]
+            main = torch.cuda.current_stream()
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=self.device)
+                self._gathered = torch.cuda.Event()
             self._symm.barrier(channel=0)
             kernels.gather_bytes(self._dec_ptrs, self.k, self.dec_all)
+            self._gathered.record(main)
+            # the guarded dense side on a second stream: its no-ops overlap the merge (exactly
+            # one of the two sides does work in any step)
+            self._side.wait_event(self._gathered)
+            with torch.cuda.stream(self._side):
+                self._dense.partial(w[self.lo:self.lo + self.k], self.bucket)
+                self._symm.barrier(channel=1)
+                self._dense.reduce_sgd(lr, first, out)
             self._peer_merge(w, lr, first, out)
-            self._dense.partial(w[self.lo:self.lo + self.k], self.bucket)
-            self._symm.barrier(channel=0)
-            self._dense.reduce_sgd(lr, first, out)
+            main.wait_stream(self._side)
             self._symm.barrier(channel=0)
             dec_host = torch.empty(self.W, dtype=torch.uint8, pin_memory=True)
             dec_host.copy_(self.dec_all, non_blocking=True)
