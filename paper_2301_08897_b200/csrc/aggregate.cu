@@ -156,6 +156,7 @@ template <typename TI, typename TO> struct AggArgs {
     // guard_mode 1 = run only if every guard byte is non-zero, 2 = only if some byte is zero
     const uint8_t* guard;
     int guard_n, guard_mode;
+    int balance;  // k_merge_ws: cost-balanced tile ranges (else equal ranges)
 };
 
 template <typename TI, typename TO>
@@ -613,7 +614,9 @@ k_merge(const AggArgs<float, TO> a) {
 // ---------------------------------------------------------------------------------------
 // k_merge_ws: persistent, warp-specialised merge + fused momentum SGD for the case the hot
 // path produces (every worker sparse, float32, <= 16 workers).  One CTA per SM owns the
-// contiguous tile range [b*tpb, (b+1)*tpb); a tile's entries (worker-major, ascending index
+// tiles b, b + G, b + 2G, ... (G = grid; round-robin, so concentrated regions of kept entries --
+// real gradients put most of them in a few layers -- spread evenly over the CTAs); a tile's
+// entries (worker-major, ascending index
 // inside a worker) are processed in chunks of <= MW_ECAP entries (one unless oversized).
 //   producer warps (12): warp w stages worker w's run (w < nw) of the next chunk with
 //     cp.async (LDGSTS) while, for the current chunk, (1) each entry is pushed onto its
@@ -640,14 +643,32 @@ constexpr int MW_HALF = AG_TILE / 2;
 constexpr unsigned MW_NIL = 0xffffu;
 enum { BAR_FULL = 1, BAR_EMPTY = 3, BAR_PROD = 5, BAR_CONS = 6 };
 
-inline size_t mw_smem_bytes(int tpb) {
+constexpr unsigned long long MW_BASE = 1024;  // a tile's streaming cost, in entry-equivalents
+constexpr size_t MW_STATIC = 2 * 1024;        // static shared memory of k_merge_ws (bound)
+
+inline size_t mw_smem_bytes(int tpb, int nw) {
     return (size_t)MW_STAGES * 2 * AG_TILE * sizeof(float)             // p/buf ring [S][2][TILE]
            + 2 * AG_TILE * sizeof(double)                                // values [2][TILE]
            + (size_t)AG_TILE * sizeof(unsigned)                          // heads [TILE]
            + (size_t)MW_ECAP * sizeof(uint2)                             // nodes [ECAP]
            + MW_SLOTS * (size_t)MW_ECAP * (sizeof(uint32_t) + sizeof(float) + 1)  // staging [3][ECAP]
            + 2 * AG_TILE                                                 // marks [2][TILE]
-           + (size_t)MP_MAXW * (tpb + 1) * sizeof(int);                  // offsets slice
+           + 0 * (size_t)nw * (size_t)tpb;                                // (offsets come through a ring)
+}
+
+inline int mw_balance() {
+    static const int on = [] {
+        const char* e = getenv("SG_MERGE_BALANCE");
+        return e && *e == '0' ? 0 : 1;
+    }();
+    return on;
+}
+
+// One CTA per SM over cost-balanced contiguous tile ranges.
+inline size_t mw_launch_shape(long long ntiles, int nw, int sms, int& tpb, int& grid) {
+    tpb = 0;
+    grid = (int)(ntiles < sms ? ntiles : sms);
+    return mw_smem_bytes(0, nw);
 }
 
 template <typename TO>
@@ -663,7 +684,9 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
     unsigned* head = reinterpret_cast<unsigned*>(sval + MW_SLOTS * MW_ECAP);  // [TILE]
     uint8_t* mark = reinterpret_cast<uint8_t*>(head + AG_TILE);          // [2][TILE]
     uint8_t* swk = mark + 2 * AG_TILE;                                   // [SLOTS][ECAP] worker ids
-    int* soff = reinterpret_cast<int*>(swk + MW_SLOTS * MW_ECAP);        // [nw][tpb + 1]
+    constexpr int OR = 8;                    // tile-offset ring: filled 4 tiles ahead of the cursor
+    __shared__ int so_lo[OR][MP_MAXW];       // worker j's merge offsets at the tile's two edges
+    __shared__ int so_hi[OR][MP_MAXW];
     __shared__ int4 s_hdr[MW_SLOTS];  // staged chunk: {tile, c0, entries, last}
     __shared__ __align__(8) unsigned long long fullb[MW_STAGES];
     __shared__ const uint32_t* s_ib[MP_MAXW];  // worker j's entries (local, or a peer GPU's)
@@ -678,29 +701,134 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
     }
     __syncthreads();
     if (!s_ok) return;  // not all-sparse: k_merge handles this call
-    const long long t_begin = (long long)blockIdx.x * tpb;
-    if (t_begin >= a.ntiles) return;
-    const int nt = (int)(a.ntiles - t_begin < tpb ? a.ntiles - t_begin : tpb);
-    const int sw = tpb + 1;
+    // ---- this CTA's contiguous tile range, balanced by cost ------------------------------
+    // cost(tile) = MW_BASE + entries of all workers in the tile.  Real gradients put most kept
+    // entries in a few layers; equal-cost contiguous ranges give those tiles to many CTAs
+    // while each CTA still streams one contiguous region (the fastest order for the p/buf
+    // stream).  Every CTA derives the same partition: a coarse prefix over blocks of CB tiles,
+    // refined inside one block for its own two bounds.
+    const long long G = gridDim.x, ntl = a.ntiles;
+    const long long CB = ntl > 64LL * 1024 ? (ntl + 1023) / 1024 : 64;
+    const int nblk = (int)((ntl + CB - 1) / CB);  // <= 1024
+    // (scratch in the p/buf ring, which the TMA fills only after the partition is known)
+    unsigned long long* s_cp = reinterpret_cast<unsigned long long*>(ring);  // [1025] cost of tiles [0, k*CB)
+    unsigned long long* s_wsum = s_cp + 1032;                                 // [MW_THREADS / 32]
+    __shared__ long long s_bound[2];
+    auto off_at = [&](int j, long long t) -> long long {
+        return a.peer ? a.offw[j][t] : a.off[(long long)j * (ntl + 1) + t];
+    };
+    auto tile_cost = [&](long long t) -> unsigned long long {
+        unsigned long long c = MW_BASE;
+        for (int j = 0; j < nw; ++j) c += (unsigned long long)(off_at(j, t + 1) - off_at(j, t));
+        return c;
+    };
+    if (a.balance) {
+        // coarse costs: thread t owns blocks 2t, 2t+1; block-wide inclusive scan
+        unsigned long long v[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int k = 2 * tid + u;
+            v[u] = 0;
+            if (k < nblk) {
+                const long long t0 = k * CB, t1 = t0 + CB < ntl ? t0 + CB : ntl;
+                unsigned long long c = (unsigned long long)(t1 - t0) * MW_BASE;
+                for (int j = 0; j < nw; ++j) c += (unsigned long long)(off_at(j, t1) - off_at(j, t0));
+                v[u] = c;
+            }
+        }
+        const int lane = tid & 31, warp = tid >> 5;
+        unsigned long long incl = v[0] + v[1];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        unsigned long long wb = 0;
+        for (int i = 0; i < warp; ++i) wb += s_wsum[i];
+        const unsigned long long ex = wb + incl - (v[0] + v[1]);
+        if (2 * tid < nblk) s_cp[2 * tid + 1] = ex + v[0];
+        if (2 * tid + 1 < nblk) s_cp[2 * tid + 2] = ex + v[0] + v[1];
+        if (tid == 0) s_cp[0] = 0;
+        __syncthreads();
+    }
+    const unsigned long long total = s_cp[nblk];
+    auto coarse_of = [&](unsigned long long target) {  // s_cp[k] <= target < s_cp[k + 1]
+        int lo = 0, hi = nblk;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_cp[mid] <= target) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    };
+    long long t_begin, t_end;
+    if (!a.balance) {  // equal contiguous ranges
+        const long long share = (ntl + G - 1) / G;
+        t_begin = blockIdx.x * share;
+        t_end = t_begin + share < ntl ? t_begin + share : ntl;
+    } else {
+        // warps 0 and 1 refine bounds b and b + 1: the first tile whose preceding cost >= target
+        const int warp = tid >> 5, lane = tid & 31;
+        if (warp < 2) {
+            const long long b = (long long)blockIdx.x + warp;
+            long long res = ntl;
+            if (b == 0) {
+                res = 0;
+            } else if (b < G) {
+                const unsigned long long target = total * (unsigned long long)b / (unsigned long long)G;
+                const int k = coarse_of(target);
+                const long long t0 = k * CB, t1 = t0 + CB < ntl ? t0 + CB : ntl;
+                unsigned long long run = s_cp[k];  // cost before tile t0 + (chunk start)
+                res = t1;
+                for (long long c0 = t0; c0 < t1; c0 += 32) {
+                    const long long t = c0 + lane;
+                    const unsigned long long c = t < t1 ? tile_cost(t) : 0ull;
+                    unsigned long long inc = c;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+                        if (lane >= o) inc += y;
+                    }
+                    const unsigned long long before = run + inc - c;  // cost of tiles < t
+                    const unsigned hit = __ballot_sync(FULL, t < t1 && before >= target);
+                    if (hit) {
+                        res = c0 + __ffs(hit) - 1;
+                        break;
+                    }
+                    run += __shfl_sync(FULL, inc, 31);
+                }
+            }
+            if (lane == 0) s_bound[warp] = res;
+        }
+        __syncthreads();
+        t_begin = s_bound[0];
+        t_end = s_bound[1];
+    }
+    if (t_begin >= t_end) return;
+    const int nt = (int)(t_end - t_begin);
+    auto tile_of = [&](int i) { return t_begin + i; };
     // ring stage s <- p/buf of tile i (full tiles only; a partial last tile is read directly)
     unsigned long long policy = 0;
     auto issue = [&](int i) {
-        const long long tb = (t_begin + i) * AG_TILE;
-        if (tb + AG_TILE > a.dim) return;
+        const long long tb = tile_of(i) * AG_TILE;
         const int s = i % MW_STAGES;
+        if (tb + AG_TILE > a.dim) {  // the row's partial tile is read directly: just advance the phase
+            mbar_arrive(&fullb[s]);
+            return;
+        }
         mbar_expect_tx(&fullb[s], 2 * AG_TILE * sizeof(float));
         bulk_g2s(ring + (s * 2) * AG_TILE, a.p + tb, AG_TILE * sizeof(float), &fullb[s], policy);
         bulk_g2s(ring + (s * 2 + 1) * AG_TILE, a.buf + tb, AG_TILE * sizeof(float), &fullb[s], policy);
     };
+    __syncthreads();  // the partition scratch in the ring is dead
     if (tid == 0) {
         policy = policy_evict_first();
         for (int s = 0; s < MW_STAGES; ++s) mbar_init(&fullb[s], 1);
         fence_mbar_init();
+        fence_proxy_async();  // generic writes to the ring before the first bulk copies into it
         for (int i = 0; i < MW_STAGES && i < nt; ++i) issue(i);
-    }
-    for (int q = tid; q < nw * (nt + 1); q += MW_THREADS) {
-        const int j = q / (nt + 1), i = q - j * (nt + 1);
-        soff[j * sw + i] = a.peer ? a.offw[j][t_begin + i] : a.off[(long long)j * (a.ntiles + 1) + t_begin + i];
     }
     for (int q = tid; q < AG_TILE; q += MW_THREADS) head[q] = MW_NIL;
     for (int q = tid; q < 2 * AG_TILE / 4; q += MW_THREADS) reinterpret_cast<unsigned*>(mark)[q] = 0u;
@@ -714,8 +842,20 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
         // ------------------------------- producers -------------------------------
         const int pt = tid - MW_CONS, lane = pt & 31, pw = pt >> 5;
         // per-warp view of tile i: lane j < nw holds worker j's entry count and start
+        // the cursor enters tile i: warp 0 fetches tile i + 4's per-worker offsets into the
+        // ring (read 4 cursor advances -- and at least 4 producer barriers -- later)
+        // (asynchronous: the copies join the current staging group, complete before that chunk is
+        // processed and are read only when the cursor reaches the tile)
+        auto prefetch_offsets = [&](int i) {
+            if (pw == 0 && lane < nw && i < nt) {
+                const long long t = tile_of(i);
+                const int* o = a.peer ? a.offw[lane] : a.off + (long long)lane * (ntl + 1);
+                cp_async4(&so_lo[i % OR][lane], o + t);
+                cp_async4(&so_hi[i % OR][lane], o + t + 1);
+            }
+        };
         auto tile_runs = [&](int i, int& cnt, int& pre, int& tot) {
-            cnt = lane < nw ? soff[lane * sw + i + 1] - soff[lane * sw + i] : 0;
+            cnt = lane < nw ? so_hi[i % OR][lane] - so_lo[i % OR][lane] : 0;
             int incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -728,6 +868,10 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
         // Staging cursor: the next chunk to stage is entries [c0, min(E, c0 + ECAP)) of tile
         // ci (cnt/pre: the tile's per-worker runs); ci == nt marks the end.
         int ci = 0, cc0 = 0, cE, ccnt, cpre;
+        for (int i = 0; i <= 4; ++i) prefetch_offsets(i);
+        cp_async_commit();
+        cp_async_wait<0>();
+        bar_sync(BAR_PROD, MW_PROD);
         tile_runs(0, ccnt, cpre, cE);
         auto stage_next = [&](int slot) {  // stage the cursor's chunk into slot (async), advance
             if (ci < nt) {
@@ -735,7 +879,7 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
                 for (int j = pw; j < nw; j += MW_PW) {
                     const int pj = __shfl_sync(FULL, cpre, j), nj = __shfl_sync(FULL, ccnt, j);
                     const int lo = pj > cc0 ? pj : cc0, hi = pj + nj < c1 ? pj + nj : c1;
-                    const long long g0 = soff[j * sw + ci] - pj;
+                    const long long g0 = so_lo[ci % OR][j] - pj;
                     const uint32_t* ib = s_ib[j];
                     const float* vb = s_vb[j];
                     for (int e = lo + lane; e < hi; e += 32) {
@@ -750,6 +894,7 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
                 } else {
                     ++ci;
                     cc0 = 0;
+                    prefetch_offsets(ci + 4);
                     if (ci < nt) tile_runs(ci, ccnt, cpre, cE);
                 }
             } else if (pt == 0) {
@@ -770,7 +915,7 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
             if (i >= nt) break;
             stage_next((s + 2) % MW_SLOTS);
             const int b = i & 1;
-            const uint32_t tb = (uint32_t)((t_begin + i) * AG_TILE);
+            const uint32_t tb = (uint32_t)(tile_of(i) * AG_TILE);
             double* ab = acc + b * AG_TILE;
             uint8_t* mb = mark + b * AG_TILE;
             const uint32_t* si = sidx + slot * MW_ECAP;
@@ -827,7 +972,7 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
     const bool first = a.first != 0;
     const int q0 = 4 * tid;  // positions q0 + {0..3} and MW_HALF + q0 + {0..3}
     for (int i = 0; i < nt; ++i) {
-        const long long tb = (t_begin + i) * AG_TILE;
+        const long long tb = tile_of(i) * AG_TILE;
         const int b = i & 1, s = i % MW_STAGES;
         const bool full = tb + AG_TILE <= a.dim;
         if (full) mbar_wait(&fullb[s], (unsigned)(i / MW_STAGES) & 1u);
@@ -976,15 +1121,11 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
         const int sms = num_sms();
         a.pipe = comp && vec && p && nw <= MP_MAXW;
         if (a.pipe) {
-            // one CTA per SM; the per-CTA offsets slice bounds the tiles per CTA (227 KB of
-            // shared memory, static included): larger rows run in more than one wave
-            const size_t budget = 227 * 1024 - 1024;
-            const int tpb_max = (int)((budget - mw_smem_bytes(0)) / (MP_MAXW * sizeof(int)));
-            int tpb = (int)((ntiles + sms - 1) / sms);
-            if (tpb > tpb_max) tpb = tpb_max;
-            const size_t sm = mw_smem_bytes(tpb);
+            int tpb, grid;
+            const size_t sm = mw_launch_shape(ntiles, nw, sms, tpb, grid);
+            a.balance = mw_balance();
             cudaFuncSetAttribute(k_merge_ws<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k_merge_ws<TO>, dim3((unsigned)((ntiles + tpb - 1) / tpb)), dim3(MW_THREADS), sm, stream, a, tpb);
+            launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a, tpb);
             debug_sync("k_merge_ws", stream);
         }
         cudaFuncSetAttribute(k_merge<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM);
@@ -1046,13 +1187,11 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
     a.vec_ok = 1;
     a.pipe = 1;
     const int sms = num_sms();
-    const size_t budget = 227 * 1024 - 1024;
-    const int tpb_max = (int)((budget - mw_smem_bytes(0)) / (MP_MAXW * sizeof(int)));
-    int tpb = (int)((ntiles + sms - 1) / sms);
-    if (tpb > tpb_max) tpb = tpb_max;
-    const size_t sm = mw_smem_bytes(tpb);
+    int tpb, grid;
+    const size_t sm = mw_launch_shape(ntiles, nw, sms, tpb, grid);
+    a.balance = mw_balance();
     cudaFuncSetAttribute(k_merge_ws<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_pdl(k_merge_ws<float>, dim3((unsigned)((ntiles + tpb - 1) / tpb)), dim3(MW_THREADS), sm, stream, a, tpb);
+    launch_pdl(k_merge_ws<float>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a, tpb);
     debug_sync("k_merge_ws(peers)", stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
