@@ -975,19 +975,29 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
         const long long tb = tile_of(i) * AG_TILE;
         const int b = i & 1, s = i % MW_STAGES;
         const bool full = tb + AG_TILE <= a.dim;
-        if (full) mbar_wait(&fullb[s], (unsigned)(i / MW_STAGES) & 1u);
+        // take the tile's aggregate values and release the hand-off buffer right away, so the
+        // producers can build tile i + 2 while this tile's SGD runs
         bar_sync(BAR_FULL + b, MW_CONS + MW_PROD);
         const double* ab = acc + b * AG_TILE;
         uint8_t* mb = mark + b * AG_TILE;
+        double g[8];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int qh = hh * MW_HALF + q0;
+            const unsigned mk = *reinterpret_cast<const unsigned*>(mb + qh);
+            g[4 * hh] = (mk & 0xffu) ? ab[qh] : 0.0;
+            g[4 * hh + 1] = (mk & 0xff00u) ? ab[qh + 1] : 0.0;
+            g[4 * hh + 2] = (mk & 0xff0000u) ? ab[qh + 2] : 0.0;
+            g[4 * hh + 3] = (mk & 0xff000000u) ? ab[qh + 3] : 0.0;
+            if (mk) *reinterpret_cast<unsigned*>(mb + qh) = 0u;
+        }
+        if (i + 2 < nt) bar_arrive(BAR_EMPTY + b, MW_CONS + MW_PROD);  // the producer may refill buffer b
+        if (full) mbar_wait(&fullb[s], (unsigned)(i / MW_STAGES) & 1u);
         const float* rp = ring + (s * 2) * AG_TILE;
         const float* rb = ring + (s * 2 + 1) * AG_TILE;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
             const int qh = hh * MW_HALF + q0;
-            const unsigned mk = *reinterpret_cast<const unsigned*>(mb + qh);
-            const double g[4] = {(mk & 0xffu) ? ab[qh] : 0.0, (mk & 0xff00u) ? ab[qh + 1] : 0.0,
-                                 (mk & 0xff0000u) ? ab[qh + 2] : 0.0, (mk & 0xff000000u) ? ab[qh + 3] : 0.0};
-            if (mk) *reinterpret_cast<unsigned*>(mb + qh) = 0u;
             const long long e = tb + qh;
             float pv[4], bv[4];
             if (full) {
@@ -1008,24 +1018,24 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
             for (int c = 0; c < 4; ++c) {
                 pd[c] = (double)pv[c];
                 bd[c] = (double)bv[c];
-                sgd_elem(g[c], pd[c], bd[c], a.lr, a.mu, a.wd, first);
+                sgd_elem(g[4 * hh + c], pd[c], bd[c], a.lr, a.mu, a.wd, first);
             }
             if (full) {
                 *reinterpret_cast<float4*>(a.p + e) = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
                 *reinterpret_cast<float4*>(a.buf + e) = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
                 if (a.out)
-                    *reinterpret_cast<float4*>(a.out + e) = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+                    *reinterpret_cast<float4*>(a.out + e) = make_float4((float)g[4 * hh], (float)g[4 * hh + 1],
+                                                                        (float)g[4 * hh + 2], (float)g[4 * hh + 3]);
             } else {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     if (e + c >= a.dim) continue;
                     a.p[e + c] = (float)pd[c];
                     a.buf[e + c] = (float)bd[c];
-                    if (a.out) a.out[e + c] = (TO)g[c];
+                    if (a.out) a.out[e + c] = (TO)g[4 * hh + c];
                 }
             }
         }
-        if (i + 2 < nt) bar_arrive(BAR_EMPTY + b, MW_CONS + MW_PROD);  // the producer may refill buffer b
         if (i + MW_STAGES < nt) {
             bar_sync(BAR_CONS, MW_CONS);  // ring stage s fully read
             if (tid == 0) {
