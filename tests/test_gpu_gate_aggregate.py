@@ -223,3 +223,51 @@ def test_guarded_dense_exchange_and_peer_merge(cuda):
                                        weight_decay=wd, first_step=False)
             assert torch.equal(params, p2) and torch.equal(buf, b2)
             assert np.max(np.abs(got - pw)) <= 1e-5 * np.max(np.abs(pw))
+
+
+@pytest.mark.parametrize("workers", [8, 16])
+def test_concentrated_payloads_merge_bit_exact(cuda, workers):
+    """Real gradients concentrate the kept entries in a few layers: here a 3 % region of the
+    row carries large values, so its tiles hold far more entries than one staging chunk
+    (the merge's multi-chunk path) and the cost-balanced tile ranges split the region over
+    many CTAs.  All-sparse merge + fused momentum SGD through the Top-k kernels' own payloads
+    and tile offsets: aggregate and updated state equal f32(oracle) bit for bit."""
+    from paper_2301_08897_b200 import kernels
+
+    rng = np.random.default_rng(11)
+    W, D = workers, 3_000_017
+    lo, hi = D // 2, D // 2 + D * 3 // 100
+    g = []
+    for j in range(W):
+        x = rng.standard_normal(D, dtype=np.float32) * 1e-3
+        x[lo:hi] = rng.standard_normal(hi - lo, dtype=np.float32) * (1 + 0.1 * j)  # the hot layer
+        g.append(x.astype(np.float32))
+    w = comm_ref.rate_weights(list(range(3, 3 + W)))
+    m = comm_ref.topk_count(D, 0.02)
+    bucket = torch.from_numpy(np.stack([np.pad(x, (0, (-D) % 4)) for x in g])).to(cuda)
+    idx = torch.empty((W, m), dtype=torch.int32, device=cuda)
+    val = torch.empty((W, m), dtype=torch.float32, device=cuda)
+    toff = torch.empty((W, kernels.merge_tiles(D) + 1), dtype=torch.int32, device=cuda)
+    kernels.topk_gate(bucket, m, dim=D, out=(idx, val, torch.empty((W, 2), dtype=torch.float64, device=cuda),
+                                           None, None), tile_off=toff)
+    per_tile = np.diff(toff.cpu().numpy(), axis=1).sum(axis=0)
+    assert per_tile.max() > 1024  # multi-chunk tiles are exercised
+    for j in (0, W - 1):  # the Top-k itself on concentrated data
+        want_i, want_v = comm_ref.topk(g[j].astype(np.float64), 0.02, "threshold")
+        assert np.array_equal(idx[j].cpu().numpy().astype(np.int64), want_i)
+        assert np.array_equal(val[j].cpu().numpy().astype(np.float64), want_v)
+    payloads = [(D, idx[j].cpu().numpy().astype(np.int64), val[j].cpu().numpy().astype(np.float64)) for j in range(W)]
+    want = comm_ref.aggregate(payloads, w)
+    p0 = rng.standard_normal(D, dtype=np.float32)
+    b0 = rng.standard_normal(D, dtype=np.float32)
+    p = torch.from_numpy(p0.copy()).to(cuda)
+    b = torch.from_numpy(b0.copy()).to(cuda)
+    out = torch.empty(D, dtype=torch.float32, device=cuda)
+    row_ptr = torch.arange(0, (W + 1) * m, m, dtype=torch.int64, device=cuda)
+    kernels.weighted_aggregate(w, D, compressed=torch.ones(W, dtype=torch.uint8, device=cuda), idx=idx, val=val,
+                               row_ptr=row_ptr, tile_off=toff, out=out, params=p, momentum_buf=b, lr=0.05,
+                               momentum=0.9, weight_decay=1e-4, first_step=False)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.astype(np.float32).view(np.uint32))
+    pw, bw = comm_ref.sgd_momentum(p0.astype(np.float64), b0.astype(np.float64), want, 0.05, 0.9, 1e-4)
+    assert np.array_equal(p.cpu().numpy().view(np.uint32), pw.astype(np.float32).view(np.uint32))
+    assert np.array_equal(b.cpu().numpy().view(np.uint32), bw.astype(np.float32).view(np.uint32))
