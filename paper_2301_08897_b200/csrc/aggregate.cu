@@ -157,6 +157,7 @@ template <typename TI, typename TO> struct AggArgs {
     const uint8_t* guard;
     int guard_n, guard_mode;
     int balance;  // k_merge_ws: cost-balanced tile ranges (else equal ranges)
+    int cost_j0, cost_j1;  // workers whose offsets estimate the tile costs (local memory)
 };
 
 template <typename TI, typename TO>
@@ -717,9 +718,14 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
     auto off_at = [&](int j, long long t) -> long long {
         return a.peer ? a.offw[j][t] : a.off[(long long)j * (ntl + 1) + t];
     };
+    // (the cost estimate reads the offsets of workers cost_j0..cost_j1 only -- on the peer path
+    // this rank's own, so the partition needs no NVLink round trips; each rank's partition is
+    // private, the tiles' results do not depend on it)
+    const int cj0 = a.cost_j0, cj1 = a.cost_j1;
+    const unsigned long long base = MW_BASE * (unsigned long long)(cj1 - cj0) / (unsigned long long)nw + 1;
     auto tile_cost = [&](long long t) -> unsigned long long {
-        unsigned long long c = MW_BASE;
-        for (int j = 0; j < nw; ++j) c += (unsigned long long)(off_at(j, t + 1) - off_at(j, t));
+        unsigned long long c = base;
+        for (int j = cj0; j < cj1; ++j) c += (unsigned long long)(off_at(j, t + 1) - off_at(j, t));
         return c;
     };
     if (a.balance) {
@@ -731,8 +737,8 @@ k_merge_ws(const AggArgs<float, TO> a, int tpb) {
             v[u] = 0;
             if (k < nblk) {
                 const long long t0 = k * CB, t1 = t0 + CB < ntl ? t0 + CB : ntl;
-                unsigned long long c = (unsigned long long)(t1 - t0) * MW_BASE;
-                for (int j = 0; j < nw; ++j) c += (unsigned long long)(off_at(j, t1) - off_at(j, t0));
+                unsigned long long c = (unsigned long long)(t1 - t0) * base;
+                for (int j = cj0; j < cj1; ++j) c += (unsigned long long)(off_at(j, t1) - off_at(j, t0));
                 v[u] = c;
             }
         }
@@ -1134,6 +1140,8 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
             int tpb, grid;
             const size_t sm = mw_launch_shape(ntiles, nw, sms, tpb, grid);
             a.balance = mw_balance();
+            a.cost_j0 = 0;
+            a.cost_j1 = nw;
             cudaFuncSetAttribute(k_merge_ws<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a, tpb);
             debug_sync("k_merge_ws", stream);
@@ -1200,6 +1208,22 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
     int tpb, grid;
     const size_t sm = mw_launch_shape(ntiles, nw, sms, tpb, grid);
     a.balance = mw_balance();
+    {  // cost estimate from the workers whose payloads live on this device
+        int dev = -1;
+        cudaGetDevice(&dev);
+        int j0 = -1, j1 = -1;
+        for (int j = 0; j < nw; ++j) {
+            cudaPointerAttributes at;
+            if (cudaPointerGetAttributes(&at, off_ptrs[j]) == cudaSuccess && at.device == dev &&
+                at.type == cudaMemoryTypeDevice) {
+                if (j0 < 0) j0 = j;
+                j1 = j + 1;
+            }
+        }
+        cudaGetLastError();
+        a.cost_j0 = j0 < 0 ? 0 : j0;
+        a.cost_j1 = j0 < 0 ? nw : j1;
+    }
     cudaFuncSetAttribute(k_merge_ws<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     launch_pdl(k_merge_ws<float>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a, tpb);
     debug_sync("k_merge_ws(peers)", stream);
