@@ -108,10 +108,13 @@ def test_multi_gpu_exchange_matches_single_gpu(cuda):
 
     n = 4 if torch.cuda.device_count() >= 4 else 2
     # peer path (symmetric buffers read in place by the merge) and the NCCL all-gather path
-    for p2p, sparse_path in (("1", "sparse-peer"), ("0", "sparse-allgather")):
+    # (and one worker per rank, the 8-GPU shape: W = P)
+    for port, p2p, workers, sparse_path in (("29531", "1", "8", "sparse-peer"), ("29532", "0", "8", "sparse-allgather"),
+                                            ("29533", "1", str(n), "sparse-peer")):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-               "--master-addr", "127.0.0.1", "--master-port", "2953" + p2p, str(ROOT / "tools" / "multi_check.py")]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "SG_P2P": p2p})
+               "--master-addr", "127.0.0.1", "--master-port", port, str(ROOT / "tools" / "multi_check.py")]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                           env={**os.environ, "SG_P2P": p2p, "SG_CHECK_WORKERS": workers})
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
         rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
         assert rep["ok"] and rep["world"] == n

@@ -21,7 +21,8 @@ import torch.distributed as dist
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2301_08897_b200 import build, comm, exchange  # noqa: E402
 
-D, W = 4_000_037, 8
+D = 4_000_037
+W = int(os.environ.get("SG_CHECK_WORKERS", "8"))  # W = P gives one worker per rank (the 8-GPU shape)
 
 
 def fill(ex, family, step):
@@ -36,7 +37,7 @@ def fill(ex, family, step):
 
 def run(family, cr, delta, group, dev, steps=3):
     ex = exchange.GradientExchange(D, W, cr=cr, delta=delta, momentum=0.9, weight_decay=1e-4, group=group, device=dev)
-    w = comm.weights_from_rates([31, 30, 1, 30, 42, 66, 22, 14])
+    w = comm.weights_from_rates([31, 30, 1, 30, 42, 66, 22, 14][:W])
     paths = []
     for s in range(steps):
         fill(ex, family, s)
