@@ -645,16 +645,14 @@ constexpr unsigned MW_NIL = 0xffffu;
 enum { BAR_FULL = 1, BAR_EMPTY = 3, BAR_PROD = 5, BAR_CONS = 6 };
 
 constexpr unsigned long long MW_BASE = 1024;  // a tile's streaming cost, in entry-equivalents
-constexpr size_t MW_STATIC = 2 * 1024;        // static shared memory of k_merge_ws (bound)
 
-inline size_t mw_smem_bytes(int tpb, int nw) {
+inline size_t mw_smem_bytes() {
     return (size_t)MW_STAGES * 2 * AG_TILE * sizeof(float)             // p/buf ring [S][2][TILE]
            + 2 * AG_TILE * sizeof(double)                                // values [2][TILE]
            + (size_t)AG_TILE * sizeof(unsigned)                          // heads [TILE]
            + (size_t)MW_ECAP * sizeof(uint2)                             // nodes [ECAP]
-           + MW_SLOTS * (size_t)MW_ECAP * (sizeof(uint32_t) + sizeof(float) + 1)  // staging [3][ECAP]
-           + 2 * AG_TILE                                                 // marks [2][TILE]
-           + 0 * (size_t)nw * (size_t)tpb;                                // (offsets come through a ring)
+           + MW_SLOTS * (size_t)MW_ECAP * (sizeof(uint32_t) + sizeof(float) + 1)  // staging + worker ids
+           + 2 * AG_TILE;                                                // marks [2][TILE]
 }
 
 inline int mw_balance() {
@@ -666,15 +664,11 @@ inline int mw_balance() {
 }
 
 // One CTA per SM over cost-balanced contiguous tile ranges.
-inline size_t mw_launch_shape(long long ntiles, int nw, int sms, int& tpb, int& grid) {
-    tpb = 0;
-    grid = (int)(ntiles < sms ? ntiles : sms);
-    return mw_smem_bytes(0, nw);
-}
+inline int mw_grid(long long ntiles, int sms) { return (int)(ntiles < sms ? ntiles : sms); }
 
 template <typename TO>
 __global__ void __launch_bounds__(MW_THREADS, 1)
-k_merge_ws(const AggArgs<float, TO> a, int tpb) {
+k_merge_ws(const AggArgs<float, TO> a) {
     pdl_enter();
     extern __shared__ __align__(128) unsigned char mw_smem[];
     float* ring = reinterpret_cast<float*>(mw_smem);                     // [S][2][TILE]
@@ -1137,13 +1131,13 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
         const int sms = num_sms();
         a.pipe = comp && vec && p && nw <= MP_MAXW;
         if (a.pipe) {
-            int tpb, grid;
-            const size_t sm = mw_launch_shape(ntiles, nw, sms, tpb, grid);
+            const int grid = mw_grid(ntiles, sms);
+            const size_t sm = mw_smem_bytes();
             a.balance = mw_balance();
             a.cost_j0 = 0;
             a.cost_j1 = nw;
             cudaFuncSetAttribute(k_merge_ws<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a, tpb);
+            launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a);
             debug_sync("k_merge_ws", stream);
         }
         cudaFuncSetAttribute(k_merge<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM);
@@ -1205,8 +1199,8 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
     a.vec_ok = 1;
     a.pipe = 1;
     const int sms = num_sms();
-    int tpb, grid;
-    const size_t sm = mw_launch_shape(ntiles, nw, sms, tpb, grid);
+    const int grid = mw_grid(ntiles, sms);
+    const size_t sm = mw_smem_bytes();
     a.balance = mw_balance();
     {  // cost estimate from the workers whose payloads live on this device
         int dev = -1;
@@ -1225,7 +1219,7 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
         a.cost_j1 = j0 < 0 ? nw : j1;
     }
     cudaFuncSetAttribute(k_merge_ws<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_pdl(k_merge_ws<float>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a, tpb);
+    launch_pdl(k_merge_ws<float>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a);
     debug_sync("k_merge_ws(peers)", stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
