@@ -146,7 +146,8 @@ class GradientExchange:
                 words = (dw + 2 * k * m + k * nt1 + 3) // 4 * 4
                 self.pack_words, self.pack_dw = words, dw
                 self._symm = None
-                if device.type == "cuda" and os.environ.get("SG_P2P", "1") != "0":
+                # (the peer merge takes up to 16 workers; more go through the NCCL all-gather path)
+                if device.type == "cuda" and os.environ.get("SG_P2P", "1") != "0" and self.W <= 16:
                     # symmetric (peer-mapped) send buffer: the merge reads the other ranks'
                     # payloads in place over NVLink instead of an all-gather
                     try:
