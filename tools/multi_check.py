@@ -37,7 +37,7 @@ def fill(ex, family, step):
 
 def run(family, cr, delta, group, dev, steps=3):
     ex = exchange.GradientExchange(D, W, cr=cr, delta=delta, momentum=0.9, weight_decay=1e-4, group=group, device=dev)
-    w = comm.weights_from_rates([31, 30, 1, 30, 42, 66, 22, 14][:W])
+    w = comm.weights_from_rates(([31, 30, 1, 30, 42, 66, 22, 14] * 8)[:W])
     paths = []
     for s in range(steps):
         fill(ex, family, s)
