@@ -119,3 +119,27 @@ def test_multi_gpu_exchange_matches_single_gpu(cuda):
         rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
         assert rep["ok"] and rep["world"] == n
         assert rep["cases"][0]["paths"] == [sparse_path] * 3, rep["cases"][0]
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multi_gpu_protocol_stress(cuda):
+    """20 steps whose decisions switch between all-compressed and mixed (tools/multi_stress.py):
+    every rank bit-identical after every step, on the peer path and the NCCL path."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    n = 4 if torch.cuda.device_count() >= 4 else 2
+    for port, p2p, paths in (("29541", "1", {"dense-peer", "sparse-peer"}),
+                             ("29542", "0", {"dense-allreduce", "sparse-allgather"})):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", "--master-port", port, str(ROOT / "tools" / "multi_stress.py"),
+               "--steps", "20"]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env={**os.environ, "SG_P2P": p2p})
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+        assert rep["ok"] and rep["rank_mismatch_steps"] == 0
+        assert set(rep["paths"]) == paths, rep
