@@ -385,18 +385,21 @@ def run_ours(args):
         cpu = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
+        size = "ResNet-152-sized" if D == R_DIM else ("VGG-19-sized" if D == 143_667_240 else "flat-gradient")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 (f64 accumulation)", "data": "synthetic",
             "config": {
-                "workload": (f"ResNet-152-sized adaptive Top-k aggregation: W={W} workers x D={D}, cr={args.cr}, "
+                "workload": (f"{size} adaptive Top-k aggregation: W={W} workers x D={D}, cr={args.cr}, "
                              f"delta={args.delta}, S1 rates {rates}, gate+exchange+weighted merge+fused momentum SGD"
                              if compression else
-                             f"ResNet-152-sized weighted dense aggregation: W={W} workers x D={D}, S1 rates {rates}, "
+                             f"{size} weighted dense aggregation: W={W} workers x D={D}, S1 rates {rates}, "
                              f"+ fused momentum SGD"),
                 "family": args.family, "workers_per_gpu": k, "parallelism": f"workers sharded {k}/GPU over {world} GPU(s)",
-                "l2": "inputs larger than L2 (k x 241 MB bucket per GPU)", "paths": sorted(set(paths)),
+                "l2": (f"inputs larger than L2 ({k} x {D * 4 / 1e6:.0f} MB bucket per GPU)" if k * D * 4 > 126e6 else
+                       f"inputs L2-resident ({k} x {D * 4 / 1e6:.1f} MB bucket per GPU): sweep point, not a bench line"),
+                "paths": sorted(set(paths)),
             },
             "roofline": roof,
             "step_roofline": step_roof,

@@ -157,6 +157,7 @@ template <typename TI, typename TO> struct AggArgs {
     const uint8_t* guard;
     int guard_n, guard_mode;
     int balance;  // k_merge_ws: cost-balanced tile ranges (else equal ranges)
+    int own;        // all-sparse merge kernel: -1 by density, 0 k_merge_ws, 1 k_merge_own
     int cost_j0, cost_j1;  // workers whose offsets estimate the tile costs (local memory)
 };
 
@@ -655,6 +656,28 @@ inline size_t mw_smem_bytes() {
            + 2 * AG_TILE;                                                // marks [2][TILE]
 }
 
+// All-sparse merges with >= MO_DENSITY kept entries per position on average (e.g. cr 0.1)
+// take k_merge_own, the sparser ones k_merge_ws; both fold in the same order, so the choice
+// (made on the device from the tile offsets of workers cost_j0..cost_j1, this GPU's own on the
+// peer path) never changes a result.
+constexpr double MO_DENSITY = 0.25;
+template <typename TO>
+SG_DEV bool merge_is_dense(const AggArgs<float, TO>& a) {
+    if (a.own >= 0) return a.own != 0;
+    long long tot = 0;
+    const long long ntl = a.ntiles;
+    for (int j = a.cost_j0; j < a.cost_j1; ++j)
+        tot += a.peer ? (long long)(a.offw[j][ntl] - a.offw[j][0])
+                      : (long long)(a.off[(long long)j * (ntl + 1) + ntl] - a.off[(long long)j * (ntl + 1)]);
+    const int nl = a.cost_j1 - a.cost_j0;
+    return nl > 0 && (double)tot * (double)a.nw >= MO_DENSITY * (double)a.dim * (double)nl;
+}
+
+inline int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e && *e ? atoi(e) : dflt;
+}
+
 inline int mw_balance() {
     static const int on = [] {
         const char* e = getenv("SG_MERGE_BALANCE");
@@ -692,10 +715,10 @@ k_merge_ws(const AggArgs<float, TO> a) {
     if (tid == 0) {
         int ok = nw <= MP_MAXW;
         for (int j = 0; j < nw && ok; ++j) ok = a.comp[j] != 0;
-        s_ok = ok;
+        s_ok = ok && !merge_is_dense(a);
     }
     __syncthreads();
-    if (!s_ok) return;  // not all-sparse: k_merge handles this call
+    if (!s_ok) return;  // not all-sparse (k_merge), or dense payloads (k_merge_own)
     // ---- this CTA's contiguous tile range, balanced by cost ------------------------------
     // cost(tile) = MW_BASE + entries of all workers in the tile.  Real gradients put most kept
     // entries in a few layers; equal-cost contiguous ranges give those tiles to many CTAs
@@ -1046,6 +1069,231 @@ k_merge_ws(const AggArgs<float, TO> a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// k_merge_own: the all-sparse merge + fused momentum SGD for dense payloads (on average
+// >= MO_DENSITY kept entries per position, e.g. cr 0.1), where k_merge_ws's per-chunk list
+// building is latency-bound.  Position-owned and barrier-light: thread t owns positions
+// [8t, 8t + 8) of the tile and keeps their float64 sums in registers.
+//   (1) every thread starts its p/buf loads for the tile (consumed at the end, so the HBM
+//       latency hides behind (2)-(3));
+//   (2) one pass over the tile's entries (worker runs concatenated) records, for every
+//       (worker, owner), the first entry of the worker's run inside the owner's positions,
+//       and pulls the values into L1;
+//   (3) each owner walks, in ascending worker order -- the reference's fold (comm.py:70-78):
+//       +0, then + w_j * v_j -- the entries of each worker's run that fall in its positions;
+//   (4) momentum SGD (nn.py:167-171 order, binary64) and 128-bit stores.
+// Tiles are dealt round-robin over a grid of 2 CTAs per SM.  Results are bit-identical to
+// k_merge_ws (the same per-position fold order).
+// ---------------------------------------------------------------------------------------
+constexpr int MO_THREADS = 512;
+constexpr int MO_PER = AG_TILE / MO_THREADS;  // 8 positions per thread
+constexpr unsigned MO_NONE = 0xffffu;
+constexpr int MO_U = 4;  // start-pass entries per thread per round
+static_assert(MO_PER == 8, "two float4 per thread");
+
+SG_DEV void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+template <typename TO>
+__global__ void __launch_bounds__(MO_THREADS, 2)
+k_merge_own(const AggArgs<float, TO> a) {
+    pdl_wait();  // no early trigger: the next kernel's CTAs must not take this grid's SM slots
+    __shared__ uint16_t rstart[MP_MAXW][MO_THREADS];
+    extern __shared__ __align__(16) unsigned char mo_smem[];
+    double (*sacc)[MO_THREADS] = reinterpret_cast<double (*)[MO_THREADS]>(mo_smem);  // [MO_PER][MO_THREADS]
+    __shared__ const uint32_t* s_ib[MP_MAXW];
+    __shared__ const float* s_vb[MP_MAXW];
+    __shared__ int s_cnt[MP_MAXW], s_pre[MP_MAXW + 1];
+    __shared__ int s_ok;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nw = a.nw;
+    if (tid == 0) {
+        int ok = nw <= MP_MAXW;
+        for (int j = 0; j < nw && ok; ++j) ok = a.comp[j] != 0;
+        s_ok = ok && merge_is_dense(a);
+    }
+    for (int x = tid; x < MP_MAXW * MO_THREADS / 2; x += MO_THREADS)
+        reinterpret_cast<unsigned*>(&rstart[0][0])[x] = 0xffffffffu;
+#pragma unroll
+    for (int c = 0; c < MO_PER; ++c) sacc[c][tid] = 0.0;
+    __syncthreads();
+    if (!s_ok) return;  // not all-sparse (k_merge), or sparse payloads (k_merge_ws)
+    const long long ntl = a.ntiles;
+    const bool first = a.first != 0;
+    const int q0 = tid * MO_PER;
+    // warp 0 lane j < nw: worker j's run [lo, lo + cnt) of the next tile, loaded a tile ahead
+    auto load_run = [&](long long t, int& lo, int& cnt) {
+        lo = 0;
+        cnt = 0;
+        if (lane < nw && t < ntl) {
+            if (a.peer) {
+                lo = a.offw[lane][t];
+                cnt = a.offw[lane][t + 1] - lo;
+            } else {
+                const int* o = a.off + (long long)lane * (ntl + 1);
+                lo = o[t];
+                cnt = o[t + 1] - lo;
+            }
+        }
+    };
+    int nlo = 0, ncnt = 0;
+    if (tid < 32) load_run(blockIdx.x, nlo, ncnt);
+    for (long long t = blockIdx.x; t < ntl; t += gridDim.x) {
+        const long long tb = t * AG_TILE;
+        const bool full = tb + AG_TILE <= a.dim;
+        // (1) p/buf of this thread's positions
+        float pv[MO_PER], bv[MO_PER];
+        if (full) {
+            const float4* pp = reinterpret_cast<const float4*>(a.p + tb + q0);
+            const float4* bp = reinterpret_cast<const float4*>(a.buf + tb + q0);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const float4 u = __ldcs(pp + r), z = __ldcs(bp + r);
+                pv[4 * r] = u.x; pv[4 * r + 1] = u.y; pv[4 * r + 2] = u.z; pv[4 * r + 3] = u.w;
+                bv[4 * r] = z.x; bv[4 * r + 1] = z.y; bv[4 * r + 2] = z.z; bv[4 * r + 3] = z.w;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < MO_PER; ++c) {
+                const bool ok = tb + q0 + c < a.dim;
+                pv[c] = ok ? a.p[tb + q0 + c] : 0.f;
+                bv[c] = ok ? a.buf[tb + q0 + c] : 0.f;
+            }
+        }
+        // the tile's worker runs (warp 0); the previous tile's walks are complete
+        __syncthreads();
+        if (tid < 32) {
+            const int lo = nlo, cnt = ncnt;
+            load_run(t + gridDim.x, nlo, ncnt);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane < nw) {
+                s_ib[lane] = (a.peer ? a.idxw[lane] : a.idx + a.row_ptr[lane]) + lo;
+                s_vb[lane] = (a.peer ? a.valw[lane] : a.val + a.row_ptr[lane]) + lo;
+                s_cnt[lane] = cnt;
+                s_pre[lane] = incl - cnt;
+            }
+            if (lane == 31) s_pre[nw] = incl;
+        }
+        __syncthreads();
+        // (2) run starts per (worker, owner); MO_U entries per thread with their loads in flight
+        // together
+        const int E = s_pre[nw];
+        for (int base = 0; base < E; base += MO_U * MO_THREADS) {
+            unsigned x[MO_U], pr[MO_U];
+            int jw[MO_U], rr[MO_U];
+#pragma unroll
+            for (int u = 0; u < MO_U; ++u) {
+                const int e = base + u * MO_THREADS + tid;
+                int j = 0;
+                if (e < E) {
+                    int hi = nw;
+                    while (hi - j > 1) {
+                        const int mid = (j + hi) >> 1;
+                        if (s_pre[mid] <= e) j = mid;
+                        else hi = mid;
+                    }
+                }
+                jw[u] = j;
+                rr[u] = e - s_pre[j];
+                x[u] = e < E ? s_ib[j][rr[u]] - (uint32_t)tb : 0u;
+                pr[u] = e < E && lane == 0 && rr[u] > 0 ? s_ib[j][rr[u] - 1] - (uint32_t)tb : 0u;
+                if (e < E) prefetch_l1(s_vb[j] + rr[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < MO_U; ++u) {
+                const int e = base + u * MO_THREADS + tid;
+                const unsigned up = __shfl_up_sync(FULL, x[u], 1);
+                const unsigned prev = lane == 0 ? pr[u] : up;
+                if (e < E) {
+                    const unsigned o = x[u] / MO_PER;
+                    if (rr[u] == 0 || prev / MO_PER != o) rstart[jw[u]][o] = (uint16_t)rr[u];
+                }
+            }
+        }
+        __syncthreads();
+        // (3) ascending-worker fold of this thread's positions into sacc[c][tid] (position
+        // q0 + c; the transposed layout keeps a warp's accesses on distinct banks), all +0
+        // between tiles
+        for (int j = 0; j < nw; ++j) {
+            const unsigned r0 = rstart[j][tid];
+            if (r0 == MO_NONE) continue;
+            rstart[j][tid] = (uint16_t)MO_NONE;
+            const uint32_t* ib = s_ib[j];
+            const float* vb = s_vb[j];
+            const int n = s_cnt[j];
+            const double wj = a.w[j];
+            for (int r = (int)r0; r < n; ++r) {
+                const unsigned x = ib[r] - (uint32_t)tb - (uint32_t)q0;
+                if (x >= (unsigned)MO_PER) break;
+                const double v = dmul(wj, (double)vb[r]);
+                double* sa = &sacc[x][tid];
+                *sa = dadd(*sa, v);
+            }
+        }
+        double acc[MO_PER];
+#pragma unroll
+        for (int c = 0; c < MO_PER; ++c) {
+            acc[c] = sacc[c][tid];
+            sacc[c][tid] = 0.0;
+        }
+        // (4) momentum SGD, stores
+        double pd[MO_PER], bd[MO_PER];
+#pragma unroll
+        for (int c = 0; c < MO_PER; ++c) {
+            pd[c] = (double)pv[c];
+            bd[c] = (double)bv[c];
+            sgd_elem(acc[c], pd[c], bd[c], a.lr, a.mu, a.wd, first);
+        }
+        if (full) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const long long e = tb + q0 + 4 * r;
+                __stcs(reinterpret_cast<float4*>(a.p + e),
+                       make_float4((float)pd[4 * r], (float)pd[4 * r + 1], (float)pd[4 * r + 2], (float)pd[4 * r + 3]));
+                __stcs(reinterpret_cast<float4*>(a.buf + e),
+                       make_float4((float)bd[4 * r], (float)bd[4 * r + 1], (float)bd[4 * r + 2], (float)bd[4 * r + 3]));
+                if (a.out)
+                    *reinterpret_cast<float4*>(a.out + e) = make_float4((float)acc[4 * r], (float)acc[4 * r + 1],
+                                                                        (float)acc[4 * r + 2], (float)acc[4 * r + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < MO_PER; ++c) {
+                const long long e = tb + q0 + c;
+                if (e >= a.dim) continue;
+                a.p[e] = (float)pd[c];
+                a.buf[e] = (float)bd[c];
+                if (a.out) a.out[e] = (TO)acc[c];
+            }
+        }
+    }
+}
+
+
+// The all-sparse merge pair: k_merge_ws then k_merge_own; each exits unless the device-side
+// density test picks it (a.own forces one, and the other is not launched).
+template <typename TO>
+void launch_sparse_merge(const AggArgs<float, TO>& a, int grid, size_t sm, int sms, cudaStream_t stream) {
+    if (a.own != 1) {
+        cudaFuncSetAttribute(k_merge_ws<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a);
+        debug_sync("k_merge_ws", stream);
+    }
+    if (a.own != 0) {
+        long long g2 = 2LL * sms;
+        if (g2 > a.ntiles) g2 = a.ntiles;
+        const int dsm = MO_PER * MO_THREADS * (int)sizeof(double);
+        cudaFuncSetAttribute(k_merge_own<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+        launch_pdl(k_merge_own<TO>, dim3((unsigned)g2), dim3(MO_THREADS), (size_t)dsm, stream, a);
+        debug_sync("k_merge_own", stream);
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_sgd(T* __restrict__ p, T* __restrict__ buf, const T* __restrict__ g, long long dim, double lr,
@@ -1129,16 +1377,15 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
     if constexpr (sizeof(TI) == 4 && sizeof(TO) == 4)
     {
         const int sms = num_sms();
-        a.pipe = comp && vec && p && nw <= MP_MAXW;
+        a.pipe = comp && vec && p && nw <= MP_MAXW && env_int("SG_MERGE_WS", 1);
         if (a.pipe) {
             const int grid = mw_grid(ntiles, sms);
             const size_t sm = mw_smem_bytes();
             a.balance = mw_balance();
             a.cost_j0 = 0;
             a.cost_j1 = nw;
-            cudaFuncSetAttribute(k_merge_ws<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a);
-            debug_sync("k_merge_ws", stream);
+            a.own = env_int("SG_MERGE_OWN", -1);
+            launch_sparse_merge(a, grid, sm, sms, stream);
         }
         cudaFuncSetAttribute(k_merge<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM);
         long long grid = (long long)sms * 2;
@@ -1218,9 +1465,8 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
         a.cost_j0 = j0 < 0 ? 0 : j0;
         a.cost_j1 = j0 < 0 ? nw : j1;
     }
-    cudaFuncSetAttribute(k_merge_ws<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_pdl(k_merge_ws<float>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a);
-    debug_sync("k_merge_ws(peers)", stream);
+    a.own = env_int("SG_MERGE_OWN", -1);
+    launch_sparse_merge(a, grid, sm, sms, stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

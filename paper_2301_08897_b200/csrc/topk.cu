@@ -154,9 +154,12 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     const size_t cap = (size_t)k * p.nseg * p.segcap;
     p.off_cidx = take(sizeof(uint32_t) * cap);
     p.off_cval = take(sizeof(T) * cap);
-    p.off_bkey = take(sizeof(K) * cap);
-    p.off_bidx = take(sizeof(uint32_t) * cap);
-    p.off_bpos = take(sizeof(uint32_t) * cap);
+    // boundary lists: only the in-CTA resolve reads them, so RES entries per worker; a larger
+    // boundary is counted, not stored, and resolved from the candidate lists (slow mode)
+    const size_t bcap = (size_t)k * TopkTraits<T>::RES;
+    p.off_bkey = take(sizeof(K) * bcap);
+    p.off_bidx = take(sizeof(uint32_t) * bcap);
+    p.off_bpos = take(sizeof(uint32_t) * bcap);
     p.total = o + 256;  // slack for base alignment
     return p;
 }
@@ -929,7 +932,7 @@ SG_DEV int sub_of(long long n, long long off, int split) {
 }
 
 template <typename T> struct CollectArgs {
-    long long segcap, cap;
+    long long segcap, cap;         // cap: boundary entries stored per worker (RES)
     int nseg, tps, split, nsub;
     uint32_t* bpos;                // [k][cap] boundary entry's position in its segment list
     SelState<typename KeyOf<T>::K>* sel;
@@ -1036,6 +1039,7 @@ k_collect(CollectArgs<T> a) {
             while (bm) {
                 const int u = __ffs(bm) - 1;
                 bm &= bm - 1;
+                if (q >= (unsigned long long)a.cap) break;  // oversized: counted only (slow mode)
                 bk[q] = KO::key(x[u]);
                 bi[q] = ci[e0 + u];
                 bp[q] = (uint32_t)(e0 + u);
@@ -1187,8 +1191,9 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
 // case (every boundary fits one CTA's shared memory) needs no grid-wide step: CTA 0 of each
 // worker resolves it in shared memory (resolve_small) and the other CTAs exit.  If some
 // worker's boundary is oversized (heavy ties), all G*k CTAs -- co-resident by cooperative
-// launch -- run the radix rounds over that worker's boundary keys in global memory with a
-// grid barrier between the histogram and the bin pick; its write then takes the slow mode.
+// launch -- run the radix rounds over that worker's candidate lists in global memory (the
+// boundary itself was only counted) with a grid barrier between the histogram and the bin
+// pick; its write then takes the slow mode.
 // --------------------------------------------------------------------------------------
 template <typename T> struct ResolveArgs {
     SelState<typename KeyOf<T>::K>* sel;
@@ -1239,7 +1244,7 @@ k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
     // slow mode: radix rounds over the oversized boundary sets
     const unsigned nblocks = gridDim.x * gridDim.y;
     unsigned gen = 0;
-    const K* src = a.bkey + (long long)w * a.cap;
+    using KO = KeyOf<T>;
     for (int round = 0; round < TopkTraits<T>::ROUNDS_MAX; ++round) {
         if (tid == 0) st = ld_cg_state(r.sel + w);
         for (int i = tid; i < SEL_BINS; i += NT) hist[i] = 0;
@@ -1248,9 +1253,13 @@ k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
         if (slow && !st.done) {
             const K lo = st.lo, span = st.span;
             const int shift = st.shift;
-            for (long long i = (long long)x * NT + tid; i < (long long)h; i += (long long)gridDim.x * NT) {
-                const K key = src[i];
-                if (key >= lo && key - lo <= span) atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
+            for (int seg = 0; seg < a.nseg; ++seg) {
+                const long long n = a.segcnt[(long long)w * a.nseg + seg];
+                const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
+                for (long long i = (long long)x * NT + tid; i < n; i += (long long)gridDim.x * NT) {
+                    const K key = KO::key(cv[i]);
+                    if (key >= lo && key - lo <= span) atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
+                }
             }
             __syncthreads();
             for (int i = tid; i < SEL_BINS; i += NT)
@@ -1798,7 +1807,6 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     unsigned* c_fb = ctr + 8 + k;
     unsigned* c_col = ctr + 8 + 2 * k;
     unsigned* c_res = ctr + 8 + 3 * k;
-    const long long capw = (long long)p.nseg * p.segcap;
 
     const bool vec_ok = (reinterpret_cast<size_t>(g) % 16 == 0) && ((ld * (long long)sizeof(T)) % 16 == 0);
     const int sms = num_sms();
@@ -1858,7 +1866,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     // 3. per-segment counts + boundary, in-CTA resolve
     CollectArgs<T> ca;
     ca.segcap = p.segcap;
-    ca.cap = capw;
+    ca.cap = TopkTraits<T>::RES;
     ca.nseg = p.nseg;
     ca.tps = p.tps;
     ca.split = p.split;

@@ -8,6 +8,7 @@ no CPU path.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -24,6 +25,11 @@ TOPK_LAUNCHES = {torch.float32: 2 + 2 + 1 + 1 + 1 + 1, torch.float64: 2 + 2 + 1 
 
 def _count(n: int) -> None:
     LAUNCHES["n"] += n
+
+
+def _sparse_merge_launches() -> int:
+    """k_merge_ws + k_merge_own (one exits by payload density) unless SG_MERGE_OWN forces one."""
+    return 1 if os.environ.get("SG_MERGE_OWN", "") in ("0", "1") else 2
 
 
 def require_cuda(t: torch.Tensor | None = None) -> None:
@@ -205,7 +211,7 @@ def weighted_aggregate(
     )
     _capi.check(st, "sg_weighted_aggregate")
     pipe = dt == torch.float32 and compressed is not None and params is not None
-    _count(1 + (1 if pipe else 0) + (1 if ws is not None else 0))
+    _count(1 + (_sparse_merge_launches() if pipe else 0) + (1 if ws is not None else 0))
     return out
 
 
@@ -232,7 +238,7 @@ class MergeLauncher:
         st = self._fn(self._nw, self._wp, comp, None, 0, idx, val, rp, toff, self._dim, _ptr(out), self._p,
                       self._b, float(lr), self._mu, self._wd, int(bool(first_step)), None, 0, _stream())
         _capi.check(st, "sg_weighted_aggregate")
-        _count(2)
+        _count(1 + _sparse_merge_launches())
 
 
 class PeerMergeLauncher:
@@ -258,7 +264,7 @@ class PeerMergeLauncher:
         st = self._fn(self._nw, self._wp, self._comp, self._ip, self._vp, self._op, self._dim, _ptr(out),
                       self._p, self._b, float(lr), self._mu, self._wd, int(bool(first_step)), _stream())
         _capi.check(st, "sg_weighted_aggregate_peers_f32")
-        _count(1)
+        _count(_sparse_merge_launches())
 
 
 class GuardedDenseLaunchers:

@@ -153,13 +153,16 @@ def test_float32_aggregate_is_correctly_rounded(cuda):
     assert np.array_equal(b.cpu().numpy().view(np.uint32), bw.astype(np.float32).view(np.uint32))
 
 
-def test_guarded_dense_exchange_and_peer_merge(cuda):
+@pytest.mark.parametrize("merge_own", ["", "1"])
+def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own, monkeypatch):
     """The multi-GPU entry points on one GPU (peer pointers may be local): two "ranks" of two
     workers each.  Mixed decisions: each rank's guarded partial (sg_weighted_partial_f32),
     summed in rank order with momentum SGD (sg_peer_reduce_sgd_f32), equals the oracle fold +
     SGD within the fp32 tolerance, and the all-sparse merge over per-worker pointers
     (sg_weighted_aggregate_peers_f32) is a no-op.  All compressed: the reverse, and the peer
-    merge is bit-identical to sg_weighted_aggregate_f32 on the same payloads."""
+    merge is bit-identical to sg_weighted_aggregate_f32 on the same payloads (merge_own "1":
+    both through k_merge_own)."""
+    monkeypatch.setenv("SG_MERGE_OWN", merge_own)
     from paper_2301_08897_b200 import kernels
 
     D, k, P = 100_003, 2, 2
@@ -225,25 +228,26 @@ def test_guarded_dense_exchange_and_peer_merge(cuda):
             assert np.max(np.abs(got - pw)) <= 1e-5 * np.max(np.abs(pw))
 
 
-@pytest.mark.parametrize("workers", [8, 16])
-def test_concentrated_payloads_merge_bit_exact(cuda, workers):
+@pytest.mark.parametrize("workers,hot,cr", [(8, 0.03, 0.02), (16, 0.03, 0.02), (8, 1.0, 0.1), (3, 1.0, 0.3)])
+def test_concentrated_payloads_merge_bit_exact(cuda, workers, hot, cr, monkeypatch):
     """Real gradients concentrate the kept entries in a few layers: here a 3 % region of the
     row carries large values, so its tiles hold far more entries than one staging chunk
     (the merge's multi-chunk path) and the cost-balanced tile ranges split the region over
-    many CTAs.  All-sparse merge + fused momentum SGD through the Top-k kernels' own payloads
+    many CTAs.  The hot=1.0 cases are uniformly dense payloads (cr 0.1 / 0.3: every tile's
+    chunks take the position-owned fold).  All-sparse merge + fused momentum SGD through the Top-k kernels' own payloads
     and tile offsets: aggregate and updated state equal f32(oracle) bit for bit."""
     from paper_2301_08897_b200 import kernels
 
     rng = np.random.default_rng(11)
     W, D = workers, 3_000_017
-    lo, hi = D // 2, D // 2 + D * 3 // 100
+    lo, hi = (D // 2, D // 2 + int(D * hot)) if hot < 1 else (0, D)
     g = []
     for j in range(W):
         x = rng.standard_normal(D, dtype=np.float32) * 1e-3
         x[lo:hi] = rng.standard_normal(hi - lo, dtype=np.float32) * (1 + 0.1 * j)  # the hot layer
         g.append(x.astype(np.float32))
     w = comm_ref.rate_weights(list(range(3, 3 + W)))
-    m = comm_ref.topk_count(D, 0.02)
+    m = comm_ref.topk_count(D, cr)
     bucket = torch.from_numpy(np.stack([np.pad(x, (0, (-D) % 4)) for x in g])).to(cuda)
     idx = torch.empty((W, m), dtype=torch.int32, device=cuda)
     val = torch.empty((W, m), dtype=torch.float32, device=cuda)
@@ -253,21 +257,24 @@ def test_concentrated_payloads_merge_bit_exact(cuda, workers):
     per_tile = np.diff(toff.cpu().numpy(), axis=1).sum(axis=0)
     assert per_tile.max() > 1024  # multi-chunk tiles are exercised
     for j in (0, W - 1):  # the Top-k itself on concentrated data
-        want_i, want_v = comm_ref.topk(g[j].astype(np.float64), 0.02, "threshold")
+        want_i, want_v = comm_ref.topk(g[j].astype(np.float64), cr, "threshold")
         assert np.array_equal(idx[j].cpu().numpy().astype(np.int64), want_i)
         assert np.array_equal(val[j].cpu().numpy().astype(np.float64), want_v)
     payloads = [(D, idx[j].cpu().numpy().astype(np.int64), val[j].cpu().numpy().astype(np.float64)) for j in range(W)]
     want = comm_ref.aggregate(payloads, w)
     p0 = rng.standard_normal(D, dtype=np.float32)
     b0 = rng.standard_normal(D, dtype=np.float32)
-    p = torch.from_numpy(p0.copy()).to(cuda)
-    b = torch.from_numpy(b0.copy()).to(cuda)
-    out = torch.empty(D, dtype=torch.float32, device=cuda)
-    row_ptr = torch.arange(0, (W + 1) * m, m, dtype=torch.int64, device=cuda)
-    kernels.weighted_aggregate(w, D, compressed=torch.ones(W, dtype=torch.uint8, device=cuda), idx=idx, val=val,
-                               row_ptr=row_ptr, tile_off=toff, out=out, params=p, momentum_buf=b, lr=0.05,
-                               momentum=0.9, weight_decay=1e-4, first_step=False)
-    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.astype(np.float32).view(np.uint32))
     pw, bw = comm_ref.sgd_momentum(p0.astype(np.float64), b0.astype(np.float64), want, 0.05, 0.9, 1e-4)
-    assert np.array_equal(p.cpu().numpy().view(np.uint32), pw.astype(np.float32).view(np.uint32))
-    assert np.array_equal(b.cpu().numpy().view(np.uint32), bw.astype(np.float32).view(np.uint32))
+    row_ptr = torch.arange(0, (W + 1) * m, m, dtype=torch.int64, device=cuda)
+    # by density (k_merge_ws for the sparse cases, k_merge_own for hot=1.0), then each forced
+    for mode in ("", "0", "1"):
+        monkeypatch.setenv("SG_MERGE_OWN", mode)
+        p = torch.from_numpy(p0.copy()).to(cuda)
+        b = torch.from_numpy(b0.copy()).to(cuda)
+        out = torch.empty(D, dtype=torch.float32, device=cuda)
+        kernels.weighted_aggregate(w, D, compressed=torch.ones(W, dtype=torch.uint8, device=cuda), idx=idx, val=val,
+                                   row_ptr=row_ptr, tile_off=toff, out=out, params=p, momentum_buf=b, lr=0.05,
+                                   momentum=0.9, weight_decay=1e-4, first_step=False)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want.astype(np.float32).view(np.uint32)), mode
+        assert np.array_equal(p.cpu().numpy().view(np.uint32), pw.astype(np.float32).view(np.uint32)), mode
+        assert np.array_equal(b.cpu().numpy().view(np.uint32), bw.astype(np.float32).view(np.uint32)), mode
