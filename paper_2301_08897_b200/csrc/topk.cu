@@ -58,7 +58,7 @@ template <typename T> struct TopkTraits;
 template <> struct TopkTraits<float> {
     static constexpr int SAMPLE = 16384;
     static constexpr int ROUNDS_MAX = 3;  // after round 0: <= 31 bits left (open top bin)
-    static constexpr int RES = 12288;     // boundary entries resolved inside one CTA
+    static constexpr int RES = 15360;     // boundary entries resolved inside one CTA
 };
 template <> struct TopkTraits<double> {
     static constexpr int SAMPLE = 8192;
@@ -1253,12 +1253,25 @@ k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
         if (slow && !st.done) {
             const K lo = st.lo, span = st.span;
             const int shift = st.shift;
-            for (int seg = 0; seg < a.nseg; ++seg) {
-                const long long n = a.segcnt[(long long)w * a.nseg + seg];
+            // CTA x takes segments x, x + G, ...; its 1024 threads stream each with RS_U
+            // independent loads in flight
+            constexpr int RS_U = 4;
+            for (int seg = x; seg < a.nseg; seg += gridDim.x) {
+                const int n = (int)a.segcnt[(long long)w * a.nseg + seg];
                 const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
-                for (long long i = (long long)x * NT + tid; i < n; i += (long long)gridDim.x * NT) {
-                    const K key = KO::key(cv[i]);
-                    if (key >= lo && key - lo <= span) atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
+                for (int i0 = 0; i0 < n; i0 += RS_U * NT) {
+                    T v[RS_U];
+#pragma unroll
+                    for (int u = 0; u < RS_U; ++u) {
+                        const int i = i0 + u * NT + tid;
+                        v[u] = i < n ? __ldcg(cv + i) : T(0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < RS_U; ++u) {
+                        const K key = KO::key(v[u]);
+                        if (i0 + u * NT + tid < n && key >= lo && key - lo <= span)
+                            atomicAdd(&hist[digit<K>(key, lo, shift, SEL_BINS)], 1u);
+                    }
                 }
             }
             __syncthreads();
