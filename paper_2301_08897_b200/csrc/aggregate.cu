@@ -1073,34 +1073,33 @@ k_merge_ws(const AggArgs<float, TO> a) {
 // ---------------------------------------------------------------------------------------
 // k_merge_own: the all-sparse merge + fused momentum SGD for dense payloads (on average
 // >= MO_DENSITY kept entries per position, e.g. cr 0.1), where k_merge_ws's per-chunk list
-// building is latency-bound.  Position-owned and barrier-light: thread t owns positions
-// [8t, 8t + 8) of the tile and keeps their float64 sums in registers.
-//   (1) every thread starts its p/buf loads for the tile (consumed at the end, so the HBM
-//       latency hides behind (2)-(3));
-//   (2) one pass over the tile's entries (worker runs concatenated) records, for every
-//       (worker, owner), the first entry of the worker's run inside the owner's positions,
-//       and pulls the values into L1;
-//   (3) each owner walks, in ascending worker order -- the reference's fold (comm.py:70-78):
-//       +0, then + w_j * v_j -- the entries of each worker's run that fall in its positions;
-//   (4) momentum SGD (nn.py:167-171 order, binary64) and 128-bit stores.
+// building is latency-bound.  Per tile (4096 positions, 512 threads):
+//   (1) every thread starts the p/buf loads of its 8 positions (consumed at the end, so the
+//       HBM latency hides behind (2)-(3)); warp 0 loads the next tile's worker runs;
+//   (2) the tile's entries (worker runs concatenated) are staged in shared memory, several
+//       per thread with their loads in flight together;
+//   (3) the float64 sums are folded worker by worker in ascending order -- the reference's
+//       fold (comm.py:70-78): +0, then + w_j * v_j.  One worker's positions are distinct, so
+//       its entries scatter without conflicts; a CTA barrier orders consecutive workers;
+//   (4) momentum SGD (nn.py:167-171 order, binary64), 128-bit streaming stores.
 // Tiles are dealt round-robin over a grid of 2 CTAs per SM.  Results are bit-identical to
 // k_merge_ws (the same per-position fold order).
 // ---------------------------------------------------------------------------------------
 constexpr int MO_THREADS = 512;
 constexpr int MO_PER = AG_TILE / MO_THREADS;  // 8 positions per thread
-constexpr unsigned MO_NONE = 0xffffu;
 constexpr int MO_U = 4;  // start-pass entries per thread per round
+constexpr int MO_ECAP = 8192;  // a tile's first MO_ECAP entries are staged in shared memory
+constexpr int MO_SMEM = MO_PER * MO_THREADS * (int)sizeof(double) + MO_ECAP * (int)(sizeof(float) + sizeof(uint16_t));
 static_assert(MO_PER == 8, "two float4 per thread");
-
-SG_DEV void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
 template <typename TO>
 __global__ void __launch_bounds__(MO_THREADS, 2)
 k_merge_own(const AggArgs<float, TO> a) {
     pdl_wait();  // no early trigger: the next kernel's CTAs must not take this grid's SM slots
-    __shared__ uint16_t rstart[MP_MAXW][MO_THREADS];
     extern __shared__ __align__(16) unsigned char mo_smem[];
     double (*sacc)[MO_THREADS] = reinterpret_cast<double (*)[MO_THREADS]>(mo_smem);  // [MO_PER][MO_THREADS]
+    float* st_v = reinterpret_cast<float*>(mo_smem + MO_PER * MO_THREADS * sizeof(double));  // [MO_ECAP]
+    uint16_t* st_q = reinterpret_cast<uint16_t*>(st_v + MO_ECAP);  // [MO_ECAP] position in the tile
     __shared__ const uint32_t* s_ib[MP_MAXW];
     __shared__ const float* s_vb[MP_MAXW];
     __shared__ int s_cnt[MP_MAXW], s_pre[MP_MAXW + 1];
@@ -1112,8 +1111,6 @@ k_merge_own(const AggArgs<float, TO> a) {
         for (int j = 0; j < nw && ok; ++j) ok = a.comp[j] != 0;
         s_ok = ok && merge_is_dense(a);
     }
-    for (int x = tid; x < MP_MAXW * MO_THREADS / 2; x += MO_THREADS)
-        reinterpret_cast<unsigned*>(&rstart[0][0])[x] = 0xffffffffu;
 #pragma unroll
     for (int c = 0; c < MO_PER; ++c) sacc[c][tid] = 0.0;
     __syncthreads();
@@ -1180,59 +1177,52 @@ k_merge_own(const AggArgs<float, TO> a) {
             if (lane == 31) s_pre[nw] = incl;
         }
         __syncthreads();
-        // (2) run starts per (worker, owner); MO_U entries per thread with their loads in flight
-        // together
+        // (2) stage entries [c0, c0 + MO_ECAP) (worker-major) in shared memory, MO_U per thread
+        // with their loads in flight together; (3) fold them worker by worker in ascending
+        // order -- a worker's positions are distinct, so its entries scatter without conflicts,
+        // and a barrier orders consecutive workers
         const int E = s_pre[nw];
-        for (int base = 0; base < E; base += MO_U * MO_THREADS) {
-            unsigned x[MO_U], pr[MO_U];
-            int jw[MO_U], rr[MO_U];
+        for (int c0 = 0; c0 < E; c0 += MO_ECAP) {
+            const int c1 = E - c0 < MO_ECAP ? E : c0 + MO_ECAP;
+            for (int base = c0; base < c1; base += MO_U * MO_THREADS) {
+                unsigned x[MO_U];
+                float vv[MO_U];
 #pragma unroll
-            for (int u = 0; u < MO_U; ++u) {
-                const int e = base + u * MO_THREADS + tid;
-                int j = 0;
-                if (e < E) {
-                    int hi = nw;
-                    while (hi - j > 1) {
-                        const int mid = (j + hi) >> 1;
-                        if (s_pre[mid] <= e) j = mid;
-                        else hi = mid;
+                for (int u = 0; u < MO_U; ++u) {
+                    const int e = base + u * MO_THREADS + tid;
+                    int j = 0;
+                    if (e < c1) {
+                        int hi = nw;
+                        while (hi - j > 1) {
+                            const int mid = (j + hi) >> 1;
+                            if (s_pre[mid] <= e) j = mid;
+                            else hi = mid;
+                        }
+                    }
+                    const int r = e - s_pre[j];
+                    x[u] = e < c1 ? s_ib[j][r] - (uint32_t)tb : 0u;
+                    vv[u] = e < c1 ? s_vb[j][r] : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < MO_U; ++u) {
+                    const int e = base + u * MO_THREADS + tid;
+                    if (e < c1) {
+                        st_q[e - c0] = (uint16_t)x[u];
+                        st_v[e - c0] = vv[u];
                     }
                 }
-                jw[u] = j;
-                rr[u] = e - s_pre[j];
-                x[u] = e < E ? s_ib[j][rr[u]] - (uint32_t)tb : 0u;
-                pr[u] = e < E && lane == 0 && rr[u] > 0 ? s_ib[j][rr[u] - 1] - (uint32_t)tb : 0u;
-                if (e < E) prefetch_l1(s_vb[j] + rr[u]);
             }
-#pragma unroll
-            for (int u = 0; u < MO_U; ++u) {
-                const int e = base + u * MO_THREADS + tid;
-                const unsigned up = __shfl_up_sync(FULL, x[u], 1);
-                const unsigned prev = lane == 0 ? pr[u] : up;
-                if (e < E) {
-                    const unsigned o = x[u] / MO_PER;
-                    if (rr[u] == 0 || prev / MO_PER != o) rstart[jw[u]][o] = (uint16_t)rr[u];
+            __syncthreads();
+            for (int j = 0; j < nw; ++j) {
+                const int lo = s_pre[j] > c0 ? s_pre[j] : c0, hi = s_pre[j + 1] < c1 ? s_pre[j + 1] : c1;
+                if (lo >= hi) continue;  // uniform
+                const double wj = a.w[j];
+                for (int e = lo + tid; e < hi; e += MO_THREADS) {
+                    const unsigned q = st_q[e - c0];
+                    double* sa = &sacc[q % MO_PER][q / MO_PER];
+                    *sa = dadd(*sa, dmul(wj, (double)st_v[e - c0]));
                 }
-            }
-        }
-        __syncthreads();
-        // (3) ascending-worker fold of this thread's positions into sacc[c][tid] (position
-        // q0 + c; the transposed layout keeps a warp's accesses on distinct banks), all +0
-        // between tiles
-        for (int j = 0; j < nw; ++j) {
-            const unsigned r0 = rstart[j][tid];
-            if (r0 == MO_NONE) continue;
-            rstart[j][tid] = (uint16_t)MO_NONE;
-            const uint32_t* ib = s_ib[j];
-            const float* vb = s_vb[j];
-            const int n = s_cnt[j];
-            const double wj = a.w[j];
-            for (int r = (int)r0; r < n; ++r) {
-                const unsigned x = ib[r] - (uint32_t)tb - (uint32_t)q0;
-                if (x >= (unsigned)MO_PER) break;
-                const double v = dmul(wj, (double)vb[r]);
-                double* sa = &sacc[x][tid];
-                *sa = dadd(*sa, v);
+                __syncthreads();
             }
         }
         double acc[MO_PER];
@@ -1287,7 +1277,7 @@ void launch_sparse_merge(const AggArgs<float, TO>& a, int grid, size_t sm, int s
     if (a.own != 0) {
         long long g2 = 2LL * sms;
         if (g2 > a.ntiles) g2 = a.ntiles;
-        const int dsm = MO_PER * MO_THREADS * (int)sizeof(double);
+        const int dsm = MO_SMEM;
         cudaFuncSetAttribute(k_merge_own<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
         launch_pdl(k_merge_own<TO>, dim3((unsigned)g2), dim3(MO_THREADS), (size_t)dsm, stream, a);
         debug_sync("k_merge_own", stream);
