@@ -660,7 +660,7 @@ inline size_t mw_smem_bytes() {
 // take k_merge_own, the sparser ones k_merge_ws; both fold in the same order, so the choice
 // (made on the device from the tile offsets of workers cost_j0..cost_j1, this GPU's own on the
 // peer path) never changes a result.
-constexpr double MO_DENSITY = 0.25;
+constexpr double MO_DENSITY = 0.2;
 template <typename TO>
 SG_DEV bool merge_is_dense(const AggArgs<float, TO>& a) {
     if (a.own >= 0) return a.own != 0;
