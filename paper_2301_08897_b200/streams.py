@@ -227,6 +227,35 @@ class DeviceSampler:
     def set_augmentation(self, table: np.ndarray | None) -> None:
         self.augment = None if table is None else torch.from_numpy(np.ascontiguousarray(table)).to(self.device, dtype=self.dtype)
 
+    def _upload(self, parts):
+        """One pinned host buffer and one H2D copy for every small index array of a step;
+        returns device views (int64, or int32 for parts given as int32)."""
+        sizes = [(a.size * a.itemsize + 7) // 8 for a in parts]
+        total = max(sum(sizes), 1)
+        if getattr(self, "_host", None) is None or self._host.numel() < total:
+            self._host = torch.empty(max(total, 1024), dtype=torch.int64, pin_memory=True)
+            self._dev = torch.empty(max(total, 1024), dtype=torch.int64, device=self.device)
+        else:
+            # the previous step's copy must have left the pinned buffer before it is refilled
+            self._copied.synchronize()
+        h = self._host.numpy()
+        off, spans = 0, []
+        for a, n in zip(parts, sizes):
+            if a.dtype == np.int32:
+                h[off:off + n].view(np.int32)[:a.size] = a
+            else:
+                h[off:off + n] = a
+            spans.append((off, n, a.dtype, a.size))
+            off += n
+        self._dev[:total].copy_(self._host[:total], non_blocking=True)
+        self._copied = torch.cuda.Event()
+        self._copied.record()
+        out = []
+        for o, n, dt, size in spans:
+            v = self._dev[o:o + n]
+            out.append(v.view(torch.int32)[:size] if dt == np.int32 else v[:size])
+        return out
+
     def stage(self, draws: list[range], plan=None, picks=None):
         """Rows of every device's batch (CSR) and the gathered batch.
 
@@ -234,33 +263,33 @@ class DeviceSampler:
         come from :func:`injection_plan` / :func:`injection_picks`.  Returns
         (x [rows, F], y [rows], ptr [n_dev + 1] host int64) with device d's batch in
         rows ptr[d]:ptr[d+1] in the reference's order (own samples, then injected ones).
+        All the step's small index arrays go to the device in one pinned copy.
         """
         dev = self.device
         b = np.array([len(r) for r in draws], dtype=np.int64)
         head = np.array([r.start for r in draws], dtype=np.int64)
-        base_ptr = np.concatenate([[0], np.cumsum(b)])
+        base_ptr = np.concatenate([[0], np.cumsum(b)]).astype(np.int64)
         total = int(base_ptr[-1])
-        rows = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
-        kernels.resolve_stream_rows(
-            torch.from_numpy(head).to(dev), torch.from_numpy(b).to(dev), torch.from_numpy(base_ptr).to(dev),
-            self.pool_ptr, self.pool_rows, total, rows)
         ptr = base_ptr
+        parts = [head, b, base_ptr]
         if plan:
             counts = np.array([c for _, c in plan], dtype=np.int64)
             sizes = b.copy()
             for (s, c) in plan:
                 sizes += c
                 sizes[s] -= c
-            ptr = np.concatenate([[0], np.cumsum(sizes)])
+            ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+            pick_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+            all_picks = np.concatenate(picks).astype(np.int64) if len(picks) else np.zeros(0, dtype=np.int64)
+            senders = np.array([s for s, _ in plan], dtype=np.int32)
+            parts += [senders, pick_ptr, all_picks if all_picks.size else np.zeros(1, dtype=np.int64), ptr]
+        views = self._upload(parts)
+        rows = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+        kernels.resolve_stream_rows(views[0], views[1], views[2], self.pool_ptr, self.pool_rows, total, rows)
+        if plan:
+            d_senders, d_pick_ptr, d_picks, d_ptr = views[3:]
             out_rows = torch.empty(max(int(ptr[-1]), 1), dtype=torch.int64, device=dev)
-            pick_ptr = np.concatenate([[0], np.cumsum(counts)])
-            all_picks = np.concatenate(picks) if len(picks) else np.zeros(0, dtype=np.int64)
-            kernels.inject_rows(
-                torch.from_numpy(base_ptr).to(dev), rows,
-                torch.tensor([s for s, _ in plan], dtype=torch.int32, device=dev),
-                torch.from_numpy(pick_ptr).to(dev),
-                torch.from_numpy(all_picks.astype(np.int64)).to(dev) if all_picks.size else torch.zeros(1, dtype=torch.int64, device=dev),
-                torch.from_numpy(ptr).to(dev), out_rows)
+            kernels.inject_rows(views[2], rows, d_senders, d_pick_ptr, d_picks, d_ptr, out_rows)
             rows = out_rows
         n = int(ptr[-1])
         x = torch.empty((n, self.train_x.shape[1]), dtype=self.dtype, device=dev)
