@@ -125,6 +125,15 @@ int sg_weighted_aggregate_f64(int nw, const double* weights, const uint8_t* comp
                               double lr, double momentum, double weight_decay, int first_step,
                               void* workspace, size_t workspace_bytes, void* stream);
 
+/* Which kernel takes the all-sparse float32 merges of sg_weighted_aggregate_f32 /
+ * sg_weighted_aggregate_peers_f32 (process-wide; the environment variable SG_MERGE_OWN
+ * overrides it): -1 (default) launches both and the device picks by payload density (>= 0.2
+ * kept entries per position: k_merge_own, else k_merge_ws), 0 only k_merge_ws, 1 only
+ * k_merge_own.  Both fold in the same order, so every mode gives bit-identical results; a
+ * caller that knows its density (GradientExchange: W*m/dim) saves the launch of the kernel
+ * that would exit.  No reference counterpart (launch policy only). */
+void sg_set_merge_kernel(int mode);
+
 /* ---- Multi-GPU merge over peer memory (one process per GPU, NVLink) -----------------------
  * The all-sparse case of sg_weighted_aggregate_f32 with fused momentum SGD, where worker j's
  * payload is addressed by per-worker device pointers that may point into other GPUs' memory

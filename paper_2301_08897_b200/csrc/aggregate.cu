@@ -678,6 +678,9 @@ inline int env_int(const char* name, int dflt) {
     return e && *e ? atoi(e) : dflt;
 }
 
+int g_merge_kernel = -1;  // sg_set_merge_kernel
+inline int merge_kernel_mode() { return env_int("SG_MERGE_OWN", g_merge_kernel); }
+
 inline int mw_balance() {
     static const int on = [] {
         const char* e = getenv("SG_MERGE_BALANCE");
@@ -1374,7 +1377,7 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
             a.balance = mw_balance();
             a.cost_j0 = 0;
             a.cost_j1 = nw;
-            a.own = env_int("SG_MERGE_OWN", -1);
+            a.own = merge_kernel_mode();
             launch_sparse_merge(a, grid, sm, sms, stream);
         }
         cudaFuncSetAttribute(k_merge<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM);
@@ -1455,7 +1458,7 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
         a.cost_j0 = j0 < 0 ? 0 : j0;
         a.cost_j1 = j0 < 0 ? nw : j1;
     }
-    a.own = env_int("SG_MERGE_OWN", -1);
+    a.own = merge_kernel_mode();
     launch_sparse_merge(a, grid, sm, sms, stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
@@ -1612,6 +1615,8 @@ int sg_peer_reduce_sgd_f32(int nranks, const float* const* partials, const uint8
                guard_n, (long long)dim, out, params, momentum_buf, lr, momentum, weight_decay, first_step);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
+
+void sg_set_merge_kernel(int mode) { sg::g_merge_kernel = mode < 0 ? -1 : (mode > 0 ? 1 : 0); }
 
 int sg_gather_bytes(int nsrc, const uint8_t* const* src, int64_t each, uint8_t* dst, void* stream) {
     if (nsrc < 1 || nsrc > MAX_WORKERS || each < 1 || !src || !dst) return SG_ERR_INVALID;

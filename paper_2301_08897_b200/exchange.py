@@ -136,6 +136,11 @@ class GradientExchange:
         recs["raw_gate"] = int(raw_gate)
         self.states = self.ops.make_states(recs)
         self.packed = compression and self.world > 1 and dtype == torch.float32
+        if compression and device.type == "cuda" and dtype == torch.float32:
+            # all-sparse merge kernel by payload density (W*m kept entries over dim positions):
+            # only the one that will run is launched; near the 0.2 crossover the device decides
+            dens = self.W * m / dim
+            kernels.set_merge_kernel(0 if dens < 0.1 else (1 if dens >= 0.3 else -1))
         if compression:
             nt1 = kernels.merge_tiles(dim) + 1
             if self.packed:

@@ -27,9 +27,21 @@ def _count(n: int) -> None:
     LAUNCHES["n"] += n
 
 
+_MERGE_MODE = {"mode": -1}
+
+
+def set_merge_kernel(mode: int) -> None:
+    """sg_set_merge_kernel: -1 device picks by density, 0 k_merge_ws only, 1 k_merge_own only."""
+    _capi.load().sg_set_merge_kernel(int(mode))
+    _MERGE_MODE["mode"] = -1 if mode < 0 else (1 if mode > 0 else 0)
+
+
 def _sparse_merge_launches() -> int:
-    """k_merge_ws + k_merge_own (one exits by payload density) unless SG_MERGE_OWN forces one."""
-    return 1 if os.environ.get("SG_MERGE_OWN", "") in ("0", "1") else 2
+    """k_merge_ws + k_merge_own (one exits by payload density) unless one is forced."""
+    env = os.environ.get("SG_MERGE_OWN", "")
+    if env:
+        return 1 if int(env) >= 0 else 2
+    return 2 if _MERGE_MODE["mode"] < 0 else 1
 
 
 def require_cuda(t: torch.Tensor | None = None) -> None:

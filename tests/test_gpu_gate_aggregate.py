@@ -165,6 +165,8 @@ def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own, monkeypatch):
     monkeypatch.setenv("SG_MERGE_OWN", merge_own)
     from paper_2301_08897_b200 import kernels
 
+    kernels.set_merge_kernel(-1)
+
     D, k, P = 100_003, 2, 2
     W = k * P
     rng = np.random.default_rng(7)
@@ -267,6 +269,7 @@ def test_concentrated_payloads_merge_bit_exact(cuda, workers, hot, cr, monkeypat
     pw, bw = comm_ref.sgd_momentum(p0.astype(np.float64), b0.astype(np.float64), want, 0.05, 0.9, 1e-4)
     row_ptr = torch.arange(0, (W + 1) * m, m, dtype=torch.int64, device=cuda)
     # by density (k_merge_ws for the sparse cases, k_merge_own for hot=1.0), then each forced
+    kernels.set_merge_kernel(-1)
     for mode in ("", "0", "1"):
         monkeypatch.setenv("SG_MERGE_OWN", mode)
         p = torch.from_numpy(p0.copy()).to(cuda)

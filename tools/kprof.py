@@ -23,10 +23,11 @@ def main():
     ap.add_argument("--dim", type=int, default=bench.R_DIM)
     ap.add_argument("--cr", type=float, default=0.01)
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--workers", type=int, default=8)
     args = ap.parse_args()
     build.build()
     dev = torch.device("cuda", 0)
-    W = 8
+    W = args.workers
     rates, w = bench.rates_weights(W)
     ex = exchange.GradientExchange(args.dim, W, cr=args.cr, delta=0.3, momentum=0.9, weight_decay=1e-4, device=dev)
     bench.synth_bucket(ex, "heavy", 0)
