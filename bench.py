@@ -36,6 +36,7 @@ METRIC = "aggregated grad elems/sec & HBM GB/s (%roofline) per step at 1/2/4/8 B
 UNIT = "elem/s"
 MEASURED = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
+NVLINK_GBPS = 900.0  # NVLink 5 per direction per GPU (nominal; no nccl-tests busbw taken)
 
 
 def parse():
@@ -316,6 +317,16 @@ def run_ours(args):
         step_bytes = k * 4 * D + 16 * D
     step_s = t_ms / 1e3 / K
     step_roof = {"bytes_per_step": step_bytes, "achieved": step_bytes / step_s / 1e9, "frac": step_bytes / step_s / 1e9 / hbm}
+    # NVLink bytes each GPU receives per step: the other ranks' sparse payloads,
+    # or the dense all-reduce's 2(P-1)/P * 4D (busbw convention); nominal 900 GB/s per direction
+    if world > 1:
+        nvl = (world - 1) * k * 8 * m if (compression and all_sparse) else 2 * (world - 1) / world * 4 * D
+        nvl_frac = nvl / step_s / 1e9 / NVLINK_GBPS
+        step_roof["nvlink"] = {"bytes_per_step": nvl, "achieved": nvl / step_s / 1e9, "peak": NVLINK_GBPS,
+                               "peak_kind": "nominal", "frac": nvl_frac}
+        step_roof["binding"] = "nvlink" if nvl_frac > step_roof["frac"] else "hbm"
+    else:
+        step_roof["binding"] = "hbm"
 
     # ---- end to end through the public API with host buffers --------------------------
     e2e = None
@@ -403,6 +414,7 @@ def run_ours(args):
             },
             "roofline": roof,
             "step_roofline": step_roof,
+            "per_gpu_value": k * D * K / (t_ms / 1e3),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -55,7 +55,8 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     ok = True
     report = {"world": world, "cases": []}
-    for family, cr, delta in (("heavy", 0.01, 0.5), ("normal", 0.01, 0.3), ("mixed", 0.1, 0.5)):
+    # (heavy, 0.1: all compressed at 0.8 kept entries per position -> k_merge_own over peer memory)
+    for family, cr, delta in (("heavy", 0.01, 0.5), ("normal", 0.01, 0.3), ("mixed", 0.1, 0.5), ("heavy", 0.1, 0.5)):
         p, a, paths = run(family, cr, delta, dist.group.WORLD, dev)
         # every rank holds identical bytes
         t = torch.from_numpy(p).to(dev)
