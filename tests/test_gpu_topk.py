@@ -138,3 +138,49 @@ def test_topk_constant_and_all_nan(cuda):
         # the whole row is one tie group: the oversized-boundary (cooperative) resolve ran
         st = kernels.topk_stats(torch.float32, 1, g.size, m, cuda)
         assert int(st[0, 3]) == 1, st
+
+
+@pytest.mark.parametrize("D,cr,fam", [(143_667_240, 0.01, "heavy"), (143_667_240, 0.1, "heavy"),
+                                      ((1 << 30) + 5, 0.01, "ties")])
+def test_topk_full_size_properties(cuda, D, cr, fam):
+    """BASELINE sizes too large for the host oracle (VGG-19, the 1B end of the sweep): the
+    size-independent properties of the reference's selection, checked on the device.  Exactly m
+    ascending indices; values are bit copies; every dropped |g| <= every kept |g| (no element
+    above the threshold T = min kept |g| is dropped, none below is kept); ties at T go to the
+    lowest indices (np.lexsort order); merge offsets count the kept indices below each tile;
+    the squared norms match a float64 reduction."""
+    from paper_2301_08897_b200 import kernels
+
+    m = comm_ref.topk_count(D, cr)
+    ld = (D + 3) // 4 * 4
+    gen = torch.Generator(device=cuda).manual_seed(11)
+    g = torch.randn((1, ld), device=cuda, generator=gen)
+    if fam == "heavy":
+        g.mul_(torch.exp(1.5 * torch.randn((1, ld), device=cuda, generator=gen)))
+    else:  # family (iii): quantised values, so the threshold sits inside a large tie group
+        g.mul_(8).round_().div_(8)
+    g[0, D:] = 0
+    nt = kernels.merge_tiles(D)
+    toff = torch.empty((1, nt + 1), dtype=torch.int32, device=cuda)
+    idx, val, norms2, _, _ = kernels.topk_gate(g, m, dim=D, tile_off=toff)
+    x = g[0, :D]
+    i = idx[0].long()
+    assert i.numel() == m
+    assert bool((i[1:] > i[:-1]).all()) and int(i[0]) >= 0 and int(i[-1]) < D
+    assert torch.equal(val[0].view(torch.int32), x[i].view(torch.int32))
+    a = x.abs()
+    T = float(a[i].min())
+    kept = torch.zeros(D, dtype=torch.bool, device=cuda)
+    kept[i] = True
+    assert int((a > T).sum()) <= m <= int((a >= T).sum())
+    assert not bool((~kept & (a > T)).any())
+    tie = a == T
+    n_tie_kept = m - int((a > T).sum())
+    tie_idx = torch.nonzero(tie).flatten()
+    assert torch.equal(torch.nonzero(tie & kept).flatten(), tie_idx[:n_tie_kept])
+    bounds = torch.searchsorted(i, torch.arange(nt + 1, device=cuda, dtype=torch.int64) * kernels.MERGE_TILE)
+    assert torch.equal(toff[0].long(), bounds)
+    s_full = float((x.double() ** 2).sum())
+    s_topk = float((val[0].double() ** 2).sum())
+    assert abs(float(norms2[0, 0]) - s_full) <= 1e-9 * s_full
+    assert abs(float(norms2[0, 1]) - s_topk) <= 1e-9 * s_topk
