@@ -296,3 +296,96 @@ class DeviceSampler:
         y = torch.empty(n, dtype=torch.int64, device=dev)
         kernels.gather_batch(self.train_x, self.augment, self.train_y, rows[:n], x, y)
         return x, y, ptr
+
+
+class ShardedSampler:
+    """the pool-sharded dataset, with injected samples moved between GPUs
+    instead of a replicated train set.
+
+    One process per GPU; rank r owns the contiguous devices [lo, lo + k) (the exchange's worker
+    sharding) and holds only the train rows of their pools.  Every rank runs the same host
+    planning (stream buffers, ``injection_plan`` / ``injection_picks`` with the shared seeds), so
+    each knows every sender's share count and the layout of the exchanged buffer without a
+    size exchange.  Per step:
+      1. the local devices' own batches: ``DeviceSampler.stage`` on the shard (rows resolved,
+         x = train_x[rows] + augment[rows] gathered on the device);
+      2. each local sender's shared samples (its pre-injection batch at the picked positions)
+         are materialised rows of step 1, so they are gathered into a send buffer;
+      3. one ``all_gather_into_tensor`` (NCCL over NVLink) of the padded send buffers -- the
+         allgatherv of datagen.inject's wire format (datagen.py:182-210, SPEC.md:169);
+      4. each local device's batch = its own rows, then every other sender's shared rows in plan
+         order (datagen.py:204-207), assembled by one device gather.
+    Bit-identical to ``DeviceSampler`` over the replicated set (tools/multi_sampler_check.py).
+    """
+
+    def __init__(self, train_x: np.ndarray, train_y: np.ndarray, pools: list[np.ndarray], lo: int, k: int, *,
+                 group=None, device: torch.device | None = None, dtype: torch.dtype = torch.float64):
+        self.n_dev, self.lo, self.k, self.group = len(pools), lo, k, group
+        local = [np.asarray(pools[d], dtype=np.int64) for d in range(lo, lo + k)]
+        self._rows = np.concatenate(local) if local else np.zeros(0, dtype=np.int64)
+        offs = np.concatenate([[0], np.cumsum([len(p) for p in local])])
+        local_pools = [np.arange(offs[i], offs[i + 1], dtype=np.int64) for i in range(k)]
+        self.inner = DeviceSampler(np.asarray(train_x)[self._rows], np.asarray(train_y)[self._rows], local_pools,
+                                   device=device, dtype=dtype)
+        self.device = self.inner.device
+        self.F = self.inner.train_x.shape[1]
+
+    def set_augmentation(self, table: np.ndarray | None) -> None:
+        self.inner.set_augmentation(None if table is None else np.asarray(table)[self._rows])
+
+    def stage(self, draws: list[range], plan=None, picks=None):
+        """``draws``: all n_dev id ranges (identical on every rank).  Returns (x, y, ptr) for the
+        LOCAL devices: device lo + i's batch in rows ptr[i]:ptr[i + 1]."""
+        import torch.distributed as dist
+
+        lo, k, dev = self.lo, self.k, self.device
+        x_own, y_own, ptr_own = self.inner.stage(draws[lo:lo + k])
+        if not plan:
+            return x_own, y_own, ptr_own
+        world = dist.get_world_size(self.group)
+        kk = [self.n_dev // world] * world  # devices per rank (the exchange's even sharding)
+        owner = np.repeat(np.arange(world), kk)
+        per_rank = np.zeros(world, dtype=np.int64)
+        for s, c in plan:
+            per_rank[owner[s]] += c
+        smax = max(int(per_rank.max()), 1)
+        rank = dist.get_rank(self.group)
+        # 2. send buffer: this rank's senders' shares in plan order (positions in x_own)
+        send_pos = [ptr_own[s - lo] + np.asarray(p, dtype=np.int64)
+                    for (s, c), p in zip(plan, picks) if owner[s] == rank and c]
+        send_pos = np.concatenate(send_pos) if send_pos else np.zeros(0, dtype=np.int64)
+        sx = torch.zeros((smax, self.F), dtype=x_own.dtype, device=dev)
+        sy = torch.zeros(smax, dtype=torch.int64, device=dev)
+        if send_pos.size:
+            d_pos = self.inner._upload([send_pos])[0]
+            kernels.gather_batch(x_own, None, y_own, d_pos, sx[:send_pos.size], sy[:send_pos.size])
+        # 3. allgatherv as one padded all-gather
+        gx = torch.empty((world * smax, self.F), dtype=x_own.dtype, device=dev)
+        gy = torch.empty(world * smax, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(gx, sx, group=self.group)
+        dist.all_gather_into_tensor(gy, sy, group=self.group)
+        # 4. source = [x_own ; gathered]; sender s's shares start at n_own + owner(s)*smax + (its
+        # offset among its rank's senders)
+        n_own = int(ptr_own[-1])
+        start = np.zeros(len(plan), dtype=np.int64)
+        fill = np.zeros(world, dtype=np.int64)
+        for i, (s, c) in enumerate(plan):
+            start[i] = n_own + owner[s] * smax + fill[owner[s]]
+            fill[owner[s]] += c
+        rows, ptr = [], [0]
+        for i in range(k):
+            d = lo + i
+            mine = [np.arange(ptr_own[i], ptr_own[i + 1], dtype=np.int64)]
+            mine += [np.arange(start[j], start[j] + c, dtype=np.int64) for j, (s, c) in enumerate(plan) if s != d and c]
+            rows += mine
+            ptr.append(ptr[-1] + sum(r.size for r in mine))
+        rows = np.concatenate(rows) if rows else np.zeros(0, dtype=np.int64)
+        src_x = torch.cat([x_own, gx])
+        src_y = torch.cat([y_own, gy])
+        n = rows.size
+        x = torch.empty((n, self.F), dtype=x_own.dtype, device=dev)
+        y = torch.empty(n, dtype=torch.int64, device=dev)
+        if n:
+            d_rows = self.inner._upload([rows])[0]
+            kernels.gather_batch(src_x, None, src_y, d_rows, x, y)
+        return x, y, np.asarray(ptr, dtype=np.int64)

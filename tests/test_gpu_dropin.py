@@ -135,3 +135,23 @@ def test_stream_buffer_drives_device_sampler(cuda):
         for q, r in zip(bufs, refs):
             q.enqueue_arrivals(1.0 + 0.001 * sum(b))
             r.enqueue(1.0 + 0.001 * sum(b))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_sharded_sampler_matches_replicated(cuda):
+    """pool-sharded dataset, injected samples moved between GPUs by one
+    all-gather per step; every rank's batches are bit-identical to the replicated sampler's."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    n = 4 if torch.cuda.device_count() >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", str(ROOT / "tools" / "multi_sampler_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert rep["ok"] and rep["world"] == n and rep["bit_identical_to_replicated"]
