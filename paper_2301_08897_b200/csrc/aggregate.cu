@@ -661,16 +661,31 @@ inline size_t mw_smem_bytes() {
 // (made on the device from the tile offsets of workers cost_j0..cost_j1, this GPU's own on the
 // peer path) never changes a result.
 constexpr double MO_DENSITY = 0.2;
+// Warp-cooperative (call from a whole warp): 1 if every worker compressed and the sparse
+// merge of this call belongs to the kernel that asked (want_dense: k_merge_own), else 0.
+// One load per lane, so the test costs one round trip.
 template <typename TO>
-SG_DEV bool merge_is_dense(const AggArgs<float, TO>& a) {
-    if (a.own >= 0) return a.own != 0;
-    long long tot = 0;
-    const long long ntl = a.ntiles;
-    for (int j = a.cost_j0; j < a.cost_j1; ++j)
-        tot += a.peer ? (long long)(a.offw[j][ntl] - a.offw[j][0])
-                      : (long long)(a.off[(long long)j * (ntl + 1) + ntl] - a.off[(long long)j * (ntl + 1)]);
-    const int nl = a.cost_j1 - a.cost_j0;
-    return nl > 0 && (double)tot * (double)a.nw >= MO_DENSITY * (double)a.dim * (double)nl;
+SG_DEV int sparse_merge_is_mine(const AggArgs<float, TO>& a, bool want_dense) {
+    const int lane = threadIdx.x & 31, nw = a.nw;
+    if (nw > MP_MAXW) return 0;
+    const bool comp = lane >= nw || a.comp[lane] != 0;
+    long long part = 0;
+    if (a.own < 0 && lane >= a.cost_j0 && lane < a.cost_j1) {
+        const long long ntl = a.ntiles;
+        part = a.peer ? (long long)(a.offw[lane][ntl] - a.offw[lane][0])
+                      : (long long)(a.off[(long long)lane * (ntl + 1) + ntl] - a.off[(long long)lane * (ntl + 1)]);
+    }
+    const bool all_comp = __all_sync(FULL, comp);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+    bool dense;
+    if (a.own >= 0) {
+        dense = a.own != 0;
+    } else {
+        const int nl = a.cost_j1 - a.cost_j0;
+        dense = nl > 0 && (double)part * (double)nw >= MO_DENSITY * (double)a.dim * (double)nl;
+    }
+    return all_comp && dense == want_dense;
 }
 
 inline int env_int(const char* name, int dflt) {
@@ -715,10 +730,9 @@ k_merge_ws(const AggArgs<float, TO> a) {
     __shared__ int s_ok;
     const int tid = threadIdx.x;
     const int nw = a.nw;
-    if (tid == 0) {
-        int ok = nw <= MP_MAXW;
-        for (int j = 0; j < nw && ok; ++j) ok = a.comp[j] != 0;
-        s_ok = ok && !merge_is_dense(a);
+    if (tid < 32) {
+        const int mine = sparse_merge_is_mine(a, false);
+        if (tid == 0) s_ok = mine;
     }
     __syncthreads();
     if (!s_ok) return;  // not all-sparse (k_merge), or dense payloads (k_merge_own)
@@ -1090,9 +1104,8 @@ k_merge_ws(const AggArgs<float, TO> a) {
 // ---------------------------------------------------------------------------------------
 constexpr int MO_THREADS = 512;
 constexpr int MO_PER = AG_TILE / MO_THREADS;  // 8 positions per thread
-constexpr int MO_U = 4;  // start-pass entries per thread per round
-constexpr int MO_ECAP = 8192;  // a tile's first MO_ECAP entries are staged in shared memory
-constexpr int MO_SMEM = MO_PER * MO_THREADS * (int)sizeof(double) + MO_ECAP * (int)(sizeof(float) + sizeof(uint16_t));
+constexpr int MO_ECAP = 4096;  // entries staged per chunk (a whole tile's, unless oversized)
+constexpr int MO_SMEM = MO_PER * MO_THREADS * (int)sizeof(double) + 2 * MO_ECAP * (int)(sizeof(float) + sizeof(uint32_t));
 static_assert(MO_PER == 8, "two float4 per thread");
 
 template <typename TO>
@@ -1101,27 +1114,26 @@ k_merge_own(const AggArgs<float, TO> a) {
     pdl_wait();  // no early trigger: the next kernel's CTAs must not take this grid's SM slots
     extern __shared__ __align__(16) unsigned char mo_smem[];
     double (*sacc)[MO_THREADS] = reinterpret_cast<double (*)[MO_THREADS]>(mo_smem);  // [MO_PER][MO_THREADS]
-    float* st_v = reinterpret_cast<float*>(mo_smem + MO_PER * MO_THREADS * sizeof(double));  // [MO_ECAP]
-    uint16_t* st_q = reinterpret_cast<uint16_t*>(st_v + MO_ECAP);  // [MO_ECAP] position in the tile
-    __shared__ const uint32_t* s_ib[MP_MAXW];
-    __shared__ const float* s_vb[MP_MAXW];
-    __shared__ int s_cnt[MP_MAXW], s_pre[MP_MAXW + 1];
+    float* st_v0 = reinterpret_cast<float*>(mo_smem + MO_PER * MO_THREADS * sizeof(double));  // [2][MO_ECAP]
+    uint32_t* st_i0 = reinterpret_cast<uint32_t*>(st_v0 + 2 * MO_ECAP);                      // [2][MO_ECAP]
+    __shared__ const uint32_t* s_ib[2][MP_MAXW];  // run sets, double-buffered by tile parity
+    __shared__ const float* s_vb[2][MP_MAXW];
+    __shared__ int s_pre[2][MP_MAXW + 1];
     __shared__ int s_ok;
     const int tid = threadIdx.x, lane = tid & 31;
     const int nw = a.nw;
-    if (tid == 0) {
-        int ok = nw <= MP_MAXW;
-        for (int j = 0; j < nw && ok; ++j) ok = a.comp[j] != 0;
-        s_ok = ok && merge_is_dense(a);
+    if (tid < 32) {
+        const int mine = sparse_merge_is_mine(a, true);
+        if (tid == 0) s_ok = mine;
     }
 #pragma unroll
     for (int c = 0; c < MO_PER; ++c) sacc[c][tid] = 0.0;
     __syncthreads();
     if (!s_ok) return;  // not all-sparse (k_merge), or sparse payloads (k_merge_ws)
-    const long long ntl = a.ntiles;
+    const long long ntl = a.ntiles, G = gridDim.x;
     const bool first = a.first != 0;
     const int q0 = tid * MO_PER;
-    // warp 0 lane j < nw: worker j's run [lo, lo + cnt) of the next tile, loaded a tile ahead
+    // warp 0 lane j < nw: worker j's run [lo, lo + cnt) of a tile
     auto load_run = [&](long long t, int& lo, int& cnt) {
         lo = 0;
         cnt = 0;
@@ -1136,12 +1148,61 @@ k_merge_own(const AggArgs<float, TO> a) {
             }
         }
     };
+    auto publish_runs = [&](int b, int lo, int cnt) {  // warp 0: run set b <- (lo, cnt) per lane
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane < nw) {
+            s_ib[b][lane] = (a.peer ? a.idxw[lane] : a.idx + a.row_ptr[lane]) + lo;
+            s_vb[b][lane] = (a.peer ? a.valw[lane] : a.val + a.row_ptr[lane]) + lo;
+            s_pre[b][lane] = incl - cnt;
+        }
+        if (lane == 31) s_pre[b][nw] = incl;
+    };
+    // entries [c0, c1) of run set b into stage b, asynchronously (cp.async, one group)
+    auto stage = [&](int b, int c0, int c1) {
+        for (int e = c0 + tid; e < c1; e += MO_THREADS) {
+            int j = 0, hi = nw;
+            while (hi - j > 1) {
+                const int mid = (j + hi) >> 1;
+                if (s_pre[b][mid] <= e) j = mid;
+                else hi = mid;
+            }
+            const int r = e - s_pre[b][j];
+            cp_async4(st_i0 + b * MO_ECAP + (e - c0), s_ib[b][j] + r);
+            cp_async4(st_v0 + b * MO_ECAP + (e - c0), s_vb[b][j] + r);
+        }
+        cp_async_commit();
+    };
+    // prologue: runs and first chunk of this CTA's first tile; runs of the second prefetched
     int nlo = 0, ncnt = 0;
-    if (tid < 32) load_run(blockIdx.x, nlo, ncnt);
-    for (long long t = blockIdx.x; t < ntl; t += gridDim.x) {
+    if (tid < 32) {
+        int lo, cnt;
+        load_run(blockIdx.x, lo, cnt);
+        publish_runs(0, lo, cnt);
+        load_run(blockIdx.x + G, nlo, ncnt);
+    }
+    __syncthreads();
+    {
+        const int E0 = s_pre[0][nw];
+        stage(0, 0, E0 < MO_ECAP ? E0 : MO_ECAP);
+    }
+    int it = 0;
+    for (long long t = blockIdx.x; t < ntl; t += G, ++it) {
+        const int b = it & 1;
         const long long tb = t * AG_TILE;
         const bool full = tb + AG_TILE <= a.dim;
-        // (1) p/buf of this thread's positions
+        // (1) the next tile's runs into set b ^ 1 and the next tile's chunk into stage b ^ 1
+        // (both last read by the previous tile's fold, which every thread has left)
+        __syncthreads();
+        if (tid < 32) {
+            publish_runs(b ^ 1, nlo, ncnt);
+            load_run(t + 2 * G, nlo, ncnt);
+        }
+        // (2) p/buf of this thread's positions (consumed by the SGD at the end)
         float pv[MO_PER], bv[MO_PER];
         if (full) {
             const float4* pp = reinterpret_cast<const float4*>(a.p + tb + q0);
@@ -1160,73 +1221,40 @@ k_merge_own(const AggArgs<float, TO> a) {
                 bv[c] = ok ? a.buf[tb + q0 + c] : 0.f;
             }
         }
-        // the tile's worker runs (warp 0); the previous tile's walks are complete
-        __syncthreads();
-        if (tid < 32) {
-            const int lo = nlo, cnt = ncnt;
-            load_run(t + gridDim.x, nlo, ncnt);
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (lane < nw) {
-                s_ib[lane] = (a.peer ? a.idxw[lane] : a.idx + a.row_ptr[lane]) + lo;
-                s_vb[lane] = (a.peer ? a.valw[lane] : a.val + a.row_ptr[lane]) + lo;
-                s_cnt[lane] = cnt;
-                s_pre[lane] = incl - cnt;
-            }
-            if (lane == 31) s_pre[nw] = incl;
+        __syncthreads();  // run set b ^ 1 published
+        // (3) the next tile's first chunk goes in flight into stage b ^ 1 while this one folds
+        if (t + G < ntl) {
+            const int En = s_pre[b ^ 1][nw];
+            stage(b ^ 1, 0, En < MO_ECAP ? En : MO_ECAP);
+        } else {
+            cp_async_commit();
         }
-        __syncthreads();
-        // (2) stage entries [c0, c0 + MO_ECAP) (worker-major) in shared memory, MO_U per thread
-        // with their loads in flight together; (3) fold them worker by worker in ascending
-        // order -- a worker's positions are distinct, so its entries scatter without conflicts,
-        // and a barrier orders consecutive workers
-        const int E = s_pre[nw];
+        cp_async_wait<1>();  // this thread's copies of this tile's first chunk have landed
+        __syncthreads();     // everyone's
+        // (4) fold worker by worker in ascending order (comm.py:70-78: +0, then + w_j * v_j);
+        // a worker's positions are distinct, so its entries scatter without conflicts
+        const int E = s_pre[b][nw];
         for (int c0 = 0; c0 < E; c0 += MO_ECAP) {
             const int c1 = E - c0 < MO_ECAP ? E : c0 + MO_ECAP;
-            for (int base = c0; base < c1; base += MO_U * MO_THREADS) {
-                unsigned x[MO_U];
-                float vv[MO_U];
-#pragma unroll
-                for (int u = 0; u < MO_U; ++u) {
-                    const int e = base + u * MO_THREADS + tid;
-                    int j = 0;
-                    if (e < c1) {
-                        int hi = nw;
-                        while (hi - j > 1) {
-                            const int mid = (j + hi) >> 1;
-                            if (s_pre[mid] <= e) j = mid;
-                            else hi = mid;
-                        }
-                    }
-                    const int r = e - s_pre[j];
-                    x[u] = e < c1 ? s_ib[j][r] - (uint32_t)tb : 0u;
-                    vv[u] = e < c1 ? s_vb[j][r] : 0.f;
-                }
-#pragma unroll
-                for (int u = 0; u < MO_U; ++u) {
-                    const int e = base + u * MO_THREADS + tid;
-                    if (e < c1) {
-                        st_q[e - c0] = (uint16_t)x[u];
-                        st_v[e - c0] = vv[u];
-                    }
-                }
+            if (c0 > 0) {  // oversized tile: later chunks are staged synchronously into stage b
+                stage(b, c0, c1);
+                cp_async_wait<0>();
+                __syncthreads();
             }
-            __syncthreads();
+            const uint32_t* si = st_i0 + b * MO_ECAP;
+            const float* sv = st_v0 + b * MO_ECAP;
             for (int j = 0; j < nw; ++j) {
-                const int lo = s_pre[j] > c0 ? s_pre[j] : c0, hi = s_pre[j + 1] < c1 ? s_pre[j + 1] : c1;
+                const int lo = s_pre[b][j] > c0 ? s_pre[b][j] : c0, hi = s_pre[b][j + 1] < c1 ? s_pre[b][j + 1] : c1;
                 if (lo >= hi) continue;  // uniform
                 const double wj = a.w[j];
                 for (int e = lo + tid; e < hi; e += MO_THREADS) {
-                    const unsigned q = st_q[e - c0];
+                    const unsigned q = si[e - c0] - (uint32_t)tb;
                     double* sa = &sacc[q % MO_PER][q / MO_PER];
-                    *sa = dadd(*sa, dmul(wj, (double)st_v[e - c0]));
+                    *sa = dadd(*sa, dmul(wj, (double)sv[e - c0]));
                 }
                 __syncthreads();
             }
+            if (c1 < E) __syncthreads();  // stage b is restaged for the next chunk
         }
         double acc[MO_PER];
 #pragma unroll
@@ -1234,7 +1262,7 @@ k_merge_own(const AggArgs<float, TO> a) {
             acc[c] = sacc[c][tid];
             sacc[c][tid] = 0.0;
         }
-        // (4) momentum SGD, stores
+        // (5) momentum SGD, stores
         double pd[MO_PER], bd[MO_PER];
 #pragma unroll
         for (int c = 0; c < MO_PER; ++c) {
@@ -1265,6 +1293,7 @@ k_merge_own(const AggArgs<float, TO> a) {
             }
         }
     }
+    cp_async_wait<0>();
 }
 
 

@@ -137,10 +137,10 @@ class GradientExchange:
         self.states = self.ops.make_states(recs)
         self.packed = compression and self.world > 1 and dtype == torch.float32
         if compression and device.type == "cuda" and dtype == torch.float32:
-            # all-sparse merge kernel by payload density (W*m kept entries over dim positions):
-            # only the one that will run is launched; near the 0.2 crossover the device decides
-            dens = self.W * m / dim
-            kernels.set_merge_kernel(0 if dens < 0.1 else (1 if dens >= 0.3 else -1))
+            # all-sparse merge kernel by payload density: an all-compressed step always carries
+            # exactly W*m entries, so the host knows the device's choice (>= 0.2 per position:
+            # k_merge_own) and launches only that kernel
+            kernels.set_merge_kernel(1 if self.W * m >= 0.2 * dim else 0)
         if compression:
             nt1 = kernels.merge_tiles(dim) + 1
             if self.packed:
