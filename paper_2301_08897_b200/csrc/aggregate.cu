@@ -158,6 +158,7 @@ template <typename TI, typename TO> struct AggArgs {
     int guard_n, guard_mode;
     int balance;  // k_merge_ws: cost-balanced tile ranges (else equal ranges)
     int own;        // all-sparse merge kernel: -1 by density, 0 k_merge_ws, 1 k_merge_own
+    int pf;         // k_merge_own: prefetch the next tile's p / buf into L2
     int cost_j0, cost_j1;  // workers whose offsets estimate the tile costs (local memory)
 };
 
@@ -1164,16 +1165,15 @@ k_merge_own(const AggArgs<float, TO> a) {
     };
     // entries [c0, c1) of run set b into stage b, asynchronously (cp.async, one group)
     auto stage = [&](int b, int c0, int c1) {
-        for (int e = c0 + tid; e < c1; e += MO_THREADS) {
-            int j = 0, hi = nw;
-            while (hi - j > 1) {
-                const int mid = (j + hi) >> 1;
-                if (s_pre[b][mid] <= e) j = mid;
-                else hi = mid;
+        for (int j = 0; j < nw; ++j) {  // run by run: no per-entry search for the worker
+            const int pj = s_pre[b][j];
+            const int lo = pj > c0 ? pj : c0, hi = s_pre[b][j + 1] < c1 ? s_pre[b][j + 1] : c1;
+            const uint32_t* ib = s_ib[b][j] - pj;
+            const float* vb = s_vb[b][j] - pj;
+            for (int e = lo + tid; e < hi; e += MO_THREADS) {
+                cp_async4(st_i0 + b * MO_ECAP + (e - c0), ib + e);
+                cp_async4(st_v0 + b * MO_ECAP + (e - c0), vb + e);
             }
-            const int r = e - s_pre[b][j];
-            cp_async4(st_i0 + b * MO_ECAP + (e - c0), s_ib[b][j] + r);
-            cp_async4(st_v0 + b * MO_ECAP + (e - c0), s_vb[b][j] + r);
         }
         cp_async_commit();
     };
@@ -1201,6 +1201,13 @@ k_merge_own(const AggArgs<float, TO> a) {
         if (tid < 32) {
             publish_runs(b ^ 1, nlo, ncnt);
             load_run(t + 2 * G, nlo, ncnt);
+        } else if (tid < 34 && a.pf && t + G < ntl) {
+            // the next tile's p / buf into L2 now, so its loads in (2) are L2 hits while HBM
+            // streams during this tile's fold
+            const long long tn = (t + G) * AG_TILE;
+            const long long n = a.dim - tn < AG_TILE ? a.dim - tn : AG_TILE;
+            const unsigned bytes = (unsigned)(n * sizeof(float)) & ~15u;
+            if (bytes) bulk_prefetch_l2((tid == 32 ? a.p : a.buf) + tn, bytes);
         }
         // (2) p/buf of this thread's positions (consumed by the SGD at the end)
         float pv[MO_PER], bv[MO_PER];
@@ -1307,11 +1314,13 @@ void launch_sparse_merge(const AggArgs<float, TO>& a, int grid, size_t sm, int s
         debug_sync("k_merge_ws", stream);
     }
     if (a.own != 0) {
+        AggArgs<float, TO> ao = a;
+        ao.pf = env_int("SG_MERGE_PF", 1);
         long long g2 = 2LL * sms;
         if (g2 > a.ntiles) g2 = a.ntiles;
         const int dsm = MO_SMEM;
         cudaFuncSetAttribute(k_merge_own<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
-        launch_pdl(k_merge_own<TO>, dim3((unsigned)g2), dim3(MO_THREADS), (size_t)dsm, stream, a);
+        launch_pdl(k_merge_own<TO>, dim3((unsigned)g2), dim3(MO_THREADS), (size_t)dsm, stream, ao);
         debug_sync("k_merge_own", stream);
     }
 }

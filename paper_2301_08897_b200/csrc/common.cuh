@@ -216,6 +216,11 @@ SG_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memo
 SG_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 SG_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 SG_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Bulk prefetch of [src, src + bytes) into L2 (no registers, no shared memory, no completion);
+// src 16-byte aligned, bytes a multiple of 16.
+SG_DEV void bulk_prefetch_l2(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // 4-byte asynchronous global -> shared copy (LDGSTS) and its group fences.
 SG_DEV void cp_async4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
