@@ -1134,6 +1134,13 @@ k_merge_own(const AggArgs<float, TO> a) {
     const long long ntl = a.ntiles, G = gridDim.x;
     const bool first = a.first != 0;
     const int q0 = tid * MO_PER;
+    // warp 0 lane j < nw: worker j's payload base, read once (not a global load per tile)
+    const uint32_t* ib_base = nullptr;
+    const float* vb_base = nullptr;
+    if (tid < nw) {
+        ib_base = a.peer ? a.idxw[lane] : a.idx + a.row_ptr[lane];
+        vb_base = a.peer ? a.valw[lane] : a.val + a.row_ptr[lane];
+    }
     // warp 0 lane j < nw: worker j's run [lo, lo + cnt) of a tile
     auto load_run = [&](long long t, int& lo, int& cnt) {
         lo = 0;
@@ -1157,8 +1164,8 @@ k_merge_own(const AggArgs<float, TO> a) {
             if (lane >= o) incl += y;
         }
         if (lane < nw) {
-            s_ib[b][lane] = (a.peer ? a.idxw[lane] : a.idx + a.row_ptr[lane]) + lo;
-            s_vb[b][lane] = (a.peer ? a.valw[lane] : a.val + a.row_ptr[lane]) + lo;
+            s_ib[b][lane] = ib_base + lo;
+            s_vb[b][lane] = vb_base + lo;
             s_pre[b][lane] = incl - cnt;
         }
         if (lane == 31) s_pre[b][nw] = incl;
