@@ -241,7 +241,18 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL prints its version line on fd 1 when the communicator comes up: point fd 1 at
+        # stderr for that, so stdout carries only the JSON line
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            os.dup2(saved, 1)
+            os.close(saved)
         group = dist.group.WORLD
     build.build()
     W, D = args.workers, args.dim
