@@ -50,9 +50,9 @@ def parse():
     ap.add_argument("--workers", type=int, default=8)
     ap.add_argument("--cr", type=float, default=0.01)
     ap.add_argument("--delta", type=float, default=0.3)
-    ap.add_argument("--family", choices=["heavy", "normal"], default="heavy")
-    ap.add_argument("--cpu-dim", type=int, default=1 << 22, help="per-worker gradient length of the CPU sample")
-    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--family", choices=["heavy", "normal", "mixed"], default="heavy")
+    ap.add_argument("--cpu-steps", type=int, default=1, help="timed reference steps of our line's cpu_baseline")
+    ap.add_argument("--cpu-variant", choices=["B", "A"], default="B", help="A: also time one serial 1-core step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -75,88 +75,250 @@ def rates_weights(W: int):
 
 
 # ---------------------------------------------------------------------------------------
-# CPU leg: the oracle port of the reference path (oracle/comm_ref.py), timed on host cores
+# CPU leg: the UNMODIFIED reference (streamsgd from baseline/_ref, tools/install_ref.py) at the
+# bench's own shape, timed on the host cores.  The oracle port (oracle/comm_ref.py) is only a
+# declared fallback when baseline/_ref is absent ("kind": "port").
+#
+# One reference step = the per-iteration hot path of engine.py:248-283 minus the MLP:
+#   W x comm.compression_gate(g_j, state_j)       (comm.py:129-160, np.lexsort Top-k)
+#   comm.weighted_aggregate(payloads, r)          (comm.py:67-78)
+#   nn.sgd_momentum_step(opt, params, agg, lr)    (nn.py:161-172)
+# Variant B (SPEC.md:454 allows per-device parallelism): the W gates run in W
+# persistent worker processes (one per device, gradients in shared memory, one OpenBLAS
+# thread each), the aggregate and the update run serially in the parent.  Variant A (one
+# core, everything serial) is `python bench.py --impl reference --cpu-variant A`.
 # ---------------------------------------------------------------------------------------
-def _cpu_gate(args):
-    g, cr, delta = args
-    from oracle import comm_ref
-
-    st = comm_ref.GateState(cr, delta)
-    c, payload, _, _, _ = comm_ref.gate(g, st, "lexsort")
-    return c, payload
+REF_DIR = ROOT / "baseline" / "_ref"
 
 
-def cpu_synthetic(W: int, D: int, family: str, seed: int = 0):
-    rng = np.random.default_rng(seed)
-    out = []
-    for j in range(W):
-        z = rng.standard_normal(D, dtype=np.float32)
-        if family == "heavy":
-            g = np.sign(z) * np.exp(1.5 * rng.standard_normal(D, dtype=np.float32))
-        else:
-            g = z
-        out.append((g * (1 + 0.1 * j)).astype(np.float32).astype(np.float64))
-    return out
+def _ref_modules():
+    """(comm, nn, kind): the reference modules from baseline/_ref, else the oracle port."""
+    if (REF_DIR / "streamsgd" / "comm.py").exists():
+        if str(REF_DIR) not in sys.path:
+            sys.path.insert(0, str(REF_DIR))
+        import streamsgd.comm as rcomm
+        import streamsgd.nn as rnn
+
+        return rcomm, rnn, "reference"
+    return None, None, "port"
 
 
-def cpu_step_time(grads, weights, cr, delta, compression, pool):
-    """One reference step on the host: W gates (process pool), aggregate, momentum SGD."""
-    from oracle import comm_ref
+def _cpu_grad(D, family, j, seed=0):
+    """Worker j's synthetic gradient on the host: the bench's distributions,
+    float32 values held as float64 (the reference's dtype)."""
+    rng = np.random.default_rng(1000 * seed + j)
+    z = rng.standard_normal(D, dtype=np.float32)
+    if family == "heavy" or (family == "mixed" and j % 2 == 0):
+        z = np.sign(z) * np.exp(np.float32(1.5) * rng.standard_normal(D, dtype=np.float32))
+    return (z * np.float32(1 + 0.1 * j)).astype(np.float32).astype(np.float64)
 
-    D = len(grads[0])
-    t0 = time.perf_counter()
-    if compression:
-        res = pool.map(_cpu_gate, [(g, cr, delta) for g in grads])
-        payloads = [(D, *p) if c else p for c, p in res]
+
+def _gate_worker(conn, j, D, family, cr, delta, shm_name):
+    """Persistent device process j: owns g_j (shared memory) and its CompressionState."""
+    from multiprocessing import shared_memory
+
+    rcomm, _, kind = _ref_modules()
+    shm = shared_memory.SharedMemory(name=shm_name)
+    g = np.ndarray((D,), dtype=np.float64, buffer=shm.buf)
+    g[:] = _cpu_grad(D, family, j)
+    if kind == "reference":
+        state = rcomm.CompressionState(cr=cr, delta=delta)
     else:
-        payloads = grads
-    agg = comm_ref.aggregate(payloads, weights)
-    comm_ref.sgd_momentum(np.zeros(D), None, agg, 0.01, 0.9, 1e-4)
-    return time.perf_counter() - t0
+        from oracle import comm_ref
+
+        state = comm_ref.GateState(cr, delta)
+    conn.send("ready")
+    while True:
+        cmd = conn.recv()
+        if cmd == "stop":
+            break
+        if kind == "reference":
+            dec = rcomm.compression_gate(g, state)
+            # a dense payload IS the input array (comm.py:160): the parent maps the same memory
+            conn.send(("sparse", dec.payload) if dec.compressed else ("dense", None))
+        else:
+            c, payload, _, _, _ = comm_ref.gate(g, state, "lexsort")
+            conn.send(("sparse", (D, *payload)) if c else ("dense", None))
+    del g
+    shm.close()
+
+
+class CpuReference:
+    """W persistent gate processes + the serial aggregate/update in this process."""
+
+    def __init__(self, W, D, family, cr, delta, compression=True):
+        import multiprocessing as mp
+        from multiprocessing import shared_memory
+
+        self.W, self.D, self.cr, self.delta, self.compression = W, D, cr, delta, compression
+        self.comm, self.nn, self.kind = _ref_modules()
+        _, self.w = rates_weights(W)
+        self.lr = 0.1 * sum(rates_weights(W)[0]) / (W * 64)
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"  # inherited by the spawned gate processes
+        ctx = mp.get_context("spawn")
+        self.shm = [shared_memory.SharedMemory(create=True, size=8 * D) for _ in range(W)]
+        self.g = [np.ndarray((D,), dtype=np.float64, buffer=m.buf) for m in self.shm]
+        self.conns, self.procs = [], []
+        for j in range(W):
+            a, b = ctx.Pipe()
+            pr = ctx.Process(target=_gate_worker, args=(b, j, D, family, cr, delta, self.shm[j].name), daemon=True)
+            pr.start()
+            self.conns.append(a)
+            self.procs.append(pr)
+        for c in self.conns:
+            assert c.recv() == "ready"
+        self.params = np.zeros(D)
+        if self.kind == "reference":
+            self.opt = self.nn.OptimizerState(momentum=0.9, weight_decay=1e-4)
+
+    def step(self) -> float:
+        from oracle import comm_ref  # port fallback only
+
+        t0 = time.perf_counter()
+        if self.compression:
+            for c in self.conns:
+                c.send("step")
+            payloads = []
+            for j, c in enumerate(self.conns):
+                what, payload = c.recv()
+                payloads.append(payload if what == "sparse" else self.g[j])
+        else:
+            payloads = list(self.g)
+        if self.kind == "reference":
+            agg = self.comm.weighted_aggregate(payloads, self.w)
+            self.nn.sgd_momentum_step(self.opt, self.params, agg, self.lr)
+        else:
+            agg = comm_ref.aggregate(payloads, self.w)
+            comm_ref.sgd_momentum(self.params, None, agg, self.lr, 0.9, 1e-4)
+        return time.perf_counter() - t0
+
+    def close(self):
+        for c in self.conns:
+            try:
+                c.send("stop")
+            except Exception:
+                pass
+        for pr in self.procs:
+            pr.join(timeout=10)
+        for m in self.shm:
+            m.close()
+            m.unlink()
+
+
+def _cpu_serial_step(W, D, family, cr, delta, q):
+    """Variant A: one process, OPENBLAS_NUM_THREADS=1, the W gates one after another."""
+    rcomm, rnn, kind = _ref_modules()
+    _, w = rates_weights(W)
+    gs = [_cpu_grad(D, family, j) for j in range(W)]
+    states = [rcomm.CompressionState(cr=cr, delta=delta) for _ in range(W)]
+    t0 = time.perf_counter()
+    payloads = [rcomm.compression_gate(g, s).payload for g, s in zip(gs, states)]
+    agg = rcomm.weighted_aggregate(payloads, w)
+    rnn.sgd_momentum_step(rnn.OptimizerState(momentum=0.9, weight_decay=1e-4), np.zeros(D), agg, 0.01)
+    q.put(time.perf_counter() - t0)
+
+
+def host_info():
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = "unknown"
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name', '?')} {b.get('version', '?')}"
+    except Exception:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "numpy": np.__version__, "blas": blas}
 
 
 def cpu_measure(args, W, steps, warmup=1):
+    """Variant B at the bench's D: `steps` timed reference steps after `warmup` untimed ones."""
+    ref = CpuReference(W, args.dim, args.family, args.cr, args.delta, args.workload == "topk")
+    try:
+        for _ in range(warmup):
+            ref.step()
+        times = [ref.step() for _ in range(steps)]
+    finally:
+        ref.close()
+    t = statistics.median(times)
+    hi = host_info()
+    src = ("unmodified streamsgd (baseline/_ref): comm.compression_gate x W, comm.weighted_aggregate, "
+           "nn.sgd_momentum_step" if ref.kind == "reference" else "oracle port oracle/comm_ref.py (baseline/_ref absent)")
+    return {
+        "value": W * args.dim / t,
+        "unit": UNIT,
+        "cores": W,
+        "kind": ref.kind,
+        "sample": f"the full bench workload: W={W} workers x D={args.dim} f64 (fp32-valued, {args.family} family), "
+                  f"cr {args.cr}, delta {args.delta}, per step; {src}; variant B: {W} gate processes "
+                  f"(1 OpenBLAS thread each) + serial aggregate/update; median of {steps} steps after {warmup} "
+                  f"warm-up; host {hi['cpu_model']} ({hi['cpu_count']} logical CPUs), numpy {hi['numpy']}, {hi['blas']}",
+        "step_s": t,
+        "steps_s": times,
+        "host": hi,
+        "same_config": True,
+    }
+
+
+def cpu_measure_serial(args, W):
+    """Variant A: one timed serial step in a fresh single-threaded process."""
     import multiprocessing as mp
 
-    _, w = rates_weights(W)
-    grads = cpu_synthetic(W, args.cpu_dim, args.family)
-    cores = min(W, os.cpu_count() or 1)
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ctx = mp.get_context("spawn")
-    with ctx.Pool(cores) as pool:
-        for _ in range(warmup):
-            cpu_step_time(grads, w, args.cr, args.delta, args.workload == "topk", pool)
-        times = [cpu_step_time(grads, w, args.cr, args.delta, args.workload == "topk", pool) for _ in range(steps)]
-    t = statistics.median(times)
+    q = ctx.Queue()
+    pr = ctx.Process(target=_cpu_serial_step, args=(W, args.dim, args.family, args.cr, args.delta, q))
+    pr.start()
+    t = q.get()
+    pr.join()
+    return t
+
+
+def workload_config(args, W, D, rates, k, world):
+    size = "ResNet-152-sized" if D == R_DIM else ("VGG-19-sized" if D == 143_667_240 else "flat-gradient")
+    compression = args.workload == "topk"
     return {
-        "value": W * args.cpu_dim / t,
-        "unit": UNIT,
-        "cores": cores,
-        "kind": "port",
-        "sample": f"W={W} workers x D={args.cpu_dim} f64 (fp32-valued) per step, oracle/comm_ref.py "
-                  f"(np.lexsort Top-k as comm.py:94), {cores}-process pool for the gates, "
-                  f"median of {steps} steps; host cpu_count={os.cpu_count()}",
-        "step_s": t,
+        "workload": (f"{size} adaptive Top-k aggregation: W={W} workers x D={D}, cr={args.cr}, "
+                     f"delta={args.delta}, S1 rates {rates}, gate+exchange+weighted merge+fused momentum SGD"
+                     if compression else
+                     f"{size} weighted dense aggregation: W={W} workers x D={D}, S1 rates {rates}, "
+                     f"+ fused momentum SGD"),
+        "family": args.family, "workers_per_gpu": k,
+        "parallelism": f"workers sharded {k}/GPU over {world} GPU(s)",
     }
 
 
 def run_reference(args):
+    """`--impl reference`: the reference's own CPU implementation of the path at the SAME
+    config as our arm (D, W, cr, delta, family, rates), rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     W = args.workers
-    cb = cpu_measure(args, W, steps=args.steps, warmup=args.warmup)
+    rates, _ = rates_weights(W)
+    warm = min(args.warmup, 1)  # CPU code has no warm-up effect beyond first touch
+    cb = cpu_measure(args, W, steps=args.steps, warmup=warm)
     line = {
         "metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": warm,
         "ms_per_step": cb["step_s"] * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"ResNet-152-sized weighted Top-k aggregation (cr {args.cr}, delta {args.delta}), "
-                               f"{W} workers, CPU sample D={args.cpu_dim}",
-                   "family": args.family},
+        "config": workload_config(args, W, args.dim, rates, max(W // max(args.gpus, 1), 1), args.gpus),
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "same_config": True, "host": cb["host"], "step_s": cb["steps_s"],
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    if args.cpu_variant == "A":
+        t = cpu_measure_serial(args, W)
+        line["variant_a"] = {"value": W * args.dim / t, "unit": UNIT, "cores": 1, "step_s": t,
+                             "sample": "one serial step (W gates, aggregate, update), OPENBLAS_NUM_THREADS=1"}
     print(json.dumps(line), flush=True)
 
 
@@ -217,15 +379,19 @@ class Clocks:
 
 
 def synth_bucket(ex, family, rank_lo, seed=0):
+    """The synthetic gradients of SURVEY §8(d): worker j's row from its own seeded generator,
+    N(0,1)*(1 + 0.1 j) ("normal") or sign(z)*exp(1.5 z') ("heavy": the mixed-gate regime);
+    "mixed" alternates heavy (even j) and normal (odd j) workers."""
     import torch
 
     dev = ex.device
     for j in range(ex.k):
-        gen = torch.Generator(device=dev).manual_seed(seed * 1000 + rank_lo + j)
+        gj = rank_lo + j
+        gen = torch.Generator(device=dev).manual_seed(seed * 1000 + gj)
         z = torch.randn(ex.dim, device=dev, generator=gen)
-        if family == "heavy":
+        if family == "heavy" or (family == "mixed" and gj % 2 == 0):
             z = torch.sign(z) * torch.exp(1.5 * torch.randn(ex.dim, device=dev, generator=gen))
-        ex.bucket[j, :ex.dim].copy_(z * (1 + 0.1 * (rank_lo + j)))
+        ex.bucket[j, :ex.dim].copy_(z * (1 + 0.1 * gj))
 
 
 def run_ours(args):
@@ -403,22 +569,16 @@ def run_ours(args):
     clk = clocks.stop()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_measure(args, W, steps=args.cpu_steps)
+        cb = cpu_measure(args, W, steps=args.cpu_steps, warmup=0)
         cpu = {k_: cb[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
-        size = "ResNet-152-sized" if D == R_DIM else ("VGG-19-sized" if D == 143_667_240 else "flat-gradient")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 (f64 accumulation)", "data": "synthetic",
             "config": {
-                "workload": (f"{size} adaptive Top-k aggregation: W={W} workers x D={D}, cr={args.cr}, "
-                             f"delta={args.delta}, S1 rates {rates}, gate+exchange+weighted merge+fused momentum SGD"
-                             if compression else
-                             f"{size} weighted dense aggregation: W={W} workers x D={D}, S1 rates {rates}, "
-                             f"+ fused momentum SGD"),
-                "family": args.family, "workers_per_gpu": k, "parallelism": f"workers sharded {k}/GPU over {world} GPU(s)",
+                **workload_config(args, W, D, rates, k, world),
                 "l2": (f"inputs larger than L2 ({k} x {D * 4 / 1e6:.0f} MB bucket per GPU)" if k * D * 4 > 126e6 else
                        f"inputs L2-resident ({k} x {D * 4 / 1e6:.1f} MB bucket per GPU): sweep point, not a bench line"),
                 "paths": sorted(set(paths)),

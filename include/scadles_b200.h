@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 1
+#define SG_ABI_VERSION 2
 
 #define SG_OK 0
 #define SG_ERR_INVALID (-1)     /* bad argument (the reference raises ValueError) */
@@ -110,13 +110,18 @@ int sg_gate_update(const double* norms2, int k, sg_gate_state* states,
  * epilogue using the float64 aggregate: buf = buf*mu + (agg + wd*p); p = p - lr*buf
  * (first_step: buf treated as zeros).  `out` may be NULL when the step is fused. */
 size_t sg_aggregate_workspace_bytes(int nw, int64_t dim);
+/* `sparse_merge` picks the kernel for an all-sparse float32 merge with fused SGD (launch
+ * policy only, no reference counterpart; every choice gives bit-identical results): -1 launches
+ * both and the device picks by payload density (>= 0.2 kept entries per position:
+ * k_merge_own, else k_merge_ws), 0 only k_merge_ws, 1 only k_merge_own.  A caller that knows
+ * its density (GradientExchange: W*m/dim) saves the launch of the kernel that would exit. */
 int sg_weighted_aggregate_f32(int nw, const double* weights, const uint8_t* compressed,
                               const float* dense, int64_t ld_dense,
                               const uint32_t* idx, const float* val, const int64_t* row_ptr,
                               const int32_t* tile_off, int64_t dim, float* out,
                               float* params, float* momentum_buf,
                               double lr, double momentum, double weight_decay, int first_step,
-                              void* workspace, size_t workspace_bytes, void* stream);
+                              int sparse_merge, void* workspace, size_t workspace_bytes, void* stream);
 int sg_weighted_aggregate_f64(int nw, const double* weights, const uint8_t* compressed,
                               const double* dense, int64_t ld_dense,
                               const uint32_t* idx, const double* val, const int64_t* row_ptr,
@@ -124,15 +129,6 @@ int sg_weighted_aggregate_f64(int nw, const double* weights, const uint8_t* comp
                               double* params, double* momentum_buf,
                               double lr, double momentum, double weight_decay, int first_step,
                               void* workspace, size_t workspace_bytes, void* stream);
-
-/* Which kernel takes the all-sparse float32 merges of sg_weighted_aggregate_f32 /
- * sg_weighted_aggregate_peers_f32 (process-wide; the environment variable SG_MERGE_OWN
- * overrides it): -1 (default) launches both and the device picks by payload density (>= 0.2
- * kept entries per position: k_merge_own, else k_merge_ws), 0 only k_merge_ws, 1 only
- * k_merge_own.  Both fold in the same order, so every mode gives bit-identical results; a
- * caller that knows its density (GradientExchange: W*m/dim) saves the launch of the kernel
- * that would exit.  No reference counterpart (launch policy only). */
-void sg_set_merge_kernel(int mode);
 
 /* ---- Multi-GPU merge over peer memory (one process per GPU, NVLink) -----------------------
  * The all-sparse case of sg_weighted_aggregate_f32 with fused momentum SGD, where worker j's
@@ -143,14 +139,17 @@ void sg_set_merge_kernel(int mode);
  * while it streams its parameters).  The three pointer arrays are HOST arrays of nw <= 16
  * device pointers; `compressed` is the (local) device array of nw decision bytes and must be
  * all ones -- the caller checks the decisions first (workers that did not compress are
- * exchanged densely); with a zero byte the kernel writes nothing.  Replaces the
+ * exchanged densely); with a zero byte the kernel writes nothing.  Workers
+ * [local_lo, local_lo + local_n) are this device's own (their offsets are scanned to balance the
+ * tile ranges; remote ones are not); `sparse_merge` as for sg_weighted_aggregate_f32.  Replaces the
  * comm.weighted_aggregate (comm.py:67-78) + nn.sgd_momentum_step (nn.py:161-172) pair of
  * engine.py:270-283 for the all-compressed iteration. */
 int sg_weighted_aggregate_peers_f32(int nw, const double* weights, const uint8_t* compressed,
                                     const uint32_t* const* idx_ptrs, const float* const* val_ptrs,
                                     const int32_t* const* tile_off_ptrs, int64_t dim, float* out,
                                     float* params, float* momentum_buf, double lr, double momentum,
-                                    double weight_decay, int first_step, void* stream);
+                                    double weight_decay, int first_step, int local_lo, int local_n,
+                                    int sparse_merge, void* stream);
 
 /* The dense side of a mixed multi-GPU step, enqueued unconditionally and guarded on the
  * gathered decisions `guard[0..guard_n)` (device bytes): a no-op unless some worker did not

@@ -70,7 +70,7 @@ SIGNATURES = {
     "sg_weighted_aggregate_f32": (
         c_int,
         [c_int, POINTER(c_double), _P, _P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, _P,
-         c_double, c_double, c_double, c_int, _P, c_size_t, _P],
+         c_double, c_double, c_double, c_int, c_int, _P, c_size_t, _P],
     ),
     "sg_weighted_aggregate_f64": (
         c_int,
@@ -80,10 +80,9 @@ SIGNATURES = {
     "sg_weighted_aggregate_peers_f32": (
         c_int,
         [c_int, POINTER(c_double), _P, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), c_int64,
-         _P, _P, _P, c_double, c_double, c_double, c_int, _P],
+         _P, _P, _P, c_double, c_double, c_double, c_int, c_int, c_int, c_int, _P],
     ),
     "sg_gather_bytes": (c_int, [c_int, POINTER(c_void_p), c_int64, _P, _P]),
-    "sg_set_merge_kernel": (None, [c_int]),
     "sg_weighted_partial_f32": (
         c_int,
         [c_int, POINTER(c_double), _P, _P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, c_int, _P, c_size_t, _P],

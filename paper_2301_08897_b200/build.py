@@ -8,6 +8,7 @@ box with the repo snapshot.  ``python -m paper_2301_08897_b200.build`` rebuilds 
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
 import sys
 from pathlib import Path
@@ -48,11 +49,28 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every .cu for sm_100a and link the shared library in-tree."""
+    """Compile every .cu for sm_100a and link the shared library in-tree.
+
+    Safe to call from every rank of a torchrun job at once: the build holds an exclusive
+    file lock (the first caller compiles, the others wait and then find the library up to
+    date), objects go to a per-process directory, and the library is published with one
+    atomic rename.
+    """
     if not force and up_to_date():
         return LIB
-    objdir = PKG / "build"
-    objdir.mkdir(exist_ok=True)
+    import fcntl
+
+    (PKG / "build").mkdir(exist_ok=True)
+    with open(PKG / "build" / ".lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and up_to_date():  # another process built it while we waited
+            return LIB
+        return _build_locked(verbose)
+
+
+def _build_locked(verbose: bool) -> Path:
+    objdir = PKG / "build" / f"obj.{os.getpid()}"
+    objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
@@ -66,12 +84,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose and r.stderr:
             print(r.stderr, file=sys.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    shutil.rmtree(objdir, ignore_errors=True)
     return LIB
 
 

@@ -134,11 +134,19 @@ def weights_from_rates(rates) -> np.ndarray:
     return r / r.sum()
 
 
+MAX_FOLD = 64  # workers per kernel launch (sg_weighted_aggregate_*); more are folded in chunks
+
+
 def weighted_aggregate(grads, weights):
     """sum_j w_j * densify(g_j), folded in ascending j (comm.py:67-78), on the GPU.
 
     numpy / host payloads -> float64 kernel, returns a fresh float64 numpy array (bit-exact).
     CUDA float32 tensors / device payloads -> float32 kernel, returns a CUDA tensor.
+
+    Any number of workers: beyond MAX_FOLD the fold continues chunk by chunk, each chunk
+    starting from the previous chunk's float64 accumulator entered as a dense worker of
+    weight 1.0 (0 + 1.0*acc == acc exactly, and acc never holds -0.0), so the ascending-j
+    operation sequence -- and therefore every bit -- is the reference's.
     """
     w = np.asarray(weights, dtype=np.float64)
     if len(grads) != len(w):
@@ -147,7 +155,6 @@ def weighted_aggregate(grads, weights):
     if len(dims) != 1:
         raise ValueError(f"gradient dimensions differ: {sorted(dims)}")
     dim = dims.pop()
-    nw = len(grads)
     on_device = any(
         (isinstance(g, torch.Tensor) and g.is_cuda and g.dtype == torch.float32)
         or (isinstance(g, SparseGradient) and g._dev and g._val_t.dtype == torch.float32)
@@ -156,9 +163,21 @@ def weighted_aggregate(grads, weights):
     dt = torch.float32 if on_device else torch.float64
     if dim == 0:
         return torch.zeros(0, dtype=dt, device=_device()) if on_device else np.zeros(0)
+    if len(grads) <= MAX_FOLD:
+        out = _aggregate(list(grads), w, dim, dt)
+    else:
+        acc = _aggregate(list(grads[:MAX_FOLD]), w[:MAX_FOLD], dim, torch.float64)
+        for i in range(MAX_FOLD, len(grads), MAX_FOLD - 1):
+            chunk = [acc] + list(grads[i:i + MAX_FOLD - 1])
+            acc = _aggregate(chunk, np.concatenate(([1.0], w[i:i + MAX_FOLD - 1])), dim, torch.float64)
+        out = acc.to(dt)
+    return out if on_device else out.cpu().numpy()
+
+
+def _aggregate(grads, w, dim, dt):
+    """One kernel launch over <= MAX_FOLD workers; returns a CUDA tensor of dtype dt."""
     dev = _device()
-    if nw > 64:
-        raise ValueError("at most 64 workers per aggregation call")
+    nw = len(grads)
     comp = np.array([isinstance(g, SparseGradient) for g in grads], dtype=np.uint8)
     dense = None
     if not comp.all():
@@ -184,10 +203,9 @@ def weighted_aggregate(grads, weights):
             val = torch.zeros(1, dtype=dt, device=dev)
         row_ptr = torch.tensor(ptr, dtype=torch.int64, device=dev)
         comp_t = torch.from_numpy(comp).to(dev)
-    out = kernels.weighted_aggregate(
+    return kernels.weighted_aggregate(
         w, dim, compressed=comp_t, dense=dense, idx=idx, val=val, row_ptr=row_ptr, dtype=dt
     )
-    return out if on_device else out.cpu().numpy()
 
 
 def topk_count(dim: int, cr: float) -> int:

@@ -689,21 +689,9 @@ SG_DEV int sparse_merge_is_mine(const AggArgs<float, TO>& a, bool want_dense) {
     return all_comp && dense == want_dense;
 }
 
-inline int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e && *e ? atoi(e) : dflt;
-}
-
-int g_merge_kernel = -1;  // sg_set_merge_kernel
-inline int merge_kernel_mode() { return env_int("SG_MERGE_OWN", g_merge_kernel); }
-
-inline int mw_balance() {
-    static const int on = [] {
-        const char* e = getenv("SG_MERGE_BALANCE");
-        return e && *e == '0' ? 0 : 1;
-    }();
-    return on;
-}
+// Cost-balanced merge tile ranges (always on; the equal-range split was the round-1 ablation).
+inline int mw_balance() { return 1; }
+inline int merge_mode(int m) { return m < 0 ? -1 : (m > 0 ? 1 : 0); }
 
 // One CTA per SM over cost-balanced contiguous tile ranges.
 inline int mw_grid(long long ntiles, int sms) { return (int)(ntiles < sms ? ntiles : sms); }
@@ -1316,17 +1304,17 @@ k_merge_own(const AggArgs<float, TO> a) {
 template <typename TO>
 void launch_sparse_merge(const AggArgs<float, TO>& a, int grid, size_t sm, int sms, cudaStream_t stream) {
     if (a.own != 1) {
-        cudaFuncSetAttribute(k_merge_ws<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        smem_attr((const void*)k_merge_ws<TO>, (int)sm);
         launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a);
         debug_sync("k_merge_ws", stream);
     }
     if (a.own != 0) {
         AggArgs<float, TO> ao = a;
-        ao.pf = env_int("SG_MERGE_PF", 1);
+        ao.pf = 1;
         long long g2 = 2LL * sms;
         if (g2 > a.ntiles) g2 = a.ntiles;
         const int dsm = MO_SMEM;
-        cudaFuncSetAttribute(k_merge_own<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+        smem_attr((const void*)k_merge_own<TO>, dsm);
         launch_pdl(k_merge_own<TO>, dim3((unsigned)g2), dim3(MO_THREADS), (size_t)dsm, stream, ao);
         debug_sync("k_merge_own", stream);
     }
@@ -1363,8 +1351,8 @@ template <typename TI, typename TO>
 int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dense, long long ld,
               const uint32_t* idx, const TI* val, const long long* row_ptr, const int* tile_off,
               long long dim, TO* out, TO* p, TO* buf, double lr, double mu, double wd, int first,
-              void* ws, size_t ws_bytes, cudaStream_t stream, const uint8_t* guard = nullptr,
-              int guard_n = 0, int guard_mode = 0) {
+              void* ws, size_t ws_bytes, cudaStream_t stream, int sparse_merge = -1,
+              const uint8_t* guard = nullptr, int guard_n = 0, int guard_mode = 0) {
     if (nw < 1 || dim < 1 || !weights || (!out && !p)) return SG_ERR_INVALID;
     if (nw > MAX_WORKERS || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
     if (p && !buf) return SG_ERR_INVALID;
@@ -1415,17 +1403,17 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
     if constexpr (sizeof(TI) == 4 && sizeof(TO) == 4)
     {
         const int sms = num_sms();
-        a.pipe = comp && vec && p && nw <= MP_MAXW && env_int("SG_MERGE_WS", 1);
+        a.pipe = comp && vec && p && nw <= MP_MAXW;
         if (a.pipe) {
             const int grid = mw_grid(ntiles, sms);
             const size_t sm = mw_smem_bytes();
             a.balance = mw_balance();
             a.cost_j0 = 0;
             a.cost_j1 = nw;
-            a.own = merge_kernel_mode();
+            a.own = merge_mode(sparse_merge);
             launch_sparse_merge(a, grid, sm, sms, stream);
         }
-        cudaFuncSetAttribute(k_merge<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MG_SMEM);
+        smem_attr((const void*)k_merge<TO>, (int)MG_SMEM);
         long long grid = (long long)sms * 2;
         if (grid > ntiles) grid = ntiles;
         launch_pdl(k_merge<TO>, dim3((unsigned)grid), dim3(MG_THREADS), MG_SMEM, stream, a);
@@ -1453,7 +1441,8 @@ int sgd(T* p, T* buf, const T* g, long long dim, double lr, double mu, double wd
 // Merge + fused SGD over workers whose payloads are addressed per worker (peer GPUs).
 int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const uint32_t* const* idx_ptrs,
                     const float* const* val_ptrs, const int32_t* const* off_ptrs, long long dim, float* out,
-                    float* p, float* buf, double lr, double mu, double wd, int first, cudaStream_t stream) {
+                    float* p, float* buf, double lr, double mu, double wd, int first, int local_lo, int local_n,
+                    int sparse_merge, cudaStream_t stream) {
     if (nw < 1 || dim < 1 || !weights || !comp || !idx_ptrs || !val_ptrs || !off_ptrs || !p || !buf)
         return SG_ERR_INVALID;
     if (nw > PEER_MAXW || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
@@ -1487,23 +1476,12 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
     const int grid = mw_grid(ntiles, sms);
     const size_t sm = mw_smem_bytes();
     a.balance = mw_balance();
-    {  // cost estimate from the workers whose payloads live on this device
-        int dev = -1;
-        cudaGetDevice(&dev);
-        int j0 = -1, j1 = -1;
-        for (int j = 0; j < nw; ++j) {
-            cudaPointerAttributes at;
-            if (cudaPointerGetAttributes(&at, off_ptrs[j]) == cudaSuccess && at.device == dev &&
-                at.type == cudaMemoryTypeDevice) {
-                if (j0 < 0) j0 = j;
-                j1 = j + 1;
-            }
-        }
-        cudaGetLastError();
-        a.cost_j0 = j0 < 0 ? 0 : j0;
-        a.cost_j1 = j0 < 0 ? nw : j1;
-    }
-    a.own = merge_kernel_mode();
+    // the balanced ranges are costed from the workers whose payloads live on this device
+    // (the caller names them: local reads are cheap to scan, remote ones are not)
+    if (local_lo < 0 || local_n < 0 || local_lo + local_n > nw) return SG_ERR_INVALID;
+    a.cost_j0 = local_n > 0 ? local_lo : 0;
+    a.cost_j1 = local_n > 0 ? local_lo + local_n : nw;
+    a.own = merge_mode(sparse_merge);
     launch_sparse_merge(a, grid, sm, sms, stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
@@ -1585,11 +1563,11 @@ int sg_weighted_aggregate_f32(int nw, const double* weights, const uint8_t* comp
                               const float* val, const int64_t* row_ptr, const int32_t* tile_off,
                               int64_t dim, float* out, float* params, float* momentum_buf,
                               double lr, double momentum, double weight_decay, int first_step,
-                              void* workspace, size_t workspace_bytes, void* stream) {
+                              int sparse_merge, void* workspace, size_t workspace_bytes, void* stream) {
     return aggregate<float, float>(nw, weights, compressed, dense, ld_dense, idx, val,
                                    reinterpret_cast<const long long*>(row_ptr), tile_off, dim, out,
                                    params, momentum_buf, lr, momentum, weight_decay, first_step,
-                                   workspace, workspace_bytes, (cudaStream_t)stream);
+                                   workspace, workspace_bytes, (cudaStream_t)stream, sparse_merge);
 }
 
 int sg_weighted_aggregate_f64(int nw, const double* weights, const uint8_t* compressed,
@@ -1622,9 +1600,11 @@ int sg_weighted_aggregate_peers_f32(int nw, const double* weights, const uint8_t
                                     const uint32_t* const* idx_ptrs, const float* const* val_ptrs,
                                     const int32_t* const* tile_off_ptrs, int64_t dim, float* out,
                                     float* params, float* momentum_buf, double lr, double momentum,
-                                    double weight_decay, int first_step, void* stream) {
+                                    double weight_decay, int first_step, int local_lo, int local_n,
+                                    int sparse_merge, void* stream) {
     return aggregate_peers(nw, weights, compressed, idx_ptrs, val_ptrs, tile_off_ptrs, dim, out, params,
-                           momentum_buf, lr, momentum, weight_decay, first_step, (cudaStream_t)stream);
+                           momentum_buf, lr, momentum, weight_decay, first_step, local_lo, local_n,
+                           sparse_merge, (cudaStream_t)stream);
 }
 
 int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compressed, const float* dense,
@@ -1635,7 +1615,7 @@ int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compre
     return aggregate<float, float>(nw, weights, compressed, dense, ld_dense, idx, val,
                                    reinterpret_cast<const long long*>(row_ptr), tile_off, dim, out, nullptr,
                                    nullptr, 0.0, 0.0, 0.0, 0, workspace, workspace_bytes, (cudaStream_t)stream,
-                                   guard, guard_n, 2);
+                                   -1, guard, guard_n, 2);
 }
 
 int sg_peer_reduce_sgd_f32(int nranks, const float* const* partials, const uint8_t* guard, int guard_n,
@@ -1660,8 +1640,6 @@ int sg_peer_reduce_sgd_f32(int nranks, const float* const* partials, const uint8
                guard_n, (long long)dim, out, params, momentum_buf, lr, momentum, weight_decay, first_step);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
-
-void sg_set_merge_kernel(int mode) { sg::g_merge_kernel = mode < 0 ? -1 : (mode > 0 ? 1 : 0); }
 
 int sg_gather_bytes(int nsrc, const uint8_t* const* src, int64_t each, uint8_t* dst, void* stream) {
     if (nsrc < 1 || nsrc > MAX_WORKERS || each < 1 || !src || !dst) return SG_ERR_INVALID;

@@ -2,6 +2,10 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <mutex>
+#include <tuple>
+#include <vector>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -307,6 +311,21 @@ inline void debug_sync(const char* what, cudaStream_t stream) {
     if (!on) return;
     const cudaError_t e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) fprintf(stderr, "[scadles_b200] %s: %s\n", what, cudaGetErrorString(e));
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size): the
+// attribute is a per-context property, so the launchers do not pay the driver call per launch.
+inline cudaError_t smem_attr(const void* kern, int bytes) {
+    static std::mutex mu;
+    static std::vector<std::tuple<const void*, int, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& t : done)
+        if (std::get<0>(t) == kern && std::get<1>(t) == dev && std::get<2>(t) >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.emplace_back(kern, dev, bytes);
+    return e;
 }
 
 inline int num_sms() {

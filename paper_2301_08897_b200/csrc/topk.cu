@@ -1760,13 +1760,16 @@ __global__ void k_gate_update(const double* norms2, int k, sg_gate_state* states
 // --------------------------------------------------------------------------------------
 constexpr size_t MN_SMEM = (size_t)MN_STAGES * MN_TILE * sizeof(float);
 
-template <typename T> int segments_per_worker(int k) {
-    int dev = 0, sms = 148, per_sm = 4;
+// Resident main-pass CTAs per SM, queried once per device (the plan is rebuilt on every call).
+template <typename T> int main_ctas_per_sm() {
+    static int cache[64] = {0};
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < 64 && cache[dev] > 0) return cache[dev];
+    int per_sm = 0;
     cudaError_t e;
     if constexpr (sizeof(T) == 4) {
-        cudaFuncSetAttribute(k_main_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MN_SMEM);
+        smem_attr((const void*)k_main_tma, (int)MN_SMEM);
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_main_tma, TK_THREADS, MN_SMEM);
     } else {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_main<T>, TK_THREADS, 0);
@@ -1776,7 +1779,12 @@ template <typename T> int segments_per_worker(int k) {
         per_sm = sizeof(T) == 4 ? 3 : 4;
     }
     if (per_sm < 1) per_sm = 1;
-    const int s = sms * per_sm / k;
+    if (dev >= 0 && dev < 64) cache[dev] = per_sm;
+    return per_sm;
+}
+
+template <typename T> int segments_per_worker(int k) {
+    const int s = num_sms() * main_ctas_per_sm<T>() / k;
     return s < 1 ? 1 : s;
 }
 
@@ -1900,7 +1908,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     debug_sync("k_collect", stream);
     // 4. resolve: in-CTA for the normal boundary, cooperative radix rounds for oversized ones
     const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES + sizeof(unsigned) * (NSUB_MAX + BMAX);
-    cudaFuncSetAttribute(k_resolve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem);
+    smem_attr((const void*)k_resolve<T>, (int)res_smem);
     ResolveArgs<T> ra;
     ra.sel = sel;
     ra.hist = histr;
@@ -1938,11 +1946,11 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.decision = decision;
     wa.rho = rho;
     const size_t wr_smem = align_up(sizeof(unsigned) * (size_t)p.tps, 16) + (size_t)WF_SPAN * (sizeof(T) + sizeof(uint32_t));
-    cudaFuncSetAttribute(k_write<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wr_smem);
+    smem_attr((const void*)k_write<T>, (int)wr_smem);
     launch_pdl(k_write<T>, dim3(subgrid), dim3(TK_THREADS), wr_smem, stream, wa);
     debug_sync("k_write", stream);
     const size_t fin_smem = sizeof(double) * (size_t)k * (p.nseg + p.nsub);
-    cudaFuncSetAttribute(k_finish<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem);
+    smem_attr((const void*)k_finish<T>, (int)fin_smem);
     launch_pdl(k_finish<T>, dim3(1), dim3(TK_THREADS), fin_smem, stream, wa);
     debug_sync("k_finish", stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;

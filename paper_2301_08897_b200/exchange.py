@@ -43,15 +43,16 @@ class CudaOps:
 
     name = "cuda"
 
-    def __init__(self, device: torch.device):
+    def __init__(self, device: torch.device, sparse_merge: int = -1):
         kernels.require_cuda()
         self.device = device
+        self.sparse_merge = sparse_merge  # all-sparse merge kernel (see kernels.weighted_aggregate)
 
     def topk_gate(self, bucket, dim, m, states, out, tile_off=None):
         return kernels.topk_gate(bucket, m, states, dim=dim, out=out, tile_off=tile_off)
 
     def aggregate(self, weights, dim, **kw):
-        return kernels.weighted_aggregate(weights, dim, **kw)
+        return kernels.weighted_aggregate(weights, dim, sparse_merge=self.sparse_merge, **kw)
 
     def sgd(self, params, buf, grad, lr, momentum, weight_decay, first):
         kernels.sgd_momentum(params, buf, grad, lr, momentum, weight_decay, first)
@@ -79,6 +80,9 @@ class StepInfo:
             self._path = self._resolve()
             self._resolve = None
         return self._path
+
+
+DEC_RING = 4096
 
 
 def _padded(dim: int) -> int:
@@ -136,11 +140,12 @@ class GradientExchange:
         recs["raw_gate"] = int(raw_gate)
         self.states = self.ops.make_states(recs)
         self.packed = compression and self.world > 1 and dtype == torch.float32
-        if compression and device.type == "cuda" and dtype == torch.float32:
-            # all-sparse merge kernel by payload density: an all-compressed step always carries
-            # exactly W*m entries, so the host knows the device's choice (>= 0.2 per position:
-            # k_merge_own) and launches only that kernel
-            kernels.set_merge_kernel(1 if self.W * m >= 0.2 * dim else 0)
+        # all-sparse merge kernel by payload density: an all-compressed step always carries
+        # exactly W*m entries, so the host knows the device's choice (>= 0.2 per position:
+        # k_merge_own) and launches only that kernel
+        self.sparse_merge = 1 if self.W * m >= 0.2 * dim else 0
+        if isinstance(self.ops, CudaOps):
+            self.ops.sparse_merge = self.sparse_merge
         if compression:
             nt1 = kernels.merge_tiles(dim) + 1
             if self.packed:
@@ -151,20 +156,10 @@ class GradientExchange:
                 words = (dw + 2 * k * m + k * nt1 + 3) // 4 * 4
                 self.pack_words, self.pack_dw = words, dw
                 self._symm = None
+                self._partial_h = None
                 # (the peer merge takes up to 16 workers; more go through the NCCL all-gather path)
                 if device.type == "cuda" and os.environ.get("SG_P2P", "1") != "0" and self.W <= 16:
-                    # symmetric (peer-mapped) send buffer: the merge reads the other ranks'
-                    # payloads in place over NVLink instead of an all-gather
-                    try:
-                        import torch.distributed._symmetric_memory as symm_mem
-
-                        pack = symm_mem.empty(words, dtype=torch.int32, device=device)
-                        pack.zero_()
-                        grp = group if group is not None else dist.group.WORLD
-                        self._symm = symm_mem.rendezvous(pack, grp.group_name)
-                        self.pack = pack
-                    except Exception:  # no peer mapping on this system: NCCL all-gather path
-                        self._symm = None
+                    self._setup_peer_buffers(words)
                 if self._symm is None:
                     self.pack = torch.zeros(words, dtype=torch.int32, **z)
                 self.decision = self.pack[:dw].view(torch.uint8)[:k]
@@ -189,14 +184,12 @@ class GradientExchange:
                 off_p = [b + 4 * (dw + 2 * k * m + j * nt1) for b in bases for j in range(k)]
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
                 self._peer_merge = kernels.PeerMergeLauncher(dim, self.dec_all, idx_p, val_p, off_p, self.params,
-                                                             self.momentum_buf, momentum, weight_decay)
+                                                             self.momentum_buf, momentum, weight_decay,
+                                                             local_lo=self.lo, local_n=self.k,
+                                                             sparse_merge=self.sparse_merge)
                 # mixed decisions: each rank's partial in a peer-mapped buffer, reduced in rank order
-                import torch.distributed._symmetric_memory as symm_mem
-
                 self._side = None
-                self._partial_buf = symm_mem.empty(self.ld, dtype=torch.float32, device=device)
-                grp = group if group is not None else dist.group.WORLD
-                ph = symm_mem.rendezvous(self._partial_buf, grp.group_name)
+                ph = self._partial_h
                 poff = self._partial_buf.data_ptr() - ph.buffer_ptrs[self.rank]
                 self._dense = kernels.GuardedDenseLaunchers(
                     k, dim, self.ld, self.decision, self.idx, self.val, self.row_ptr_local, self.tile_off,
@@ -228,8 +221,36 @@ class GradientExchange:
                 self.tile_off_all = (torch.empty((self.W, nt1), dtype=torch.int32, **z)
                                      if self.tile_off is not None else None)
         self.partial = torch.empty(dim, dtype=dtype, **z) if self.world > 1 else None
+        self._dec_ring = None
         self.aggregate = None
         self.steps = 0
+
+    def _setup_peer_buffers(self, words: int) -> None:
+        """Symmetric (peer-mapped) send and partial buffers, so the merge reads the other
+        ranks' payloads in place over NVLink instead of an all-gather.  The choice is
+        collective: every rank reports whether both rendezvous succeeded and the peer path is
+        taken only if all did (otherwise every rank takes the NCCL all-gather path -- a rank
+        that silently fell back alone would hang the others in the peer barriers)."""
+        ok = 1
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            grp = self.group if self.group is not None else dist.group.WORLD
+            pack = symm_mem.empty(words, dtype=torch.int32, device=self.device)
+            pack.zero_()
+            symm = symm_mem.rendezvous(pack, grp.group_name)
+            part = symm_mem.empty(self.ld, dtype=torch.float32, device=self.device)
+            part_h = symm_mem.rendezvous(part, grp.group_name)
+        except Exception:  # no peer mapping on this system
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
+        if self.group is not None or dist.is_initialized():
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 1:
+            self._symm, self.pack = symm, pack
+            self._partial_buf, self._partial_h = part, part_h
+        else:
+            self._symm = None
 
     # -- the step ---------------------------------------------------------------------------
 
@@ -308,7 +329,12 @@ class GradientExchange:
             self._peer_merge(w, lr, first, out)
             main.wait_stream(self._side)
             self._symm.barrier(channel=0)
-            dec_host = torch.empty(self.W, dtype=torch.uint8, pin_memory=True)
+            # the step's decisions for the lazily resolved path name: one pinned slot per
+            # step in a ring allocated once (a StepInfo's path must be read within
+            # DEC_RING steps of the step that made it)
+            if self._dec_ring is None:
+                self._dec_ring = torch.empty((DEC_RING, self.W), dtype=torch.uint8, pin_memory=True)
+            dec_host = self._dec_ring[self.steps % DEC_RING]
             dec_host.copy_(self.dec_all, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record()
@@ -342,7 +368,8 @@ class GradientExchange:
                     if self._merge is None:
                         self._merge = kernels.MergeLauncher(self.W, dim, self.dec_all, self.idx_all, self.val_all,
                                                             self.row_ptr_all, self.tile_off_all, self.params,
-                                                            self.momentum_buf, self.momentum, self.weight_decay)
+                                                            self.momentum_buf, self.momentum, self.weight_decay,
+                                                            sparse_merge=self.sparse_merge)
                     self._merge(w, opt["lr"], opt["first_step"], out)
                 else:
                     self.ops.aggregate(w, dim, compressed=self.dec_all, idx=self.idx_all, val=self.val_all,

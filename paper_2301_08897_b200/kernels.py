@@ -27,21 +27,9 @@ def _count(n: int) -> None:
     LAUNCHES["n"] += n
 
 
-_MERGE_MODE = {"mode": -1}
-
-
-def set_merge_kernel(mode: int) -> None:
-    """sg_set_merge_kernel: -1 device picks by density, 0 k_merge_ws only, 1 k_merge_own only."""
-    _capi.load().sg_set_merge_kernel(int(mode))
-    _MERGE_MODE["mode"] = -1 if mode < 0 else (1 if mode > 0 else 0)
-
-
-def _sparse_merge_launches() -> int:
-    """k_merge_ws + k_merge_own (one exits by payload density) unless one is forced."""
-    env = os.environ.get("SG_MERGE_OWN", "")
-    if env:
-        return 1 if int(env) >= 0 else 2
-    return 2 if _MERGE_MODE["mode"] < 0 else 1
+def _sparse_merge_launches(sparse_merge: int) -> int:
+    """k_merge_ws + k_merge_own (one exits by payload density) unless the caller picked one."""
+    return 2 if sparse_merge < 0 else 1
 
 
 def require_cuda(t: torch.Tensor | None = None) -> None:
@@ -193,8 +181,12 @@ def weighted_aggregate(
     weight_decay: float = 0.0,
     first_step: bool = False,
     dtype: torch.dtype | None = None,
+    sparse_merge: int = -1,
 ):
-    """sum_j w_j * densify(payload_j) (+ optional fused momentum-SGD) on the GPU."""
+    """sum_j w_j * densify(payload_j) (+ optional fused momentum-SGD) on the GPU.
+
+    ``sparse_merge``: all-sparse float32 merge kernel (-1 the device picks by density,
+    0 k_merge_ws, 1 k_merge_own; identical results)."""
     w, wp = _capi.weights_ptr(np.asarray(weights, dtype=np.float64))
     nw = len(w)
     ref = next(t for t in (dense, val, params, out) if t is not None)
@@ -215,15 +207,18 @@ def weighted_aggregate(
     if compressed is not None and tile_off is None:
         nbytes = int(_capi.load().sg_aggregate_workspace_bytes(nw, dim))
         ws = Workspace.get(nbytes, dev)
-    fn = _capi.load().sg_weighted_aggregate_f32 if dt == torch.float32 else _capi.load().sg_weighted_aggregate_f64
-    st = fn(
-        nw, wp, _ptr(compressed), _ptr(dense), ld, _ptr(idx), _ptr(val), _ptr(row_ptr), _ptr(tile_off), dim,
-        _ptr(out), _ptr(params), _ptr(momentum_buf), float(lr), float(momentum), float(weight_decay),
-        int(bool(first_step)), _ptr(ws), nbytes if ws is not None else 0, _stream(),
-    )
+    lib = _capi.load()
+    common = (nw, wp, _ptr(compressed), _ptr(dense), ld, _ptr(idx), _ptr(val), _ptr(row_ptr), _ptr(tile_off), dim,
+              _ptr(out), _ptr(params), _ptr(momentum_buf), float(lr), float(momentum), float(weight_decay),
+              int(bool(first_step)))
+    tail = (_ptr(ws), nbytes if ws is not None else 0, _stream())
+    if dt == torch.float32:
+        st = lib.sg_weighted_aggregate_f32(*common, int(sparse_merge), *tail)
+    else:
+        st = lib.sg_weighted_aggregate_f64(*common, *tail)
     _capi.check(st, "sg_weighted_aggregate")
     pipe = dt == torch.float32 and compressed is not None and params is not None
-    _count(1 + (_sparse_merge_launches() if pipe else 0) + (1 if ws is not None else 0))
+    _count(1 + (_sparse_merge_launches(sparse_merge) if pipe else 0) + (1 if ws is not None else 0))
     return out
 
 
@@ -233,9 +228,10 @@ class MergeLauncher:
     the decision read and the launch is a single ctypes call)."""
 
     def __init__(self, nw: int, dim: int, compressed, idx, val, row_ptr, tile_off, params, momentum_buf,
-                 momentum: float, weight_decay: float):
+                 momentum: float, weight_decay: float, sparse_merge: int = -1):
         require_cuda(params)
         self._fn = _capi.load().sg_weighted_aggregate_f32
+        self._sm = int(sparse_merge)
         self._nw, self._dim = nw, dim
         self._w = np.zeros(nw, dtype=np.float64)
         _, self._wp = _capi.weights_ptr(self._w)
@@ -248,9 +244,9 @@ class MergeLauncher:
         self._w[:] = weights
         comp, idx, val, rp, toff = self._ptrs
         st = self._fn(self._nw, self._wp, comp, None, 0, idx, val, rp, toff, self._dim, _ptr(out), self._p,
-                      self._b, float(lr), self._mu, self._wd, int(bool(first_step)), None, 0, _stream())
+                      self._b, float(lr), self._mu, self._wd, int(bool(first_step)), self._sm, None, 0, _stream())
         _capi.check(st, "sg_weighted_aggregate")
-        _count(1 + _sparse_merge_launches())
+        _count(1 + _sparse_merge_launches(self._sm))
 
 
 class PeerMergeLauncher:
@@ -258,9 +254,10 @@ class PeerMergeLauncher:
     merge offsets are read through raw device addresses (other GPUs' symmetric buffers)."""
 
     def __init__(self, dim: int, compressed: torch.Tensor, idx_ptrs, val_ptrs, off_ptrs, params, momentum_buf,
-                 momentum: float, weight_decay: float):
+                 momentum: float, weight_decay: float, local_lo: int = 0, local_n: int = 0, sparse_merge: int = -1):
         require_cuda(params)
         nw = len(idx_ptrs)
+        self._lo, self._ln, self._sm = int(local_lo), int(local_n), int(sparse_merge)
         self._fn = _capi.load().sg_weighted_aggregate_peers_f32
         self._nw, self._dim = nw, dim
         self._w = np.zeros(nw, dtype=np.float64)
@@ -274,9 +271,10 @@ class PeerMergeLauncher:
     def __call__(self, weights, lr: float, first_step: bool, out: torch.Tensor | None = None) -> None:
         self._w[:] = weights
         st = self._fn(self._nw, self._wp, self._comp, self._ip, self._vp, self._op, self._dim, _ptr(out),
-                      self._p, self._b, float(lr), self._mu, self._wd, int(bool(first_step)), _stream())
+                      self._p, self._b, float(lr), self._mu, self._wd, int(bool(first_step)), self._lo, self._ln,
+                      self._sm, _stream())
         _capi.check(st, "sg_weighted_aggregate_peers_f32")
-        _count(_sparse_merge_launches())
+        _count(_sparse_merge_launches(self._sm))
 
 
 class GuardedDenseLaunchers:
@@ -325,6 +323,15 @@ def gather_bytes(src_ptrs, each: int, dst: torch.Tensor) -> None:
 
 def sgd_momentum(params, momentum_buf, grad, lr, momentum, weight_decay, first_step):
     require_cuda(params)
+    for name, t in (("grad", grad), ("momentum_buf", momentum_buf)):
+        require_cuda(t)
+        if t.dtype != params.dtype or t.numel() != params.numel():
+            raise ValueError(f"{name} must match params in dtype and size "
+                             f"({t.dtype}[{t.numel()}] vs {params.dtype}[{params.numel()}])")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    if params.dtype not in (torch.float32, torch.float64) or not params.is_contiguous():
+        raise ValueError("params must be a contiguous float32 or float64 CUDA tensor")
     lib = _capi.load()
     fn = lib.sg_sgd_momentum_f32 if params.dtype == torch.float32 else lib.sg_sgd_momentum_f64
     st = fn(params.data_ptr(), momentum_buf.data_ptr(), grad.data_ptr(), params.numel(), float(lr),

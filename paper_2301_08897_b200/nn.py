@@ -36,8 +36,10 @@ class OptimizerState:
 
 
 def _as_device(x, dtype):
+    """``x`` as a CUDA tensor of ``dtype`` (device tensors of another dtype are converted, so
+    the kernel never reads a buffer as the wrong element type)."""
     if isinstance(x, torch.Tensor) and x.is_cuda:
-        return x
+        return x if x.dtype == dtype else x.to(dtype)
     kernels.require_cuda()
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(
         torch.device("cuda", torch.cuda.current_device()), dtype=dtype
@@ -59,7 +61,8 @@ def sgd_momentum_step(state: OptimizerState, params, grad, lr: float):
     first = state.momentum_buffer is None
     if first:
         buf = torch.empty_like(p)
-    elif isinstance(state.momentum_buffer, torch.Tensor) and state.momentum_buffer.is_cuda:
+    elif (isinstance(state.momentum_buffer, torch.Tensor) and state.momentum_buffer.is_cuda
+          and state.momentum_buffer.dtype == dt):
         buf = state.momentum_buffer
     else:
         buf = _as_device(state.momentum_buffer, dt)

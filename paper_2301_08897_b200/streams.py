@@ -203,6 +203,16 @@ def injection_bytes(plan, n_devices: int, sample_bytes: int) -> int:
     return sum(c * (n_devices - 1) * sample_bytes for _, c in plan if c)
 
 
+class _Done:
+    """Event stand-in for host-memory staging (test ops): copies are synchronous."""
+
+    def record(self):
+        pass
+
+    def synchronize(self):
+        pass
+
+
 class DeviceSampler:
     """Per-iteration batch staging on the GPU.
 
@@ -212,10 +222,18 @@ class DeviceSampler:
     """
 
     def __init__(self, train_x: np.ndarray, train_y: np.ndarray, pools: list[np.ndarray], *,
-                 device: torch.device | None = None, dtype: torch.dtype = torch.float64):
-        kernels.require_cuda()
-        self.device = device or torch.device("cuda", torch.cuda.current_device())
+                 device: torch.device | None = None, dtype: torch.dtype = torch.float64, ops=None):
+        # ``ops`` (tests only): a stand-in for the three kernels with the same contract, so the
+        # multi-rank protocol of ShardedSampler can run on CPU over gloo; the product path is
+        # always the sm_100a kernels
+        self.ops = ops if ops is not None else kernels
+        if ops is None:
+            kernels.require_cuda()
+            self.device = device or torch.device("cuda", torch.cuda.current_device())
+        else:
+            self.device = device or torch.device("cpu")
         self.dtype = dtype
+        self.pool_lens = [len(p) for p in pools]
         self.train_x = torch.from_numpy(np.ascontiguousarray(train_x)).to(self.device, dtype=dtype)
         self.train_y = torch.from_numpy(np.asarray(train_y, dtype=np.int64)).to(self.device)
         lens = [len(p) for p in pools]
@@ -233,7 +251,7 @@ class DeviceSampler:
         sizes = [(a.size * a.itemsize + 7) // 8 for a in parts]
         total = max(sum(sizes), 1)
         if getattr(self, "_host", None) is None or self._host.numel() < total:
-            self._host = torch.empty(max(total, 1024), dtype=torch.int64, pin_memory=True)
+            self._host = torch.empty(max(total, 1024), dtype=torch.int64, pin_memory=self.device.type == "cuda")
             self._dev = torch.empty(max(total, 1024), dtype=torch.int64, device=self.device)
         else:
             # the previous step's copy must have left the pinned buffer before it is refilled
@@ -248,7 +266,7 @@ class DeviceSampler:
             spans.append((off, n, a.dtype, a.size))
             off += n
         self._dev[:total].copy_(self._host[:total], non_blocking=True)
-        self._copied = torch.cuda.Event()
+        self._copied = torch.cuda.Event() if self.device.type == "cuda" else _Done()
         self._copied.record()
         out = []
         for o, n, dt, size in spans:
@@ -267,6 +285,9 @@ class DeviceSampler:
         """
         dev = self.device
         b = np.array([len(r) for r in draws], dtype=np.int64)
+        for d, n in enumerate(b):
+            if n and not self.pool_lens[d]:  # the reference fails at `a % len(pool)` (engine.py:224-227)
+                raise ZeroDivisionError(f"integer modulo by zero (device {d} draws from an empty pool)")
         head = np.array([r.start for r in draws], dtype=np.int64)
         base_ptr = np.concatenate([[0], np.cumsum(b)]).astype(np.int64)
         total = int(base_ptr[-1])
@@ -285,16 +306,16 @@ class DeviceSampler:
             parts += [senders, pick_ptr, all_picks if all_picks.size else np.zeros(1, dtype=np.int64), ptr]
         views = self._upload(parts)
         rows = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
-        kernels.resolve_stream_rows(views[0], views[1], views[2], self.pool_ptr, self.pool_rows, total, rows)
+        self.ops.resolve_stream_rows(views[0], views[1], views[2], self.pool_ptr, self.pool_rows, total, rows)
         if plan:
             d_senders, d_pick_ptr, d_picks, d_ptr = views[3:]
             out_rows = torch.empty(max(int(ptr[-1]), 1), dtype=torch.int64, device=dev)
-            kernels.inject_rows(views[2], rows, d_senders, d_pick_ptr, d_picks, d_ptr, out_rows)
+            self.ops.inject_rows(views[2], rows, d_senders, d_pick_ptr, d_picks, d_ptr, out_rows)
             rows = out_rows
         n = int(ptr[-1])
         x = torch.empty((n, self.train_x.shape[1]), dtype=self.dtype, device=dev)
         y = torch.empty(n, dtype=torch.int64, device=dev)
-        kernels.gather_batch(self.train_x, self.augment, self.train_y, rows[:n], x, y)
+        self.ops.gather_batch(self.train_x, self.augment, self.train_y, rows[:n], x, y)
         return x, y, ptr
 
 
@@ -319,14 +340,15 @@ class ShardedSampler:
     """
 
     def __init__(self, train_x: np.ndarray, train_y: np.ndarray, pools: list[np.ndarray], lo: int, k: int, *,
-                 group=None, device: torch.device | None = None, dtype: torch.dtype = torch.float64):
+                 group=None, device: torch.device | None = None, dtype: torch.dtype = torch.float64, ops=None):
         self.n_dev, self.lo, self.k, self.group = len(pools), lo, k, group
         local = [np.asarray(pools[d], dtype=np.int64) for d in range(lo, lo + k)]
         self._rows = np.concatenate(local) if local else np.zeros(0, dtype=np.int64)
         offs = np.concatenate([[0], np.cumsum([len(p) for p in local])])
         local_pools = [np.arange(offs[i], offs[i + 1], dtype=np.int64) for i in range(k)]
         self.inner = DeviceSampler(np.asarray(train_x)[self._rows], np.asarray(train_y)[self._rows], local_pools,
-                                   device=device, dtype=dtype)
+                                   device=device, dtype=dtype, ops=ops)
+        self.ops = self.inner.ops
         self.device = self.inner.device
         self.F = self.inner.train_x.shape[1]
 
@@ -358,7 +380,7 @@ class ShardedSampler:
         sy = torch.zeros(smax, dtype=torch.int64, device=dev)
         if send_pos.size:
             d_pos = self.inner._upload([send_pos])[0]
-            kernels.gather_batch(x_own, None, y_own, d_pos, sx[:send_pos.size], sy[:send_pos.size])
+            self.ops.gather_batch(x_own, None, y_own, d_pos, sx[:send_pos.size], sy[:send_pos.size])
         # 3. allgatherv as one padded all-gather
         gx = torch.empty((world * smax, self.F), dtype=x_own.dtype, device=dev)
         gy = torch.empty(world * smax, dtype=torch.int64, device=dev)
@@ -387,5 +409,5 @@ class ShardedSampler:
         y = torch.empty(n, dtype=torch.int64, device=dev)
         if n:
             d_rows = self.inner._upload([rows])[0]
-            kernels.gather_batch(src_x, None, src_y, d_rows, x, y)
+            self.ops.gather_batch(src_x, None, src_y, d_rows, x, y)
         return x, y, np.asarray(ptr, dtype=np.int64)

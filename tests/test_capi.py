@@ -51,7 +51,7 @@ def test_sass_is_sm100a_with_tma(lib):
 
 
 def test_abi_version_and_status(lib):
-    assert lib.sg_abi_version() == 1
+    assert lib.sg_abi_version() == 2
     assert lib.sg_status_string(0) == b"ok"
     assert lib.sg_status_string(-1) == b"invalid argument"
     assert lib.sg_status_string(-3).startswith(b"workspace")
@@ -70,7 +70,7 @@ def test_invalid_arguments_rejected_without_a_gpu(lib):
     assert lib.sg_topk_gate_f32(None, 1, 10, 10, 1, None, None, None, None, None, None, None, None, 0, None) == -1
     w = (ctypes.c_double * 2)(0.5, 0.5)
     assert lib.sg_weighted_aggregate_f32(0, w, None, None, 0, None, None, None, None, 10, None, None, None,
-                                         0.0, 0.0, 0.0, 0, None, 0, None) == -1
+                                         0.0, 0.0, 0.0, 0, -1, None, 0, None) == -1
     assert lib.sg_sgd_momentum_f32(None, None, None, 10, 0.1, 0.9, 0.0, 1, None) == -1
     assert lib.sg_gather_batch_f64(None, None, None, 4, None, 1, None, None, None) == -1
     assert lib.sg_topk_workspace_bytes_f32(1, 10, 11) == 0  # m > dim

@@ -44,10 +44,19 @@ def test_engine_replay_bit_exact(cuda):
 
 
 def _reference_engine():
+    """The unmodified reference from baseline/_ref (tools/install_ref.py puts it there and it
+    travels with the gpurun snapshot).  Missing is a FAILURE, not a skip: this test is the
+    evidence for the drop-in claim."""
     ref = ROOT / "baseline" / "_ref"
-    if not (ref / "streamsgd").exists():
-        pytest.skip("reference package not installed in baseline/_ref")
-    sys.path.insert(0, str(ref))
+    if not (ref / "streamsgd").exists() and Path("/root/reference/pkg").exists():
+        sys.path.insert(0, str(ROOT / "tools"))
+        import install_ref
+
+        install_ref.install(quiet=True)
+    assert (ref / "streamsgd" / "engine.py").exists(), \
+        "reference package missing from baseline/_ref: run tools/install_ref.py before the GPU call"
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
     import streamsgd.cli as cli
     import streamsgd.config as config
     import streamsgd.engine as engine

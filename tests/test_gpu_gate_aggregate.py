@@ -153,19 +153,16 @@ def test_float32_aggregate_is_correctly_rounded(cuda):
     assert np.array_equal(b.cpu().numpy().view(np.uint32), bw.astype(np.float32).view(np.uint32))
 
 
-@pytest.mark.parametrize("merge_own", ["", "1"])
-def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own, monkeypatch):
+@pytest.mark.parametrize("merge_own", [-1, 1])
+def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own):
     """The multi-GPU entry points on one GPU (peer pointers may be local): two "ranks" of two
     workers each.  Mixed decisions: each rank's guarded partial (sg_weighted_partial_f32),
     summed in rank order with momentum SGD (sg_peer_reduce_sgd_f32), equals the oracle fold +
     SGD within the fp32 tolerance, and the all-sparse merge over per-worker pointers
     (sg_weighted_aggregate_peers_f32) is a no-op.  All compressed: the reverse, and the peer
-    merge is bit-identical to sg_weighted_aggregate_f32 on the same payloads (merge_own "1":
+    merge is bit-identical to sg_weighted_aggregate_f32 on the same payloads (merge_own 1:
     both through k_merge_own)."""
-    monkeypatch.setenv("SG_MERGE_OWN", merge_own)
     from paper_2301_08897_b200 import kernels
-
-    kernels.set_merge_kernel(-1)
 
     D, k, P = 100_003, 2, 2
     W = k * P
@@ -200,7 +197,8 @@ def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own, monkeypatch):
         partials = [torch.zeros(ld, dtype=torch.float32, device=cuda) for _ in range(P)]
         merge = kernels.PeerMergeLauncher(D, dec_all, [ranks[j // k][1][j % k].data_ptr() for j in range(W)],
                                           [ranks[j // k][2][j % k].data_ptr() for j in range(W)],
-                                          [ranks[j // k][3][j % k].data_ptr() for j in range(W)], params, buf, mu, wd)
+                                          [ranks[j // k][3][j % k].data_ptr() for j in range(W)], params, buf, mu, wd,
+                                          local_lo=0, local_n=k, sparse_merge=merge_own)
         merge(w, lr, False)
         for r in range(P):
             dl = kernels.GuardedDenseLaunchers(k, D, ld, dec_all[r * k:(r + 1) * k], ranks[r][1], ranks[r][2], rp,
@@ -225,13 +223,13 @@ def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own, monkeypatch):
             rp_all = torch.arange(0, (W + 1) * m, m, dtype=torch.int64, device=cuda)
             kernels.weighted_aggregate(w, D, compressed=dec_all, idx=idx_all, val=val_all, row_ptr=rp_all,
                                        tile_off=toff_all, params=p2, momentum_buf=b2, lr=lr, momentum=mu,
-                                       weight_decay=wd, first_step=False)
+                                       weight_decay=wd, first_step=False, sparse_merge=merge_own)
             assert torch.equal(params, p2) and torch.equal(buf, b2)
             assert np.max(np.abs(got - pw)) <= 1e-5 * np.max(np.abs(pw))
 
 
 @pytest.mark.parametrize("workers,hot,cr", [(8, 0.03, 0.02), (16, 0.03, 0.02), (8, 1.0, 0.1), (3, 1.0, 0.3)])
-def test_concentrated_payloads_merge_bit_exact(cuda, workers, hot, cr, monkeypatch):
+def test_concentrated_payloads_merge_bit_exact(cuda, workers, hot, cr):
     """Real gradients concentrate the kept entries in a few layers: here a 3 % region of the
     row carries large values, so its tiles hold far more entries than one staging chunk
     (the merge's multi-chunk path) and the cost-balanced tile ranges split the region over
@@ -269,15 +267,13 @@ def test_concentrated_payloads_merge_bit_exact(cuda, workers, hot, cr, monkeypat
     pw, bw = comm_ref.sgd_momentum(p0.astype(np.float64), b0.astype(np.float64), want, 0.05, 0.9, 1e-4)
     row_ptr = torch.arange(0, (W + 1) * m, m, dtype=torch.int64, device=cuda)
     # by density (k_merge_ws for the sparse cases, k_merge_own for hot=1.0), then each forced
-    kernels.set_merge_kernel(-1)
-    for mode in ("", "0", "1"):
-        monkeypatch.setenv("SG_MERGE_OWN", mode)
+    for mode in (-1, 0, 1):
         p = torch.from_numpy(p0.copy()).to(cuda)
         b = torch.from_numpy(b0.copy()).to(cuda)
         out = torch.empty(D, dtype=torch.float32, device=cuda)
         kernels.weighted_aggregate(w, D, compressed=torch.ones(W, dtype=torch.uint8, device=cuda), idx=idx, val=val,
                                    row_ptr=row_ptr, tile_off=toff, out=out, params=p, momentum_buf=b, lr=0.05,
-                                   momentum=0.9, weight_decay=1e-4, first_step=False)
+                                   momentum=0.9, weight_decay=1e-4, first_step=False, sparse_merge=mode)
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want.astype(np.float32).view(np.uint32)), mode
         assert np.array_equal(p.cpu().numpy().view(np.uint32), pw.astype(np.float32).view(np.uint32)), mode
         assert np.array_equal(b.cpu().numpy().view(np.uint32), bw.astype(np.float32).view(np.uint32)), mode

@@ -136,3 +136,60 @@ def test_partition_matches_reference():
         assert np.array_equal(pools[d], z[f"iidpool{d}"])
     with pytest.raises(ValueError):
         streams.partition(z["train_y"], 8, "noniid", 3, 0)
+
+
+# -- a14: lr_at_epoch / scale_lr (reference nn.py:175-190; known answers from test_nn.py:160-183) ----
+
+
+def test_scale_lr_known_answers_and_errors():
+    from paper_2301_08897_b200 import nn
+
+    assert nn.scale_lr(0.1, 1024, 1024) == 0.1
+    assert nn.scale_lr(0.1, 2048, 1024) == pytest.approx(0.2)
+    assert nn.scale_lr(0.01, 16 * 38, 1024) == pytest.approx(0.0059375)
+    # the engine's rate_matched lr (engine.py:277-281): base 0.1, S1 rates, B = n*64
+    assert nn.scale_lr(0.1, 236, 8 * 64) == 0.1 * 236 / 512
+    with pytest.raises(ValueError, match="base global batch must be >= 1"):
+        nn.scale_lr(0.1, 10, 0)
+    with pytest.raises(ValueError, match="sum of rates must be >= 1"):
+        nn.scale_lr(0.1, 0.5, 64)
+
+
+def test_lr_at_epoch_step_decay_compounds():
+    from paper_2301_08897_b200 import nn
+
+    schedule = [(75, 0.2), (150, 0.2), (225, 0.2)]
+    assert nn.lr_at_epoch(0.1, schedule, 10) == 0.1
+    assert nn.lr_at_epoch(0.1, schedule, 75) == pytest.approx(0.02)
+    assert nn.lr_at_epoch(0.1, schedule, 200) == pytest.approx(0.004)
+    assert nn.lr_at_epoch(0.1, schedule, 300) == pytest.approx(0.0008)
+    assert nn.lr_at_epoch(0.5, [], 1000) == 0.5
+
+
+@pytest.mark.parametrize("epoch", [0, 1, 2, 3, 74, 75, 149, 150, 224, 225, 1000])
+def test_lr_rules_bit_identical_to_reference(epoch):
+    """Same floating-point operation order as the reference (the lr feeds metrics.csv's
+    lr_used column, which must match byte for byte)."""
+    ref = _reference_nn()
+    from paper_2301_08897_b200 import nn
+
+    for sched in ([], [(1, 0.5)], [(75, 0.2), (150, 0.2), (225, 0.2)], [(2, 0.1), (3, 0.3)]):
+        for base in (0.1, 0.05, 0.3):
+            assert nn.lr_at_epoch(base, sched, epoch).hex() == ref.lr_at_epoch(base, sched, epoch).hex()
+            for s, b in ((204, 256), (236, 512), (1, 1), (9999, 64)):
+                assert nn.scale_lr(base, s, b).hex() == ref.scale_lr(base, s, b).hex()
+
+
+def _reference_nn():
+    import sys
+
+    from conftest import ROOT
+
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "streamsgd" / "nn.py").exists():
+        pytest.skip("reference not installed in baseline/_ref (tools/install_ref.py)")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import streamsgd.nn as ref_nn
+
+    return ref_nn

@@ -29,6 +29,8 @@ def main():
     z = torch.randn(ex.bucket.shape, device=dev, generator=gen)
     if args.family == "heavy":
         z = torch.sign(z) * torch.exp(1.5 * torch.randn(ex.bucket.shape, device=dev, generator=gen))
+    elif args.family == "tie":  # heavy ties at the threshold: the oversized-boundary (slow) resolve
+        z = torch.round(z * 2) / 2
     ex.bucket.copy_(z)
     w = np.full(args.workers, 1.0 / args.workers)
     for _ in range(args.steps):
