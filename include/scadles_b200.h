@@ -151,22 +151,33 @@ int sg_weighted_aggregate_peers_f32(int nw, const double* weights, const uint8_t
                                     double weight_decay, int first_step, int local_lo, int local_n,
                                     int sparse_merge, void* stream);
 
-/* The dense side of a mixed multi-GPU step, enqueued unconditionally and guarded on the
- * gathered decisions `guard[0..guard_n)` (device bytes): a no-op unless some worker did not
- * compress.  sg_weighted_partial_f32 folds this rank's workers (dense rows or payloads, the
- * sg_weighted_aggregate_f32 argument meaning) into `out` (the rank's partial, float32);
- * sg_peer_reduce_sgd_f32 sums the nranks partials (HOST array of device pointers, peers'
- * memory allowed, 16-byte aligned) in ascending rank order in float64 and applies momentum
- * SGD (nn.py:161-172), writing the aggregate to `out` if non-NULL.  Together they replace the
- * partial + all-reduce + SGD of engine.py:270-283 when decisions are mixed, without a host
- * read of the decisions. */
+/* The dense side of a mixed (or dense-workload) multi-GPU step over peer memory, O(D) NVLink
+ * bytes per rank (a ring all-reduce's 2(P-1)/P * 4D), every launch guarded on the gathered
+ * decisions `guard[0..guard_n)` (device bytes; a no-op unless some worker did not compress;
+ * guard_n = 0: unconditional).  Together they replace the partial + all-reduce + SGD of
+ * engine.py:270-283 when decisions are mixed, without a host read of the decisions:
+ *   sg_weighted_partial_f32     this rank's workers (dense rows or payloads, the
+ *                               sg_weighted_aggregate_f32 argument meaning) folded into `out`,
+ *                               the rank's partial (float32);
+ *   sg_peer_reduce_slice_f32    position-sharded reduce: rank `rank` owns slice
+ *                               [rank*L, min((rank+1)*L, dim)), L = sg_peer_slice_len(dim, P);
+ *                               dst[slice] = sum_q w_q * src_q[slice] in ascending q (float64,
+ *                               round-to-nearest, rounded once to float32; weights NULL = 1.0).
+ *                               src: HOST array of nranks <= 8 device pointers (peers' memory
+ *                               allowed, 16-byte aligned); dst may be src[rank];
+ *   sg_peer_allgather_sgd_f32   element i's aggregate read from src[owner(i)] (the reduced
+ *                               slices), momentum SGD (nn.py:161-172) on the full replica;
+ *                               `out` (optional) receives the aggregate. */
 int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compressed, const float* dense,
                             int64_t ld_dense, const uint32_t* idx, const float* val, const int64_t* row_ptr,
                             const int32_t* tile_off, int64_t dim, float* out, const uint8_t* guard,
                             int guard_n, void* workspace, size_t workspace_bytes, void* stream);
-int sg_peer_reduce_sgd_f32(int nranks, const float* const* partials, const uint8_t* guard, int guard_n,
-                           int64_t dim, float* out, float* params, float* momentum_buf, double lr,
-                           double momentum, double weight_decay, int first_step, void* stream);
+int64_t sg_peer_slice_len(int64_t dim, int nranks);
+int sg_peer_reduce_slice_f32(int nranks, const float* const* src, const double* weights, int rank,
+                             const uint8_t* guard, int guard_n, int64_t dim, float* dst, void* stream);
+int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, const uint8_t* guard, int guard_n, int64_t dim,
+                              float* out, float* params, float* momentum_buf, double lr, double momentum,
+                              double weight_decay, int first_step, void* stream);
 
 /* dst[i * each + b] = src[i][b] for i < nsrc (<= 64 device pointers in a HOST array; peers'
  * memory allowed): gathers the ranks' decision bytes before the host reads them. */

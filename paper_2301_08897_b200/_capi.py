@@ -87,7 +87,12 @@ SIGNATURES = {
         c_int,
         [c_int, POINTER(c_double), _P, _P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, c_int, _P, c_size_t, _P],
     ),
-    "sg_peer_reduce_sgd_f32": (
+    "sg_peer_slice_len": (c_int64, [c_int64, c_int]),
+    "sg_peer_reduce_slice_f32": (
+        c_int,
+        [c_int, POINTER(c_void_p), POINTER(c_double), c_int, _P, c_int, c_int64, _P, _P],
+    ),
+    "sg_peer_allgather_sgd_f32": (
         c_int,
         [c_int, POINTER(c_void_p), _P, c_int, c_int64, _P, _P, _P, c_double, c_double, c_double, c_int, _P],
     ),

@@ -1486,54 +1486,127 @@ int aggregate_peers(int nw, const double* weights, const uint8_t* comp, const ui
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
+// The dense exchange of a mixed (or dense-workload) multi-GPU step without a collective
+// library, O(D) NVLink bytes per rank: position-sharded reduce, then an all-gather fused with
+// momentum SGD.  Rank r owns slice r = [r*L, min((r+1)*L, dim)) with L = peer_slice_len(dim, P)
+// (a multiple of 4 elements, so slices stay 16-byte aligned).
+//   k_peer_reduce_slice   g[slice r] = sum_q w_q * src_q[slice r] in ascending q (float64,
+//                         IEEE round-to-nearest), rounded once to float32 and written to
+//                         dst[slice r] (dst may be this rank's own source: slice r of a rank's
+//                         partial is read by that rank only).  Reads (P-1)/P * 4D over NVLink.
+//   k_peer_allgather_sgd  every rank reads element i's aggregate from its owner's buffer
+//                         (P-1)/P * 4D over NVLink) and applies momentum SGD (nn.py:167-171
+//                         order, binary64) to its full replica, so replicas stay bit-identical.
+// Both are guarded: a no-op unless some worker in `guard` did not compress (guard NULL: always).
+inline long long peer_slice_len(long long dim, int P) {
+    const long long per = (dim + P - 1) / P;
+    return (per + 3) / 4 * 4;
+}
+
 struct PeerRows {
     const float* p[MAX_WORKERS];
+    double w[MAX_WORKERS];
 };
 
-// The dense exchange of a mixed multi-GPU step without a collective library: every rank's
-// local partial sum sits in a peer-mapped buffer; g = sum over ranks in ascending rank order
-// (float64), then momentum SGD (nn.py:167-171 order, binary64).  Guarded: a no-op unless some
-// worker in `guard` did not compress.
-__global__ void __launch_bounds__(256)
-k_peer_reduce_sgd(PeerRows src, int P, const uint8_t* __restrict__ guard, int gn, long long dim,
-                  float* __restrict__ out, float* __restrict__ p, float* __restrict__ b, double lr, double mu,
-                  double wd, int first) {
-    pdl_enter();
+SG_DEV bool peer_guard_run(const uint8_t* guard, int gn) {
     __shared__ int s_run;
     if (threadIdx.x == 0) {
-        int any0 = 0;
+        int any0 = guard == nullptr ? 1 : 0;
         for (int j = 0; j < gn; ++j) any0 |= guard[j] == 0;
         s_run = any0;
     }
     __syncthreads();
-    if (!s_run) return;
-    const long long n4 = dim / 4, stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-        double g[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int r = 0; r < P; ++r) {
-            const float4 x = reinterpret_cast<const float4*>(src.p[r])[i];
-            g[0] = dadd(g[0], (double)x.x);
-            g[1] = dadd(g[1], (double)x.y);
-            g[2] = dadd(g[2], (double)x.z);
-            g[3] = dadd(g[3], (double)x.w);
+    return s_run != 0;
+}
+
+__global__ void __launch_bounds__(256)
+k_peer_reduce_slice(PeerRows src, int P, int unit_w, long long lo, long long hi, const uint8_t* __restrict__ guard,
+                    int gn, float* __restrict__ dst) {
+    pdl_enter();
+    if (!peer_guard_run(guard, gn)) return;
+    const long long n4 = (hi - lo) / 4, stride = (long long)gridDim.x * blockDim.x;
+    constexpr int U = 2;  // float4 groups per thread per iteration: P*U independent loads in flight
+    for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+        float4 x[U][MAX_PEERS];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = i0 + u * stride;
+            if (i < n4) {
+#pragma unroll
+                for (int r = 0; r < MAX_PEERS; ++r)
+                    if (r < P) x[u][r] = __ldcv(reinterpret_cast<const float4*>(src.p[r] + lo) + i);
+            }
         }
-        const float4 pv = reinterpret_cast<const float4*>(p)[i], bv = reinterpret_cast<const float4*>(b)[i];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = i0 + u * stride;
+            if (i >= n4) continue;
+            double g[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int r = 0; r < MAX_PEERS; ++r) {
+                if (r >= P) break;
+                const double wr = src.w[r];
+                const float4 v = x[u][r];
+                if (unit_w) {
+                    g[0] = dadd(g[0], (double)v.x);
+                    g[1] = dadd(g[1], (double)v.y);
+                    g[2] = dadd(g[2], (double)v.z);
+                    g[3] = dadd(g[3], (double)v.w);
+                } else {
+                    g[0] = dadd(g[0], dmul(wr, (double)v.x));
+                    g[1] = dadd(g[1], dmul(wr, (double)v.y));
+                    g[2] = dadd(g[2], dmul(wr, (double)v.z));
+                    g[3] = dadd(g[3], dmul(wr, (double)v.w));
+                }
+            }
+            reinterpret_cast<float4*>(dst + lo)[i] = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+        }
+    }
+    // ragged tail of the last slice (dim not a multiple of 4)
+    for (long long q = lo + n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += stride) {
+        double g = 0.0;
+        for (int r = 0; r < P; ++r) g = unit_w ? dadd(g, (double)src.p[r][q]) : dadd(g, dmul(src.w[r], (double)src.p[r][q]));
+        dst[q] = (float)g;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_peer_allgather_sgd(PeerRows src, int P, long long L, const uint8_t* __restrict__ guard, int gn, long long dim,
+                     float* __restrict__ out, float* __restrict__ p, float* __restrict__ b, double lr, double mu,
+                     double wd, int first) {
+    pdl_enter();
+    if (!peer_guard_run(guard, gn)) return;
+    const long long n4 = dim / 4, stride = (long long)gridDim.x * blockDim.x;
+    const long long L4 = L / 4;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const int q = (int)(i / L4);
+        const float4 gv = __ldcv(reinterpret_cast<const float4*>(src.p[q]) + i);
+        const float4 pv = reinterpret_cast<const float4*>(p)[i];
+        const float4 bv = first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(b)[i];
+        double g[4] = {gv.x, gv.y, gv.z, gv.w};
         double pd[4] = {pv.x, pv.y, pv.z, pv.w}, bd[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
         for (int c = 0; c < 4; ++c) sgd_elem(g[c], pd[c], bd[c], lr, mu, wd, first != 0);
         reinterpret_cast<float4*>(p)[i] = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
         reinterpret_cast<float4*>(b)[i] = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
-        if (out) reinterpret_cast<float4*>(out)[i] = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+        if (out) reinterpret_cast<float4*>(out)[i] = gv;
     }
-    for (long long q = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < dim; q += stride) {
-        double g = 0.0;
-        for (int r = 0; r < P; ++r) g = dadd(g, (double)src.p[r][q]);
-        double pq = p[q], bq = b[q];
+    for (long long qd = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; qd < dim; qd += stride) {
+        const int q = (int)(qd / L);
+        const double g = (double)__ldcv(src.p[q] + qd);
+        double pq = p[qd], bq = first ? 0.0 : (double)b[qd];
         sgd_elem(g, pq, bq, lr, mu, wd, first != 0);
-        p[q] = (float)pq;
-        b[q] = (float)bq;
-        if (out) out[q] = (float)g;
+        p[qd] = (float)pq;
+        b[qd] = (float)bq;
+        if (out) out[qd] = (float)g;
     }
+}
+
+inline long long peer_blocks(long long n4) {
+    long long blocks = (n4 + 255) / 256;
+    const long long cap = (long long)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    return blocks < 1 ? 1 : blocks;
 }
 
 struct GatherSrc {
@@ -1618,26 +1691,51 @@ int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compre
                                    -1, guard, guard_n, 2);
 }
 
-int sg_peer_reduce_sgd_f32(int nranks, const float* const* partials, const uint8_t* guard, int guard_n,
-                           int64_t dim, float* out, float* params, float* momentum_buf, double lr,
-                           double momentum, double weight_decay, int first_step, void* stream) {
-    if (nranks < 1 || nranks > MAX_WORKERS || !partials || !guard || guard_n < 1 || guard_n > MAX_WORKERS ||
-        dim < 1 || !params || !momentum_buf)
+int64_t sg_peer_slice_len(int64_t dim, int nranks) {
+    if (dim < 1 || nranks < 1) return -1;
+    return peer_slice_len(dim, nranks);
+}
+
+int sg_peer_reduce_slice_f32(int nranks, const float* const* src, const double* weights, int rank,
+                             const uint8_t* guard, int guard_n, int64_t dim, float* dst, void* stream) {
+    if (nranks < 1 || nranks > MAX_PEERS || !src || !dst || rank < 0 || rank >= nranks || dim < 1 ||
+        guard_n < 0 || guard_n > MAX_WORKERS || (guard_n > 0 && !guard))
         return SG_ERR_INVALID;
-    PeerRows r;
+    if (dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
+    PeerRows r = {};
     for (int i = 0; i < nranks; ++i) {
-        if (!partials[i] || reinterpret_cast<size_t>(partials[i]) % 16) return SG_ERR_UNSUPPORTED;
-        r.p[i] = partials[i];
+        if (!src[i] || reinterpret_cast<size_t>(src[i]) % 16) return SG_ERR_UNSUPPORTED;
+        r.p[i] = src[i];
+        r.w[i] = weights ? weights[i] : 1.0;
+    }
+    if (reinterpret_cast<size_t>(dst) % 16) return SG_ERR_UNSUPPORTED;
+    const long long L = peer_slice_len(dim, nranks);
+    long long lo = (long long)rank * L, hi = lo + L < dim ? lo + L : dim;
+    if (lo > dim) lo = dim;
+    if (hi < lo) hi = lo;
+    launch_pdl(k_peer_reduce_slice, dim3((unsigned)peer_blocks((hi - lo) / 4 / 2 + 1)), dim3(256), 0,
+               (cudaStream_t)stream, r, nranks, weights ? 0 : 1, lo, hi, guard_n > 0 ? guard : nullptr, guard_n, dst);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, const uint8_t* guard, int guard_n, int64_t dim,
+                              float* out, float* params, float* momentum_buf, double lr, double momentum,
+                              double weight_decay, int first_step, void* stream) {
+    if (nranks < 1 || nranks > MAX_PEERS || !src || dim < 1 || !params || !momentum_buf || guard_n < 0 ||
+        guard_n > MAX_WORKERS || (guard_n > 0 && !guard))
+        return SG_ERR_INVALID;
+    if (dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
+    PeerRows r = {};
+    for (int i = 0; i < nranks; ++i) {
+        if (!src[i] || reinterpret_cast<size_t>(src[i]) % 16) return SG_ERR_UNSUPPORTED;
+        r.p[i] = src[i];
     }
     if (reinterpret_cast<size_t>(params) % 16 || reinterpret_cast<size_t>(momentum_buf) % 16 ||
         (out && reinterpret_cast<size_t>(out) % 16))
         return SG_ERR_UNSUPPORTED;
-    long long blocks = (dim / 4 + 255) / 256;
-    const long long cap = (long long)num_sms() * 8;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    launch_pdl(k_peer_reduce_sgd, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream, r, nranks, guard,
-               guard_n, (long long)dim, out, params, momentum_buf, lr, momentum, weight_decay, first_step);
+    launch_pdl(k_peer_allgather_sgd, dim3((unsigned)peer_blocks(dim / 4)), dim3(256), 0, (cudaStream_t)stream, r,
+               nranks, (long long)peer_slice_len(dim, nranks), guard_n > 0 ? guard : nullptr, guard_n, (long long)dim,
+               out, params, momentum_buf, lr, momentum, weight_decay, first_step);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

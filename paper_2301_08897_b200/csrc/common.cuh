@@ -22,6 +22,7 @@ namespace sg {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAX_WORKERS = 64;
+constexpr int MAX_PEERS = 8;  // GPUs of one NVSwitch node in a peer-memory exchange
 
 // ---------------------------------------------------------------------------------------
 // Top-k ordering key.  The reference orders by np.lexsort((arange, -|g|)) (comm.py:94):

@@ -194,7 +194,7 @@ class GradientExchange:
                 self._dense = kernels.GuardedDenseLaunchers(
                     k, dim, self.ld, self.decision, self.idx, self.val, self.row_ptr_local, self.tile_off,
                     self._partial_buf, [ph.buffer_ptrs[r] + poff for r in range(P)], self.dec_all,
-                    self.params, self.momentum_buf, momentum, weight_decay)
+                    self.params, self.momentum_buf, momentum, weight_decay, self.rank)
             elif self.packed:
                 P, words, dw = self.world, self.pack_words, self.pack_dw
                 self.pack_all = torch.empty(P * words, dtype=torch.int32, **z)
@@ -220,26 +220,53 @@ class GradientExchange:
                 self.row_ptr_all = torch.arange(0, (self.W + 1) * m, m, dtype=torch.int64, **z)
                 self.tile_off_all = (torch.empty((self.W, nt1), dtype=torch.int32, **z)
                                      if self.tile_off is not None else None)
+        # dense workload at P > 1 over peer memory: partial -> position-sharded reduce ->
+        # all-gather fused with SGD (O(D) NVLink bytes per rank), no collective library
+        self._dense_peer = None
+        if (not compression and self.world > 1 and dtype == torch.float32 and device.type == "cuda"
+                and os.environ.get("SG_P2P", "1") != "0" and self.world <= 8):
+            self._symm = None
+            self._partial_h = None
+            self._setup_peer_buffers(None)
+            if self._partial_h is not None:
+                ph = self._partial_h
+                poff = self._partial_buf.data_ptr() - ph.buffer_ptrs[self.rank]
+                self._dense_peer = kernels.GuardedDenseLaunchers(
+                    k, dim, self.ld, None, None, None, None, None, self._partial_buf,
+                    [ph.buffer_ptrs[r] + poff for r in range(self.world)], None, self.params, self.momentum_buf,
+                    momentum, weight_decay, self.rank)
+        # float64 ("exact") mode at P > 1: every rank folds all W payloads in ascending worker
+        # order (the dense rows are gathered too), so the aggregate and the update are
+        # bit-identical to the reference's at any P (the drop-in / metrics path, small D)
+        self.exact = dtype == torch.float64 and self.world > 1
+        if self.exact:
+            self.bucket_all = torch.empty((self.W, self.ld), dtype=dtype, **z)
+            if not compression:
+                self.dec_all = None
         self.partial = torch.empty(dim, dtype=dtype, **z) if self.world > 1 else None
         self._dec_ring = None
         self.aggregate = None
         self.steps = 0
 
-    def _setup_peer_buffers(self, words: int) -> None:
-        """Symmetric (peer-mapped) send and partial buffers, so the merge reads the other
-        ranks' payloads in place over NVLink instead of an all-gather.  The choice is
-        collective: every rank reports whether both rendezvous succeeded and the peer path is
-        taken only if all did (otherwise every rank takes the NCCL all-gather path -- a rank
-        that silently fell back alone would hang the others in the peer barriers)."""
+    def _setup_peer_buffers(self, words: int | None) -> None:
+        """Symmetric (peer-mapped) send buffer (``words`` int32; None: none) and partial buffer,
+        so the merge reads the other ranks' payloads, and the dense side their partials, in
+        place over NVLink.  The choice is collective: every rank reports whether every
+        rendezvous succeeded and the peer path is taken only if all did (otherwise every rank
+        takes the NCCL path -- a rank that silently fell back alone would hang the others in
+        the peer barriers)."""
         ok = 1
+        symm = pack = None
         try:
             import torch.distributed._symmetric_memory as symm_mem
 
             grp = self.group if self.group is not None else dist.group.WORLD
-            pack = symm_mem.empty(words, dtype=torch.int32, device=self.device)
-            pack.zero_()
-            symm = symm_mem.rendezvous(pack, grp.group_name)
+            if words is not None:
+                pack = symm_mem.empty(words, dtype=torch.int32, device=self.device)
+                pack.zero_()
+                symm = symm_mem.rendezvous(pack, grp.group_name)
             part = symm_mem.empty(self.ld, dtype=torch.float32, device=self.device)
+            part.zero_()
             part_h = symm_mem.rendezvous(part, grp.group_name)
         except Exception:  # no peer mapping on this system
             ok = 0
@@ -251,6 +278,7 @@ class GradientExchange:
             self._partial_buf, self._partial_h = part, part_h
         else:
             self._symm = None
+            self._partial_h = None
 
     # -- the step ---------------------------------------------------------------------------
 
@@ -304,6 +332,18 @@ class GradientExchange:
     def _exchange(self, w, out, opt) -> str:
         g = self.group
         dim = self.dim
+        if self.exact:
+            return self._exact_exchange(w, out, opt)
+        if self._dense_peer is not None:
+            # dense workload over peer memory: O(D) NVLink bytes per rank, fused update
+            h = self._partial_h
+            self._dense_peer.partial(w[self.lo:self.lo + self.k], self.bucket)
+            h.barrier(channel=0)
+            self._dense_peer.reduce_slice()
+            h.barrier(channel=0)
+            self._dense_peer.allgather_sgd(opt["lr"], opt["first_step"], out)
+            h.barrier(channel=0)  # no rank rewrites its partial while a peer still reads it
+            return "dense-peer"
         if self.packed and self._symm is not None:
             # Peer path, no host synchronisation: after a device barrier (every rank's Top-k has
             # written its symmetric send buffer) the W decisions are gathered on device, and both
@@ -324,8 +364,10 @@ class GradientExchange:
             self._side.wait_event(self._gathered)
             with torch.cuda.stream(self._side):
                 self._dense.partial(w[self.lo:self.lo + self.k], self.bucket)
-                self._symm.barrier(channel=1)
-                self._dense.reduce_sgd(lr, first, out)
+                self._symm.barrier(channel=1)  # every rank's partial is written
+                self._dense.reduce_slice()
+                self._symm.barrier(channel=1)  # every rank's slice is reduced
+                self._dense.allgather_sgd(lr, first, out)
             self._peer_merge(w, lr, first, out)
             main.wait_stream(self._side)
             self._symm.barrier(channel=0)
@@ -389,6 +431,28 @@ class GradientExchange:
                                row_ptr=self.row_ptr_all, tile_off=self.tile_off_all, out=out, **opt)
             return "sparse-allgather"
         return self._dense_exchange(w, out, opt)
+
+    def _exact_exchange(self, w, out, opt) -> str:
+        """float64 mode: all-gather decisions, payloads and (if any worker stayed dense) the
+        dense rows; every rank folds the W workers in ascending order with the fused update
+        (comm.py:75-77 order), so every rank's bytes equal the one-process reference's."""
+        g = self.group
+        dim = self.dim
+        if self.compression:
+            dist.all_gather_into_tensor(self.dec_all, self.decision, group=g)
+            all_compressed = bool(self.dec_all.min().item() == 1)
+            dist.all_gather_into_tensor(self.idx_all.view(-1), self.idx.view(-1), group=g)
+            dist.all_gather_into_tensor(self.val_all.view(-1), self.val.view(-1), group=g)
+        else:
+            all_compressed = False
+        if not all_compressed:
+            dist.all_gather_into_tensor(self.bucket_all.view(-1), self.bucket.view(-1), group=g)
+        if self.compression:
+            self.ops.aggregate(w, dim, compressed=self.dec_all, dense=None if all_compressed else self.bucket_all,
+                               idx=self.idx_all, val=self.val_all, row_ptr=self.row_ptr_all, out=out, **opt)
+        else:
+            self.ops.aggregate(w, dim, dense=self.bucket_all, out=out, **opt)
+        return "exact-allgather"
 
     def _dense_exchange(self, w, out, opt) -> str:
         """Mixed decisions: local partial (dense rows + local payloads), all-reduce, SGD."""

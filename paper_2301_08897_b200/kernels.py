@@ -278,37 +278,55 @@ class PeerMergeLauncher:
 
 
 class GuardedDenseLaunchers:
-    """The mixed-decision side of a multi-GPU step, enqueued every step and guarded on the
-    gathered decisions: this rank's partial (sg_weighted_partial_f32) into its peer-mapped
-    buffer, and the rank-ordered reduction + SGD over every rank's partial
-    (sg_peer_reduce_sgd_f32).  Both are no-ops when every worker compressed."""
+    """The dense side of a multi-GPU step over peer memory, O(D) NVLink bytes per rank:
+    this rank's partial (sg_weighted_partial_f32) into its peer-mapped buffer, the
+    position-sharded reduce of its slice over every rank's partial (sg_peer_reduce_slice_f32,
+    written in place into its own buffer) and the all-gather of the reduced slices fused with
+    momentum SGD (sg_peer_allgather_sgd_f32).  Guarded on the gathered decisions: no-ops when
+    every worker compressed (``guard`` None: the dense workload, always run)."""
 
     def __init__(self, k: int, dim: int, ld: int, compressed, idx, val, row_ptr, tile_off, partial: torch.Tensor,
-                 partial_ptrs, guard: torch.Tensor, params, momentum_buf, momentum: float, weight_decay: float):
+                 partial_ptrs, guard, params, momentum_buf, momentum: float, weight_decay: float, rank: int):
         lib = _capi.load()
-        self._part, self._red = lib.sg_weighted_partial_f32, lib.sg_peer_reduce_sgd_f32
-        self._k, self._dim, self._ld = k, dim, ld
+        self._part, self._red, self._ag = lib.sg_weighted_partial_f32, lib.sg_peer_reduce_slice_f32, \
+            lib.sg_peer_allgather_sgd_f32
+        self._k, self._dim, self._ld, self._rank = k, dim, ld, int(rank)
         self._w = np.zeros(k, dtype=np.float64)
         _, self._wp = _capi.weights_ptr(self._w)
-        self._comp, self._idx, self._val = compressed.data_ptr(), idx.data_ptr(), val.data_ptr()
-        self._rp, self._toff = row_ptr.data_ptr(), tile_off.data_ptr()
+        self._comp = _ptr(compressed)
+        self._idx, self._val = _ptr(idx), _ptr(val)
+        self._rp, self._toff = _ptr(row_ptr), _ptr(tile_off)
         self._partial = partial.data_ptr()
         self._pp = (ctypes.c_void_p * len(partial_ptrs))(*partial_ptrs)
-        self._guard, self._gn = guard.data_ptr(), guard.numel()
+        self._guard, self._gn = (guard.data_ptr(), guard.numel()) if guard is not None else (None, 0)
         self._p, self._b = params.data_ptr(), momentum_buf.data_ptr()
         self._mu, self._wd = float(momentum), float(weight_decay)
+        self._ws = None
 
     def partial(self, local_weights, bucket: torch.Tensor) -> None:
         self._w[:] = local_weights
+        if self._comp is None:  # dense workload: a weighted row fold, the same kernel family
+            st = _capi.load().sg_weighted_aggregate_f32(
+                self._k, self._wp, None, bucket.data_ptr(), self._ld, None, None, None, None, self._dim,
+                self._partial, None, None, 0.0, 0.0, 0.0, 0, -1, None, 0, _stream())
+            _capi.check(st, "sg_weighted_aggregate_f32")
+            _count(1)
+            return
         st = self._part(self._k, self._wp, self._comp, bucket.data_ptr(), self._ld, self._idx, self._val, self._rp,
                         self._toff, self._dim, self._partial, self._guard, self._gn, None, 0, _stream())
         _capi.check(st, "sg_weighted_partial_f32")
         _count(1)
 
-    def reduce_sgd(self, lr: float, first_step: bool, out: torch.Tensor | None = None) -> None:
-        st = self._red(len(self._pp), self._pp, self._guard, self._gn, self._dim, _ptr(out), self._p, self._b,
-                       float(lr), self._mu, self._wd, int(bool(first_step)), _stream())
-        _capi.check(st, "sg_peer_reduce_sgd_f32")
+    def reduce_slice(self) -> None:
+        st = self._red(len(self._pp), self._pp, None, self._rank, self._guard, self._gn, self._dim, self._partial,
+                       _stream())
+        _capi.check(st, "sg_peer_reduce_slice_f32")
+        _count(1)
+
+    def allgather_sgd(self, lr: float, first_step: bool, out: torch.Tensor | None = None) -> None:
+        st = self._ag(len(self._pp), self._pp, self._guard, self._gn, self._dim, _ptr(out), self._p, self._b,
+                      float(lr), self._mu, self._wd, int(bool(first_step)), _stream())
+        _capi.check(st, "sg_peer_allgather_sgd_f32")
         _count(1)
 
 

@@ -14,44 +14,11 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from host_ops import NumpySamplerOps
 from paper_2301_08897_b200 import streams
 
 N_TRAIN, F, LABELS, N_DEV, LPD = 1_200, 24, 100, 8, 25
 RATES = [31, 30, 1, 30, 42, 66, 22, 14]
-
-
-class NumpySamplerOps:
-    """Test-only stand-in for kernels.{resolve_stream_rows, inject_rows, gather_batch}."""
-
-    @staticmethod
-    def resolve_stream_rows(head, b, out_ptr, pool_ptr, pool_rows, total, out):
-        for d in range(head.numel()):
-            lo, n = int(pool_ptr[d]), int(pool_ptr[d + 1] - pool_ptr[d])
-            for i in range(int(b[d])):
-                out[int(out_ptr[d]) + i] = pool_rows[lo + (int(head[d]) + i) % n]
-
-    @staticmethod
-    def inject_rows(base_ptr, base_rows, senders, pick_ptr, picks, out_ptr, out_rows):
-        n_dev = base_ptr.numel() - 1
-        for d in range(n_dev):
-            o = int(out_ptr[d])
-            own = base_rows[int(base_ptr[d]):int(base_ptr[d + 1])]
-            out_rows[o:o + own.numel()] = own
-            o += own.numel()
-            for k in range(senders.numel()):
-                s = int(senders[k])
-                if s == d:
-                    continue
-                for q in range(int(pick_ptr[k]), int(pick_ptr[k + 1])):
-                    out_rows[o] = base_rows[int(base_ptr[s]) + int(picks[q])]
-                    o += 1
-
-    @staticmethod
-    def gather_batch(train_x, augment, train_y, rows, x_out, y_out):
-        r = rows.long()
-        x_out.copy_(train_x[r] + augment[r] if augment is not None else train_x[r])
-        if y_out is not None:
-            y_out.copy_(train_y[r])
 
 
 def data():

@@ -119,6 +119,8 @@ def test_multi_gpu_exchange_matches_single_gpu(cuda):
         rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
         assert rep["ok"] and rep["world"] == n
         assert rep["cases"][0]["paths"] == [sparse_path] * 3, rep["cases"][0]
+        dense_path = "dense-peer" if p2p == "1" else "dense-allreduce"
+        assert rep["cases"][-1]["paths"] == [dense_path] * 3, rep["cases"][-1]  # the dense workload
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")

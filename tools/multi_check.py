@@ -36,7 +36,9 @@ def fill(ex, family, step):
 
 
 def run(family, cr, delta, group, dev, steps=3):
-    ex = exchange.GradientExchange(D, W, cr=cr, delta=delta, momentum=0.9, weight_decay=1e-4, group=group, device=dev)
+    compression = cr is not None
+    ex = exchange.GradientExchange(D, W, cr=cr or 0.01, delta=delta or 0.3, compression=compression, momentum=0.9,
+                                   weight_decay=1e-4, group=group, device=dev)
     w = comm.weights_from_rates(([31, 30, 1, 30, 42, 66, 22, 14] * 8)[:W])
     paths = []
     for s in range(steps):
@@ -56,7 +58,9 @@ def main():
     ok = True
     report = {"world": world, "cases": []}
     # (heavy, 0.1: all compressed at 0.8 kept entries per position -> k_merge_own over peer memory)
-    for family, cr, delta in (("heavy", 0.01, 0.5), ("normal", 0.01, 0.3), ("mixed", 0.1, 0.5), ("heavy", 0.1, 0.5)):
+    # (None: the dense workload, compression off -> peer reduce-scatter + all-gather/SGD or NCCL)
+    for family, cr, delta in (("heavy", 0.01, 0.5), ("normal", 0.01, 0.3), ("mixed", 0.1, 0.5), ("heavy", 0.1, 0.5),
+                              ("normal", None, None)):
         p, a, paths = run(family, cr, delta, dist.group.WORLD, dev)
         # every rank holds identical bytes
         t = torch.from_numpy(p).to(dev)
