@@ -71,6 +71,11 @@ int64_t sg_topk_count(int64_t dim, double cr);
  * (unaligned rows fall back to scalar loads, still on the GPU). */
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m);
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m);
+/* The float32 path is one persistent cooperative kernel whose workspace carries zero-state
+ * between calls: the first sg_topk_workspace_zero_bytes_f32(k, dim, m) bytes must be zero
+ * before the first call and whenever (k, dim, m) change; every call leaves them zeroed.  Its
+ * candidate pool holds ~2m entries (not D), so the workspace is ~16 m + 1.2 MB per worker. */
+size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m);
 int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m,
                      uint32_t* idx, float* val, double* norms2,
                      sg_gate_state* states, uint8_t* decision, double* rho,
@@ -83,11 +88,19 @@ int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m,
 
 /* Diagnostics of the most recent sg_topk_gate_* call that used `workspace` (same k, dim, m):
  * out[4j..4j+3] (device int64) = {candidates kept by the main pass, boundary entries, fallback
- * pass taken (0/1), oversized-tie write mode (0/1)} for worker j. */
+ * pass taken (0/1), oversized-tie write mode (0/1)} for worker j.  float32: {candidates,
+ * boundary entries, estimate undershot (0/1), exact multi-pass fallback taken (0/1)}. */
 int sg_topk_stats_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes,
                       int64_t* out, void* stream);
 int sg_topk_stats_f64(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes,
                       int64_t* out, void* stream);
+
+/* float32 diagnostics: segments (CTAs) per worker of the persistent Top-k kernel, and the
+ * %globaltimer stamps (ns) of its phases in the last call: out[(w*nseg + s)*8 + i] = {start,
+ * estimate done, main pass done, selection known, CTA done, cleanup done (last CTA only), -, -}. */
+int sg_topk_segments_f32(int k, int64_t dim, int64_t m);
+int sg_topk_phases_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes, uint64_t* out,
+                       int64_t out_len, void* stream);
 
 /* Gate update alone from precomputed norms2[2k] (comm.py:143-160). */
 int sg_gate_update(const double* norms2, int k, sg_gate_state* states,
@@ -167,7 +180,8 @@ int sg_weighted_aggregate_peers_f32(int nw, const double* weights, const uint8_t
  *                               allowed, 16-byte aligned); dst may be src[rank];
  *   sg_peer_allgather_sgd_f32   element i's aggregate read from src[owner(i)] (the reduced
  *                               slices), momentum SGD (nn.py:161-172) on the full replica;
- *                               `out` (optional) receives the aggregate. */
+ *                               `out` (optional) receives the aggregate; `rank` staggers the
+ *                               slice order so the P ranks pull from P different owners. */
 int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compressed, const float* dense,
                             int64_t ld_dense, const uint32_t* idx, const float* val, const int64_t* row_ptr,
                             const int32_t* tile_off, int64_t dim, float* out, const uint8_t* guard,
@@ -175,8 +189,8 @@ int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compre
 int64_t sg_peer_slice_len(int64_t dim, int nranks);
 int sg_peer_reduce_slice_f32(int nranks, const float* const* src, const double* weights, int rank,
                              const uint8_t* guard, int guard_n, int64_t dim, float* dst, void* stream);
-int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, const uint8_t* guard, int guard_n, int64_t dim,
-                              float* out, float* params, float* momentum_buf, double lr, double momentum,
+int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, int rank, const uint8_t* guard, int guard_n,
+                              int64_t dim, float* out, float* params, float* momentum_buf, double lr, double momentum,
                               double weight_decay, int first_step, void* stream);
 
 /* dst[i * each + b] = src[i][b] for i < nsrc (<= 64 device pointers in a HOST array; peers'

@@ -61,9 +61,12 @@ SIGNATURES = {
     "sg_topk_count": (c_int64, [c_int64, c_double]),
     "sg_topk_workspace_bytes_f32": (c_size_t, [c_int, c_int64, c_int64]),
     "sg_topk_workspace_bytes_f64": (c_size_t, [c_int, c_int64, c_int64]),
+    "sg_topk_workspace_zero_bytes_f32": (c_size_t, [c_int, c_int64, c_int64]),
     "sg_topk_gate_f32": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
     "sg_topk_gate_f64": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
     "sg_gate_update": (c_int, [_P, c_int, _P, _P, _P, _P]),
+    "sg_topk_segments_f32": (c_int, [c_int, c_int64, c_int64]),
+    "sg_topk_phases_f32": (c_int, [c_int, c_int64, c_int64, _P, c_size_t, _P, c_int64, _P]),
     "sg_topk_stats_f32": (c_int, [c_int, c_int64, c_int64, _P, c_size_t, _P, _P]),
     "sg_topk_stats_f64": (c_int, [c_int, c_int64, c_int64, _P, c_size_t, _P, _P]),
     "sg_aggregate_workspace_bytes": (c_size_t, [c_int, c_int64]),
@@ -94,7 +97,7 @@ SIGNATURES = {
     ),
     "sg_peer_allgather_sgd_f32": (
         c_int,
-        [c_int, POINTER(c_void_p), _P, c_int, c_int64, _P, _P, _P, c_double, c_double, c_double, c_int, _P],
+        [c_int, POINTER(c_void_p), c_int, _P, c_int, c_int64, _P, _P, _P, c_double, c_double, c_double, c_int, _P],
     ),
     "sg_sgd_momentum_f32": (c_int, [_P, _P, _P, c_int64, c_double, c_double, c_double, c_int, _P]),
     "sg_sgd_momentum_f64": (c_int, [_P, _P, _P, c_int64, c_double, c_double, c_double, c_int, _P]),

@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libscadles_b200.so"
-SOURCES = ["capi.cu", "topk.cu", "aggregate.cu", "gather.cu"]
+SOURCES = ["capi.cu", "topk.cu", "topk_fused.cu", "aggregate.cu", "gather.cu"]
 HEADERS = ["common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

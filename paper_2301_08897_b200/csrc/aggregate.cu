@@ -1571,25 +1571,45 @@ k_peer_reduce_slice(PeerRows src, int P, int unit_w, long long lo, long long hi,
 }
 
 __global__ void __launch_bounds__(256)
-k_peer_allgather_sgd(PeerRows src, int P, long long L, const uint8_t* __restrict__ guard, int gn, long long dim,
-                     float* __restrict__ out, float* __restrict__ p, float* __restrict__ b, double lr, double mu,
-                     double wd, int first) {
+k_peer_allgather_sgd(PeerRows src, int P, int rank, long long L, const uint8_t* __restrict__ guard, int gn,
+                     long long dim, float* __restrict__ out, float* __restrict__ p, float* __restrict__ b, double lr,
+                     double mu, double wd, int first) {
     pdl_enter();
     if (!peer_guard_run(guard, gn)) return;
     const long long n4 = dim / 4, stride = (long long)gridDim.x * blockDim.x;
     const long long L4 = L / 4;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-        const int q = (int)(i / L4);
-        const float4 gv = __ldcv(reinterpret_cast<const float4*>(src.p[q]) + i);
-        const float4 pv = reinterpret_cast<const float4*>(p)[i];
-        const float4 bv = first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(b)[i];
-        double g[4] = {gv.x, gv.y, gv.z, gv.w};
-        double pd[4] = {pv.x, pv.y, pv.z, pv.w}, bd[4] = {bv.x, bv.y, bv.z, bv.w};
+    // rank r walks the slices starting at slice r + 1: at any moment the P ranks pull from P
+    // different owners, so every GPU's NVLink egress serves one reader instead of all of them
+    long long start = ((long long)(rank + 1) % P) * L4;
+    if (start >= n4) start = 0;
+    constexpr int U = 2;  // independent float4 groups per thread in flight
+    for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < n4; j0 += stride * U) {
+        float4 gv[U], pv[U], bv[U];
+        long long ii[U];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) sgd_elem(g[c], pd[c], bd[c], lr, mu, wd, first != 0);
-        reinterpret_cast<float4*>(p)[i] = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
-        reinterpret_cast<float4*>(b)[i] = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
-        if (out) reinterpret_cast<float4*>(out)[i] = gv;
+        for (int u = 0; u < U; ++u) {
+            const long long j = j0 + u * stride;
+            long long i = j + start;
+            if (i >= n4) i -= n4;
+            ii[u] = j < n4 ? i : -1;
+            if (j < n4) {
+                gv[u] = __ldcv(reinterpret_cast<const float4*>(src.p[(int)(i / L4)]) + i);
+                pv[u] = reinterpret_cast<const float4*>(p)[i];
+                bv[u] = first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(b)[i];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = ii[u];
+            if (i < 0) continue;
+            double g[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+            double pd[4] = {pv[u].x, pv[u].y, pv[u].z, pv[u].w}, bd[4] = {bv[u].x, bv[u].y, bv[u].z, bv[u].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sgd_elem(g[c], pd[c], bd[c], lr, mu, wd, first != 0);
+            reinterpret_cast<float4*>(p)[i] = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
+            reinterpret_cast<float4*>(b)[i] = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
+            if (out) reinterpret_cast<float4*>(out)[i] = gv[u];
+        }
     }
     for (long long qd = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; qd < dim; qd += stride) {
         const int q = (int)(qd / L);
@@ -1718,10 +1738,11 @@ int sg_peer_reduce_slice_f32(int nranks, const float* const* src, const double* 
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
-int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, const uint8_t* guard, int guard_n, int64_t dim,
-                              float* out, float* params, float* momentum_buf, double lr, double momentum,
+int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, int rank, const uint8_t* guard, int guard_n,
+                              int64_t dim, float* out, float* params, float* momentum_buf, double lr, double momentum,
                               double weight_decay, int first_step, void* stream) {
     if (nranks < 1 || nranks > MAX_PEERS || !src || dim < 1 || !params || !momentum_buf || guard_n < 0 ||
+        rank < 0 || rank >= nranks ||
         guard_n > MAX_WORKERS || (guard_n > 0 && !guard))
         return SG_ERR_INVALID;
     if (dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
@@ -1733,8 +1754,9 @@ int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, const uint8_t
     if (reinterpret_cast<size_t>(params) % 16 || reinterpret_cast<size_t>(momentum_buf) % 16 ||
         (out && reinterpret_cast<size_t>(out) % 16))
         return SG_ERR_UNSUPPORTED;
-    launch_pdl(k_peer_allgather_sgd, dim3((unsigned)peer_blocks(dim / 4)), dim3(256), 0, (cudaStream_t)stream, r,
-               nranks, (long long)peer_slice_len(dim, nranks), guard_n > 0 ? guard : nullptr, guard_n, (long long)dim,
+    launch_pdl(k_peer_allgather_sgd, dim3((unsigned)peer_blocks(dim / 4 / 2 + 1)), dim3(256), 0, (cudaStream_t)stream,
+               r, nranks, rank, (long long)peer_slice_len(dim, nranks), guard_n > 0 ? guard : nullptr, guard_n,
+               (long long)dim,
                out, params, momentum_buf, lr, momentum, weight_decay, first_step);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }

@@ -1970,6 +1970,24 @@ int topk_stats(int k, long long dim, long long m, const void* ws, size_t ws_byte
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 
+// The float32 path is the persistent fused kernel (topk_fused.cu).
+int topk_fused_f32(const float* g, int k, long long ld, long long dim, long long m, uint32_t* idx, float* val,
+                   double* norms2, sg_gate_state* states, uint8_t* decision, double* rho, int* tile_off, void* ws,
+                   size_t ws_bytes, int nseg_target, cudaStream_t stream);
+size_t topk_fused_workspace_bytes(int k, long long dim, long long m, int nseg_target);
+size_t topk_fused_zero_bytes(int k, long long dim, long long m, int nseg_target);
+int topk_fused_ctas_per_sm();
+int topk_fused_stats(int k, long long dim, long long m, int nseg_target, const void* ws, size_t ws_bytes,
+                     int64_t* out, cudaStream_t stream);
+int topk_fused_segments(int k, long long dim, long long m, int nseg_target);
+int topk_fused_phases(int k, long long dim, long long m, int nseg_target, const void* ws, size_t ws_bytes,
+                      unsigned long long* out, long long out_len, cudaStream_t stream);
+
+inline int fused_segments(int k) {
+    const int s = num_sms() * topk_fused_ctas_per_sm() / k;
+    return s < 1 ? 1 : s;
+}
+
 }  // namespace sg
 
 using namespace sg;
@@ -1978,7 +1996,12 @@ extern "C" {
 
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m) {
     if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
-    return make_plan<float>(k, dim, m, segments_per_worker<float>(k), (long long)num_sms() * CW_PER_SM).total;
+    return topk_fused_workspace_bytes(k, dim, m, fused_segments(k));
+}
+
+size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m) {
+    if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
+    return topk_fused_zero_bytes(k, dim, m, fused_segments(k));
 }
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m) {
     if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
@@ -1989,8 +2012,10 @@ int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m, 
                      float* val, double* norms2, sg_gate_state* states, uint8_t* decision,
                      double* rho, int32_t* tile_off, void* workspace, size_t workspace_bytes,
                      void* stream) {
-    return topk_gate<float>(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, tile_off,
-                            workspace, workspace_bytes, (cudaStream_t)stream);
+    if (!g || !idx || !val || !norms2 || k < 1 || dim < 1 || m < 1 || m > dim || ld < dim) return SG_ERR_INVALID;
+    if (k > MAX_WORKERS || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
+    return topk_fused_f32(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, tile_off, workspace,
+                          workspace_bytes, fused_segments(k), (cudaStream_t)stream);
 }
 int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m, uint32_t* idx,
                      double* val, double* norms2, sg_gate_state* states, uint8_t* decision,
@@ -2001,8 +2026,21 @@ int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m,
 
 int sg_topk_stats_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes, int64_t* out,
                       void* stream) {
-    return topk_stats<float>(k, dim, m, workspace, workspace_bytes, out, (cudaStream_t)stream);
+    if (!workspace || !out || k < 1 || dim < 1 || m < 1 || m > dim) return SG_ERR_INVALID;
+    return topk_fused_stats(k, dim, m, fused_segments(k), workspace, workspace_bytes, out, (cudaStream_t)stream);
 }
+int sg_topk_segments_f32(int k, int64_t dim, int64_t m) {
+    if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return -1;
+    return topk_fused_segments(k, dim, m, fused_segments(k));
+}
+
+int sg_topk_phases_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes, uint64_t* out,
+                       int64_t out_len, void* stream) {
+    if (!workspace || !out || k < 1 || dim < 1 || m < 1 || m > dim || out_len < 0) return SG_ERR_INVALID;
+    return topk_fused_phases(k, dim, m, fused_segments(k), workspace, workspace_bytes,
+                             reinterpret_cast<unsigned long long*>(out), out_len, (cudaStream_t)stream);
+}
+
 int sg_topk_stats_f64(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes, int64_t* out,
                       void* stream) {
     return topk_stats<double>(k, dim, m, workspace, workspace_bytes, out, (cudaStream_t)stream);

@@ -1,0 +1,1359 @@
+// Float32 Top-k + squared norms + adaptive gate as ONE persistent kernel (items 3 and 4).
+//
+// Replaces reference pkg/src/streamsgd/comm.py:90-96 (topk_sparsify: np.lexsort on -|g| with
+// the index as tie-break, kept indices re-sorted ascending) and comm.py:129-160
+// (compression_gate) for the k workers of one GPU: one cooperative launch, grid (nseg, k),
+// every CTA resident (3 per SM), the phases separated by per-worker device barriers instead
+// of kernel boundaries.  Per CTA (worker w, segment s = a contiguous range of 16 KB tiles):
+//
+//   S  sample   the first tiles of the segment already stream into the TMA ring while the
+//               CTA reads its share of worker w's stratified sample (131072 keys in
+//               32-element chunks, one per stratum); two radix rounds over the sample (key
+//               bits [30:19], then [18:8]) give `est`, at or below the r_est-th largest
+//               sample key, r_est = q*S + 4 sigma: count(key >= est) >= m except with
+//               probability ~3e-5, and C = count(key >= est) is ~1.03 m (cr 0.1) to ~1.35 m
+//               (cr 0.001).  (D <= S: the sample is the whole row, r_est = m.)
+//   M  main     THE single read of the bucket: TMA ring (cp.async.bulk, 3 x 16 KB stages,
+//               L2 evict-first), fp64 sum of squares, branch-free candidate mask, one block
+//               scan per tile; candidates (index, value) go in index order into pool chunks of
+//               8192 entries reserved with one atomic each (the next chunk is reserved one
+//               switch ahead, so its latency is off the critical path); a 4096-bin histogram
+//               of candidate keys over [est, sample max] stays in shared memory.
+//   B  bin      every CTA reads the worker's merged histogram, finds the bin b* holding rank
+//               m, takes its own count above b* from its own histogram and appends its
+//               boundary entries (key in b*) to the worker's boundary list.
+//   R  resolve  the worker's leader CTA (s = 0) radix-selects T (the m-th largest key) and
+//               the tie cut (the `need` lowest indices among key == T are kept, as
+//               np.lexsort) from the boundary list -- in shared memory when it fits -- and
+//               releases a flag.
+//   W  write    kept count -> decoupled look-back over the worker's segments -> ordered
+//               compaction of the kept candidates (coalesced idx / val stores), the merge
+//               tile offsets, the fp64 sum of kept squares.
+//   G  gate     the last CTA reduces the norms in a fixed order and applies the gate in IEEE
+//               round-to-nearest (comm.py:143-159), then leaves the scratch zeroed.
+//
+// Exact fallback ("slow mode", uniform per worker, rare): fewer than m keys reached est, the
+// candidate pool (~2m) overflowed, or the boundary bin exceeds its list (massive ties): the
+// worker's CTAs run an exact radix select over the full data (3 histogram passes, a count
+// pass, an ordered write pass).  Both modes produce identical results.
+#include "common.cuh"
+
+namespace sg {
+namespace fz {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int TILE = 4096;        // elements per tile (= the merge tile)
+constexpr int TSHIFT = 12;
+constexpr int STAGES = 3;
+constexpr int HB = 4096;          // candidate histogram bins
+constexpr int HB_BITS = 12;
+constexpr int RB = 2048;          // radix bins of the resolve / slow rounds
+constexpr int RB_BITS = 11;
+constexpr int SAMPLE = 131072;    // sample keys per worker
+constexpr int CHUNK = 32;         // sample chunk (one warp load)
+constexpr int PCH = 8192;         // pool chunk (entries; >= 2 tiles of candidates)
+constexpr int RES = 6144;         // boundary entries resolved in shared memory
+constexpr int MAXSEG = 1024;
+constexpr int NPH = 8;            // phase timestamps per CTA (diagnostics)
+constexpr size_t RING_BYTES = (size_t)STAGES * TILE * sizeof(float);  // 48 KB dynamic smem
+static_assert(PCH >= 2 * TILE, "a chunk switch cannot happen on two consecutive tiles");
+static_assert(2 * RES * 4 <= (int)RING_BYTES, "the resolve buffers live in the ring");
+static_assert(MAXSEG <= HB, "the leader counts kept boundary entries per segment in shared memory");
+
+enum { M_FAST = 0, M_SLOW = 1 };
+
+struct Sel {  // per-worker selection result (written by the leader, read by every CTA)
+    unsigned T, cut, mode, pad;
+    unsigned long long h;  // boundary entries
+};
+
+struct Plan {
+    int k, nseg, tps, maxch;
+    long long dim, m, ntiles, s_eff, nch_s, r_est, cap, bcap;
+    size_t o_bar, o_flag, o_poolctr, o_count, o_bndn, o_ovf, o_smax, o_done, o_histA, o_histB, o_hist0, o_hist1,
+        o_histR, zero_end;
+    size_t o_sel, o_pmain, o_pwrite, o_chunks, o_nch, o_cgt, o_ceq, o_abv, o_base, o_bkey, o_bidx, o_bseg, o_cidx,
+        o_cval, o_stats, o_times, total;
+};
+
+inline Plan make_plan(int k, long long dim, long long m, int nseg_target) {
+    Plan p{};
+    p.k = k;
+    p.dim = dim;
+    p.m = m;
+    p.ntiles = (dim + TILE - 1) / TILE;
+    long long segs = nseg_target < 1 ? 1 : nseg_target;
+    if (segs > MAXSEG) segs = MAXSEG;
+    if (segs > p.ntiles) segs = p.ntiles;
+    p.tps = (int)((p.ntiles + segs - 1) / segs);
+    p.nseg = (int)((p.ntiles + p.tps - 1) / p.tps);
+    if (dim <= SAMPLE) {  // the whole row is the sample: est is the m-th largest key's bin edge
+        p.s_eff = dim;
+        p.nch_s = 0;
+        p.r_est = m;
+    } else {
+        p.nch_s = SAMPLE / CHUNK;
+        p.s_eff = p.nch_s * CHUNK;
+        const double q = (double)m / (double)dim;
+        const double mean = q * (double)p.s_eff;
+        const double sd = __builtin_sqrt(mean * (1.0 - q) + 1.0);
+        p.r_est = (long long)(mean + 4.0 * sd + 4.0) + 1;
+    }
+    // pool: ~2m candidates plus the chunk slack of every CTA (<= 2 partly used chunks each)
+    long long c = 2 * m + 4096;
+    if (c > dim) c = dim;
+    p.cap = align_up((size_t)(c + 2LL * PCH * p.nseg), 256);
+    p.bcap = p.cap / 4 > RES ? p.cap / 4 : RES;
+    p.maxch = p.tps + 3;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+    // -- zero-initialised state (every call leaves it zeroed) --
+    p.o_bar = take(sizeof(unsigned) * k);
+    p.o_flag = take(sizeof(unsigned) * k);
+    p.o_poolctr = take(sizeof(unsigned long long) * k);
+    p.o_count = take(sizeof(unsigned long long) * k);
+    p.o_bndn = take(sizeof(unsigned long long) * k);
+    p.o_ovf = take(sizeof(unsigned) * k);
+    p.o_smax = take(sizeof(unsigned) * k);
+    p.o_done = take(sizeof(unsigned) * 4);
+    p.o_histA = take(sizeof(unsigned) * (size_t)k * HB);
+    p.o_histB = take(sizeof(unsigned) * (size_t)k * RB);
+    p.o_hist0 = take(sizeof(unsigned) * (size_t)k * HB);
+    p.o_hist1 = take(sizeof(unsigned) * (size_t)k * RB);
+    p.o_histR = take(sizeof(unsigned) * (size_t)k * 3 * RB);
+    p.zero_end = o;
+    // -- scratch (no initial state) --
+    p.o_sel = take(sizeof(Sel) * k);
+    p.o_pmain = take(sizeof(double) * (size_t)k * p.nseg);
+    p.o_pwrite = take(sizeof(double) * (size_t)k * p.nseg);
+    p.o_chunks = take(sizeof(uint2) * (size_t)k * p.nseg * p.maxch);
+    p.o_nch = take(sizeof(unsigned) * (size_t)k * p.nseg);
+    p.o_cgt = take(sizeof(unsigned) * (size_t)k * p.nseg);
+    p.o_ceq = take(sizeof(unsigned) * (size_t)k * p.nseg);
+    p.o_abv = take(sizeof(unsigned long long) * (size_t)k * p.nseg);
+    p.o_base = take(sizeof(unsigned) * (size_t)k * p.nseg);
+    p.o_bkey = take(sizeof(unsigned) * (size_t)k * p.bcap);
+    p.o_bidx = take(sizeof(unsigned) * (size_t)k * p.bcap);
+    p.o_bseg = take(sizeof(unsigned short) * (size_t)k * p.bcap);
+    p.o_cidx = take(sizeof(uint32_t) * (size_t)k * (p.cap + PCH));
+    p.o_cval = take(sizeof(float) * (size_t)k * (p.cap + PCH));
+    p.o_stats = take(sizeof(long long) * 4 * (size_t)k);
+    p.o_times = take(sizeof(unsigned long long) * NPH * (size_t)k * p.nseg);
+    p.total = o + 256;
+    return p;
+}
+
+struct Args {
+    const float* g;
+    long long ld, dim, m, ntiles, nch_s, r_est, cap, bcap;
+    int k, nseg, tps, maxch, vec;
+    unsigned* bar;
+    unsigned* flag;
+    unsigned long long* poolctr;
+    unsigned long long* count;
+    unsigned long long* bndn;
+    unsigned* ovf;
+    unsigned* smax;
+    unsigned* done;
+    unsigned* histA;
+    unsigned* histB;
+    unsigned* hist0;
+    unsigned* hist1;
+    unsigned* histR;
+    Sel* sel;
+    double* pmain;
+    double* pwrite;
+    uint2* chunks;
+    unsigned* nch;
+    unsigned* cgt;
+    unsigned* ceq;
+    unsigned long long* abv;
+    unsigned* base;
+    unsigned* bkey;
+    unsigned* bidx;
+    unsigned short* bseg;
+    uint32_t* cidx;
+    float* cval;
+    long long* stats;
+    unsigned long long* times;
+    uint32_t* idx;
+    float* val;
+    int* tile_off;
+    double* norms2;
+    sg_gate_state* states;
+    uint8_t* decision;
+    double* rho;
+};
+
+using KO = KeyOf<float>;
+
+SG_DEV unsigned long long mix64f(unsigned long long x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+SG_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+SG_DEV void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Per-worker device barrier: the worker's nseg CTAs are co-resident (cooperative launch).
+// Barrier j of a call waits for the counter to reach j * nseg.
+SG_DEV void worker_barrier(unsigned* ctr, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        while (ld_acquire_gpu(ctr) < target) __nanosleep(32);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+struct Smem {
+    unsigned hist[HB];  // this CTA's histogram (sample rounds, then candidates, then radix bins)
+    unsigned long long full[STAGES];
+    unsigned wt[NW];
+    unsigned wl[NW];
+    unsigned long long bsum[NW];
+    double red[NW];
+    unsigned next_base, cur_base;
+    int bin;
+    unsigned long long above, total;
+    unsigned long long scal[4];
+    unsigned u[4];
+    int last;
+};
+
+// Block-wide: the bin of an NB-bin histogram holding the rank-th largest, scanning from the
+// top (thread t owns bins NB-1-PER*t-i).  bin = -1 if the total is below rank.
+template <int NB>
+SG_DEV void find_bin_top(const unsigned* hist, unsigned long long rank, Smem& S, int& bin,
+                         unsigned long long& above, unsigned long long& total) {
+    constexpr int PER = NB / NT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int top = NB - 1 - PER * tid;
+    unsigned long long s = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) s += hist[top - i];
+    unsigned long long incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) S.bsum[warp] = incl;
+    if (tid == 0) S.bin = -1;
+    __syncthreads();
+    unsigned long long wb = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        wb += i < warp ? S.bsum[i] : 0ull;
+        tot += S.bsum[i];
+    }
+    incl += wb;
+    const unsigned long long ex = incl - s;
+    if (ex < rank && incl >= rank) {  // exactly one thread holds the rank
+        unsigned long long cum = ex;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const unsigned h = hist[top - i];
+            if (cum + h >= rank) {
+                S.bin = top - i;
+                S.above = cum;
+                break;
+            }
+            cum += h;
+        }
+    }
+    __syncthreads();
+    bin = S.bin;
+    above = bin >= 0 ? S.above : 0ull;
+    total = tot;
+    __syncthreads();
+}
+
+SG_DEV int digit_shift_u32(unsigned span, int bits) {
+    const int bl = span ? 32 - __clz((int)span) : 0;
+    return bl > bits ? bl - bits : 0;
+}
+
+// Bin of key in [lo, lo + span] with shift `sh` and an open top bin.
+SG_DEV unsigned hbin(unsigned key, unsigned lo, int sh, unsigned nb) {
+    const unsigned d = (key - lo) >> sh;
+    return d >= nb - 1 ? nb - 1 : d;
+}
+
+// Radix-select window over keys [lo, lo + span] (span == 0: the key is lo).
+struct Win {
+    unsigned lo, span;
+    int shift;
+    unsigned long long rank;  // 1-based from the top inside the window
+};
+
+SG_DEV void win_narrow(Win& s, int bin, unsigned long long above, unsigned nb, int next_bits) {
+    const unsigned off = (unsigned)bin << s.shift;
+    s.rank -= above;
+    const unsigned lo = s.lo + off;
+    const unsigned rest = s.span - off;
+    unsigned span = rest;
+    if ((unsigned)bin != nb - 1) {
+        const unsigned width = (1u << s.shift) - 1u;
+        span = rest < width ? rest : width;
+    }
+    s.lo = lo;
+    s.span = span;
+    s.shift = digit_shift_u32(span, next_bits);
+}
+
+// Block-cooperative exact select over n (key, idx) entries (shared or global memory): T = the
+// wn.rank-th largest key in window wn, cut = the need-th smallest index among key == T with
+// need = the rank left inside T's class (0xffffffff when every tie is kept).  `hist` holds RB
+// bins.  Results are uniform over the block.
+SG_DEV void select_entries(const unsigned* keys, const unsigned* ids, long long n, Win wn, unsigned* hist, Smem& S,
+                           unsigned& T_out, unsigned& cut_out) {
+    const int tid = threadIdx.x;
+    for (int round = 0; round < 4 && wn.span != 0; ++round) {
+        for (int i = tid; i < RB; i += NT) hist[i] = 0;
+        __syncthreads();
+        for (long long i = tid; i < n; i += NT) {
+            const unsigned key = keys[i];
+            if (key >= wn.lo && key - wn.lo <= wn.span) atomicAdd(&hist[hbin(key, wn.lo, wn.shift, RB)], 1u);
+        }
+        __syncthreads();
+        int bin;
+        unsigned long long above, tot;
+        find_bin_top<RB>(hist, wn.rank, S, bin, above, tot);
+        if (bin < 0) wn.span = 0;  // inconsistent counts (cannot happen): keep the window's lowest key
+        else win_narrow(wn, bin, above, RB, RB_BITS);
+    }
+    const unsigned T = wn.lo;
+    const unsigned long long need = wn.rank;
+    // ties at T: the need-th smallest index = the (eq - need + 1)-th largest index among them
+    unsigned c = 0;
+    for (long long i = tid; i < n; i += NT) c += keys[i] == T;
+    c = __reduce_add_sync(FULL, c);
+    if (tid == 0) S.u[0] = 0;
+    __syncthreads();
+    if ((tid & 31) == 0) atomicAdd(&S.u[0], c);
+    __syncthreads();
+    const unsigned long long eq = S.u[0];
+    unsigned cut = 0xffffffffu;
+    if (eq > need) {
+        Win iw;
+        iw.lo = 0;
+        iw.span = 0xffffffffu;
+        iw.shift = digit_shift_u32(0xffffffffu, RB_BITS);
+        iw.rank = eq - need + 1;
+        for (int round = 0; round < 4 && iw.span != 0; ++round) {
+            for (int i = tid; i < RB; i += NT) hist[i] = 0;
+            __syncthreads();
+            for (long long i = tid; i < n; i += NT) {
+                if (keys[i] != T) continue;
+                const unsigned x = ids[i];
+                if (x >= iw.lo && x - iw.lo <= iw.span) atomicAdd(&hist[hbin(x, iw.lo, iw.shift, RB)], 1u);
+            }
+            __syncthreads();
+            int bin;
+            unsigned long long above, tot;
+            find_bin_top<RB>(hist, iw.rank, S, bin, above, tot);
+            if (bin < 0) iw.span = 0;
+            else win_narrow(iw, bin, above, RB, RB_BITS);
+        }
+        cut = iw.lo;
+    }
+    T_out = T;
+    cut_out = cut;
+}
+
+// Block exclusive scan of per-thread counts; returns the block total.
+SG_DEV unsigned block_scan(unsigned cnt, Smem& S, unsigned& excl) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) S.wt[warp] = incl;
+    __syncthreads();
+    unsigned wb = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        const unsigned t = S.wt[i];
+        wb += i < warp ? t : 0u;
+        tot += t;
+    }
+    excl = wb + incl - cnt;
+    __syncthreads();
+    return tot;
+}
+
+SG_DEV unsigned long long block_sum_u64(unsigned long long v, Smem& S) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    v = warp_sum_u64(v);
+    if (lane == 0) S.bsum[warp] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) t += S.bsum[i];
+    __syncthreads();
+    return t;
+}
+
+// Fixed-order block sum (every thread gets the same bits).
+SG_DEV double block_sum_fixed(double v, Smem& S) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    v = warp_sum(v);
+    if (lane == 0) S.red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) t = dadd(t, S.red[i]);
+    __syncthreads();
+    return t;
+}
+
+// Visit this CTA's candidates in index order, EPT consecutive per thread per block of
+// NT * EPT: f(x[EPT], xi[EPT], nvalid, block entries) is called by every thread for every
+// block (block-uniform control flow).
+template <int EPT, typename F>
+SG_DEV void for_candidates(const Args& a, int w, int seg, F&& f) {
+    const int tid = threadIdx.x;
+    constexpr int SPAN = NT * EPT;
+    const uint32_t* ci = a.cidx + (long long)w * (a.cap + PCH);
+    const float* cv = a.cval + (long long)w * (a.cap + PCH);
+    const uint2* ch = a.chunks + ((long long)w * a.nseg + seg) * a.maxch;
+    const unsigned nch = a.nch[(long long)w * a.nseg + seg];
+    for (unsigned c = 0; c < nch; ++c) {
+        const uint2 cr = ch[c];
+        const unsigned cb = cr.x, cn = cr.y;
+        for (unsigned b0 = 0; b0 < cn; b0 += SPAN) {
+            const unsigned e0 = b0 + tid * EPT;
+            float x[EPT];
+            uint32_t xi[EPT];
+            if (e0 + EPT <= cn) {  // chunk bases and e0 are 4-aligned
+#pragma unroll
+                for (int r = 0; r < EPT / 4; ++r) {
+                    const float4 v4 = __ldcg(reinterpret_cast<const float4*>(cv + cb + e0) + r);
+                    const uint4 i4 = __ldcg(reinterpret_cast<const uint4*>(ci + cb + e0) + r);
+                    x[4 * r] = v4.x; x[4 * r + 1] = v4.y; x[4 * r + 2] = v4.z; x[4 * r + 3] = v4.w;
+                    xi[4 * r] = i4.x; xi[4 * r + 1] = i4.y; xi[4 * r + 2] = i4.z; xi[4 * r + 3] = i4.w;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < EPT; ++u) {
+                    const bool ok = e0 + u < cn;
+                    x[u] = ok ? __ldcg(cv + cb + e0 + u) : 0.f;
+                    xi[u] = ok ? __ldcg(ci + cb + e0 + u) : 0u;
+                }
+            }
+            const int nv = e0 >= cn ? 0 : (int)(cn - e0 < (unsigned)EPT ? cn - e0 : EPT);
+            f(x, xi, nv, cn - b0 < (unsigned)SPAN ? cn - b0 : (unsigned)SPAN);
+        }
+    }
+}
+
+// Ordered compaction of this CTA's kept candidates at out_base, merge tile offsets, and the
+// fp64 sum of kept squares (fast mode).
+SG_DEV double write_kept(const Args& a, Smem& S, unsigned char* stage, int w, int seg, unsigned T, unsigned cut,
+                         unsigned out_base, long long t0, int nt) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int EPT = 8;
+    uint32_t* oi = a.idx + (long long)w * a.m;
+    float* ov = a.val + (long long)w * a.m;
+    int* toff = a.tile_off ? a.tile_off + (long long)w * (a.ntiles + 1) : nullptr;
+    float* st_v = reinterpret_cast<float*>(stage);
+    uint32_t* st_i = reinterpret_cast<uint32_t*>(st_v + NT * EPT);
+    unsigned g32 = out_base;
+    int tp = (int)t0 - 1;  // tile of the previous candidate (block-uniform)
+    double ss = 0.0;
+    for_candidates<EPT>(a, w, seg, [&](const float (&x)[EPT], const uint32_t (&xi)[EPT], int nv, unsigned) {
+        unsigned kf = 0;
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const unsigned key = KO::key(x[u]);
+            kf |= (u < nv && (key > T || (key == T && xi[u] <= cut)) ? 1u : 0u) << u;
+        }
+        // the warp's last candidate index (entries are contiguous, so a warp without entries
+        // is followed only by warps without entries)
+        const uint32_t mylast = nv > 0 ? xi[nv - 1] : 0u;
+        const unsigned hm = __ballot_sync(FULL, nv > 0);
+        const uint32_t left = __shfl_up_sync(FULL, mylast, 1);
+        if (hm && lane == 31 - __clz((int)hm)) S.wl[warp] = mylast;
+        if (!hm && lane == 0) S.wl[warp] = 0xffffffffu;
+        unsigned excl;
+        const unsigned tot = block_scan(__popc(kf), S, excl);
+        const unsigned pos = g32 + excl;
+        if (toff && nv > 0) {
+            // tiles (tile(previous candidate), tile(this candidate)] start at this candidate
+            const int prev_t = lane > 0 ? (int)(left >> TSHIFT) : (warp > 0 ? (int)(S.wl[warp - 1] >> TSHIFT) : tp);
+            if ((int)(xi[nv - 1] >> TSHIFT) != prev_t) {
+                int tq = prev_t;
+#pragma unroll
+                for (int u = 0; u < EPT; ++u) {
+                    if (u >= nv) break;
+                    const int tc = (int)(xi[u] >> TSHIFT);
+                    for (int t = tq + 1; t <= tc; ++t) toff[t] = (int)(pos + __popc(kf & ((1u << u) - 1u)));
+                    tq = tc;
+                }
+            }
+        }
+        unsigned lp = excl, kk = kf;
+        while (kk) {
+            const int u = __ffs(kk) - 1;
+            kk &= kk - 1;
+            st_i[lp] = xi[u];
+            st_v[lp] = x[u];
+            ++lp;
+        }
+        int ntp = tp;
+#pragma unroll
+        for (int q = NW - 1; q >= 0; --q) {
+            if (S.wl[q] != 0xffffffffu) {
+                ntp = (int)(S.wl[q] >> TSHIFT);
+                break;
+            }
+        }
+        __syncthreads();
+        for (unsigned q = tid; q < tot; q += NT) {
+            const float y = st_v[q];
+            oi[g32 + q] = st_i[q];
+            ov[g32 + q] = y;
+            ss = fma((double)y, (double)y, ss);
+        }
+        g32 += tot;
+        tp = ntp;
+        __syncthreads();
+    });
+    if (toff) {
+        for (int t = tp + 1 + tid; t < (int)(t0 + nt); t += NT) toff[t] = (int)g32;
+        if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
+    }
+    return ss;
+}
+
+// Streams this CTA's segment with direct loads: f(tile, base, v[16]) per thread, thread t
+// holding elements [base, base + 16) of each tile (base = tile*TILE + 16t).
+template <typename F>
+SG_DEV void stream_segment(const Args& a, const float* row, long long t_begin, long long t_end, F&& f) {
+    const int tid = threadIdx.x;
+    for (long long t = t_begin; t < t_end; ++t) {
+        const long long base = t * TILE + (long long)tid * 16;
+        float v[16];
+        if (a.vec && base + 16 <= a.dim) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float4 x = ld_stream(reinterpret_cast<const float4*>(row + base) + r);
+                v[4 * r] = x.x; v[4 * r + 1] = x.y; v[4 * r + 2] = x.z; v[4 * r + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int b = 0; b < 16; ++b) v[b] = base + b < a.dim ? row[base + b] : 0.f;
+        }
+        f(t, base, v);
+    }
+}
+
+// The exact multi-pass fallback over the full data (rare; identical results).
+SG_DEV double slow_mode(const Args& a, Smem& S, unsigned char* stage, int w, int seg, const float* row,
+                        long long t_begin, long long t_end, unsigned& epoch) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned nseg = (unsigned)a.nseg;
+    unsigned* bar = a.bar + w;
+    // 1. T: 3 radix rounds of 11 bits over the full key range
+    Win wn;
+    wn.lo = 0;
+    wn.span = KO::KMAX;
+    wn.shift = digit_shift_u32(KO::KMAX, RB_BITS);
+    wn.rank = (unsigned long long)a.m;
+    for (int round = 0; round < 3 && wn.span != 0; ++round) {
+        for (int i = tid; i < RB; i += NT) S.hist[i] = 0;
+        __syncthreads();
+        const unsigned lo = wn.lo, span = wn.span;
+        const int sh = wn.shift;
+        stream_segment(a, row, t_begin, t_end, [&](long long, long long base, const float (&v)[16]) {
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const unsigned key = KO::key(v[b]);
+                if (base + b < a.dim && key >= lo && key - lo <= span) atomicAdd(&S.hist[hbin(key, lo, sh, RB)], 1u);
+            }
+        });
+        __syncthreads();
+        unsigned* gh = a.histR + ((long long)w * 3 + round) * RB;
+        for (int i = tid; i < RB; i += NT)
+            if (S.hist[i]) atomicAdd(gh + i, S.hist[i]);
+        worker_barrier(bar, (++epoch) * nseg);
+        for (int i = tid; i < RB; i += NT) S.hist[i] = __ldcg(gh + i);
+        __syncthreads();
+        int bin;
+        unsigned long long above, tot;
+        find_bin_top<RB>(S.hist, wn.rank, S, bin, above, tot);
+        if (bin < 0) wn.span = 0;
+        else win_narrow(wn, bin, above, RB, RB_BITS);
+    }
+    const unsigned T = wn.lo;
+    // 2. per-segment counts of key > T and key == T
+    unsigned cg = 0, ce = 0;
+    stream_segment(a, row, t_begin, t_end, [&](long long, long long base, const float (&v)[16]) {
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const unsigned key = KO::key(v[b]);
+            const bool ok = base + b < a.dim;
+            cg += ok && key > T;
+            ce += ok && key == T;
+        }
+    });
+    const unsigned long long cgs = block_sum_u64(cg, S), ces = block_sum_u64(ce, S);
+    if (tid == 0) {
+        a.cgt[(long long)w * a.nseg + seg] = (unsigned)cgs;
+        a.ceq[(long long)w * a.nseg + seg] = (unsigned)ces;
+    }
+    worker_barrier(bar, (++epoch) * nseg);
+    if (tid == 0) {
+        unsigned long long gb = 0, eb = 0, gtot = 0;
+        for (int q = 0; q < a.nseg; ++q) {
+            const unsigned long long g_ = __ldcg(a.cgt + (long long)w * a.nseg + q);
+            const unsigned long long e_ = __ldcg(a.ceq + (long long)w * a.nseg + q);
+            if (q < seg) {
+                gb += g_;
+                eb += e_;
+            }
+            gtot += g_;
+        }
+        S.scal[0] = gb;
+        S.scal[1] = eb;
+        S.scal[2] = gtot;
+    }
+    __syncthreads();
+    const unsigned long long need = (unsigned long long)a.m - S.scal[2];  // ties kept (lowest indices)
+    const unsigned long long eqb = S.scal[1];
+    const unsigned long long quota = need > eqb ? need - eqb : 0ull;  // this segment's kept ties
+    unsigned g32 = (unsigned)(S.scal[0] + (eqb < need ? eqb : need));
+    unsigned eq_seen = 0;
+    // 3. ordered write pass
+    uint32_t* oi = a.idx + (long long)w * a.m;
+    float* ov = a.val + (long long)w * a.m;
+    int* toff = a.tile_off ? a.tile_off + (long long)w * (a.ntiles + 1) : nullptr;
+    float* st_v = reinterpret_cast<float*>(stage);
+    uint32_t* st_i = reinterpret_cast<uint32_t*>(st_v + TILE);
+    double ss = 0.0;
+    stream_segment(a, row, t_begin, t_end, [&](long long t, long long base, const float (&v)[16]) {
+        unsigned gtm = 0, eqm = 0;
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const bool ok = base + b < a.dim;
+            const unsigned key = KO::key(v[b]);
+            gtm |= (ok && key > T ? 1u : 0u) << b;
+            eqm |= (ok && key == T ? 1u : 0u) << b;
+        }
+        unsigned eexcl;
+        const unsigned etot = block_scan(__popc(eqm), S, eexcl);
+        unsigned er = eq_seen + eexcl;  // segment tie rank of this thread's first tie
+        unsigned keptm = gtm;
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            if ((eqm >> b) & 1u) {
+                if ((unsigned long long)er < quota) keptm |= 1u << b;
+                ++er;
+            }
+        }
+        unsigned excl;
+        const unsigned tot = block_scan(__popc(keptm), S, excl);
+        if (toff && tid == 0) toff[t] = (int)g32;
+        unsigned lp = excl, kk = keptm;
+        while (kk) {
+            const int b = __ffs(kk) - 1;
+            kk &= kk - 1;
+            st_i[lp] = (uint32_t)(base + b);
+            st_v[lp] = v[b];
+            ++lp;
+        }
+        __syncthreads();
+        for (unsigned q = tid; q < tot; q += NT) {
+            const float y = st_v[q];
+            oi[g32 + q] = st_i[q];
+            ov[g32 + q] = y;
+            ss = fma((double)y, (double)y, ss);
+        }
+        g32 += tot;
+        eq_seen += etot;
+        __syncthreads();
+    });
+    if (toff && tid == 0 && t_end == a.ntiles) toff[a.ntiles] = (int)a.m;
+    (void)lane;
+    (void)warp;
+    return ss;
+}
+
+SG_DEV void gate_math_f(sg_gate_state& s, double s_full, double s_topk, uint8_t& dec, double& rho) {
+    if (!s.initialized) {
+        s.ewma_full = s_full;
+        s.ewma_topk = s_topk;
+        s.initialized = 1;
+    } else {
+        const double f = s.ewma_factor;
+        const double one_m_f = dsub(1.0, f);
+        s.ewma_full = dadd(dmul(f, s.ewma_full), dmul(one_m_f, s_full));
+        s.ewma_topk = dadd(dmul(f, s.ewma_topk), dmul(one_m_f, s_topk));
+    }
+    const double full = s.raw_gate ? s_full : s.ewma_full;
+    const double kept = s.raw_gate ? s_topk : s.ewma_topk;
+    const double r = full == 0.0 ? 0.0 : ddiv(fabs(dsub(full, kept)), full);
+    const bool compressed = r <= s.delta;  // NaN compares false -> dense, as in numpy
+    if (compressed) s.n_compressed += 1;
+    else s.n_uncompressed += 1;
+    dec = compressed ? 1 : 0;
+    rho = r;
+}
+
+__global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
+    pdl_enter();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* ring = reinterpret_cast<float*>(smem_raw);
+    __shared__ Smem S;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = blockIdx.y, seg = blockIdx.x;
+    const unsigned nseg = (unsigned)a.nseg;
+    unsigned* bar = a.bar + w;
+    unsigned epoch = 0;
+    const float* row = a.g + (long long)w * a.ld;
+    const long long t_begin = (long long)seg * a.tps;
+    const long long t_end = t_begin + a.tps < a.ntiles ? t_begin + a.tps : a.ntiles;
+    const int ntl = (int)(t_end - t_begin);
+    // full tiles come through the TMA ring (aligned rows); the row's partial last tile, or
+    // every tile of an unaligned row, is read directly
+    const int nfull = !a.vec ? 0 : ((t_end * TILE <= a.dim) ? ntl : ntl - 1);
+    unsigned long long tm[5] = {0, 0, 0, 0, 0};  // phase timestamps (thread 0): start, est, main, flag, end
+    if (tid == 0) tm[0] = gtimer();
+    unsigned long long policy = 0;
+    auto issue = [&](int i) {
+        const int s = i % STAGES;
+        mbar_expect_tx(&S.full[s], TILE * 4);
+        bulk_g2s(ring + s * TILE, row + (t_begin + i) * TILE, TILE * 4, &S.full[s], policy);
+    };
+    if (tid == 0) {
+        policy = policy_evict_first();
+        for (int s = 0; s < STAGES; ++s) mbar_init(&S.full[s], 1);
+        fence_mbar_init();
+        for (int i = 0; i < STAGES && i < nfull; ++i) issue(i);
+    }
+    // ---------------- S: sample -> est --------------------------------------------------------
+    for (int i = tid; i < HB; i += NT) S.hist[i] = 0;
+    __syncthreads();
+    const bool exact = a.nch_s == 0;
+    auto for_sample = [&](auto&& f) {
+        if (exact) {  // the whole row, split evenly over the worker's CTAs
+            const long long L = (a.dim + a.nseg - 1) / a.nseg;
+            const long long lo = (long long)seg * L, hi = lo + L < a.dim ? lo + L : a.dim;
+            for (long long i = lo + tid; i < hi; i += NT) f(KO::key(row[i]));
+        } else {  // chunk c of stratum c at a hashed offset; warp-sized coalesced loads,
+                  // SB chunks per warp in flight
+            constexpr int SB = 8;
+            const long long stratum = a.dim / a.nch_s;
+            const long long step = (long long)a.nseg * NW;
+            for (long long c0 = (long long)seg * NW + warp; c0 < a.nch_s; c0 += step * SB) {
+                float v[SB];
+#pragma unroll
+                for (int u = 0; u < SB; ++u) {
+                    const long long c = c0 + u * step;
+                    v[u] = 0.f;
+                    if (c < a.nch_s) {
+                        const unsigned h = (unsigned)mix64f((unsigned long long)c * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
+                        const long long off = (long long)(((unsigned long long)h * (unsigned long long)(stratum - CHUNK + 1)) >> 32);
+                        v[u] = __ldg(row + c * stratum + off + lane);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < SB; ++u)
+                    if (c0 + u * step < a.nch_s) f(KO::key(v[u]));
+            }
+        }
+    };
+    unsigned kmx = 0;
+    for_sample([&](unsigned key) {
+        atomicAdd(&S.hist[key >> 19], 1u);
+        kmx = key > kmx ? key : kmx;
+    });
+    kmx = warp_max<unsigned>(kmx);
+    if (lane == 0 && kmx) atomicMax(a.smax + w, kmx);
+    __syncthreads();
+    unsigned* gA = a.histA + (long long)w * HB;
+    for (int i = tid; i < HB; i += NT)
+        if (S.hist[i]) atomicAdd(gA + i, S.hist[i]);
+    worker_barrier(bar, (++epoch) * nseg);
+    for (int i = tid; i < HB; i += NT) S.hist[i] = __ldcg(gA + i);
+    __syncthreads();
+    int binA;
+    unsigned long long aboveA, totA;
+    find_bin_top<HB>(S.hist, (unsigned long long)a.r_est, S, binA, aboveA, totA);
+    for (int i = tid; i < RB; i += NT) S.hist[i] = 0;
+    __syncthreads();
+    if (binA >= 0) {
+        for_sample([&](unsigned key) {
+            if ((int)(key >> 19) == binA) atomicAdd(&S.hist[(key >> 8) & (RB - 1)], 1u);
+        });
+    }
+    __syncthreads();
+    unsigned* gB = a.histB + (long long)w * RB;
+    for (int i = tid; i < RB; i += NT)
+        if (S.hist[i]) atomicAdd(gB + i, S.hist[i]);
+    worker_barrier(bar, (++epoch) * nseg);
+    unsigned est = 0;
+    if (binA >= 0) {
+        for (int i = tid; i < RB; i += NT) S.hist[i] = __ldcg(gB + i);
+        __syncthreads();
+        int binB;
+        unsigned long long aboveB, totB;
+        find_bin_top<RB>(S.hist, (unsigned long long)a.r_est - aboveA, S, binB, aboveB, totB);
+        est = ((unsigned)binA << 19) | (binB >= 0 ? ((unsigned)binB << 8) : 0u);
+    }
+    if (tid == 0) tm[1] = gtimer();
+    const unsigned smax = __ldcg(a.smax + w);
+    const int shift0 = digit_shift_u32(smax > est ? smax - est : 0u, HB_BITS);
+    const bool take_all = est == 0;
+    const float thr = take_all ? 0.f : __uint_as_float(est - 1u);  // key >= est <=> |x| >= thr
+    // ---------------- M: the main pass --------------------------------------------------------
+    for (int i = tid; i < HB; i += NT) S.hist[i] = 0;
+    uint32_t* ci = a.cidx + (long long)w * (a.cap + PCH);
+    float* cv = a.cval + (long long)w * (a.cap + PCH);
+    uint2* chl = a.chunks + ((long long)w * a.nseg + seg) * a.maxch;
+    const unsigned cap = (unsigned)a.cap;
+    if (tid == 0) {
+        const unsigned long long b0 = atomicAdd(a.poolctr + w, 2ull * PCH);
+        S.cur_base = (unsigned)(b0 < (unsigned long long)cap ? b0 : cap);
+        S.next_base = (unsigned)(b0 + PCH < (unsigned long long)cap ? b0 + PCH : cap);
+    }
+    __syncthreads();
+    unsigned cur = S.cur_base, nxt = S.next_base, fill = 0, nchunk = 0;
+    unsigned long long r0 = 0;  // thread 0: the pending chunk reservation
+    int pend = 0;               // 1: reserved this tile (published next tile), 2: published
+    double ss = 0.0, ss1 = 0.0;
+    unsigned run = 0;
+    const int rot = (lane >> 1) & 3;
+    int s = 0;
+    unsigned phase = 0;
+    for (int i = 0; i < ntl; ++i) {
+        if (pend == 2) {
+            nxt = S.next_base;
+            pend = 0;
+        } else if (pend == 1) {
+            if (tid == 0) S.next_base = (unsigned)(r0 < (unsigned long long)cap ? r0 : cap);
+            pend = 2;
+        }
+        const long long tile = t_begin + i;
+        const long long base = tile * TILE;
+        const float* src;
+        unsigned M = 0;
+        if (i < nfull) {
+            src = ring + s * TILE;
+            mbar_wait(&S.full[s], phase);
+            const float4* t4 = reinterpret_cast<const float4*>(src);
+            float4 y[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) y[r] = t4[tid * 4 + ((r + rot) & 3)];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float4 v = y[r];
+                double& sr = (r & 1) ? ss1 : ss;  // two chains: half the DFMA dependency depth
+                sr = fma((double)v.x, (double)v.x, sr);
+                sr = fma((double)v.y, (double)v.y, sr);
+                sr = fma((double)v.z, (double)v.z, sr);
+                sr = fma((double)v.w, (double)v.w, sr);
+                const unsigned m4 = (fabsf(v.x) >= thr ? 1u : 0u) | (fabsf(v.y) >= thr ? 2u : 0u) |
+                                    (fabsf(v.z) >= thr ? 4u : 0u) | (fabsf(v.w) >= thr ? 8u : 0u);
+                M |= m4 << (((r + rot) & 3) * 4);
+            }
+            if (take_all) M = 0xffffu;
+        } else {  // direct, bounds-checked
+            src = row + base;
+            const long long left = a.dim - base - tid * 16;
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                if (b < left) {
+                    const float x = src[tid * 16 + b];
+                    double& sr = (b & 1) ? ss1 : ss;
+                    sr = fma((double)x, (double)x, sr);
+                    if (take_all || fabsf(x) >= thr) M |= 1u << b;
+                }
+            }
+        }
+        // block scan of the tile's candidate counts
+        const unsigned n = __popc(M);
+        unsigned incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) S.wt[warp] = incl;
+        __syncthreads();
+        const unsigned wtv = lane < NW ? S.wt[lane] : 0u;
+        unsigned wi = wtv;
+#pragma unroll
+        for (int o = 1; o < NW; o <<= 1) {
+            const unsigned yv = __shfl_up_sync(FULL, wi, o);
+            if (lane >= o) wi += yv;
+        }
+        const unsigned woff = __shfl_sync(FULL, wi - wtv, warp);
+        const unsigned total = __shfl_sync(FULL, wi, NW - 1);
+        if (total) {
+            if (fill + total > (unsigned)PCH) {  // move to the pre-reserved chunk
+                if (tid == 0) {
+                    chl[nchunk] = make_uint2(cur, fill);
+                    r0 = atomicAdd(a.poolctr + w, (unsigned long long)PCH);
+                }
+                if (fill) ++nchunk;
+                cur = nxt;
+                fill = 0;
+                pend = 1;
+            }
+            const bool room = cur < cap;
+            if (!room && tid == 0) a.ovf[w] = 1u;
+            unsigned pos = cur + fill + woff + incl - n;
+            unsigned MM = M;
+            while (MM) {
+                const int b = __ffs(MM) - 1;
+                MM &= MM - 1;
+                const int off = tid * 16 + b;
+                const float val = src[off];
+                const unsigned key = KO::key(val);
+                atomicAdd(&S.hist[hbin(key, est, shift0, HB)], 1u);
+                if (room) {
+                    ci[pos] = (uint32_t)(base + off);
+                    cv[pos] = val;
+                }
+                ++pos;
+            }
+            fill += total;
+            run += total;
+        }
+        __syncthreads();  // the stage is consumed, S.wt reusable
+        if (i < nfull) {
+            if (tid == 0 && i + STAGES < nfull) {
+                fence_proxy_async();
+                issue(i + STAGES);
+            }
+            if (++s == STAGES) {
+                s = 0;
+                phase ^= 1u;
+            }
+        }
+    }
+    if (tid == 0) {
+        if (fill) chl[nchunk] = make_uint2(cur, fill);
+        a.nch[(long long)w * a.nseg + seg] = nchunk + (fill ? 1u : 0u);
+    }
+    {
+        const double t = block_sum_fixed(dadd(ss, ss1), S);
+        if (tid == 0) {
+            a.pmain[(long long)w * a.nseg + seg] = t;
+            if (run) atomicAdd(a.count + w, (unsigned long long)run);
+        }
+    }
+    unsigned* g0 = a.hist0 + (long long)w * HB;
+    for (int i = tid; i < HB; i += NT)
+        if (S.hist[i]) atomicAdd(g0 + i, S.hist[i]);
+    worker_barrier(bar, (++epoch) * nseg);
+    // ---------------- B / R / W ----------------------------------------------------------------
+    if (tid == 0) tm[2] = gtimer();
+    const bool leader = seg == 0;
+    if (leader) {  // every CTA is past its reads of the sample histograms
+        for (int i = tid; i < HB; i += NT) gA[i] = 0;
+        for (int i = tid; i < RB; i += NT) gB[i] = 0;
+    }
+    const unsigned long long C = __ldcg(a.count + w);
+    const bool ovf = __ldcg(a.ovf + w) != 0;
+    bool slow = C < (unsigned long long)a.m || ovf;
+    unsigned* gtmp = reinterpret_cast<unsigned*>(ring);  // the ring is free: merged histogram
+    int bstar = -1;
+    unsigned long long above = 0, hb = 0, tot0 = 0;
+    unsigned blo = 0, bspan = 0;
+    if (!slow) {
+        for (int i = tid; i < HB; i += NT) gtmp[i] = __ldcg(g0 + i);
+        __syncthreads();
+        find_bin_top<HB>(gtmp, (unsigned long long)a.m, S, bstar, above, tot0);
+        if (bstar < 0) {
+            slow = true;
+        } else {
+            hb = gtmp[bstar];
+            blo = est + ((unsigned)bstar << shift0);
+            bspan = bstar == HB - 1 ? KO::KMAX - blo : ((1u << shift0) - 1u);
+            if (hb > (unsigned long long)a.bcap || a.nseg > 65535) slow = true;
+        }
+    }
+    double ss_topk = 0.0;
+    if (!slow) {
+        unsigned* bk = a.bkey + (long long)w * a.bcap;
+        unsigned* bi = a.bidx + (long long)w * a.bcap;
+        unsigned short* bs = a.bseg + (long long)w * a.bcap;
+        unsigned* g1 = a.hist1 + (long long)w * RB;
+        const int shift1 = digit_shift_u32(bspan, RB_BITS);
+        // my count above b*, from my own histogram, for the leader's segment bases
+        unsigned long long my_above = 0;
+        for (int i = bstar + 1 + tid; i < HB; i += NT) my_above += S.hist[i];
+        my_above = block_sum_u64(my_above, S);
+        if (tid == 0) a.abv[(long long)w * a.nseg + seg] = my_above;
+        // my boundary entries -> the worker's list (warp-aggregated appends) and their next
+        // radix digit -> the worker's second-level histogram
+        for (int i = tid; i < RB; i += NT) S.hist[i] = 0;
+        __syncthreads();
+        {
+            const float* cvw = a.cval + (long long)w * (a.cap + PCH);
+            const uint32_t* ciw = a.cidx + (long long)w * (a.cap + PCH);
+            const uint2* ch = a.chunks + ((long long)w * a.nseg + seg) * a.maxch;
+            const unsigned nch = a.nch[(long long)w * a.nseg + seg];
+            for (unsigned c = 0; c < nch; ++c) {
+                const uint2 cr = ch[c];
+                for (unsigned b0 = 0; b0 < cr.y; b0 += NT * 4) {
+                    const unsigned e0 = b0 + tid * 4;
+                    float x[4];
+                    if (e0 + 4 <= cr.y) {
+                        const float4 v4 = __ldcg(reinterpret_cast<const float4*>(cvw + cr.x + e0));
+                        x[0] = v4.x; x[1] = v4.y; x[2] = v4.z; x[3] = v4.w;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) x[u] = e0 + u < cr.y ? __ldcg(cvw + cr.x + e0 + u) : 0.f;
+                    }
+                    unsigned bm = 0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const unsigned key = KO::key(x[u]);
+                        bm |= (e0 + u < cr.y && key >= blo && key - blo <= bspan ? 1u : 0u) << u;
+                    }
+                    const unsigned nb = __popc(bm);
+                    if (__any_sync(FULL, nb != 0)) {
+                        unsigned inc = nb;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const unsigned yv = __shfl_up_sync(FULL, inc, o);
+                            if (lane >= o) inc += yv;
+                        }
+                        unsigned long long wb = 0;
+                        if (lane == 31 && inc) wb = atomicAdd(a.bndn + w, (unsigned long long)inc);
+                        wb = __shfl_sync(FULL, wb, 31);
+                        unsigned long long q = wb + inc - nb;
+                        while (bm) {
+                            const int u = __ffs(bm) - 1;
+                            bm &= bm - 1;
+                            const unsigned key = KO::key(x[u]);
+                            atomicAdd(&S.hist[hbin(key, blo, shift1, RB)], 1u);
+                            if (q < (unsigned long long)a.bcap) {
+                                bk[q] = key;
+                                bi[q] = __ldcg(ciw + cr.x + e0 + u);
+                                bs[q] = (unsigned short)seg;
+                            }
+                            ++q;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < RB; i += NT)
+            if (S.hist[i]) atomicAdd(g1 + i, S.hist[i]);
+        // arrive; the leader waits for every CTA, resolves T / the tie cut, computes every
+        // segment's output base, and releases the flag
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(bar, 1u);
+        }
+        ++epoch;
+        if (leader) {
+            if (tid == 0) {
+                while (ld_acquire_gpu(bar) < epoch * nseg) __nanosleep(32);
+                __threadfence();
+            }
+            __syncthreads();
+            for (int i = tid; i < HB; i += NT) g0[i] = 0;  // every CTA has read it
+            const unsigned long long h = __ldcg(a.bndn + w);
+            // second level: the sub-bin of b* holding rank m - above
+            for (int i = tid; i < RB; i += NT) S.hist[i] = __ldcg(g1 + i);
+            __syncthreads();
+            Win wn;
+            wn.lo = blo;
+            wn.span = bspan;
+            wn.shift = shift1;
+            wn.rank = (unsigned long long)a.m - above;
+            {
+                int b2;
+                unsigned long long ab2, t2;
+                find_bin_top<RB>(S.hist, wn.rank, S, b2, ab2, t2);
+                if (b2 >= 0) win_narrow(wn, b2, ab2, RB, RB_BITS);
+            }
+            for (int i = tid; i < RB; i += NT) g1[i] = 0;
+            unsigned T, cut;
+            if (h <= (unsigned long long)RES) {
+                unsigned* sk = reinterpret_cast<unsigned*>(ring);
+                unsigned* si = sk + RES;
+                for (long long i = tid; i < (long long)h; i += NT) {
+                    sk[i] = __ldcg(bk + i);
+                    si[i] = __ldcg(bi + i);
+                }
+                __syncthreads();
+                select_entries(sk, si, (long long)h, wn, S.hist, S, T, cut);
+            } else {
+                select_entries(bk, bi, (long long)h, wn, S.hist, S, T, cut);
+            }
+            // kept boundary entries per segment, then every segment's output base
+            unsigned* kb = S.hist;  // nseg <= MAXSEG counters
+            for (int i = tid; i < a.nseg; i += NT) kb[i] = 0;
+            __syncthreads();
+            for (long long i = tid; i < (long long)h; i += NT) {
+                const unsigned key = __ldcg(bk + i);
+                if (key > T || (key == T && __ldcg(bi + i) <= cut)) atomicAdd(&kb[__ldcg(bs + i)], 1u);
+            }
+            __syncthreads();
+            {
+                constexpr int PER = MAXSEG / NT;
+                unsigned long long v[PER], sum = 0;
+#pragma unroll
+                for (int u = 0; u < PER; ++u) {
+                    const int q = tid * PER + u;
+                    v[u] = q < a.nseg ? __ldcg(a.abv + (long long)w * a.nseg + q) + kb[q] : 0ull;
+                    sum += v[u];
+                }
+                unsigned long long incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned long long yv = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += yv;
+                }
+                if (lane == 31) S.bsum[warp] = incl;
+                __syncthreads();
+                unsigned long long run_b = incl - sum;
+#pragma unroll
+                for (int i = 0; i < NW; ++i) run_b += i < warp ? S.bsum[i] : 0ull;
+#pragma unroll
+                for (int u = 0; u < PER; ++u) {
+                    const int q = tid * PER + u;
+                    if (q < a.nseg) a.base[(long long)w * a.nseg + q] = (unsigned)run_b;
+                    run_b += v[u];
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                Sel o;
+                o.T = T;
+                o.cut = cut;
+                o.mode = M_FAST;
+                o.pad = 0;
+                o.h = h;
+                a.sel[w] = o;
+                __threadfence();
+                st_release_u32(a.flag + w, 1u);
+            }
+        }
+        if (tid == 0) {
+            while (ld_acquire_gpu(a.flag + w) == 0u) __nanosleep(32);
+            S.u[0] = __ldcg(&a.sel[w].T);
+            S.u[1] = __ldcg(&a.sel[w].cut);
+            S.u[2] = __ldcg(a.base + (long long)w * a.nseg + seg);
+            tm[3] = gtimer();
+        }
+        __syncthreads();
+        ss_topk = write_kept(a, S, smem_raw, w, seg, S.u[0], S.u[1], S.u[2], t_begin, ntl);
+    } else {
+        ss_topk = slow_mode(a, S, smem_raw, w, seg, row, t_begin, t_end, epoch);
+        if (leader) {  // every CTA is past the reads of the slow-mode histograms and hist0
+            worker_barrier(bar, (++epoch) * nseg);
+            for (int i = tid; i < HB; i += NT) g0[i] = 0;
+            for (int i = tid; i < 3 * RB; i += NT) a.histR[(long long)w * 3 * RB + i] = 0;
+        } else {
+            worker_barrier(bar, (++epoch) * nseg);
+        }
+        if (tid == 0) tm[3] = gtimer();
+    }
+    {
+        const double t = block_sum_fixed(ss_topk, S);
+        if (tid == 0) a.pwrite[(long long)w * a.nseg + seg] = t;
+    }
+    if (leader && tid == 0) {
+        long long* st = a.stats + 4 * w;
+        st[0] = (long long)C;
+        st[1] = slow ? 0 : (long long)__ldcg(a.bndn + w);
+        st[2] = C < (unsigned long long)a.m ? 1 : 0;
+        st[3] = slow ? 1 : 0;
+    }
+    // ---------------- G: the last CTA reduces the norms, gates, and cleans up -----------------
+    __syncthreads();
+    if (tid == 0) {
+        tm[4] = gtimer();
+        unsigned long long* tp = a.times + ((long long)w * a.nseg + seg) * NPH;
+        for (int i = 0; i < 5; ++i) tp[i] = tm[i];
+        __threadfence();
+        S.last = atomicAdd(a.done, 1u) == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (!S.last) return;
+    __threadfence();
+    for (int ww = warp; ww < a.k; ww += NW) {
+        double sf = 0.0, sk = 0.0;
+        for (int i = lane; i < a.nseg; i += 32) {
+            sf = dadd(sf, __ldcg(a.pmain + (long long)ww * a.nseg + i));
+            sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nseg + i));
+        }
+        sf = warp_sum(sf);
+        sk = warp_sum(sk);
+        if (lane == 0) {
+            a.norms2[2 * ww] = sf;
+            a.norms2[2 * ww + 1] = sk;
+            if (a.states) {
+                sg_gate_state st = a.states[ww];
+                uint8_t d;
+                double r;
+                gate_math_f(st, sf, sk, d, r);
+                a.states[ww] = st;
+                if (a.decision) a.decision[ww] = d;
+                if (a.rho) a.rho[ww] = r;
+            }
+        }
+    }
+    // leave the zero-state for the next call (histograms were cleared by the leaders)
+    for (int i = tid; i < a.k; i += NT) {
+        a.bar[i] = 0;
+        a.flag[i] = 0;
+        a.poolctr[i] = 0;
+        a.count[i] = 0;
+        a.bndn[i] = 0;
+        a.ovf[i] = 0;
+        a.smax[i] = 0;
+    }
+    if (tid == 0) {
+        a.done[0] = 0;
+        unsigned long long* tp = a.times + ((long long)w * a.nseg + seg) * NPH;
+        tp[5] = gtimer();
+    }
+}
+
+}  // namespace fz
+
+int topk_fused_f32(const float* g, int k, long long ld, long long dim, long long m, uint32_t* idx, float* val,
+                   double* norms2, sg_gate_state* states, uint8_t* decision, double* rho, int* tile_off, void* ws,
+                   size_t ws_bytes, int nseg_target, cudaStream_t stream) {
+    using namespace fz;
+    const Plan p = make_plan(k, dim, m, nseg_target);
+    if (!ws || ws_bytes < p.total) return SG_ERR_WORKSPACE;
+    unsigned char* base = reinterpret_cast<unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    auto at = [&](size_t off) { return base + off; };
+    Args a;
+    a.g = g;
+    a.ld = ld;
+    a.dim = dim;
+    a.m = m;
+    a.ntiles = p.ntiles;
+    a.nch_s = p.nch_s;
+    a.r_est = p.r_est;
+    a.cap = p.cap;
+    a.bcap = p.bcap;
+    a.k = k;
+    a.nseg = p.nseg;
+    a.tps = p.tps;
+    a.maxch = p.maxch;
+    a.vec = (reinterpret_cast<size_t>(g) % 16 == 0) && ((ld * 4) % 16 == 0);
+    a.bar = reinterpret_cast<unsigned*>(at(p.o_bar));
+    a.flag = reinterpret_cast<unsigned*>(at(p.o_flag));
+    a.poolctr = reinterpret_cast<unsigned long long*>(at(p.o_poolctr));
+    a.count = reinterpret_cast<unsigned long long*>(at(p.o_count));
+    a.bndn = reinterpret_cast<unsigned long long*>(at(p.o_bndn));
+    a.ovf = reinterpret_cast<unsigned*>(at(p.o_ovf));
+    a.smax = reinterpret_cast<unsigned*>(at(p.o_smax));
+    a.done = reinterpret_cast<unsigned*>(at(p.o_done));
+    a.histA = reinterpret_cast<unsigned*>(at(p.o_histA));
+    a.histB = reinterpret_cast<unsigned*>(at(p.o_histB));
+    a.hist0 = reinterpret_cast<unsigned*>(at(p.o_hist0));
+    a.hist1 = reinterpret_cast<unsigned*>(at(p.o_hist1));
+    a.histR = reinterpret_cast<unsigned*>(at(p.o_histR));
+    a.sel = reinterpret_cast<Sel*>(at(p.o_sel));
+    a.pmain = reinterpret_cast<double*>(at(p.o_pmain));
+    a.pwrite = reinterpret_cast<double*>(at(p.o_pwrite));
+    a.chunks = reinterpret_cast<uint2*>(at(p.o_chunks));
+    a.nch = reinterpret_cast<unsigned*>(at(p.o_nch));
+    a.cgt = reinterpret_cast<unsigned*>(at(p.o_cgt));
+    a.ceq = reinterpret_cast<unsigned*>(at(p.o_ceq));
+    a.abv = reinterpret_cast<unsigned long long*>(at(p.o_abv));
+    a.base = reinterpret_cast<unsigned*>(at(p.o_base));
+    a.bkey = reinterpret_cast<unsigned*>(at(p.o_bkey));
+    a.bidx = reinterpret_cast<unsigned*>(at(p.o_bidx));
+    a.bseg = reinterpret_cast<unsigned short*>(at(p.o_bseg));
+    a.cidx = reinterpret_cast<uint32_t*>(at(p.o_cidx));
+    a.cval = reinterpret_cast<float*>(at(p.o_cval));
+    a.stats = reinterpret_cast<long long*>(at(p.o_stats));
+    a.times = reinterpret_cast<unsigned long long*>(at(p.o_times));
+    a.idx = idx;
+    a.val = val;
+    a.tile_off = tile_off;
+    a.norms2 = norms2;
+    a.states = states;
+    a.decision = decision;
+    a.rho = rho;
+    smem_attr((const void*)k_topk_fused, (int)RING_BYTES);
+    launch_coop(k_topk_fused, dim3((unsigned)p.nseg, (unsigned)k), dim3(NT), RING_BYTES, stream, a);
+    debug_sync("k_topk_fused", stream);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+size_t topk_fused_workspace_bytes(int k, long long dim, long long m, int nseg_target) {
+    return fz::make_plan(k, dim, m, nseg_target).total;
+}
+
+size_t topk_fused_zero_bytes(int k, long long dim, long long m, int nseg_target) {
+    return fz::make_plan(k, dim, m, nseg_target).zero_end + 256;
+}
+
+int topk_fused_ctas_per_sm() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && cache[dev] > 0) return cache[dev];
+    int per_sm = 0;
+    smem_attr((const void*)fz::k_topk_fused, (int)fz::RING_BYTES);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fz::k_topk_fused, fz::NT, fz::RING_BYTES) != cudaSuccess) {
+        cudaGetLastError();
+        per_sm = 2;
+    }
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 3) per_sm = 3;
+    if (dev >= 0 && dev < 64) cache[dev] = per_sm;
+    return per_sm;
+}
+
+int topk_fused_segments(int k, long long dim, long long m, int nseg_target) {
+    return fz::make_plan(k, dim, m, nseg_target).nseg;
+}
+
+// Phase timestamps (%globaltimer, ns) of the last call: [w][seg][8] = {start, estimate done,
+// main pass done (after its barrier), selection known, CTA done, cleanup done (last CTA)}.
+int topk_fused_phases(int k, long long dim, long long m, int nseg_target, const void* ws, size_t ws_bytes,
+                      unsigned long long* out, long long out_len, cudaStream_t stream) {
+    const fz::Plan p = fz::make_plan(k, dim, m, nseg_target);
+    if (!ws || ws_bytes < p.total) return SG_ERR_WORKSPACE;
+    const long long n = (long long)k * p.nseg * fz::NPH;
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    return cudaMemcpyAsync(out, base + p.o_times, sizeof(unsigned long long) * (size_t)(n < out_len ? n : out_len),
+                           cudaMemcpyDeviceToDevice, stream) == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+// Diagnostics of the last call on this workspace: {candidates, boundary entries,
+// estimate undershot (0/1), slow mode (0/1)} per worker.
+int topk_fused_stats(int k, long long dim, long long m, int nseg_target, const void* ws, size_t ws_bytes,
+                     int64_t* out, cudaStream_t stream) {
+    const fz::Plan p = fz::make_plan(k, dim, m, nseg_target);
+    if (!ws || ws_bytes < p.total) return SG_ERR_WORKSPACE;
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    return cudaMemcpyAsync(out, base + p.o_stats, sizeof(long long) * 4 * (size_t)k, cudaMemcpyDeviceToDevice,
+                           stream) == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+}  // namespace sg

@@ -20,7 +20,7 @@ _GATE_BYTES = _capi.GATE_STATE_DTYPE.itemsize
 # Kernel launches issued through this module (each C-ABI entry point launches a fixed
 # sequence; see csrc/topk.cu and csrc/aggregate.cu).  bench.py reports the count.
 LAUNCHES = {"n": 0}
-TOPK_LAUNCHES = {torch.float32: 2 + 2 + 1 + 1 + 1 + 1, torch.float64: 2 + 2 + 1 + 1 + 1 + 1}
+TOPK_LAUNCHES = {torch.float32: 1, torch.float64: 2 + 2 + 1 + 1 + 1 + 1}
 
 
 def _count(n: int) -> None:
@@ -48,18 +48,35 @@ def _stream() -> int:
 
 
 class Workspace:
-    """Grow-only device scratch buffer owned by the Python caller (one per device)."""
+    """Grow-only device scratch buffers owned by the Python caller, one per (device, kind,
+    slot).  ``slot`` separates calls that may run concurrently on different streams; ``kind``
+    keeps the float32 Top-k workspace (which carries zero-initialised state between calls,
+    see sg_topk_workspace_zero_bytes_f32) apart from every other user."""
 
-    _cache: dict[tuple[int, int], torch.Tensor] = {}
+    _cache: dict[tuple, torch.Tensor] = {}
+    _keys: dict[tuple, tuple] = {}
 
     @classmethod
-    def get(cls, nbytes: int, device: torch.device, slot: int = 0) -> torch.Tensor:
-        """``slot`` separates calls that may run concurrently on different streams."""
+    def get(cls, nbytes: int, device: torch.device, slot: int = 0, kind: str = "scratch") -> torch.Tensor:
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        buf = cls._cache.get((idx, slot))
+        key = (idx, kind, slot)
+        buf = cls._cache.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
-            cls._cache[(idx, slot)] = buf
+            buf = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            cls._cache[key] = buf
+            cls._keys.pop(key, None)
+        return buf
+
+    @classmethod
+    def get_topk(cls, nbytes: int, zero_bytes: int, plan_key: tuple, device: torch.device, slot: int = 0):
+        """The float32 Top-k workspace: zero-filled when created and whenever the plan
+        (k, dim, m) changes; every call leaves its zero-state region zeroed again."""
+        buf = cls.get(nbytes, device, slot, kind="topk32")
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        key = (idx, "topk32", slot)
+        if cls._keys.get(key) != plan_key:
+            buf[:min(int(zero_bytes), buf.numel())].zero_()
+            cls._keys[key] = plan_key
         return buf
 
 
@@ -127,8 +144,12 @@ def topk_gate(
     nbytes = topk_workspace_bytes(g.dtype, k, D, m)
     if nbytes == 0:
         raise ValueError("invalid top-k shape")
-    ws = Workspace.get(nbytes, dev, workspace_slot)
     lib = _capi.load()
+    if g.dtype == torch.float32:
+        zb = int(lib.sg_topk_workspace_zero_bytes_f32(k, D, m))
+        ws = Workspace.get_topk(nbytes, zb, (k, D, m), dev, workspace_slot)
+    else:
+        ws = Workspace.get(nbytes, dev, workspace_slot, kind="topk64")
     args = [g2.data_ptr(), k, ld, D, m, idx.data_ptr(), val.data_ptr(), norms2.data_ptr(),
             _ptr(states), _ptr(decision), _ptr(rho)]
     if g.dtype == torch.float32:
@@ -144,12 +165,26 @@ def topk_gate(
 
 def topk_stats(dtype: torch.dtype, k: int, dim: int, m: int, device: torch.device, workspace_slot: int = 0) -> np.ndarray:
     """Per-worker {candidates, boundary, fallback, slow} of the last topk_gate call (synchronises)."""
-    ws = Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, workspace_slot)
+    if dtype == torch.float32:
+        ws = Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, workspace_slot, kind="topk32")
+    else:
+        ws = Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, workspace_slot, kind="topk64")
     out = torch.zeros((k, 4), dtype=torch.int64, device=device)
     lib = _capi.load()
     fn = lib.sg_topk_stats_f32 if dtype == torch.float32 else lib.sg_topk_stats_f64
     _capi.check(fn(k, dim, m, ws.data_ptr(), ws.numel(), out.data_ptr(), _stream()), "sg_topk_stats")
     return out.cpu().numpy()
+
+
+def topk_phases(k: int, dim: int, m: int, device: torch.device, workspace_slot: int = 0) -> np.ndarray:
+    """float32 Top-k phase timestamps of the last call (ns, [k, nseg, 8]; synchronises)."""
+    lib = _capi.load()
+    nseg = int(lib.sg_topk_segments_f32(k, dim, m))
+    ws = Workspace.get(topk_workspace_bytes(torch.float32, k, dim, m), device, workspace_slot, kind="topk32")
+    out = torch.zeros(k * nseg * 8, dtype=torch.int64, device=device)
+    _capi.check(lib.sg_topk_phases_f32(k, dim, m, ws.data_ptr(), ws.numel(), out.data_ptr(), out.numel(), _stream()),
+                "sg_topk_phases_f32")
+    return out.cpu().numpy().reshape(k, nseg, 8)
 
 
 def gate_update(norms2: torch.Tensor, states: torch.Tensor):
@@ -324,7 +359,7 @@ class GuardedDenseLaunchers:
         _count(1)
 
     def allgather_sgd(self, lr: float, first_step: bool, out: torch.Tensor | None = None) -> None:
-        st = self._ag(len(self._pp), self._pp, self._guard, self._gn, self._dim, _ptr(out), self._p, self._b,
+        st = self._ag(len(self._pp), self._pp, self._rank, self._guard, self._gn, self._dim, _ptr(out), self._p, self._b,
                       float(lr), self._mu, self._wd, int(bool(first_step)), _stream())
         _capi.check(st, "sg_peer_allgather_sgd_f32")
         _count(1)

@@ -156,8 +156,9 @@ def test_float32_aggregate_is_correctly_rounded(cuda):
 @pytest.mark.parametrize("merge_own", [-1, 1])
 def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own):
     """The multi-GPU entry points on one GPU (peer pointers may be local): two "ranks" of two
-    workers each.  Mixed decisions: each rank's guarded partial (sg_weighted_partial_f32),
-    summed in rank order with momentum SGD (sg_peer_reduce_sgd_f32), equals the oracle fold +
+    workers each.  Mixed decisions: each rank's guarded partial (sg_weighted_partial_f32), the
+    position-sharded reduce of each rank's slice (sg_peer_reduce_slice_f32) and the all-gather
+    of the slices fused with momentum SGD (sg_peer_allgather_sgd_f32) equal the oracle fold +
     SGD within the fp32 tolerance, and the all-sparse merge over per-worker pointers
     (sg_weighted_aggregate_peers_f32) is a no-op.  All compressed: the reverse, and the peer
     merge is bit-identical to sg_weighted_aggregate_f32 on the same payloads (merge_own 1:
@@ -200,12 +201,14 @@ def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own):
                                           [ranks[j // k][3][j % k].data_ptr() for j in range(W)], params, buf, mu, wd,
                                           local_lo=0, local_n=k, sparse_merge=merge_own)
         merge(w, lr, False)
+        dls = [kernels.GuardedDenseLaunchers(k, D, ld, dec_all[r * k:(r + 1) * k], ranks[r][1], ranks[r][2], rp,
+                                             ranks[r][3], partials[r], [t.data_ptr() for t in partials], dec_all,
+                                             params, buf, mu, wd, r) for r in range(P)]
+        for r in range(P):  # each "rank": its partial, then its slice of the position-sharded reduce
+            dls[r].partial(w[r * k:(r + 1) * k], ranks[r][0])
         for r in range(P):
-            dl = kernels.GuardedDenseLaunchers(k, D, ld, dec_all[r * k:(r + 1) * k], ranks[r][1], ranks[r][2], rp,
-                                               ranks[r][3], partials[r], [t.data_ptr() for t in partials], dec_all,
-                                               params, buf, mu, wd)
-            dl.partial(w[r * k:(r + 1) * k], ranks[r][0])
-        dl.reduce_sgd(lr, False)
+            dls[r].reduce_slice()
+        dls[0].allgather_sgd(lr, False)  # one replica: the reduced slices gathered + momentum SGD
         torch.cuda.synchronize()
         pl = [payload[j] if dec[j] else G[j].astype(np.float64) for j in range(W)]
         agg = comm_ref.aggregate(pl, w)
