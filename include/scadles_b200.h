@@ -71,11 +71,21 @@ int64_t sg_topk_count(int64_t dim, double cr);
  * (unaligned rows fall back to scalar loads, still on the GPU). */
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m);
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m);
-/* The float32 path is one persistent cooperative kernel whose workspace carries zero-state
- * between calls: the first sg_topk_workspace_zero_bytes_f32(k, dim, m) bytes must be zero
- * before the first call and whenever (k, dim, m) change; every call leaves them zeroed.  Its
- * candidate pool holds ~2m entries (not D), so the workspace is ~16 m + 1.2 MB per worker. */
+/* Persistent float32 variant: the same contract as sg_topk_gate_f32 in ONE cooperative
+ * kernel (sample -> estimate -> single read -> select -> ordered write -> gate, synchronised
+ * per worker on the device), with a ~2m-entry candidate pool instead of per-segment slots of D
+ * (workspace ~16 m + 2 MB per worker).  Its workspace carries zero-state between calls: the
+ * first sg_topk_workspace_zero_bytes_f32(k, dim, m) bytes must be zero before the first call
+ * and whenever (k, dim, m) change; every call leaves them zeroed. */
+size_t sg_topk_workspace_bytes_fused_f32(int k, int64_t dim, int64_t m);
 size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m);
+int sg_topk_gate_fused_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m,
+                           uint32_t* idx, float* val, double* norms2,
+                           sg_gate_state* states, uint8_t* decision, double* rho,
+                           int32_t* tile_off,
+                           void* workspace, size_t workspace_bytes, void* stream);
+int sg_topk_stats_fused_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes,
+                            int64_t* out, void* stream);
 int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m,
                      uint32_t* idx, float* val, double* norms2,
                      sg_gate_state* states, uint8_t* decision, double* rho,
@@ -88,16 +98,16 @@ int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m,
 
 /* Diagnostics of the most recent sg_topk_gate_* call that used `workspace` (same k, dim, m):
  * out[4j..4j+3] (device int64) = {candidates kept by the main pass, boundary entries, fallback
- * pass taken (0/1), oversized-tie write mode (0/1)} for worker j.  float32: {candidates,
- * boundary entries, estimate undershot (0/1), exact multi-pass fallback taken (0/1)}. */
+ * pass taken (0/1), oversized-tie write mode (0/1)} for worker j.  (The fused variant's stats:
+ * {candidates, boundary entries, estimate undershot (0/1), exact multi-pass fallback (0/1)}.) */
 int sg_topk_stats_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes,
                       int64_t* out, void* stream);
 int sg_topk_stats_f64(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes,
                       int64_t* out, void* stream);
 
-/* float32 diagnostics: segments (CTAs) per worker of the persistent Top-k kernel, and the
- * %globaltimer stamps (ns) of its phases in the last call: out[(w*nseg + s)*8 + i] = {start,
- * estimate done, main pass done, selection known, CTA done, cleanup done (last CTA only), -, -}. */
+/* Fused-variant diagnostics: segments (CTAs) per worker of the persistent Top-k kernel, and the
+ * %globaltimer stamps (ns) of its phases in the last call: out[(w*nseg + s)*16 + i], the phase
+ * list in csrc/topk_fused.cu (start, sample, estimate, main pass, selection, write, done). */
 int sg_topk_segments_f32(int k, int64_t dim, int64_t m);
 int sg_topk_phases_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes, uint64_t* out,
                        int64_t out_len, void* stream);

@@ -1996,6 +1996,11 @@ extern "C" {
 
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m) {
     if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
+    return make_plan<float>(k, dim, m, segments_per_worker<float>(k), (long long)num_sms() * CW_PER_SM).total;
+}
+
+size_t sg_topk_workspace_bytes_fused_f32(int k, int64_t dim, int64_t m) {
+    if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
     return topk_fused_workspace_bytes(k, dim, m, fused_segments(k));
 }
 
@@ -2012,6 +2017,14 @@ int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m, 
                      float* val, double* norms2, sg_gate_state* states, uint8_t* decision,
                      double* rho, int32_t* tile_off, void* workspace, size_t workspace_bytes,
                      void* stream) {
+    return topk_gate<float>(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, tile_off,
+                            workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int sg_topk_gate_fused_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m, uint32_t* idx,
+                           float* val, double* norms2, sg_gate_state* states, uint8_t* decision,
+                           double* rho, int32_t* tile_off, void* workspace, size_t workspace_bytes,
+                           void* stream) {
     if (!g || !idx || !val || !norms2 || k < 1 || dim < 1 || m < 1 || m > dim || ld < dim) return SG_ERR_INVALID;
     if (k > MAX_WORKERS || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
     return topk_fused_f32(g, k, ld, dim, m, idx, val, norms2, states, decision, rho, tile_off, workspace,
@@ -2026,6 +2039,11 @@ int sg_topk_gate_f64(const double* g, int k, int64_t ld, int64_t dim, int64_t m,
 
 int sg_topk_stats_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes, int64_t* out,
                       void* stream) {
+    return topk_stats<float>(k, dim, m, workspace, workspace_bytes, out, (cudaStream_t)stream);
+}
+
+int sg_topk_stats_fused_f32(int k, int64_t dim, int64_t m, const void* workspace, size_t workspace_bytes,
+                            int64_t* out, void* stream) {
     if (!workspace || !out || k < 1 || dim < 1 || m < 1 || m > dim) return SG_ERR_INVALID;
     return topk_fused_stats(k, dim, m, fused_segments(k), workspace, workspace_bytes, out, (cudaStream_t)stream);
 }

@@ -55,7 +55,11 @@ constexpr int CHUNK = 32;         // sample chunk (one warp load)
 constexpr int PCH = 8192;         // pool chunk (entries; >= 2 tiles of candidates)
 constexpr int RES = 6144;         // boundary entries resolved in shared memory
 constexpr int MAXSEG = 1024;
-constexpr int NPH = 8;            // phase timestamps per CTA (diagnostics)
+constexpr int NPH = 16;           // phase timestamps per CTA (diagnostics)
+constexpr int SB_BINS = 8192;     // sample histogram bins (key bits [30:18])
+constexpr int SB_SHIFT = 18;
+constexpr int SMALL = 1024;       // boundary entries ranked directly by the leader
+constexpr int NSAMP = 32;         // CTAs per worker that read the sample
 constexpr size_t RING_BYTES = (size_t)STAGES * TILE * sizeof(float);  // 48 KB dynamic smem
 static_assert(PCH >= 2 * TILE, "a chunk switch cannot happen on two consecutive tiles");
 static_assert(2 * RES * 4 <= (int)RING_BYTES, "the resolve buffers live in the ring");
@@ -68,13 +72,19 @@ struct Sel {  // per-worker selection result (written by the leader, read by eve
     unsigned long long h;  // boundary entries
 };
 
+struct Pub {  // per-worker values the leader publishes to the worker's CTAs (behind a flag)
+    unsigned est, smax, blo, bspan;
+    int bstar, shift1, slow, pad;
+    unsigned long long above, C;
+};
+
 struct Plan {
     int k, nseg, tps, maxch;
     long long dim, m, ntiles, s_eff, nch_s, r_est, cap, bcap;
-    size_t o_bar, o_flag, o_poolctr, o_count, o_bndn, o_ovf, o_smax, o_done, o_histA, o_histB, o_hist0, o_hist1,
+    size_t o_bar, o_sbar, o_flag, o_poolctr, o_count, o_bndn, o_ovf, o_smax, o_done, o_histA, o_hist0, o_hist1,
         o_histR, zero_end;
-    size_t o_sel, o_pmain, o_pwrite, o_chunks, o_nch, o_cgt, o_ceq, o_abv, o_base, o_bkey, o_bidx, o_bseg, o_cidx,
-        o_cval, o_stats, o_times, total;
+    size_t o_sel, o_pub, o_pmain, o_pwrite, o_chunks, o_nch, o_cgt, o_ceq, o_abv, o_base, o_bkey, o_bidx, o_bseg, o_pool,
+        o_stats, o_times, total;
 };
 
 inline Plan make_plan(int k, long long dim, long long m, int nseg_target) {
@@ -110,21 +120,22 @@ inline Plan make_plan(int k, long long dim, long long m, int nseg_target) {
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
     // -- zero-initialised state (every call leaves it zeroed) --
     p.o_bar = take(sizeof(unsigned) * k);
-    p.o_flag = take(sizeof(unsigned) * k);
+    p.o_sbar = take(sizeof(unsigned) * k);
+    p.o_flag = take(sizeof(unsigned) * 4 * k);
     p.o_poolctr = take(sizeof(unsigned long long) * k);
     p.o_count = take(sizeof(unsigned long long) * k);
     p.o_bndn = take(sizeof(unsigned long long) * k);
     p.o_ovf = take(sizeof(unsigned) * k);
     p.o_smax = take(sizeof(unsigned) * k);
     p.o_done = take(sizeof(unsigned) * 4);
-    p.o_histA = take(sizeof(unsigned) * (size_t)k * HB);
-    p.o_histB = take(sizeof(unsigned) * (size_t)k * RB);
+    p.o_histA = take(sizeof(unsigned) * (size_t)k * SB_BINS);
     p.o_hist0 = take(sizeof(unsigned) * (size_t)k * HB);
     p.o_hist1 = take(sizeof(unsigned) * (size_t)k * RB);
     p.o_histR = take(sizeof(unsigned) * (size_t)k * 3 * RB);
     p.zero_end = o;
     // -- scratch (no initial state) --
     p.o_sel = take(sizeof(Sel) * k);
+    p.o_pub = take(sizeof(Pub) * k);
     p.o_pmain = take(sizeof(double) * (size_t)k * p.nseg);
     p.o_pwrite = take(sizeof(double) * (size_t)k * p.nseg);
     p.o_chunks = take(sizeof(uint2) * (size_t)k * p.nseg * p.maxch);
@@ -136,8 +147,7 @@ inline Plan make_plan(int k, long long dim, long long m, int nseg_target) {
     p.o_bkey = take(sizeof(unsigned) * (size_t)k * p.bcap);
     p.o_bidx = take(sizeof(unsigned) * (size_t)k * p.bcap);
     p.o_bseg = take(sizeof(unsigned short) * (size_t)k * p.bcap);
-    p.o_cidx = take(sizeof(uint32_t) * (size_t)k * (p.cap + PCH));
-    p.o_cval = take(sizeof(float) * (size_t)k * (p.cap + PCH));
+    p.o_pool = take(sizeof(uint2) * (size_t)k * (p.cap + PCH));
     p.o_stats = take(sizeof(long long) * 4 * (size_t)k);
     p.o_times = take(sizeof(unsigned long long) * NPH * (size_t)k * p.nseg);
     p.total = o + 256;
@@ -149,7 +159,9 @@ struct Args {
     long long ld, dim, m, ntiles, nch_s, r_est, cap, bcap;
     int k, nseg, tps, maxch, vec;
     unsigned* bar;
-    unsigned* flag;
+    unsigned* sbar;
+    unsigned* flag;  // [k][4]: 0 estimate, 1 boundary bin, 2 selection
+    Pub* pub;
     unsigned long long* poolctr;
     unsigned long long* count;
     unsigned long long* bndn;
@@ -157,7 +169,6 @@ struct Args {
     unsigned* smax;
     unsigned* done;
     unsigned* histA;
-    unsigned* histB;
     unsigned* hist0;
     unsigned* hist1;
     unsigned* histR;
@@ -173,8 +184,7 @@ struct Args {
     unsigned* bkey;
     unsigned* bidx;
     unsigned short* bseg;
-    uint32_t* cidx;
-    float* cval;
+    uint2* pool;  // candidates: (index, value bits), chunks of PCH in index order per CTA
     long long* stats;
     unsigned long long* times;
     uint32_t* idx;
@@ -207,14 +217,42 @@ SG_DEV void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Leader/flag synchronisation: CTAs arrive on a per-worker counter (fire-and-forget release
+// add), the worker's leader CTA waits for the arrivals it needs, computes, publishes, and
+// releases a flag the others poll.  Only one CTA per worker reads merged histograms (no
+// hot-spot reads of shared lines by every CTA).
+SG_DEV void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+SG_DEV void cta_arrive(unsigned* ctr) {
+    __threadfence();  // every thread's prior global writes, before the CTA's release
+    __syncthreads();
+    if (threadIdx.x == 0) red_release_add(ctr, 1u);
+}
+SG_DEV void cta_wait_count(const unsigned* ctr, unsigned target) {
+    if (threadIdx.x == 0)
+        while (ld_acquire_gpu(ctr) < target) __nanosleep(64);
+    __syncthreads();
+}
+SG_DEV void cta_release_flag(unsigned* f) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_u32(f, 1u);
+}
+SG_DEV void cta_wait_flag(const unsigned* f) {
+    if (threadIdx.x == 0)
+        while (ld_acquire_gpu(f) == 0u) __nanosleep(64);
+    __syncthreads();
+}
+
 // Per-worker device barrier: the worker's nseg CTAs are co-resident (cooperative launch).
 // Barrier j of a call waits for the counter to reach j * nseg.
 SG_DEV void worker_barrier(unsigned* ctr, unsigned target) {
+    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1u);
-        while (ld_acquire_gpu(ctr) < target) __nanosleep(32);
+        red_release_add(ctr, 1u);
+        while (ld_acquire_gpu(ctr) < target) __nanosleep(64);
         __threadfence();
     }
     __syncthreads();
@@ -275,6 +313,59 @@ SG_DEV void find_bin_top(const unsigned* hist, unsigned long long rank, Smem& S,
             }
             cum += h;
         }
+    }
+    __syncthreads();
+    bin = S.bin;
+    above = bin >= 0 ? S.above : 0ull;
+    total = tot;
+    __syncthreads();
+}
+
+// find_bin_top over a histogram in global memory: each thread's PER bins are loaded into
+// registers once (independent loads in flight), so the owning thread's walk is local.
+template <int NB>
+SG_DEV void find_bin_top_g(const unsigned* ghist, unsigned long long rank, Smem& S, int& bin,
+                           unsigned long long& above, unsigned long long& total) {
+    constexpr int PER = NB / NT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int top = NB - 1 - PER * tid;
+    unsigned hv[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) hv[i] = __ldcg(ghist + top - i);
+    unsigned long long s = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) s += hv[i];
+    unsigned long long incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) S.bsum[warp] = incl;
+    if (tid == 0) S.bin = -1;
+    __syncthreads();
+    unsigned long long wb = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        wb += i < warp ? S.bsum[i] : 0ull;
+        tot += S.bsum[i];
+    }
+    incl += wb;
+    const unsigned long long ex = incl - s;
+    if (ex < rank && incl >= rank) {
+        unsigned long long cum = ex;
+        int b = -1;
+        unsigned long long ab = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            if (b < 0 && cum + hv[i] >= rank) {
+                b = top - i;
+                ab = cum;
+            }
+            cum += hv[i];
+        }
+        S.bin = b;
+        S.above = ab;
     }
     __syncthreads();
     bin = S.bin;
@@ -425,42 +516,64 @@ SG_DEV double block_sum_fixed(double v, Smem& S) {
 }
 
 // Visit this CTA's candidates in index order, EPT consecutive per thread per block of
-// NT * EPT: f(x[EPT], xi[EPT], nvalid, block entries) is called by every thread for every
-// block (block-uniform control flow).
+// NT * EPT, with the next block's loads in flight: f(x[EPT], xi[EPT], nvalid) is called by
+// every thread for every block (block-uniform control flow).
+template <int EPT>
+SG_DEV void load_block(const uint2* pool, uint2 cr, unsigned b0, uint4 (&v)[EPT / 2]) {
+    const unsigned e0 = b0 + threadIdx.x * EPT;
+    if (e0 + EPT <= cr.y) {  // chunk bases and e0 are even: 16-byte loads of two entries
+#pragma unroll
+        for (int r = 0; r < EPT / 2; ++r) v[r] = __ldcg(reinterpret_cast<const uint4*>(pool + cr.x + e0) + r);
+    } else {
+#pragma unroll
+        for (int r = 0; r < EPT / 2; ++r) {
+            const uint2 p0 = e0 + 2 * r < cr.y ? __ldcg(pool + cr.x + e0 + 2 * r) : make_uint2(0u, 0u);
+            const uint2 p1 = e0 + 2 * r + 1 < cr.y ? __ldcg(pool + cr.x + e0 + 2 * r + 1) : make_uint2(0u, 0u);
+            v[r] = make_uint4(p0.x, p0.y, p1.x, p1.y);
+        }
+    }
+}
+
 template <int EPT, typename F>
 SG_DEV void for_candidates(const Args& a, int w, int seg, F&& f) {
-    const int tid = threadIdx.x;
     constexpr int SPAN = NT * EPT;
-    const uint32_t* ci = a.cidx + (long long)w * (a.cap + PCH);
-    const float* cv = a.cval + (long long)w * (a.cap + PCH);
+    const uint2* pool = a.pool + (long long)w * (a.cap + PCH);
     const uint2* ch = a.chunks + ((long long)w * a.nseg + seg) * a.maxch;
     const unsigned nch = a.nch[(long long)w * a.nseg + seg];
-    for (unsigned c = 0; c < nch; ++c) {
-        const uint2 cr = ch[c];
-        const unsigned cb = cr.x, cn = cr.y;
-        for (unsigned b0 = 0; b0 < cn; b0 += SPAN) {
-            const unsigned e0 = b0 + tid * EPT;
-            float x[EPT];
-            uint32_t xi[EPT];
-            if (e0 + EPT <= cn) {  // chunk bases and e0 are 4-aligned
-#pragma unroll
-                for (int r = 0; r < EPT / 4; ++r) {
-                    const float4 v4 = __ldcg(reinterpret_cast<const float4*>(cv + cb + e0) + r);
-                    const uint4 i4 = __ldcg(reinterpret_cast<const uint4*>(ci + cb + e0) + r);
-                    x[4 * r] = v4.x; x[4 * r + 1] = v4.y; x[4 * r + 2] = v4.z; x[4 * r + 3] = v4.w;
-                    xi[4 * r] = i4.x; xi[4 * r + 1] = i4.y; xi[4 * r + 2] = i4.z; xi[4 * r + 3] = i4.w;
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < EPT; ++u) {
-                    const bool ok = e0 + u < cn;
-                    x[u] = ok ? __ldcg(cv + cb + e0 + u) : 0.f;
-                    xi[u] = ok ? __ldcg(ci + cb + e0 + u) : 0u;
-                }
-            }
-            const int nv = e0 >= cn ? 0 : (int)(cn - e0 < (unsigned)EPT ? cn - e0 : EPT);
-            f(x, xi, nv, cn - b0 < (unsigned)SPAN ? cn - b0 : (unsigned)SPAN);
+    if (nch == 0) return;
+    unsigned c = 0, b0 = 0;
+    uint2 cr = ch[0];
+    uint4 cur[EPT / 2];
+    load_block<EPT>(pool, cr, b0, cur);
+    for (;;) {
+        unsigned nc = c, nb = b0 + SPAN;
+        uint2 ncr = cr;
+        if (nb >= cr.y) {
+            nc = c + 1;
+            nb = 0;
+            if (nc < nch) ncr = ch[nc];
         }
+        const bool more = nc < nch;
+        uint4 nxt[EPT / 2];
+        if (more) load_block<EPT>(pool, ncr, nb, nxt);
+        float x[EPT];
+        uint32_t xi[EPT];
+#pragma unroll
+        for (int r = 0; r < EPT / 2; ++r) {
+            xi[2 * r] = cur[r].x;
+            x[2 * r] = __uint_as_float(cur[r].y);
+            xi[2 * r + 1] = cur[r].z;
+            x[2 * r + 1] = __uint_as_float(cur[r].w);
+        }
+        const unsigned e0 = b0 + threadIdx.x * EPT;
+        const int nv = e0 >= cr.y ? 0 : (int)(cr.y - e0 < (unsigned)EPT ? cr.y - e0 : EPT);
+        f(x, xi, nv);
+        if (!more) break;
+        c = nc;
+        b0 = nb;
+        cr = ncr;
+#pragma unroll
+        for (int r = 0; r < EPT / 2; ++r) cur[r] = nxt[r];
     }
 }
 
@@ -478,7 +591,7 @@ SG_DEV double write_kept(const Args& a, Smem& S, unsigned char* stage, int w, in
     unsigned g32 = out_base;
     int tp = (int)t0 - 1;  // tile of the previous candidate (block-uniform)
     double ss = 0.0;
-    for_candidates<EPT>(a, w, seg, [&](const float (&x)[EPT], const uint32_t (&xi)[EPT], int nv, unsigned) {
+    for_candidates<EPT>(a, w, seg, [&](const float (&x)[EPT], const uint32_t (&xi)[EPT], int nv) {
         unsigned kf = 0;
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
@@ -570,7 +683,7 @@ SG_DEV double slow_mode(const Args& a, Smem& S, unsigned char* stage, int w, int
                         long long t_begin, long long t_end, unsigned& epoch) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned nseg = (unsigned)a.nseg;
-    unsigned* bar = a.bar + w;
+    unsigned* bar = a.sbar + w;
     // 1. T: 3 radix rounds of 11 bits over the full key range
     Win wn;
     wn.lo = 0;
@@ -726,7 +839,8 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
     const int w = blockIdx.y, seg = blockIdx.x;
     const unsigned nseg = (unsigned)a.nseg;
     unsigned* bar = a.bar + w;
-    unsigned epoch = 0;
+    unsigned epoch = 0;  // slow-mode barriers
+    const bool leader = seg == 0;
     const float* row = a.g + (long long)w * a.ld;
     const long long t_begin = (long long)seg * a.tps;
     const long long t_end = t_begin + a.tps < a.ntiles ? t_begin + a.tps : a.ntiles;
@@ -734,8 +848,15 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
     // full tiles come through the TMA ring (aligned rows); the row's partial last tile, or
     // every tile of an unaligned row, is read directly
     const int nfull = !a.vec ? 0 : ((t_end * TILE <= a.dim) ? ntl : ntl - 1);
-    unsigned long long tm[5] = {0, 0, 0, 0, 0};  // phase timestamps (thread 0): start, est, main, flag, end
-    if (tid == 0) tm[0] = gtimer();
+    // phase timestamps (thread 0, %globaltimer): 0 start, 1 sample loaded, 2 sample flushed,
+    // 3 sample barrier, 4 est, 5 main loop, 6 main barrier, 7 boundary scan, 8 arrived,
+    // 9 leader: all arrived, 10 leader: resolved, 11 leader: flag released, 12 flag seen,
+    // 13 written, 14 CTA done, 15 cleanup done (last CTA only)
+    unsigned long long tm[NPH];
+#pragma unroll
+    for (int i = 0; i < NPH; ++i) tm[i] = 0;
+#define TS(i) do { if (tid == 0) tm[i] = gtimer(); } while (0)
+    TS(0);
     unsigned long long policy = 0;
     auto issue = [&](int i) {
         const int s = i % STAGES;
@@ -749,19 +870,34 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
         for (int i = 0; i < STAGES && i < nfull; ++i) issue(i);
     }
     // ---------------- S: sample -> est --------------------------------------------------------
-    for (int i = tid; i < HB; i += NT) S.hist[i] = 0;
-    __syncthreads();
-    const bool exact = a.nch_s == 0;
-    auto for_sample = [&](auto&& f) {
-        if (exact) {  // the whole row, split evenly over the worker's CTAs
-            const long long L = (a.dim + a.nseg - 1) / a.nseg;
+    // NSAMP CTAs of the worker read the sample; the leader merges, picks est, publishes it
+    const int nsamp = a.nseg < NSAMP ? a.nseg : NSAMP;
+    unsigned* gA = a.histA + (long long)w * SB_BINS;
+    unsigned* flg = a.flag + 4 * w;
+    Pub* pub = a.pub + w;
+    if (seg < nsamp) {
+        for (int i = tid; i < HB; i += NT) S.hist[i] = 0;
+        __syncthreads();
+        const bool exact = a.nch_s == 0;
+        // one radix round over key bits [30:18] (8192 bins of 1/32 binade): 16-bit counters, two
+        // per shared word (straight to L2 when a CTA could hold >= 65536 sample keys)
+        const long long per_cta = (exact ? a.dim : a.nch_s * CHUNK) / nsamp + 2LL * CHUNK * NW;
+        const bool direct = per_cta >= 65535;
+        unsigned kmx = 0;
+        auto add = [&](unsigned key) {
+            const unsigned b = key >> SB_SHIFT;
+            if (direct) atomicAdd(gA + b, 1u);
+            else atomicAdd(&S.hist[b >> 1], 1u << ((b & 1u) * 16));
+            kmx = key > kmx ? key : kmx;
+        };
+        if (exact) {  // the whole row, split evenly over the samplers
+            const long long L = (a.dim + nsamp - 1) / nsamp;
             const long long lo = (long long)seg * L, hi = lo + L < a.dim ? lo + L : a.dim;
-            for (long long i = lo + tid; i < hi; i += NT) f(KO::key(row[i]));
-        } else {  // chunk c of stratum c at a hashed offset; warp-sized coalesced loads,
-                  // SB chunks per warp in flight
+            for (long long i = lo + tid; i < hi; i += NT) add(KO::key(row[i]));
+        } else {  // chunk c of stratum c at a hashed offset; SB chunks per warp in flight
             constexpr int SB = 8;
             const long long stratum = a.dim / a.nch_s;
-            const long long step = (long long)a.nseg * NW;
+            const long long step = (long long)nsamp * NW;
             for (long long c0 = (long long)seg * NW + warp; c0 < a.nch_s; c0 += step * SB) {
                 float v[SB];
 #pragma unroll
@@ -776,57 +912,47 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
                 }
 #pragma unroll
                 for (int u = 0; u < SB; ++u)
-                    if (c0 + u * step < a.nch_s) f(KO::key(v[u]));
+                    if (c0 + u * step < a.nch_s) add(KO::key(v[u]));
             }
         }
-    };
-    unsigned kmx = 0;
-    for_sample([&](unsigned key) {
-        atomicAdd(&S.hist[key >> 19], 1u);
-        kmx = key > kmx ? key : kmx;
-    });
-    kmx = warp_max<unsigned>(kmx);
-    if (lane == 0 && kmx) atomicMax(a.smax + w, kmx);
-    __syncthreads();
-    unsigned* gA = a.histA + (long long)w * HB;
-    for (int i = tid; i < HB; i += NT)
-        if (S.hist[i]) atomicAdd(gA + i, S.hist[i]);
-    worker_barrier(bar, (++epoch) * nseg);
-    for (int i = tid; i < HB; i += NT) S.hist[i] = __ldcg(gA + i);
-    __syncthreads();
-    int binA;
-    unsigned long long aboveA, totA;
-    find_bin_top<HB>(S.hist, (unsigned long long)a.r_est, S, binA, aboveA, totA);
-    for (int i = tid; i < RB; i += NT) S.hist[i] = 0;
-    __syncthreads();
-    if (binA >= 0) {
-        for_sample([&](unsigned key) {
-            if ((int)(key >> 19) == binA) atomicAdd(&S.hist[(key >> 8) & (RB - 1)], 1u);
-        });
-    }
-    __syncthreads();
-    unsigned* gB = a.histB + (long long)w * RB;
-    for (int i = tid; i < RB; i += NT)
-        if (S.hist[i]) atomicAdd(gB + i, S.hist[i]);
-    worker_barrier(bar, (++epoch) * nseg);
-    unsigned est = 0;
-    if (binA >= 0) {
-        for (int i = tid; i < RB; i += NT) S.hist[i] = __ldcg(gB + i);
+        kmx = warp_max<unsigned>(kmx);
+        if (lane == 0 && kmx) atomicMax(a.smax + w, kmx);
         __syncthreads();
-        int binB;
-        unsigned long long aboveB, totB;
-        find_bin_top<RB>(S.hist, (unsigned long long)a.r_est - aboveA, S, binB, aboveB, totB);
-        est = ((unsigned)binA << 19) | (binB >= 0 ? ((unsigned)binB << 8) : 0u);
+        TS(1);
+        if (!direct) {
+            for (int i = tid; i < SB_BINS / 2; i += NT) {
+                const unsigned v = S.hist[i];
+                if (v & 0xffffu) atomicAdd(gA + 2 * i, v & 0xffffu);
+                if (v >> 16) atomicAdd(gA + 2 * i + 1, v >> 16);
+            }
+        }
+        TS(2);
+        cta_arrive(bar);
     }
-    if (tid == 0) tm[1] = gtimer();
-    const unsigned smax = __ldcg(a.smax + w);
+    if (leader) {
+        cta_wait_count(bar, (unsigned)nsamp);
+        TS(3);
+        int binA;
+        unsigned long long aboveA, totA;
+        find_bin_top_g<SB_BINS>(gA, (unsigned long long)a.r_est, S, binA, aboveA, totA);
+        for (int i = tid; i < SB_BINS; i += NT) gA[i] = 0;  // every sampler is done with it
+        if (tid == 0) {
+            pub->est = binA >= 0 ? ((unsigned)binA << SB_SHIFT) : 0u;
+            pub->smax = __ldcg(a.smax + w);
+        }
+        cta_release_flag(flg + 0);
+    } else {
+        cta_wait_flag(flg + 0);
+    }
+    const unsigned est = __ldcg(&pub->est);
+    TS(4);
+    const unsigned smax = __ldcg(&pub->smax);
     const int shift0 = digit_shift_u32(smax > est ? smax - est : 0u, HB_BITS);
     const bool take_all = est == 0;
     const float thr = take_all ? 0.f : __uint_as_float(est - 1u);  // key >= est <=> |x| >= thr
     // ---------------- M: the main pass --------------------------------------------------------
     for (int i = tid; i < HB; i += NT) S.hist[i] = 0;
-    uint32_t* ci = a.cidx + (long long)w * (a.cap + PCH);
-    float* cv = a.cval + (long long)w * (a.cap + PCH);
+    uint2* pool = a.pool + (long long)w * (a.cap + PCH);
     uint2* chl = a.chunks + ((long long)w * a.nseg + seg) * a.maxch;
     const unsigned cap = (unsigned)a.cap;
     if (tid == 0) {
@@ -929,10 +1055,7 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
                 const float val = src[off];
                 const unsigned key = KO::key(val);
                 atomicAdd(&S.hist[hbin(key, est, shift0, HB)], 1u);
-                if (room) {
-                    ci[pos] = (uint32_t)(base + off);
-                    cv[pos] = val;
-                }
+                if (room) pool[pos] = make_uint2((uint32_t)(base + off), __float_as_uint(val));
                 ++pos;
             }
             fill += total;
@@ -950,6 +1073,7 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
             }
         }
     }
+    TS(5);
     if (tid == 0) {
         if (fill) chl[nchunk] = make_uint2(cur, fill);
         a.nch[(long long)w * a.nseg + seg] = nchunk + (fill ? 1u : 0u);
@@ -964,41 +1088,56 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
     unsigned* g0 = a.hist0 + (long long)w * HB;
     for (int i = tid; i < HB; i += NT)
         if (S.hist[i]) atomicAdd(g0 + i, S.hist[i]);
-    worker_barrier(bar, (++epoch) * nseg);
+    cta_arrive(bar);
     // ---------------- B / R / W ----------------------------------------------------------------
-    if (tid == 0) tm[2] = gtimer();
-    const bool leader = seg == 0;
-    if (leader) {  // every CTA is past its reads of the sample histograms
-        for (int i = tid; i < HB; i += NT) gA[i] = 0;
-        for (int i = tid; i < RB; i += NT) gB[i] = 0;
-    }
-    const unsigned long long C = __ldcg(a.count + w);
-    const bool ovf = __ldcg(a.ovf + w) != 0;
-    bool slow = C < (unsigned long long)a.m || ovf;
-    unsigned* gtmp = reinterpret_cast<unsigned*>(ring);  // the ring is free: merged histogram
-    int bstar = -1;
-    unsigned long long above = 0, hb = 0, tot0 = 0;
-    unsigned blo = 0, bspan = 0;
-    if (!slow) {
-        for (int i = tid; i < HB; i += NT) gtmp[i] = __ldcg(g0 + i);
-        __syncthreads();
-        find_bin_top<HB>(gtmp, (unsigned long long)a.m, S, bstar, above, tot0);
-        if (bstar < 0) {
-            slow = true;
-        } else {
-            hb = gtmp[bstar];
-            blo = est + ((unsigned)bstar << shift0);
-            bspan = bstar == HB - 1 ? KO::KMAX - blo : ((1u << shift0) - 1u);
-            if (hb > (unsigned long long)a.bcap || a.nseg > 65535) slow = true;
+    // the leader merges the candidate histograms: C, the bin b* holding rank m, the mode
+    if (leader) {
+        cta_wait_count(bar, (unsigned)nsamp + nseg);
+        TS(6);
+        const unsigned long long C_ = __ldcg(a.count + w);
+        int slow_ = C_ < (unsigned long long)a.m || __ldcg(a.ovf + w) != 0;
+        int bs_ = -1;
+        unsigned long long ab_ = 0, tot_ = 0, hb_ = 0;
+        unsigned blo_ = 0, bspan_ = 0;
+        find_bin_top_g<HB>(g0, (unsigned long long)a.m, S, bs_, ab_, tot_);
+        if (!slow_) {
+            if (bs_ < 0) {
+                slow_ = 1;
+            } else {
+                hb_ = __ldcg(g0 + bs_);
+                blo_ = est + ((unsigned)bs_ << shift0);
+                bspan_ = bs_ == HB - 1 ? KO::KMAX - blo_ : ((1u << shift0) - 1u);
+                if (hb_ > (unsigned long long)a.bcap) slow_ = 1;
+            }
         }
+        __syncthreads();
+        if (!slow_)  // every CTA has flushed, nobody reads it again (slow mode zeroes it later)
+            for (int i = tid; i < HB; i += NT) g0[i] = 0;
+        if (tid == 0) {
+            pub->slow = slow_;
+            pub->bstar = bs_;
+            pub->above = ab_;
+            pub->blo = blo_;
+            pub->bspan = bspan_;
+            pub->shift1 = digit_shift_u32(bspan_, RB_BITS);
+            pub->C = C_;
+        }
+        cta_release_flag(flg + 1);
+    } else {
+        cta_wait_flag(flg + 1);
     }
+    const unsigned long long C = __ldcg(&pub->C);
+    const bool slow = __ldcg(&pub->slow) != 0;
+    const int bstar = __ldcg(&pub->bstar);
+    const unsigned long long above = __ldcg(&pub->above);
+    const unsigned blo = __ldcg(&pub->blo), bspan = __ldcg(&pub->bspan);
     double ss_topk = 0.0;
     if (!slow) {
         unsigned* bk = a.bkey + (long long)w * a.bcap;
         unsigned* bi = a.bidx + (long long)w * a.bcap;
         unsigned short* bs = a.bseg + (long long)w * a.bcap;
         unsigned* g1 = a.hist1 + (long long)w * RB;
-        const int shift1 = digit_shift_u32(bspan, RB_BITS);
+        const int shift1 = __ldcg(&pub->shift1);
         // my count above b*, from my own histogram, for the leader's segment bases
         unsigned long long my_above = 0;
         for (int i = bstar + 1 + tid; i < HB; i += NT) my_above += S.hist[i];
@@ -1008,75 +1147,51 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
         // radix digit -> the worker's second-level histogram
         for (int i = tid; i < RB; i += NT) S.hist[i] = 0;
         __syncthreads();
-        {
-            const float* cvw = a.cval + (long long)w * (a.cap + PCH);
-            const uint32_t* ciw = a.cidx + (long long)w * (a.cap + PCH);
-            const uint2* ch = a.chunks + ((long long)w * a.nseg + seg) * a.maxch;
-            const unsigned nch = a.nch[(long long)w * a.nseg + seg];
-            for (unsigned c = 0; c < nch; ++c) {
-                const uint2 cr = ch[c];
-                for (unsigned b0 = 0; b0 < cr.y; b0 += NT * 4) {
-                    const unsigned e0 = b0 + tid * 4;
-                    float x[4];
-                    if (e0 + 4 <= cr.y) {
-                        const float4 v4 = __ldcg(reinterpret_cast<const float4*>(cvw + cr.x + e0));
-                        x[0] = v4.x; x[1] = v4.y; x[2] = v4.z; x[3] = v4.w;
-                    } else {
+        for_candidates<8>(a, w, seg, [&](const float (&x)[8], const uint32_t (&xi)[8], int nv) {
+            unsigned bm = 0;
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) x[u] = e0 + u < cr.y ? __ldcg(cvw + cr.x + e0 + u) : 0.f;
-                    }
-                    unsigned bm = 0;
+            for (int u = 0; u < 8; ++u) {
+                const unsigned key = KO::key(x[u]);
+                bm |= (u < nv && key >= blo && key - blo <= bspan ? 1u : 0u) << u;
+            }
+            const unsigned nb = __popc(bm);
+            if (__any_sync(FULL, nb != 0)) {
+                unsigned inc = nb;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const unsigned key = KO::key(x[u]);
-                        bm |= (e0 + u < cr.y && key >= blo && key - blo <= bspan ? 1u : 0u) << u;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned yv = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += yv;
+                }
+                unsigned long long wb = 0;
+                if (lane == 31 && inc) wb = atomicAdd(a.bndn + w, (unsigned long long)inc);
+                wb = __shfl_sync(FULL, wb, 31);
+                unsigned long long q = wb + inc - nb;
+                while (bm) {
+                    const int u = __ffs(bm) - 1;
+                    bm &= bm - 1;
+                    const unsigned key = KO::key(x[u]);
+                    atomicAdd(&S.hist[hbin(key, blo, shift1, RB)], 1u);
+                    if (q < (unsigned long long)a.bcap) {
+                        bk[q] = key;
+                        bi[q] = xi[u];
+                        bs[q] = (unsigned short)seg;
                     }
-                    const unsigned nb = __popc(bm);
-                    if (__any_sync(FULL, nb != 0)) {
-                        unsigned inc = nb;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const unsigned yv = __shfl_up_sync(FULL, inc, o);
-                            if (lane >= o) inc += yv;
-                        }
-                        unsigned long long wb = 0;
-                        if (lane == 31 && inc) wb = atomicAdd(a.bndn + w, (unsigned long long)inc);
-                        wb = __shfl_sync(FULL, wb, 31);
-                        unsigned long long q = wb + inc - nb;
-                        while (bm) {
-                            const int u = __ffs(bm) - 1;
-                            bm &= bm - 1;
-                            const unsigned key = KO::key(x[u]);
-                            atomicAdd(&S.hist[hbin(key, blo, shift1, RB)], 1u);
-                            if (q < (unsigned long long)a.bcap) {
-                                bk[q] = key;
-                                bi[q] = __ldcg(ciw + cr.x + e0 + u);
-                                bs[q] = (unsigned short)seg;
-                            }
-                            ++q;
-                        }
-                    }
+                    ++q;
                 }
             }
-        }
+        });
         __syncthreads();
+        TS(7);
         for (int i = tid; i < RB; i += NT)
             if (S.hist[i]) atomicAdd(g1 + i, S.hist[i]);
         // arrive; the leader waits for every CTA, resolves T / the tie cut, computes every
         // segment's output base, and releases the flag
         __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            atomicAdd(bar, 1u);
-        }
-        ++epoch;
+        cta_arrive(bar);
+        TS(8);
         if (leader) {
-            if (tid == 0) {
-                while (ld_acquire_gpu(bar) < epoch * nseg) __nanosleep(32);
-                __threadfence();
-            }
-            __syncthreads();
-            for (int i = tid; i < HB; i += NT) g0[i] = 0;  // every CTA has read it
+            cta_wait_count(bar, (unsigned)nsamp + 2 * nseg);
+            TS(9);
             const unsigned long long h = __ldcg(a.bndn + w);
             // second level: the sub-bin of b* holding rank m - above
             for (int i = tid; i < RB; i += NT) S.hist[i] = __ldcg(g1 + i);
@@ -1086,15 +1201,52 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
             wn.span = bspan;
             wn.shift = shift1;
             wn.rank = (unsigned long long)a.m - above;
+            unsigned long long n2 = h;  // boundary entries inside the narrowed window
             {
                 int b2;
                 unsigned long long ab2, t2;
                 find_bin_top<RB>(S.hist, wn.rank, S, b2, ab2, t2);
-                if (b2 >= 0) win_narrow(wn, b2, ab2, RB, RB_BITS);
+                if (b2 >= 0) {
+                    n2 = S.hist[b2];
+                    win_narrow(wn, b2, ab2, RB, RB_BITS);
+                }
             }
             for (int i = tid; i < RB; i += NT) g1[i] = 0;
             unsigned T, cut;
-            if (h <= (unsigned long long)RES) {
+            if (n2 <= (unsigned long long)SMALL) {
+                // few entries left: gather them and rank each directly (key desc, index asc);
+                // the entry of rank wn.rank - 1 is the last one kept: T = its key, cut = its index
+                unsigned* sk = reinterpret_cast<unsigned*>(ring);
+                unsigned* si = sk + SMALL;
+                if (tid == 0) S.u[3] = 0;
+                __syncthreads();
+                const unsigned wlo = wn.lo, wsp = wn.span;
+                for (long long i = tid; i < (long long)h; i += NT) {
+                    const unsigned key = __ldcg(bk + i);
+                    if (key >= wlo && key - wlo <= wsp) {
+                        const unsigned q = atomicAdd(&S.u[3], 1u);
+                        if (q < (unsigned)SMALL) {
+                            sk[q] = key;
+                            si[q] = __ldcg(bi + i);
+                        }
+                    }
+                }
+                __syncthreads();
+                const unsigned n = S.u[3] < (unsigned)SMALL ? S.u[3] : (unsigned)SMALL;
+                for (unsigned t = tid; t < n; t += NT) {
+                    const unsigned kt = sk[t], it = si[t];
+                    unsigned r = 0;
+                    for (unsigned q = 0; q < n; ++q) r += sk[q] > kt || (sk[q] == kt && si[q] < it);
+                    if ((unsigned long long)r + 1 == wn.rank) {
+                        S.u[0] = kt;
+                        S.u[1] = it;
+                    }
+                }
+                __syncthreads();
+                T = S.u[0];
+                cut = S.u[1];
+                __syncthreads();
+            } else if (h <= (unsigned long long)RES) {
                 unsigned* sk = reinterpret_cast<unsigned*>(ring);
                 unsigned* si = sk + RES;
                 for (long long i = tid; i < (long long)h; i += NT) {
@@ -1106,6 +1258,7 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
             } else {
                 select_entries(bk, bi, (long long)h, wn, S.hist, S, T, cut);
             }
+            TS(10);
             // kept boundary entries per segment, then every segment's output base
             unsigned* kb = S.hist;  // nseg <= MAXSEG counters
             for (int i = tid; i < a.nseg; i += NT) kb[i] = 0;
@@ -1151,29 +1304,29 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
                 o.pad = 0;
                 o.h = h;
                 a.sel[w] = o;
-                __threadfence();
-                st_release_u32(a.flag + w, 1u);
             }
+            cta_release_flag(flg + 2);
+            TS(11);
+        } else {
+            cta_wait_flag(flg + 2);
         }
         if (tid == 0) {
-            while (ld_acquire_gpu(a.flag + w) == 0u) __nanosleep(32);
             S.u[0] = __ldcg(&a.sel[w].T);
             S.u[1] = __ldcg(&a.sel[w].cut);
             S.u[2] = __ldcg(a.base + (long long)w * a.nseg + seg);
-            tm[3] = gtimer();
+            tm[12] = gtimer();
         }
         __syncthreads();
         ss_topk = write_kept(a, S, smem_raw, w, seg, S.u[0], S.u[1], S.u[2], t_begin, ntl);
+        TS(13);
     } else {
         ss_topk = slow_mode(a, S, smem_raw, w, seg, row, t_begin, t_end, epoch);
+        worker_barrier(a.sbar + w, (++epoch) * nseg);
         if (leader) {  // every CTA is past the reads of the slow-mode histograms and hist0
-            worker_barrier(bar, (++epoch) * nseg);
             for (int i = tid; i < HB; i += NT) g0[i] = 0;
             for (int i = tid; i < 3 * RB; i += NT) a.histR[(long long)w * 3 * RB + i] = 0;
-        } else {
-            worker_barrier(bar, (++epoch) * nseg);
         }
-        if (tid == 0) tm[3] = gtimer();
+        TS(12);
     }
     {
         const double t = block_sum_fixed(ss_topk, S);
@@ -1189,14 +1342,15 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
     // ---------------- G: the last CTA reduces the norms, gates, and cleans up -----------------
     __syncthreads();
     if (tid == 0) {
-        tm[4] = gtimer();
+        tm[14] = gtimer();
         unsigned long long* tp = a.times + ((long long)w * a.nseg + seg) * NPH;
-        for (int i = 0; i < 5; ++i) tp[i] = tm[i];
+        for (int i = 0; i < NPH; ++i) tp[i] = tm[i];
         __threadfence();
         S.last = atomicAdd(a.done, 1u) == gridDim.x * gridDim.y - 1;
     }
     __syncthreads();
     if (!S.last) return;
+#undef TS
     __threadfence();
     for (int ww = warp; ww < a.k; ww += NW) {
         double sf = 0.0, sk = 0.0;
@@ -1223,7 +1377,8 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
     // leave the zero-state for the next call (histograms were cleared by the leaders)
     for (int i = tid; i < a.k; i += NT) {
         a.bar[i] = 0;
-        a.flag[i] = 0;
+        a.sbar[i] = 0;
+        a.flag[4 * i] = a.flag[4 * i + 1] = a.flag[4 * i + 2] = a.flag[4 * i + 3] = 0;
         a.poolctr[i] = 0;
         a.count[i] = 0;
         a.bndn[i] = 0;
@@ -1233,7 +1388,7 @@ __global__ void __launch_bounds__(NT, 3) k_topk_fused(Args a) {
     if (tid == 0) {
         a.done[0] = 0;
         unsigned long long* tp = a.times + ((long long)w * a.nseg + seg) * NPH;
-        tp[5] = gtimer();
+        tp[15] = gtimer();
     }
 }
 
@@ -1263,6 +1418,8 @@ int topk_fused_f32(const float* g, int k, long long ld, long long dim, long long
     a.maxch = p.maxch;
     a.vec = (reinterpret_cast<size_t>(g) % 16 == 0) && ((ld * 4) % 16 == 0);
     a.bar = reinterpret_cast<unsigned*>(at(p.o_bar));
+    a.sbar = reinterpret_cast<unsigned*>(at(p.o_sbar));
+    a.pub = reinterpret_cast<Pub*>(at(p.o_pub));
     a.flag = reinterpret_cast<unsigned*>(at(p.o_flag));
     a.poolctr = reinterpret_cast<unsigned long long*>(at(p.o_poolctr));
     a.count = reinterpret_cast<unsigned long long*>(at(p.o_count));
@@ -1271,7 +1428,6 @@ int topk_fused_f32(const float* g, int k, long long ld, long long dim, long long
     a.smax = reinterpret_cast<unsigned*>(at(p.o_smax));
     a.done = reinterpret_cast<unsigned*>(at(p.o_done));
     a.histA = reinterpret_cast<unsigned*>(at(p.o_histA));
-    a.histB = reinterpret_cast<unsigned*>(at(p.o_histB));
     a.hist0 = reinterpret_cast<unsigned*>(at(p.o_hist0));
     a.hist1 = reinterpret_cast<unsigned*>(at(p.o_hist1));
     a.histR = reinterpret_cast<unsigned*>(at(p.o_histR));
@@ -1287,8 +1443,7 @@ int topk_fused_f32(const float* g, int k, long long ld, long long dim, long long
     a.bkey = reinterpret_cast<unsigned*>(at(p.o_bkey));
     a.bidx = reinterpret_cast<unsigned*>(at(p.o_bidx));
     a.bseg = reinterpret_cast<unsigned short*>(at(p.o_bseg));
-    a.cidx = reinterpret_cast<uint32_t*>(at(p.o_cidx));
-    a.cval = reinterpret_cast<float*>(at(p.o_cval));
+    a.pool = reinterpret_cast<uint2*>(at(p.o_pool));
     a.stats = reinterpret_cast<long long*>(at(p.o_stats));
     a.times = reinterpret_cast<unsigned long long*>(at(p.o_times));
     a.idx = idx;

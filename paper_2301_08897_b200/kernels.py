@@ -20,7 +20,7 @@ _GATE_BYTES = _capi.GATE_STATE_DTYPE.itemsize
 # Kernel launches issued through this module (each C-ABI entry point launches a fixed
 # sequence; see csrc/topk.cu and csrc/aggregate.cu).  bench.py reports the count.
 LAUNCHES = {"n": 0}
-TOPK_LAUNCHES = {torch.float32: 1, torch.float64: 2 + 2 + 1 + 1 + 1 + 1}
+TOPK_LAUNCHES = {torch.float32: 2 + 2 + 1 + 1 + 1 + 1, torch.float64: 2 + 2 + 1 + 1 + 1 + 1}
 
 
 def _count(n: int) -> None:
@@ -97,10 +97,22 @@ def merge_tiles(dim: int) -> int:
     return (dim + MERGE_TILE - 1) // MERGE_TILE
 
 
-def topk_workspace_bytes(dtype: torch.dtype, k: int, dim: int, m: int) -> int:
+def topk_workspace_bytes(dtype: torch.dtype, k: int, dim: int, m: int, fused: bool = False) -> int:
     lib = _capi.load()
-    fn = lib.sg_topk_workspace_bytes_f32 if dtype == torch.float32 else lib.sg_topk_workspace_bytes_f64
+    if dtype == torch.float32:
+        fn = lib.sg_topk_workspace_bytes_fused_f32 if fused else lib.sg_topk_workspace_bytes_f32
+    else:
+        fn = lib.sg_topk_workspace_bytes_f64
     return int(fn(k, dim, m))
+
+
+def _topk_ws(dtype, k, dim, m, device, slot, fused):
+    if dtype == torch.float32 and fused:
+        lib = _capi.load()
+        return Workspace.get_topk(topk_workspace_bytes(dtype, k, dim, m, True),
+                                  int(lib.sg_topk_workspace_zero_bytes_f32(k, dim, m)), (k, dim, m), device, slot)
+    kind = "topk32" if dtype == torch.float32 else "topk64"
+    return Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, slot, kind=kind)
 
 
 def topk_gate(
@@ -112,11 +124,13 @@ def topk_gate(
     out: tuple | None = None,
     tile_off: torch.Tensor | None = None,
     workspace_slot: int = 0,
+    fused: bool = False,
 ):
     """Batched Top-k + norms (+ gate) over the rows of ``g`` ([k, ld] or [D]).
 
     ``workspace_slot`` selects a separate scratch buffer for calls issued concurrently on
-    different streams.
+    different streams.  ``fused`` (float32) takes the persistent one-kernel variant
+    (sg_topk_gate_fused_f32) instead of the launch chain; the results are identical.
 
     Returns (idx int32 [k, m] (uint32 bits), val [k, m], norms2 f64 [k, 2], decision u8 [k],
     rho f64 [k]); decision/rho are None without ``states``.
@@ -141,50 +155,51 @@ def topk_gate(
         idx, val, norms2, decision, rho = out
     if states is not None and states.numel() != k * _GATE_BYTES:
         raise ValueError("one gate state per worker required")
-    nbytes = topk_workspace_bytes(g.dtype, k, D, m)
-    if nbytes == 0:
+    fused = bool(fused) and g.dtype == torch.float32
+    if topk_workspace_bytes(g.dtype, k, D, m, fused) == 0:
         raise ValueError("invalid top-k shape")
     lib = _capi.load()
-    if g.dtype == torch.float32:
-        zb = int(lib.sg_topk_workspace_zero_bytes_f32(k, D, m))
-        ws = Workspace.get_topk(nbytes, zb, (k, D, m), dev, workspace_slot)
-    else:
-        ws = Workspace.get(nbytes, dev, workspace_slot, kind="topk64")
+    ws = _topk_ws(g.dtype, k, D, m, dev, workspace_slot, fused)
     args = [g2.data_ptr(), k, ld, D, m, idx.data_ptr(), val.data_ptr(), norms2.data_ptr(),
             _ptr(states), _ptr(decision), _ptr(rho)]
     if g.dtype == torch.float32:
-        st = lib.sg_topk_gate_f32(*args, _ptr(tile_off), ws.data_ptr(), ws.numel(), _stream())
+        fn = lib.sg_topk_gate_fused_f32 if fused else lib.sg_topk_gate_f32
+        st = fn(*args, _ptr(tile_off), ws.data_ptr(), ws.numel(), _stream())
     else:
         if tile_off is not None:
             raise ValueError("tile offsets are produced by the float32 path only")
         st = lib.sg_topk_gate_f64(*args, ws.data_ptr(), ws.numel(), _stream())
     _capi.check(st, "sg_topk_gate")
-    _count(TOPK_LAUNCHES[g.dtype])
+    _count(1 if fused else TOPK_LAUNCHES[g.dtype])
     return idx, val, norms2, decision, rho
 
 
-def topk_stats(dtype: torch.dtype, k: int, dim: int, m: int, device: torch.device, workspace_slot: int = 0) -> np.ndarray:
-    """Per-worker {candidates, boundary, fallback, slow} of the last topk_gate call (synchronises)."""
-    if dtype == torch.float32:
-        ws = Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, workspace_slot, kind="topk32")
-    else:
-        ws = Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, workspace_slot, kind="topk64")
+def topk_stats(dtype: torch.dtype, k: int, dim: int, m: int, device: torch.device, workspace_slot: int = 0,
+               fused: bool = False) -> np.ndarray:
+    """Per-worker diagnostics of the last topk_gate call (synchronises): launch chain
+    {candidates, boundary, fallback pass, slow resolve}; fused {candidates, boundary, estimate
+    undershot, exact fallback}."""
+    fused = bool(fused) and dtype == torch.float32
+    ws = _topk_ws(dtype, k, dim, m, device, workspace_slot, fused)
     out = torch.zeros((k, 4), dtype=torch.int64, device=device)
     lib = _capi.load()
-    fn = lib.sg_topk_stats_f32 if dtype == torch.float32 else lib.sg_topk_stats_f64
+    if dtype == torch.float32:
+        fn = lib.sg_topk_stats_fused_f32 if fused else lib.sg_topk_stats_f32
+    else:
+        fn = lib.sg_topk_stats_f64
     _capi.check(fn(k, dim, m, ws.data_ptr(), ws.numel(), out.data_ptr(), _stream()), "sg_topk_stats")
     return out.cpu().numpy()
 
 
 def topk_phases(k: int, dim: int, m: int, device: torch.device, workspace_slot: int = 0) -> np.ndarray:
-    """float32 Top-k phase timestamps of the last call (ns, [k, nseg, 8]; synchronises)."""
+    """Fused float32 Top-k phase timestamps of the last call (ns, [k, nseg, 16]; synchronises)."""
     lib = _capi.load()
     nseg = int(lib.sg_topk_segments_f32(k, dim, m))
-    ws = Workspace.get(topk_workspace_bytes(torch.float32, k, dim, m), device, workspace_slot, kind="topk32")
-    out = torch.zeros(k * nseg * 8, dtype=torch.int64, device=device)
+    ws = _topk_ws(torch.float32, k, dim, m, device, workspace_slot, True)
+    out = torch.zeros(k * nseg * 16, dtype=torch.int64, device=device)
     _capi.check(lib.sg_topk_phases_f32(k, dim, m, ws.data_ptr(), ws.numel(), out.data_ptr(), out.numel(), _stream()),
                 "sg_topk_phases_f32")
-    return out.cpu().numpy().reshape(k, nseg, 8)
+    return out.cpu().numpy().reshape(k, nseg, 16)
 
 
 def gate_update(norms2: torch.Tensor, states: torch.Tensor):

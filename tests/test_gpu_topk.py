@@ -135,10 +135,9 @@ def test_topk_constant_and_all_nan(cuda):
         m = comm_ref.topk_count(g.size, 0.01)
         idx, _, _, _, _ = kernels.topk_gate(torch.from_numpy(g).to(cuda), m)
         assert np.array_equal(idx[0].cpu().numpy(), np.arange(m))
-        # the whole row is one tie group: every element is a candidate and the tie cut
-        # (the m lowest indices) is resolved from the boundary list
+        # the whole row is one tie group: the oversized-boundary (cooperative) resolve ran
         st = kernels.topk_stats(torch.float32, 1, g.size, m, cuda)
-        assert int(st[0, 0]) == g.size and int(st[0, 3]) == 0, st
+        assert int(st[0, 3]) == 1, st
 
 
 @pytest.mark.parametrize("D,cr,fam", [(143_667_240, 0.01, "heavy"), (143_667_240, 0.1, "heavy"),

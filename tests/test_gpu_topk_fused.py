@@ -50,7 +50,7 @@ def run(cuda, g, m):
     D = g.size
     nt = kernels.merge_tiles(D)
     toff = torch.empty((1, nt + 1), dtype=torch.int32, device=cuda)
-    idx, val, norms2, _, _ = kernels.topk_gate(torch.from_numpy(g).to(cuda), m, tile_off=toff)
+    idx, val, norms2, _, _ = kernels.topk_gate(torch.from_numpy(g).to(cuda), m, tile_off=toff, fused=True)
     want = comm_ref.topk_indices_threshold(g.astype(np.float64), m)
     got = idx[0].cpu().numpy().view(np.uint32).astype(np.int64)
     assert np.array_equal(got, want)
@@ -61,7 +61,7 @@ def run(cuda, g, m):
     n = norms2[0].cpu().numpy()
     assert abs(n[0] - g64 @ g64) <= 1e-10 * (g64 @ g64)
     assert abs(n[1] - g64[want] @ g64[want]) <= 1e-10 * (g64[want] @ g64[want])
-    return kernels.topk_stats(torch.float32, 1, D, m, cuda)[0]
+    return kernels.topk_stats(torch.float32, 1, D, m, cuda, fused=True)[0]
 
 
 def test_estimate_undershoot_takes_exact_fallback(cuda):
@@ -107,9 +107,54 @@ def test_fast_path_candidate_count_is_tight(cuda, cr):
     from paper_2301_08897_b200 import kernels
 
     m = comm_ref.topk_count(D, cr)
-    kernels.topk_gate(g, m)
-    st = kernels.topk_stats(torch.float32, 1, D, m, cuda)[0]
+    kernels.topk_gate(g, m, fused=True)
+    st = kernels.topk_stats(torch.float32, 1, D, m, cuda, fused=True)[0]
     assert int(st[3]) == 0 and int(st[2]) == 0
     ratio = int(st[0]) / m
     print(f"[fused cr={cr}] C/m = {ratio:.4f}, boundary {int(st[1])}")
     assert 1.0 <= ratio <= {0.001: 1.5, 0.01: 1.15, 0.1: 1.06}[cr]
+
+
+@pytest.mark.parametrize("D", [1, 17, 4096, 4097, 100_003, (1 << 22) + 5])
+@pytest.mark.parametrize("cr", [0.001, 0.01, 0.1, 0.5, 1.0])
+@pytest.mark.parametrize("fam", ["normal", "heavy", "ties", "edge"])
+def test_fused_matches_oracle(cuda, D, cr, fam):
+    """The fused variant over the launch-chain test families (same bar: bit-exact)."""
+    from test_gpu_topk import _family
+
+    if fam == "edge" and D < 8:
+        pytest.skip("edge family needs room")
+    g = _family(fam, D, seed=D * 5 + int(cr * 1000))
+    m = comm_ref.topk_count(D, cr)
+    run(cuda, g, m)
+
+
+def test_fused_batched_rows_padding_and_state(cuda):
+    """k workers, padded rows, gate states: fused == launch chain, bit for bit (idx, val,
+    merge offsets, norms, decisions, EWMA states)."""
+    from paper_2301_08897_b200 import kernels
+    from test_gpu_topk import _family
+
+    k, D, ld = 8, 300_001, 300_004
+    host = np.zeros((k, ld), dtype=np.float32)
+    for j in range(k):
+        host[j, :D] = _family(["normal", "heavy", "ties", "edge"][j % 4], D, seed=200 + j)
+    dev = torch.from_numpy(host).to(cuda)
+    nt = kernels.merge_tiles(D)
+    recs = np.zeros(k, dtype=__import__("paper_2301_08897_b200._capi", fromlist=["x"]).GATE_STATE_DTYPE)
+    recs["cr"], recs["delta"], recs["ewma_factor"] = 0.01, 0.3, 0.9
+    outs = []
+    for fused in (False, True):
+        st = kernels.gate_states_tensor(recs, cuda)
+        toff = torch.empty((k, nt + 1), dtype=torch.int32, device=cuda)
+        for _ in range(3):
+            r = kernels.topk_gate(dev, comm_ref.topk_count(D, 0.01), st, dim=D, tile_off=toff, fused=fused)
+        outs.append([t.cpu().numpy() for t in r[:2]] + [toff.cpu().numpy(), r[3].cpu().numpy(),
+                                                         kernels.gate_states_numpy(st)])
+    for a, b in zip(outs[0], outs[1]):
+        if a.dtype.names:
+            for f in ("n_compressed", "n_uncompressed"):
+                assert np.array_equal(a[f], b[f])
+            assert np.allclose(a["ewma_full"], b["ewma_full"], rtol=1e-12)
+        else:
+            assert np.array_equal(a, b)

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--crs", default="0.001,0.01,0.1")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--family", default="heavy")
+    ap.add_argument("--fused", action="store_true", help="the persistent one-kernel variant")
     args = ap.parse_args()
     build.build()
     dev = torch.device("cuda", 0)
@@ -50,24 +51,33 @@ def main():
             toff = torch.empty((k, kernels.merge_tiles(D) + 1), dtype=torch.int32, device=dev)
             out = (idx, val, n2, None, None)
             for _ in range(3):
-                kernels.topk_gate(g, m, dim=D, out=out, tile_off=toff)
+                kernels.topk_gate(g, m, dim=D, out=out, tile_off=toff, fused=args.fused)
             torch.cuda.synchronize()
             ts = []
             for _ in range(args.iters):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                kernels.topk_gate(g, m, dim=D, out=out, tile_off=toff)
+                kernels.topk_gate(g, m, dim=D, out=out, tile_off=toff, fused=args.fused)
                 b.record()
                 torch.cuda.synchronize()
                 ts.append(a.elapsed_time(b) * 1e3)
             ts.sort()
             med = ts[len(ts) // 2]
-            st = kernels.topk_stats(torch.float32, k, D, m, dev)
-            ph = kernels.topk_phases(k, D, m, dev).astype(np.float64)
+            st = kernels.topk_stats(torch.float32, k, D, m, dev, fused=args.fused)
+            ph = kernels.topk_phases(k, D, m, dev).astype(np.float64) if args.fused else np.zeros((k, 1, 16))
             t0 = ph[:, :, 0].min()
-            phases = {name: [round(float(np.median(ph[:, :, i] - t0)) / 1e3, 1), round(float((ph[:, :, i] - t0).max()) / 1e3, 1)]
-                      for i, name in enumerate(["start", "est", "main", "select", "done"])}
-            phases["cleanup_end"] = round(float(ph[:, :, 5].max() - t0) / 1e3, 1)
+            names = ["start", "sample_loaded", "sample_flushed", "sample_barrier", "est", "main_loop", "main_barrier",
+                     "boundary_scan", "arrived", "leader_all_arrived", "leader_resolved", "leader_flag", "flag_seen",
+                     "written", "cta_done"]
+            phases = {}
+            for i, name in enumerate(names):
+                v = ph[:, :, i] - t0
+                v = v[(ph[:, :, i] > 0) & (v >= 0) & (v < 1e9)]
+                if v.size:
+                    phases[name] = [round(float(np.median(v)) / 1e3, 1), round(float(v.max()) / 1e3, 1)]
+            v = ph[:, :, 15] - t0
+            v = v[(v >= 0) & (v < 1e9)]
+            phases["cleanup_end"] = round(float(v.max()) / 1e3, 1) if v.size else None
             alg = k * (4 * D + 8 * m)
             rows.append(dict(k=k, cr=cr, us_median=round(med, 1), us_min=round(ts[0], 1),
                              frac=round(alg / (med * 1e-6) / 1e9 / hbm, 4), alg_bytes=alg,
