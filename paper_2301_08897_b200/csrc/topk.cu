@@ -44,7 +44,7 @@ constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
-constexpr int EST_G = 16;        // sampling CTAs per worker (k_sample)
+constexpr int EST_G = 64;        // sampling CTAs per worker (k_sample)
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
 constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
@@ -56,12 +56,14 @@ enum { WR_FAST = 0, WR_SLOW = 1 };
 
 template <typename T> struct TopkTraits;
 template <> struct TopkTraits<float> {
-    static constexpr int SAMPLE = 16384;
+    static constexpr int SAMPLE = 131072;
+    static constexpr double Z = 4.0;      // sigmas of binomial slack (undershoot ~3e-5 per call)
     static constexpr int ROUNDS_MAX = 3;  // after round 0: <= 31 bits left (open top bin)
     static constexpr int RES = 15360;     // boundary entries resolved inside one CTA
 };
 template <> struct TopkTraits<double> {
     static constexpr int SAMPLE = 8192;
+    static constexpr double Z = 6.0;
     static constexpr int ROUNDS_MAX = 6;  // after round 0: <= 63 bits left (open top bin)
     static constexpr int RES = 8192;
 };
@@ -86,7 +88,8 @@ template <typename K> struct SelState {
 // --------------------------------------------------------------------------------------
 struct TopkPlan {
     int k, nseg, tps;  // segments per worker, tiles per segment
-    int split, nsub;   // CTAs per segment in the collect/write passes, nseg * split
+    int split, nsub;   // (unused) / collect-write grid per worker (>= Σ parts)
+    int nsubt;         // target sub-range count apportioned over the segments by candidates
     long long dim, m;
     long long s_eff, stride, r_est;
     long long ntiles, segcap;
@@ -111,7 +114,7 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
         const double q = (double)m / (double)dim;
         const double mean = q * (double)p.s_eff;
         const double sd = __builtin_sqrt(mean * (1.0 - q) + 1.0);
-        p.r_est = (long long)(mean + 6.0 * sd + 8.0) + 1;
+        p.r_est = (long long)(mean + TopkTraits<T>::Z * sd + 4.0) + 1;
     }
     const long long te = tile_elems<T>();
     p.ntiles = (dim + te - 1) / te;
@@ -124,11 +127,16 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     {
         // collect/write: about one wave of CTAs (cta_target) over all sub-ranges, each CTA
         // streaming its sub-range with the next chunk's loads in flight
-        long long want = cta_target / ((long long)p.nseg * k);
-        const long long cap = NSUB_MAX / p.nseg;
-        if (want > cap) want = cap;
-        p.split = want < 1 ? 1 : (int)want;
-        p.nsub = p.nseg * p.split;  // <= max(nseg, NSUB_MAX) = NSUB_MAX
+        // sub-ranges are apportioned to segments by candidate count on the device (adaptive
+        // split: concentrated real gradients put most candidates in a few segments), so the
+        // grid is the target plus one per segment (every segment gets at least one)
+        long long want = cta_target / k;
+        if (want > NSUB_MAX - p.nseg) want = NSUB_MAX - p.nseg;
+        if (want < p.nseg) want = p.nseg;
+        p.nsubt = (int)want;
+        p.nsub = p.nsubt + p.nseg;
+        if (p.nsub > NSUB_MAX) p.nsub = NSUB_MAX;
+        p.split = 0;
     }
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
@@ -931,9 +939,51 @@ SG_DEV int sub_of(long long n, long long off, int split) {
     return i;
 }
 
+// Adaptive split: segment s of a worker gets parts_s = max(1, ceil(n_s * nsubt / C)) sub-ranges
+// (C = the worker's candidates), so the collect/write CTAs are balanced by candidate count, not
+// by position; sub-ranges are numbered in index order (segment, then part).
+SG_DEV unsigned parts_of(unsigned n, unsigned long long C, int nsubt) {
+    if (C == 0) return 1u;
+    const unsigned long long q = ((unsigned long long)n * (unsigned long long)nsubt + C - 1) / C;
+    return q < 1 ? 1u : (unsigned)q;
+}
+
+// Warp-cooperative (all 32 lanes): sub-range `sub` -> (segment, part, parts of that segment);
+// seg = -1 beyond the worker's last sub-range.
+SG_DEV void map_sub(const unsigned* segcnt, int nseg, int nsubt, int sub, int& seg, int& part, int& split) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long C = 0;
+    for (int i = lane; i < nseg; i += 32) C += segcnt[i];
+    for (int o = 16; o > 0; o >>= 1) C += __shfl_xor_sync(FULL, C, o);
+    seg = -1;
+    part = 0;
+    split = 1;
+    unsigned run = 0;
+    for (int b = 0; b < nseg; b += 32) {
+        const int si = b + lane;
+        const unsigned ps = si < nseg ? parts_of(segcnt[si], C, nsubt) : 0u;
+        unsigned incl = ps;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const unsigned hit = __ballot_sync(FULL, si < nseg && run + incl > (unsigned)sub);
+        if (hit) {
+            const int f = __ffs(hit) - 1;
+            const unsigned ex = __shfl_sync(FULL, incl - ps, f);
+            seg = b + f;
+            part = sub - (int)(run + ex);
+            split = (int)__shfl_sync(FULL, ps, f);
+            return;
+        }
+        run += __shfl_sync(FULL, incl, 31);
+    }
+}
+
 template <typename T> struct CollectArgs {
     long long segcap, cap;         // cap: boundary entries stored per worker (RES)
-    int nseg, tps, split, nsub;
+    int nseg, tps, split, nsub, nsubt;
     uint32_t* bpos;                // [k][cap] boundary entry's position in its segment list
     SelState<typename KeyOf<T>::K>* sel;
     const unsigned* segcnt;
@@ -993,13 +1043,29 @@ k_collect(CollectArgs<T> a) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
     __shared__ unsigned s_gt[TK_NW];
+    __shared__ int s_map[3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int w = blockIdx.y, sub = blockIdx.x, seg = sub / a.split, part = sub % a.split;
+    const int w = blockIdx.y, sub = blockIdx.x;
+    if (warp == 0) {
+        int sg_, pt_, sp_;
+        map_sub(a.segcnt + (long long)w * a.nseg, a.nseg, a.nsubt, sub, sg_, pt_, sp_);
+        if (lane == 0) {
+            s_map[0] = sg_;
+            s_map[1] = pt_;
+            s_map[2] = sp_;
+        }
+    }
+    __syncthreads();
+    const int seg = s_map[0], part = s_map[1], split = s_map[2];
+    if (seg < 0) {  // beyond the worker's sub-ranges
+        if (tid == 0) a.seggt[(long long)w * a.nsub + sub] = 0;
+        return;
+    }
     const SelState<K> st = a.sel[w];
     const K lo = st.lo, span = st.span;
     const long long nseg_c = a.segcnt[(long long)w * a.nseg + seg];
-    const int lo32 = (int)sub_lo(nseg_c, part, a.split);
-    const int hi32 = (int)(part + 1 == a.split ? nseg_c : sub_lo(nseg_c, part + 1, a.split));
+    const int lo32 = (int)sub_lo(nseg_c, part, split);
+    const int hi32 = (int)(part + 1 == split ? nseg_c : sub_lo(nseg_c, part + 1, split));
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     K* bk = a.bkey + (long long)w * a.cap;
@@ -1084,7 +1150,8 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
     uint32_t* sp = si + RES;                               // position in the segment list
     unsigned* kb = sp + RES;                               // [nsub]
     unsigned* sc = kb + NSUB_MAX;                          // [nseg] segment candidate counts
-    uint8_t* sf = reinterpret_cast<uint8_t*>(sc + BMAX);
+    unsigned* pp = sc + BMAX;                              // [nseg + 1] sub-range prefix (adaptive split)
+    uint8_t* sf = reinterpret_cast<uint8_t*>(pp + BMAX + 1);
     const K* bk = a.bkey + (long long)w * a.cap;
     const uint32_t* bi = a.bidx + (long long)w * a.cap;
     const uint32_t* bpp = a.bpos + (long long)w * a.cap;
@@ -1098,6 +1165,17 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
     if (tid == 0) {
         sst = a.sel[w];
         s_eq = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {  // parts per segment -> prefix (same apportioning as map_sub)
+        unsigned long long C = 0;
+        for (int i = 0; i < a.nseg; ++i) C += sc[i];
+        unsigned run = 0;
+        for (int i = 0; i < a.nseg; ++i) {
+            pp[i] = run;
+            run += parts_of(sc[i], C, a.nsubt);
+        }
+        pp[a.nseg] = run;
     }
     SG_PH();
     block_select<K, NT>(sk, (long long)h, sst, hist);
@@ -1144,7 +1222,7 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
         const K key = sk[i];
         if (key > T_ || (key == T_ && si[i] <= cut)) {
             const int seg = (int)((si[i] / TILE) / a.tps);
-            atomicAdd(&kb[seg * a.split + sub_of((long long)sc[seg], sp[i], a.split)], 1u);
+            atomicAdd(&kb[pp[seg] + sub_of((long long)sc[seg], sp[i], (int)(pp[seg + 1] - pp[seg]))], 1u);
         }
     }
     __syncthreads();
@@ -1312,7 +1390,7 @@ k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
 // --------------------------------------------------------------------------------------
 template <typename T> struct WriteArgs {
     long long ntiles, segcap, m;
-    int k, nseg, tps, split, nsub;
+    int k, nseg, tps, split, nsub, nsubt;
     const SelState<typename KeyOf<T>::K>* sel;
     const unsigned* tstart;
     const unsigned* segcnt;
@@ -1375,41 +1453,6 @@ SG_DEV void write_tail(const WriteArgs<T>& a, double ss) {
     }
 }
 
-// After k_write: fixed-order reductions of the per-segment / per-sub-range partial norms and
-// the gate (comm.py:129-160), one CTA.
-template <typename T>
-__global__ void __launch_bounds__(TK_THREADS) k_finish(WriteArgs<T> a) {
-    pdl_enter();
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // all partials in one parallel round trip, then fixed-order sums from shared memory
-    extern __shared__ __align__(16) unsigned char fin_smem[];
-    double* pm = reinterpret_cast<double*>(fin_smem);  // [k][nseg]
-    double* pw = pm + (size_t)a.k * a.nseg;            // [k][nsub]
-    for (int i = tid; i < a.k * a.nseg; i += TK_THREADS) pm[i] = __ldcg(a.pmain + i);
-    for (int i = tid; i < a.k * a.nsub; i += TK_THREADS) pw[i] = __ldcg(a.pwrite + i);
-    __syncthreads();
-    for (int ww = warp; ww < a.k; ww += TK_NW) {
-        double sf = 0.0, sk = 0.0;
-        for (int i = lane; i < a.nseg; i += 32) sf = dadd(sf, pm[(long long)ww * a.nseg + i]);
-        for (int i = lane; i < a.nsub; i += 32) sk = dadd(sk, pw[(long long)ww * a.nsub + i]);
-        sf = warp_sum(sf);
-        sk = warp_sum(sk);
-        if (lane == 0) {
-            a.norms2[2 * ww] = sf;
-            a.norms2[2 * ww + 1] = sk;
-            if (a.states) {
-                sg_gate_state s = a.states[ww];
-                uint8_t d;
-                double r;
-                gate_math(s, sf, sk, d, r);
-                a.states[ww] = s;
-                if (a.decision) a.decision[ww] = d;
-                if (a.rho) a.rho[ww] = r;
-            }
-        }
-    }
-}
-
 // Fast-mode write (T and the tie cut are final).  The CTA streams its sub-range in chunks of
 // WF_SPAN entries, thread t owning WF_EPT consecutive entries, with the next chunk's loads in
 // flight while the current one is processed: one block scan of the kept counts gives every
@@ -1421,17 +1464,18 @@ constexpr int WF_SPAN = TK_THREADS * WF_EPT;  // 1024 entries per chunk
 
 template <typename T>
 SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
-                         typename KeyOf<T>::K T_, unsigned cut, unsigned char* stage) {
+                         typename KeyOf<T>::K T_, unsigned cut, unsigned char* stage, int seg_, int part_,
+                         int split_) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
     __shared__ unsigned s_wt[TK_NW];
     __shared__ uint32_t s_wl[TK_NW];  // last candidate index of each warp's run in the chunk
     __shared__ uint32_t s_carry;      // last candidate index before the chunk
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int w = blockIdx.y, sub = blockIdx.x, seg = sub / a.split, part = sub % a.split;
+    const int w = blockIdx.y, sub = blockIdx.x, seg = seg_, part = part_, split = split_;
     const long long nsc = a.segcnt[(long long)w * a.nseg + seg];
-    const int lo32 = (int)sub_lo(nsc, part, a.split);
-    const int n32 = (int)(part + 1 == a.split ? nsc : sub_lo(nsc, part + 1, a.split));
+    const int lo32 = (int)sub_lo(nsc, part, split);
+    const int n32 = (int)(part + 1 == split ? nsc : sub_lo(nsc, part + 1, split));
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     uint32_t* oi = a.idx + (long long)w * a.m;
@@ -1525,7 +1569,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
         g32 += tot;
         __syncthreads();  // s_wt, s_wl and the staging are reused
     }
-    if (toff && part + 1 == a.split) {
+    if (toff && part + 1 == split) {
         // tiles after the segment's last candidate (to the segment end): offset = kept total
         const int tl = nsc > 0 ? (int)(ci[nsc - 1] >> MERGE_SHIFT) : (int)t0 - 1;
         for (int t = tl + 1 + tid; t < (int)(t0 + nt); t += TK_THREADS) toff[t] = (int)g32;
@@ -1535,9 +1579,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
 }
 
 template <typename T>
-__global__ void __launch_bounds__(TK_THREADS, CW_PER_SM)
-k_write(WriteArgs<T> a) {
-    pdl_enter();
+SG_DEV void write_body(const WriteArgs<T>& a) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
     constexpr int TILE = tile_elems<T>();
@@ -1546,17 +1588,33 @@ k_write(WriteArgs<T> a) {
     __shared__ unsigned long long s_gb, s_eb;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned* s_ts = reinterpret_cast<unsigned*>(smem_raw);  // [tps] tile starts of this segment
+    __shared__ int s_map[3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int w = blockIdx.y, sub = blockIdx.x, seg = sub / a.split, part = sub % a.split;
+    const int w = blockIdx.y, sub = blockIdx.x;
+    if (warp == 0) {
+        int sg_, pt_, sp_;
+        map_sub(a.segcnt + (long long)w * a.nseg, a.nseg, a.nsubt, sub, sg_, pt_, sp_);
+        if (lane == 0) {
+            s_map[0] = sg_;
+            s_map[1] = pt_;
+            s_map[2] = sp_;
+        }
+    }
+    __syncthreads();
+    const int seg = s_map[0], part = s_map[1], split = s_map[2];
+    if (seg < 0) {  // beyond the worker's sub-ranges: no kept entries, no norm
+        if (tid == 0) a.pwrite[(long long)w * a.nsub + sub] = 0.0;
+        return;
+    }
     const SelState<K> st = a.sel[w];
     const K T_ = st.T;
     const unsigned cut = st.idx_cut;
     const unsigned long long need = st.rank;
     const bool slow = st.wmode == WR_SLOW;
     const long long nsc = a.segcnt[(long long)w * a.nseg + seg];
-    const long long i_lo = sub_lo(nsc, part, a.split);
-    const long long n = part + 1 == a.split ? nsc : sub_lo(nsc, part + 1, a.split);  // end of the sub-range
-    const bool last_part = part + 1 == a.split;
+    const long long i_lo = sub_lo(nsc, part, split);
+    const long long n = part + 1 == split ? nsc : sub_lo(nsc, part + 1, split);  // end of the sub-range
+    const bool last_part = part + 1 == split;
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     const long long t0 = (long long)seg * a.tps;
@@ -1565,7 +1623,7 @@ k_write(WriteArgs<T> a) {
 
     if (!slow) {
         write_tail<T>(a, write_fast<T>(a, nt, t0, toff, T_, cut,
-                                       smem_raw + align_up(sizeof(unsigned) * (size_t)a.tps, 16)));
+                                       smem_raw + align_up(sizeof(unsigned) * (size_t)a.tps, 16), seg, part, split));
         return;
     }
     if (toff) {
@@ -1724,6 +1782,46 @@ k_write(WriteArgs<T> a) {
         if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }
     write_tail<T>(a, ss);
+}
+
+// k_write: the ordered compaction of every sub-range, then -- in the last CTA to finish --
+// the fixed-order norm reductions and the gate (comm.py:129-160), formerly a separate
+// one-CTA launch.
+template <typename T>
+__global__ void __launch_bounds__(TK_THREADS, CW_PER_SM)
+k_write(WriteArgs<T> a) {
+    pdl_enter();
+    write_body<T>(a);
+    __shared__ int s_lastw;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        s_lastw = atomicAdd(a.done, 1u) == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (!s_lastw) return;
+    __threadfence();
+    for (int ww = warp; ww < a.k; ww += TK_NW) {
+        double sf = 0.0, sk = 0.0;
+        for (int i = lane; i < a.nseg; i += 32) sf = dadd(sf, __ldcg(a.pmain + (long long)ww * a.nseg + i));
+        for (int i = lane; i < a.nsub; i += 32) sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nsub + i));
+        sf = warp_sum(sf);
+        sk = warp_sum(sk);
+        if (lane == 0) {
+            a.norms2[2 * ww] = sf;
+            a.norms2[2 * ww + 1] = sk;
+            if (a.states) {
+                sg_gate_state st = a.states[ww];
+                uint8_t d;
+                double r;
+                gate_math(st, sf, sk, d, r);
+                a.states[ww] = st;
+                if (a.decision) a.decision[ww] = d;
+                if (a.rho) a.rho[ww] = r;
+            }
+        }
+    }
 }
 
 // Diagnostics of the last sg_topk_gate call on this workspace, per worker:
@@ -1892,6 +1990,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ca.tps = p.tps;
     ca.split = p.split;
     ca.nsub = p.nsub;
+    ca.nsubt = p.nsubt;
     ca.bpos = reinterpret_cast<uint32_t*>(at(p.off_bpos));
     ca.sel = sel;
     ca.segcnt = segcnt;
@@ -1907,7 +2006,8 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     launch_pdl(k_collect<T>, dim3(subgrid), dim3(TK_THREADS), 0, stream, ca);
     debug_sync("k_collect", stream);
     // 4. resolve: in-CTA for the normal boundary, cooperative radix rounds for oversized ones
-    const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES + sizeof(unsigned) * (NSUB_MAX + BMAX);
+    const size_t res_smem = (sizeof(K) + 2 * sizeof(uint32_t) + 1) * TopkTraits<T>::RES +
+                            sizeof(unsigned) * (NSUB_MAX + 2 * BMAX + 1);
     smem_attr((const void*)k_resolve<T>, (int)res_smem);
     ResolveArgs<T> ra;
     ra.sel = sel;
@@ -1928,6 +2028,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.tps = p.tps;
     wa.split = p.split;
     wa.nsub = p.nsub;
+    wa.nsubt = p.nsubt;
     wa.sel = sel;
     wa.tstart = tstart;
     wa.segcnt = segcnt;
@@ -1935,7 +2036,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.cidx = cidx;
     wa.cval = cval;
     wa.status = status;
-    wa.done = ctr + 1;
+    wa.done = ctr + 1;  // k_write's last-CTA counter (zeroed per call by k_sample)
     wa.idx = idx;
     wa.val = val;
     wa.tile_off = tile_off;
@@ -1949,10 +2050,6 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     smem_attr((const void*)k_write<T>, (int)wr_smem);
     launch_pdl(k_write<T>, dim3(subgrid), dim3(TK_THREADS), wr_smem, stream, wa);
     debug_sync("k_write", stream);
-    const size_t fin_smem = sizeof(double) * (size_t)k * (p.nseg + p.nsub);
-    smem_attr((const void*)k_finish<T>, (int)fin_smem);
-    launch_pdl(k_finish<T>, dim3(1), dim3(TK_THREADS), fin_smem, stream, wa);
-    debug_sync("k_finish", stream);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

@@ -289,13 +289,31 @@ class GradientExchange:
             (self.idx, self.val, self.norms2, self.decision, self.rho), self.tile_off,
         )
 
-    def step(self, weights, lr: float, *, keep_aggregate: bool = False, topk_events=None) -> StepInfo:
+    def gate_worker(self, j: int, workspace_slot: int = 1) -> None:
+        """Top-k + norms + gate of local worker j alone, on the current stream -- for
+        overlapping a finished worker's gate with the next worker's backward pass (DDP-style:
+        launch it on a side stream once worker j's gradient row is complete, then call
+        ``step(..., gated=True)``).  Same results as the batched gate."""
+        if not self.compression:
+            return
+        if not isinstance(self.ops, CudaOps):
+            raise ValueError("per-worker gating needs the CUDA ops")
+        gb = _capi.GATE_STATE_DTYPE.itemsize
+        out = (self.idx[j:j + 1], self.val[j:j + 1], self.norms2[j:j + 1], self.decision[j:j + 1], self.rho[j:j + 1])
+        kernels.topk_gate(self.bucket[j:j + 1], self.m, self.states[j * gb:(j + 1) * gb], dim=self.dim, out=out,
+                          tile_off=None if self.tile_off is None else self.tile_off[j:j + 1],
+                          workspace_slot=workspace_slot)
+
+    def step(self, weights, lr: float, *, keep_aggregate: bool = False, topk_events=None,
+             gated: bool = False) -> StepInfo:
         """One synchronous iteration over the gradients currently in ``bucket``.
 
         ``weights`` holds all W aggregation weights (host float64).  With
         ``keep_aggregate`` the aggregated gradient is also written to ``self.aggregate``.
         ``topk_events`` = (start, end) CUDA events recorded around the Top-k/gate launch
-        sequence on the current stream (bench.py's per-kernel roofline timing).
+        sequence on the current stream (bench.py's per-kernel roofline timing).  ``gated``:
+        every local worker was already gated with :meth:`gate_worker` (overlapped with the
+        backward passes); the stream must be ordered after those launches.
         """
         w = np.asarray(weights, dtype=np.float64)
         if w.shape != (self.W,):
@@ -306,7 +324,7 @@ class GradientExchange:
         if keep_aggregate and self.aggregate is None:
             self.aggregate = torch.empty(dim, dtype=self.dtype, device=self.device)
         out = self.aggregate if keep_aggregate else None
-        if self.compression:
+        if self.compression and not gated:
             if topk_events is not None:
                 topk_events[0].record()
             self.gate()

@@ -20,7 +20,7 @@ _GATE_BYTES = _capi.GATE_STATE_DTYPE.itemsize
 # Kernel launches issued through this module (each C-ABI entry point launches a fixed
 # sequence; see csrc/topk.cu and csrc/aggregate.cu).  bench.py reports the count.
 LAUNCHES = {"n": 0}
-TOPK_LAUNCHES = {torch.float32: 2 + 2 + 1 + 1 + 1 + 1, torch.float64: 2 + 2 + 1 + 1 + 1 + 1}
+TOPK_LAUNCHES = {torch.float32: 2 + 2 + 1 + 1 + 1, torch.float64: 2 + 2 + 1 + 1 + 1}
 
 
 def _count(n: int) -> None:

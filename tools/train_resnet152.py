@@ -39,6 +39,9 @@ def main():
     ap.add_argument("--cr", type=float, default=0.01)
     ap.add_argument("--delta", type=float, default=0.3)
     ap.add_argument("--stats", action="store_true", help="print the Top-k diagnostics of the last step")
+    ap.add_argument("--overlap", action="store_true",
+                    help="gate each worker on a side stream as soon as its backward is done (overlaps the next "
+                         "worker's forward/backward); the step then only exchanges and merges")
     args = ap.parse_args()
     build.build()
     import torchvision
@@ -66,6 +69,8 @@ def main():
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     loss_fn = torch.nn.CrossEntropyLoss()
     rows = []
+    side = torch.cuda.Stream(device=dev)
+    main = torch.cuda.current_stream()
     for step in range(args.steps):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         e[0].record()
@@ -79,13 +84,24 @@ def main():
                 loss = loss_fn(model(x), y)
             loss.backward()
             losses.append(loss.detach())
+            if args.overlap:  # worker j's row is complete: its gate runs beside the next backward
+                done = torch.cuda.Event()
+                done.record(main)
+                side.wait_event(done)
+                with torch.cuda.stream(side):
+                    ex.gate_worker(j)
         model_bucket.release_grads(model)
+        if args.overlap:
+            main.wait_stream(side)
         e[1].record()
         if group is not None:  # time the exchange itself, not the wait for the slowest rank's backward
             torch.cuda.synchronize()
             dist.barrier()
             e[1].record()
-        info = ex.step(w, lr, topk_events=(e[3], e[4]))
+        if args.overlap:
+            e[3].record()
+            e[4].record()
+        info = ex.step(w, lr, topk_events=None if args.overlap else (e[3], e[4]), gated=args.overlap)
         e[2].record()
         torch.cuda.synchronize()
         rows.append(dict(step=step, backward_ms=e[0].elapsed_time(e[1]), exchange_ms=e[1].elapsed_time(e[2]),
@@ -109,7 +125,7 @@ def main():
     p0 = next(model.parameters())
     bound = p0.data_ptr() == ex.params.data_ptr()
     if rank == 0:
-        print(json.dumps(dict(model="resnet152", params=D, workers=W, gpus=dist.get_world_size() if group else 1,
+        print(json.dumps(dict(model="resnet152", params=D, workers=W, overlap=args.overlap, gpus=dist.get_world_size() if group else 1,
                               workers_per_gpu=ex.k, res=args.res, batches=batch, lr=lr, replicas_identical=same,
                               params_bound=bound, steady_backward_ms=float(np.median([r["backward_ms"] for r in rows[1:]] or [0])),
                               steady_exchange_ms=float(np.median([r["exchange_ms"] for r in rows[1:]] or [0])),
