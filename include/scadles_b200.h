@@ -199,6 +199,12 @@ int sg_weighted_partial_f32(int nw, const double* weights, const uint8_t* compre
 int64_t sg_peer_slice_len(int64_t dim, int nranks);
 int sg_peer_reduce_slice_f32(int nranks, const float* const* src, const double* weights, int rank,
                              const uint8_t* guard, int guard_n, int64_t dim, float* dst, void* stream);
+/* Reduce-and-push variant: rank `rank`'s reduced slice is written (posted NVLink stores) into
+ * every rank's buffer dsts[q] (HOST array of nranks device pointers, peers' memory allowed), so
+ * after a barrier every rank holds the full aggregate locally and updates with
+ * sg_peer_allgather_sgd_f32(1, &own_buffer, 0, ...). */
+int sg_peer_reduce_push_f32(int nranks, const float* const* src, const double* weights, int rank,
+                            const uint8_t* guard, int guard_n, int64_t dim, float* const* dsts, void* stream);
 int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, int rank, const uint8_t* guard, int guard_n,
                               int64_t dim, float* out, float* params, float* momentum_buf, double lr, double momentum,
                               double weight_decay, int first_step, void* stream);

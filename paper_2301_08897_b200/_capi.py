@@ -98,6 +98,10 @@ SIGNATURES = {
         c_int,
         [c_int, POINTER(c_void_p), POINTER(c_double), c_int, _P, c_int, c_int64, _P, _P],
     ),
+    "sg_peer_reduce_push_f32": (
+        c_int,
+        [c_int, POINTER(c_void_p), POINTER(c_double), c_int, _P, c_int, c_int64, POINTER(c_void_p), _P],
+    ),
     "sg_peer_allgather_sgd_f32": (
         c_int,
         [c_int, POINTER(c_void_p), c_int, _P, c_int, c_int64, _P, _P, _P, c_double, c_double, c_double, c_int, _P],

@@ -1345,7 +1345,53 @@ k_sgd(T* __restrict__ p, T* __restrict__ buf, const T* __restrict__ g, long long
     }
 }
 
+struct WArr {
+    double v[8];
+};
+
 inline long long ag_tiles(long long dim) { return (dim + AG_TILE - 1) / AG_TILE; }
+
+// Dense rows only, no update (the dense workload's per-rank partial at P > 1):
+// out = sum_j w_j * row_j in ascending j (float64, round-to-nearest), rounded once; float4
+// loads of every row in flight per thread, grid-stride over the row.
+template <int NWMAX>
+__global__ void __launch_bounds__(256)
+k_weighted_rows(const float* __restrict__ dense, long long ld, int nw, WArr w, long long dim, float* __restrict__ out,
+                const uint8_t* __restrict__ guard, int gn) {
+    pdl_enter();
+    if (guard) {
+        __shared__ int s_run;
+        if (threadIdx.x == 0) {
+            int any0 = 0;
+            for (int j = 0; j < gn; ++j) any0 |= guard[j] == 0;
+            s_run = any0;
+        }
+        __syncthreads();
+        if (!s_run) return;
+    }
+    const long long n4 = dim / 4, stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 x[NWMAX];
+#pragma unroll
+        for (int j = 0; j < NWMAX; ++j)
+            if (j < nw) x[j] = ld_stream(reinterpret_cast<const float4*>(dense + j * ld) + i);
+        double g[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < NWMAX; ++j) {
+            if (j >= nw) break;
+            g[0] = dadd(g[0], dmul(w.v[j], (double)x[j].x));
+            g[1] = dadd(g[1], dmul(w.v[j], (double)x[j].y));
+            g[2] = dadd(g[2], dmul(w.v[j], (double)x[j].z));
+            g[3] = dadd(g[3], dmul(w.v[j], (double)x[j].w));
+        }
+        reinterpret_cast<float4*>(out)[i] = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+    }
+    for (long long q = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < dim; q += stride) {
+        double g = 0.0;
+        for (int j = 0; j < nw; ++j) g = dadd(g, dmul(w.v[j], (double)dense[j * ld + q]));
+        out[q] = (float)g;
+    }
+}
 
 template <typename TI, typename TO>
 int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dense, long long ld,
@@ -1403,6 +1449,16 @@ int aggregate(int nw, const double* weights, const uint8_t* comp, const TI* dens
     if constexpr (sizeof(TI) == 4 && sizeof(TO) == 4)
     {
         const int sms = num_sms();
+        if (!comp && !p && vec && nw <= 8) {  // dense rows, no update: the streaming fold
+            WArr wa;
+            for (int j = 0; j < nw; ++j) wa.v[j] = weights[j];
+            long long blocks = (dim / 4 + 255) / 256;
+            if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
+            if (blocks < 1) blocks = 1;
+            launch_pdl(k_weighted_rows<8>, dim3((unsigned)blocks), dim3(256), 0, stream, reinterpret_cast<const float*>(dense),
+                       ld, nw, wa, dim, reinterpret_cast<float*>(out), guard, guard_n);
+            return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+        }
         a.pipe = comp && vec && p && nw <= MP_MAXW;
         if (a.pipe) {
             const int grid = mw_grid(ntiles, sms);
@@ -1519,9 +1575,13 @@ SG_DEV bool peer_guard_run(const uint8_t* guard, int gn) {
     return s_run != 0;
 }
 
+struct PeerDst {
+    float* p[MAX_PEERS];
+};
+
 __global__ void __launch_bounds__(256)
 k_peer_reduce_slice(PeerRows src, int P, int unit_w, long long lo, long long hi, const uint8_t* __restrict__ guard,
-                    int gn, float* __restrict__ dst) {
+                    int gn, PeerDst dsts, int nd) {
     pdl_enter();
     if (!peer_guard_run(guard, gn)) return;
     const long long n4 = (hi - lo) / 4, stride = (long long)gridDim.x * blockDim.x;
@@ -1559,14 +1619,17 @@ k_peer_reduce_slice(PeerRows src, int P, int unit_w, long long lo, long long hi,
                     g[3] = dadd(g[3], dmul(wr, (double)v.w));
                 }
             }
-            reinterpret_cast<float4*>(dst + lo)[i] = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+            const float4 o = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+            // the reduced slice goes to every destination (this rank's buffer, or pushed into
+            // every rank's aggregate buffer: posted NVLink writes instead of later pulls)
+            for (int d = 0; d < nd; ++d) reinterpret_cast<float4*>(dsts.p[d] + lo)[i] = o;
         }
     }
     // ragged tail of the last slice (dim not a multiple of 4)
     for (long long q = lo + n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += stride) {
         double g = 0.0;
         for (int r = 0; r < P; ++r) g = unit_w ? dadd(g, (double)src.p[r][q]) : dadd(g, dmul(src.w[r], (double)src.p[r][q]));
-        dst[q] = (float)g;
+        for (int d = 0; d < nd; ++d) dsts.p[d][q] = (float)g;
     }
 }
 
@@ -1733,8 +1796,35 @@ int sg_peer_reduce_slice_f32(int nranks, const float* const* src, const double* 
     long long lo = (long long)rank * L, hi = lo + L < dim ? lo + L : dim;
     if (lo > dim) lo = dim;
     if (hi < lo) hi = lo;
+    PeerDst d = {};
+    d.p[0] = dst;
     launch_pdl(k_peer_reduce_slice, dim3((unsigned)peer_blocks((hi - lo) / 4 / 2 + 1)), dim3(256), 0,
-               (cudaStream_t)stream, r, nranks, weights ? 0 : 1, lo, hi, guard_n > 0 ? guard : nullptr, guard_n, dst);
+               (cudaStream_t)stream, r, nranks, weights ? 0 : 1, lo, hi, guard_n > 0 ? guard : nullptr, guard_n, d, 1);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+int sg_peer_reduce_push_f32(int nranks, const float* const* src, const double* weights, int rank,
+                            const uint8_t* guard, int guard_n, int64_t dim, float* const* dsts, void* stream) {
+    if (nranks < 1 || nranks > MAX_PEERS || !src || !dsts || rank < 0 || rank >= nranks || dim < 1 ||
+        guard_n < 0 || guard_n > MAX_WORKERS || (guard_n > 0 && !guard))
+        return SG_ERR_INVALID;
+    if (dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
+    PeerRows r = {};
+    PeerDst d = {};
+    for (int i = 0; i < nranks; ++i) {
+        if (!src[i] || !dsts[i] || reinterpret_cast<size_t>(src[i]) % 16 || reinterpret_cast<size_t>(dsts[i]) % 16)
+            return SG_ERR_UNSUPPORTED;
+        r.p[i] = src[i];
+        r.w[i] = weights ? weights[i] : 1.0;
+        d.p[i] = dsts[(rank + 1 + i) % nranks];  // stagger the push targets over the ranks
+    }
+    const long long L = peer_slice_len(dim, nranks);
+    long long lo = (long long)rank * L, hi = lo + L < dim ? lo + L : dim;
+    if (lo > dim) lo = dim;
+    if (hi < lo) hi = lo;
+    launch_pdl(k_peer_reduce_slice, dim3((unsigned)peer_blocks((hi - lo) / 4 / 2 + 1)), dim3(256), 0,
+               (cudaStream_t)stream, r, nranks, weights ? 0 : 1, lo, hi, guard_n > 0 ? guard : nullptr, guard_n, d,
+               nranks);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

@@ -157,6 +157,7 @@ class GradientExchange:
                 self.pack_words, self.pack_dw = words, dw
                 self._symm = None
                 self._partial_h = None
+                self._agg_h = None
                 # (the peer merge takes up to 16 workers; more go through the NCCL all-gather path)
                 if device.type == "cuda" and os.environ.get("SG_P2P", "1") != "0" and self.W <= 16:
                     self._setup_peer_buffers(words)
@@ -194,7 +195,7 @@ class GradientExchange:
                 self._dense = kernels.GuardedDenseLaunchers(
                     k, dim, self.ld, self.decision, self.idx, self.val, self.row_ptr_local, self.tile_off,
                     self._partial_buf, [ph.buffer_ptrs[r] + poff for r in range(P)], self.dec_all,
-                    self.params, self.momentum_buf, momentum, weight_decay, self.rank)
+                    self.params, self.momentum_buf, momentum, weight_decay, self.rank, **self._push_args())
             elif self.packed:
                 P, words, dw = self.world, self.pack_words, self.pack_dw
                 self.pack_all = torch.empty(P * words, dtype=torch.int32, **z)
@@ -227,6 +228,7 @@ class GradientExchange:
                 and os.environ.get("SG_P2P", "1") != "0" and self.world <= 8):
             self._symm = None
             self._partial_h = None
+            self._agg_h = None
             self._setup_peer_buffers(None)
             if self._partial_h is not None:
                 ph = self._partial_h
@@ -234,7 +236,7 @@ class GradientExchange:
                 self._dense_peer = kernels.GuardedDenseLaunchers(
                     k, dim, self.ld, None, None, None, None, None, self._partial_buf,
                     [ph.buffer_ptrs[r] + poff for r in range(self.world)], None, self.params, self.momentum_buf,
-                    momentum, weight_decay, self.rank)
+                    momentum, weight_decay, self.rank, **self._push_args())
         # float64 ("exact") mode at P > 1: every rank folds all W payloads in ascending worker
         # order (the dense rows are gathered too), so the aggregate and the update are
         # bit-identical to the reference's at any P (the drop-in / metrics path, small D)
@@ -247,6 +249,27 @@ class GradientExchange:
         self._dec_ring = None
         self.aggregate = None
         self.steps = 0
+
+    def _push_args(self) -> dict:
+        """Dense side in push mode (default): every rank's reduced slice is pushed into every
+        rank's aggregate buffer; SG_DENSE_PULL=1 keeps the pull all-gather (A/B runs)."""
+        if os.environ.get("SG_DENSE_PULL", "0") == "1":
+            return {}
+        h = self._agg_h
+        off = self._agg_buf.data_ptr() - h.buffer_ptrs[self.rank]
+        return dict(agg=self._agg_buf, agg_ptrs=[h.buffer_ptrs[r] + off for r in range(self.world)])
+
+    def _dense_side(self, launchers, lr, first, out, barrier) -> None:
+        """partial -> barrier -> reduce (push, or pull at the all-gather) -> barrier -> SGD."""
+        barrier()
+        if launchers._aggp is not None:
+            launchers.reduce_push()
+            barrier()
+            launchers.local_sgd(lr, first, out)
+        else:
+            launchers.reduce_slice()
+            barrier()
+            launchers.allgather_sgd(lr, first, out)
 
     def _setup_peer_buffers(self, words: int | None) -> None:
         """Symmetric (peer-mapped) send buffer (``words`` int32; None: none) and partial buffer,
@@ -268,6 +291,9 @@ class GradientExchange:
             part = symm_mem.empty(self.ld, dtype=torch.float32, device=self.device)
             part.zero_()
             part_h = symm_mem.rendezvous(part, grp.group_name)
+            agg = symm_mem.empty(self.ld, dtype=torch.float32, device=self.device)
+            agg.zero_()
+            agg_h = symm_mem.rendezvous(agg, grp.group_name)
         except Exception:  # no peer mapping on this system
             ok = 0
         flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
@@ -276,9 +302,11 @@ class GradientExchange:
         if int(flag.item()) == 1:
             self._symm, self.pack = symm, pack
             self._partial_buf, self._partial_h = part, part_h
+            self._agg_buf, self._agg_h = agg, agg_h
         else:
             self._symm = None
             self._partial_h = None
+            self._agg_h = None
 
     # -- the step ---------------------------------------------------------------------------
 
@@ -356,11 +384,8 @@ class GradientExchange:
             # dense workload over peer memory: O(D) NVLink bytes per rank, fused update
             h = self._partial_h
             self._dense_peer.partial(w[self.lo:self.lo + self.k], self.bucket)
-            h.barrier(channel=0)
-            self._dense_peer.reduce_slice()
-            h.barrier(channel=0)
-            self._dense_peer.allgather_sgd(opt["lr"], opt["first_step"], out)
-            h.barrier(channel=0)  # no rank rewrites its partial while a peer still reads it
+            self._dense_side(self._dense_peer, opt["lr"], opt["first_step"], out, lambda: h.barrier(channel=0))
+            h.barrier(channel=0)  # no rank rewrites its partial / aggregate while a peer still uses it
             return "dense-peer"
         if self.packed and self._symm is not None:
             # Peer path, no host synchronisation: after a device barrier (every rank's Top-k has
@@ -382,10 +407,7 @@ class GradientExchange:
             self._side.wait_event(self._gathered)
             with torch.cuda.stream(self._side):
                 self._dense.partial(w[self.lo:self.lo + self.k], self.bucket)
-                self._symm.barrier(channel=1)  # every rank's partial is written
-                self._dense.reduce_slice()
-                self._symm.barrier(channel=1)  # every rank's slice is reduced
-                self._dense.allgather_sgd(lr, first, out)
+                self._dense_side(self._dense, lr, first, out, lambda: self._symm.barrier(channel=1))
             self._peer_merge(w, lr, first, out)
             main.wait_stream(self._side)
             self._symm.barrier(channel=0)

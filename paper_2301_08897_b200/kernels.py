@@ -336,8 +336,14 @@ class GuardedDenseLaunchers:
     every worker compressed (``guard`` None: the dense workload, always run)."""
 
     def __init__(self, k: int, dim: int, ld: int, compressed, idx, val, row_ptr, tile_off, partial: torch.Tensor,
-                 partial_ptrs, guard, params, momentum_buf, momentum: float, weight_decay: float, rank: int):
+                 partial_ptrs, guard, params, momentum_buf, momentum: float, weight_decay: float, rank: int,
+                 agg: torch.Tensor | None = None, agg_ptrs=None):
         lib = _capi.load()
+        # push mode (agg given): the reduced slice is pushed into every rank's aggregate buffer
+        # (sg_peer_reduce_push_f32) and each rank updates from its own copy
+        self._agg = agg.data_ptr() if agg is not None else None
+        self._aggp = (ctypes.c_void_p * len(agg_ptrs))(*agg_ptrs) if agg_ptrs is not None else None
+        self._own = (ctypes.c_void_p * 1)(self._agg) if agg is not None else None
         self._part, self._red, self._ag = lib.sg_weighted_partial_f32, lib.sg_peer_reduce_slice_f32, \
             lib.sg_peer_allgather_sgd_f32
         self._k, self._dim, self._ld, self._rank = k, dim, ld, int(rank)
@@ -365,6 +371,19 @@ class GuardedDenseLaunchers:
         st = self._part(self._k, self._wp, self._comp, bucket.data_ptr(), self._ld, self._idx, self._val, self._rp,
                         self._toff, self._dim, self._partial, self._guard, self._gn, None, 0, _stream())
         _capi.check(st, "sg_weighted_partial_f32")
+        _count(1)
+
+    def reduce_push(self) -> None:
+        st = _capi.load().sg_peer_reduce_push_f32(len(self._pp), self._pp, None, self._rank, self._guard, self._gn,
+                                                  self._dim, self._aggp, _stream())
+        _capi.check(st, "sg_peer_reduce_push_f32")
+        _count(1)
+
+    def local_sgd(self, lr: float, first_step: bool, out: torch.Tensor | None = None) -> None:
+        """Momentum SGD from this rank's pushed copy of the aggregate (guarded like the rest)."""
+        st = self._ag(1, self._own, 0, self._guard, self._gn, self._dim, _ptr(out), self._p, self._b,
+                      float(lr), self._mu, self._wd, int(bool(first_step)), _stream())
+        _capi.check(st, "sg_peer_allgather_sgd_f32")
         _count(1)
 
     def reduce_slice(self) -> None:

@@ -158,6 +158,6 @@ def test_fused_batched_rows_padding_and_state(cuda):
         if a.dtype.names:
             for f in ("n_compressed", "n_uncompressed"):
                 assert np.array_equal(a[f], b[f])
-            assert np.allclose(a["ewma_full"], b["ewma_full"], rtol=1e-12)
+            assert np.allclose(a["ewma_full"], b["ewma_full"], rtol=1e-12, equal_nan=True)
         else:
             assert np.array_equal(a, b)
