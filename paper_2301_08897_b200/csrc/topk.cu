@@ -44,7 +44,7 @@ constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
-constexpr int EST_G = 64;        // sampling CTAs per worker (k_sample)
+constexpr int EST_G = 16;        // sampling CTAs per worker (k_sample)
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
 constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
@@ -95,7 +95,7 @@ struct TopkPlan {
     long long ntiles, segcap;
     size_t off_count, off_maxkey, off_ctr, off_bndn, off_hist0, off_hist0fb, off_histr, off_status, zero_end;
     size_t off_sel, off_samp, off_mm, off_cnt, off_tstart, off_segcnt, off_seggt, off_segbase, off_pmain, off_pwrite,
-        off_cidx, off_cval, off_bkey, off_bidx, off_bpos, total;
+        off_cidx, off_cval, off_bkey, off_bidx, off_bpos, off_pp, off_submap, total;
 };
 
 template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int segs_per_worker, long long cta_target) {
@@ -164,6 +164,8 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.off_segbase = take(sizeof(unsigned) * (size_t)k * p.nsub);
     p.off_pmain = take(sizeof(double) * (size_t)k * p.nseg);
     p.off_pwrite = take(sizeof(double) * (size_t)k * p.nsub);
+    p.off_pp = take(sizeof(unsigned) * (size_t)k * (BMAX + 1));
+    p.off_submap = take(sizeof(uint2) * (size_t)k * NSUB_MAX);
     const size_t cap = (size_t)k * p.nseg * p.segcap;
     p.off_cidx = take(sizeof(uint32_t) * cap);
     p.off_cval = take(sizeof(T) * cap);
@@ -555,6 +557,9 @@ template <typename T> struct MainArgs {
     typename KeyOf<T>::K* maxkey;
     unsigned* hist0;    // [k][H0_BINS] (pass-specific)
     unsigned* done;     // [k] (pass-specific)
+    int nsubt, nsub;
+    unsigned* pp;       // [k][BMAX + 1] sub-range prefix per segment (adaptive split)
+    uint2* submap;      // [k][NSUB_MAX] sub-range -> (segment, part | parts << 16); x = ~0u unused
 };
 
 // Per-lane exclusive prefix and warp total of a small count n (0..7) via 3 ballots.
@@ -589,6 +594,15 @@ SG_DEV void load_tile(const T* row, long long base, long long dim, bool vec, typ
             else x[r] = make_double2(t[0], t[1]);
         }
     }
+}
+
+// Adaptive split: segment s of a worker gets parts_s = max(1, ceil(n_s * nsubt / C)) sub-ranges
+// (C = the worker's candidates), so the collect/write CTAs are balanced by candidate count, not
+// by position; sub-ranges are numbered in index order (segment, then part).
+SG_DEV unsigned parts_of(unsigned n, unsigned long long C, int nsubt) {
+    if (C == 0) return 1u;
+    const unsigned long long q = ((unsigned long long)n * (unsigned long long)nsubt + C - 1) / C;
+    return q < 1 ? 1u : (unsigned)q;
 }
 
 // Segment epilogue shared by both main-pass kernels: fixed-tree partial norm, segment count,
@@ -641,6 +655,47 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
             *stp = s;
         }
         return;
+    }
+    // the adaptive collect/write split, computed once here (the last CTA of the worker's
+    // pass): parts per segment by candidate count, their prefix and the sub-range map
+    {
+        const unsigned* sc = a.segcnt + (long long)w * a.nseg;
+        constexpr int PER = BMAX / TK_THREADS;
+        unsigned pv[PER], sum = 0;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int q = tid * PER + u;
+            pv[u] = q < a.nseg ? parts_of(__ldcg(sc + q), C, a.nsubt) : 0u;
+            sum += pv[u];
+        }
+        __shared__ unsigned s_ps[TK_NW];
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_ps[warp] = incl;
+        __syncthreads();
+        unsigned run = incl - sum;
+        for (int i = 0; i < warp; ++i) run += s_ps[i];
+        unsigned* pp = a.pp + (long long)w * (BMAX + 1);
+        uint2* sm = a.submap + (long long)w * NSUB_MAX;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int q = tid * PER + u;
+            if (q < a.nseg) {
+                pp[q] = run;
+                for (unsigned t = 0; t < pv[u] && run + t < (unsigned)a.nsub; ++t)
+                    sm[run + t] = make_uint2((unsigned)q, t | (pv[u] << 16));
+            }
+            run += pv[u];
+        }
+        __shared__ unsigned s_tot;
+        if (tid == TK_THREADS - 1) s_tot = run;
+        __syncthreads();
+        if (tid == 0) pp[a.nseg] = s_tot;
+        for (int i = (int)s_tot + tid; i < a.nsub; i += TK_THREADS) sm[i] = make_uint2(0xffffffffu, 0u);
     }
     int bin;
     unsigned long long above;
@@ -944,51 +999,11 @@ SG_DEV int sub_of(long long n, long long off, int split) {
     return i;
 }
 
-// Adaptive split: segment s of a worker gets parts_s = max(1, ceil(n_s * nsubt / C)) sub-ranges
-// (C = the worker's candidates), so the collect/write CTAs are balanced by candidate count, not
-// by position; sub-ranges are numbered in index order (segment, then part).
-SG_DEV unsigned parts_of(unsigned n, unsigned long long C, int nsubt) {
-    if (C == 0) return 1u;
-    const unsigned long long q = ((unsigned long long)n * (unsigned long long)nsubt + C - 1) / C;
-    return q < 1 ? 1u : (unsigned)q;
-}
-
-// Warp-cooperative (all 32 lanes): sub-range `sub` -> (segment, part, parts of that segment);
-// seg = -1 beyond the worker's last sub-range.
-SG_DEV void map_sub(const unsigned* segcnt, int nseg, int nsubt, int sub, int& seg, int& part, int& split) {
-    const int lane = threadIdx.x & 31;
-    unsigned long long C = 0;
-    for (int i = lane; i < nseg; i += 32) C += segcnt[i];
-    for (int o = 16; o > 0; o >>= 1) C += __shfl_xor_sync(FULL, C, o);
-    seg = -1;
-    part = 0;
-    split = 1;
-    unsigned run = 0;
-    for (int b = 0; b < nseg; b += 32) {
-        const int si = b + lane;
-        const unsigned ps = si < nseg ? parts_of(segcnt[si], C, nsubt) : 0u;
-        unsigned incl = ps;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const unsigned hit = __ballot_sync(FULL, si < nseg && run + incl > (unsigned)sub);
-        if (hit) {
-            const int f = __ffs(hit) - 1;
-            const unsigned ex = __shfl_sync(FULL, incl - ps, f);
-            seg = b + f;
-            part = sub - (int)(run + ex);
-            split = (int)__shfl_sync(FULL, ps, f);
-            return;
-        }
-        run += __shfl_sync(FULL, incl, 31);
-    }
-}
-
 template <typename T> struct CollectArgs {
     long long segcap, cap;         // cap: boundary entries stored per worker (RES)
     int nseg, tps, split, nsub, nsubt;
+    const unsigned* pp;            // [k][BMAX + 1] (from the main pass's last CTA)
+    const uint2* submap;           // [k][NSUB_MAX]
     uint32_t* bpos;                // [k][cap] boundary entry's position in its segment list
     SelState<typename KeyOf<T>::K>* sel;
     const unsigned* segcnt;
@@ -1051,14 +1066,11 @@ k_collect(CollectArgs<T> a) {
     __shared__ int s_map[3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, sub = blockIdx.x;
-    if (warp == 0) {
-        int sg_, pt_, sp_;
-        map_sub(a.segcnt + (long long)w * a.nseg, a.nseg, a.nsubt, sub, sg_, pt_, sp_);
-        if (lane == 0) {
-            s_map[0] = sg_;
-            s_map[1] = pt_;
-            s_map[2] = sp_;
-        }
+    if (tid == 0) {
+        const uint2 e = a.submap[(long long)w * NSUB_MAX + sub];
+        s_map[0] = e.x == 0xffffffffu ? -1 : (int)e.x;
+        s_map[1] = (int)(e.y & 0xffffu);
+        s_map[2] = (int)(e.y >> 16);
     }
     __syncthreads();
     const int seg = s_map[0], part = s_map[1], split = s_map[2];
@@ -1171,17 +1183,7 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
         sst = a.sel[w];
         s_eq = 0;
     }
-    __syncthreads();
-    if (tid == 0) {  // parts per segment -> prefix (same apportioning as map_sub)
-        unsigned long long C = 0;
-        for (int i = 0; i < a.nseg; ++i) C += sc[i];
-        unsigned run = 0;
-        for (int i = 0; i < a.nseg; ++i) {
-            pp[i] = run;
-            run += parts_of(sc[i], C, a.nsubt);
-        }
-        pp[a.nseg] = run;
-    }
+    for (int i = tid; i <= a.nseg; i += NT) pp[i] = __ldcg(a.pp + (long long)w * (BMAX + 1) + i);
     SG_PH();
     block_select<K, NT>(sk, (long long)h, sst, hist);
     SG_PH();
@@ -1396,6 +1398,7 @@ k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
 template <typename T> struct WriteArgs {
     long long ntiles, segcap, m;
     int k, nseg, tps, split, nsub, nsubt;
+    const uint2* submap;
     const SelState<typename KeyOf<T>::K>* sel;
     const unsigned* tstart;
     const unsigned* segcnt;
@@ -1596,14 +1599,11 @@ SG_DEV void write_body(const WriteArgs<T>& a) {
     __shared__ int s_map[3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, sub = blockIdx.x;
-    if (warp == 0) {
-        int sg_, pt_, sp_;
-        map_sub(a.segcnt + (long long)w * a.nseg, a.nseg, a.nsubt, sub, sg_, pt_, sp_);
-        if (lane == 0) {
-            s_map[0] = sg_;
-            s_map[1] = pt_;
-            s_map[2] = sp_;
-        }
+    if (tid == 0) {
+        const uint2 e = a.submap[(long long)w * NSUB_MAX + sub];
+        s_map[0] = e.x == 0xffffffffu ? -1 : (int)e.x;
+        s_map[1] = (int)(e.y & 0xffffu);
+        s_map[2] = (int)(e.y >> 16);
     }
     __syncthreads();
     const int seg = s_map[0], part = s_map[1], split = s_map[2];
@@ -1968,6 +1968,10 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ma.maxkey = maxkey;
     ma.hist0 = hist0;
     ma.done = c_main;
+    ma.nsubt = p.nsubt;
+    ma.nsub = p.nsub;
+    ma.pp = reinterpret_cast<unsigned*>(at(p.off_pp));
+    ma.submap = reinterpret_cast<uint2*>(at(p.off_submap));
     const dim3 sgrid((unsigned)p.nseg, (unsigned)k);
     bool tma = false;
     if constexpr (sizeof(T) == 4) tma = vec_ok;
@@ -1996,6 +2000,8 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ca.split = p.split;
     ca.nsub = p.nsub;
     ca.nsubt = p.nsubt;
+    ca.pp = ma.pp;
+    ca.submap = ma.submap;
     ca.bpos = reinterpret_cast<uint32_t*>(at(p.off_bpos));
     ca.sel = sel;
     ca.segcnt = segcnt;
@@ -2034,6 +2040,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.split = p.split;
     wa.nsub = p.nsub;
     wa.nsubt = p.nsubt;
+    wa.submap = ma.submap;
     wa.sel = sel;
     wa.tstart = tstart;
     wa.segcnt = segcnt;
