@@ -71,14 +71,17 @@ int64_t sg_topk_count(int64_t dim, double cr);
  * (unaligned rows fall back to scalar loads, still on the GPU). */
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m);
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m);
+/* float32 workspaces carry zero-state between calls: the first
+ * sg_topk_workspace_zero_bytes_f32(k, dim, m) bytes (launch chain) or
+ * sg_topk_workspace_zero_bytes_fused_f32 bytes (fused variant) must be zero before the first
+ * call and whenever (k, dim, m) change; every call leaves them as it found them. */
+size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m);
 /* Persistent float32 variant: the same contract as sg_topk_gate_f32 in ONE cooperative
  * kernel (sample -> estimate -> single read -> select -> ordered write -> gate, synchronised
  * per worker on the device), with a ~2m-entry candidate pool instead of per-segment slots of D
- * (workspace ~16 m + 2 MB per worker).  Its workspace carries zero-state between calls: the
- * first sg_topk_workspace_zero_bytes_f32(k, dim, m) bytes must be zero before the first call
- * and whenever (k, dim, m) change; every call leaves them zeroed. */
+ * (workspace ~16 m + 2 MB per worker). */
 size_t sg_topk_workspace_bytes_fused_f32(int k, int64_t dim, int64_t m);
-size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m);
+size_t sg_topk_workspace_zero_bytes_fused_f32(int k, int64_t dim, int64_t m);
 int sg_topk_gate_fused_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m,
                            uint32_t* idx, float* val, double* norms2,
                            sg_gate_state* states, uint8_t* decision, double* rho,

@@ -63,6 +63,7 @@ SIGNATURES = {
     "sg_topk_workspace_bytes_f64": (c_size_t, [c_int, c_int64, c_int64]),
     "sg_topk_workspace_zero_bytes_f32": (c_size_t, [c_int, c_int64, c_int64]),
     "sg_topk_workspace_bytes_fused_f32": (c_size_t, [c_int, c_int64, c_int64]),
+    "sg_topk_workspace_zero_bytes_fused_f32": (c_size_t, [c_int, c_int64, c_int64]),
     "sg_topk_gate_fused_f32": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),
     "sg_topk_stats_fused_f32": (c_int, [c_int, c_int64, c_int64, _P, c_size_t, _P, _P]),
     "sg_topk_gate_f32": (c_int, [_P, c_int, c_int64, c_int64, c_int64, _P, _P, _P, _P, _P, _P, _P, _P, c_size_t, _P]),

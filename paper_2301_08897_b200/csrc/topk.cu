@@ -44,7 +44,7 @@ constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
-constexpr int EST_G = 16;        // sampling CTAs per worker (k_sample)
+constexpr int EST_G = 64;        // sampling CTAs per worker (k_sample)
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
 constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
@@ -95,7 +95,7 @@ struct TopkPlan {
     long long ntiles, segcap;
     size_t off_count, off_maxkey, off_ctr, off_bndn, off_hist0, off_hist0fb, off_histr, off_status, zero_end;
     size_t off_sel, off_samp, off_mm, off_cnt, off_tstart, off_segcnt, off_seggt, off_segbase, off_pmain, off_pwrite,
-        off_cidx, off_cval, off_bkey, off_bidx, off_bpos, off_pp, off_submap, total;
+        off_cidx, off_cval, off_bkey, off_bidx, off_bpos, off_pp, off_submap, off_hs1, total;
 };
 
 template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int segs_per_worker, long long cta_target) {
@@ -104,11 +104,10 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.k = k;
     p.dim = dim;
     p.m = m;
-    // sample size: the small sample keeps the estimate's latency low where the candidate
-    // overshoot is cheap (cr < 0.05); at higher ratios the candidates dominate the traffic,
-    // so the full sample tightens C toward m (C/m ~1.04 at cr 0.1 vs ~1.15)
+    // sample: 131072 keys (f32) with 4 sigma slack keep C = count(key >= est) near m (C/m
+    // ~1.04 at cr 0.1, ~1.1 at cr 0.01), which matters most on real gradients, whose kept
+    // entries crowd into a few layers
     long long S = TopkTraits<T>::SAMPLE;  // a multiple of CHUNK
-    if (sizeof(T) == 4 && (double)m < 0.05 * (double)dim) S = 16384;
     p.s_eff = dim <= S ? dim : S;
     p.stride = dim / p.s_eff;
     if (p.s_eff == dim) {
@@ -135,12 +134,14 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
         // sub-ranges are apportioned to segments by candidate count on the device (adaptive
         // split: concentrated real gradients put most candidates in a few segments), so the
         // grid is the target plus one per segment (every segment gets at least one)
-        long long want = cta_target / k;
-        if (want > NSUB_MAX - p.nseg) want = NSUB_MAX - p.nseg;
-        if (want < p.nseg) want = p.nseg;
-        p.nsubt = (int)want;
-        p.nsub = p.nsubt + p.nseg;
-        if (p.nsub > NSUB_MAX) p.nsub = NSUB_MAX;
+        // grid = one wave of CTAs per worker (cta_target / k, at least one per segment); the
+        // apportioned target leaves one guaranteed part per segment inside it
+        long long grid = cta_target / k;
+        if (grid > NSUB_MAX) grid = NSUB_MAX;
+        if (grid < 2LL * p.nseg) grid = 2LL * p.nseg;
+        if (grid > NSUB_MAX) grid = NSUB_MAX;
+        p.nsub = (int)grid;
+        p.nsubt = p.nsub - p.nseg > 0 ? p.nsub - p.nseg : 1;
         p.split = 0;
     }
     size_t o = 0;
@@ -175,6 +176,9 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.off_bkey = take(sizeof(K) * bcap);
     p.off_bidx = take(sizeof(uint32_t) * bcap);
     p.off_bpos = take(sizeof(uint32_t) * bcap);
+    // float32 sample histogram (key bits [30:20]): filled by k_sample, read and re-zeroed by
+    // k_estimate, so it is zero between calls (outside k_sample's per-call zero range)
+    p.off_hs1 = take(sizeof(unsigned) * (size_t)k * SEL_BINS);
     p.total = o + 256;  // slack for base alignment
     return p;
 }
@@ -403,12 +407,18 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
          typename KeyOf<T>::K* __restrict__ samp, typename KeyOf<T>::K* __restrict__ mm,
-         uint4* __restrict__ zero, long long zero_vec) {
+         uint4* __restrict__ zero, long long zero_vec, unsigned* __restrict__ hs1) {
     pdl_enter();
     using KO = KeyOf<T>;
     using K = typename KO::K;
+    constexpr bool H1 = sizeof(K) == 4;  // float32: level-1 histogram of the sample here
     __shared__ K s_min[8], s_max[8];
+    __shared__ unsigned s_h1[H1 ? SEL_BINS : 1];
     const int x = blockIdx.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if constexpr (H1) {
+        for (int i = tid; i < SEL_BINS; i += 256) s_h1[i] = 0;
+        __syncthreads();
+    }
     const long long cta = (long long)w * gridDim.x + x;
     for (long long i = cta * 256 + tid; i < zero_vec; i += (long long)gridDim.x * gridDim.y * 256)
         zero[i] = make_uint4(0, 0, 0, 0);
@@ -421,6 +431,7 @@ k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
         for (long long i = lo + tid; i < hi; i += 256) {
             const K key = KO::key(row[i]);
             sk[i] = key;
+            if constexpr (H1) atomicAdd(&s_h1[(unsigned)(key >> 20)], 1u);
             mn = key < mn ? key : mn;
             mx = key > mx ? key : mx;
         }
@@ -447,6 +458,7 @@ k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
                 if (c < nch) {
                     const K key = KO::key(v[u]);
                     sk[c * CHUNK + lane] = key;
+                    if constexpr (H1) atomicAdd(&s_h1[(unsigned)(key >> 20)], 1u);
                     mn = key < mn ? key : mn;
                     mx = key > mx ? key : mx;
                 }
@@ -472,6 +484,11 @@ k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
         mm[cta * 2] = a;
         mm[cta * 2 + 1] = b;
     }
+    if constexpr (H1) {
+        unsigned* gh = hs1 + (long long)w * SEL_BINS;
+        for (int i = tid; i < SEL_BINS; i += 256)
+            if (s_h1[i]) atomicAdd(gh + i, s_h1[i]);
+    }
 }
 
 // k_estimate: one CTA per worker; est = the lower edge of the 2048-bin histogram bin (over the
@@ -481,7 +498,8 @@ k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
 template <typename T>
 __global__ void __launch_bounds__(EST_THREADS)
 k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf<T>::K* __restrict__ samp,
-           const typename KeyOf<T>::K* __restrict__ mm, int G, SelState<typename KeyOf<T>::K>* __restrict__ sel) {
+           const typename KeyOf<T>::K* __restrict__ mm, int G, SelState<typename KeyOf<T>::K>* __restrict__ sel,
+           unsigned* __restrict__ hs1) {
     pdl_enter();
     using KO = KeyOf<T>;
     using K = typename KO::K;
@@ -513,16 +531,49 @@ k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf
     const int shift = s_shift;
     const long long ns = (s_eff / CHUNK) * CHUNK == s_eff || s_eff == dim ? s_eff : (s_eff / CHUNK) * CHUNK;
     const K* sk = samp + (long long)w * TopkTraits<T>::SAMPLE;
-    if (r_est <= ns) {
-        for (long long i = tid; i < ns; i += EST_THREADS) atomicAdd(&hist[digit<K>(sk[i], lo, shift, SEL_BINS)], 1u);
-    }
-    __syncthreads();
     K est = 0;
-    if (r_est <= ns) {  // uniform
-        int bin;
-        unsigned long long above;
-        block_find_bin_from_top<SEL_BINS, EST_THREADS>(hist, (unsigned long long)r_est, bin, above);
-        est = bin < 0 ? (K)0 : lo + ((K)bin << shift);
+    if constexpr (sizeof(K) == 4) {
+        // float32: two fixed-digit rounds -- the sampling CTAs already histogrammed key bits
+        // [30:20] (level 1, no contended atomics here); level 2 (bits [19:9]) only over the
+        // sample keys inside the chosen level-1 bin.  est is the 512-key bin edge at or below
+        // the r_est-th largest sample key.
+        (void)lo;
+        (void)shift;
+        unsigned* gh = hs1 + (long long)w * SEL_BINS;
+        for (int i = tid; i < SEL_BINS; i += EST_THREADS) hist[i] = __ldcg(gh + i);
+        __syncthreads();
+        if (r_est <= ns) {
+            int b1;
+            unsigned long long a1;
+            block_find_bin_from_top<SEL_BINS, EST_THREADS>(hist, (unsigned long long)r_est, b1, a1);
+            for (int i = tid; i < SEL_BINS; i += EST_THREADS) gh[i] = 0;  // zero for the next call
+            if (b1 >= 0) {
+                for (int i = tid; i < SEL_BINS; i += EST_THREADS) hist[i] = 0;
+                __syncthreads();
+                for (long long i = tid; i < ns; i += EST_THREADS) {
+                    const K key = sk[i];
+                    if ((int)(key >> 20) == b1) atomicAdd(&hist[(key >> 9) & (SEL_BINS - 1)], 1u);
+                }
+                __syncthreads();
+                int b2;
+                unsigned long long a2;
+                block_find_bin_from_top<SEL_BINS, EST_THREADS>(hist, (unsigned long long)r_est - a1, b2, a2);
+                est = ((K)b1 << 20) | (b2 >= 0 ? ((K)b2 << 9) : (K)0);
+            }
+        } else {
+            for (int i = tid; i < SEL_BINS; i += EST_THREADS) gh[i] = 0;
+        }
+    } else {
+        if (r_est <= ns) {
+            for (long long i = tid; i < ns; i += EST_THREADS) atomicAdd(&hist[digit<K>(sk[i], lo, shift, SEL_BINS)], 1u);
+        }
+        __syncthreads();
+        if (r_est <= ns) {  // uniform
+            int bin;
+            unsigned long long above;
+            block_find_bin_from_top<SEL_BINS, EST_THREADS>(hist, (unsigned long long)r_est, bin, above);
+            est = bin < 0 ? (K)0 : lo + ((K)bin << shift);
+        }
     }
     {
         if (tid == 0) {
@@ -1938,11 +1989,12 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     // 1. sample (+ zero the small scratch, incl. the slow-mode look-back status words), estimate
     K* samp = reinterpret_cast<K*>(at(p.off_samp));
     K* mm = reinterpret_cast<K*>(at(p.off_mm));
+    unsigned* hs1 = reinterpret_cast<unsigned*>(at(p.off_hs1));
     launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm,
-               reinterpret_cast<uint4*>(base), (long long)(p.zero_end / 16));
+               reinterpret_cast<uint4*>(base), (long long)(p.zero_end / 16), hs1);
     debug_sync("k_sample", stream);
     launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), 0, stream, dim, p.s_eff, p.r_est,
-               (const K*)samp, (const K*)mm, EST_G, sel);
+               (const K*)samp, (const K*)mm, EST_G, sel, hs1);
     debug_sync("k_estimate", stream);
     // 2. main streaming pass, then the (normally empty) fallback pass
     MainArgs<T> ma;
@@ -2114,6 +2166,11 @@ size_t sg_topk_workspace_bytes_fused_f32(int k, int64_t dim, int64_t m) {
 }
 
 size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m) {
+    // the launch chain keeps its sample histogram zeroed between calls (k_estimate clears it)
+    return sg_topk_workspace_bytes_f32(k, dim, m);
+}
+
+size_t sg_topk_workspace_zero_bytes_fused_f32(int k, int64_t dim, int64_t m) {
     if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
     return topk_fused_zero_bytes(k, dim, m, fused_segments(k));
 }

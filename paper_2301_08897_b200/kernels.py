@@ -68,12 +68,13 @@ class Workspace:
         return buf
 
     @classmethod
-    def get_topk(cls, nbytes: int, zero_bytes: int, plan_key: tuple, device: torch.device, slot: int = 0):
-        """The float32 Top-k workspace: zero-filled when created and whenever the plan
-        (k, dim, m) changes; every call leaves its zero-state region zeroed again."""
-        buf = cls.get(nbytes, device, slot, kind="topk32")
+    def get_topk(cls, nbytes: int, zero_bytes: int, plan_key: tuple, device: torch.device, slot: int = 0,
+                 kind: str = "topk32"):
+        """A float32 Top-k workspace: zero-filled when created and whenever the plan
+        (k, dim, m) changes; every call leaves its zero-state region as it found it."""
+        buf = cls.get(nbytes, device, slot, kind=kind)
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        key = (idx, "topk32", slot)
+        key = (idx, kind, slot)
         if cls._keys.get(key) != plan_key:
             buf[:min(int(zero_bytes), buf.numel())].zero_()
             cls._keys[key] = plan_key
@@ -107,12 +108,18 @@ def topk_workspace_bytes(dtype: torch.dtype, k: int, dim: int, m: int, fused: bo
 
 
 def _topk_ws(dtype, k, dim, m, device, slot, fused):
-    if dtype == torch.float32 and fused:
+    """float32 workspaces carry zero-state between calls: zero-filled when created and
+    whenever the plan (k, dim, m) changes (sg_topk_workspace_zero_bytes_*)."""
+    if dtype == torch.float32:
         lib = _capi.load()
-        return Workspace.get_topk(topk_workspace_bytes(dtype, k, dim, m, True),
-                                  int(lib.sg_topk_workspace_zero_bytes_f32(k, dim, m)), (k, dim, m), device, slot)
-    kind = "topk32" if dtype == torch.float32 else "topk64"
-    return Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, slot, kind=kind)
+        if fused:
+            return Workspace.get_topk(topk_workspace_bytes(dtype, k, dim, m, True),
+                                      int(lib.sg_topk_workspace_zero_bytes_fused_f32(k, dim, m)), (k, dim, m), device,
+                                      slot, kind="topk32f")
+        return Workspace.get_topk(topk_workspace_bytes(dtype, k, dim, m),
+                                  int(lib.sg_topk_workspace_zero_bytes_f32(k, dim, m)), (k, dim, m), device, slot,
+                                  kind="topk32")
+    return Workspace.get(topk_workspace_bytes(dtype, k, dim, m), device, slot, kind="topk64")
 
 
 def topk_gate(
