@@ -71,10 +71,10 @@ int64_t sg_topk_count(int64_t dim, double cr);
  * (unaligned rows fall back to scalar loads, still on the GPU). */
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m);
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m);
-/* float32 workspaces carry zero-state between calls: the first
- * sg_topk_workspace_zero_bytes_f32(k, dim, m) bytes (launch chain) or
- * sg_topk_workspace_zero_bytes_fused_f32 bytes (fused variant) must be zero before the first
- * call and whenever (k, dim, m) change; every call leaves them as it found them. */
+/* Zero-state of a workspace between calls: the first sg_topk_workspace_zero_bytes_f32 bytes
+ * (launch chain: 0, it keeps none) or sg_topk_workspace_zero_bytes_fused_f32 bytes (fused
+ * variant) must be zero before the first call and whenever (k, dim, m) change; every call
+ * leaves them as it found them. */
 size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m);
 /* Persistent float32 variant: the same contract as sg_topk_gate_f32 in ONE cooperative
  * kernel (sample -> estimate -> single read -> select -> ordered write -> gate, synchronised
@@ -208,6 +208,20 @@ int sg_peer_reduce_slice_f32(int nranks, const float* const* src, const double* 
  * sg_peer_allgather_sgd_f32(1, &own_buffer, 0, ...). */
 int sg_peer_reduce_push_f32(int nranks, const float* const* src, const double* weights, int rank,
                             const uint8_t* guard, int guard_n, int64_t dim, float* const* dsts, void* stream);
+/* The whole dense side in ONE cooperative launch per rank: the partial fold of this rank's
+ * dense rows (or, dense == NULL, a partial already in partials[rank]), the position-sharded
+ * reduce (chunks of 16384 elements round-robin over the ranks) pushed into every rank's
+ * aggregate buffer, and the momentum SGD from the local copy, overlapped chunk by chunk and
+ * synchronised across GPUs by per-chunk epoch flags (flags[q]: rank q's peer-mapped array of
+ * sg_dense_exchange_flag_words(dim, P) zero-initialised words; epoch >= 1, increasing by one per
+ * call, identical on every rank).  partials / aggs / flags: HOST arrays of nranks device
+ * pointers (peers' memory).  Replaces the partial + all-reduce + SGD of engine.py:270-283. */
+size_t sg_dense_exchange_flag_words(int64_t dim, int nranks);
+int sg_dense_exchange_f32(int nranks, int rank, int k, const double* weights, const float* dense, int64_t ld,
+                          int64_t dim, const float* const* partials, float* const* aggs, unsigned* const* flags,
+                          unsigned epoch, const uint8_t* guard, int guard_n, float* out, float* params,
+                          float* momentum_buf, double lr, double momentum, double weight_decay, int first_step,
+                          void* stream);
 int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, int rank, const uint8_t* guard, int guard_n,
                               int64_t dim, float* out, float* params, float* momentum_buf, double lr, double momentum,
                               double weight_decay, int first_step, void* stream);

@@ -1685,6 +1685,172 @@ k_peer_allgather_sgd(PeerRows src, int P, int rank, long long L, const uint8_t* 
     }
 }
 
+// ---- The pipelined dense exchange: partial -> reduce -> push -> update in ONE launch ---------
+// The dense side of a multi-GPU step as a single cooperative kernel per rank whose three CTA
+// roles overlap over chunks of XC elements, synchronised across GPUs by per-chunk epoch flags
+// in peer-mapped memory instead of barriers between phases:
+//   partial  (role 0)  this rank's weighted fold of its dense rows for chunk c (or, with the
+//                      partial precomputed, nothing) -> raise pflag[owner(c)][c][rank]
+//   reduce   (role 1)  for the chunks this rank owns (c % P == rank): wait until every rank's
+//                      partial of c is up, sum them in ascending rank order (float64, pulled
+//                      over NVLink), push the float32 result into every rank's aggregate
+//                      buffer, raise aflag[q][c] on every rank q
+//   update   (role 2)  for every chunk: wait for aflag[c] (local), momentum SGD (nn.py:167-171
+//                      order, binary64) from the local copy of the aggregate
+// HBM work (the fold, the update) overlaps the NVLink pulls and pushes of other chunks.  Flags
+// carry the step's epoch (monotone), so no reset; a rank's buffers are reused only after the
+// previous launch completed, which already implies every owner consumed them (the update role
+// waits for every chunk's aggregate).  Guarded like the rest of the dense side.
+constexpr int XC = 16384;  // chunk elements (64 KB of float32)
+
+struct DxArgs {
+    const float* dense;    // this rank's [k][ld] rows (role 0 folds them) or nullptr
+    long long ld, dim;
+    int k, P, rank, nchunk, roles_per;  // roles_per: CTAs per role
+    WArr w;                // this rank's worker weights
+    const float* partial_src[MAX_PEERS];  // every rank's partial buffer (peers' memory)
+    float* partial_own;    // this rank's partial buffer (role 0 writes it)
+    float* agg[MAX_PEERS];  // every rank's aggregate buffer (role 1 pushes into them)
+    const float* agg_own;
+    unsigned* pflag[MAX_PEERS];  // rank q's pflag array [nchunk][P]
+    unsigned* aflag[MAX_PEERS];  // rank q's aflag array [nchunk]
+    unsigned* pflag_own;
+    unsigned* aflag_own;
+    unsigned epoch;
+    const uint8_t* guard;
+    int gn;
+    float* out;
+    float* p;
+    float* b;
+    double lr, mu, wd;
+    int first;
+};
+
+SG_DEV void st_release_sys(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+SG_DEV unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+SG_DEV void wait_epoch(const unsigned* f, unsigned epoch) {
+    while ((int)(ld_acquire_sys(f) - epoch) < 0) __nanosleep(100);
+}
+
+__global__ void __launch_bounds__(256)
+k_dense_exchange(DxArgs a) {
+    pdl_enter();
+    {
+        __shared__ int s_run;
+        if (threadIdx.x == 0) {
+            int any0 = a.guard == nullptr ? 1 : 0;
+            for (int j = 0; j < a.gn; ++j) any0 |= a.guard[j] == 0;
+            s_run = any0;
+        }
+        __syncthreads();
+        if (!s_run) return;
+    }
+    const int role = blockIdx.x / a.roles_per, rb = blockIdx.x % a.roles_per, R = a.roles_per;
+    const int tid = threadIdx.x;
+    const int P = a.P;
+    if (role == 0) {
+        for (int c = rb; c < a.nchunk; c += R) {
+            const long long lo = (long long)c * XC, hi = lo + XC < a.dim ? lo + XC : a.dim;
+            if (a.dense) {
+                const long long n4 = (hi - lo) / 4;
+                for (long long i = tid; i < n4; i += 256) {
+                    double g[4] = {0.0, 0.0, 0.0, 0.0};
+                    for (int j = 0; j < a.k; ++j) {
+                        const float4 x = ld_stream(reinterpret_cast<const float4*>(a.dense + j * a.ld + lo) + i);
+                        g[0] = dadd(g[0], dmul(a.w.v[j], (double)x.x));
+                        g[1] = dadd(g[1], dmul(a.w.v[j], (double)x.y));
+                        g[2] = dadd(g[2], dmul(a.w.v[j], (double)x.z));
+                        g[3] = dadd(g[3], dmul(a.w.v[j], (double)x.w));
+                    }
+                    reinterpret_cast<float4*>(a.partial_own + lo)[i] =
+                        make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+                }
+                for (long long q = lo + n4 * 4 + tid; q < hi; q += 256) {
+                    double g = 0.0;
+                    for (int j = 0; j < a.k; ++j) g = dadd(g, dmul(a.w.v[j], (double)a.dense[j * a.ld + q]));
+                    a.partial_own[q] = (float)g;
+                }
+            }
+            __threadfence_system();
+            __syncthreads();
+            if (tid == 0) st_release_sys(a.pflag[c % P] + (long long)c * P + a.rank, a.epoch);
+        }
+    } else if (role == 1) {
+        __shared__ int s_dummy;
+        (void)s_dummy;
+        for (int i0 = rb;; i0 += R) {
+            const int c = a.rank + i0 * P;
+            if (c >= a.nchunk) break;
+            if (tid < P) wait_epoch(a.pflag_own + (long long)c * P + tid, a.epoch);
+            __syncthreads();
+            const long long lo = (long long)c * XC, hi = lo + XC < a.dim ? lo + XC : a.dim;
+            const long long n4 = (hi - lo) / 4;
+            for (long long i = tid; i < n4; i += 256) {
+                float4 x[MAX_PEERS];
+#pragma unroll
+                for (int r = 0; r < MAX_PEERS; ++r)
+                    if (r < P) x[r] = __ldcg(reinterpret_cast<const float4*>(a.partial_src[r] + lo) + i);
+                double g[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int r = 0; r < MAX_PEERS; ++r) {
+                    if (r >= P) break;
+                    g[0] = dadd(g[0], (double)x[r].x);
+                    g[1] = dadd(g[1], (double)x[r].y);
+                    g[2] = dadd(g[2], (double)x[r].z);
+                    g[3] = dadd(g[3], (double)x[r].w);
+                }
+                const float4 o = make_float4((float)g[0], (float)g[1], (float)g[2], (float)g[3]);
+                for (int d = 0; d < P; ++d) {
+                    const int q = (a.rank + 1 + d) % P;  // stagger the push targets
+                    reinterpret_cast<float4*>(a.agg[q] + lo)[i] = o;
+                }
+            }
+            for (long long qd = lo + n4 * 4 + tid; qd < hi; qd += 256) {
+                double g = 0.0;
+                for (int r = 0; r < P; ++r) g = dadd(g, (double)__ldcg(a.partial_src[r] + qd));
+                for (int q = 0; q < P; ++q) a.agg[q][qd] = (float)g;
+            }
+            __threadfence_system();
+            __syncthreads();
+            if (tid < P) st_release_sys(a.aflag[tid] + c, a.epoch);
+        }
+    } else {
+        for (int c = rb; c < a.nchunk; c += R) {
+            if (tid == 0) wait_epoch(a.aflag_own + c, a.epoch);
+            __syncthreads();
+            const long long lo = (long long)c * XC, hi = lo + XC < a.dim ? lo + XC : a.dim;
+            const long long n4 = (hi - lo) / 4;
+            for (long long i = tid; i < n4; i += 256) {
+                const float4 gv = __ldcg(reinterpret_cast<const float4*>(a.agg_own + lo) + i);
+                const float4 pv = reinterpret_cast<const float4*>(a.p + lo)[i];
+                const float4 bv = a.first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(a.b + lo)[i];
+                double g[4] = {gv.x, gv.y, gv.z, gv.w};
+                double pd[4] = {pv.x, pv.y, pv.z, pv.w}, bd[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) sgd_elem(g[e], pd[e], bd[e], a.lr, a.mu, a.wd, a.first != 0);
+                reinterpret_cast<float4*>(a.p + lo)[i] = make_float4((float)pd[0], (float)pd[1], (float)pd[2], (float)pd[3]);
+                reinterpret_cast<float4*>(a.b + lo)[i] = make_float4((float)bd[0], (float)bd[1], (float)bd[2], (float)bd[3]);
+                if (a.out) reinterpret_cast<float4*>(a.out + lo)[i] = gv;
+            }
+            for (long long qd = lo + n4 * 4 + tid; qd < hi; qd += 256) {
+                const double g = (double)__ldcg(a.agg_own + qd);
+                double pq = a.p[qd], bq = a.first ? 0.0 : (double)a.b[qd];
+                sgd_elem(g, pq, bq, a.lr, a.mu, a.wd, a.first != 0);
+                a.p[qd] = (float)pq;
+                a.b[qd] = (float)bq;
+                if (a.out) a.out[qd] = (float)g;
+            }
+            __syncthreads();
+        }
+    }
+}
+
 inline long long peer_blocks(long long n4) {
     long long blocks = (n4 + 255) / 256;
     const long long cap = (long long)num_sms() * 8;
@@ -1825,6 +1991,63 @@ int sg_peer_reduce_push_f32(int nranks, const float* const* src, const double* w
     launch_pdl(k_peer_reduce_slice, dim3((unsigned)peer_blocks((hi - lo) / 4 / 2 + 1)), dim3(256), 0,
                (cudaStream_t)stream, r, nranks, weights ? 0 : 1, lo, hi, guard_n > 0 ? guard : nullptr, guard_n, d,
                nranks);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+size_t sg_dense_exchange_flag_words(int64_t dim, int nranks) {
+    if (dim < 1 || nranks < 1) return 0;
+    const long long nchunk = (dim + XC - 1) / XC;
+    return (size_t)nchunk * (size_t)nranks + (size_t)nchunk;
+}
+
+int sg_dense_exchange_f32(int nranks, int rank, int k, const double* weights, const float* dense, int64_t ld,
+                          int64_t dim, const float* const* partials, float* const* aggs, unsigned* const* flags,
+                          unsigned epoch, const uint8_t* guard, int guard_n, float* out, float* params,
+                          float* momentum_buf, double lr, double momentum, double weight_decay, int first_step,
+                          void* stream) {
+    if (nranks < 1 || nranks > MAX_PEERS || rank < 0 || rank >= nranks || !partials || !aggs || !flags || dim < 1 ||
+        !params || !momentum_buf || guard_n < 0 || guard_n > MAX_WORKERS || (guard_n > 0 && !guard) || epoch == 0)
+        return SG_ERR_INVALID;
+    if (dense && (k < 1 || k > 8 || !weights || ld < dim)) return SG_ERR_INVALID;
+    if (dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
+    DxArgs a = {};
+    a.dense = dense;
+    a.ld = ld;
+    a.dim = dim;
+    a.k = dense ? k : 0;
+    a.P = nranks;
+    a.rank = rank;
+    a.nchunk = (int)((dim + XC - 1) / XC);
+    for (int j = 0; dense && j < k; ++j) a.w.v[j] = weights[j];
+    const long long pw = (long long)a.nchunk * nranks;  // pflag words; aflag follows
+    for (int q = 0; q < nranks; ++q) {
+        if (!partials[q] || !aggs[q] || !flags[q] || reinterpret_cast<size_t>(partials[q]) % 16 ||
+            reinterpret_cast<size_t>(aggs[q]) % 16)
+            return SG_ERR_UNSUPPORTED;
+        a.partial_src[q] = partials[q];
+        a.agg[q] = aggs[q];
+        a.pflag[q] = flags[q];
+        a.aflag[q] = flags[q] + pw;
+    }
+    a.partial_own = const_cast<float*>(partials[rank]);
+    a.agg_own = aggs[rank];
+    a.pflag_own = flags[rank];
+    a.aflag_own = flags[rank] + pw;
+    a.epoch = epoch;
+    a.guard = guard_n > 0 ? guard : nullptr;
+    a.gn = guard_n;
+    a.out = out;
+    a.p = params;
+    a.b = momentum_buf;
+    a.lr = lr;
+    a.mu = momentum;
+    a.wd = weight_decay;
+    a.first = first_step;
+    if (reinterpret_cast<size_t>(params) % 16 || reinterpret_cast<size_t>(momentum_buf) % 16 ||
+        (out && reinterpret_cast<size_t>(out) % 16) || (dense && (reinterpret_cast<size_t>(dense) % 16 || ld % 4)))
+        return SG_ERR_UNSUPPORTED;
+    a.roles_per = num_sms();  // one CTA per SM per role, all co-resident (cooperative launch)
+    launch_coop(k_dense_exchange, dim3((unsigned)(3 * a.roles_per)), dim3(256), 0, (cudaStream_t)stream, a);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

@@ -44,7 +44,7 @@ constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
-constexpr int EST_G = 64;        // sampling CTAs per worker (k_sample)
+constexpr int EST_G = 16;        // sampling CTAs per worker (k_sample)
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
 constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
@@ -176,9 +176,9 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.off_bkey = take(sizeof(K) * bcap);
     p.off_bidx = take(sizeof(uint32_t) * bcap);
     p.off_bpos = take(sizeof(uint32_t) * bcap);
-    // float32 sample histogram (key bits [30:20]): filled by k_sample, read and re-zeroed by
-    // k_estimate, so it is zero between calls (outside k_sample's per-call zero range)
-    p.off_hs1 = take(sizeof(unsigned) * (size_t)k * SEL_BINS);
+    // float32 level-1 sample histograms (key bits [30:20]): one dense row per sampling CTA,
+    // written whole by k_sample (no atomics, no state between calls), summed by k_estimate
+    p.off_hs1 = take(sizeof(unsigned) * (size_t)k * EST_G * SEL_BINS);
     p.total = o + 256;  // slack for base alignment
     return p;
 }
@@ -413,7 +413,7 @@ k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
     using K = typename KO::K;
     constexpr bool H1 = sizeof(K) == 4;  // float32: level-1 histogram of the sample here
     __shared__ K s_min[8], s_max[8];
-    __shared__ unsigned s_h1[H1 ? SEL_BINS : 1];
+    __shared__ __align__(16) unsigned s_h1[H1 ? SEL_BINS : 1];
     const int x = blockIdx.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if constexpr (H1) {
         for (int i = tid; i < SEL_BINS; i += 256) s_h1[i] = 0;
@@ -484,10 +484,10 @@ k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
         mm[cta * 2] = a;
         mm[cta * 2 + 1] = b;
     }
-    if constexpr (H1) {
-        unsigned* gh = hs1 + (long long)w * SEL_BINS;
-        for (int i = tid; i < SEL_BINS; i += 256)
-            if (s_h1[i]) atomicAdd(gh + i, s_h1[i]);
+    if constexpr (H1) {  // this CTA's row, written whole (coalesced 16-byte stores)
+        uint4* gh = reinterpret_cast<uint4*>(hs1 + cta * SEL_BINS);
+        const uint4* sh = reinterpret_cast<const uint4*>(s_h1);
+        for (int i = tid; i < SEL_BINS / 4; i += 256) gh[i] = sh[i];
     }
 }
 
@@ -539,18 +539,41 @@ k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf
         // the r_est-th largest sample key.
         (void)lo;
         (void)shift;
-        unsigned* gh = hs1 + (long long)w * SEL_BINS;
-        for (int i = tid; i < SEL_BINS; i += EST_THREADS) hist[i] = __ldcg(gh + i);
+        const unsigned* gh = hs1 + (long long)w * G * SEL_BINS;
+        for (int i = tid; i < SEL_BINS; i += EST_THREADS) {
+            unsigned v = 0;
+            for (int r = 0; r < G; ++r) v += __ldcg(gh + (long long)r * SEL_BINS + i);
+            hist[i] = v;
+        }
         __syncthreads();
         if (r_est <= ns) {
             int b1;
             unsigned long long a1;
             block_find_bin_from_top<SEL_BINS, EST_THREADS>(hist, (unsigned long long)r_est, b1, a1);
-            for (int i = tid; i < SEL_BINS; i += EST_THREADS) gh[i] = 0;  // zero for the next call
             if (b1 >= 0) {
                 for (int i = tid; i < SEL_BINS; i += EST_THREADS) hist[i] = 0;
                 __syncthreads();
-                for (long long i = tid; i < ns; i += EST_THREADS) {
+                // level 2 over the keys of bin b1: 16-byte loads, several in flight
+                const long long n4 = ns / 4;
+                const uint4* s4 = reinterpret_cast<const uint4*>(sk);
+                constexpr int U = 8;
+                for (long long i0 = tid; i0 < n4; i0 += (long long)EST_THREADS * U) {
+                    uint4 v[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const long long i = i0 + (long long)u * EST_THREADS;
+                        v[u] = i < n4 ? __ldcg(s4 + i) : make_uint4(0u, 0u, 0u, 0u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (i0 + (long long)u * EST_THREADS >= n4) break;
+                        const unsigned kk[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if ((int)(kk[c] >> 20) == b1) atomicAdd(&hist[(kk[c] >> 9) & (SEL_BINS - 1)], 1u);
+                    }
+                }
+                for (long long i = n4 * 4 + tid; i < ns; i += EST_THREADS) {
                     const K key = sk[i];
                     if ((int)(key >> 20) == b1) atomicAdd(&hist[(key >> 9) & (SEL_BINS - 1)], 1u);
                 }
@@ -560,8 +583,6 @@ k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf
                 block_find_bin_from_top<SEL_BINS, EST_THREADS>(hist, (unsigned long long)r_est - a1, b2, a2);
                 est = ((K)b1 << 20) | (b2 >= 0 ? ((K)b2 << 9) : (K)0);
             }
-        } else {
-            for (int i = tid; i < SEL_BINS; i += EST_THREADS) gh[i] = 0;
         }
     } else {
         if (r_est <= ns) {
@@ -2166,8 +2187,10 @@ size_t sg_topk_workspace_bytes_fused_f32(int k, int64_t dim, int64_t m) {
 }
 
 size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m) {
-    // the launch chain keeps its sample histogram zeroed between calls (k_estimate clears it)
-    return sg_topk_workspace_bytes_f32(k, dim, m);
+    (void)k;  // the launch chain keeps no state between calls
+    (void)dim;
+    (void)m;
+    return 0;
 }
 
 size_t sg_topk_workspace_zero_bytes_fused_f32(int k, int64_t dim, int64_t m) {

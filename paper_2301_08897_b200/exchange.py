@@ -229,6 +229,7 @@ class GradientExchange:
             self._symm = None
             self._partial_h = None
             self._agg_h = None
+            self._flag_h = None
             self._setup_peer_buffers(None)
             if self._partial_h is not None:
                 ph = self._partial_h
@@ -251,16 +252,29 @@ class GradientExchange:
         self.steps = 0
 
     def _push_args(self) -> dict:
-        """Dense side in push mode (default): every rank's reduced slice is pushed into every
-        rank's aggregate buffer; SG_DENSE_PULL=1 keeps the pull all-gather (A/B runs)."""
-        if os.environ.get("SG_DENSE_PULL", "0") == "1":
+        """Dense side mode (SG_DENSE_MODE, for A/B runs): "fused" (default) -- one pipelined
+        launch (sg_dense_exchange_f32); "push" -- reduce-and-push, barrier, local update;
+        "pull" -- reduce, barrier, pull all-gather fused with the update."""
+        mode = os.environ.get("SG_DENSE_MODE", "fused")
+        if mode == "pull":
             return {}
         h = self._agg_h
         off = self._agg_buf.data_ptr() - h.buffer_ptrs[self.rank]
-        return dict(agg=self._agg_buf, agg_ptrs=[h.buffer_ptrs[r] + off for r in range(self.world)])
+        args = dict(agg=self._agg_buf, agg_ptrs=[h.buffer_ptrs[r] + off for r in range(self.world)])
+        if mode == "fused":
+            fh = self._flag_h
+            foff = self._flag_buf.data_ptr() - fh.buffer_ptrs[self.rank]
+            args["flag_ptrs"] = [fh.buffer_ptrs[r] + foff for r in range(self.world)]
+        return args
 
-    def _dense_side(self, launchers, lr, first, out, barrier) -> None:
-        """partial -> barrier -> reduce (push, or pull at the all-gather) -> barrier -> SGD."""
+    def _dense_side(self, launchers, lr, first, out, barrier, w_local=None, bucket=None) -> None:
+        """The dense side after the local partial: fused pipelined launch, or
+        barrier -> reduce (push, or pull at the all-gather) -> barrier -> SGD."""
+        if launchers._flags is not None:
+            launchers.dense_exchange(w_local, bucket, lr, first, out)
+            return
+        if bucket is not None:
+            launchers.partial(w_local, bucket)
         barrier()
         if launchers._aggp is not None:
             launchers.reduce_push()
@@ -294,6 +308,10 @@ class GradientExchange:
             agg = symm_mem.empty(self.ld, dtype=torch.float32, device=self.device)
             agg.zero_()
             agg_h = symm_mem.rendezvous(agg, grp.group_name)
+            nfw = int(_capi.load().sg_dense_exchange_flag_words(self.dim, self.world))
+            flg = symm_mem.empty(max(nfw, 4), dtype=torch.int32, device=self.device)
+            flg.zero_()
+            flg_h = symm_mem.rendezvous(flg, grp.group_name)
         except Exception:  # no peer mapping on this system
             ok = 0
         flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
@@ -303,10 +321,12 @@ class GradientExchange:
             self._symm, self.pack = symm, pack
             self._partial_buf, self._partial_h = part, part_h
             self._agg_buf, self._agg_h = agg, agg_h
+            self._flag_buf, self._flag_h = flg, flg_h
         else:
             self._symm = None
             self._partial_h = None
             self._agg_h = None
+            self._flag_h = None
 
     # -- the step ---------------------------------------------------------------------------
 
@@ -383,9 +403,10 @@ class GradientExchange:
         if self._dense_peer is not None:
             # dense workload over peer memory: O(D) NVLink bytes per rank, fused update
             h = self._partial_h
-            self._dense_peer.partial(w[self.lo:self.lo + self.k], self.bucket)
-            self._dense_side(self._dense_peer, opt["lr"], opt["first_step"], out, lambda: h.barrier(channel=0))
-            h.barrier(channel=0)  # no rank rewrites its partial / aggregate while a peer still uses it
+            self._dense_side(self._dense_peer, opt["lr"], opt["first_step"], out, lambda: h.barrier(channel=0),
+                             w_local=w[self.lo:self.lo + self.k], bucket=self.bucket)
+            if self._dense_peer._flags is None:
+                h.barrier(channel=0)  # no rank rewrites its partial / aggregate while a peer still uses it
             return "dense-peer"
         if self.packed and self._symm is not None:
             # Peer path, no host synchronisation: after a device barrier (every rank's Top-k has
@@ -406,6 +427,8 @@ class GradientExchange:
             # one of the two sides does work in any step)
             self._side.wait_event(self._gathered)
             with torch.cuda.stream(self._side):
+                # mixed decisions: the local partial densifies the compressed local workers,
+                # then the dense side exchanges it (a no-op when every worker compressed)
                 self._dense.partial(w[self.lo:self.lo + self.k], self.bucket)
                 self._dense_side(self._dense, lr, first, out, lambda: self._symm.barrier(channel=1))
             self._peer_merge(w, lr, first, out)

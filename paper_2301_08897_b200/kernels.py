@@ -344,8 +344,11 @@ class GuardedDenseLaunchers:
 
     def __init__(self, k: int, dim: int, ld: int, compressed, idx, val, row_ptr, tile_off, partial: torch.Tensor,
                  partial_ptrs, guard, params, momentum_buf, momentum: float, weight_decay: float, rank: int,
-                 agg: torch.Tensor | None = None, agg_ptrs=None):
+                 agg: torch.Tensor | None = None, agg_ptrs=None, flag_ptrs=None):
         lib = _capi.load()
+        # fused mode (flag_ptrs given): the whole dense side in one pipelined launch
+        self._flags = (ctypes.c_void_p * len(flag_ptrs))(*flag_ptrs) if flag_ptrs is not None else None
+        self._epoch = 0
         # push mode (agg given): the reduced slice is pushed into every rank's aggregate buffer
         # (sg_peer_reduce_push_f32) and each rank updates from its own copy
         self._agg = agg.data_ptr() if agg is not None else None
@@ -378,6 +381,20 @@ class GuardedDenseLaunchers:
         st = self._part(self._k, self._wp, self._comp, bucket.data_ptr(), self._ld, self._idx, self._val, self._rp,
                         self._toff, self._dim, self._partial, self._guard, self._gn, None, 0, _stream())
         _capi.check(st, "sg_weighted_partial_f32")
+        _count(1)
+
+    def dense_exchange(self, local_weights, bucket: torch.Tensor | None, lr: float, first_step: bool,
+                       out: torch.Tensor | None = None) -> None:
+        """sg_dense_exchange_f32: fold (bucket rows, or the partial already written) -> reduce ->
+        push -> update, pipelined over chunks in one cooperative launch."""
+        self._epoch += 1
+        if bucket is not None:
+            self._w[:] = local_weights
+        st = _capi.load().sg_dense_exchange_f32(
+            len(self._pp), self._rank, self._k, self._wp, _ptr(bucket), self._ld, self._dim, self._pp, self._aggp,
+            self._flags, self._epoch, self._guard, self._gn, _ptr(out), self._p, self._b, float(lr), self._mu,
+            self._wd, int(bool(first_step)), _stream())
+        _capi.check(st, "sg_dense_exchange_f32")
         _count(1)
 
     def reduce_push(self) -> None:

@@ -41,6 +41,25 @@ def main():
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     rows = []
     wl = w[ex.lo:ex.lo + ex.k]
+    if dp._flags is not None:  # fused: one pipelined launch for the whole dense side
+        ts = []
+        for _ in range(10):
+            dist.barrier()
+            torch.cuda.synchronize()
+            ev[0].record()
+            dp.dense_exchange(wl, ex.bucket, 0.01, False, None)
+            ev[6].record()
+            torch.cuda.synchronize()
+            ts.append(ev[0].elapsed_time(ev[6]))
+        t = torch.tensor([float(np.median(ts))], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            L = (D + P - 1) // P
+            print(json.dumps(dict(P=P, mode="fused", total_us_max_over_ranks=round(float(t.item()) * 1e3, 1),
+                                  nvlink_GBps_per_direction=round(2 * (P - 1) * L * 4 / (float(t.item()) * 1e-3) / 1e9 / 2, 1))),
+                  flush=True)
+        dist.destroy_process_group()
+        return
     for _ in range(10):
         dist.barrier()
         torch.cuda.synchronize()
