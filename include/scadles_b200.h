@@ -216,6 +216,13 @@ int sg_peer_reduce_push_f32(int nranks, const float* const* src, const double* w
  * sg_dense_exchange_flag_words(dim, P) zero-initialised words; epoch >= 1, increasing by one per
  * call, identical on every rank).  partials / aggs / flags: HOST arrays of nranks device
  * pointers (peers' memory).  Replaces the partial + all-reduce + SGD of engine.py:270-283. */
+/* NVLink SHARP: rank `rank`'s slice (sg_peer_slice_len) of the dense side reduced IN THE
+ * SWITCH over every rank's partial (multimem.ld_reduce on the multicast address mc_src of the
+ * peer-mapped partial buffers, float32 adds) and broadcast to every rank's aggregate buffer
+ * with one multicast store (mc_dst).  After a barrier each rank updates from its own copy
+ * (sg_peer_allgather_sgd_f32 with one source).  4D NVLink bytes per rank and direction. */
+int sg_nvls_reduce_bcast_f32(int nranks, int rank, const float* mc_src, float* mc_dst, int64_t dim,
+                             const uint8_t* guard, int guard_n, void* stream);
 size_t sg_dense_exchange_flag_words(int64_t dim, int nranks);
 int sg_dense_exchange_f32(int nranks, int rank, int k, const double* weights, const float* dense, int64_t ld,
                           int64_t dim, const float* const* partials, float* const* aggs, unsigned* const* flags,

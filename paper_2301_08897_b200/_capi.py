@@ -104,6 +104,7 @@ SIGNATURES = {
         [c_int, POINTER(c_void_p), POINTER(c_double), c_int, _P, c_int, c_int64, POINTER(c_void_p), _P],
     ),
     "sg_dense_exchange_flag_words": (c_size_t, [c_int64, c_int]),
+    "sg_nvls_reduce_bcast_f32": (c_int, [c_int, c_int, _P, _P, c_int64, _P, c_int, _P]),
     "sg_dense_exchange_f32": (
         c_int,
         [c_int, c_int, c_int, POINTER(c_double), _P, c_int64, c_int64, POINTER(c_void_p), POINTER(c_void_p),

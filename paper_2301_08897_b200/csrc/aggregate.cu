@@ -1851,6 +1851,57 @@ k_dense_exchange(DxArgs a) {
     }
 }
 
+// ---- NVLink SHARP (NVLS) reduce + broadcast through the switch ---------------------------------
+// Rank r's slice of the dense side in one pass over multicast addresses: each 16-byte group is
+// summed IN THE SWITCH over every rank's partial (multimem.ld_reduce, float32 adds) and the sum
+// is written back to every rank's aggregate buffer with one multicast store (multimem.st).
+// Per rank and direction that moves 4D bytes over NVLink instead of the 2(P-1)/P * 4D of a
+// ring or of the pull/push exchanges; the result is identical on every rank (each element is
+// reduced once, by its owner).  Guarded like the rest of the dense side.
+SG_DEV float4 mm_ld_reduce_add_v4(const float* mc) {
+    float4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(mc) : "memory");
+    return v;
+}
+SG_DEV void mm_st_v4(float* mc, float4 v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};"
+                 ::"l"(mc), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+SG_DEV float mm_ld_reduce_add(const float* mc) {
+    float v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(mc) : "memory");
+    return v;
+}
+SG_DEV void mm_st(float* mc, float v) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256)
+k_nvls_reduce_bcast(const float* mc_src, float* mc_dst, long long lo, long long hi, const uint8_t* __restrict__ guard,
+                    int gn) {
+    pdl_enter();
+    if (!peer_guard_run(guard, gn)) return;
+    const long long n4 = (hi - lo) / 4, stride = (long long)gridDim.x * blockDim.x;
+    constexpr int U = 4;  // independent multicast reductions in flight per thread
+    for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = i0 + u * stride;
+            if (i < n4) v[u] = mm_ld_reduce_add_v4(mc_src + lo + 4 * i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = i0 + u * stride;
+            if (i < n4) mm_st_v4(mc_dst + lo + 4 * i, v[u]);
+        }
+    }
+    for (long long q = lo + n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += stride)
+        mm_st(mc_dst + q, mm_ld_reduce_add(mc_src + q));
+    __threadfence_system();  // the multicast stores are visible system-wide before the barrier
+}
+
 inline long long peer_blocks(long long n4) {
     long long blocks = (n4 + 255) / 256;
     const long long cap = (long long)num_sms() * 8;
@@ -1991,6 +2042,21 @@ int sg_peer_reduce_push_f32(int nranks, const float* const* src, const double* w
     launch_pdl(k_peer_reduce_slice, dim3((unsigned)peer_blocks((hi - lo) / 4 / 2 + 1)), dim3(256), 0,
                (cudaStream_t)stream, r, nranks, weights ? 0 : 1, lo, hi, guard_n > 0 ? guard : nullptr, guard_n, d,
                nranks);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+int sg_nvls_reduce_bcast_f32(int nranks, int rank, const float* mc_src, float* mc_dst, int64_t dim,
+                             const uint8_t* guard, int guard_n, void* stream) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || !mc_src || !mc_dst || dim < 1 || guard_n < 0 ||
+        guard_n > MAX_WORKERS || (guard_n > 0 && !guard))
+        return SG_ERR_INVALID;
+    if (reinterpret_cast<size_t>(mc_src) % 16 || reinterpret_cast<size_t>(mc_dst) % 16) return SG_ERR_UNSUPPORTED;
+    const long long L = peer_slice_len(dim, nranks);
+    long long lo = (long long)rank * L, hi = lo + L < dim ? lo + L : dim;
+    if (lo > dim) lo = dim;
+    if (hi < lo) hi = lo;
+    launch_pdl(k_nvls_reduce_bcast, dim3((unsigned)peer_blocks((hi - lo) / 4 / 4 + 1)), dim3(256), 0,
+               (cudaStream_t)stream, mc_src, mc_dst, lo, hi, guard_n > 0 ? guard : nullptr, guard_n);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

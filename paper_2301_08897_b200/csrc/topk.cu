@@ -44,7 +44,7 @@ constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
-constexpr int EST_G = 16;        // sampling CTAs per worker (k_sample)
+constexpr int EST_G = 32;        // sampling CTAs per worker (k_sample)
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
 constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
@@ -439,7 +439,7 @@ k_sample(const T* __restrict__ g, long long ld, long long dim, long long s_eff,
         const long long nch = s_eff / CHUNK;
         const long long stratum = dim / nch;  // >= CHUNK because dim > s_eff
         const int gw = x * 8 + warp, nwarps = gridDim.x * 8;
-        constexpr int BATCH = 4;
+        constexpr int BATCH = 8;
         for (long long c0 = gw; c0 < nch; c0 += (long long)nwarps * BATCH) {
             T v[BATCH];
 #pragma unroll

@@ -255,17 +255,38 @@ class GradientExchange:
         """Dense side mode (SG_DENSE_MODE, for A/B runs): "fused" (default) -- one pipelined
         launch (sg_dense_exchange_f32); "push" -- reduce-and-push, barrier, local update;
         "pull" -- reduce, barrier, pull all-gather fused with the update."""
-        mode = os.environ.get("SG_DENSE_MODE", "fused")
+        mode = os.environ.get("SG_DENSE_MODE", "nvls")
+        if mode == "nvls" and not self._multicast_ok():
+            mode = "pull"
         if mode == "pull":
             return {}
         h = self._agg_h
         off = self._agg_buf.data_ptr() - h.buffer_ptrs[self.rank]
         args = dict(agg=self._agg_buf, agg_ptrs=[h.buffer_ptrs[r] + off for r in range(self.world)])
+        if mode == "nvls":
+            ph = self._partial_h
+            poff = self._partial_buf.data_ptr() - ph.buffer_ptrs[self.rank]
+            args["mc_partial"] = int(ph.multicast_ptr) + poff
+            args["mc_agg"] = int(h.multicast_ptr) + off
         if mode == "fused":
             fh = self._flag_h
             foff = self._flag_buf.data_ptr() - fh.buffer_ptrs[self.rank]
             args["flag_ptrs"] = [fh.buffer_ptrs[r] + foff for r in range(self.world)]
         return args
+
+    def _multicast_ok(self) -> bool:
+        """NVLS multicast on both peer-mapped buffers, on every rank (collective decision)."""
+        ok = 1
+        try:
+            for h in (self._partial_h, self._agg_h):
+                if not (h.has_multicast_support() if callable(getattr(h, "has_multicast_support", None))
+                        else h.has_multicast_support) or int(h.multicast_ptr) == 0:
+                    ok = 0
+        except Exception:
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        return int(flag.item()) == 1
 
     def _dense_side(self, launchers, lr, first, out, barrier, w_local=None, bucket=None) -> None:
         """The dense side after the local partial: fused pipelined launch, or
@@ -276,7 +297,11 @@ class GradientExchange:
         if bucket is not None:
             launchers.partial(w_local, bucket)
         barrier()
-        if launchers._aggp is not None:
+        if launchers._mc is not None:  # NVLS: reduce in the switch, multicast the slice
+            launchers.nvls_reduce_bcast()
+            barrier()
+            launchers.local_sgd(lr, first, out)
+        elif launchers._aggp is not None:
             launchers.reduce_push()
             barrier()
             launchers.local_sgd(lr, first, out)

@@ -344,8 +344,10 @@ class GuardedDenseLaunchers:
 
     def __init__(self, k: int, dim: int, ld: int, compressed, idx, val, row_ptr, tile_off, partial: torch.Tensor,
                  partial_ptrs, guard, params, momentum_buf, momentum: float, weight_decay: float, rank: int,
-                 agg: torch.Tensor | None = None, agg_ptrs=None, flag_ptrs=None):
+                 agg: torch.Tensor | None = None, agg_ptrs=None, flag_ptrs=None, mc_partial=None, mc_agg=None):
         lib = _capi.load()
+        # NVLS mode (multicast addresses given): reduce in the switch + multicast broadcast
+        self._mc = (mc_partial, mc_agg) if mc_partial else None
         # fused mode (flag_ptrs given): the whole dense side in one pipelined launch
         self._flags = (ctypes.c_void_p * len(flag_ptrs))(*flag_ptrs) if flag_ptrs is not None else None
         self._epoch = 0
@@ -395,6 +397,12 @@ class GuardedDenseLaunchers:
             self._flags, self._epoch, self._guard, self._gn, _ptr(out), self._p, self._b, float(lr), self._mu,
             self._wd, int(bool(first_step)), _stream())
         _capi.check(st, "sg_dense_exchange_f32")
+        _count(1)
+
+    def nvls_reduce_bcast(self) -> None:
+        st = _capi.load().sg_nvls_reduce_bcast_f32(len(self._pp), self._rank, self._mc[0], self._mc[1], self._dim,
+                                                   self._guard, self._gn, _stream())
+        _capi.check(st, "sg_nvls_reduce_bcast_f32")
         _count(1)
 
     def reduce_push(self) -> None:

@@ -68,7 +68,9 @@ def main():
         ev[1].record()
         h.barrier(channel=0)
         ev[2].record()
-        if dp._aggp is not None:
+        if dp._mc is not None:
+            dp.nvls_reduce_bcast()
+        elif dp._aggp is not None:
             dp.reduce_push()
         else:
             dp.reduce_slice()
@@ -102,9 +104,11 @@ def main():
     t_ar = float(np.median(ts)) / 1e3
     L = (D + P - 1) // P
     nvl = (P - 1) * L * 4  # bytes read over NVLink per rank, each of the two phases
-    rep = dict(rank=rank, P=P, mode="pull" if dp._aggp is None else "push", partial_us=med[0], bar1_us=med[1], reduce_us=med[2], bar2_us=med[3],
+    rep = dict(rank=rank, P=P, mode="nvls" if dp._mc is not None else ("pull" if dp._aggp is None else "push"),
+               partial_us=med[0], bar1_us=med[1], reduce_us=med[2], bar2_us=med[3],
                allgather_sgd_us=med[4], bar3_us=med[5], total_us=med[6],
                reduce_nvlink_GBps=nvl / (med[2] * 1e-6) / 1e9, allgather_nvlink_GBps=nvl / (med[4] * 1e-6) / 1e9,
+               nvls_reduce_bcast_GBps_4D=4 * D / (med[2] * 1e-6) / 1e9,
                nccl_allreduce_us=t_ar * 1e6, nccl_busbw_GBps=2 * (P - 1) / P * 4 * D / t_ar / 1e9)
     if rank == 0:
         print(json.dumps({k: (round(v, 1) if isinstance(v, float) else v) for k, v in rep.items()}), flush=True)
