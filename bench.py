@@ -36,7 +36,7 @@ METRIC = "aggregated grad elems/sec & HBM GB/s (%roofline) per step at 1/2/4/8 B
 UNIT = "elem/s"
 MEASURED = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
-NVLINK_GBPS = 900.0  # NVLink 5 per direction per GPU (nominal; no nccl-tests busbw taken)
+NVLINK_GBPS = 900.0  # NVLink 5 per direction per GPU, nominal (N > 1 measures the NCCL busbw instead)
 
 
 def parse():
@@ -442,6 +442,24 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # NVLink roofline denominator at N > 1: the measured NCCL all-reduce bus bandwidth of a
+    # D-float buffer on this box (busbw = 2(P-1)/P * bytes / t), not the nominal 900 GB/s
+    nvl_peak, nvl_kind = NVLINK_GBPS, "nominal"
+    if world > 1:
+        buf = torch.randn(D, device=dev)
+        for _ in range(2):
+            dist.all_reduce(buf)
+        barrier()
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record()
+        for _ in range(3):
+            dist.all_reduce(buf)
+        b_ev.record()
+        barrier()
+        t_ar = reduce_max(a_ev.elapsed_time(b_ev)) / 3 / 1e3
+        nvl_peak, nvl_kind = 2 * (world - 1) / world * 4 * D / t_ar / 1e9, "measured NCCL all-reduce busbw"
+        del buf
+
     # ---- device-resident timing -------------------------------------------------------
     cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
     clocks = Clocks(cvd.split(",")[local] if cvd else local)
@@ -498,9 +516,9 @@ def run_ours(args):
     # or the dense all-reduce's 2(P-1)/P * 4D (busbw convention); nominal 900 GB/s per direction
     if world > 1:
         nvl = (world - 1) * k * 8 * m if (compression and all_sparse) else 2 * (world - 1) / world * 4 * D
-        nvl_frac = nvl / step_s / 1e9 / NVLINK_GBPS
-        step_roof["nvlink"] = {"bytes_per_step": nvl, "achieved": nvl / step_s / 1e9, "peak": NVLINK_GBPS,
-                               "peak_kind": "nominal", "frac": nvl_frac}
+        nvl_frac = nvl / step_s / 1e9 / nvl_peak
+        step_roof["nvlink"] = {"bytes_per_step": nvl, "achieved": nvl / step_s / 1e9, "peak": nvl_peak,
+                               "peak_kind": nvl_kind, "frac": nvl_frac}
         step_roof["binding"] = "nvlink" if nvl_frac > step_roof["frac"] else "hbm"
     else:
         step_roof["binding"] = "hbm"

@@ -22,6 +22,15 @@ def main():
     # a peer read inside a torch kernel, and a raw-pointer offset
     local_ptr, peer_ptr = h.buffer_ptrs[rank], h.buffer_ptrs[(rank + 1) % world]
     print(rank, "delta words", (peer_ptr - local_ptr) // 4, flush=True)
+    from torch._C._distributed_c10d import _SymmetricMemory as S
+    try:
+        print(rank, "device multicast support", S.has_multicast_support(torch._C._autograd.DeviceType.CUDA, local), flush=True)
+    except Exception as e:  # noqa: BLE001
+        print(rank, "has_multicast_support(device) failed", repr(e), flush=True)
+    try:
+        print(rank, "handle multicast_ptr", h.multicast_ptr, flush=True)
+    except Exception as e:  # noqa: BLE001
+        print(rank, "multicast_ptr failed", repr(e), flush=True)
     h.barrier(channel=0)
     dist.destroy_process_group()
 
