@@ -160,6 +160,7 @@ template <typename TI, typename TO> struct AggArgs {
     int own;        // all-sparse merge kernel: -1 by density, 0 k_merge_ws, 1 k_merge_own
     int pf;         // k_merge_own: prefetch the next tile's p / buf into L2
     int cost_j0, cost_j1;  // workers whose offsets estimate the tile costs (local memory)
+    int direct;     // k_merge_ws: chunks of multi-chunk tiles fold run by run (no lists)
 };
 
 template <typename TI, typename TO>
@@ -689,6 +690,14 @@ SG_DEV int sparse_merge_is_mine(const AggArgs<float, TO>& a, bool want_dense) {
     return all_comp && dense == want_dense;
 }
 
+inline int mw_direct() {  // SG_MW_DIRECT=0: every chunk through the position lists (A/B runs)
+    static const int v = [] {
+        const char* e = getenv("SG_MW_DIRECT");
+        return (e && *e == '0') ? 0 : 1;
+    }();
+    return v;
+}
+
 // Cost-balanced merge tile ranges (always on; the equal-range split was the round-1 ablation).
 inline int mw_balance() { return 1; }
 inline int merge_mode(int m) { return m < 0 ? -1 : (m > 0 ? 1 : 0); }
@@ -713,6 +722,7 @@ k_merge_ws(const AggArgs<float, TO> a) {
     __shared__ int so_lo[OR][MP_MAXW];       // worker j's merge offsets at the tile's two edges
     __shared__ int so_hi[OR][MP_MAXW];
     __shared__ int4 s_hdr[MW_SLOTS];  // staged chunk: {tile, c0, entries, last}
+    __shared__ int s_direct[MW_SLOTS];  // staged chunk folds run by run (long worker runs)
     __shared__ __align__(8) unsigned long long fullb[MW_STAGES];
     __shared__ const uint32_t* s_ib[MP_MAXW];  // worker j's entries (local, or a peer GPU's)
     __shared__ const float* s_vb[MP_MAXW];
@@ -917,6 +927,10 @@ k_merge_ws(const AggArgs<float, TO> a) {
                         swk[slot * MW_ECAP + (e - cc0)] = (uint8_t)j;
                     }
                 }
+                // fold mode: tiles of more than one chunk (candidate-dense; their chunks hold a
+                // few long worker runs) fold run by run.  (A per-chunk run-length test here cost
+                // ~6 % of the sparse merge: it sits on the staging path of every chunk.)
+                if (pt == 0) s_direct[slot] = a.direct && cE > MW_ECAP;
                 if (pt == 0) s_hdr[slot] = make_int4(ci, cc0, c1 - cc0, c1 == cE);
                 if (c1 < cE) {
                     cc0 = c1;
@@ -950,6 +964,31 @@ k_merge_ws(const AggArgs<float, TO> a) {
             const uint32_t* si = sidx + slot * MW_ECAP;
             const float* sv = sval + slot * MW_ECAP;
             const uint8_t* sw8 = swk + slot * MW_ECAP;
+            // Candidate-dense tiles (real gradients) give chunks of one or a few long worker
+            // runs (entries [c0, c0 + ne) of the tile's worker-major order):
+            // one worker's positions are distinct, so such a chunk folds run by run straight
+            // into the tile (a producer barrier between runs keeps the ascending worker order)
+            // -- no lists, the same operations in the same order as the list fold below.
+            if (s_direct[slot]) {
+                if (c0 == 0 && i >= 2) bar_sync(BAR_EMPTY + b, MW_CONS + MW_PROD);  // buffer b released
+                int pre = 0, done = 0;
+                for (int j = 0; j < nw; ++j) {
+                    const int cnt = so_hi[i % OR][j] - so_lo[i % OR][j];
+                    const int lo = pre > c0 ? pre : c0, hi = pre + cnt < c0 + ne ? pre + cnt : c0 + ne;
+                    pre += cnt;
+                    if (hi <= lo) continue;
+                    if (done++) bar_sync(BAR_PROD, MW_PROD);  // the previous run's folds are visible
+                    const double wj = a.w[j];
+                    for (int n = lo - c0 + pt; n < hi - c0; n += MW_PROD) {
+                        const unsigned q = si[n] - tb;
+                        const double r = mb[q] ? ab[q] : 0.0;
+                        ab[q] = dadd(r, dmul(wj, (double)sv[n]));
+                        mb[q] = 1;
+                    }
+                }
+                if (hd.w) bar_arrive(BAR_FULL + b, MW_CONS + MW_PROD);  // buffer b holds tile i's values
+                continue;
+            }
             // (1) push every entry onto its position's list
             for (int n = pt; n < ne; n += MW_PROD) {
                 const unsigned q = si[n] - tb;
@@ -1304,8 +1343,10 @@ k_merge_own(const AggArgs<float, TO> a) {
 template <typename TO>
 void launch_sparse_merge(const AggArgs<float, TO>& a, int grid, size_t sm, int sms, cudaStream_t stream) {
     if (a.own != 1) {
+        AggArgs<float, TO> aw = a;
+        aw.direct = mw_direct();
         smem_attr((const void*)k_merge_ws<TO>, (int)sm);
-        launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, a);
+        launch_pdl(k_merge_ws<TO>, dim3((unsigned)grid), dim3(MW_THREADS), sm, stream, aw);
         debug_sync("k_merge_ws", stream);
     }
     if (a.own != 0) {

@@ -1,6 +1,7 @@
 // Shared device helpers for the ScaDLES B200 hot path (sm_100a only).
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <mutex>
@@ -114,6 +115,14 @@ template <typename K> SG_DEV K warp_max(K v) {
     }
     return v;
 }
+template <typename K> SG_DEV K warp_min(K v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        K u = __shfl_xor_sync(FULL, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
 // Fixed-order butterfly: every lane ends with the same bits regardless of scheduling.
 SG_DEV double warp_sum(double v) {
 #pragma unroll
@@ -194,6 +203,11 @@ SG_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long l
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+// the same, default L2 policy
+SG_DEV void bulk_g2s_plain(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 SG_DEV unsigned long long policy_evict_first() {
     unsigned long long p;

@@ -611,6 +611,214 @@ k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf
     }
 }
 
+// k_sample_est (float32): sample + estimate in ONE launch.  A cluster of SE_CL CTAs per worker
+// gathers the same stratified sample as k_sample (chunk c at the same hashed offset), each CTA
+// keeping its 1/SE_CL of the keys in shared memory with its level-1 histogram (key bits
+// [30:20]).  Over distributed shared memory: CTA r reduces bin slice r of the cluster's
+// level-1 histograms, every CTA reads the reduced histogram and picks the same level-1 bin
+// b1, then scans only its own resident keys for that bin into CTA 0's level-2 histogram (bits
+// [19:9]); CTA 0 picks b2 and publishes est = (b1 << 20) | (b2 << 9) -- the value k_sample +
+// k_estimate compute, without the sample's trip through global memory, the per-CTA rows and
+// the one-CTA re-scan.
+// --------------------------------------------------------------------------------------
+// SG_SAMPLE_EST=0 selects the two-launch k_sample + k_estimate (A/B runs)
+inline bool sample_est_fused() {
+    static const bool on = [] {
+        const char* e = getenv("SG_SAMPLE_EST");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+inline bool se_tma() {  // SG_SE_TMA=0: the sample by per-warp loads (A/B runs)
+    static const bool on = [] {
+        const char* e = getenv("SG_SE_TMA");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+constexpr int SE_CL = 8;                                       // cluster CTAs per worker
+constexpr int SE_THREADS = 512;
+constexpr int SE_KEYS = TopkTraits<float>::SAMPLE / SE_CL;     // resident keys per CTA
+constexpr int SE_SLICE = SEL_BINS / SE_CL;                     // level-1 bins reduced per CTA
+constexpr size_t SE_SMEM = sizeof(uint32_t) * SE_KEYS;          // dynamic: the resident keys
+static_assert(SE_SLICE <= SE_THREADS && SEL_BINS % SE_THREADS == 0, "sample/estimate layout");
+
+__global__ void __cluster_dims__(SE_CL, 1, 1) __launch_bounds__(SE_THREADS)
+k_sample_est_f32(const float* __restrict__ g, long long ld, long long dim, long long s_eff, long long r_est,
+                 SelState<uint32_t>* __restrict__ sel, uint4* __restrict__ zero, long long zero_vec, int tma) {
+    pdl_enter();
+    namespace cg = cooperative_groups;
+    using KO = KeyOf<float>;
+    using K = uint32_t;
+    extern __shared__ __align__(16) K s_keys[];
+    __shared__ __align__(16) unsigned h1[SEL_BINS];   // own level-1 histogram, then the reduced one
+    __shared__ unsigned red[SE_SLICE];                // this CTA's slice of the reduced level 1
+    __shared__ unsigned h2[SEL_BINS];                 // level 2 (CTA 0's is the cluster's)
+    __shared__ K s_mn[SE_THREADS / 32], s_mx[SE_THREADS / 32];
+    __shared__ K s_cmn, s_cmx;
+    __shared__ __align__(8) unsigned long long s_bar;
+    cg::cluster_group cl = cg::this_cluster();
+    const int x = (int)cl.block_rank(), w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = SE_THREADS / 32;
+    for (int i = tid; i < SEL_BINS; i += SE_THREADS) {
+        h1[i] = 0;
+        h2[i] = 0;
+    }
+    {
+        const long long cta = (long long)w * SE_CL + x, ncta = (long long)SE_CL * gridDim.y;
+        for (long long i = cta * SE_THREADS + tid; i < zero_vec; i += ncta * SE_THREADS) zero[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    const float* row = g + (long long)w * ld;
+    K mn = KO::KMAX, mx = 0;
+    int nk = 0;  // resident keys of this CTA
+    if (s_eff == dim) {  // the sample is the whole row (dim <= SAMPLE)
+        const long long slice = (dim + SE_CL - 1) / SE_CL;
+        const long long lo = x * slice, hi = lo + slice < dim ? lo + slice : dim;
+        nk = hi > lo ? (int)(hi - lo) : 0;
+        for (int i = tid; i < nk; i += SE_THREADS) {
+            const K key = KO::key(row[lo + i]);
+            s_keys[i] = key;
+            atomicAdd(&h1[key >> 20], 1u);
+            mn = key < mn ? key : mn;
+            mx = key > mx ? key : mx;
+        }
+    } else if (tma) {
+        // chunks [x * cpc, (x + 1) * cpc) of this worker's nch = s_eff / CHUNK, one per stratum,
+        // fetched by 128-byte bulk copies (the TMA keeps them all in flight; 16-byte aligned
+        // starts inside the stratum), then keyed in place
+        const long long nch = s_eff / CHUNK;
+        const long long stratum = dim / nch;  // >= 40 (host check)
+        const int cpc = (int)((nch + SE_CL - 1) / SE_CL);
+        const long long c_lo = (long long)x * cpc;
+        const int nc = (int)(c_lo + cpc <= nch ? cpc : (nch > c_lo ? nch - c_lo : 0));
+        nk = nc * CHUNK;
+        if (tid == 0) {
+            mbar_init(&s_bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (warp == 0 && nc > 0) {
+            if (lane == 0) mbar_expect_tx(&s_bar, (unsigned)nc * CHUNK * 4u);
+            __syncwarp();
+            for (int cl_ = lane; cl_ < nc; cl_ += 32) {
+                const long long c = c_lo + cl_;
+                const unsigned h = (unsigned)mix64((unsigned long long)c * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
+                const long long off = (long long)(((unsigned long long)h * (unsigned long long)(stratum - CHUNK - 3 + 1)) >> 32);
+                const long long start = ((c * stratum + 3) & ~3LL) + (off & ~3LL);
+                bulk_g2s_plain(s_keys + cl_ * CHUNK, row + start, CHUNK * 4u, &s_bar);
+            }
+        }
+        if (nc > 0) mbar_wait(&s_bar, 0u);
+        for (int i = tid; i < nk; i += SE_THREADS) {
+            const K key = KO::key(__uint_as_float(s_keys[i]));
+            s_keys[i] = key;
+            atomicAdd(&h1[key >> 20], 1u);
+            mn = key < mn ? key : mn;
+            mx = key > mx ? key : mx;
+        }
+    } else {
+        // chunks [x * cpc, (x + 1) * cpc) of this worker's nch = s_eff / CHUNK, the same chunk
+        // positions as k_sample
+        const long long nch = s_eff / CHUNK;
+        const long long stratum = dim / nch;
+        const int cpc = (int)((nch + SE_CL - 1) / SE_CL);
+        const long long c_lo = (long long)x * cpc;
+        const int nc = (int)(c_lo + cpc <= nch ? cpc : (nch > c_lo ? nch - c_lo : 0));
+        nk = nc * CHUNK;
+        constexpr int BATCH = 16;
+        for (int c0 = warp; c0 < nc; c0 += NW * BATCH) {
+            float v[BATCH];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int cl_ = c0 + u * NW;
+                v[u] = 0.f;
+                if (cl_ < nc) {
+                    const long long c = c_lo + cl_;
+                    const unsigned h = (unsigned)mix64((unsigned long long)c * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
+                    const long long off = (long long)(((unsigned long long)h * (unsigned long long)(stratum - CHUNK + 1)) >> 32);
+                    v[u] = __ldg(row + c * stratum + off + lane);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int cl_ = c0 + u * NW;
+                if (cl_ < nc) {
+                    const K key = KO::key(v[u]);
+                    s_keys[cl_ * CHUNK + lane] = key;
+                    atomicAdd(&h1[key >> 20], 1u);
+                    mn = key < mn ? key : mn;
+                    mx = key > mx ? key : mx;
+                }
+            }
+        }
+    }
+    mn = warp_min<K>(mn);
+    mx = warp_max<K>(mx);
+    if (lane == 0) {
+        s_mn[warp] = mn;
+        s_mx[warp] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        K a = KO::KMAX, b = 0;
+        for (int i = 0; i < NW; ++i) {
+            a = s_mn[i] < a ? s_mn[i] : a;
+            b = s_mx[i] > b ? s_mx[i] : b;
+        }
+        s_cmn = a;
+        s_cmx = b;
+    }
+    cl.sync();  // every CTA's level-1 histogram and key range are complete
+    if (tid < SE_SLICE) {
+        unsigned v = 0;
+#pragma unroll
+        for (int r = 0; r < SE_CL; ++r) v += cl.map_shared_rank(h1, r)[x * SE_SLICE + tid];
+        red[tid] = v;
+    }
+    K smax = 0;
+    if (x == 0) {
+        for (int r = 0; r < SE_CL; ++r) {
+            const K b = *cl.map_shared_rank(&s_cmx, r);
+            smax = b > smax ? b : smax;
+        }
+    }
+    cl.sync();  // reduced slices complete; the per-CTA level-1 rows are no longer read
+    for (int i = tid; i < SEL_BINS; i += SE_THREADS) h1[i] = cl.map_shared_rank(red, i / SE_SLICE)[i % SE_SLICE];
+    __syncthreads();
+    const long long ns = s_eff;
+    int b1 = -1;
+    unsigned long long a1 = 0;
+    if (r_est <= ns) block_find_bin_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)r_est, b1, a1);
+    if (b1 >= 0) {
+        unsigned* h2c = cl.map_shared_rank(h2, 0);
+        for (int i = tid; i < nk; i += SE_THREADS) {
+            const K key = s_keys[i];
+            if ((int)(key >> 20) == b1) atomicAdd(&h2c[(key >> 9) & (SEL_BINS - 1)], 1u);
+        }
+    }
+    cl.sync();  // CTA 0's level-2 histogram complete; no remote shared memory is read after this
+    if (x != 0) return;
+    K est = 0;
+    if (b1 >= 0) {
+        int b2;
+        unsigned long long a2;
+        block_find_bin_from_top<SEL_BINS, SE_THREADS>(h2, (unsigned long long)r_est - a1, b2, a2);
+        est = ((K)b1 << 20) | (b2 >= 0 ? ((K)b2 << 9) : (K)0);
+    }
+    if (tid == 0) {
+        SelState<K> o{};
+        o.smax = smax;
+        o.est = est;
+        o.shift0 = digit_shift<K>(o.smax > est ? o.smax - est : (K)0, H0_BITS);
+        o.done = 0;
+        o.mode = MODE_NORMAL;
+        o.wmode = WR_FAST;
+        o.idx_cut = 0xffffffffu;
+        sel[w] = o;
+    }
+}
+
 // --------------------------------------------------------------------------------------
 // k_main: the streaming pass (pass 0) or the fallback pass (pass 1).
 // --------------------------------------------------------------------------------------
@@ -632,6 +840,7 @@ template <typename T> struct MainArgs {
     int nsubt, nsub;
     unsigned* pp;       // [k][BMAX + 1] sub-range prefix per segment (adaptive split)
     uint2* submap;      // [k][NSUB_MAX] sub-range -> (segment, part | parts << 16); x = ~0u unused
+    unsigned dense_thr; // k_main_tma: candidates per tile above which placement is staged
 };
 
 // Per-lane exclusive prefix and warp total of a small count n (0..7) via 3 ballots.
@@ -800,6 +1009,14 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
 // --------------------------------------------------------------------------------------
 constexpr int MN_STAGES = 3;
 constexpr int MN_TILE = 4096;
+constexpr unsigned MN_DENSE = 256;  // candidates per tile above which placement is staged
+inline unsigned mn_dense() {  // SG_MN_DENSE overrides (A/B runs)
+    static const unsigned v = [] {
+        const char* e = getenv("SG_MN_DENSE");
+        return e && *e ? (unsigned)strtoul(e, nullptr, 10) : MN_DENSE;
+    }();
+    return v;
+}
 
 __global__ void __launch_bounds__(TK_THREADS, 3)
 k_main_tma(MainArgs<float> a) {
@@ -810,6 +1027,7 @@ k_main_tma(MainArgs<float> a) {
     __shared__ __align__(8) unsigned long long full[MN_STAGES];
     __shared__ unsigned hist[H0_BINS];
     __shared__ unsigned s_wtot[TK_NW];
+    __shared__ unsigned short s_stage[MN_TILE];  // dense tiles: candidate offsets in index order
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, seg = blockIdx.x;
     SelState<K>* stp = a.sel + w;
@@ -883,7 +1101,29 @@ k_main_tma(MainArgs<float> a) {
         }
         const unsigned woff = __shfl_sync(FULL, wi - wt, warp);
         const unsigned total = __shfl_sync(FULL, wi, TK_NW - 1);
-        if (M) place(M, base, src, n, incl, woff);
+        if (total > a.dense_thr) {
+            // candidate-dense tile (real gradients crowd their large entries into a few layers):
+            // stage the offsets in index order, then write them coalesced, one candidate per
+            // thread per round (the lane-local path would issue 16 scattered stores per thread).
+            // (A warp-aggregated histogram via __match_any_sync measured 1.4x slower here.)
+            unsigned pos = woff + incl - n;
+            for (unsigned R = M; R; R &= R - 1) s_stage[pos++] = (unsigned short)(tid * 16 + __ffs(R) - 1);
+            __syncthreads();
+            for (unsigned j0 = 0; j0 < total; j0 += TK_THREADS) {
+                const unsigned j = j0 + tid;
+                if (j < total) {
+                    const int off = s_stage[j];
+                    const float val = src[off];
+                    const K key = KeyOf<float>::key(val);
+                    mx = key > mx ? key : mx;
+                    ci[run + j] = (uint32_t)(base + off);
+                    cv[run + j] = val;
+                    atomicAdd(&hist[digit<K>(key, est, shift0, H0_BINS)], 1u);
+                }
+            }
+        } else if (M) {
+            place(M, base, src, n, incl, woff);
+        }
         if (tid == 0) {
             const long long ti = (long long)w * a.ntiles + tile;
             a.cnt[ti] = total;
@@ -1958,9 +2198,23 @@ template <typename T> int main_ctas_per_sm() {
     return per_sm;
 }
 
-template <typename T> int segments_per_worker(int k) {
-    const int s = num_sms() * main_ctas_per_sm<T>() / k;
-    return s < 1 ? 1 : s;
+// Main-pass segments per worker: a whole number of waves of CTAs over all workers (a partial
+// last wave leaves HBM idle in the tail), as many as give segments of ~MAIN_SEG_TILES tiles.
+// Real gradients crowd their candidates into a few layers and a candidate-dense segment runs
+// ~2x slower than a sparse one; with short segments (4 waves at k = 8) the hardware's CTA
+// scheduler evens that out (ResNet-152, k = 8: main pass 0.89 -> 0.38 ms).  At k = 1 one wave
+// already gives short segments.
+constexpr long long MAIN_SEG_TILES = 64;
+
+template <typename T> int segments_per_worker(int k, long long dim) {
+    long long wave = (long long)num_sms() * main_ctas_per_sm<T>() / k;
+    if (wave < 1) wave = 1;
+    const long long ntiles = (dim + tile_elems<T>() - 1) / tile_elems<T>();
+    long long waves = (ntiles + MAIN_SEG_TILES * wave / 2) / (MAIN_SEG_TILES * wave);  // rounded
+    if (waves < 1) waves = 1;
+    long long s = waves * wave;
+    if (s > BMAX) s = BMAX;
+    return (int)s;
 }
 
 template <typename T>
@@ -1973,7 +2227,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
         return SG_ERR_INVALID;
     if (k > MAX_WORKERS || dim >= (1ll << 31)) return SG_ERR_UNSUPPORTED;
     if (tile_off && TILE != MERGE_TILE) return SG_ERR_INVALID;
-    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k), (long long)num_sms() * CW_PER_SM);
+    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k, dim), (long long)num_sms() * CW_PER_SM);
     if (!ws || ws_bytes < p.total) return SG_ERR_WORKSPACE;
     unsigned char* base = reinterpret_cast<unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
     auto at = [&](size_t off) { return base + off; };
@@ -2011,12 +2265,34 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     K* samp = reinterpret_cast<K*>(at(p.off_samp));
     K* mm = reinterpret_cast<K*>(at(p.off_mm));
     unsigned* hs1 = reinterpret_cast<unsigned*>(at(p.off_hs1));
-    launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm,
-               reinterpret_cast<uint4*>(base), (long long)(p.zero_end / 16), hs1);
-    debug_sync("k_sample", stream);
-    launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), 0, stream, dim, p.s_eff, p.r_est,
-               (const K*)samp, (const K*)mm, EST_G, sel, hs1);
-    debug_sync("k_estimate", stream);
+    if constexpr (sizeof(K) == 4) {
+        if (sample_est_fused()) {
+            // one clustered launch: the sample stays in shared memory
+            cudaError_t e = smem_attr((const void*)k_sample_est_f32, (int)SE_SMEM);
+            if (e != cudaSuccess) return e;
+            // bulk-copy sampling needs 16-byte aligned rows and strata of >= 40 elements
+            const int tma = se_tma() && p.s_eff < dim && (reinterpret_cast<size_t>(g) % 16 == 0) && (ld % 4 == 0) &&
+                            dim / (p.s_eff / CHUNK) >= 40;
+            launch_pdl(k_sample_est_f32, dim3(SE_CL, k), dim3(SE_THREADS), SE_SMEM, stream, (const float*)g, ld, dim,
+                       p.s_eff, p.r_est, reinterpret_cast<SelState<uint32_t>*>(sel), reinterpret_cast<uint4*>(base),
+                       (long long)(p.zero_end / 16), tma);
+            debug_sync("k_sample_est", stream);
+        } else {
+            launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm,
+                       reinterpret_cast<uint4*>(base), (long long)(p.zero_end / 16), hs1);
+            debug_sync("k_sample", stream);
+            launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), 0, stream, dim, p.s_eff, p.r_est,
+                       (const K*)samp, (const K*)mm, EST_G, sel, hs1);
+            debug_sync("k_estimate", stream);
+        }
+    } else {
+        launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm,
+                   reinterpret_cast<uint4*>(base), (long long)(p.zero_end / 16), hs1);
+        debug_sync("k_sample", stream);
+        launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), 0, stream, dim, p.s_eff, p.r_est,
+                   (const K*)samp, (const K*)mm, EST_G, sel, hs1);
+        debug_sync("k_estimate", stream);
+    }
     // 2. main streaming pass, then the (normally empty) fallback pass
     MainArgs<T> ma;
     ma.g = g;
@@ -2045,6 +2321,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ma.nsub = p.nsub;
     ma.pp = reinterpret_cast<unsigned*>(at(p.off_pp));
     ma.submap = reinterpret_cast<uint2*>(at(p.off_submap));
+    ma.dense_thr = mn_dense();
     const dim3 sgrid((unsigned)p.nseg, (unsigned)k);
     bool tma = false;
     if constexpr (sizeof(T) == 4) tma = vec_ok;
@@ -2142,7 +2419,7 @@ template <typename T>
 int topk_stats(int k, long long dim, long long m, const void* ws, size_t ws_bytes, int64_t* out, cudaStream_t stream) {
     using K = typename KeyOf<T>::K;
     if (!ws || !out || k < 1 || dim < 1 || m < 1 || m > dim) return SG_ERR_INVALID;
-    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k), (long long)num_sms() * CW_PER_SM);
+    const TopkPlan p = make_plan<T>(k, dim, m, segments_per_worker<T>(k, dim), (long long)num_sms() * CW_PER_SM);
     if (ws_bytes < p.total) return SG_ERR_WORKSPACE;
     const unsigned char* base = reinterpret_cast<const unsigned char*>(align_up(reinterpret_cast<size_t>(ws), 256));
     launch_pdl(k_topk_stats<T>, dim3(1), dim3(64), 0, stream, reinterpret_cast<const SelState<K>*>(base + p.off_sel),
@@ -2178,7 +2455,7 @@ extern "C" {
 
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m) {
     if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
-    return make_plan<float>(k, dim, m, segments_per_worker<float>(k), (long long)num_sms() * CW_PER_SM).total;
+    return make_plan<float>(k, dim, m, segments_per_worker<float>(k, dim), (long long)num_sms() * CW_PER_SM).total;
 }
 
 size_t sg_topk_workspace_bytes_fused_f32(int k, int64_t dim, int64_t m) {
@@ -2199,7 +2476,7 @@ size_t sg_topk_workspace_zero_bytes_fused_f32(int k, int64_t dim, int64_t m) {
 }
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m) {
     if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
-    return make_plan<double>(k, dim, m, segments_per_worker<double>(k), (long long)num_sms() * CW_PER_SM).total;
+    return make_plan<double>(k, dim, m, segments_per_worker<double>(k, dim), (long long)num_sms() * CW_PER_SM).total;
 }
 
 int sg_topk_gate_f32(const float* g, int k, int64_t ld, int64_t dim, int64_t m, uint32_t* idx,

@@ -20,7 +20,10 @@ _GATE_BYTES = _capi.GATE_STATE_DTYPE.itemsize
 # Kernel launches issued through this module (each C-ABI entry point launches a fixed
 # sequence; see csrc/topk.cu and csrc/aggregate.cu).  bench.py reports the count.
 LAUNCHES = {"n": 0}
-TOPK_LAUNCHES = {torch.float32: 2 + 2 + 1 + 1 + 1, torch.float64: 2 + 2 + 1 + 1 + 1}
+# float32: sample+estimate (one clustered launch; two with SG_SAMPLE_EST=0), main + fallback,
+# collect, resolve, write(+gate); float64: sample, estimate, main + fallback, collect, resolve, write
+TOPK_LAUNCHES = {torch.float32: (1 if os.environ.get("SG_SAMPLE_EST", "1") != "0" else 2) + 2 + 1 + 1 + 1,
+                 torch.float64: 2 + 2 + 1 + 1 + 1}
 
 
 def _count(n: int) -> None:

@@ -235,8 +235,9 @@ def test_guarded_dense_exchange_and_peer_merge(cuda, merge_own):
 def test_concentrated_payloads_merge_bit_exact(cuda, workers, hot, cr):
     """Real gradients concentrate the kept entries in a few layers: here a 3 % region of the
     row carries large values, so its tiles hold far more entries than one staging chunk
-    (the merge's multi-chunk path) and the cost-balanced tile ranges split the region over
-    many CTAs.  The hot=1.0 cases are uniformly dense payloads (cr 0.1 / 0.3: every tile's
+    (the merge's multi-chunk path; its chunks hold one or two long worker runs, which
+    k_merge_ws folds run by run without lists) and the cost-balanced tile ranges split the
+    region over many CTAs.  The hot=1.0 cases are uniformly dense payloads (cr 0.1 / 0.3: every tile's
     chunks take the position-owned fold).  All-sparse merge + fused momentum SGD through the Top-k kernels' own payloads
     and tile offsets: aggregate and updated state equal f32(oracle) bit for bit."""
     from paper_2301_08897_b200 import kernels

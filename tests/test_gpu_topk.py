@@ -92,6 +92,39 @@ def test_topk_matches_oracle(cuda, D, cr, fam):
             assert np.isnan(a) == np.isnan(b)
 
 
+def _layers(D: int, seed: int) -> np.ndarray:
+    """Real-gradient shape: small entries everywhere, a few contiguous "layers" holding the
+    large ones (candidate-dense tiles in the main pass), bfloat16-rounded values (ties)."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal(D, dtype=np.float32) * np.float32(1e-4)
+    for b in range(3):
+        lo = int(rng.integers(0, max(1, D - D // 60)))
+        n = D // 100 + 1
+        g[lo:lo + n] = rng.standard_normal(min(n, D - lo), dtype=np.float32) * np.float32(10.0 ** -b)
+    u = g.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return u.view(np.float32)
+
+
+@pytest.mark.parametrize("D", [1 << 20, (1 << 22) + 5, 10_000_019])
+@pytest.mark.parametrize("cr", [0.001, 0.01, 0.1])
+def test_topk_concentrated_layers(cuda, D, cr):
+    """Candidates crowded into a few contiguous blocks (the staged dense-tile placement of the
+    main pass and the candidate-count split of collect/write), bit-exact in both variants."""
+    from paper_2301_08897_b200 import kernels
+
+    k = 2
+    host = np.stack([_layers(D, seed=D + 31 * j + int(cr * 1e4)) for j in range(k)])
+    dev = torch.from_numpy(host).to(cuda)
+    m = comm_ref.topk_count(D, cr)
+    for fused in (False, True):
+        idx, val, norms2, _, _ = kernels.topk_gate(dev, m, fused=fused)
+        for j in range(k):
+            want = comm_ref.topk_indices_threshold(host[j].astype(np.float64), m)
+            assert np.array_equal(idx[j].cpu().numpy().astype(np.int64), want), (j, fused)
+            assert np.array_equal(val[j].cpu().numpy().view(np.uint32), host[j][want].view(np.uint32))
+
+
 def test_topk_batched_rows_and_padding(cuda):
     """k workers in one launch, rows with a padded leading dimension."""
     from paper_2301_08897_b200 import kernels
