@@ -72,9 +72,9 @@ int64_t sg_topk_count(int64_t dim, double cr);
 size_t sg_topk_workspace_bytes_f32(int k, int64_t dim, int64_t m);
 size_t sg_topk_workspace_bytes_f64(int k, int64_t dim, int64_t m);
 /* Zero-state of a workspace between calls: the first sg_topk_workspace_zero_bytes_f32 bytes
- * (launch chain: 0, it keeps none) or sg_topk_workspace_zero_bytes_fused_f32 bytes (fused
- * variant) must be zero before the first call and whenever (k, dim, m) change; every call
- * leaves them as it found them. */
+ * (launch chain: the sampler's histogram, key range and arrival counters) or
+ * sg_topk_workspace_zero_bytes_fused_f32 bytes (fused variant) must be zero before the first
+ * call and whenever (k, dim, m) change; every call leaves them as it found them. */
 size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m);
 /* Persistent float32 variant: the same contract as sg_topk_gate_f32 in ONE cooperative
  * kernel (sample -> estimate -> single read -> select -> ordered write -> gate, synchronised

@@ -45,6 +45,7 @@ constexpr int SEL_BITS = 11;
 constexpr int SEL_BINS = 1 << SEL_BITS;
 constexpr int EST_THREADS = 1024;
 constexpr int EST_G = 32;        // sampling CTAs per worker (k_sample)
+constexpr int SE_GMAX = 128;     // sampling CTAs per worker (k_sample_est), at most
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
 constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
@@ -71,7 +72,7 @@ template <> struct TopkTraits<double> {
 template <typename T> constexpr int tile_elems() { return TK_THREADS * TK_ROUNDS * Vec16<T>::N; }
 
 template <typename K> struct SelState {
-    K est, smax;               // from k_estimate
+    K est, smax;               // from the estimate: smax bounds the round-0 histogram's fine range
     K lo, span;                // current key range [lo, lo + span]
     K T;                       // final threshold key
     unsigned long long rank;   // remaining 1-based rank from the top inside the range
@@ -92,8 +93,11 @@ struct TopkPlan {
     int nsubt;         // target sub-range count apportioned over the segments by candidates
     long long dim, m;
     long long s_eff, stride, r_est;
+    long long r_hi;  // float32 sample: rank whose level-1 bin bounds the main pass's fine histogram (0: none)
     long long ntiles, segcap;
-    size_t off_count, off_maxkey, off_ctr, off_bndn, off_hist0, off_hist0fb, off_histr, off_status, zero_end;
+    size_t off_se_h1, off_se_mm, off_se_done, state_end;  // zero state between calls (k_sample_est)
+    size_t zero_begin, off_count, off_maxkey, off_ctr, off_bndn, off_hist0, off_hist0fb, off_histr, off_status, zero_end;
+    size_t off_boff;
     size_t off_sel, off_samp, off_mm, off_cnt, off_tstart, off_segcnt, off_seggt, off_segbase, off_pmain, off_pwrite,
         off_cidx, off_cval, off_bkey, off_bidx, off_bpos, off_pp, off_submap, off_hs1, total;
 };
@@ -119,6 +123,11 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
         const double sd = __builtin_sqrt(mean * (1.0 - q) + 1.0);
         const double z = S == TopkTraits<T>::SAMPLE ? TopkTraits<T>::Z : 6.0;
         p.r_est = (long long)(mean + z * sd + 4.0) + 1;
+        // the mirror bound: fewer than m keys lie above the r_hi-th largest sample key's level-1
+        // bin (same odds), so the round-0 histogram of the candidates spans [est, that bin's
+        // top] instead of [est, sample max] -- ~32x finer bins, a boundary bin far below RES
+        const double r_hi = mean - z * sd - 4.0;
+        p.r_hi = r_hi >= 1.0 ? (long long)r_hi : 0;
     }
     const long long te = tile_elems<T>();
     p.ntiles = (dim + te - 1) / te;
@@ -146,6 +155,13 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     }
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+    // zero state: restored by k_sample_est's last CTA per worker (float32 chain)
+    p.off_se_h1 = take(sizeof(unsigned) * (size_t)k * SEL_BINS);
+    p.off_se_mm = take(sizeof(unsigned) * 2 * (size_t)k);
+    p.off_se_done = take(sizeof(unsigned) * (size_t)k);
+    p.state_end = o;
+    // per-call scratch zeroed by the first kernel of the chain
+    p.zero_begin = o;
     p.off_count = take(sizeof(unsigned long long) * 2 * k);  // [pass][k]
     p.off_maxkey = take(sizeof(K) * k);
     p.off_ctr = take(sizeof(unsigned) * (8 + 16 * (size_t)k));  // see the counter map in topk_gate
@@ -166,7 +182,7 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     p.off_pmain = take(sizeof(double) * (size_t)k * p.nseg);
     p.off_pwrite = take(sizeof(double) * (size_t)k * p.nsub);
     p.off_pp = take(sizeof(unsigned) * (size_t)k * (BMAX + 1));
-    p.off_submap = take(sizeof(uint2) * (size_t)k * NSUB_MAX);
+    p.off_submap = take(sizeof(uint4) * (size_t)k * NSUB_MAX);
     const size_t cap = (size_t)k * p.nseg * p.segcap;
     p.off_cidx = take(sizeof(uint32_t) * cap);
     p.off_cval = take(sizeof(T) * cap);
@@ -179,6 +195,7 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     // float32 level-1 sample histograms (key bits [30:20]): one dense row per sampling CTA,
     // written whole by k_sample (no atomics, no state between calls), summed by k_estimate
     p.off_hs1 = take(sizeof(unsigned) * (size_t)k * EST_G * SEL_BINS);
+    p.off_boff = take(sizeof(uint16_t) * (size_t)k * SE_GMAX * (SEL_BINS + 1));
     p.total = o + 256;  // slack for base alignment
     return p;
 }
@@ -611,15 +628,20 @@ k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf
     }
 }
 
-// k_sample_est (float32): sample + estimate in ONE launch.  A cluster of SE_CL CTAs per worker
-// gathers the same stratified sample as k_sample (chunk c at the same hashed offset), each CTA
-// keeping its 1/SE_CL of the keys in shared memory with its level-1 histogram (key bits
-// [30:20]).  Over distributed shared memory: CTA r reduces bin slice r of the cluster's
-// level-1 histograms, every CTA reads the reduced histogram and picks the same level-1 bin
-// b1, then scans only its own resident keys for that bin into CTA 0's level-2 histogram (bits
-// [19:9]); CTA 0 picks b2 and publishes est = (b1 << 20) | (b2 << 9) -- the value k_sample +
-// k_estimate compute, without the sample's trip through global memory, the per-CTA rows and
-// the one-CTA re-scan.
+// --------------------------------------------------------------------------------------
+// k_sample_est (float32): sample + estimate in ONE launch, spread over many SMs.
+// The sample: S = 131072 keys per worker as 512 chunks of 256 elements (1 KB, one DRAM row),
+// one at a hashed offset inside each of 512 strata of the row.  The reads are random, so their
+// cost is DRAM row activations (128-byte chunks, 8x the activations, measured 25 us at k = 8).
+// G CTAs per worker (G = se_ctas(k): 128 at k = 1 .. 32 at k = 8) each take 512/G chunks, key
+// them in shared memory, histogram key bits [30:20] (level 1), add the non-zero bins to the
+// worker's global level-1 histogram and write the keys BUCKETED by level-1 bin (a counting
+// sort in shared memory) with the bucket offsets.  The worker's last CTA to finish picks the
+// level-1 bin b1 holding the r_est-th largest sample key, reads only the keys of bin b1 from
+// every CTA's bucket (a few % of the sample), picks the level-2 bin (bits [19:9]), publishes
+// est = (b1 << 20) | (b2 << 9) and restores the zero state it used (global histogram, key
+// range, arrival counter).  (One 8-CTA cluster per worker with the sample in distributed
+// shared memory measured 26 us at k = 1: the sampling rate is per SM.)
 // --------------------------------------------------------------------------------------
 // SG_SAMPLE_EST=0 selects the two-launch k_sample + k_estimate (A/B runs)
 inline bool sample_est_fused() {
@@ -629,126 +651,112 @@ inline bool sample_est_fused() {
     }();
     return on;
 }
-inline bool se_tma() {  // SG_SE_TMA=0: the sample by per-warp loads (A/B runs)
-    static const bool on = [] {
-        const char* e = getenv("SG_SE_TMA");
-        return !(e && *e == '0');
-    }();
-    return on;
+constexpr int SE_THREADS = 256;
+constexpr int SE_GMIN = 8;
+constexpr int SE_CHUNK = 256;  // sample chunk (elements): one 1 KB DRAM row
+inline int se_ctas(int k) {  // a power of two: the 512 sample chunks split evenly
+    int g = SE_GMAX;
+    while (g > SE_GMIN && g * k > 256) g >>= 1;
+    return g;
 }
-constexpr int SE_CL = 8;                                       // cluster CTAs per worker
-constexpr int SE_THREADS = 512;
-constexpr int SE_KEYS = TopkTraits<float>::SAMPLE / SE_CL;     // resident keys per CTA
-constexpr int SE_SLICE = SEL_BINS / SE_CL;                     // level-1 bins reduced per CTA
-constexpr size_t SE_SMEM = sizeof(uint32_t) * SE_KEYS;          // dynamic: the resident keys
-static_assert(SE_SLICE <= SE_THREADS && SEL_BINS % SE_THREADS == 0, "sample/estimate layout");
+inline size_t se_smem(int G) { return 2 * sizeof(uint32_t) * (size_t)(TopkTraits<float>::SAMPLE / G); }
 
-__global__ void __cluster_dims__(SE_CL, 1, 1) __launch_bounds__(SE_THREADS)
-k_sample_est_f32(const float* __restrict__ g, long long ld, long long dim, long long s_eff, long long r_est,
-                 SelState<uint32_t>* __restrict__ sel, uint4* __restrict__ zero, long long zero_vec, int tma) {
+struct SampleEstArgs {
+    const float* g;
+    long long ld, dim, s_eff, r_est, r_hi;
+    int vec;                // 16-byte aligned rows and strata of >= SE_CHUNK + 4 elements
+    SelState<uint32_t>* sel;
+    uint4* zero;            // per-call scratch zeroed here (the later kernels' counters)
+    long long zero_vec;
+    uint32_t* bkeys;        // [k][SAMPLE] keys bucketed by level-1 bin, CTA-major
+    uint16_t* boff;         // [k][G][SEL_BINS + 1] bucket offsets of each CTA
+    unsigned* h1g;          // [k][SEL_BINS] zero state: level-1 histogram
+    unsigned* mmg;          // [k][2] zero state: ~min key, max key
+    unsigned* doneg;        // [k] zero state: arrivals
+};
+
+__global__ void __launch_bounds__(SE_THREADS)
+k_sample_est_f32(SampleEstArgs a) {
     pdl_enter();
-    namespace cg = cooperative_groups;
     using KO = KeyOf<float>;
     using K = uint32_t;
-    extern __shared__ __align__(16) K s_keys[];
-    __shared__ __align__(16) unsigned h1[SEL_BINS];   // own level-1 histogram, then the reduced one
-    __shared__ unsigned red[SE_SLICE];                // this CTA's slice of the reduced level 1
-    __shared__ unsigned h2[SEL_BINS];                 // level 2 (CTA 0's is the cluster's)
+    extern __shared__ __align__(16) K se_smem_raw[];
+    __shared__ unsigned h1[SEL_BINS];      // this CTA's level-1 histogram, then bucket cursors
+    __shared__ unsigned s_wsum[SE_THREADS / 32];
     __shared__ K s_mn[SE_THREADS / 32], s_mx[SE_THREADS / 32];
-    __shared__ K s_cmn, s_cmx;
-    __shared__ __align__(8) unsigned long long s_bar;
-    cg::cluster_group cl = cg::this_cluster();
-    const int x = (int)cl.block_rank(), w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ int s_last;
+    const int x = blockIdx.x, G = gridDim.x, w = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = SE_THREADS / 32;
-    for (int i = tid; i < SEL_BINS; i += SE_THREADS) {
-        h1[i] = 0;
-        h2[i] = 0;
-    }
+    const int per = TopkTraits<float>::SAMPLE / G;  // keys per CTA (sampled case)
+    K* keys = se_smem_raw;                          // [per]
+    K* buck = se_smem_raw + per;                    // [per]
+    for (int i = tid; i < SEL_BINS; i += SE_THREADS) h1[i] = 0;
     {
-        const long long cta = (long long)w * SE_CL + x, ncta = (long long)SE_CL * gridDim.y;
-        for (long long i = cta * SE_THREADS + tid; i < zero_vec; i += ncta * SE_THREADS) zero[i] = make_uint4(0, 0, 0, 0);
+        const long long cta = (long long)w * G + x, ncta = (long long)G * gridDim.y;
+        for (long long i = cta * SE_THREADS + tid; i < a.zero_vec; i += ncta * SE_THREADS) a.zero[i] = make_uint4(0, 0, 0, 0);
     }
     __syncthreads();
-    const float* row = g + (long long)w * ld;
+    const float* row = a.g + (long long)w * a.ld;
     K mn = KO::KMAX, mx = 0;
-    int nk = 0;  // resident keys of this CTA
-    if (s_eff == dim) {  // the sample is the whole row (dim <= SAMPLE)
-        const long long slice = (dim + SE_CL - 1) / SE_CL;
-        const long long lo = x * slice, hi = lo + slice < dim ? lo + slice : dim;
+    int nk = 0;
+    if (a.s_eff == a.dim) {  // the sample is the whole row (dim <= SAMPLE)
+        const long long slice = (a.dim + G - 1) / G;
+        const long long lo = x * slice, hi = lo + slice < a.dim ? lo + slice : a.dim;
         nk = hi > lo ? (int)(hi - lo) : 0;
         for (int i = tid; i < nk; i += SE_THREADS) {
             const K key = KO::key(row[lo + i]);
-            s_keys[i] = key;
-            atomicAdd(&h1[key >> 20], 1u);
-            mn = key < mn ? key : mn;
-            mx = key > mx ? key : mx;
-        }
-    } else if (tma) {
-        // chunks [x * cpc, (x + 1) * cpc) of this worker's nch = s_eff / CHUNK, one per stratum,
-        // fetched by 128-byte bulk copies (the TMA keeps them all in flight; 16-byte aligned
-        // starts inside the stratum), then keyed in place
-        const long long nch = s_eff / CHUNK;
-        const long long stratum = dim / nch;  // >= 40 (host check)
-        const int cpc = (int)((nch + SE_CL - 1) / SE_CL);
-        const long long c_lo = (long long)x * cpc;
-        const int nc = (int)(c_lo + cpc <= nch ? cpc : (nch > c_lo ? nch - c_lo : 0));
-        nk = nc * CHUNK;
-        if (tid == 0) {
-            mbar_init(&s_bar, 1);
-            fence_mbar_init();
-        }
-        __syncthreads();
-        if (warp == 0 && nc > 0) {
-            if (lane == 0) mbar_expect_tx(&s_bar, (unsigned)nc * CHUNK * 4u);
-            __syncwarp();
-            for (int cl_ = lane; cl_ < nc; cl_ += 32) {
-                const long long c = c_lo + cl_;
-                const unsigned h = (unsigned)mix64((unsigned long long)c * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
-                const long long off = (long long)(((unsigned long long)h * (unsigned long long)(stratum - CHUNK - 3 + 1)) >> 32);
-                const long long start = ((c * stratum + 3) & ~3LL) + (off & ~3LL);
-                bulk_g2s_plain(s_keys + cl_ * CHUNK, row + start, CHUNK * 4u, &s_bar);
-            }
-        }
-        if (nc > 0) mbar_wait(&s_bar, 0u);
-        for (int i = tid; i < nk; i += SE_THREADS) {
-            const K key = KO::key(__uint_as_float(s_keys[i]));
-            s_keys[i] = key;
+            keys[i] = key;
             atomicAdd(&h1[key >> 20], 1u);
             mn = key < mn ? key : mn;
             mx = key > mx ? key : mx;
         }
     } else {
-        // chunks [x * cpc, (x + 1) * cpc) of this worker's nch = s_eff / CHUNK, the same chunk
-        // positions as k_sample
-        const long long nch = s_eff / CHUNK;
-        const long long stratum = dim / nch;
-        const int cpc = (int)((nch + SE_CL - 1) / SE_CL);
-        const long long c_lo = (long long)x * cpc;
-        const int nc = (int)(c_lo + cpc <= nch ? cpc : (nch > c_lo ? nch - c_lo : 0));
-        nk = nc * CHUNK;
-        constexpr int BATCH = 16;
+        // chunks [x * nc, (x + 1) * nc) of the worker's nch = s_eff / SE_CHUNK, one 1 KB chunk
+        // at a hashed offset inside each stratum: the random reads are DRAM-row bound, so a
+        // whole row per chunk (not 128-byte chunks) keeps the activations 8x fewer
+        const long long nch = a.s_eff / SE_CHUNK;  // 512
+        const long long stratum = a.dim / nch;
+        const int nc = (int)(nch / G);
+        const long long c_lo = (long long)x * nc;
+        nk = nc * SE_CHUNK;
+        constexpr int BATCH = 4;
+        constexpr int PL = SE_CHUNK / 32;  // 8 elements per lane per chunk
         for (int c0 = warp; c0 < nc; c0 += NW * BATCH) {
-            float v[BATCH];
+            float v[BATCH][PL];
 #pragma unroll
             for (int u = 0; u < BATCH; ++u) {
-                const int cl_ = c0 + u * NW;
-                v[u] = 0.f;
-                if (cl_ < nc) {
-                    const long long c = c_lo + cl_;
+                const int cl = c0 + u * NW;
+#pragma unroll
+                for (int j = 0; j < PL; ++j) v[u][j] = 0.f;
+                if (cl < nc) {
+                    const long long c = c_lo + cl;
                     const unsigned h = (unsigned)mix64((unsigned long long)c * 0x9e3779b97f4a7c15ull + (unsigned long long)w);
-                    const long long off = (long long)(((unsigned long long)h * (unsigned long long)(stratum - CHUNK + 1)) >> 32);
-                    v[u] = __ldg(row + c * stratum + off + lane);
+                    if (a.vec) {  // 16-byte aligned start inside the stratum, two float4 per lane
+                        const long long off = (long long)(((unsigned long long)h * (unsigned long long)(stratum - SE_CHUNK - 3 + 1)) >> 32);
+                        const float4* src = reinterpret_cast<const float4*>(row + ((c * stratum + 3) & ~3LL) + (off & ~3LL));
+                        const float4 p0 = __ldg(src + lane), p1 = __ldg(src + 32 + lane);
+                        v[u][0] = p0.x; v[u][1] = p0.y; v[u][2] = p0.z; v[u][3] = p0.w;
+                        v[u][4] = p1.x; v[u][5] = p1.y; v[u][6] = p1.z; v[u][7] = p1.w;
+                    } else {
+                        const long long off = (long long)(((unsigned long long)h * (unsigned long long)(stratum - SE_CHUNK + 1)) >> 32);
+                        const float* src = row + c * stratum + off;
+#pragma unroll
+                        for (int j = 0; j < PL; ++j) v[u][j] = __ldg(src + j * 32 + lane);
+                    }
                 }
             }
 #pragma unroll
             for (int u = 0; u < BATCH; ++u) {
-                const int cl_ = c0 + u * NW;
-                if (cl_ < nc) {
-                    const K key = KO::key(v[u]);
-                    s_keys[cl_ * CHUNK + lane] = key;
-                    atomicAdd(&h1[key >> 20], 1u);
-                    mn = key < mn ? key : mn;
-                    mx = key > mx ? key : mx;
+                const int cl = c0 + u * NW;
+                if (cl < nc) {
+#pragma unroll
+                    for (int j = 0; j < PL; ++j) {
+                        const K key = KO::key(v[u][j]);
+                        keys[cl * SE_CHUNK + j * 32 + lane] = key;
+                        atomicAdd(&h1[key >> 20], 1u);
+                        mn = key < mn ? key : mn;
+                        mx = key > mx ? key : mx;
+                    }
                 }
             }
         }
@@ -760,63 +768,139 @@ k_sample_est_f32(const float* __restrict__ g, long long ld, long long dim, long 
         s_mx[warp] = mx;
     }
     __syncthreads();
-    if (tid == 0) {
-        K a = KO::KMAX, b = 0;
-        for (int i = 0; i < NW; ++i) {
-            a = s_mn[i] < a ? s_mn[i] : a;
-            b = s_mx[i] > b ? s_mx[i] : b;
-        }
-        s_cmn = a;
-        s_cmx = b;
-    }
-    cl.sync();  // every CTA's level-1 histogram and key range are complete
-    if (tid < SE_SLICE) {
-        unsigned v = 0;
+    // publish: the non-zero level-1 bins, the key range; then the exclusive bucket offsets
+    constexpr int PB = SEL_BINS / SE_THREADS;  // 8 bins per thread
+    unsigned hv[PB], hs = 0;
+    unsigned* h1w = a.h1g + (long long)w * SEL_BINS;
 #pragma unroll
-        for (int r = 0; r < SE_CL; ++r) v += cl.map_shared_rank(h1, r)[x * SE_SLICE + tid];
-        red[tid] = v;
+    for (int u = 0; u < PB; ++u) {
+        hv[u] = h1[tid * PB + u];
+        if (hv[u]) atomicAdd(h1w + tid * PB + u, hv[u]);
+        hs += hv[u];
     }
-    K smax = 0;
-    if (x == 0) {
-        for (int r = 0; r < SE_CL; ++r) {
-            const K b = *cl.map_shared_rank(&s_cmx, r);
-            smax = b > smax ? b : smax;
+    if (tid == 0) {
+        K mn2 = KO::KMAX, mx2 = 0;
+        for (int i = 0; i < NW; ++i) {
+            mn2 = s_mn[i] < mn2 ? s_mn[i] : mn2;
+            mx2 = s_mx[i] > mx2 ? s_mx[i] : mx2;
         }
+        atomicMax(a.mmg + 2 * w, ~mn2);  // zero state 0 == ~KMAX
+        atomicMax(a.mmg + 2 * w + 1, mx2);
     }
-    cl.sync();  // reduced slices complete; the per-CTA level-1 rows are no longer read
-    for (int i = tid; i < SEL_BINS; i += SE_THREADS) h1[i] = cl.map_shared_rank(red, i / SE_SLICE)[i % SE_SLICE];
+    unsigned incl = hs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
     __syncthreads();
-    const long long ns = s_eff;
+    unsigned run = incl - hs;
+    for (int i = 0; i < warp; ++i) run += s_wsum[i];
+    uint16_t* bo = a.boff + ((long long)w * G + x) * (SEL_BINS + 1);
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+        h1[tid * PB + u] = run;  // bucket cursor
+        bo[tid * PB + u] = (uint16_t)run;
+        run += hv[u];
+    }
+    if (tid == SE_THREADS - 1) bo[SEL_BINS] = (uint16_t)run;
+    __syncthreads();
+    for (int i = tid; i < nk; i += SE_THREADS) {
+        const K key = keys[i];
+        buck[atomicAdd(&h1[key >> 20], 1u)] = key;
+    }
+    __syncthreads();
+    K* bk = a.bkeys + (long long)w * TopkTraits<float>::SAMPLE + (long long)x * per;
+    for (int i = tid; i < nk; i += SE_THREADS) bk[i] = buck[i];
+    // the worker's last CTA estimates
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.doneg + w, 1u) == (unsigned)G - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int i = tid; i < SEL_BINS; i += SE_THREADS) h1[i] = __ldcg(h1w + i);
+    __syncthreads();
+    K est = 0;
     int b1 = -1;
     unsigned long long a1 = 0;
-    if (r_est <= ns) block_find_bin_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)r_est, b1, a1);
-    if (b1 >= 0) {
-        unsigned* h2c = cl.map_shared_rank(h2, 0);
-        for (int i = tid; i < nk; i += SE_THREADS) {
-            const K key = s_keys[i];
-            if ((int)(key >> 20) == b1) atomicAdd(&h2c[(key >> 9) & (SEL_BINS - 1)], 1u);
-        }
+    if (a.r_est <= a.s_eff) block_find_bin_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)a.r_est, b1, a1);
+    K ucap = KO::KMAX;  // upper end of the main pass's fine histogram range (see make_plan)
+    if (a.r_hi >= 1 && b1 >= 0) {
+        int bh;
+        unsigned long long ah;
+        block_find_bin_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)a.r_hi, bh, ah);
+        if (bh >= 0 && bh < SEL_BINS - 1) ucap = (K)(bh + 1) << 20;
     }
-    cl.sync();  // CTA 0's level-2 histogram complete; no remote shared memory is read after this
-    if (x != 0) return;
-    K est = 0;
+    __syncthreads();  // h1 is reused for level 2
+    for (int i = tid; i < SEL_BINS; i += SE_THREADS) h1[i] = 0;
+    __syncthreads();
     if (b1 >= 0) {
+        // level 2 over bin b1 of every CTA's bucketed keys: thread c < G fetches CTA c's bucket
+        // bounds (all in one round trip), a scan of the bucket sizes, then every thread takes
+        // keys of the concatenated buckets (independent loads)
+        __shared__ int s_o0[SE_GMAX], s_pre[SE_GMAX + 1];
+        int cnt = 0;
+        if (tid < G) {
+            const uint16_t* bc = a.boff + ((long long)w * G + tid) * (SEL_BINS + 1);
+            const int o0 = __ldcg(bc + b1);
+            cnt = __ldcg(bc + b1 + 1) - o0;
+            s_o0[tid] = o0;
+        }
+        static_assert(SE_GMAX <= SE_THREADS, "one bucket per thread");
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_wsum[warp] = (unsigned)inc;
+        __syncthreads();
+        int wb = 0;
+        for (int i = 0; i < warp; ++i) wb += (int)s_wsum[i];
+        if (tid < G) s_pre[tid] = wb + inc - cnt;
+        if (tid == 0) {
+            int t = 0;
+            for (int i = 0; i < NW; ++i) t += (int)s_wsum[i];
+            s_pre[G] = t;
+        }
+        __syncthreads();
+        const int total = s_pre[G];
+        const K* kw = a.bkeys + (long long)w * TopkTraits<float>::SAMPLE;
+        for (int i = tid; i < total; i += SE_THREADS) {
+            int l = 0, h = G;  // the bucket c with s_pre[c] <= i < s_pre[c + 1]
+            while (h - l > 1) {
+                const int mid = (l + h) >> 1;
+                if (s_pre[mid] <= i) l = mid;
+                else h = mid;
+            }
+            const K key = __ldcg(kw + (long long)l * per + s_o0[l] + (i - s_pre[l]));
+            atomicAdd(&h1[(key >> 9) & (SEL_BINS - 1)], 1u);
+        }
+        __syncthreads();
         int b2;
         unsigned long long a2;
-        block_find_bin_from_top<SEL_BINS, SE_THREADS>(h2, (unsigned long long)r_est - a1, b2, a2);
+        block_find_bin_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)a.r_est - a1, b2, a2);
         est = ((K)b1 << 20) | (b2 >= 0 ? ((K)b2 << 9) : (K)0);
     }
     if (tid == 0) {
         SelState<K> o{};
-        o.smax = smax;
+        const K smax = __ldcg(a.mmg + 2 * w + 1);
+        o.smax = smax < ucap ? smax : ucap;
         o.est = est;
         o.shift0 = digit_shift<K>(o.smax > est ? o.smax - est : (K)0, H0_BITS);
         o.done = 0;
         o.mode = MODE_NORMAL;
         o.wmode = WR_FAST;
         o.idx_cut = 0xffffffffu;
-        sel[w] = o;
+        a.sel[w] = o;
+        // restore the zero state
+        a.mmg[2 * w] = 0;
+        a.mmg[2 * w + 1] = 0;
+        a.doneg[w] = 0;
     }
+    for (int i = tid; i < SEL_BINS; i += SE_THREADS) h1w[i] = 0;
 }
 
 // --------------------------------------------------------------------------------------
@@ -839,7 +923,7 @@ template <typename T> struct MainArgs {
     unsigned* done;     // [k] (pass-specific)
     int nsubt, nsub;
     unsigned* pp;       // [k][BMAX + 1] sub-range prefix per segment (adaptive split)
-    uint2* submap;      // [k][NSUB_MAX] sub-range -> (segment, part | parts << 16); x = ~0u unused
+    uint4* submap;      // [k][NSUB_MAX] sub-range -> (segment, part | parts << 16, lo, hi); x = ~0u unused
     unsigned dense_thr; // k_main_tma: candidates per tile above which placement is staged
 };
 
@@ -875,6 +959,23 @@ SG_DEV void load_tile(const T* row, long long base, long long dim, bool vec, typ
             else x[r] = make_double2(t[0], t[1]);
         }
     }
+}
+
+// Sub-range i of a segment's n candidates for the split collect/write passes: starts are
+// 4-aligned so the writer's 16-byte loads stay aligned.
+SG_DEV long long sub_lo(long long n, int i, int split) {
+    // floor(n * i / split) in 32-bit: n = q * split + r  =>  q * i + (r * i) / split
+    const unsigned nn = (unsigned)n, sp = (unsigned)split;
+    const unsigned q = nn / sp, r = nn - q * sp;
+    return i == 0 ? 0 : (long long)((q * (unsigned)i + (r * (unsigned)i) / sp) & ~3u);
+}
+SG_DEV int sub_of(long long n, long long off, int split) {
+    // the largest i with sub_lo(n, i) <= off: a proportional guess, then a short walk
+    int i = n > 0 ? (int)(((unsigned long long)off * (unsigned)split) / (unsigned long long)n) : 0;
+    if (i > split - 1) i = split - 1;
+    while (i > 0 && sub_lo(n, i, split) > off) --i;
+    while (i + 1 < split && sub_lo(n, i + 1, split) <= off) ++i;
+    return i;
 }
 
 // Adaptive split: segment s of a worker gets parts_s = max(1, ceil(n_s * nsubt / C)) sub-ranges
@@ -942,11 +1043,12 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
     {
         const unsigned* sc = a.segcnt + (long long)w * a.nseg;
         constexpr int PER = BMAX / TK_THREADS;
-        unsigned pv[PER], sum = 0;
+        unsigned pv[PER], nv[PER], sum = 0;
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
             const int q = tid * PER + u;
-            pv[u] = q < a.nseg ? parts_of(__ldcg(sc + q), C, a.nsubt) : 0u;
+            nv[u] = q < a.nseg ? __ldcg(sc + q) : 0u;
+            pv[u] = q < a.nseg ? parts_of(nv[u], C, a.nsubt) : 0u;
             sum += pv[u];
         }
         __shared__ unsigned s_ps[TK_NW];
@@ -961,14 +1063,18 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
         unsigned run = incl - sum;
         for (int i = 0; i < warp; ++i) run += s_ps[i];
         unsigned* pp = a.pp + (long long)w * (BMAX + 1);
-        uint2* sm = a.submap + (long long)w * NSUB_MAX;
+        uint4* sm = a.submap + (long long)w * NSUB_MAX;
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
             const int q = tid * PER + u;
             if (q < a.nseg) {
                 pp[q] = run;
-                for (unsigned t = 0; t < pv[u] && run + t < (unsigned)a.nsub; ++t)
-                    sm[run + t] = make_uint2((unsigned)q, t | (pv[u] << 16));
+                unsigned lo = 0;
+                for (unsigned t = 0; t < pv[u] && run + t < (unsigned)a.nsub; ++t) {
+                    const unsigned hi = t + 1 == pv[u] ? nv[u] : (unsigned)sub_lo(nv[u], (int)t + 1, (int)pv[u]);
+                    sm[run + t] = make_uint4((unsigned)q, t | (pv[u] << 16), lo, hi);
+                    lo = hi;
+                }
             }
             run += pv[u];
         }
@@ -976,7 +1082,7 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
         if (tid == TK_THREADS - 1) s_tot = run;
         __syncthreads();
         if (tid == 0) pp[a.nseg] = s_tot;
-        for (int i = (int)s_tot + tid; i < a.nsub; i += TK_THREADS) sm[i] = make_uint2(0xffffffffu, 0u);
+        for (int i = (int)s_tot + tid; i < a.nsub; i += TK_THREADS) sm[i] = make_uint4(0xffffffffu, 0u, 0u, 0u);
     }
     int bin;
     unsigned long long above;
@@ -1294,28 +1400,11 @@ k_main(MainArgs<T> a) {
 // --------------------------------------------------------------------------------------
 // k_collect: per-segment counts above the rank-m bin + boundary entries; last CTA resolves.
 // --------------------------------------------------------------------------------------
-// Sub-range i of a segment's n candidates for the split collect/write passes: starts are
-// 4-aligned so the writer's 16-byte loads stay aligned.
-SG_DEV long long sub_lo(long long n, int i, int split) {
-    // floor(n * i / split) in 32-bit: n = q * split + r  =>  q * i + (r * i) / split
-    const unsigned nn = (unsigned)n, sp = (unsigned)split;
-    const unsigned q = nn / sp, r = nn - q * sp;
-    return i == 0 ? 0 : (long long)((q * (unsigned)i + (r * (unsigned)i) / sp) & ~3u);
-}
-SG_DEV int sub_of(long long n, long long off, int split) {
-    // the largest i with sub_lo(n, i) <= off: a proportional guess, then a short walk
-    int i = n > 0 ? (int)(((unsigned long long)off * (unsigned)split) / (unsigned long long)n) : 0;
-    if (i > split - 1) i = split - 1;
-    while (i > 0 && sub_lo(n, i, split) > off) --i;
-    while (i + 1 < split && sub_lo(n, i + 1, split) <= off) ++i;
-    return i;
-}
-
 template <typename T> struct CollectArgs {
     long long segcap, cap;         // cap: boundary entries stored per worker (RES)
     int nseg, tps, split, nsub, nsubt;
     const unsigned* pp;            // [k][BMAX + 1] (from the main pass's last CTA)
-    const uint2* submap;           // [k][NSUB_MAX]
+    const uint4* submap;           // [k][NSUB_MAX]
     uint32_t* bpos;                // [k][cap] boundary entry's position in its segment list
     SelState<typename KeyOf<T>::K>* sel;
     const unsigned* segcnt;
@@ -1375,26 +1464,17 @@ k_collect(CollectArgs<T> a) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
     __shared__ unsigned s_gt[TK_NW];
-    __shared__ int s_map[3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, sub = blockIdx.x;
-    if (tid == 0) {
-        const uint2 e = a.submap[(long long)w * NSUB_MAX + sub];
-        s_map[0] = e.x == 0xffffffffu ? -1 : (int)e.x;
-        s_map[1] = (int)(e.y & 0xffffu);
-        s_map[2] = (int)(e.y >> 16);
-    }
-    __syncthreads();
-    const int seg = s_map[0], part = s_map[1], split = s_map[2];
+    const uint4 e = a.submap[(long long)w * NSUB_MAX + sub];  // (uniform: every thread loads it)
+    const int seg = e.x == 0xffffffffu ? -1 : (int)e.x;
     if (seg < 0) {  // beyond the worker's sub-ranges
         if (tid == 0) a.seggt[(long long)w * a.nsub + sub] = 0;
         return;
     }
     const SelState<K> st = a.sel[w];
     const K lo = st.lo, span = st.span;
-    const long long nseg_c = a.segcnt[(long long)w * a.nseg + seg];
-    const int lo32 = (int)sub_lo(nseg_c, part, split);
-    const int hi32 = (int)(part + 1 == split ? nseg_c : sub_lo(nseg_c, part + 1, split));
+    const int lo32 = (int)e.z, hi32 = (int)e.w;
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     K* bk = a.bkey + (long long)w * a.cap;
@@ -1710,7 +1790,7 @@ k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
 template <typename T> struct WriteArgs {
     long long ntiles, segcap, m;
     int k, nseg, tps, split, nsub, nsubt;
-    const uint2* submap;
+    const uint4* submap;
     const SelState<typename KeyOf<T>::K>* sel;
     const unsigned* tstart;
     const unsigned* segcnt;
@@ -1777,25 +1857,23 @@ SG_DEV void write_tail(const WriteArgs<T>& a, double ss) {
 // WF_SPAN entries, thread t owning WF_EPT consecutive entries, with the next chunk's loads in
 // flight while the current one is processed: one block scan of the kept counts gives every
 // kept entry its output slot; the kept run is compacted in shared memory and stored
-// coalesced; each thread sets the merge offsets of the tiles whose first candidate lies in
-// its run (read off the tile changes between consecutive candidate indices).
+// coalesced.  Merge offsets: toff[t] = kept entries with index < 4096 t.  This CTA owns the
+// tile boundaries after the candidate before its range up to its last candidate (the whole
+// segment tail for the segment's last part); a boundary between two consecutive kept entries
+// gets the second one's slot, so the store loop sets them, one kept entry per thread.
 constexpr int WF_EPT = 4;
 constexpr int WF_SPAN = TK_THREADS * WF_EPT;  // 1024 entries per chunk
 
 template <typename T>
 SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
-                         typename KeyOf<T>::K T_, unsigned cut, unsigned char* stage, int seg_, int part_,
-                         int split_) {
+                         typename KeyOf<T>::K T_, unsigned cut, unsigned char* stage, int seg, int lo32, int n32,
+                         bool last_part) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
     __shared__ unsigned s_wt[TK_NW];
-    __shared__ uint32_t s_wl[TK_NW];  // last candidate index of each warp's run in the chunk
-    __shared__ uint32_t s_carry;      // last candidate index before the chunk
+    __shared__ int s_ltile;  // tile of the last kept entry so far (initially of the candidate before the range)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int w = blockIdx.y, sub = blockIdx.x, seg = seg_, part = part_, split = split_;
-    const long long nsc = a.segcnt[(long long)w * a.nseg + seg];
-    const int lo32 = (int)sub_lo(nsc, part, split);
-    const int n32 = (int)(part + 1 == split ? nsc : sub_lo(nsc, part + 1, split));
+    const int w = blockIdx.y, sub = blockIdx.x;
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     uint32_t* oi = a.idx + (long long)w * a.m;
@@ -1806,7 +1884,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
         load16<T, WF_EPT>(cv, lo32 + tid * WF_EPT, n32, v);
         load16_idx<WF_EPT>(ci, lo32 + tid * WF_EPT, n32, ii);
     }
-    if (tid == 0) s_carry = toff && lo32 > 0 && lo32 < n32 ? ci[lo32 - 1] : 0u;
+    if (tid == 0) s_ltile = lo32 > 0 ? (int)(ci[lo32 - 1] >> MERGE_SHIFT) : (int)t0 - 1;
     unsigned g32 = a.segbase[(long long)w * a.nsub + sub];
     T* st_v = reinterpret_cast<T*>(stage);                        // [WF_SPAN]
     uint32_t* st_i = reinterpret_cast<uint32_t*>(st_v + WF_SPAN);  // [WF_SPAN]
@@ -1837,11 +1915,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             const unsigned y = __shfl_up_sync(FULL, incl, o);
             if (lane >= o) incl += y;
         }
-        const uint32_t left = __shfl_up_sync(FULL, xi[WF_EPT - 1], 1);
-        if (lane == 31) {
-            s_wt[warp] = incl;
-            s_wl[warp] = xi[WF_EPT - 1];
-        }
+        if (lane == 31) s_wt[warp] = incl;
         __syncthreads();
         unsigned wb = 0, tot = 0;
 #pragma unroll
@@ -1849,23 +1923,6 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             const unsigned t = s_wt[i];
             wb += i < warp ? t : 0u;
             tot += t;
-        }
-        const unsigned pos = g32 + wb + incl - cnt;  // output slot of this thread's first kept entry
-        if (toff && e0 < n32) {
-            // merge offsets: every tile t with tile(previous candidate) < t <= tile(this
-            // candidate) starts at this candidate: toff[t] = kept entries before it
-            const uint32_t prev = lane > 0 ? left : (warp > 0 ? s_wl[warp - 1] : s_carry);
-            int tp = e0 == 0 ? (int)t0 - 1 : (int)(prev >> MERGE_SHIFT);
-            const int ul = (e0 + WF_EPT <= n32 ? WF_EPT : n32 - e0) - 1;  // last valid entry
-            if ((int)(xi[ul] >> MERGE_SHIFT) != tp) {  // a tile starts in this run (rare)
-#pragma unroll
-                for (int u = 0; u < WF_EPT; ++u) {
-                    if (u > ul) break;
-                    const int tc = (int)(xi[u] >> MERGE_SHIFT);
-                    for (int t = tp + 1; t <= tc; ++t) toff[t] = (int)(pos + __popc(kf & ((1u << u) - 1u)));
-                    tp = tc;
-                }
-            }
         }
         // compact into shared memory, then coalesced stores of the chunk's kept run
         unsigned lp = wb + incl - cnt;
@@ -1877,23 +1934,34 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             ++lp;
         }
         __syncthreads();
+        const int lt0 = s_ltile;
+        int lt_new = -2;
         for (unsigned q = tid; q < tot; q += TK_THREADS) {
+            const uint32_t iq = st_i[q];
+            if (toff) {  // boundaries after the previous kept entry up to this one
+                const int tc = (int)(iq >> MERGE_SHIFT);
+                const int tp = q > 0 ? (int)(st_i[q - 1] >> MERGE_SHIFT) : lt0;
+                for (int t = tp + 1; t <= tc; ++t) toff[t] = (int)(g32 + q);
+                if (q + 1 == tot) lt_new = tc;
+            }
             if (g32 + q < (unsigned)a.m) {
                 const T y = st_v[q];
-                oi[g32 + q] = st_i[q];
+                oi[g32 + q] = iq;
                 ov[g32 + q] = y;
                 ss = fma((double)y, (double)y, ss);
             }
         }
-        if (tid == TK_THREADS - 1) s_carry = xi[WF_EPT - 1];  // the next chunk's predecessor
         g32 += tot;
-        __syncthreads();  // s_wt, s_wl and the staging are reused
+        __syncthreads();  // s_wt, s_ltile and the staging are reused
+        if (lt_new != -2) s_ltile = lt_new;
     }
-    if (toff && part + 1 == split) {
-        // tiles after the segment's last candidate (to the segment end): offset = kept total
-        const int tl = nsc > 0 ? (int)(ci[nsc - 1] >> MERGE_SHIFT) : (int)t0 - 1;
-        for (int t = tl + 1 + tid; t < (int)(t0 + nt); t += TK_THREADS) toff[t] = (int)g32;
-        if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
+    if (toff) {
+        // boundaries after the last kept entry: up to this range's last candidate, or to the
+        // segment end for its last part
+        __syncthreads();
+        const int tend = last_part ? (int)(t0 + nt) - 1 : (n32 > 0 ? (int)(ci[n32 - 1] >> MERGE_SHIFT) : (int)t0 - 1);
+        for (int t = s_ltile + 1 + tid; t <= tend; t += TK_THREADS) toff[t] = (int)g32;
+        if (last_part && tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }
     return ss;
 }
@@ -1908,17 +1976,11 @@ SG_DEV void write_body(const WriteArgs<T>& a) {
     __shared__ unsigned long long s_gb, s_eb;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned* s_ts = reinterpret_cast<unsigned*>(smem_raw);  // [tps] tile starts of this segment
-    __shared__ int s_map[3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, sub = blockIdx.x;
-    if (tid == 0) {
-        const uint2 e = a.submap[(long long)w * NSUB_MAX + sub];
-        s_map[0] = e.x == 0xffffffffu ? -1 : (int)e.x;
-        s_map[1] = (int)(e.y & 0xffffu);
-        s_map[2] = (int)(e.y >> 16);
-    }
-    __syncthreads();
-    const int seg = s_map[0], part = s_map[1], split = s_map[2];
+    const uint4 e = a.submap[(long long)w * NSUB_MAX + sub];  // (uniform: every thread loads it)
+    const int seg = e.x == 0xffffffffu ? -1 : (int)e.x;
+    const int part = (int)(e.y & 0xffffu), split = (int)(e.y >> 16);
     if (seg < 0) {  // beyond the worker's sub-ranges: no kept entries, no norm
         if (tid == 0) a.pwrite[(long long)w * a.nsub + sub] = 0.0;
         return;
@@ -1928,9 +1990,8 @@ SG_DEV void write_body(const WriteArgs<T>& a) {
     const unsigned cut = st.idx_cut;
     const unsigned long long need = st.rank;
     const bool slow = st.wmode == WR_SLOW;
-    const long long nsc = a.segcnt[(long long)w * a.nseg + seg];
-    const long long i_lo = sub_lo(nsc, part, split);
-    const long long n = part + 1 == split ? nsc : sub_lo(nsc, part + 1, split);  // end of the sub-range
+    const long long i_lo = e.z;
+    const long long n = e.w;  // end of the sub-range
     const bool last_part = part + 1 == split;
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
@@ -1940,7 +2001,8 @@ SG_DEV void write_body(const WriteArgs<T>& a) {
 
     if (!slow) {
         write_tail<T>(a, write_fast<T>(a, nt, t0, toff, T_, cut,
-                                       smem_raw + align_up(sizeof(unsigned) * (size_t)a.tps, 16), seg, part, split));
+                                       smem_raw + align_up(sizeof(unsigned) * (size_t)a.tps, 16), seg, (int)i_lo,
+                                       (int)n, last_part));
         return;
     }
     if (toff) {
@@ -2265,29 +2327,42 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     K* samp = reinterpret_cast<K*>(at(p.off_samp));
     K* mm = reinterpret_cast<K*>(at(p.off_mm));
     unsigned* hs1 = reinterpret_cast<unsigned*>(at(p.off_hs1));
+    uint4* zero = reinterpret_cast<uint4*>(base + p.zero_begin);
+    const long long zero_vec = (long long)((p.zero_end - p.zero_begin) / 16);
     if constexpr (sizeof(K) == 4) {
         if (sample_est_fused()) {
-            // one clustered launch: the sample stays in shared memory
-            cudaError_t e = smem_attr((const void*)k_sample_est_f32, (int)SE_SMEM);
+            const int G = se_ctas(k);
+            cudaError_t e = smem_attr((const void*)k_sample_est_f32, (int)se_smem(G));
             if (e != cudaSuccess) return e;
-            // bulk-copy sampling needs 16-byte aligned rows and strata of >= 40 elements
-            const int tma = se_tma() && p.s_eff < dim && (reinterpret_cast<size_t>(g) % 16 == 0) && (ld % 4 == 0) &&
-                            dim / (p.s_eff / CHUNK) >= 40;
-            launch_pdl(k_sample_est_f32, dim3(SE_CL, k), dim3(SE_THREADS), SE_SMEM, stream, (const float*)g, ld, dim,
-                       p.s_eff, p.r_est, reinterpret_cast<SelState<uint32_t>*>(sel), reinterpret_cast<uint4*>(base),
-                       (long long)(p.zero_end / 16), tma);
+            SampleEstArgs sa;
+            sa.g = (const float*)g;
+            sa.ld = ld;
+            sa.dim = dim;
+            sa.s_eff = p.s_eff;
+            sa.r_est = p.r_est;
+            sa.r_hi = p.r_hi;
+            sa.vec = (reinterpret_cast<size_t>(g) % 16 == 0) && (ld % 4 == 0) && p.s_eff < dim &&
+                     dim / (p.s_eff / SE_CHUNK) >= SE_CHUNK + 4;
+            sa.sel = reinterpret_cast<SelState<uint32_t>*>(sel);
+            sa.zero = zero;
+            sa.zero_vec = zero_vec;
+            sa.bkeys = reinterpret_cast<uint32_t*>(samp);
+            sa.boff = reinterpret_cast<uint16_t*>(at(p.off_boff));
+            sa.h1g = reinterpret_cast<unsigned*>(at(p.off_se_h1));
+            sa.mmg = reinterpret_cast<unsigned*>(at(p.off_se_mm));
+            sa.doneg = reinterpret_cast<unsigned*>(at(p.off_se_done));
+            launch_pdl(k_sample_est_f32, dim3(G, k), dim3(SE_THREADS), se_smem(G), stream, sa);
             debug_sync("k_sample_est", stream);
         } else {
-            launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm,
-                       reinterpret_cast<uint4*>(base), (long long)(p.zero_end / 16), hs1);
+            launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm, zero, zero_vec,
+                       hs1);
             debug_sync("k_sample", stream);
             launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), 0, stream, dim, p.s_eff, p.r_est,
                        (const K*)samp, (const K*)mm, EST_G, sel, hs1);
             debug_sync("k_estimate", stream);
         }
     } else {
-        launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm,
-                   reinterpret_cast<uint4*>(base), (long long)(p.zero_end / 16), hs1);
+        launch_pdl(k_sample<T>, dim3(EST_G, k), dim3(256), 0, stream, g, ld, dim, p.s_eff, samp, mm, zero, zero_vec, hs1);
         debug_sync("k_sample", stream);
         launch_pdl(k_estimate<T>, dim3(k), dim3(EST_THREADS), 0, stream, dim, p.s_eff, p.r_est,
                    (const K*)samp, (const K*)mm, EST_G, sel, hs1);
@@ -2320,7 +2395,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ma.nsubt = p.nsubt;
     ma.nsub = p.nsub;
     ma.pp = reinterpret_cast<unsigned*>(at(p.off_pp));
-    ma.submap = reinterpret_cast<uint2*>(at(p.off_submap));
+    ma.submap = reinterpret_cast<uint4*>(at(p.off_submap));
     ma.dense_thr = mn_dense();
     const dim3 sgrid((unsigned)p.nseg, (unsigned)k);
     bool tma = false;
@@ -2464,10 +2539,11 @@ size_t sg_topk_workspace_bytes_fused_f32(int k, int64_t dim, int64_t m) {
 }
 
 size_t sg_topk_workspace_zero_bytes_f32(int k, int64_t dim, int64_t m) {
-    (void)k;  // the launch chain keeps no state between calls
-    (void)dim;
-    (void)m;
-    return 0;
+    // k_sample_est's histogram / key range / arrival counters (restored by every call), plus the
+    // slack of the 256-byte base alignment
+    if (k < 1 || dim < 1 || m < 1 || m > dim || k > MAX_WORKERS) return 0;
+    return make_plan<float>(k, dim, m, segments_per_worker<float>(k, dim), (long long)num_sms() * CW_PER_SM).state_end +
+           256;
 }
 
 size_t sg_topk_workspace_zero_bytes_fused_f32(int k, int64_t dim, int64_t m) {

@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/c35; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_topk.py tests/test_gpu_topk_fused.py tests/test_gpu_bench_parity.py tests/test_gpu_race_stress.py tests/test_gpu_real_gradient.py tests/test_gpu_gate_aggregate.py tests/test_gpu_dropin.py -m gpu -x -q -rs > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+timeout 300 python tools/topk_timing.py --iters 10 > $O/topk.txt 2>&1
+M="--metrics gpu__time_duration.sum --clock-control none --csv"
+timeout 600 ncu $M --log-file $O/k1.csv python tools/one_step.py --steps 2 --workers 1 > $O/k1.log 2>&1
+timeout 600 ncu $M --log-file $O/k8.csv python tools/one_step.py --steps 2 > $O/k8.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline --no-e2e > $O/bench.json 2> $O/bench.err
+timeout 600 python tools/train_resnet152.py --steps 4 > $O/train.json 2> $O/train.err

@@ -1,36 +1,51 @@
-"""Per-CUDA-source-line instruction and stall totals from an .ncu-rep (needs -lineinfo)."""
-import csv
-import subprocess
-import sys
-from collections import defaultdict
+"""Aggregate an ncu source page (--page source --csv --print-source cuda,sass) per CUDA source
+line: warp-stall samples, executed warp instructions and the top stall reasons.
 
-rep, kern = sys.argv[1], sys.argv[2]
-n = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{kern}"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(out.splitlines()))
+    ncu -i REP --page source --csv --print-source cuda,sass -k regex:NAME > x.csv
+    python tools/ncu_lines.py x.csv [N]
+"""
+import collections
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+fname = "?"
 hdr = None
-agg = defaultdict(lambda: [0, 0, ""])
+agg = collections.defaultdict(lambda: collections.Counter())
+text = {}
 cur = None
-for x in rows:
-    if x and x[0] == "Line No":
-        hdr = x
+for r in rows:
+    if not r:
         continue
-    if hdr is None or len(x) < 8:
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
         continue
-    if x[0]:
-        cur = (x[0], x[1])
+    if r[0] == "Line No":
+        hdr = r
         continue
-    try:
-        ws = int(x[4] or 0)
-        ie = int(x[7] or 0)
-    except ValueError:
+    if hdr is None or len(r) < len(hdr):
         continue
-    a = agg[cur]
-    a[0] += ie
-    a[1] += ws
-tot_i = sum(v[0] for v in agg.values())
-tot_s = sum(v[1] for v in agg.values())
-print(f"total warp-instr {tot_i}  samples {tot_s}")
-for (ln, src), (ie, ws, _) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:n]:
-    print(f"{ie:11d} {100*ie/max(tot_i,1):5.1f}%  st {ws:6d}  L{ln:>4} {src.strip()[:90]}")
+    if r[0].strip().isdigit():
+        cur = (fname, int(r[0]))
+        text[cur] = r[1].strip()
+    if cur is None or not r[2].strip():
+        continue
+    d = dict(zip(hdr[2:], r[2:]))
+    c = agg[cur]
+    for k in ("Warp Stall Sampling (All Samples)", "Instructions Executed"):
+        v = d.get(k, "")
+        if v.replace(".", "").isdigit():
+            c[k] += float(v)
+    for k, v in d.items():
+        if k.startswith("stall_") and "Not Issued" not in k and v.replace(".", "").isdigit():
+            c[k] += float(v)
+tot = sum(c["Warp Stall Sampling (All Samples)"] for c in agg.values())
+toti = sum(c["Instructions Executed"] for c in agg.values())
+print(f"samples {tot:.0f}  warp instructions {toti:.0f}")
+top = sorted(agg.items(), key=lambda kv: -kv[1]["Warp Stall Sampling (All Samples)"])[:N]
+for (f, ln), c in sorted(top, key=lambda kv: kv[0]):
+    s = c["Warp Stall Sampling (All Samples)"]
+    st = sorted(((v, k[6:]) for k, v in c.items() if k.startswith("stall_")), reverse=True)[:3]
+    print(f"{f}:{ln:<5d} {100 * s / tot:5.1f}% inst {c['Instructions Executed']:10.0f}  "
+          f"{' '.join(f'{k}={v:.0f}' for v, k in st):40s} {text.get((f, ln), '')[:70]}")
