@@ -1941,7 +1941,10 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             if (toff) {  // boundaries after the previous kept entry up to this one
                 const int tc = (int)(iq >> MERGE_SHIFT);
                 const int tp = q > 0 ? (int)(st_i[q - 1] >> MERGE_SHIFT) : lt0;
-                for (int t = tp + 1; t <= tc; ++t) toff[t] = (int)(g32 + q);
+                if (tc != tp) {  // rare: this entry is the first kept one of tile(s) (tp, tc]
+#pragma unroll 1
+                    for (int t = tp + 1; t <= tc; ++t) toff[t] = (int)(g32 + q);
+                }
                 if (q + 1 == tot) lt_new = tc;
             }
             if (g32 + q < (unsigned)a.m) {
