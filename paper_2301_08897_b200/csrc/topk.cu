@@ -925,6 +925,7 @@ template <typename T> struct MainArgs {
     unsigned* pp;       // [k][BMAX + 1] sub-range prefix per segment (adaptive split)
     uint4* submap;      // [k][NSUB_MAX] sub-range -> (segment, part | parts << 16, lo, hi); x = ~0u unused
     unsigned dense_thr; // k_main_tma: candidates per tile above which placement is staged
+    int split_late;     // fallback launch: build the split of pass 0 when the fallback is not taken
 };
 
 // Per-lane exclusive prefix and warp total of a small count n (0..7) via 3 ballots.
@@ -987,10 +988,62 @@ SG_DEV unsigned parts_of(unsigned n, unsigned long long C, int nsubt) {
     return q < 1 ? 1u : (unsigned)q;
 }
 
+// The adaptive collect/write split of worker w: parts per segment by candidate count
+// (parts_of), their prefix and the sub-range map with each sub-range's candidate bounds.
+// Block-uniform; C = the worker's candidate count.
+template <typename T>
+SG_DEV void build_submap(const MainArgs<T>& a, int w, unsigned long long C) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {
+        const unsigned* sc = a.segcnt + (long long)w * a.nseg;
+        constexpr int PER = BMAX / TK_THREADS;
+        unsigned pv[PER], nv[PER], sum = 0;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int q = tid * PER + u;
+            nv[u] = q < a.nseg ? __ldcg(sc + q) : 0u;
+            pv[u] = q < a.nseg ? parts_of(nv[u], C, a.nsubt) : 0u;
+            sum += pv[u];
+        }
+        __shared__ unsigned s_ps[TK_NW];
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_ps[warp] = incl;
+        __syncthreads();
+        unsigned run = incl - sum;
+        for (int i = 0; i < warp; ++i) run += s_ps[i];
+        unsigned* pp = a.pp + (long long)w * (BMAX + 1);
+        uint4* sm = a.submap + (long long)w * NSUB_MAX;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int q = tid * PER + u;
+            if (q < a.nseg) {
+                pp[q] = run;
+                unsigned lo = 0;
+                for (unsigned t = 0; t < pv[u] && run + t < (unsigned)a.nsub; ++t) {
+                    const unsigned hi = t + 1 == pv[u] ? nv[u] : (unsigned)sub_lo(nv[u], (int)t + 1, (int)pv[u]);
+                    sm[run + t] = make_uint4((unsigned)q, t | (pv[u] << 16), lo, hi);
+                    lo = hi;
+                }
+            }
+            run += pv[u];
+        }
+        __shared__ unsigned s_tot;
+        if (tid == TK_THREADS - 1) s_tot = run;
+        __syncthreads();
+        if (tid == 0) pp[a.nseg] = s_tot;
+        for (int i = (int)s_tot + tid; i < a.nsub; i += TK_THREADS) sm[i] = make_uint4(0xffffffffu, 0u, 0u, 0u);
+    }
+}
+
 // Segment epilogue shared by both main-pass kernels: fixed-tree partial norm, segment count,
 // max key, round-0 histogram flush; the last CTA of each worker picks the rank-m bin (or
 // flags the fallback pass when fewer than m keys reached est).
-template <typename T>
+template <typename T, bool SPLIT>
 SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typename KeyOf<T>::K mx, unsigned run,
                         unsigned* hist, typename KeyOf<T>::K est, int shift0) {
     using K = typename KeyOf<T>::K;
@@ -1038,52 +1091,9 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
         }
         return;
     }
-    // the adaptive collect/write split, computed once here (the last CTA of the worker's
-    // pass): parts per segment by candidate count, their prefix and the sub-range map
-    {
-        const unsigned* sc = a.segcnt + (long long)w * a.nseg;
-        constexpr int PER = BMAX / TK_THREADS;
-        unsigned pv[PER], nv[PER], sum = 0;
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int q = tid * PER + u;
-            nv[u] = q < a.nseg ? __ldcg(sc + q) : 0u;
-            pv[u] = q < a.nseg ? parts_of(nv[u], C, a.nsubt) : 0u;
-            sum += pv[u];
-        }
-        __shared__ unsigned s_ps[TK_NW];
-        unsigned incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) s_ps[warp] = incl;
-        __syncthreads();
-        unsigned run = incl - sum;
-        for (int i = 0; i < warp; ++i) run += s_ps[i];
-        unsigned* pp = a.pp + (long long)w * (BMAX + 1);
-        uint4* sm = a.submap + (long long)w * NSUB_MAX;
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int q = tid * PER + u;
-            if (q < a.nseg) {
-                pp[q] = run;
-                unsigned lo = 0;
-                for (unsigned t = 0; t < pv[u] && run + t < (unsigned)a.nsub; ++t) {
-                    const unsigned hi = t + 1 == pv[u] ? nv[u] : (unsigned)sub_lo(nv[u], (int)t + 1, (int)pv[u]);
-                    sm[run + t] = make_uint4((unsigned)q, t | (pv[u] << 16), lo, hi);
-                    lo = hi;
-                }
-            }
-            run += pv[u];
-        }
-        __shared__ unsigned s_tot;
-        if (tid == TK_THREADS - 1) s_tot = run;
-        __syncthreads();
-        if (tid == 0) pp[a.nseg] = s_tot;
-        for (int i = (int)s_tot + tid; i < a.nsub; i += TK_THREADS) sm[i] = make_uint4(0xffffffffu, 0u, 0u, 0u);
-    }
+    // the adaptive collect/write split (k_main's: the TMA pass leaves it to the fallback
+    // launch, which always runs, so the streaming kernel carries none of its code)
+    if constexpr (SPLIT) build_submap<T>(a, w, C);
     int bin;
     unsigned long long above;
     block_find_bin_from_top<H0_BINS, TK_THREADS>(hist, (unsigned long long)a.m, bin, above);
@@ -1290,7 +1300,7 @@ k_main_tma(MainArgs<float> a) {
         scan_and_place(M, base, tile, src);
         __syncthreads();
     }
-    main_finish<float>(a, w, seg, dadd(ss, ss1), mx, run, hist, est, shift0);
+    main_finish<float, false>(a, w, seg, dadd(ss, ss1), mx, run, hist, est, shift0);
 }
 
 template <typename T>
@@ -1309,7 +1319,11 @@ k_main(MainArgs<T> a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, seg = blockIdx.x;
     SelState<K>* stp = a.sel + w;
-    if (a.pass == 1 && stp->mode != MODE_FALLBACK) return;
+    if (a.pass == 1 && stp->mode != MODE_FALLBACK) {
+        // not taken: the split of the (TMA) main pass, by the worker's first CTA
+        if (a.split_late && seg == 0) build_submap<T>(a, w, __ldcg(a.count + w));
+        return;
+    }
     const K est = a.pass == 1 ? (K)0 : stp->est;
     const int shift0 = a.pass == 1 ? digit_shift<K>(KO::KMAX, H0_BITS) : stp->shift0;
     for (int i = tid; i < H0_BINS; i += TK_THREADS) hist[i] = 0;
@@ -1394,7 +1408,7 @@ k_main(MainArgs<T> a) {
             }
         }
     }
-    main_finish<T>(a, w, seg, ss, mx, s_run, hist, est, shift0);
+    main_finish<T, true>(a, w, seg, ss, mx, s_run, hist, est, shift0);
 }
 
 // --------------------------------------------------------------------------------------
@@ -2400,6 +2414,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ma.pp = reinterpret_cast<unsigned*>(at(p.off_pp));
     ma.submap = reinterpret_cast<uint4*>(at(p.off_submap));
     ma.dense_thr = mn_dense();
+    ma.split_late = 0;
     const dim3 sgrid((unsigned)p.nseg, (unsigned)k);
     bool tma = false;
     if constexpr (sizeof(T) == 4) tma = vec_ok;
@@ -2417,7 +2432,10 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ma.pass = 1;
     ma.hist0 = hist0fb;
     ma.done = c_fb;
-    launch_main();
+    ma.split_late = tma ? 1 : 0;
+    // the fallback pass (normally an early exit) is the generic kernel: it also builds the split
+    // after the TMA pass
+    launch_pdl(k_main<T>, dim3(sgrid), dim3(TK_THREADS), 0, stream, ma);
     debug_sync("k_main(fb)", stream);
     // 3. per-segment counts + boundary, in-CTA resolve
     CollectArgs<T> ca;
