@@ -68,14 +68,21 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return _build_locked(verbose)
 
 
-def _build_locked(verbose: bool) -> Path:
+def build_variant(out: Path, extra: list[str]) -> Path:
+    """A diagnostic build (e.g. ``-DSG_STAMPS``) linked to ``out``, leaving the product
+    library untouched; load it by pointing ``_capi.LIB_PATH`` at ``out`` before the first call."""
+    (PKG / "build").mkdir(exist_ok=True)
+    return _build_locked(False, extra=extra, lib=Path(out))
+
+
+def _build_locked(verbose: bool, extra: list[str] | None = None, lib: Path = LIB) -> Path:
     objdir = PKG / "build" / f"obj.{os.getpid()}"
     objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
-        extra = os.environ.get("SG_NVCC_EXTRA", "").split()  # e.g. -DSG_PHASES (diagnostic builds)
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
+        flags = os.environ.get("SG_NVCC_EXTRA", "").split() + list(extra or [])  # e.g. -DSG_PHASES (diagnostics)
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *flags, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -84,14 +91,14 @@ def _build_locked(verbose: bool) -> Path:
         if verbose and r.stderr:
             print(r.stderr, file=sys.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
+    tmp = lib.with_suffix(f".so.tmp{os.getpid()}")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     shutil.rmtree(objdir, ignore_errors=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -367,6 +367,7 @@ template <typename TO>
 __global__ void __launch_bounds__(MG_THREADS, 2)
 k_merge(const AggArgs<float, TO> a) {
     pdl_enter();
+    SG_STAMP(1);
     extern __shared__ __align__(128) unsigned char mg_smem[];
     double* acc_s = reinterpret_cast<double*>(mg_smem);                   // [AG_TILE]
     float* ent_val = reinterpret_cast<float*>(acc_s + AG_TILE);            // [MG_ECAP]
@@ -709,6 +710,7 @@ template <typename TO>
 __global__ void __launch_bounds__(MW_THREADS, 1)
 k_merge_ws(const AggArgs<float, TO> a) {
     pdl_enter();
+    SG_STAMP(0);
     extern __shared__ __align__(128) unsigned char mw_smem[];
     float* ring = reinterpret_cast<float*>(mw_smem);                     // [S][2][TILE]
     double* acc = reinterpret_cast<double*>(ring + MW_STAGES * 2 * AG_TILE);  // [2][TILE]
@@ -1140,6 +1142,7 @@ template <typename TO>
 __global__ void __launch_bounds__(MO_THREADS, 2)
 k_merge_own(const AggArgs<float, TO> a) {
     pdl_wait();  // no early trigger: the next kernel's CTAs must not take this grid's SM slots
+    SG_STAMP(2);
     extern __shared__ __align__(16) unsigned char mo_smem[];
     double (*sacc)[MO_THREADS] = reinterpret_cast<double (*)[MO_THREADS]>(mo_smem);  // [MO_PER][MO_THREADS]
     float* st_v0 = reinterpret_cast<float*>(mo_smem + MO_PER * MO_THREADS * sizeof(double));  // [2][MO_ECAP]
@@ -1964,6 +1967,8 @@ __global__ void k_gather_bytes(GatherSrc src, int nsrc, long long each, uint8_t*
 }  // namespace sg
 
 using namespace sg;
+
+SG_STAMPS_EXPORT(sg_diag_stamps_agg)
 
 extern "C" {
 

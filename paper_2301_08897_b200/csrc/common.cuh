@@ -338,6 +338,42 @@ inline cudaError_t smem_attr(const void* kern, int bytes) {
     return e;
 }
 
+// Diagnostic build only (-DSG_STAMPS via SG_NVCC_EXTRA): per-kernel first-CTA start and
+// last-CTA end on %globaltimer, one slot pair per kernel id and translation unit, read and
+// reset by sg_diag_stamps_<tu> (tools/stamps.py).  The product build compiles none of it.
+#ifdef SG_STAMPS
+SG_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+static __device__ unsigned long long g_stamp[2 * 16];
+struct StampScope {
+    int id;
+    __device__ explicit StampScope(int i) : id(i) {
+        if (threadIdx.x == 0) atomicMin(&g_stamp[2 * id], gtimer());
+    }
+    __device__ ~StampScope() {
+        if (threadIdx.x == 0) atomicMax(&g_stamp[2 * id + 1], gtimer());
+    }
+};
+#define SG_STAMP(id) ::sg::StampScope sg_stamp_scope_##id(id)
+#define SG_STAMPS_EXPORT(name)                                                             \
+    extern "C" int name(unsigned long long* out) {                                        \
+        if (cudaMemcpyFromSymbol(out, ::sg::g_stamp, sizeof(::sg::g_stamp)) != cudaSuccess) \
+            return SG_ERR_CUDA;                                                            \
+        unsigned long long init[2 * 16];                                                   \
+        for (int i = 0; i < 16; ++i) {                                                     \
+            init[2 * i] = ~0ull;                                                           \
+            init[2 * i + 1] = 0ull;                                                        \
+        }                                                                                  \
+        return cudaMemcpyToSymbol(::sg::g_stamp, init, sizeof(init)) == cudaSuccess ? SG_OK : SG_ERR_CUDA; \
+    }
+#else
+#define SG_STAMP(id) do { } while (0)
+#define SG_STAMPS_EXPORT(name)
+#endif
+
 inline int num_sms() {
     int dev = 0, n = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);

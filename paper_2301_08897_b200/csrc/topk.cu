@@ -678,6 +678,7 @@ struct SampleEstArgs {
 __global__ void __launch_bounds__(SE_THREADS)
 k_sample_est_f32(SampleEstArgs a) {
     pdl_enter();
+    SG_STAMP(0);
     using KO = KeyOf<float>;
     using K = uint32_t;
     extern __shared__ __align__(16) K se_smem_raw[];
@@ -1136,7 +1137,11 @@ inline unsigned mn_dense() {  // SG_MN_DENSE overrides (A/B runs)
 
 __global__ void __launch_bounds__(TK_THREADS, 3)
 k_main_tma(MainArgs<float> a) {
-    pdl_enter();
+    SG_STAMP(1);
+    // The prologue does not depend on the estimate: the ring starts filling while k_sample_est
+    // may still be running (PDL).  (Prefetching further tiles of the segment into L2 here as
+    // well measured 1-3% slower at k = 1..8.)
+    pdl_trigger();
     using K = uint32_t;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* ring = reinterpret_cast<float*>(smem_raw);
@@ -1146,19 +1151,10 @@ k_main_tma(MainArgs<float> a) {
     __shared__ unsigned short s_stage[MN_TILE];  // dense tiles: candidate offsets in index order
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, seg = blockIdx.x;
-    SelState<K>* stp = a.sel + w;
-    if (a.pass == 1 && stp->mode != MODE_FALLBACK) return;
-    const K est = a.pass == 1 ? 0u : stp->est;
-    const int shift0 = a.pass == 1 ? digit_shift<K>(KeyOf<float>::KMAX, H0_BITS) : stp->shift0;
-    const bool take_all = est == 0;
-    const float thr = take_all ? 0.f : __uint_as_float(est - 1u);  // key >= est <=> |x| >= thr
-    for (int i = tid; i < H0_BINS; i += TK_THREADS) hist[i] = 0;
     const float* row = a.g + (long long)w * a.ld;
     const long long t_begin = (long long)seg * a.tps;
     const long long t_end = t_begin + a.tps < a.ntiles ? t_begin + a.tps : a.ntiles;
     const int ntl = (int)(t_end - t_begin);
-    uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
-    float* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     unsigned long long policy = 0;
     auto issue = [&](int i) {  // tile t_begin + i -> stage i % MN_STAGES (full tiles only)
         const long long base = (t_begin + i) * MN_TILE;
@@ -1173,6 +1169,16 @@ k_main_tma(MainArgs<float> a) {
         fence_mbar_init();
         for (int i = 0; i < MN_STAGES && i < ntl; ++i) issue(i);
     }
+    for (int i = tid; i < H0_BINS; i += TK_THREADS) hist[i] = 0;
+    pdl_wait();
+    SG_STAMP(6);
+    SelState<K>* stp = a.sel + w;  // pass 0 only (the fallback pass is k_main)
+    const K est = stp->est;
+    const int shift0 = stp->shift0;
+    const bool take_all = est == 0;
+    const float thr = take_all ? 0.f : __uint_as_float(est - 1u);  // key >= est <=> |x| >= thr
+    uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
+    float* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     __syncthreads();
     double ss = 0.0, ss1 = 0.0;
     K mx = 0;
@@ -1307,6 +1313,7 @@ template <typename T>
 __global__ void __launch_bounds__(TK_THREADS, 4)
 k_main(MainArgs<T> a) {
     pdl_enter();
+    SG_STAMP(2);
     using KO = KeyOf<T>;
     using K = typename KO::K;
     using VT = Vec16<T>;
@@ -1475,6 +1482,7 @@ template <typename T>
 __global__ void __launch_bounds__(TK_THREADS, CW_PER_SM)
 k_collect(CollectArgs<T> a) {
     pdl_enter();
+    SG_STAMP(3);
     using KO = KeyOf<T>;
     using K = typename KO::K;
     __shared__ unsigned s_gt[TK_NW];
@@ -1720,6 +1728,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024)
 k_resolve(CollectArgs<T> a, ResolveArgs<T> r) {
     pdl_enter();
+    SG_STAMP(4);
     using K = typename KeyOf<T>::K;
     constexpr int RES = TopkTraits<T>::RES;
     constexpr int NT = 1024;
@@ -2187,6 +2196,7 @@ template <typename T>
 __global__ void __launch_bounds__(TK_THREADS, CW_PER_SM)
 k_write(WriteArgs<T> a) {
     pdl_enter();
+    SG_STAMP(5);
     write_body<T>(a);
     __shared__ int s_lastw;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2546,6 +2556,8 @@ inline int fused_segments(int k) {
 }  // namespace sg
 
 using namespace sg;
+
+SG_STAMPS_EXPORT(sg_diag_stamps_topk)
 
 extern "C" {
 
