@@ -305,10 +305,14 @@ inline void launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sm
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_on() ? 2 : 1;
-    if (cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) != cudaSuccess && cfg.numAttrs == 2) {
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess && cfg.numAttrs == 2) {
         cudaGetLastError();
+        if (getenv("SG_COOP_REPORT")) fprintf(stderr, "[scadles_b200] cooperative+PDL launch refused: %s\n", cudaGetErrorString(e));
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    } else if (getenv("SG_COOP_REPORT")) {
+        fprintf(stderr, "[scadles_b200] cooperative launch with %d attribute(s): %s\n", cfg.numAttrs, cudaGetErrorString(e));
     }
 }
 
@@ -358,6 +362,15 @@ struct StampScope {
     }
 };
 #define SG_STAMP(id) ::sg::StampScope sg_stamp_scope_##id(id)
+// first and last CTA (thread 0) to reach this point
+#define SG_MARK(id)                                               \
+    do {                                                          \
+        if (threadIdx.x == 0) {                                   \
+            const unsigned long long t_ = ::sg::gtimer();         \
+            atomicMin(&::sg::g_stamp[2 * (id)], t_);              \
+            atomicMax(&::sg::g_stamp[2 * (id) + 1], t_);          \
+        }                                                         \
+    } while (0)
 #define SG_STAMPS_EXPORT(name)                                                             \
     extern "C" int name(unsigned long long* out) {                                        \
         if (cudaMemcpyFromSymbol(out, ::sg::g_stamp, sizeof(::sg::g_stamp)) != cudaSuccess) \
@@ -371,6 +384,7 @@ struct StampScope {
     }
 #else
 #define SG_STAMP(id) do { } while (0)
+#define SG_MARK(id) do { } while (0)
 #define SG_STAMPS_EXPORT(name)
 #endif
 

@@ -200,6 +200,18 @@ template <typename T> TopkPlan make_plan(int k, long long dim, long long m, int 
     return p;
 }
 
+// A block's copy of PER * NT global words into shared memory with all PER loads of a thread in
+// flight before the first store: a last-CTA tail reading a histogram one round trip per
+// iteration cost ~0.7 us per iteration.
+template <int PER, int NT, typename U>
+SG_DEV void ld_cg_rows(U* dst, const U* src, int tid) {
+    U v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) v[u] = __ldcg(src + tid + u * NT);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) dst[tid + u * NT] = v[u];
+}
+
 // --------------------------------------------------------------------------------------
 // Radix-select helpers.
 // --------------------------------------------------------------------------------------
@@ -697,6 +709,7 @@ k_sample_est_f32(SampleEstArgs a) {
         for (long long i = cta * SE_THREADS + tid; i < a.zero_vec; i += ncta * SE_THREADS) a.zero[i] = make_uint4(0, 0, 0, 0);
     }
     __syncthreads();
+    SG_MARK(8);
     const float* row = a.g + (long long)w * a.ld;
     K mn = KO::KMAX, mx = 0;
     int nk = 0;
@@ -769,6 +782,7 @@ k_sample_est_f32(SampleEstArgs a) {
         s_mx[warp] = mx;
     }
     __syncthreads();
+    SG_MARK(9);
     // publish: the non-zero level-1 bins, the key range; then the exclusive bucket offsets
     constexpr int PB = SEL_BINS / SE_THREADS;  // 8 bins per thread
     unsigned hv[PB], hs = 0;
@@ -817,12 +831,14 @@ k_sample_est_f32(SampleEstArgs a) {
     // the worker's last CTA estimates
     __threadfence();
     __syncthreads();
+    SG_MARK(10);
     if (tid == 0) s_last = atomicAdd(a.doneg + w, 1u) == (unsigned)G - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (int i = tid; i < SEL_BINS; i += SE_THREADS) h1[i] = __ldcg(h1w + i);
+    ld_cg_rows<SEL_BINS / SE_THREADS, SE_THREADS>(h1, h1w, tid);
     __syncthreads();
+    SG_MARK(11);
     K est = 0;
     int b1 = -1;
     unsigned long long a1 = 0;
@@ -868,6 +884,7 @@ k_sample_est_f32(SampleEstArgs a) {
         }
         __syncthreads();
         const int total = s_pre[G];
+        SG_MARK(12);
         const K* kw = a.bkeys + (long long)w * TopkTraits<float>::SAMPLE;
         for (int i = tid; i < total; i += SE_THREADS) {
             int l = 0, h = G;  // the bucket c with s_pre[c] <= i < s_pre[c + 1]
@@ -880,6 +897,7 @@ k_sample_est_f32(SampleEstArgs a) {
             atomicAdd(&h1[(key >> 9) & (SEL_BINS - 1)], 1u);
         }
         __syncthreads();
+        SG_MARK(13);
         int b2;
         unsigned long long a2;
         block_find_bin_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)a.r_est - a1, b2, a2);
@@ -1081,7 +1099,7 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (int i = tid; i < H0_BINS; i += blockDim.x) hist[i] = __ldcg(gh + i);
+    ld_cg_rows<H0_BINS / TK_THREADS, TK_THREADS>(hist, gh, tid);
     __syncthreads();
     const unsigned long long C = __ldcg(a.count + (long long)a.pass * a.k + w);
     if (C < (unsigned long long)a.m) {
@@ -2189,6 +2207,23 @@ SG_DEV void write_body(const WriteArgs<T>& a) {
     write_tail<T>(a, ss);
 }
 
+// Lane `lane`'s partial of a fixed-order norm reduction: p[lane] + p[lane + 32] + ... in
+// ascending order (the order the gate's bits depend on), with the loads of OS_U consecutive
+// terms in flight at once -- the last CTA's serial tail was one L2 round trip per term.
+constexpr int OS_U = 16;
+SG_DEV double lane_ordered_sum(const double* p, int n, int lane) {
+    double s = 0.0;
+    for (int i0 = lane; i0 < n; i0 += 32 * OS_U) {
+        double v[OS_U];
+#pragma unroll
+        for (int u = 0; u < OS_U; ++u) v[u] = i0 + 32 * u < n ? __ldcg(p + i0 + 32 * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < OS_U; ++u)
+            if (i0 + 32 * u < n) s = dadd(s, v[u]);
+    }
+    return s;
+}
+
 // k_write: the ordered compaction of every sub-range, then -- in the last CTA to finish --
 // the fixed-order norm reductions and the gate (comm.py:129-160), formerly a separate
 // one-CTA launch.
@@ -2201,6 +2236,7 @@ k_write(WriteArgs<T> a) {
     __shared__ int s_lastw;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __syncthreads();
+    SG_MARK(14);
     if (tid == 0) {
         __threadfence();
         s_lastw = atomicAdd(a.done, 1u) == gridDim.x * gridDim.y - 1;
@@ -2208,10 +2244,10 @@ k_write(WriteArgs<T> a) {
     __syncthreads();
     if (!s_lastw) return;
     __threadfence();
+    SG_MARK(15);
     for (int ww = warp; ww < a.k; ww += TK_NW) {
-        double sf = 0.0, sk = 0.0;
-        for (int i = lane; i < a.nseg; i += 32) sf = dadd(sf, __ldcg(a.pmain + (long long)ww * a.nseg + i));
-        for (int i = lane; i < a.nsub; i += 32) sk = dadd(sk, __ldcg(a.pwrite + (long long)ww * a.nsub + i));
+        double sf = lane_ordered_sum(a.pmain + (long long)ww * a.nseg, a.nseg, lane);
+        double sk = lane_ordered_sum(a.pwrite + (long long)ww * a.nsub, a.nsub, lane);
         sf = warp_sum(sf);
         sk = warp_sum(sk);
         if (lane == 0) {

@@ -26,7 +26,8 @@ import bench  # noqa: E402
 from paper_2301_08897_b200 import _capi, build  # noqa: E402
 
 TOPK = {0: "sample_est", 1: "main_tma(resident)", 6: "main_tma(after wait)", 2: "main_fb", 3: "collect", 4: "resolve",
-        5: "write"}
+        5: "write", 8: "se:zeroed", 9: "se:sampled", 10: "se:bucketed", 11: "se:last:h1", 12: "se:last:b1 bounds",
+        13: "se:last:level2", 14: "write:body done", 15: "write:last CTA"}
 AGG = {0: "merge_ws", 1: "merge", 2: "merge_own"}
 
 
