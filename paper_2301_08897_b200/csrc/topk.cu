@@ -1895,116 +1895,122 @@ SG_DEV void write_tail(const WriteArgs<T>& a, double ss) {
 }
 
 // Fast-mode write (T and the tie cut are final).  The CTA streams its sub-range in chunks of
-// WF_SPAN entries, thread t owning WF_EPT consecutive entries, with the next chunk's loads in
-// flight while the current one is processed: one block scan of the kept counts gives every
-// kept entry its output slot; the kept run is compacted in shared memory and stored
-// coalesced.  Merge offsets: toff[t] = kept entries with index < 4096 t.  This CTA owns the
-// tile boundaries after the candidate before its range up to its last candidate (the whole
-// segment tail for the segment's last part); a boundary between two consecutive kept entries
-// gets the second one's slot, so the store loop sets them, one kept entry per thread.
-constexpr int WF_EPT = 4;
-constexpr int WF_SPAN = TK_THREADS * WF_EPT;  // 1024 entries per chunk
+// WF_SPAN entries: round r of a chunk is entries [base + 256 r, base + 256 (r + 1)), one per
+// thread, so every warp load and every warp store of a round covers consecutive entries
+// (coalesced, from registers -- no shared-memory staging).  The kept entries' output slots come
+// from one barrier per chunk: each (round, warp) publishes its kept count (a ballot) and the tile
+// of its last kept entry, and after the barrier a 32-lane scan over the (round, warp) slots gives
+// every kept entry its slot.  Merge offsets: toff[t] = kept entries with index < 4096 t.  A kept
+// entry whose tile differs from the previous kept entry's (the previous lane of its ballot, else
+// the last (round, warp) slot holding one, else the previous chunk's) sets the offsets of the
+// tiles in between.  This CTA owns the boundaries after the candidate before its range up to
+// its last candidate (the whole segment tail for the segment's last part).  The next chunk's
+// loads are in flight while the current one is processed.
+constexpr int WF_R = 4;                      // rounds (entries per thread) per chunk
+constexpr int WF_SPAN = TK_THREADS * WF_R;   // 1024 entries per chunk
+static_assert(WF_R * TK_NW == 32, "one lane per (round, warp) slot");
 
 template <typename T>
 SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
-                         typename KeyOf<T>::K T_, unsigned cut, unsigned char* stage, int seg, int lo32, int n32,
-                         bool last_part) {
+                         typename KeyOf<T>::K T_, unsigned cut, int seg, int lo32, int n32, bool last_part) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
-    __shared__ unsigned s_wt[TK_NW];
-    __shared__ int s_ltile;  // tile of the last kept entry so far (initially of the candidate before the range)
+    __shared__ unsigned s_wt[2][32];  // (round, warp) kept counts, by chunk parity
+    __shared__ int s_wl[2][32];       // tile of the (round, warp)'s last kept entry, -1: none
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, sub = blockIdx.x;
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     uint32_t* oi = a.idx + (long long)w * a.m;
     T* ov = a.val + (long long)w * a.m;
-    T v[WF_EPT];
-    uint32_t ii[WF_EPT];
-    if (lo32 < n32) {
-        load16<T, WF_EPT>(cv, lo32 + tid * WF_EPT, n32, v);
-        load16_idx<WF_EPT>(ci, lo32 + tid * WF_EPT, n32, ii);
-    }
-    if (tid == 0) s_ltile = lo32 > 0 ? (int)(ci[lo32 - 1] >> MERGE_SHIFT) : (int)t0 - 1;
-    unsigned g32 = a.segbase[(long long)w * a.nsub + sub];
-    T* st_v = reinterpret_cast<T*>(stage);                        // [WF_SPAN]
-    uint32_t* st_i = reinterpret_cast<uint32_t*>(st_v + WF_SPAN);  // [WF_SPAN]
-    double ss = 0.0;
-    for (int base = lo32; base < n32; base += WF_SPAN) {
-        const int e0 = base + tid * WF_EPT;
-        T x[WF_EPT];
-        uint32_t xi[WF_EPT];
+    const unsigned lt_mask = lanemask_lt();
+    T v[WF_R];
+    uint32_t ii[WF_R];
 #pragma unroll
-        for (int u = 0; u < WF_EPT; ++u) {
-            x[u] = v[u];
-            xi[u] = ii[u];
+    for (int r = 0; r < WF_R; ++r) {
+        const int e = lo32 + r * TK_THREADS + tid;
+        v[r] = e < n32 ? cv[e] : (T)0;
+        ii[r] = e < n32 ? ci[e] : 0u;
+    }
+    // tile of the candidate before the range (uniform)
+    int ltile = lo32 > 0 ? (int)(ci[lo32 - 1] >> MERGE_SHIFT) : (int)t0 - 1;
+    unsigned g32 = a.segbase[(long long)w * a.nsub + sub];
+    double ss = 0.0;
+    int par = 0;
+    for (int base = lo32; base < n32; base += WF_SPAN, par ^= 1) {
+        T x[WF_R];
+        uint32_t xi[WF_R];
+#pragma unroll
+        for (int r = 0; r < WF_R; ++r) {
+            x[r] = v[r];
+            xi[r] = ii[r];
         }
         if (base + WF_SPAN < n32) {  // next chunk in flight
-            load16<T, WF_EPT>(cv, e0 + WF_SPAN, n32, v);
-            load16_idx<WF_EPT>(ci, e0 + WF_SPAN, n32, ii);
-        }
-        unsigned kf = 0;
 #pragma unroll
-        for (int u = 0; u < WF_EPT; ++u) {
-            const K key = KO::key(x[u]);
-            kf |= (e0 + u < n32 && (key > T_ || (key == T_ && xi[u] <= cut)) ? 1u : 0u) << u;
+            for (int r = 0; r < WF_R; ++r) {
+                const int e = base + WF_SPAN + r * TK_THREADS + tid;
+                v[r] = e < n32 ? cv[e] : (T)0;
+                ii[r] = e < n32 ? ci[e] : 0u;
+            }
         }
-        const unsigned cnt = __popc(kf);
-        unsigned incl = cnt;
+        unsigned ball[WF_R];
+#pragma unroll
+        for (int r = 0; r < WF_R; ++r) {
+            const int e = base + r * TK_THREADS + tid;
+            const K key = KO::key(x[r]);
+            ball[r] = __ballot_sync(FULL, e < n32 && (key > T_ || (key == T_ && xi[r] <= cut)));
+            const int hl = ball[r] ? 31 - __clz((int)ball[r]) : 0;
+            const int lt = __shfl_sync(FULL, (int)(xi[r] >> MERGE_SHIFT), hl);
+            if (lane == 0) {
+                s_wt[par][r * TK_NW + warp] = __popc(ball[r]);
+                s_wl[par][r * TK_NW + warp] = ball[r] ? lt : -1;
+            }
+        }
+        __syncthreads();
+        // lane i <-> slot i = (round i / TK_NW, warp i % TK_NW), in index order
+        const unsigned c = s_wt[par][lane];
+        unsigned incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned y = __shfl_up_sync(FULL, incl, o);
             if (lane >= o) incl += y;
         }
-        if (lane == 31) s_wt[warp] = incl;
-        __syncthreads();
-        unsigned wb = 0, tot = 0;
+        const unsigned excl = incl - c, tot = __shfl_sync(FULL, incl, 31);
+        const int wl = s_wl[par][lane];
+        const unsigned has = __ballot_sync(FULL, wl >= 0);
 #pragma unroll
-        for (int i = 0; i < TK_NW; ++i) {
-            const unsigned t = s_wt[i];
-            wb += i < warp ? t : 0u;
-            tot += t;
-        }
-        // compact into shared memory, then coalesced stores of the chunk's kept run
-        unsigned lp = wb + incl - cnt;
-        while (kf) {
-            const int u = __ffs(kf) - 1;
-            kf &= kf - 1;
-            st_i[lp] = xi[u];
-            st_v[lp] = x[u];
-            ++lp;
-        }
-        __syncthreads();
-        const int lt0 = s_ltile;
-        int lt_new = -2;
-        for (unsigned q = tid; q < tot; q += TK_THREADS) {
-            const uint32_t iq = st_i[q];
-            if (toff) {  // boundaries after the previous kept entry up to this one
-                const int tc = (int)(iq >> MERGE_SHIFT);
-                const int tp = q > 0 ? (int)(st_i[q - 1] >> MERGE_SHIFT) : lt0;
-                if (tc != tp) {  // rare: this entry is the first kept one of tile(s) (tp, tc]
+        for (int r = 0; r < WF_R; ++r) {
+            const int slot = r * TK_NW + warp;
+            const unsigned sbase = __shfl_sync(FULL, excl, slot);
+            const unsigned lower = ball[r] & lt_mask;
+            const int tile = (int)(xi[r] >> MERGE_SHIFT);
+            const int pl = __shfl_sync(FULL, tile, lower ? 31 - __clz((int)lower) : 0);
+            const unsigned hb = has & ((1u << slot) - 1u);
+            const int ps = __shfl_sync(FULL, wl, hb ? 31 - __clz((int)hb) : 0);
+            if ((ball[r] >> lane) & 1u) {
+                const unsigned pos = g32 + sbase + __popc(lower);
+                if (toff) {
+                    const int tp = lower ? pl : (hb ? ps : ltile);
+                    if (tile != tp) {  // rare: this entry is the first kept one of tile(s) (tp, tile]
 #pragma unroll 1
-                    for (int t = tp + 1; t <= tc; ++t) toff[t] = (int)(g32 + q);
+                        for (int t = tp + 1; t <= tile; ++t) toff[t] = (int)pos;
+                    }
                 }
-                if (q + 1 == tot) lt_new = tc;
-            }
-            if (g32 + q < (unsigned)a.m) {
-                const T y = st_v[q];
-                oi[g32 + q] = iq;
-                ov[g32 + q] = y;
-                ss = fma((double)y, (double)y, ss);
+                if (pos < (unsigned)a.m) {
+                    oi[pos] = xi[r];
+                    ov[pos] = x[r];
+                    ss = fma((double)x[r], (double)x[r], ss);
+                }
             }
         }
         g32 += tot;
-        __syncthreads();  // s_wt, s_ltile and the staging are reused
-        if (lt_new != -2) s_ltile = lt_new;
+        if (has) ltile = __shfl_sync(FULL, wl, 31 - __clz((int)has));
     }
     if (toff) {
         // boundaries after the last kept entry: up to this range's last candidate, or to the
         // segment end for its last part
-        __syncthreads();
         const int tend = last_part ? (int)(t0 + nt) - 1 : (n32 > 0 ? (int)(ci[n32 - 1] >> MERGE_SHIFT) : (int)t0 - 1);
-        for (int t = s_ltile + 1 + tid; t <= tend; t += TK_THREADS) toff[t] = (int)g32;
+        for (int t = ltile + 1 + tid; t <= tend; t += TK_THREADS) toff[t] = (int)g32;
         if (last_part && tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }
     return ss;
@@ -2044,9 +2050,7 @@ SG_DEV void write_body(const WriteArgs<T>& a) {
     int* toff = (OFFS && a.tile_off) ? a.tile_off + (long long)w * (a.ntiles + 1) : nullptr;
 
     if (!slow) {
-        write_tail<T>(a, write_fast<T>(a, nt, t0, toff, T_, cut,
-                                       smem_raw + align_up(sizeof(unsigned) * (size_t)a.tps, 16), seg, (int)i_lo,
-                                       (int)n, last_part));
+        write_tail<T>(a, write_fast<T>(a, nt, t0, toff, T_, cut, seg, (int)i_lo, (int)n, last_part));
         return;
     }
     if (toff) {
@@ -2550,7 +2554,7 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.states = states;
     wa.decision = decision;
     wa.rho = rho;
-    const size_t wr_smem = align_up(sizeof(unsigned) * (size_t)p.tps, 16) + (size_t)WF_SPAN * (sizeof(T) + sizeof(uint32_t));
+    const size_t wr_smem = align_up(sizeof(unsigned) * (size_t)p.tps, 16);  // slow mode: the segment's tile starts
     smem_attr((const void*)k_write<T>, (int)wr_smem);
     launch_pdl(k_write<T>, dim3(subgrid), dim3(TK_THREADS), wr_smem, stream, wa);
     debug_sync("k_write", stream);
