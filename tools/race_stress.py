@@ -1,5 +1,5 @@
-"""Race / determinism stress (compute-sanitizer is closed on this GPU pool, so this is the
-substitute the round uses): every kernel family with shared-memory hand-offs, mbarrier rings,
+"""Race / determinism stress (also the small case run under compute-sanitizer, one tool per
+gpurun call: tools/gpu/call63.sh): every kernel family with shared-memory hand-offs, mbarrier rings,
 cooperative grid barriers, decoupled look-back or device-side flags is re-run many times on
 fixed inputs, with shapes chosen to exercise its concurrent paths, and every output byte is
 compared across repetitions (a race shows up as a run-to-run difference) and once against
@@ -45,13 +45,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--dim", type=int, default=0, help="override D (small for compute-sanitizer runs)")
     args = ap.parse_args()
     build.build()
     dev = torch.device("cuda", 0)
     reps = 8 if args.quick else args.reps
     report = {"reps": reps, "cases": []}
     ok_all = True
-    D = 1_000_003 if args.quick else 4_000_037
+    D = args.dim if args.dim > 0 else (1_000_003 if args.quick else 4_000_037)
     cases = [("heavy", 8, 0.01, False), ("ties", 2, 0.3, False), ("hot", 8, 0.1, False), ("heavy", 8, 0.01, True),
              ("ties", 2, 0.3, True), ("hot", 4, 0.1, True), ("heavy", 1, 0.001, True)]
     rates = [31, 30, 1, 30, 42, 66, 22, 14]
