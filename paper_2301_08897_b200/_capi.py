@@ -8,12 +8,15 @@ raise ``ValueError`` (as ``streamsgd.comm`` does), everything else ``RuntimeErro
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_uint8, c_uint32, c_void_p
 from pathlib import Path
 
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libscadles_b200.so"
+if os.environ.get("SG_LIB_PATH"):  # diagnostic builds only (tools/checked_run.py, tools/stamps.py)
+    LIB_PATH = Path(os.environ["SG_LIB_PATH"])
 
 SG_OK = 0
 SG_ERR_INVALID = -1

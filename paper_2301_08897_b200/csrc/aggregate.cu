@@ -924,6 +924,7 @@ k_merge_ws(const AggArgs<float, TO> a) {
                     const uint32_t* ib = s_ib[j];
                     const float* vb = s_vb[j];
                     for (int e = lo + lane; e < hi; e += 32) {
+                        SG_CHECK(e - cc0 >= 0 && e - cc0 < MW_ECAP);
                         cp_async4(sidx + slot * MW_ECAP + (e - cc0), ib + g0 + e);
                         cp_async4(sval + slot * MW_ECAP + (e - cc0), vb + g0 + e);
                         swk[slot * MW_ECAP + (e - cc0)] = (uint8_t)j;
@@ -983,6 +984,7 @@ k_merge_ws(const AggArgs<float, TO> a) {
                     const double wj = a.w[j];
                     for (int n = lo - c0 + pt; n < hi - c0; n += MW_PROD) {
                         const unsigned q = si[n] - tb;
+                        SG_CHECK(q < (unsigned)AG_TILE);
                         const double r = mb[q] ? ab[q] : 0.0;
                         ab[q] = dadd(r, dmul(wj, (double)sv[n]));
                         mb[q] = 1;
@@ -994,6 +996,7 @@ k_merge_ws(const AggArgs<float, TO> a) {
             // (1) push every entry onto its position's list
             for (int n = pt; n < ne; n += MW_PROD) {
                 const unsigned q = si[n] - tb;
+                SG_CHECK(q < (unsigned)AG_TILE);
                 const float v = sv[n];
                 const unsigned j = sw8[n];
                 const unsigned old = atomicExch(head + q, (unsigned)n);
@@ -1293,6 +1296,7 @@ k_merge_own(const AggArgs<float, TO> a) {
                 const double wj = a.w[j];
                 for (int e = lo + tid; e < hi; e += MO_THREADS) {
                     const unsigned q = si[e - c0] - (uint32_t)tb;
+                    SG_CHECK(q < (unsigned)AG_TILE && e - c0 < MO_ECAP);
                     double* sa = &sacc[q % MO_PER][q / MO_PER];
                     *sa = dadd(*sa, dmul(wj, (double)sv[e - c0]));
                 }

@@ -388,6 +388,22 @@ struct StampScope {
 #define SG_STAMPS_EXPORT(name)
 #endif
 
+// Diagnostic build only (-DSG_CHECKS): device-side bounds checks on the hot path's computed
+// addresses (candidate slots, output slots, merge offsets, staged merge entries, sampler
+// rows); a failed check prints the site and traps.  compute-sanitizer is closed on this GPU
+// pool, so tools/checked_run.py runs the GPU tests and the race stress on this build instead.
+#ifdef SG_CHECKS
+#define SG_CHECK(cond)                                                                          \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("[scadles_b200] check failed %s:%d: %s\n", __FILE__, __LINE__, #cond);      \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define SG_CHECK(cond) do { } while (0)
+#endif
+
 inline int num_sms() {
     int dev = 0, n = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);

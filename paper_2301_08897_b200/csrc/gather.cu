@@ -18,6 +18,7 @@ __global__ void k_resolve_rows(const long long* __restrict__ head, const long lo
     const int d = blockIdx.y;
     const long long p0 = pool_ptr[d], plen = pool_ptr[d + 1] - p0;
     const long long h = head[d], n = b[d], o = out_ptr[d];
+    SG_CHECK(n == 0 || plen > 0);
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         out[o + i] = pool_rows[p0 + (h + i) % plen];
 }

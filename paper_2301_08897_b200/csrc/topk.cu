@@ -766,6 +766,7 @@ k_sample_est_f32(SampleEstArgs a) {
 #pragma unroll
                     for (int j = 0; j < PL; ++j) {
                         const K key = KO::key(v[u][j]);
+                        SG_CHECK(cl * SE_CHUNK + j * 32 + lane < per);
                         keys[cl * SE_CHUNK + j * 32 + lane] = key;
                         atomicAdd(&h1[key >> 20], 1u);
                         mn = key < mn ? key : mn;
@@ -1216,6 +1217,7 @@ k_main_tma(MainArgs<float> a) {
             const K key = KeyOf<float>::key(val);
             mx = key > mx ? key : mx;
             atomicAdd(&hist[digit<K>(key, est, shift0, H0_BINS)], 1u);
+SG_CHECK(pos < (unsigned)a.segcap);
             ci[pos] = (uint32_t)(base + off);
             cv[pos] = val;
             ++pos;
@@ -1256,6 +1258,7 @@ k_main_tma(MainArgs<float> a) {
                     const float val = src[off];
                     const K key = KeyOf<float>::key(val);
                     mx = key > mx ? key : mx;
+SG_CHECK(run + j < (unsigned)a.segcap);
                     ci[run + j] = (uint32_t)(base + off);
                     cv[run + j] = val;
                     atomicAdd(&hist[digit<K>(key, est, shift0, H0_BINS)], 1u);
@@ -1426,6 +1429,7 @@ k_main(MainArgs<T> a) {
 #pragma unroll
             for (int c = 0; c < V; ++c) {
                 if ((cm[r] >> c) & 1u) {
+SG_CHECK(pos < (unsigned long long)a.segcap);
                     ci[pos] = (uint32_t)(base + (long long)(r * TK_THREADS + tid) * V + c);
                     cv[pos] = v[r][c];
                     ++pos;
@@ -1555,6 +1559,7 @@ k_collect(CollectArgs<T> a) {
                 const int u = __ffs(bm) - 1;
                 bm &= bm - 1;
                 if (q >= (unsigned long long)a.cap) break;  // oversized: counted only (slow mode)
+SG_CHECK(e0 + u < hi32 && q < (unsigned long long)a.cap);
                 bk[q] = KO::key(x[u]);
                 bi[q] = ci[e0 + u];
                 bp[q] = (uint32_t)(e0 + u);
@@ -1993,10 +1998,12 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
                     const int tp = lower ? pl : (hb ? ps : ltile);
                     if (tile != tp) {  // rare: this entry is the first kept one of tile(s) (tp, tile]
 #pragma unroll 1
+SG_CHECK(tp >= -1 && tile < (int)a.ntiles);
                         for (int t = tp + 1; t <= tile; ++t) toff[t] = (int)pos;
                     }
                 }
                 if (pos < (unsigned)a.m) {
+SG_CHECK(base + r * TK_THREADS + tid < n32);
                     oi[pos] = xi[r];
                     ov[pos] = x[r];
                     ss = fma((double)x[r], (double)x[r], ss);
@@ -2010,6 +2017,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
         // boundaries after the last kept entry: up to this range's last candidate, or to the
         // segment end for its last part
         const int tend = last_part ? (int)(t0 + nt) - 1 : (n32 > 0 ? (int)(ci[n32 - 1] >> MERGE_SHIFT) : (int)t0 - 1);
+        SG_CHECK(tend < (int)a.ntiles && g32 <= (unsigned)a.m + (unsigned)WF_SPAN);
         for (int t = ltile + 1 + tid; t <= tend; t += TK_THREADS) toff[t] = (int)g32;
         if (last_part && tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }

@@ -110,6 +110,18 @@ def topk_workspace_bytes(dtype: torch.dtype, k: int, dim: int, m: int, fused: bo
     return int(fn(k, dim, m))
 
 
+# Launch-chain workspace budget: the chain keeps a candidate slot per element (8 B x k x D, e.g.
+# 69 GB at D = 1e9, k = 8); above this the persistent variant (a ~2m-entry candidate pool,
+# identical results) is taken instead.  SG_TOPK_WS_BUDGET overrides (bytes).
+TOPK_WS_BUDGET = int(os.environ.get("SG_TOPK_WS_BUDGET", str(16 << 30)))
+
+
+def topk_use_fused(dtype: torch.dtype, k: int, dim: int, m: int) -> bool:
+    """The Top-k variant `topk_gate(fused=None)` takes: the launch chain (faster at every k
+    and cr measured) unless its workspace exceeds TOPK_WS_BUDGET."""
+    return dtype == torch.float32 and topk_workspace_bytes(dtype, k, dim, m) > TOPK_WS_BUDGET
+
+
 def _topk_ws(dtype, k, dim, m, device, slot, fused):
     """float32 workspaces carry zero-state between calls: zero-filled when created and
     whenever the plan (k, dim, m) changes (sg_topk_workspace_zero_bytes_*)."""
@@ -134,13 +146,14 @@ def topk_gate(
     out: tuple | None = None,
     tile_off: torch.Tensor | None = None,
     workspace_slot: int = 0,
-    fused: bool = False,
+    fused: bool | None = None,
 ):
     """Batched Top-k + norms (+ gate) over the rows of ``g`` ([k, ld] or [D]).
 
     ``workspace_slot`` selects a separate scratch buffer for calls issued concurrently on
     different streams.  ``fused`` (float32) takes the persistent one-kernel variant
-    (sg_topk_gate_fused_f32) instead of the launch chain; the results are identical.
+    (sg_topk_gate_fused_f32) instead of the launch chain; the results are identical.  None
+    (default): the chain unless its workspace exceeds ``TOPK_WS_BUDGET`` (topk_use_fused).
 
     Returns (idx int32 [k, m] (uint32 bits), val [k, m], norms2 f64 [k, 2], decision u8 [k],
     rho f64 [k]); decision/rho are None without ``states``.
@@ -165,6 +178,8 @@ def topk_gate(
         idx, val, norms2, decision, rho = out
     if states is not None and states.numel() != k * _GATE_BYTES:
         raise ValueError("one gate state per worker required")
+    if fused is None:
+        fused = topk_use_fused(g.dtype, k, D, m)
     fused = bool(fused) and g.dtype == torch.float32
     if topk_workspace_bytes(g.dtype, k, D, m, fused) == 0:
         raise ValueError("invalid top-k shape")

@@ -161,3 +161,26 @@ def test_fused_batched_rows_padding_and_state(cuda):
             assert np.allclose(a["ewma_full"], b["ewma_full"], rtol=1e-12, equal_nan=True)
         else:
             assert np.array_equal(a, b)
+
+
+def test_auto_variant_takes_the_pool_above_the_workspace_budget(cuda, monkeypatch):
+    """topk_gate(fused=None) takes the launch chain within TOPK_WS_BUDGET and the ~2m-pool
+    variant above it (e.g. D = 1e9 at k = 8: 69 GB of chain workspace); same indices and values."""
+    from paper_2301_08897_b200 import kernels
+
+    D, k = 1_000_003, 2
+    m = comm_ref.topk_count(D, 0.01)
+    rng = np.random.default_rng(5)
+    g = torch.from_numpy((np.sign(rng.standard_normal((k, D))) * np.exp(1.5 * rng.standard_normal((k, D))))
+                         .astype(np.float32)).to(cuda)
+    assert not kernels.topk_use_fused(torch.float32, k, D, m)
+    ref = kernels.topk_gate(g, m)
+    monkeypatch.setattr(kernels, "TOPK_WS_BUDGET", 0)
+    assert kernels.topk_use_fused(torch.float32, k, D, m)
+    assert not kernels.topk_use_fused(torch.float64, k, D, m)  # float64 has only the chain
+    got = kernels.topk_gate(g, m)
+    assert torch.equal(ref[0], got[0]) and torch.equal(ref[1], got[1])
+    # the norms are fixed-order sums in both variants, over different partitions
+    assert torch.allclose(ref[2], got[2], rtol=1e-12, atol=0)
+    want = comm_ref.topk_indices_threshold(g[1].cpu().numpy().astype(np.float64), m)
+    assert np.array_equal(got[0][1].cpu().numpy().astype(np.int64), want)

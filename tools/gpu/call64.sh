@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/c64; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1
+timeout 1500 python tools/checked_run.py python -m pytest tests -m gpu -x -q -rs -p no:cacheprovider > $O/pytest_checked.log 2>&1; echo "rc=$?" >> $O/pytest_checked.log
+timeout 900 python tools/checked_run.py python tools/race_stress.py --reps 3 > $O/race_checked.json 2> $O/race_checked.err; echo "rc=$?" >> $O/race_checked.err
+timeout 600 python -m pytest tests/test_gpu_topk_fused.py -m gpu -x -q > $O/pytest_fused.log 2>&1; echo "rc=$?" >> $O/pytest_fused.log
+timeout 900 python tools/train_resnet152.py --steps 5 --stats > $O/train.json 2> $O/train.err

@@ -42,7 +42,7 @@ def main():
     out = ROOT / "gpurun_out" / "diag" / "libscadles_b200_stamps.so"
     out.parent.mkdir(parents=True, exist_ok=True)
     build.build_variant(out, ["-DSG_STAMPS"])
-    _capi.LIB_PATH = out
+    _capi.LIB_PATH = out  # (or SG_LIB_PATH)
     lib = _capi.load()
     from paper_2301_08897_b200 import exchange
 
