@@ -233,6 +233,13 @@ int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, int rank, con
                               int64_t dim, float* out, float* params, float* momentum_buf, double lr, double momentum,
                               double weight_decay, int first_step, void* stream);
 
+/* NVLink SHARP payload broadcast: `words` 32-bit words (a multiple of 4, 16-byte aligned) of
+ * this rank's packed Top-k output [decisions | idx | val | merge offsets] copied to the multicast
+ * address mc_dst of its slot in every rank's peer-mapped gather buffer (multimem.st: one NVLink
+ * write per byte, replicated in the switch), so after a barrier every rank merges all W payloads
+ * from its own HBM.  Replaces the sparse allgather of engine.py:255-265 / SURVEY §8(e). */
+int sg_multicast_copy_u32(const void* src, void* mc_dst, int64_t words, void* stream);
+
 /* dst[i * each + b] = src[i][b] for i < nsrc (<= 64 device pointers in a HOST array; peers'
  * memory allowed): gathers the ranks' decision bytes before the host reads them. */
 int sg_gather_bytes(int nsrc, const uint8_t* const* src, int64_t each, uint8_t* dst, void* stream);

@@ -1950,6 +1950,31 @@ k_nvls_reduce_bcast(const float* mc_src, float* mc_dst, long long lo, long long 
     __threadfence_system();  // the multicast stores are visible system-wide before the barrier
 }
 
+// Multicast copy of n4 16-byte vectors (the payload broadcast, sg_multicast_copy_u32): local
+// HBM reads, multimem.st to every rank's copy through the switch, U vectors in flight per thread.
+__global__ void __launch_bounds__(256)
+k_mc_copy(const uint4* __restrict__ src, float* mc_dst, long long n4) {
+    pdl_enter();
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    constexpr int U = 4;
+    for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = i0 + u * stride;
+            if (i < n4) v[u] = ld_stream(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = i0 + u * stride;
+            if (i < n4)  // a plain store: the words' bits (NaN payloads, indices) pass unchanged (tested)
+                mm_st_v4(mc_dst + 4 * i, make_float4(__uint_as_float(v[u].x), __uint_as_float(v[u].y),
+                                                     __uint_as_float(v[u].z), __uint_as_float(v[u].w)));
+        }
+    }
+    __threadfence_system();  // the multicast stores are visible system-wide before the barrier
+}
+
 inline long long peer_blocks(long long n4) {
     long long blocks = (n4 + 255) / 256;
     const long long cap = (long long)num_sms() * 8;
@@ -2187,6 +2212,16 @@ int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, int rank, con
                r, nranks, rank, (long long)peer_slice_len(dim, nranks), guard_n > 0 ? guard : nullptr, guard_n,
                (long long)dim,
                out, params, momentum_buf, lr, momentum, weight_decay, first_step);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+int sg_multicast_copy_u32(const void* src, void* mc_dst, int64_t words, void* stream) {
+    if (!src || !mc_dst || words < 4 || words % 4 || reinterpret_cast<size_t>(src) % 16 ||
+        reinterpret_cast<size_t>(mc_dst) % 16)
+        return SG_ERR_INVALID;
+    const long long n4 = words / 4;
+    launch_pdl(k_mc_copy, dim3((unsigned)peer_blocks(n4 / 4 + 1)), dim3(256), 0, (cudaStream_t)stream,
+               reinterpret_cast<const uint4*>(src), reinterpret_cast<float*>(mc_dst), n4);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

@@ -177,8 +177,19 @@ class GradientExchange:
             self.row_ptr_local = torch.arange(0, (k + 1) * m, m, dtype=torch.int64, **z)
             if self.packed and self._symm is not None:
                 P, words, dw = self.world, self.pack_words, self.pack_dw
-                off0 = self.pack.data_ptr() - self._symm.buffer_ptrs[self.rank]
-                bases = [self._symm.buffer_ptrs[r] + off0 for r in range(P)]  # rank r's pack
+                self._mc_dst = None
+                if self._gath is not None:
+                    # payload broadcast: rank r's pack lands in slot r of every rank's gather
+                    # buffer, so the merge reads all W payloads from local HBM
+                    g0 = self._gath.data_ptr()
+                    bases = [g0 + 4 * r * words for r in range(P)]
+                    goff = g0 - self._gath_h.buffer_ptrs[self.rank]
+                    self._mc_dst = int(self._gath_h.multicast_ptr) + goff + 4 * self.rank * words
+                    merge_local = (0, self.W)
+                else:
+                    off0 = self.pack.data_ptr() - self._symm.buffer_ptrs[self.rank]
+                    bases = [self._symm.buffer_ptrs[r] + off0 for r in range(P)]  # rank r's pack
+                    merge_local = (self.lo, self.k)
                 self._dec_ptrs = bases
                 idx_p = [b + 4 * (dw + j * m) for b in bases for j in range(k)]
                 val_p = [b + 4 * (dw + k * m + j * m) for b in bases for j in range(k)]
@@ -186,7 +197,7 @@ class GradientExchange:
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
                 self._peer_merge = kernels.PeerMergeLauncher(dim, self.dec_all, idx_p, val_p, off_p, self.params,
                                                              self.momentum_buf, momentum, weight_decay,
-                                                             local_lo=self.lo, local_n=self.k,
+                                                             local_lo=merge_local[0], local_n=merge_local[1],
                                                              sparse_merge=self.sparse_merge)
                 # mixed decisions: each rank's partial in a peer-mapped buffer, reduced in rank order
                 self._side = None
@@ -320,7 +331,7 @@ class GradientExchange:
         takes the NCCL path -- a rank that silently fell back alone would hang the others in
         the peer barriers)."""
         ok = 1
-        symm = pack = None
+        symm = pack = gath_h = None
         try:
             import torch.distributed._symmetric_memory as symm_mem
 
@@ -329,6 +340,10 @@ class GradientExchange:
                 pack = symm_mem.empty(words, dtype=torch.int32, device=self.device)
                 pack.zero_()
                 symm = symm_mem.rendezvous(pack, grp.group_name)
+                # the gather buffer of the payload broadcast: slot r <- rank r's pack (multicast)
+                gath = symm_mem.empty(self.world * words, dtype=torch.int32, device=self.device)
+                gath.zero_()
+                gath_h = symm_mem.rendezvous(gath, grp.group_name)
             part = symm_mem.empty(self.ld, dtype=torch.float32, device=self.device)
             part.zero_()
             part_h = symm_mem.rendezvous(part, grp.group_name)
@@ -344,6 +359,14 @@ class GradientExchange:
         flag = torch.tensor([ok], dtype=torch.int32, device=self.device)
         if self.group is not None or dist.is_initialized():
             dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        self._gath = self._gath_h = None
+        if int(flag.item()) == 1 and words is not None and os.environ.get("SG_PAYLOAD_MC", "1") != "0":
+            # NVLS multicast on every rank (collective): the payloads are broadcast through the
+            # switch and merged from local memory; otherwise the merge reads them over NVLink
+            mc = torch.tensor([1 if int(gath_h.multicast_ptr) != 0 else 0], dtype=torch.int32, device=self.device)
+            dist.all_reduce(mc, op=dist.ReduceOp.MIN, group=self.group)
+            if int(mc.item()) == 1:
+                self._gath, self._gath_h = gath, gath_h
         if int(flag.item()) == 1:
             self._symm, self.pack = symm, pack
             self._partial_buf, self._partial_h = part, part_h
@@ -447,6 +470,8 @@ class GradientExchange:
             if self._side is None:
                 self._side = torch.cuda.Stream(device=self.device)
                 self._gathered = torch.cuda.Event()
+            if self._mc_dst is not None:
+                kernels.multicast_copy(self.pack, self._mc_dst)
             self._symm.barrier(channel=0)
             kernels.gather_bytes(self._dec_ptrs, self.k, self.dec_all)
             self._gathered.record(main)

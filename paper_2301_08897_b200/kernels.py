@@ -449,6 +449,15 @@ class GuardedDenseLaunchers:
         _count(1)
 
 
+def multicast_copy(src: torch.Tensor, mc_dst: int) -> None:
+    """Copy ``src`` (int32 words, a multiple of 4) to the multicast address ``mc_dst`` of a
+    peer-mapped buffer: every rank's copy receives it (sg_multicast_copy_u32)."""
+    require_cuda(src)
+    _capi.check(_capi.load().sg_multicast_copy_u32(src.data_ptr(), int(mc_dst), src.numel(), _stream()),
+                "sg_multicast_copy_u32")
+    _count(1)
+
+
 def gather_bytes(src_ptrs, each: int, dst: torch.Tensor) -> None:
     """dst[i*each:(i+1)*each] = bytes at device address src_ptrs[i] (peers' memory allowed)."""
     require_cuda(dst)

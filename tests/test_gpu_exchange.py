@@ -109,12 +109,16 @@ def test_multi_gpu_exchange_matches_single_gpu(cuda):
     n = 4 if torch.cuda.device_count() >= 4 else 2
     # peer path (symmetric buffers read in place by the merge) and the NCCL all-gather path
     # (and one worker per rank, the 8-GPU shape: W = P)
-    for port, p2p, workers, sparse_path in (("29531", "1", "8", "sparse-peer"), ("29532", "0", "8", "sparse-allgather"),
-                                            ("29533", "1", str(n), "sparse-peer")):
+    # (SG_PAYLOAD_MC=0: the merge reads the peers' payloads over NVLink instead of merging a
+    # multicast-broadcast copy from local memory)
+    for port, p2p, workers, sparse_path, mc in (("29531", "1", "8", "sparse-peer", "1"),
+                                                ("29532", "0", "8", "sparse-allgather", "1"),
+                                                ("29533", "1", str(n), "sparse-peer", "1"),
+                                                ("29534", "1", "8", "sparse-peer", "0")):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                "--master-addr", "127.0.0.1", "--master-port", port, str(ROOT / "tools" / "multi_check.py")]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
-                           env={**os.environ, "SG_P2P": p2p, "SG_CHECK_WORKERS": workers})
+                           env={**os.environ, "SG_P2P": p2p, "SG_CHECK_WORKERS": workers, "SG_PAYLOAD_MC": mc})
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
         rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
         assert rep["ok"] and rep["world"] == n
@@ -145,3 +149,23 @@ def test_multi_gpu_protocol_stress(cuda):
         rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
         assert rep["ok"] and rep["rank_mismatch_steps"] == 0
         assert set(rep["paths"]) == paths, rep
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multicast_payload_broadcast_keeps_every_bit_pattern(cuda):
+    """The payload broadcast (multimem.st through the switch) delivers NaN payloads, -0, infinities
+    and index words in float32's NaN range unchanged into every rank's slot (tools/mc_check.py)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    n = 4 if torch.cuda.device_count() >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29545", str(ROOT / "tools" / "mc_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rep = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert rep["ok"] and rep["world"] == n
