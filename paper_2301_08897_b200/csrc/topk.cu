@@ -2313,6 +2313,14 @@ __global__ void k_gate_update(const double* norms2, int k, sg_gate_state* states
 constexpr size_t MN_SMEM = (size_t)MN_STAGES * MN_TILE * sizeof(float);
 
 // Resident main-pass CTAs per SM, queried once per device (the plan is rebuilt on every call).
+inline bool resolve_coop() {  // SG_RESOLVE_COOP=0: k_resolve without the cooperative attribute (A/B runs)
+    static const bool on = [] {
+        const char* e = getenv("SG_RESOLVE_COOP");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 template <typename T> int main_ctas_per_sm() {
     static int cache[64] = {0};
     int dev = 0;
@@ -2531,7 +2539,10 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     int gres = sms / k;  // one 1024-thread CTA per SM: the whole grid is co-resident
     if (gres > 16) gres = 16;
     if (gres < 1) gres = 1;
-    launch_coop(k_resolve<T>, dim3((unsigned)gres, (unsigned)k), dim3(1024), res_smem, stream, ca, ra);
+    if (resolve_coop())
+        launch_coop(k_resolve<T>, dim3((unsigned)gres, (unsigned)k), dim3(1024), res_smem, stream, ca, ra);
+    else  // A/B: a plain PDL launch (the grid still fits the SMs; its barrier needs co-residency)
+        launch_pdl(k_resolve<T>, dim3((unsigned)gres, (unsigned)k), dim3(1024), res_smem, stream, ca, ra);
     debug_sync("k_resolve", stream);
     // 5. ordered write + norms + gate
     WriteArgs<T> wa;

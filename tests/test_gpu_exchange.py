@@ -109,12 +109,12 @@ def test_multi_gpu_exchange_matches_single_gpu(cuda):
     n = 4 if torch.cuda.device_count() >= 4 else 2
     # peer path (symmetric buffers read in place by the merge) and the NCCL all-gather path
     # (and one worker per rank, the 8-GPU shape: W = P)
-    # (SG_PAYLOAD_MC=0: the merge reads the peers' payloads over NVLink instead of merging a
-    # multicast-broadcast copy from local memory)
-    for port, p2p, workers, sparse_path, mc in (("29531", "1", "8", "sparse-peer", "1"),
-                                                ("29532", "0", "8", "sparse-allgather", "1"),
-                                                ("29533", "1", str(n), "sparse-peer", "1"),
-                                                ("29534", "1", "8", "sparse-peer", "0")):
+    # (SG_PAYLOAD_MC=1: the payloads broadcast through the switch and merged from local memory,
+    # instead of the default merge reading the peers' payloads over NVLink)
+    for port, p2p, workers, sparse_path, mc in (("29531", "1", "8", "sparse-peer", "0"),
+                                                ("29532", "0", "8", "sparse-allgather", "0"),
+                                                ("29533", "1", str(n), "sparse-peer", "0"),
+                                                ("29534", "1", "8", "sparse-peer", "1")):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                "--master-addr", "127.0.0.1", "--master-port", port, str(ROOT / "tools" / "multi_check.py")]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
