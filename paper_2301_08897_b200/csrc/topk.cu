@@ -1854,6 +1854,8 @@ template <typename T> struct WriteArgs {
     sg_gate_state* states;
     uint8_t* decision;
     double* rho;
+    int ring;                     // float32 fast mode: candidate chunks through a TMA ring
+    unsigned ring_off;            // its byte offset in the dynamic shared memory
 };
 
 constexpr unsigned long long CNT_BITS = 31;
@@ -1914,6 +1916,8 @@ SG_DEV void write_tail(const WriteArgs<T>& a, double ss) {
 constexpr int WF_R = 4;                      // rounds (entries per thread) per chunk
 constexpr int WF_SPAN = TK_THREADS * WF_R;   // 1024 entries per chunk
 static_assert(WF_R * TK_NW == 32, "one lane per (round, warp) slot");
+constexpr int WT_STAGES = 3;                                 // float32 ring depth (chunks in flight)
+constexpr size_t WT_RING = (size_t)WT_STAGES * 2 * WF_SPAN * 4;
 
 template <typename T>
 SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
@@ -1931,31 +1935,74 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
     const unsigned lt_mask = lanemask_lt();
     T v[WF_R];
     uint32_t ii[WF_R];
+    // float32 with a.ring: the chunks stream through a WT_STAGES-deep shared-memory ring filled by
+    // TMA bulk copies (values then indices per stage; sub-range starts are 4-aligned and a
+    // segment's list capacity is a multiple of 4096, so a chunk rounded up to 16 bytes stays in
+    // the list); otherwise the next chunk's loads are in flight in registers
+    const bool ring_on = sizeof(T) == 4 && a.ring;
+    extern __shared__ __align__(128) unsigned char wr_smem_raw[];
+    uint32_t* ring = reinterpret_cast<uint32_t*>(wr_smem_raw + a.ring_off);  // [WT_STAGES][2][WF_SPAN]
+    __shared__ __align__(8) unsigned long long wbar[WT_STAGES];
+    const int nch = n32 > lo32 ? (n32 - lo32 + WF_SPAN - 1) / WF_SPAN : 0;
+    unsigned long long policy = 0;
+    auto issue = [&](int c) {
+        const int st = c % WT_STAGES;
+        const int b0 = lo32 + c * WF_SPAN;
+        const int n = n32 - b0 < WF_SPAN ? n32 - b0 : WF_SPAN;
+        const unsigned bytes = (unsigned)((n + 3) & ~3) * 4u;
+        uint32_t* d = ring + (size_t)st * 2 * WF_SPAN;
+        mbar_expect_tx(&wbar[st], 2 * bytes);
+        bulk_g2s(d, cv + b0, bytes, &wbar[st], policy);
+        bulk_g2s(d + WF_SPAN, ci + b0, bytes, &wbar[st], policy);
+    };
+    if (ring_on) {
+        if (tid == 0) {
+            policy = policy_evict_first();
+            for (int st = 0; st < WT_STAGES; ++st) mbar_init(&wbar[st], 1);
+            fence_mbar_init();
+            for (int c = 0; c < WT_STAGES && c < nch; ++c) issue(c);
+        }
+        __syncthreads();
+    } else {
 #pragma unroll
-    for (int r = 0; r < WF_R; ++r) {
-        const int e = lo32 + r * TK_THREADS + tid;
-        v[r] = e < n32 ? cv[e] : (T)0;
-        ii[r] = e < n32 ? ci[e] : 0u;
+        for (int r = 0; r < WF_R; ++r) {
+            const int e = lo32 + r * TK_THREADS + tid;
+            v[r] = e < n32 ? cv[e] : (T)0;
+            ii[r] = e < n32 ? ci[e] : 0u;
+        }
     }
     // tile of the candidate before the range (uniform)
     int ltile = lo32 > 0 ? (int)(ci[lo32 - 1] >> MERGE_SHIFT) : (int)t0 - 1;
     unsigned g32 = a.segbase[(long long)w * a.nsub + sub];
     double ss = 0.0;
-    int par = 0;
-    for (int base = lo32; base < n32; base += WF_SPAN, par ^= 1) {
+    int par = 0, ch = 0;
+    unsigned phase = 0;
+    for (int base = lo32; base < n32; base += WF_SPAN, par ^= 1, ++ch) {
         T x[WF_R];
         uint32_t xi[WF_R];
-#pragma unroll
-        for (int r = 0; r < WF_R; ++r) {
-            x[r] = v[r];
-            xi[r] = ii[r];
-        }
-        if (base + WF_SPAN < n32) {  // next chunk in flight
+        if (ring_on) {
+            const int st = ch % WT_STAGES;
+            mbar_wait(&wbar[st], phase);
+            if (st == WT_STAGES - 1) phase ^= 1u;
+            const uint32_t* d = ring + (size_t)st * 2 * WF_SPAN;
 #pragma unroll
             for (int r = 0; r < WF_R; ++r) {
-                const int e = base + WF_SPAN + r * TK_THREADS + tid;
-                v[r] = e < n32 ? cv[e] : (T)0;
-                ii[r] = e < n32 ? ci[e] : 0u;
+                if constexpr (sizeof(T) == 4) x[r] = __uint_as_float(d[r * TK_THREADS + tid]);
+                xi[r] = d[WF_SPAN + r * TK_THREADS + tid];
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < WF_R; ++r) {
+                x[r] = v[r];
+                xi[r] = ii[r];
+            }
+            if (base + WF_SPAN < n32) {  // next chunk in flight
+#pragma unroll
+                for (int r = 0; r < WF_R; ++r) {
+                    const int e = base + WF_SPAN + r * TK_THREADS + tid;
+                    v[r] = e < n32 ? cv[e] : (T)0;
+                    ii[r] = e < n32 ? ci[e] : 0u;
+                }
             }
         }
         unsigned ball[WF_R];
@@ -1972,6 +2019,10 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             }
         }
         __syncthreads();
+        if (ring_on && tid == 0 && ch + WT_STAGES < nch) {  // every thread has read this stage
+            fence_proxy_async();
+            issue(ch + WT_STAGES);
+        }
         // lane i <-> slot i = (round i / TK_NW, warp i % TK_NW), in index order
         const unsigned c = s_wt[par][lane];
         unsigned incl = c;
@@ -2313,6 +2364,14 @@ __global__ void k_gate_update(const double* norms2, int k, sg_gate_state* states
 constexpr size_t MN_SMEM = (size_t)MN_STAGES * MN_TILE * sizeof(float);
 
 // Resident main-pass CTAs per SM, queried once per device (the plan is rebuilt on every call).
+inline int write_ring() {  // SG_WRITE_RING=0: k_write's register double buffer (A/B runs)
+    static const int v = [] {
+        const char* e = getenv("SG_WRITE_RING");
+        return e && *e == '0' ? 0 : 1;
+    }();
+    return v;
+}
+
 inline bool resolve_coop() {  // SG_RESOLVE_COOP=0: k_resolve without the cooperative attribute (A/B runs)
     static const bool on = [] {
         const char* e = getenv("SG_RESOLVE_COOP");
@@ -2573,7 +2632,10 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.states = states;
     wa.decision = decision;
     wa.rho = rho;
-    const size_t wr_smem = align_up(sizeof(unsigned) * (size_t)p.tps, 16);  // slow mode: the segment's tile starts
+    // slow mode: the segment's tile starts; float32: then the candidate ring
+    wa.ring = sizeof(T) == 4 ? write_ring() : 0;
+    wa.ring_off = (unsigned)align_up(sizeof(unsigned) * (size_t)p.tps, 128);
+    const size_t wr_smem = wa.ring ? wa.ring_off + WT_RING : align_up(sizeof(unsigned) * (size_t)p.tps, 16);
     smem_attr((const void*)k_write<T>, (int)wr_smem);
     launch_pdl(k_write<T>, dim3(subgrid), dim3(TK_THREADS), wr_smem, stream, wa);
     debug_sync("k_write", stream);
