@@ -111,15 +111,23 @@ def topk_workspace_bytes(dtype: torch.dtype, k: int, dim: int, m: int, fused: bo
 
 
 # Launch-chain workspace budget: the chain keeps a candidate slot per element (8 B x k x D, e.g.
-# 69 GB at D = 1e9, k = 8); above this the persistent variant (a ~2m-entry candidate pool,
-# identical results) is taken instead.  SG_TOPK_WS_BUDGET overrides (bytes).
-TOPK_WS_BUDGET = int(os.environ.get("SG_TOPK_WS_BUDGET", str(16 << 30)))
+# 69 GB at D = 1e9, k = 8); above the budget the persistent variant (a ~2m-entry candidate
+# pool, identical results) is taken instead.  Default: a quarter of the device's memory (45 GB
+# on a B200); SG_TOPK_WS_BUDGET overrides (bytes).
+TOPK_WS_BUDGET = int(os.environ["SG_TOPK_WS_BUDGET"]) if os.environ.get("SG_TOPK_WS_BUDGET") else None
 
 
-def topk_use_fused(dtype: torch.dtype, k: int, dim: int, m: int) -> bool:
+def topk_ws_budget(device: torch.device | None = None) -> int:
+    if TOPK_WS_BUDGET is not None:
+        return TOPK_WS_BUDGET
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    return torch.cuda.get_device_properties(dev).total_memory // 4
+
+
+def topk_use_fused(dtype: torch.dtype, k: int, dim: int, m: int, device: torch.device | None = None) -> bool:
     """The Top-k variant `topk_gate(fused=None)` takes: the launch chain (faster at every k
-    and cr measured) unless its workspace exceeds TOPK_WS_BUDGET."""
-    return dtype == torch.float32 and topk_workspace_bytes(dtype, k, dim, m) > TOPK_WS_BUDGET
+    and cr measured) unless its workspace exceeds the budget (topk_ws_budget)."""
+    return dtype == torch.float32 and topk_workspace_bytes(dtype, k, dim, m) > topk_ws_budget(device)
 
 
 def _topk_ws(dtype, k, dim, m, device, slot, fused):
@@ -153,7 +161,7 @@ def topk_gate(
     ``workspace_slot`` selects a separate scratch buffer for calls issued concurrently on
     different streams.  ``fused`` (float32) takes the persistent one-kernel variant
     (sg_topk_gate_fused_f32) instead of the launch chain; the results are identical.  None
-    (default): the chain unless its workspace exceeds ``TOPK_WS_BUDGET`` (topk_use_fused).
+    (default): the chain unless its workspace exceeds the budget (topk_use_fused).
 
     Returns (idx int32 [k, m] (uint32 bits), val [k, m], norms2 f64 [k, 2], decision u8 [k],
     rho f64 [k]); decision/rho are None without ``states``.
@@ -179,7 +187,7 @@ def topk_gate(
     if states is not None and states.numel() != k * _GATE_BYTES:
         raise ValueError("one gate state per worker required")
     if fused is None:
-        fused = topk_use_fused(g.dtype, k, D, m)
+        fused = topk_use_fused(g.dtype, k, D, m, g.device)
     fused = bool(fused) and g.dtype == torch.float32
     if topk_workspace_bytes(g.dtype, k, D, m, fused) == 0:
         raise ValueError("invalid top-k shape")

@@ -175,7 +175,7 @@ def test_auto_variant_takes_the_pool_above_the_workspace_budget(cuda, monkeypatc
                          .astype(np.float32)).to(cuda)
     assert not kernels.topk_use_fused(torch.float32, k, D, m)
     ref = kernels.topk_gate(g, m)
-    monkeypatch.setattr(kernels, "TOPK_WS_BUDGET", 0)
+    monkeypatch.setattr(kernels, "TOPK_WS_BUDGET", 0)  # force the pool variant
     assert kernels.topk_use_fused(torch.float32, k, D, m)
     assert not kernels.topk_use_fused(torch.float64, k, D, m)  # float64 has only the chain
     got = kernels.topk_gate(g, m)
