@@ -48,7 +48,6 @@ constexpr int EST_G = 32;        // sampling CTAs per worker (k_sample)
 constexpr int SE_GMAX = 128;     // sampling CTAs per worker (k_sample_est), at most
 constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
-constexpr int MERGE_SHIFT = 12;  // log2(MERGE_TILE)
 constexpr int NSUB_MAX = 2048;      // collect/write sub-ranges per worker
 constexpr int CW_PER_SM = 6;        // resident collect/write CTAs per SM (one wave)
 
@@ -1519,6 +1518,8 @@ k_collect(CollectArgs<T> a) {
     const SelState<K> st = a.sel[w];
     const K lo = st.lo, span = st.span;
     const int lo32 = (int)e.z, hi32 = (int)e.w;
+    const bool fcmp = sizeof(T) == 4 && lo >= 1;  // (lo = 0: NaN keys are in range -- key path)
+    const float f_lo = __uint_as_float((unsigned)(lo - 1)), f_hi = __uint_as_float((unsigned)(lo + span - 1));
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
     const T* cv = a.cval + ((long long)w * a.nseg + seg) * a.segcap;
     K* bk = a.bkey + (long long)w * a.cap;
@@ -1534,13 +1535,26 @@ k_collect(CollectArgs<T> a) {
         for (int u = 0; u < CL_EPT; ++u) x[u] = v[u];
         if (base + CL_SPAN < hi32) load16<T, CL_EPT>(cv, e0 + CL_SPAN, hi32, v);  // next chunk in flight
         unsigned bm = 0;  // entries inside the rank-m bin (the boundary)
+        if (fcmp) {
+            // float32: the key tests as |x| compares (key = bits(|x|) + 1 orders like |x|; NaN
+            // compares false, as its key 0 < lo): ~3 instructions per entry instead of ~10
+            const int lim = hi32 - e0;
 #pragma unroll
-        for (int u = 0; u < CL_EPT; ++u) {
-            const K key = KO::key(x[u]);
-            const K d = key - lo;  // wraps for key < lo: excluded by the key >= lo test
-            const bool ok = e0 + u < hi32 && key >= lo;
-            gt += ok && d > span;
-            bm |= (ok && d <= span ? 1u : 0u) << u;
+            for (int u = 0; u < CL_EPT; ++u) {
+                const float ax = fabsf((float)x[u]);
+                const bool in = u < lim;
+                gt += in && ax > f_hi;
+                bm |= (in && ax >= f_lo && ax <= f_hi ? 1u : 0u) << u;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < CL_EPT; ++u) {
+                const K key = KO::key(x[u]);
+                const K d = key - lo;  // wraps for key < lo: excluded by the key >= lo test
+                const bool ok = e0 + u < hi32 && key >= lo;
+                gt += ok && d > span;
+                bm |= (ok && d <= span ? 1u : 0u) << u;
+            }
         }
         // warp-aggregated append: one global atomic per warp that holds boundary entries
         const unsigned nb = __popc(bm);
@@ -1854,8 +1868,7 @@ template <typename T> struct WriteArgs {
     sg_gate_state* states;
     uint8_t* decision;
     double* rho;
-    int ring;                     // float32 fast mode: candidate chunks through a TMA ring
-    unsigned ring_off;            // its byte offset in the dynamic shared memory
+    unsigned ring_off;            // float32: byte offset of the candidate ring in the dynamic shared memory
 };
 
 constexpr unsigned long long CNT_BITS = 31;
@@ -1903,16 +1916,15 @@ SG_DEV void write_tail(const WriteArgs<T>& a, double ss) {
 
 // Fast-mode write (T and the tie cut are final).  The CTA streams its sub-range in chunks of
 // WF_SPAN entries: round r of a chunk is entries [base + 256 r, base + 256 (r + 1)), one per
-// thread, so every warp load and every warp store of a round covers consecutive entries
-// (coalesced, from registers -- no shared-memory staging).  The kept entries' output slots come
-// from one barrier per chunk: each (round, warp) publishes its kept count (a ballot) and the tile
-// of its last kept entry, and after the barrier a 32-lane scan over the (round, warp) slots gives
-// every kept entry its slot.  Merge offsets: toff[t] = kept entries with index < 4096 t.  A kept
-// entry whose tile differs from the previous kept entry's (the previous lane of its ballot, else
-// the last (round, warp) slot holding one, else the previous chunk's) sets the offsets of the
-// tiles in between.  This CTA owns the boundaries after the candidate before its range up to
-// its last candidate (the whole segment tail for the segment's last part).  The next chunk's
-// loads are in flight while the current one is processed.
+// thread, so every warp access of a round covers consecutive entries (float32: the chunks come
+// through a TMA ring).  The kept entries' output slots come from one barrier per chunk: each
+// (round, warp) publishes its kept count (a ballot), and after the barrier a 32-lane scan over
+// the (round, warp) slots gives every entry its kept-before count.  Merge offsets,
+// toff[t] = kept entries with index < 4096 t, come from the main pass's per-tile candidate starts
+// (s_ts: tile t's first candidate's offset in the segment list): the kept-before count at that
+// offset, read from the chunk's kept-before array -- no per-entry tile logic.  A tile start lies
+// in exactly one sub-range [lo, hi); starts at the segment's end (empty trailing tiles) go to its
+// last part.
 constexpr int WF_R = 4;                      // rounds (entries per thread) per chunk
 constexpr int WF_SPAN = TK_THREADS * WF_R;   // 1024 entries per chunk
 static_assert(WF_R * TK_NW == 32, "one lane per (round, warp) slot");
@@ -1920,12 +1932,13 @@ constexpr int WT_STAGES = 3;                                 // float32 ring dep
 constexpr size_t WT_RING = (size_t)WT_STAGES * 2 * WF_SPAN * 4;
 
 template <typename T>
-SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
+SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff, const unsigned* s_ts,
                          typename KeyOf<T>::K T_, unsigned cut, int seg, int lo32, int n32, bool last_part) {
     using KO = KeyOf<T>;
     using K = typename KO::K;
     __shared__ unsigned s_wt[2][32];  // (round, warp) kept counts, by chunk parity
-    __shared__ int s_wl[2][32];       // tile of the (round, warp)'s last kept entry, -1: none
+    __shared__ unsigned s_kb[WF_SPAN];  // kept-before count of every entry of the chunk
+    __shared__ int s_jc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = blockIdx.y, sub = blockIdx.x;
     const uint32_t* ci = a.cidx + ((long long)w * a.nseg + seg) * a.segcap;
@@ -1933,13 +1946,15 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
     uint32_t* oi = a.idx + (long long)w * a.m;
     T* ov = a.val + (long long)w * a.m;
     const unsigned lt_mask = lanemask_lt();
+    const bool fcmp = sizeof(T) == 4 && T_ >= 1;  // (T = 0 keeps NaN keys -- key path)
+    const float f_T = __uint_as_float((unsigned)(T_ - 1));
     T v[WF_R];
     uint32_t ii[WF_R];
-    // float32 with a.ring: the chunks stream through a WT_STAGES-deep shared-memory ring filled by
+    // float32: the chunks stream through a WT_STAGES-deep shared-memory ring filled by
     // TMA bulk copies (values then indices per stage; sub-range starts are 4-aligned and a
     // segment's list capacity is a multiple of 4096, so a chunk rounded up to 16 bytes stays in
     // the list); otherwise the next chunk's loads are in flight in registers
-    const bool ring_on = sizeof(T) == 4 && a.ring;
+    constexpr bool ring_on = sizeof(T) == 4;
     extern __shared__ __align__(128) unsigned char wr_smem_raw[];
     uint32_t* ring = reinterpret_cast<uint32_t*>(wr_smem_raw + a.ring_off);  // [WT_STAGES][2][WF_SPAN]
     __shared__ __align__(8) unsigned long long wbar[WT_STAGES];
@@ -1955,14 +1970,13 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
         bulk_g2s(d, cv + b0, bytes, &wbar[st], policy);
         bulk_g2s(d + WF_SPAN, ci + b0, bytes, &wbar[st], policy);
     };
-    if (ring_on) {
+    if constexpr (ring_on) {
         if (tid == 0) {
             policy = policy_evict_first();
             for (int st = 0; st < WT_STAGES; ++st) mbar_init(&wbar[st], 1);
             fence_mbar_init();
             for (int c = 0; c < WT_STAGES && c < nch; ++c) issue(c);
         }
-        __syncthreads();
     } else {
 #pragma unroll
         for (int r = 0; r < WF_R; ++r) {
@@ -1971,8 +1985,17 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             ii[r] = e < n32 ? ci[e] : 0u;
         }
     }
-    // tile of the candidate before the range (uniform)
-    int ltile = lo32 > 0 ? (int)(ci[lo32 - 1] >> MERGE_SHIFT) : (int)t0 - 1;
+    if (toff && tid == 0) {  // first tile of the segment whose first candidate is >= lo32
+        int l = 0, h = nt;
+        while (l < h) {
+            const int mid = (l + h) >> 1;
+            if ((int)s_ts[mid] < lo32) l = mid + 1;
+            else h = mid;
+        }
+        s_jc = l;
+    }
+    __syncthreads();
+    int jc = toff ? s_jc : 0;
     unsigned g32 = a.segbase[(long long)w * a.nsub + sub];
     double ss = 0.0;
     int par = 0, ch = 0;
@@ -1980,7 +2003,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
     for (int base = lo32; base < n32; base += WF_SPAN, par ^= 1, ++ch) {
         T x[WF_R];
         uint32_t xi[WF_R];
-        if (ring_on) {
+        if constexpr (ring_on) {
             const int st = ch % WT_STAGES;
             mbar_wait(&wbar[st], phase);
             if (st == WT_STAGES - 1) phase ^= 1u;
@@ -2009,17 +2032,19 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
 #pragma unroll
         for (int r = 0; r < WF_R; ++r) {
             const int e = base + r * TK_THREADS + tid;
-            const K key = KO::key(x[r]);
-            ball[r] = __ballot_sync(FULL, e < n32 && (key > T_ || (key == T_ && xi[r] <= cut)));
-            const int hl = ball[r] ? 31 - __clz((int)ball[r]) : 0;
-            const int lt = __shfl_sync(FULL, (int)(xi[r] >> MERGE_SHIFT), hl);
-            if (lane == 0) {
-                s_wt[par][r * TK_NW + warp] = __popc(ball[r]);
-                s_wl[par][r * TK_NW + warp] = ball[r] ? lt : -1;
+            bool keep;
+            if (fcmp) {  // float32: the key tests as |x| compares (see k_collect)
+                const float ax = fabsf((float)x[r]);
+                keep = ax > f_T || (ax == f_T && xi[r] <= cut);
+            } else {
+                const K key = KO::key(x[r]);
+                keep = key > T_ || (key == T_ && xi[r] <= cut);
             }
+            ball[r] = __ballot_sync(FULL, e < n32 && keep);
+            if (lane == 0) s_wt[par][r * TK_NW + warp] = __popc(ball[r]);
         }
         __syncthreads();
-        if (ring_on && tid == 0 && ch + WT_STAGES < nch) {  // every thread has read this stage
+        if (ring_on && tid == 0 && ch + WT_STAGES < nch) {  // every thread has read this stage (float32)
             fence_proxy_async();
             issue(ch + WT_STAGES);
         }
@@ -2032,45 +2057,37 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             if (lane >= o) incl += y;
         }
         const unsigned excl = incl - c, tot = __shfl_sync(FULL, incl, 31);
-        const int wl = s_wl[par][lane];
-        const unsigned has = __ballot_sync(FULL, wl >= 0);
 #pragma unroll
         for (int r = 0; r < WF_R; ++r) {
-            const int slot = r * TK_NW + warp;
-            const unsigned sbase = __shfl_sync(FULL, excl, slot);
-            const unsigned lower = ball[r] & lt_mask;
-            const int tile = (int)(xi[r] >> MERGE_SHIFT);
-            const int pl = __shfl_sync(FULL, tile, lower ? 31 - __clz((int)lower) : 0);
-            const unsigned hb = has & ((1u << slot) - 1u);
-            const int ps = __shfl_sync(FULL, wl, hb ? 31 - __clz((int)hb) : 0);
+            const unsigned pos = g32 + __shfl_sync(FULL, excl, r * TK_NW + warp) + __popc(ball[r] & lt_mask);
+            if (toff) s_kb[r * TK_THREADS + tid] = pos;
             if ((ball[r] >> lane) & 1u) {
-                const unsigned pos = g32 + sbase + __popc(lower);
-                if (toff) {
-                    const int tp = lower ? pl : (hb ? ps : ltile);
-                    if (tile != tp) {  // rare: this entry is the first kept one of tile(s) (tp, tile]
-#pragma unroll 1
-SG_CHECK(tp >= -1 && tile < (int)a.ntiles);
-                        for (int t = tp + 1; t <= tile; ++t) toff[t] = (int)pos;
-                    }
-                }
                 if (pos < (unsigned)a.m) {
-SG_CHECK(base + r * TK_THREADS + tid < n32);
                     oi[pos] = xi[r];
                     ov[pos] = x[r];
                     ss = fma((double)x[r], (double)x[r], ss);
                 }
             }
         }
+        if (toff) {
+            // tiles whose first candidate lies in this chunk: merge offset = kept before it
+            __syncthreads();  // s_kb complete
+            const int c1 = base + WF_SPAN < n32 ? base + WF_SPAN : n32;
+            for (;;) {
+                const int j = jc + tid;
+                const bool in = j < nt && (int)s_ts[j] < c1;
+                if (in) toff[t0 + j] = (int)s_kb[s_ts[j] - base];
+                const int cnt = __syncthreads_count(in);
+                jc += cnt;
+                if (cnt < TK_THREADS) break;
+            }
+        }
         g32 += tot;
-        if (has) ltile = __shfl_sync(FULL, wl, 31 - __clz((int)has));
     }
-    if (toff) {
-        // boundaries after the last kept entry: up to this range's last candidate, or to the
-        // segment end for its last part
-        const int tend = last_part ? (int)(t0 + nt) - 1 : (n32 > 0 ? (int)(ci[n32 - 1] >> MERGE_SHIFT) : (int)t0 - 1);
-        SG_CHECK(tend < (int)a.ntiles && g32 <= (unsigned)a.m + (unsigned)WF_SPAN);
-        for (int t = ltile + 1 + tid; t <= tend; t += TK_THREADS) toff[t] = (int)g32;
-        if (last_part && tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
+    if (toff && last_part) {
+        // tiles with no candidate at or after the segment's last entry: offset = kept total
+        for (int j = jc + tid; j < nt; j += TK_THREADS) toff[t0 + j] = (int)g32;
+        if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }
     return ss;
 }
@@ -2108,13 +2125,13 @@ SG_DEV void write_body(const WriteArgs<T>& a) {
     const int nt = (int)(t0 + a.tps < a.ntiles ? a.tps : a.ntiles - t0);
     int* toff = (OFFS && a.tile_off) ? a.tile_off + (long long)w * (a.ntiles + 1) : nullptr;
 
-    if (!slow) {
-        write_tail<T>(a, write_fast<T>(a, nt, t0, toff, T_, cut, seg, (int)i_lo, (int)n, last_part));
-        return;
-    }
     if (toff) {
         for (int j = tid; j < nt; j += TK_THREADS) s_ts[j] = a.tstart[(long long)w * a.ntiles + t0 + j];
         __syncthreads();
+    }
+    if (!slow) {
+        write_tail<T>(a, write_fast<T>(a, nt, t0, toff, s_ts, T_, cut, seg, (int)i_lo, (int)n, last_part));
+        return;
     }
     unsigned long long gb, eb;  // kept-before counters (fast mode: gb only)
     if (!slow) {
@@ -2364,14 +2381,6 @@ __global__ void k_gate_update(const double* norms2, int k, sg_gate_state* states
 constexpr size_t MN_SMEM = (size_t)MN_STAGES * MN_TILE * sizeof(float);
 
 // Resident main-pass CTAs per SM, queried once per device (the plan is rebuilt on every call).
-inline int write_ring() {  // SG_WRITE_RING=0: k_write's register double buffer (A/B runs)
-    static const int v = [] {
-        const char* e = getenv("SG_WRITE_RING");
-        return e && *e == '0' ? 0 : 1;
-    }();
-    return v;
-}
-
 inline bool resolve_coop() {  // SG_RESOLVE_COOP=0: k_resolve without the cooperative attribute (A/B runs)
     static const bool on = [] {
         const char* e = getenv("SG_RESOLVE_COOP");
@@ -2633,9 +2642,8 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     wa.decision = decision;
     wa.rho = rho;
     // slow mode: the segment's tile starts; float32: then the candidate ring
-    wa.ring = sizeof(T) == 4 ? write_ring() : 0;
     wa.ring_off = (unsigned)align_up(sizeof(unsigned) * (size_t)p.tps, 128);
-    const size_t wr_smem = wa.ring ? wa.ring_off + WT_RING : align_up(sizeof(unsigned) * (size_t)p.tps, 16);
+    const size_t wr_smem = sizeof(T) == 4 ? wa.ring_off + WT_RING : align_up(sizeof(unsigned) * (size_t)p.tps, 16);
     smem_attr((const void*)k_write<T>, (int)wr_smem);
     launch_pdl(k_write<T>, dim3(subgrid), dim3(TK_THREADS), wr_smem, stream, wa);
     debug_sync("k_write", stream);
