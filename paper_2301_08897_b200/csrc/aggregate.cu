@@ -638,7 +638,10 @@ k_merge(const AggArgs<float, TO> a) {
 // The streaming SGD never waits on a CTA-wide barrier.
 // ---------------------------------------------------------------------------------------
 constexpr int MW_CONS = 512;
-constexpr int MW_PROD = 384;
+#ifndef SG_MW_PROD  // producer threads of k_merge_ws (diagnostic builds may override)
+#define SG_MW_PROD 384
+#endif
+constexpr int MW_PROD = SG_MW_PROD;
 constexpr int MW_PW = MW_PROD / 32;
 constexpr int MW_THREADS = MW_CONS + MW_PROD;
 constexpr int MW_ECAP = 1024;

@@ -38,10 +38,12 @@ def main():
     ap.add_argument("--cr", type=float, default=0.01)
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--family", default="heavy")
+    ap.add_argument("--nvcc", default="", help="extra nvcc flags of the diagnostic build (A/B of compile-time constants)")
+    ap.add_argument("--tag", default="stamps")
     args = ap.parse_args()
-    out = ROOT / "gpurun_out" / "diag" / "libscadles_b200_stamps.so"
+    out = ROOT / "gpurun_out" / "diag" / f"libscadles_b200_{args.tag}.so"
     out.parent.mkdir(parents=True, exist_ok=True)
-    build.build_variant(out, ["-DSG_STAMPS"])
+    build.build_variant(out, ["-DSG_STAMPS"] + args.nvcc.split())
     _capi.LIB_PATH = out  # (or SG_LIB_PATH)
     lib = _capi.load()
     from paper_2301_08897_b200 import exchange
