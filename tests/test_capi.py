@@ -100,3 +100,21 @@ def test_python_errors_mirror_reference():
         comm.weighted_aggregate([[0.0], [0.0, 1.0]], [0.5, 0.5])
     with pytest.raises(ValueError, match="no gate decisions"):
         comm.cnc_ratio(comm.CompressionState(cr=0.1, delta=0.1))
+
+
+def test_topk_variant_budget_rule(lib, monkeypatch):
+    """kernels.topk_use_fused: the launch chain while its workspace (8 B per element per worker +
+    small) fits the budget, the ~2m-pool variant above it (float32 only; float64 has the chain
+    alone).  Workspace sizes are host arithmetic, so this runs without a GPU."""
+    import torch
+
+    from paper_2301_08897_b200 import comm, kernels
+
+    monkeypatch.setattr(kernels, "TOPK_WS_BUDGET", 45 * 10**9)  # a quarter of a B200
+    for D, want in ((60_192_808, False), (143_667_240, False), (1 << 28, False), (10**9, True)):
+        m = comm.topk_count(D, 0.01)
+        chain = kernels.topk_workspace_bytes(torch.float32, 8, D, m)
+        pool = kernels.topk_workspace_bytes(torch.float32, 8, D, m, fused=True)
+        assert chain >= 8 * 8 * D and pool < chain / 10
+        assert kernels.topk_use_fused(torch.float32, 8, D, m) is want, (D, chain)
+        assert kernels.topk_use_fused(torch.float64, 8, D, m) is False
