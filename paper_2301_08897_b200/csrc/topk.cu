@@ -2062,6 +2062,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             const unsigned pos = g32 + __shfl_sync(FULL, excl, r * TK_NW + warp) + __popc(ball[r] & lt_mask);
             if (toff) s_kb[r * TK_THREADS + tid] = pos;
             if ((ball[r] >> lane) & 1u) {
+                SG_CHECK(base + r * TK_THREADS + tid < n32);
                 if (pos < (unsigned)a.m) {
                     oi[pos] = xi[r];
                     ov[pos] = x[r];
@@ -2076,7 +2077,10 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
             for (;;) {
                 const int j = jc + tid;
                 const bool in = j < nt && (int)s_ts[j] < c1;
-                if (in) toff[t0 + j] = (int)s_kb[s_ts[j] - base];
+                if (in) {
+                    SG_CHECK((int)s_ts[j] >= base && (int)s_ts[j] - base < WF_SPAN && t0 + j < a.ntiles);
+                    toff[t0 + j] = (int)s_kb[s_ts[j] - base];
+                }
                 const int cnt = __syncthreads_count(in);
                 jc += cnt;
                 if (cnt < TK_THREADS) break;
@@ -2086,6 +2090,7 @@ SG_DEV double write_fast(const WriteArgs<T>& a, int nt, long long t0, int* toff,
     }
     if (toff && last_part) {
         // tiles with no candidate at or after the segment's last entry: offset = kept total
+        SG_CHECK(t0 + nt <= a.ntiles && g32 <= (unsigned)a.m + (unsigned)WF_SPAN);
         for (int j = jc + tid; j < nt; j += TK_THREADS) toff[t0 + j] = (int)g32;
         if (tid == 0 && t0 + nt == a.ntiles) toff[a.ntiles] = (int)a.m;
     }
