@@ -613,6 +613,7 @@ def run_ours(args):
             line["topk_us"] = {"mean": statistics.mean(topk_ms) * 1e3, "min": min(topk_ms) * 1e3}
         print(json.dumps(line), flush=True)
     if group is not None:
+        ex.close()
         dist.destroy_process_group()
 
 

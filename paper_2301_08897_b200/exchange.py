@@ -163,10 +163,19 @@ class GradientExchange:
                     self._setup_peer_buffers(words)
                 if self._symm is None:
                     self.pack = torch.zeros(words, dtype=torch.int32, **z)
-                self.decision = self.pack[:dw].view(torch.uint8)[:k]
-                self.idx = self.pack[dw:dw + k * m].view(k, m)
-                self.val = self.pack[dw + k * m:dw + 2 * k * m].view(torch.float32).view(k, m)
-                self.tile_off = self.pack[dw + 2 * k * m:dw + 2 * k * m + k * nt1].view(k, nt1)
+                    packs = [self.pack]
+                else:
+                    self._pack2 = self.pack
+                    packs = [self._pack2[:words], self._pack2[words:]]
+                    self.pack = packs[0]
+
+                def views(pk):
+                    return dict(pack=pk, decision=pk[:dw].view(torch.uint8)[:k], idx=pk[dw:dw + k * m].view(k, m),
+                                val=pk[dw + k * m:dw + 2 * k * m].view(torch.float32).view(k, m),
+                                tile_off=pk[dw + 2 * k * m:dw + 2 * k * m + k * nt1].view(k, nt1))
+
+                self._views = [views(pk) for pk in packs]
+                self._set_views(0)
             else:
                 self.idx = torch.empty((k, m), dtype=torch.int32, **z)
                 self.val = torch.empty((k, m), dtype=dtype, **z)
@@ -178,35 +187,39 @@ class GradientExchange:
             if self.packed and self._symm is not None:
                 P, words, dw = self.world, self.pack_words, self.pack_dw
                 self._mc_dst = None
-                if self._gath is not None:
-                    # payload broadcast: rank r's pack lands in slot r of every rank's gather
-                    # buffer, so the merge reads all W payloads from local HBM
-                    g0 = self._gath.data_ptr()
-                    bases = [g0 + 4 * r * words for r in range(P)]
-                    goff = g0 - self._gath_h.buffer_ptrs[self.rank]
-                    self._mc_dst = int(self._gath_h.multicast_ptr) + goff + 4 * self.rank * words
-                    merge_local = (0, self.W)
-                else:
-                    off0 = self.pack.data_ptr() - self._symm.buffer_ptrs[self.rank]
-                    bases = [self._symm.buffer_ptrs[r] + off0 for r in range(P)]  # rank r's pack
-                    merge_local = (self.lo, self.k)
-                self._dec_ptrs = bases
-                idx_p = [b + 4 * (dw + j * m) for b in bases for j in range(k)]
-                val_p = [b + 4 * (dw + k * m + j * m) for b in bases for j in range(k)]
-                off_p = [b + 4 * (dw + 2 * k * m + j * nt1) for b in bases for j in range(k)]
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
-                self._peer_merge = kernels.PeerMergeLauncher(dim, self.dec_all, idx_p, val_p, off_p, self.params,
-                                                             self.momentum_buf, momentum, weight_decay,
-                                                             local_lo=merge_local[0], local_n=merge_local[1],
-                                                             sparse_merge=self.sparse_merge)
-                # mixed decisions: each rank's partial in a peer-mapped buffer, reduced in rank order
                 self._side = None
                 ph = self._partial_h
                 poff = self._partial_buf.data_ptr() - ph.buffer_ptrs[self.rank]
-                self._dense = kernels.GuardedDenseLaunchers(
-                    k, dim, self.ld, self.decision, self.idx, self.val, self.row_ptr_local, self.tile_off,
-                    self._partial_buf, [ph.buffer_ptrs[r] + poff for r in range(P)], self.dec_all,
-                    self.params, self.momentum_buf, momentum, weight_decay, self.rank, **self._push_args())
+                self._par_launch = []
+                for par, vw in enumerate(self._views):
+                    if self._gath is not None:
+                        # payload broadcast: rank r's pack lands in slot r of every rank's gather
+                        # buffer, so the merge reads all W payloads from local HBM
+                        g0 = self._gath.data_ptr()
+                        bases = [g0 + 4 * r * words for r in range(P)]
+                        goff = g0 - self._gath_h.buffer_ptrs[self.rank]
+                        self._mc_dst = int(self._gath_h.multicast_ptr) + goff + 4 * self.rank * words
+                        merge_local = (0, self.W)
+                    else:
+                        off0 = vw["pack"].data_ptr() - self._symm.buffer_ptrs[self.rank]
+                        bases = [self._symm.buffer_ptrs[r] + off0 for r in range(P)]  # rank r's pack
+                        merge_local = (self.lo, self.k)
+                    idx_p = [b + 4 * (dw + j * m) for b in bases for j in range(k)]
+                    val_p = [b + 4 * (dw + k * m + j * m) for b in bases for j in range(k)]
+                    off_p = [b + 4 * (dw + 2 * k * m + j * nt1) for b in bases for j in range(k)]
+                    merge = kernels.PeerMergeLauncher(dim, self.dec_all, idx_p, val_p, off_p, self.params,
+                                                      self.momentum_buf, momentum, weight_decay,
+                                                      local_lo=merge_local[0], local_n=merge_local[1],
+                                                      sparse_merge=self.sparse_merge)
+                    # mixed decisions: each rank's partial in a peer-mapped buffer, reduced in rank order
+                    dense = kernels.GuardedDenseLaunchers(
+                        k, dim, self.ld, vw["decision"], vw["idx"], vw["val"], self.row_ptr_local, vw["tile_off"],
+                        self._partial_buf, [ph.buffer_ptrs[r] + poff for r in range(P)], self.dec_all,
+                        self.params, self.momentum_buf, momentum, weight_decay, self.rank, **self._push_args())
+                    self._par_launch.append((bases, merge, dense))
+                    if self._gath is not None:
+                        break  # one gather buffer: no parity (the closing barrier stays)
             elif self.packed:
                 P, words, dw = self.world, self.pack_words, self.pack_dw
                 self.pack_all = torch.empty(P * words, dtype=torch.int32, **z)
@@ -261,6 +274,28 @@ class GradientExchange:
         self._dec_ring = None
         self.aggregate = None
         self.steps = 0
+        self._par = getattr(self, "_par", 0)
+        self._flip_pending = False
+
+    def close(self) -> None:
+        """Before this rank frees the exchange (or leaves the group) while peers may still be in
+        their last step: one peer barrier (the peer path keeps no closing barrier per step)."""
+        if self._flip_pending and self._symm is not None:
+            self._symm.barrier(channel=0)
+            self._flip_pending = False
+
+    def _advance(self) -> None:
+        """Before a step's first Top-k launch: move to the other send pack (peer path)."""
+        if self._flip_pending:
+            self._flip_pending = False
+            self._set_views(self._par ^ 1)
+
+    def _set_views(self, par: int) -> None:
+        """Point the public payload views (pack, decision, idx, val, tile_off) at send pack
+        ``par``: the Top-k of the next step writes there."""
+        self._par = par
+        for name, t in self._views[par].items():
+            setattr(self, name, t)
 
     def _push_args(self) -> dict:
         """Dense side mode (SG_DENSE_MODE, for the A/B runs of tools/dense_timing.py): "pull"
@@ -337,7 +372,9 @@ class GradientExchange:
 
             grp = self.group if self.group is not None else dist.group.WORLD
             if words is not None:
-                pack = symm_mem.empty(words, dtype=torch.int32, device=self.device)
+                # two send packs (step parity), so a step's Top-k never overwrites the pack a
+                # slower peer may still be merging from (no closing barrier per step)
+                pack = symm_mem.empty(2 * words, dtype=torch.int32, device=self.device)
                 pack.zero_()
                 symm = symm_mem.rendezvous(pack, grp.group_name)
                 # the gather buffer of the payload broadcast: slot r <- rank r's pack (multicast)
@@ -384,6 +421,7 @@ class GradientExchange:
 
     def gate(self) -> None:
         """Top-k + norms + gate for every local worker (no host synchronisation)."""
+        self._advance()
         self.ops.topk_gate(
             self.bucket, self.dim, self.m, self.states,
             (self.idx, self.val, self.norms2, self.decision, self.rho), self.tile_off,
@@ -398,6 +436,7 @@ class GradientExchange:
             return
         if not isinstance(self.ops, CudaOps):
             raise ValueError("per-worker gating needs the CUDA ops")
+        self._advance()
         gb = _capi.GATE_STATE_DTYPE.itemsize
         out = (self.idx[j:j + 1], self.val[j:j + 1], self.norms2[j:j + 1], self.decision[j:j + 1], self.rho[j:j + 1])
         kernels.topk_gate(self.bucket[j:j + 1], self.m, self.states[j * gb:(j + 1) * gb], dim=self.dim, out=out,
@@ -472,10 +511,11 @@ class GradientExchange:
             if self._side is None:
                 self._side = torch.cuda.Stream(device=self.device)
                 self._gathered = torch.cuda.Event()
+            bases, merge, dense = self._par_launch[self._par if len(self._par_launch) > 1 else 0]
             if self._mc_dst is not None:
                 kernels.multicast_copy(self.pack, self._mc_dst)
             self._symm.barrier(channel=0)
-            kernels.gather_bytes(self._dec_ptrs, self.k, self.dec_all)
+            kernels.gather_bytes(bases, self.k, self.dec_all)
             self._gathered.record(main)
             # the guarded dense side on a second stream: its no-ops overlap the merge (exactly
             # one of the two sides does work in any step)
@@ -483,11 +523,18 @@ class GradientExchange:
             with torch.cuda.stream(self._side):
                 # mixed decisions: the local partial densifies the compressed local workers,
                 # then the dense side exchanges it (a no-op when every worker compressed)
-                self._dense.partial(w[self.lo:self.lo + self.k], self.bucket)
-                self._dense_side(self._dense, lr, first, out, lambda: self._symm.barrier(channel=1))
-            self._peer_merge(w, lr, first, out)
+                dense.partial(w[self.lo:self.lo + self.k], self.bucket)
+                self._dense_side(dense, lr, first, out, lambda: self._symm.barrier(channel=1))
+            merge(w, lr, first, out)
             main.wait_stream(self._side)
-            self._symm.barrier(channel=0)
+            if len(self._par_launch) > 1:
+                # the next step's Top-k writes the other pack (the views flip when it starts, so
+                # they show this step's payload until then); the pack read here is rewritten two
+                # steps on, after the next step's opening barrier, which every rank passes only
+                # once its merge and dense side of this step are done (stream order)
+                self._flip_pending = True
+            else:
+                self._symm.barrier(channel=0)
             # the step's decisions for the lazily resolved path name: one pinned slot per
             # step in a ring allocated once (a StepInfo's path must be read within
             # DEC_RING steps of the step that made it)
