@@ -240,6 +240,18 @@ int sg_peer_allgather_sgd_f32(int nranks, const float* const* src, int rank, con
  * from its own HBM.  Replaces the sparse allgather of engine.py:255-265 / SURVEY §8(e). */
 int sg_multicast_copy_u32(const void* src, void* mc_dst, int64_t words, void* stream);
 
+/* Peer barrier of a multi-GPU step over peer-mapped flag words (flags: HOST array of nranks
+ * device pointers, rank q's zero-initialised array of slots x nranks unsigned words): this rank
+ * publishes `epoch` in every rank's word [slot * nranks + rank] and waits for every rank's epoch
+ * in its own words.  epoch == 0: a device counter (*counter) incremented per executed call.  With
+ * a guard (the gathered decisions) the call is skipped when every worker compressed (the dense
+ * side's barriers).  With dec_dst the ranks' decision bytes (dec_src[q], dec_each each) are
+ * gathered after the barrier.  Replaces the per-iteration synchronisation of engine.py:248-286
+ * across processes (one launch instead of a collective library barrier plus a gather). */
+int sg_peer_signal_wait(int nranks, int rank, unsigned* const* flags, int slot, unsigned epoch, unsigned* counter,
+                        const uint8_t* guard, int guard_n, const uint8_t* const* dec_src, int64_t dec_each,
+                        uint8_t* dec_dst, void* stream);
+
 /* dst[i * each + b] = src[i][b] for i < nsrc (<= 64 device pointers in a HOST array; peers'
  * memory allowed): gathers the ranks' decision bytes before the host reads them. */
 int sg_gather_bytes(int nsrc, const uint8_t* const* src, int64_t each, uint8_t* dst, void* stream);

@@ -94,6 +94,8 @@ SIGNATURES = {
     ),
     "sg_gather_bytes": (c_int, [c_int, POINTER(c_void_p), c_int64, _P, _P]),
     "sg_multicast_copy_u32": (c_int, [_P, _P, c_int64, _P]),
+    "sg_peer_signal_wait": (c_int, [c_int, c_int, POINTER(c_void_p), c_int, c_uint32, _P, _P, c_int, POINTER(c_void_p),
+                                    c_int64, _P, _P]),
     "sg_weighted_partial_f32": (
         c_int,
         [c_int, POINTER(c_double), _P, _P, c_int64, _P, _P, _P, _P, c_int64, _P, _P, c_int, _P, c_size_t, _P],

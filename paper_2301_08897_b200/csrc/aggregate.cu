@@ -1989,6 +1989,41 @@ struct GatherSrc {
     const uint8_t* p[MAX_WORKERS];
 };
 
+struct FlagPtrs {
+    unsigned* p[MAX_PEERS];
+};
+
+// Peer barrier over symmetric flag words (sg_peer_signal_wait): lane q < P writes this rank's
+// epoch into rank q's flag word [slot * P + rank] (st.release.sys over NVLink) and waits until
+// rank q's epoch in this rank's own words reaches it (ld.acquire.sys).  epoch == 0: the epoch is
+// a device-side counter incremented per executed call (identical on every rank, since every rank
+// skips or runs a guarded call alike: the guard is the gathered decisions).  Guarded calls return
+// at once when every worker compressed (the dense side has nothing to exchange).  Optionally
+// gathers the ranks' decision bytes afterwards (the opening barrier of a peer step).
+__global__ void __launch_bounds__(32)
+k_peer_signal_wait(FlagPtrs flags, int P, int rank, int slot, unsigned epoch, unsigned* counter,
+                   const uint8_t* __restrict__ guard, int gn, GatherSrc src, long long each, uint8_t* __restrict__ dst) {
+    pdl_enter();
+    const int lane = threadIdx.x;
+    if (guard && !peer_guard_run(guard, gn)) return;
+    unsigned e = epoch;
+    if (e == 0) {
+        if (lane == 0) e = *counter + 1u, *counter = e;
+        e = __shfl_sync(FULL, e, 0);
+    }
+    __threadfence_system();
+    if (lane < P) st_release_sys(flags.p[lane] + slot * P + rank, e);
+    if (lane < P) {
+        const unsigned* mine = flags.p[rank] + slot * P + lane;
+        while ((int)(ld_acquire_sys(mine) - e) < 0) __nanosleep(32);
+    }
+    __syncwarp();
+    if (dst) {
+        const long long n = (long long)P * each;
+        for (long long i = lane; i < n; i += 32) dst[i] = src.p[i / each][i % each];
+    }
+}
+
 __global__ void k_gather_bytes(GatherSrc src, int nsrc, long long each, uint8_t* __restrict__ dst) {
     pdl_enter();
     const long long n = (long long)nsrc * each;
@@ -2225,6 +2260,28 @@ int sg_multicast_copy_u32(const void* src, void* mc_dst, int64_t words, void* st
     const long long n4 = words / 4;
     launch_pdl(k_mc_copy, dim3((unsigned)peer_blocks(n4 / 4 + 1)), dim3(256), 0, (cudaStream_t)stream,
                reinterpret_cast<const uint4*>(src), reinterpret_cast<float*>(mc_dst), n4);
+    return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
+}
+
+int sg_peer_signal_wait(int nranks, int rank, unsigned* const* flags, int slot, unsigned epoch, unsigned* counter,
+                        const uint8_t* guard, int guard_n, const uint8_t* const* dec_src, int64_t dec_each,
+                        uint8_t* dec_dst, void* stream) {
+    if (nranks < 1 || nranks > MAX_PEERS || rank < 0 || rank >= nranks || !flags || slot < 0 || guard_n < 0 ||
+        guard_n > MAX_WORKERS || (guard_n > 0 && !guard) || (epoch == 0 && !counter) || (dec_dst && (!dec_src || dec_each < 1)))
+        return SG_ERR_INVALID;
+    FlagPtrs f{};
+    for (int i = 0; i < nranks; ++i) {
+        if (!flags[i]) return SG_ERR_INVALID;
+        f.p[i] = flags[i];
+    }
+    GatherSrc g{};
+    if (dec_dst)
+        for (int i = 0; i < nranks; ++i) {
+            if (!dec_src[i]) return SG_ERR_INVALID;
+            g.p[i] = dec_src[i];
+        }
+    launch_pdl(k_peer_signal_wait, dim3(1), dim3(32), 0, (cudaStream_t)stream, f, nranks, rank, slot, epoch, counter,
+               guard_n > 0 ? guard : nullptr, guard_n, g, (long long)dec_each, dec_dst);
     return cudaGetLastError() == cudaSuccess ? SG_OK : SG_ERR_CUDA;
 }
 

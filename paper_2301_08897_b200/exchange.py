@@ -189,6 +189,14 @@ class GradientExchange:
                 self._mc_dst = None
                 self.dec_all = torch.empty(self.W, dtype=torch.uint8, **z)
                 self._side = None
+                # the step's peer barriers: own flag words (one launch that also gathers the
+                # decisions; the dense side's barriers skipped on the device when every worker
+                # compressed) -- SG_PEER_BARRIER=0: the symmetric-memory library barrier (A/B)
+                self._pbar = None
+                if self._bar_h is not None and os.environ.get("SG_PEER_BARRIER", "1") != "0":
+                    boff = self._bar.data_ptr() - self._bar_h.buffer_ptrs[self.rank]
+                    self._pbar = kernels.PeerBarrier(self.rank, [self._bar_h.buffer_ptrs[r] + boff for r in range(P)],
+                                                     device)
                 ph = self._partial_h
                 poff = self._partial_buf.data_ptr() - ph.buffer_ptrs[self.rank]
                 self._par_launch = []
@@ -366,7 +374,7 @@ class GradientExchange:
         takes the NCCL path -- a rank that silently fell back alone would hang the others in
         the peer barriers)."""
         ok = 1
-        symm = pack = gath_h = None
+        symm = pack = gath_h = bar = bar_h = None
         try:
             import torch.distributed._symmetric_memory as symm_mem
 
@@ -381,6 +389,10 @@ class GradientExchange:
                 gath = symm_mem.empty(self.world * words, dtype=torch.int32, device=self.device)
                 gath.zero_()
                 gath_h = symm_mem.rendezvous(gath, grp.group_name)
+                # flag words of the step's own peer barriers (kernels.PeerBarrier)
+                bar = symm_mem.empty(kernels.PeerBarrier.SLOTS * self.world, dtype=torch.int32, device=self.device)
+                bar.zero_()
+                bar_h = symm_mem.rendezvous(bar, grp.group_name)
             part = symm_mem.empty(self.ld, dtype=torch.float32, device=self.device)
             part.zero_()
             part_h = symm_mem.rendezvous(part, grp.group_name)
@@ -406,6 +418,7 @@ class GradientExchange:
             dist.all_reduce(mc, op=dist.ReduceOp.MIN, group=self.group)
             if int(mc.item()) == 1:
                 self._gath, self._gath_h = gath, gath_h
+        self._bar, self._bar_h = (bar, bar_h) if int(flag.item()) == 1 else (None, None)
         if int(flag.item()) == 1:
             self._symm, self.pack = symm, pack
             self._partial_buf, self._partial_h = part, part_h
@@ -514,8 +527,13 @@ class GradientExchange:
             bases, merge, dense = self._par_launch[self._par if len(self._par_launch) > 1 else 0]
             if self._mc_dst is not None:
                 kernels.multicast_copy(self.pack, self._mc_dst)
-            self._symm.barrier(channel=0)
-            kernels.gather_bytes(bases, self.k, self.dec_all)
+            if self._pbar is not None:
+                self._pbar.open(self.steps + 1, bases, self.k, self.dec_all)
+                dense_barrier = lambda: self._pbar.guarded(self.dec_all)  # noqa: E731
+            else:
+                self._symm.barrier(channel=0)
+                kernels.gather_bytes(bases, self.k, self.dec_all)
+                dense_barrier = lambda: self._symm.barrier(channel=1)  # noqa: E731
             self._gathered.record(main)
             # the guarded dense side on a second stream: its no-ops overlap the merge (exactly
             # one of the two sides does work in any step)
@@ -524,7 +542,7 @@ class GradientExchange:
                 # mixed decisions: the local partial densifies the compressed local workers,
                 # then the dense side exchanges it (a no-op when every worker compressed)
                 dense.partial(w[self.lo:self.lo + self.k], self.bucket)
-                self._dense_side(dense, lr, first, out, lambda: self._symm.barrier(channel=1))
+                self._dense_side(dense, lr, first, out, dense_barrier)
             merge(w, lr, first, out)
             main.wait_stream(self._side)
             if len(self._par_launch) > 1:

@@ -466,6 +466,33 @@ def multicast_copy(src: torch.Tensor, mc_dst: int) -> None:
     _count(1)
 
 
+class PeerBarrier:
+    """sg_peer_signal_wait with the ranks' flag arrays bound once: ``open(epoch, dec_ptrs, each,
+    dst)`` -- the opening barrier of a peer step fused with the decision gather; ``guarded(guard)``
+    -- a dense-side barrier skipped on the device when every worker compressed."""
+
+    SLOTS = 2
+
+    def __init__(self, rank: int, flag_ptrs, device: torch.device):
+        self._lib = _capi.load()
+        self._P, self._rank = len(flag_ptrs), int(rank)
+        self._flags = (ctypes.c_void_p * len(flag_ptrs))(*flag_ptrs)
+        self._counter = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def open(self, epoch: int, dec_ptrs, each: int, dst: torch.Tensor) -> None:
+        src = (ctypes.c_void_p * len(dec_ptrs))(*dec_ptrs)
+        _capi.check(self._lib.sg_peer_signal_wait(self._P, self._rank, self._flags, 0, int(epoch) & 0xFFFFFFFF or 1,
+                                                  self._counter.data_ptr(), None, 0, src, int(each), dst.data_ptr(),
+                                                  _stream()), "sg_peer_signal_wait")
+        _count(1)
+
+    def guarded(self, guard: torch.Tensor) -> None:
+        _capi.check(self._lib.sg_peer_signal_wait(self._P, self._rank, self._flags, 1, 0, self._counter.data_ptr(),
+                                                  guard.data_ptr(), guard.numel(), None, 0, None, _stream()),
+                    "sg_peer_signal_wait")
+        _count(1)
+
+
 def gather_bytes(src_ptrs, each: int, dst: torch.Tensor) -> None:
     """dst[i*each:(i+1)*each] = bytes at device address src_ptrs[i] (peers' memory allowed)."""
     require_cuda(dst)
