@@ -666,8 +666,13 @@ constexpr int SE_THREADS = 256;
 constexpr int SE_GMIN = 8;
 constexpr int SE_CHUNK = 256;  // sample chunk (elements): one 1 KB DRAM row
 inline int se_ctas(int k) {  // a power of two: the 512 sample chunks split evenly
+    static const int cap = [] {  // SG_SE_G: at most this many sampling CTAs per worker (A/B runs)
+        const char* e = getenv("SG_SE_G");
+        const int v = e && *e ? atoi(e) : SE_GMAX;
+        return v >= SE_GMIN && v <= SE_GMAX ? v : SE_GMAX;
+    }();
     int g = SE_GMAX;
-    while (g > SE_GMIN && g * k > 256) g >>= 1;
+    while (g > SE_GMIN && (g * k > 256 || g > cap)) g >>= 1;
     return g;
 }
 inline size_t se_smem(int G) { return 2 * sizeof(uint32_t) * (size_t)(TopkTraits<float>::SAMPLE / G); }
