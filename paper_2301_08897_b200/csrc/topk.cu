@@ -303,6 +303,57 @@ SG_DEV void block_find_bin_from_top(const unsigned* hist, unsigned long long ran
     above = s_above;
 }
 
+// Two ranks from one block scan (the estimate's r_est and its mirror r_hi); rank 0: none (-1).
+template <int NB, int THREADS>
+SG_DEV void block_find_two_bins_from_top(const unsigned* hist, unsigned long long r1, int& bin1, unsigned long long& above1,
+                                         unsigned long long r2, int& bin2, unsigned long long& above2) {
+    constexpr int PER = NB / THREADS;
+    static_assert(PER >= 1 && NB % THREADS == 0, "bins per thread");
+    __shared__ unsigned long long s_wsum2[THREADS / 32];
+    __shared__ int s_b[2];
+    __shared__ unsigned long long s_a[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int top = NB - 1 - PER * tid;
+    unsigned long long s = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) s += hist[top - i];
+    unsigned long long incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_wsum2[warp] = incl;
+    if (tid == 0) s_b[0] = s_b[1] = -1;
+    __syncthreads();
+    unsigned long long wb = 0;
+    for (int i = 0; i < warp; ++i) wb += s_wsum2[i];
+    incl += wb;
+    const unsigned long long ex = incl - s;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const unsigned long long rank = r == 0 ? r1 : r2;
+        if (rank >= 1 && ex < rank && incl >= rank) {  // exactly one thread holds the rank
+            unsigned long long cum = ex;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const unsigned h = hist[top - i];
+                if (cum + h >= rank) {
+                    s_b[r] = top - i;
+                    s_a[r] = cum;
+                    break;
+                }
+                cum += h;
+            }
+        }
+    }
+    __syncthreads();
+    bin1 = s_b[0];
+    above1 = s_a[0];
+    bin2 = s_b[1];
+    above2 = s_a[1];
+}
+
 template <typename K> SG_DEV int digit_shift(K span, int bits) {
     const int bl = bitlen<K>(span);
     return bl > bits ? bl - bits : 0;
@@ -644,7 +695,7 @@ k_estimate(long long dim, long long s_eff, long long r_est, const typename KeyOf
 // The sample: S = 131072 keys per worker as 512 chunks of 256 elements (1 KB, one DRAM row),
 // one at a hashed offset inside each of 512 strata of the row.  The reads are random, so their
 // cost is DRAM row activations (128-byte chunks, 8x the activations, measured 25 us at k = 8).
-// G CTAs per worker (G = se_ctas(k): 128 at k = 1 .. 32 at k = 8) each take 512/G chunks, key
+// G CTAs per worker (G = se_ctas(k): 64 at k = 1, 32 otherwise) each take 512/G chunks, key
 // them in shared memory, histogram key bits [30:20] (level 1), add the non-zero bins to the
 // worker's global level-1 histogram and write the keys BUCKETED by level-1 bin (a counting
 // sort in shared memory) with the bucket offsets.  The worker's last CTA to finish picks the
@@ -671,8 +722,10 @@ inline int se_ctas(int k) {  // a power of two: the 512 sample chunks split even
         const int v = e && *e ? atoi(e) : SE_GMAX;
         return v >= SE_GMIN && v <= SE_GMAX ? v : SE_GMAX;
     }();
-    int g = SE_GMAX;
-    while (g > SE_GMIN && (g * k > 256 || g > cap)) g >>= 1;
+    // measured (tools/stamps.py, D = R): k = 1: G = 128 / 64 / 32 -> 14.6 / 12.8 / 13.1 us;
+    // k = 2: 128 / 64 / 32 -> 16.8 / 12.8 / 12.3; k = 8: 32 / 16 / 8 -> 15.2 / 15.1 / 18.1
+    int g = k == 1 ? 64 : 32;
+    while (g > SE_GMIN && g > cap) g >>= 1;
     return g;
 }
 inline size_t se_smem(int G) { return 2 * sizeof(uint32_t) * (size_t)(TopkTraits<float>::SAMPLE / G); }
@@ -847,13 +900,14 @@ k_sample_est_f32(SampleEstArgs a) {
     K est = 0;
     int b1 = -1;
     unsigned long long a1 = 0;
-    if (a.r_est <= a.s_eff) block_find_bin_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)a.r_est, b1, a1);
     K ucap = KO::KMAX;  // upper end of the main pass's fine histogram range (see make_plan)
-    if (a.r_hi >= 1 && b1 >= 0) {
+    if (a.r_est <= a.s_eff) {
+        // both ranks (r_est, and the mirror r_hi: 0 = none) from one block scan
         int bh;
         unsigned long long ah;
-        block_find_bin_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)a.r_hi, bh, ah);
-        if (bh >= 0 && bh < SEL_BINS - 1) ucap = (K)(bh + 1) << 20;
+        block_find_two_bins_from_top<SEL_BINS, SE_THREADS>(h1, (unsigned long long)a.r_est, b1, a1,
+                                                           (unsigned long long)(a.r_hi >= 1 ? a.r_hi : 0), bh, ah);
+        if (b1 >= 0 && a.r_hi >= 1 && bh >= 0 && bh < SEL_BINS - 1) ucap = (K)(bh + 1) << 20;
     }
     __syncthreads();  // h1 is reused for level 2
     for (int i = tid; i < SEL_BINS; i += SE_THREADS) h1[i] = 0;
