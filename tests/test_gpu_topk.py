@@ -217,3 +217,56 @@ def test_topk_full_size_properties(cuda, D, cr, fam):
     s_topk = float((val[0].double() ** 2).sum())
     assert abs(float(norms2[0, 0]) - s_full) <= 1e-9 * s_full
     assert abs(float(norms2[0, 1]) - s_topk) <= 1e-9 * s_topk
+
+
+def _chain_sample_mask(D, w=0, nch=512, chunk=256):
+    """The launch chain's sample positions for worker w (k_sample_est_f32, 16-byte-aligned rows):
+    one 256-element chunk per stratum of D // 512 at a hashed, 4-aligned offset."""
+    M64 = (1 << 64) - 1
+
+    def mix64(x):
+        x ^= x >> 33
+        x = (x * 0xff51afd7ed558ccd) & M64
+        x ^= x >> 33
+        x = (x * 0xc4ceb9fe1a85ec53) & M64
+        x ^= x >> 33
+        return x
+
+    stratum = D // nch
+    mask = np.zeros(D, dtype=bool)
+    for c in range(nch):
+        h = mix64((c * 0x9e3779b97f4a7c15 + w) & M64) & 0xFFFFFFFF
+        off = (h * (stratum - chunk - 3 + 1)) >> 32
+        start = ((c * stratum + 3) & ~3) + (off & ~3)
+        mask[start:start + chunk] = True
+    return mask
+
+
+def test_chain_estimate_undershoot_takes_the_fallback_pass(cuda):
+    """Large values only at the chain's sampled positions: the estimate lands above every other
+    key, fewer than m keys reach it, and the fallback pass (every element a candidate) must still
+    give the reference's selection bit for bit, with the merge offsets and norms."""
+    from paper_2301_08897_b200 import kernels
+
+    D = 4_000_036  # a multiple of 4: the sampler's 16-byte path (the positions reproduced here)
+    rng = np.random.default_rng(12)
+    g = (rng.standard_normal(D) * 1e-3).astype(np.float32)
+    mask = _chain_sample_mask(D)
+    g[mask] = (10.0 + rng.random(int(mask.sum()))).astype(np.float32)
+    m = comm_ref.topk_count(D, 0.1)  # 400,004 > the 131,072 sampled keys
+    nt = kernels.merge_tiles(D)
+    toff = torch.empty((1, nt + 1), dtype=torch.int32, device=cuda)
+    idx, val, norms2, _, _ = kernels.topk_gate(torch.from_numpy(g).to(cuda), m, tile_off=toff, fused=False)
+    st = kernels.topk_stats(torch.float32, 1, D, m, cuda)
+    assert int(st[0, 2]) == 1, st  # the fallback pass ran
+    want = comm_ref.topk_indices_threshold(g.astype(np.float64), m)
+    got = idx[0].cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, want)
+    assert np.array_equal(val[0].cpu().numpy().view(np.uint32), g[want].view(np.uint32))
+    t = toff[0].cpu().numpy()
+    assert np.array_equal(t[:-1], np.searchsorted(want, np.arange(nt) * 4096))
+    assert t[-1] == m
+    n = norms2[0].cpu().numpy()
+    g64 = g.astype(np.float64)
+    assert abs(n[0] - np.dot(g64, g64)) <= 1e-12 * np.dot(g64, g64)
+    assert abs(n[1] - np.dot(g64[want], g64[want])) <= 1e-12 * np.dot(g64[want], g64[want])
