@@ -50,6 +50,7 @@ constexpr int BMAX = 1024;  // max segments (k_main CTAs) per worker
 constexpr int MERGE_TILE = 4096;
 constexpr int NSUB_MAX = 2048;      // collect/write sub-ranges per worker
 constexpr int CW_PER_SM = 6;        // resident collect/write CTAs per SM (one wave)
+constexpr int FB_CTAS = 32;         // fallback-pass CTAs per worker (striding over the segments)
 
 enum { MODE_NORMAL = 0, MODE_FALLBACK = 1 };
 enum { WR_FAST = 0, WR_SLOW = 1 };
@@ -1154,7 +1155,7 @@ SG_DEV void main_finish(const MainArgs<T>& a, int w, int seg, double ss, typenam
         if (hist[i]) atomicAdd(gh + i, hist[i]);
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(a.done + w, 1u) == gridDim.x - 1;
+    if (tid == 0) s_last = atomicAdd(a.done + w, 1u) == (unsigned)a.nseg - 1;  // one arrival per segment
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -1403,15 +1404,19 @@ k_main(MainArgs<T> a) {
     __shared__ unsigned s_woff[32];
     __shared__ unsigned s_run, s_tbase;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int w = blockIdx.y, seg = blockIdx.x;
+    const int w = blockIdx.y;
     SelState<K>* stp = a.sel + w;
     if (a.pass == 1 && stp->mode != MODE_FALLBACK) {
         // not taken: the split of the (TMA) main pass, by the worker's first CTA
-        if (a.split_late && seg == 0) build_submap<T>(a, w, __ldcg(a.count + w));
+        if (a.split_late && blockIdx.x == 0) build_submap<T>(a, w, __ldcg(a.count + w));
         return;
     }
     const K est = a.pass == 1 ? (K)0 : stp->est;
     const int shift0 = a.pass == 1 ? digit_shift<K>(KO::KMAX, H0_BITS) : stp->shift0;
+    // one segment per CTA for the main pass; the (rare) fallback pass runs on a small grid
+    // that strides over the segments
+    for (int seg = blockIdx.x; seg < a.nseg; seg += gridDim.x) {
+    __syncthreads();  // the previous segment's histogram flush is done
     for (int i = tid; i < H0_BINS; i += TK_THREADS) hist[i] = 0;
     if (tid == 0) s_run = 0;
     const T* row = a.g + (long long)w * a.ld;
@@ -1496,6 +1501,7 @@ SG_CHECK(pos < (unsigned long long)a.segcap);
         }
     }
     main_finish<T, true>(a, w, seg, ss, mx, s_run, hist, est, shift0);
+    }
 }
 
 // --------------------------------------------------------------------------------------
@@ -2632,8 +2638,10 @@ int topk_gate(const T* g, int k, long long ld, long long dim, long long m, uint3
     ma.done = c_fb;
     ma.split_late = tma ? 1 : 0;
     // the fallback pass (normally an early exit) is the generic kernel: it also builds the split
-    // after the TMA pass
-    launch_pdl(k_main<T>, dim3(sgrid), dim3(TK_THREADS), 0, stream, ma);
+    // after the TMA pass.  A small grid striding over the segments: launching a CTA per segment
+    // only for them to exit cost ~2 us per step at k = 1
+    const unsigned fb_x = (unsigned)(p.nseg < FB_CTAS ? p.nseg : FB_CTAS);
+    launch_pdl(k_main<T>, dim3(fb_x, (unsigned)k), dim3(TK_THREADS), 0, stream, ma);
     debug_sync("k_main(fb)", stream);
     // 3. per-segment counts + boundary, in-CTA resolve
     CollectArgs<T> ca;
