@@ -1660,6 +1660,8 @@ SG_CHECK(e0 + u < hi32 && q < (unsigned long long)a.cap);
 // resolve_small: one CTA per worker finishes the select in shared memory when the
 // boundary is small (the normal case): T, the tie cut by index, per-segment output bases.
 // --------------------------------------------------------------------------------------
+constexpr int RS_DIRECT = 256;  // boundary sets ranked directly (a warp per entry); larger: radix rounds
+
 template <typename T>
 SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, unsigned* hist) {
     using K = typename KeyOf<T>::K;
@@ -1668,6 +1670,8 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
     constexpr int RES = TopkTraits<T>::RES;
     __shared__ SelState<K> sst;
     __shared__ unsigned s_eq, s_res[2];
+    __shared__ K s_T;           // direct mode: the threshold key and the tie cut
+    __shared__ unsigned s_cut0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef SG_PHASES
@@ -1688,34 +1692,96 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
     const K* bk = a.bkey + (long long)w * a.cap;
     const uint32_t* bi = a.bidx + (long long)w * a.cap;
     const uint32_t* bpp = a.bpos + (long long)w * a.cap;
-    for (long long i = tid; i < (long long)h; i += NT) {
-        sk[i] = bk[i];
-        si[i] = bi[i];
-        sp[i] = bpp[i];
+    const bool direct = h <= (unsigned long long)RS_DIRECT;  // the normal case (tens to hundreds of entries)
+    if (direct) {
+        // every load of the phase in flight before the first shared-memory store
+        static_assert(NSUB_MAX <= 2 * NT && BMAX <= NT, "two sub-range words, one segment word per thread");
+        const bool has = tid < (int)h;
+        const long long sb = (long long)w * a.nsub, cb = (long long)w * a.nseg, pb = (long long)w * (BMAX + 1);
+        K k0 = 0;
+        uint32_t i0 = 0, p0 = 0;
+        if (has) {
+            k0 = bk[tid];
+            i0 = bi[tid];
+            p0 = bpp[tid];
+        }
+        const unsigned g0 = tid < a.nsub ? a.seggt[sb + tid] : 0u;
+        const unsigned g1 = tid + NT < a.nsub ? a.seggt[sb + tid + NT] : 0u;
+        const unsigned c0 = tid < a.nseg ? a.segcnt[cb + tid] : 0u;
+        const unsigned q0 = tid <= a.nseg ? __ldcg(a.pp + pb + tid) : 0u;
+        const unsigned q1 = tid == 0 && a.nseg >= NT ? __ldcg(a.pp + pb + NT) : 0u;
+        if (has) {
+            sk[tid] = k0;
+            si[tid] = i0;
+            sp[tid] = p0;
+        }
+        if (tid < a.nsub) kb[tid] = g0;
+        if (tid + NT < a.nsub) kb[tid + NT] = g1;
+        if (tid < a.nseg) sc[tid] = c0;
+        if (tid <= a.nseg) pp[tid] = q0;
+        if (tid == 0 && a.nseg >= NT) pp[NT] = q1;
+    } else {
+        for (long long i = tid; i < (long long)h; i += NT) {
+            sk[i] = bk[i];
+            si[i] = bi[i];
+            sp[i] = bpp[i];
+        }
+        for (int i = tid; i < a.nsub; i += NT) kb[i] = a.seggt[(long long)w * a.nsub + i];
+        for (int i = tid; i < a.nseg; i += NT) sc[i] = a.segcnt[(long long)w * a.nseg + i];
+        for (int i = tid; i <= a.nseg; i += NT) pp[i] = __ldcg(a.pp + (long long)w * (BMAX + 1) + i);
     }
-    for (int i = tid; i < a.nsub; i += NT) kb[i] = a.seggt[(long long)w * a.nsub + i];
-    for (int i = tid; i < a.nseg; i += NT) sc[i] = a.segcnt[(long long)w * a.nseg + i];
     if (tid == 0) {
         sst = a.sel[w];
         s_eq = 0;
     }
-    for (int i = tid; i <= a.nseg; i += NT) pp[i] = __ldcg(a.pp + (long long)w * (BMAX + 1) + i);
     SG_PH();
-    block_select<K, NT>(sk, (long long)h, sst, hist);
+    if (direct) {
+        // rank every boundary entry in the reference's order (descending key, ascending index):
+        // the entry ranked need - 1 is the threshold T and the tie cut (np.lexsort keeps the keys
+        // above T and the lowest indices at T) -- one pass instead of radix rounds + a tie pass
+        __syncthreads();  // sst, sk, si
+        const unsigned long long need0 = sst.rank;
+        const int hn = (int)h;
+        for (int i = warp; i < hn; i += NT / 32) {  // warp per entry, 32 comparisons per ballot
+            const K kk = sk[i];
+            const uint32_t ii = si[i];
+            unsigned rank = 0;
+            for (int j0 = 0; j0 < hn; j0 += 32) {
+                const int j = j0 + lane;
+                bool before = false;
+                if (j < hn) {
+                    const K kj = sk[j];
+                    before = kj > kk || (kj == kk && si[j] < ii);
+                }
+                rank += __popc(__ballot_sync(FULL, before));
+            }
+            if (lane == 0 && (unsigned long long)rank + 1 == need0) {
+                s_T = kk;
+                s_cut0 = ii;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            sst.T = s_T;
+            sst.done = 1;
+        }
+    } else {
+        block_select<K, NT>(sk, (long long)h, sst, hist);
+    }
     SG_PH();
     const K T_ = sst.T;
     const unsigned long long need = sst.rank;
-    // ties at T: keep the `need` lowest indices among keys == T
+    // ties at T: keep the `need` lowest indices among keys == T (direct: the cut is known)
     unsigned eqc = 0;
-    for (long long i = tid; i < (long long)h; i += NT) {
+    for (long long i = direct ? (long long)h : tid; i < (long long)h; i += NT) {
         const bool e = sk[i] == T_;
         sf[i] = e;
         eqc += e;
     }
     atomicAdd(&s_eq, eqc);
     __syncthreads();
-    unsigned cut = 0xffffffffu;
-    if ((unsigned long long)s_eq > need) {
+    unsigned cut = direct ? s_cut0 : 0xffffffffu;
+    if (!direct && (unsigned long long)s_eq > need) {
         if (s_eq <= (unsigned)SEL_BINS) {
             // a small tie group: list its indices, and the cut is the one with need-1 smaller
             // (indices are distinct positions)
