@@ -1769,7 +1769,8 @@ SG_DEV void resolve_small(const CollectArgs<T>& a, int w, unsigned long long h, 
         block_select<K, NT>(sk, (long long)h, sst, hist);
     }
     SG_PH();
-    const K T_ = sst.T;
+    // (direct: s_T was written before the barrier above; sst.T is tid 0's copy for the write-back)
+    const K T_ = direct ? s_T : sst.T;
     const unsigned long long need = sst.rank;
     // ties at T: keep the `need` lowest indices among keys == T (direct: the cut is known)
     unsigned eqc = 0;
